@@ -1,0 +1,167 @@
+/*
+ * bddc_b200.h -- C ABI of the B200-native adaptive-BDDC hot path.
+ *
+ * The reference (/root/reference/proj) is a C++ class library with no FFI; its
+ * two drop-in seams are the LinearOperator pair handed to pcg
+ * (core/include/bddc/pcg.hpp:18,49-50) and the Factorization pImpl
+ * (core/include/bddc/sparse.hpp:55-66).  Each entry point below names the
+ * reference interface it replaces.  Plain pointers and sizes only; host
+ * buffers are borrowed for the duration of a call; the handle owns all device
+ * memory.  Every call returns a status code (BDDC_B200_*) mirroring the
+ * reference's exception taxonomy (core/include/bddc/types.hpp:21-63);
+ * bddc_b200_last_error() returns the message of the last failure.
+ */
+#ifndef BDDC_B200_H
+#define BDDC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (types.hpp:21-63, pcg.hpp:40-45) */
+#define BDDC_B200_OK 0
+#define BDDC_B200_ERROR 1
+#define BDDC_B200_NOT_POSITIVE_DEFINITE 2
+#define BDDC_B200_DEGENERATE_ELEMENT 3
+#define BDDC_B200_CORNER_SELECTION_FAILED 4
+#define BDDC_B200_NULLSPACE_INCLUSION_VIOLATED 5
+#define BDDC_B200_SINGULAR_GRAM 6
+#define BDDC_B200_NOT_ADJACENT 7
+#define BDDC_B200_BAD_PROBLEM_SPEC 8
+#define BDDC_B200_MAX_ITERATIONS 9
+#define BDDC_B200_CUDA_ERROR 10
+#define BDDC_B200_UNSUPPORTED 11
+
+typedef struct bddc_b200 bddc_b200_t;
+
+/* Problem description: ProblemSpec (core/include/bddc/problem.hpp:43-53) plus
+ * an optional per-element coefficient multiplier (element_scale, length =
+ * element count, x-fastest element order; NULL = 1). */
+typedef struct bddc_b200_problem {
+  int subdomains[3];
+  int elements_per_edge;
+  int physics; /* 0 scalar, 1 elasticity (types.hpp:13) */
+  int n_materials;
+  const int* material_id;
+  const double* conductivity;
+  const double* youngs;
+  const double* poisson;
+  int n_regions;
+  const int* region_box;      /* 6 per region: x0 x1 y0 y1 z0 z1 (half-open, problem.cpp:123-126) */
+  const int* region_material;
+  int n_dirichlet;
+  const int* dirichlet_face;  /* 0 xmin 1 xmax 2 ymin 3 ymax 4 zmin 5 zmax */
+  const int* dirichlet_components; /* 3 flags per entry */
+  int n_loads;
+  const int* load_face;
+  const double* load_traction; /* 3 per load */
+  const double* load_flux;
+  double body_force[3];
+  double source;
+  double tolerance;
+  int max_iterations;
+  const double* element_scale;
+} bddc_b200_problem;
+
+/* StructureSummary (core/include/bddc/experiment.hpp:48-57) */
+typedef struct bddc_b200_structure {
+  int64_t dofs, free_dofs, interface_dofs;
+  int64_t corners, classification_corners, edges, faces;
+  int64_t coarse_space_dim; /* W^c dimension */
+  int64_t subdomains, w_dim;
+} bddc_b200_structure;
+
+/* PcgResult (core/include/bddc/pcg.hpp:28-34) */
+typedef struct bddc_b200_pcg_result {
+  int64_t iterations;
+  double relative_residual;
+  double condition_estimate;
+  int converged;
+} bddc_b200_pcg_result;
+
+/* ResultRow (core/include/bddc/experiment.hpp:37-46) with device-timed phases */
+typedef struct bddc_b200_row {
+  double omega_tilde; /* NaN for non-eigenvalue modes */
+  int64_t constraint_rows;
+  double kappa;
+  int64_t iterations;
+  int converged;
+  double seconds_analysis, seconds_factorization, seconds_iterations, seconds_total;
+  double seconds_eigen, seconds_preconditioner; /* factorization = eigen + host constraints + preconditioner */
+  int64_t root_size;
+} bddc_b200_row;
+
+const char* bddc_b200_last_error(void);
+int bddc_b200_device_count(void);
+
+/* Build mesh, decomposition, Dirichlet map, substructure matrices, globs,
+ * corners and embeddings (experiment.cpp:116-128; support.hpp:89-100). */
+int bddc_b200_create(const bddc_b200_problem* problem, bddc_b200_t** out);
+/* The same from BASELINE.json config 1..5 with its seeded coefficient field;
+ * subdomains_override (3 ints) / epe_override (>0) shrink it for parity runs. */
+int bddc_b200_create_config(int config, uint64_t seed, const int* subdomains_override,
+                            int epe_override, bddc_b200_t** out);
+void bddc_b200_destroy(bddc_b200_t* h);
+
+int bddc_b200_structure_get(const bddc_b200_t* h, bddc_b200_structure* out);
+/* Index maps (spaces.hpp:23-43), for parity checks. */
+int bddc_b200_interface_dofs(const bddc_b200_t* h, int64_t* out);
+int bddc_b200_subdomain_dim(const bddc_b200_t* h, int s, int64_t* dim);
+int bddc_b200_local_to_wc(const bddc_b200_t* h, int s, int64_t* out);
+int bddc_b200_global_dof(const bddc_b200_t* h, int s, int64_t* out);
+/* Globs (globs.hpp:18-44): count, then per glob kind / node count / sharer count. */
+int bddc_b200_glob_count(const bddc_b200_t* h, int64_t* n);
+int bddc_b200_glob_info(const bddc_b200_t* h, int g, int* kind, int64_t* n_nodes, int64_t* n_subs);
+int bddc_b200_glob_nodes(const bddc_b200_t* h, int g, int64_t* nodes, int64_t* subs);
+
+/* Constraint set held by the handle (constraints.cpp:34-76). */
+int bddc_b200_constraints_arithmetic(bddc_b200_t* h, int edge_globs, int face_globs);
+int bddc_b200_constraint_rows(const bddc_b200_t* h, int64_t* rows);
+int bddc_b200_constraint_count(const bddc_b200_t* h, int64_t* n);
+int bddc_b200_constraint_get(const bddc_b200_t* h, int a, int* glob, int64_t* n_weights, double* weights);
+
+/* HarmonicExtension ctor (spaces.cpp:108-147): device A_II factorization and
+ * dense interface Schur complements. */
+int bddc_b200_analysis(bddc_b200_t* h);
+/* enrich_constraints / pair_indicator (adaptive.cpp:129-144).  fixed_count < 0
+ * uses tau; indicator_only != 0 adds no rows.  omega_tilde out. */
+int bddc_b200_enrich(bddc_b200_t* h, double tau, int max_vectors, int keep_edge, int fixed_count,
+                     int indicator_only, double* omega_tilde);
+/* Pair report k of the last enrich call (adaptive.hpp:14-22). */
+int bddc_b200_pair_count(const bddc_b200_t* h, int64_t* n);
+int bddc_b200_pair_report(const bddc_b200_t* h, int k, int* si, int* sj, int* enforced,
+                          double* omega_next, int* saturated, int64_t* n_eig, double* eigenvalues);
+/* change_of_variables + BddcPreconditioner ctor (bddc_operator.cpp:38-50). */
+int bddc_b200_setup_preconditioner(bddc_b200_t* h);
+
+/* LinearOperator seam (pcg.hpp:18): InterfaceProblem::apply (schur.cpp:12-36)
+ * and BddcPreconditioner::apply (bddc_operator.cpp:101-103); interface vectors. */
+int bddc_b200_interface_size(const bddc_b200_t* h, int64_t* n);
+int bddc_b200_schur_apply(bddc_b200_t* h, const double* x, double* y);
+int bddc_b200_precond_apply(bddc_b200_t* h, const double* r, double* z);
+/* InterfaceProblem::rhs / recover (schur.cpp:38-75). */
+int bddc_b200_rhs(bddc_b200_t* h, double* out);
+int bddc_b200_recover(bddc_b200_t* h, const double* u_interface, double* u_free);
+/* pcg + lanczos_condition_estimate (pcg.cpp:11-77).  b == NULL uses the
+ * condensed rhs; alphas/betas (length max_iterations) may be NULL.  Returns
+ * BDDC_B200_MAX_ITERATIONS with the partial result filled when capped. */
+int bddc_b200_pcg(bddc_b200_t* h, const double* b, double* x, double tolerance, int max_iterations,
+                  int preconditioned_residual, bddc_b200_pcg_result* res, double* alphas,
+                  double* betas);
+
+/* One work item of run_items (experiment.cpp:143-205): mode "c", "c+e",
+ * "c+e+f", "c+e+f-3eigv" or "adaptive"; base_faces != 0 starts the adaptive
+ * enrichment from c+e+f (BASELINE config 4).  Runs analysis if needed. */
+int bddc_b200_run_item(bddc_b200_t* h, const char* mode, double tau, int max_vectors, int keep_edge,
+                       int base_faces, bddc_b200_row* row);
+
+/* Device-timed phase seconds and work of the last calls:
+ * [analysis, eigen, preconditioner, pcg, leaf_flops, leaf_front_bytes, schur_bytes, root_size] */
+int bddc_b200_times(const bddc_b200_t* h, double out[8]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BDDC_B200_H */

@@ -1,0 +1,434 @@
+"""B200-native adaptive BDDC (arXiv 0910.5863) -- Python mirror of the C ABI.
+
+The product is the in-tree shared library `libbddc_b200.so` (C++ host layer +
+sm_100a CUDA kernels, `include/bddc_b200.h`).  This module binds it with
+ctypes and mirrors the reference library's interface for the hot path
+(`/root/reference/proj/core/include/bddc/*.hpp`): structure summary, constraint
+sets, `enrich_constraints`, the BDDC preconditioner, the interface (Schur)
+problem, `pcg`, and the experiment rows.  There is no CPU fallback: loading
+fails loudly when the library is missing, and every compute call raises when
+no CUDA device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+__all__ = ["load_library", "Problem", "BDDC", "Row", "BddcError", "EXPORTS", "emit_table"]
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libbddc_b200.so"
+
+# Status codes (include/bddc_b200.h; reference types.hpp:21-63)
+STATUS = {0: "OK", 1: "Error", 2: "NotPositiveDefinite", 3: "DegenerateElement",
+          4: "CornerSelectionFailed", 5: "NullspaceInclusionViolated", 6: "SingularGram",
+          7: "NotAdjacent", 8: "BadProblemSpec", 9: "MaxIterationsExceeded", 10: "CudaError",
+          11: "Unsupported"}
+
+
+class BddcError(RuntimeError):
+    """Raised for a non-zero status; `.kind` is the reference exception name."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__("%s: %s" % (STATUS.get(code, "Error"), message))
+        self.code = code
+        self.kind = STATUS.get(code, "Error")
+
+
+class _Problem(C.Structure):
+    _fields_ = [("subdomains", C.c_int * 3), ("elements_per_edge", C.c_int), ("physics", C.c_int),
+                ("n_materials", C.c_int), ("material_id", C.POINTER(C.c_int)),
+                ("conductivity", C.POINTER(C.c_double)), ("youngs", C.POINTER(C.c_double)),
+                ("poisson", C.POINTER(C.c_double)), ("n_regions", C.c_int),
+                ("region_box", C.POINTER(C.c_int)), ("region_material", C.POINTER(C.c_int)),
+                ("n_dirichlet", C.c_int), ("dirichlet_face", C.POINTER(C.c_int)),
+                ("dirichlet_components", C.POINTER(C.c_int)), ("n_loads", C.c_int),
+                ("load_face", C.POINTER(C.c_int)), ("load_traction", C.POINTER(C.c_double)),
+                ("load_flux", C.POINTER(C.c_double)), ("body_force", C.c_double * 3),
+                ("source", C.c_double), ("tolerance", C.c_double), ("max_iterations", C.c_int),
+                ("element_scale", C.POINTER(C.c_double))]
+
+
+class _Structure(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("dofs", "free_dofs", "interface_dofs", "corners",
+                                         "classification_corners", "edges", "faces",
+                                         "coarse_space_dim", "subdomains", "w_dim")]
+
+
+class _PcgResult(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("relative_residual", C.c_double),
+                ("condition_estimate", C.c_double), ("converged", C.c_int)]
+
+
+class _Row(C.Structure):
+    _fields_ = [("omega_tilde", C.c_double), ("constraint_rows", C.c_int64), ("kappa", C.c_double),
+                ("iterations", C.c_int64), ("converged", C.c_int),
+                ("seconds_analysis", C.c_double), ("seconds_factorization", C.c_double),
+                ("seconds_iterations", C.c_double), ("seconds_total", C.c_double),
+                ("seconds_eigen", C.c_double), ("seconds_preconditioner", C.c_double),
+                ("root_size", C.c_int64)]
+
+
+P = C.c_void_p
+D = C.POINTER(C.c_double)
+I64 = C.POINTER(C.c_int64)
+EXPORTS = {
+    "bddc_b200_last_error": (C.c_char_p, []),
+    "bddc_b200_device_count": (C.c_int, []),
+    "bddc_b200_create": (C.c_int, [C.POINTER(_Problem), C.POINTER(P)]),
+    "bddc_b200_create_config": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_int), C.c_int, C.POINTER(P)]),
+    "bddc_b200_destroy": (None, [P]),
+    "bddc_b200_structure_get": (C.c_int, [P, C.POINTER(_Structure)]),
+    "bddc_b200_interface_dofs": (C.c_int, [P, I64]),
+    "bddc_b200_subdomain_dim": (C.c_int, [P, C.c_int, I64]),
+    "bddc_b200_local_to_wc": (C.c_int, [P, C.c_int, I64]),
+    "bddc_b200_global_dof": (C.c_int, [P, C.c_int, I64]),
+    "bddc_b200_glob_count": (C.c_int, [P, I64]),
+    "bddc_b200_glob_info": (C.c_int, [P, C.c_int, C.POINTER(C.c_int), I64, I64]),
+    "bddc_b200_glob_nodes": (C.c_int, [P, C.c_int, I64, I64]),
+    "bddc_b200_constraints_arithmetic": (C.c_int, [P, C.c_int, C.c_int]),
+    "bddc_b200_constraint_rows": (C.c_int, [P, I64]),
+    "bddc_b200_constraint_count": (C.c_int, [P, I64]),
+    "bddc_b200_constraint_get": (C.c_int, [P, C.c_int, C.POINTER(C.c_int), I64, D]),
+    "bddc_b200_analysis": (C.c_int, [P]),
+    "bddc_b200_enrich": (C.c_int, [P, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, D]),
+    "bddc_b200_pair_count": (C.c_int, [P, I64]),
+    "bddc_b200_pair_report": (C.c_int, [P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int), D, C.POINTER(C.c_int), I64, D]),
+    "bddc_b200_setup_preconditioner": (C.c_int, [P]),
+    "bddc_b200_interface_size": (C.c_int, [P, I64]),
+    "bddc_b200_schur_apply": (C.c_int, [P, D, D]),
+    "bddc_b200_precond_apply": (C.c_int, [P, D, D]),
+    "bddc_b200_rhs": (C.c_int, [P, D]),
+    "bddc_b200_recover": (C.c_int, [P, D, D]),
+    "bddc_b200_pcg": (C.c_int, [P, D, D, C.c_double, C.c_int, C.c_int, C.POINTER(_PcgResult), D, D]),
+    "bddc_b200_run_item": (C.c_int, [P, C.c_char_p, C.c_double, C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(_Row)]),
+    "bddc_b200_times": (C.c_int, [P, D]),
+}
+
+_lib = None
+
+
+def load_library(build: bool = False):
+    """Load `libbddc_b200.so` (building it first when asked).  Fails loudly."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build or not LIB_PATH.exists():
+        from . import build as _build
+        _build.build()
+    if not LIB_PATH.exists():
+        raise ImportError("libbddc_b200.so is missing; run paper_0910_5863_b200/build.py")
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (res, args) in EXPORTS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise BddcError(rc, _lib.bddc_b200_last_error().decode())
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(D)
+
+
+def _iptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+FACES = {"xmin": 0, "xmax": 1, "ymin": 2, "ymax": 3, "zmin": 4, "zmax": 5}
+
+
+@dataclass
+class Problem:
+    """ProblemSpec (`problem.hpp:43-53`) plus the per-element coefficient extension."""
+    subdomains: Sequence[int] = (1, 1, 1)
+    elements_per_edge: int = 1
+    physics: str = "scalar"
+    materials: dict = field(default_factory=lambda: {0: (1.0, 1.0, 0.3)})  # id -> (k, E, nu)
+    regions: list = field(default_factory=list)       # (lo(3), hi(3), material)
+    dirichlet: list = field(default_factory=list)     # (face, (bool, bool, bool))
+    loads: list = field(default_factory=list)         # (face, traction(3), flux)
+    body_force: Sequence[float] = (0.0, 0.0, 0.0)
+    source: float = 0.0
+    tolerance: float = 1e-8
+    max_iterations: int = 500
+    element_scale: Optional[np.ndarray] = None
+
+    @staticmethod
+    def cube(subdomains, elements_per_edge, physics, clamp=True, clamp_face="xmin",
+             load_face="xmax") -> "Problem":
+        """`tests/support.hpp:32-48`."""
+        p = Problem(tuple(subdomains), elements_per_edge, physics)
+        if clamp:
+            p.dirichlet.append((clamp_face, (True, True, True)))
+        p.loads.append((load_face, (0.0, 0.0, -1.0), 1.0))
+        return p
+
+
+@dataclass
+class Row:
+    """ResultRow (`experiment.hpp:37-46`)."""
+    label: str
+    omega_tilde: float
+    constraint_rows: int
+    kappa: float
+    iterations: int
+    converged: bool
+    seconds_analysis: float
+    seconds_factorization: float
+    seconds_iterations: float
+    seconds_total: float
+    seconds_eigen: float = 0.0
+    seconds_preconditioner: float = 0.0
+    root_size: int = 0
+
+
+def emit_table(rows: List[Row], fmt="csv", include_times=True) -> str:
+    """`experiment.cpp:222-278` (kappa to 4 significant digits)."""
+    header = ["mode_or_tau", "omega_tilde", "Nc", "kappa", "it"]
+    if include_times:
+        header += ["analysis_s", "factorization_s", "iterations_s", "total_s"]
+    body = []
+    for r in rows:
+        cells = [r.label, "" if math.isnan(r.omega_tilde) else "%.4g" % r.omega_tilde,
+                 str(r.constraint_rows), "%.4g" % r.kappa,
+                 str(r.iterations) + ("" if r.converged else "*")]
+        if include_times:
+            cells += ["%.3f" % x for x in (r.seconds_analysis, r.seconds_factorization,
+                                          r.seconds_iterations, r.seconds_total)]
+        body.append(cells)
+    if fmt == "csv":
+        return "".join(",".join(c) + "\n" for c in [header] + body)
+    line = lambda cells: "|" + "".join(" %s |" % c for c in cells) + "\n"
+    return line(header) + line(["---"] * len(header)) + "".join(line(c) for c in body)
+
+
+class BDDC:
+    """One problem instance: host substructuring + the device engine."""
+
+    def __init__(self, problem: Optional[Problem] = None, *, config: Optional[int] = None,
+                 seed: int = 20091030, subdomains=None, elements_per_edge: int = 0):
+        lib = load_library()
+        self._lib = lib
+        h = P()
+        if config is not None:
+            sub = (C.c_int * 3)(*subdomains) if subdomains is not None else None
+            _check(lib.bddc_b200_create_config(config, seed, sub, elements_per_edge, C.byref(h)))
+        else:
+            _check(lib.bddc_b200_create(C.byref(self._pack(problem)), C.byref(h)))
+        self._h = h
+
+    def _pack(self, p: Problem) -> _Problem:
+        s = _Problem()
+        s.subdomains[:] = list(p.subdomains)
+        s.elements_per_edge = p.elements_per_edge
+        s.physics = 0 if p.physics == "scalar" else 1
+        keep = []
+
+        def arr(vals, ctype):
+            a = np.ascontiguousarray(np.array(vals, dtype=ctype))
+            keep.append(a)
+            return a.ctypes.data_as(C.POINTER(C.c_int if ctype == np.int32 else C.c_double))
+
+        ids = sorted(p.materials)
+        s.n_materials = len(ids)
+        s.material_id = arr(ids, np.int32)
+        s.conductivity = arr([p.materials[i][0] for i in ids], np.float64)
+        s.youngs = arr([p.materials[i][1] for i in ids], np.float64)
+        s.poisson = arr([p.materials[i][2] for i in ids], np.float64)
+        s.n_regions = len(p.regions)
+        s.region_box = arr([v for lo, hi, _ in p.regions for a in range(3) for v in (lo[a], hi[a])] or [0],
+                           np.int32)
+        s.region_material = arr([m for _, _, m in p.regions] or [0], np.int32)
+        s.n_dirichlet = len(p.dirichlet)
+        s.dirichlet_face = arr([FACES[f] for f, _ in p.dirichlet] or [0], np.int32)
+        s.dirichlet_components = arr([int(c) for _, cs in p.dirichlet for c in cs] or [0], np.int32)
+        s.n_loads = len(p.loads)
+        s.load_face = arr([FACES[f] for f, _, _ in p.loads] or [0], np.int32)
+        s.load_traction = arr([t for _, tr, _ in p.loads for t in tr] or [0.0], np.float64)
+        s.load_flux = arr([fl for _, _, fl in p.loads] or [0.0], np.float64)
+        s.body_force[:] = list(p.body_force)
+        s.source = p.source
+        s.tolerance = p.tolerance
+        s.max_iterations = p.max_iterations
+        if p.element_scale is not None:
+            s.element_scale = arr(p.element_scale, np.float64)
+        self._keep = keep
+        return s
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._lib.bddc_b200_destroy(h)
+            self._h = None
+
+    # --- structure and index maps (host) -----------------------------------
+    def structure(self) -> dict:
+        s = _Structure()
+        _check(self._lib.bddc_b200_structure_get(self._h, C.byref(s)))
+        return {n: getattr(s, n) for n, _ in _Structure._fields_}
+
+    def interface_dofs(self) -> np.ndarray:
+        n = self.structure()["interface_dofs"]
+        out = np.empty(n, dtype=np.int64)
+        _check(self._lib.bddc_b200_interface_dofs(self._h, out.ctypes.data_as(I64)))
+        return out
+
+    def _sub_array(self, fn, s):
+        dim = C.c_int64()
+        _check(self._lib.bddc_b200_subdomain_dim(self._h, s, C.byref(dim)))
+        out = np.empty(dim.value, dtype=np.int64)
+        _check(fn(self._h, s, out.ctypes.data_as(I64)))
+        return out
+
+    def local_to_wc(self, s) -> np.ndarray:
+        return self._sub_array(self._lib.bddc_b200_local_to_wc, s)
+
+    def global_dof(self, s) -> np.ndarray:
+        return self._sub_array(self._lib.bddc_b200_global_dof, s)
+
+    def globs(self):
+        n = C.c_int64()
+        _check(self._lib.bddc_b200_glob_count(self._h, C.byref(n)))
+        out = []
+        for g in range(n.value):
+            kind, nn, ns = C.c_int(), C.c_int64(), C.c_int64()
+            _check(self._lib.bddc_b200_glob_info(self._h, g, C.byref(kind), C.byref(nn), C.byref(ns)))
+            nodes = np.empty(nn.value, dtype=np.int64)
+            subs = np.empty(ns.value, dtype=np.int64)
+            _check(self._lib.bddc_b200_glob_nodes(self._h, g, nodes.ctypes.data_as(I64),
+                                                   subs.ctypes.data_as(I64)))
+            out.append((("corner", "edge", "face")[kind.value], nodes.tolist(), tuple(subs.tolist())))
+        return out
+
+    # --- constraints (constraints.cpp) --------------------------------------
+    def arithmetic_constraints(self, edge_globs: bool, face_globs: bool):
+        _check(self._lib.bddc_b200_constraints_arithmetic(self._h, int(edge_globs), int(face_globs)))
+
+    def constraint_rows(self) -> int:
+        r = C.c_int64()
+        _check(self._lib.bddc_b200_constraint_rows(self._h, C.byref(r)))
+        return r.value
+
+    def constraints(self):
+        n = C.c_int64()
+        _check(self._lib.bddc_b200_constraint_count(self._h, C.byref(n)))
+        out = []
+        for a in range(n.value):
+            g, nw = C.c_int(), C.c_int64()
+            _check(self._lib.bddc_b200_constraint_get(self._h, a, C.byref(g), C.byref(nw), None))
+            w = np.empty(nw.value)
+            _check(self._lib.bddc_b200_constraint_get(self._h, a, C.byref(g), C.byref(nw), _dptr(w)))
+            out.append((g.value, w))
+        return out
+
+    # --- device path ---------------------------------------------------------
+    def analysis(self):
+        _check(self._lib.bddc_b200_analysis(self._h))
+
+    def enrich(self, tau=10.0, max_vectors=15, keep_edge=False, fixed_count=-1,
+               indicator_only=False) -> float:
+        om = C.c_double()
+        _check(self._lib.bddc_b200_enrich(self._h, tau, max_vectors, int(keep_edge), fixed_count,
+                                          int(indicator_only), C.byref(om)))
+        return om.value
+
+    def pair_reports(self):
+        n = C.c_int64()
+        _check(self._lib.bddc_b200_pair_count(self._h, C.byref(n)))
+        out = []
+        for k in range(n.value):
+            si, sj, enf, sat = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+            om, ne = C.c_double(), C.c_int64()
+            _check(self._lib.bddc_b200_pair_report(self._h, k, C.byref(si), C.byref(sj), C.byref(enf),
+                                                   C.byref(om), C.byref(sat), C.byref(ne), None))
+            ev = np.empty(ne.value)
+            _check(self._lib.bddc_b200_pair_report(self._h, k, C.byref(si), C.byref(sj), C.byref(enf),
+                                                   C.byref(om), C.byref(sat), C.byref(ne), _dptr(ev)))
+            out.append(dict(si=si.value, sj=sj.value, enforced=enf.value, omega_next=om.value,
+                            saturated=bool(sat.value), eigenvalues=ev))
+        return out
+
+    def setup_preconditioner(self):
+        _check(self._lib.bddc_b200_setup_preconditioner(self._h))
+
+    @property
+    def interface_size(self) -> int:
+        n = C.c_int64()
+        _check(self._lib.bddc_b200_interface_size(self._h, C.byref(n)))
+        return n.value
+
+    def schur_apply(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x)
+        _check(self._lib.bddc_b200_schur_apply(self._h, _dptr(x), _dptr(y)))
+        return y
+
+    def precond_apply(self, r: np.ndarray) -> np.ndarray:
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        z = np.empty_like(r)
+        _check(self._lib.bddc_b200_precond_apply(self._h, _dptr(r), _dptr(z)))
+        return z
+
+    def rhs(self) -> np.ndarray:
+        out = np.empty(self.interface_size)
+        _check(self._lib.bddc_b200_rhs(self._h, _dptr(out)))
+        return out
+
+    def recover(self, u_interface: np.ndarray) -> np.ndarray:
+        u_interface = np.ascontiguousarray(u_interface, dtype=np.float64)
+        out = np.empty(self.structure()["free_dofs"])
+        _check(self._lib.bddc_b200_recover(self._h, _dptr(u_interface), _dptr(out)))
+        return out
+
+    def pcg(self, b: Optional[np.ndarray] = None, tolerance=1e-8, max_iterations=500,
+            preconditioned_residual=False):
+        """Returns (x, iterations, relres, kappa, converged, alphas, betas)."""
+        n = self.interface_size
+        x = np.empty(n)
+        res = _PcgResult()
+        al = np.empty(max_iterations + 1)
+        be = np.empty(max_iterations + 1)
+        bp = None
+        if b is not None:
+            b = np.ascontiguousarray(b, dtype=np.float64)
+            bp = _dptr(b)
+        rc = self._lib.bddc_b200_pcg(self._h, bp, _dptr(x), tolerance, max_iterations,
+                                     int(preconditioned_residual), C.byref(res), _dptr(al), _dptr(be))
+        if rc not in (0, 9):
+            _check(rc)
+        it = res.iterations
+        return dict(x=x, iterations=it, relative_residual=res.relative_residual,
+                    condition_estimate=res.condition_estimate, converged=bool(res.converged),
+                    alphas=al[:it].copy(), betas=be[:it].copy())
+
+    def run_item(self, mode: str, tau: float = 10.0, max_vectors: int = 15, keep_edge=False,
+                 base_faces=False) -> Row:
+        """One work item of `run_items` (`experiment.cpp:143-205`)."""
+        r = _Row()
+        _check(self._lib.bddc_b200_run_item(self._h, mode.encode(), tau, max_vectors, int(keep_edge),
+                                            int(base_faces), C.byref(r)))
+        label = ("inf" if math.isinf(tau) else "%.4g" % tau) if mode == "adaptive" else mode
+        return Row(label, r.omega_tilde, r.constraint_rows, r.kappa, r.iterations, bool(r.converged),
+                   r.seconds_analysis, r.seconds_factorization, r.seconds_iterations, r.seconds_total,
+                   r.seconds_eigen, r.seconds_preconditioner, r.root_size)
+
+    def times(self) -> dict:
+        out = np.zeros(8)
+        _check(self._lib.bddc_b200_times(self._h, _dptr(out)))
+        keys = ("analysis", "eigen", "preconditioner", "pcg", "leaf_flops", "leaf_front_bytes",
+                "schur_bytes", "root_size")
+        return dict(zip(keys, out.tolist()))

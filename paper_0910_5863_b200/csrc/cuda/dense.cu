@@ -1,0 +1,370 @@
+// Batched FP64 partial Cholesky and front solves on sm_100a (see dense.cuh).
+//
+// Algorithm: left-looking tiled Cholesky over 64x64 tiles.
+//   for each eliminated tile column j:
+//     k_syrk_column : C_ij -= L_i,[0:j) L_j,[0:j)^T  for all i >= j  (DMMA GEMM, K = 64 j)
+//     k_panel       : L_jj = chol(C_jj);  L_ij = C_ij L_jj^{-T};  Dinv_j = L_jj^{-1}
+//   k_syrk_trailing : S_ab -= L_a,[0:p) L_b,[0:p)^T for trailing tiles a >= b  (K = p)
+// The GEMM tiles stream 64x32 operand panels through a two-stage cp.async
+// pipeline into padded shared memory (ld 68 doubles: conflict-free fragment
+// loads) and issue mma.sync.aligned.m16n8k16.f64 (FP64 tensor cores).
+#include "dense.cuh"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace b200 {
+
+namespace {
+
+constexpr int LDS = 68;          // padded smem leading dimension (doubles)
+constexpr int KC = 32;           // K chunk per pipeline stage
+constexpr int GEMM_THREADS = 128;
+
+__device__ __forceinline__ void dmma(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+        "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Warp-level 32x32 slice of a 64x64 tile product over `kdim` (multiple of 16):
+// acc[m][n] += sum_k As[k*LDS + m] * Bs[k*LDS + n].
+__device__ __forceinline__ void warp_mma(const double* As, const double* Bs, int kdim,
+                                         double (&acc)[2][4][4]) {
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) & 3;
+  const int g = lane >> 2, t0 = lane & 3;
+  const int m0 = (warp & 1) * 32, n0 = (warp >> 1) * 32;
+#pragma unroll 2
+  for (int kk = 0; kk < kdim; kk += 16) {
+    double a[2][8], b[4][4];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        a[mi][v] = As[(kk + t0 + 4 * (v >> 1)) * LDS + m0 + mi * 16 + g + 8 * (v & 1)];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) b[ni][v] = Bs[(kk + t0 + 4 * v) * LDS + n0 + ni * 8 + g];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+  }
+}
+
+// Visit the accumulator elements with their tile coordinates.
+template <class F>
+__device__ __forceinline__ void for_acc(double (&acc)[2][4][4], F f) {
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) & 3;
+  const int g = lane >> 2, t0 = lane & 3;
+  const int m0 = (warp & 1) * 32, n0 = (warp >> 1) * 32;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        f(m0 + mi * 16 + g + 8 * (v >> 1), n0 + ni * 8 + 2 * t0 + (v & 1), acc[mi][ni][v]);
+}
+
+// C[i0:i0+64, j0:j0+64] -= A[i0:i0+64, 0:K] * A[j0:j0+64, 0:K]^T  (A column-major, ld)
+__device__ void tile_update(double* a, int ld, int i0, int j0, int K) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                       // [2][KC*LDS]
+  double* Bs = smem + 2 * KC * LDS;        // [2][KC*LDS]
+  double acc[2][4][4];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[mi][ni][v] = 0.0;
+  const int nchunks = K / KC;
+  auto load = [&](int c, int buf) {
+    const int k0 = c * KC;
+    for (int q = threadIdx.x; q < KC * 32; q += GEMM_THREADS) {
+      const int col = q >> 5, part = q & 31;
+      const double* srcA = a + (size_t)(k0 + col) * ld + i0 + part * 2;
+      const double* srcB = a + (size_t)(k0 + col) * ld + j0 + part * 2;
+      cp_async16(As + buf * KC * LDS + col * LDS + part * 2, srcA);
+      cp_async16(Bs + buf * KC * LDS + col * LDS + part * 2, srcB);
+    }
+    cp_async_commit();
+  };
+  if (nchunks > 0) load(0, 0);
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      load(c + 1, (c + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    warp_mma(As + (c & 1) * KC * LDS, Bs + (c & 1) * KC * LDS, KC, acc);
+    __syncthreads();
+  }
+  for_acc(acc, [&](int m, int n, double v) { a[(size_t)(j0 + n) * ld + i0 + m] -= v; });
+}
+
+__global__ void __launch_bounds__(GEMM_THREADS) k_syrk_column(const FrontDesc* ds, int j) {
+  const FrontDesc d = ds[blockIdx.y];
+  const int i = j + blockIdx.x;
+  if (j * kTile >= d.p || i * kTile >= d.n) return;
+  tile_update(d.a, d.n, i * kTile, j * kTile, j * kTile);
+}
+
+__global__ void __launch_bounds__(GEMM_THREADS) k_syrk_trailing(const FrontDesc* ds) {
+  const FrontDesc d = ds[blockIdx.y];
+  const int pt = d.p / kTile, m = d.n / kTile - pt;
+  const long t = blockIdx.x;
+  if (d.p == 0 || t >= (long)m * (m + 1) / 2) return;
+  int ii = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((long)ii * (ii + 1) / 2 > t) --ii;
+  while ((long)(ii + 1) * (ii + 2) / 2 <= t) ++ii;
+  const int jj = static_cast<int>(t - (long)ii * (ii + 1) / 2);
+  tile_update(d.a, d.n, (pt + ii) * kTile, (pt + jj) * kTile, d.p);
+}
+
+// Panel step: every CTA of tile column j factors the diagonal tile in shared
+// memory (redundantly, avoiding a launch), then solves its own tile.
+__global__ void __launch_bounds__(GEMM_THREADS) k_panel(const FrontDesc* ds, int j) {
+  const FrontDesc d = ds[blockIdx.y];
+  const int i = j + blockIdx.x;
+  if (j * kTile >= d.p || i * kTile >= d.n) return;
+  extern __shared__ __align__(16) double smem[];
+  double* L = smem;               // 64 x LDS, column-major: L[c*LDS + r]
+  double* X = smem + 64 * LDS;    // 64 x LDS
+  const int tid = threadIdx.x;
+  const size_t ld = d.n;
+  const double* diag = d.a + (size_t)(j * kTile) * ld + j * kTile;
+  for (int e = tid; e < 64 * 64; e += GEMM_THREADS) L[(e >> 6) * LDS + (e & 63)] = diag[(size_t)(e >> 6) * ld + (e & 63)];
+  __syncthreads();
+  // POTRF (lower), right-looking within the tile
+  bool bad = false;
+  for (int k = 0; k < 64; ++k) {
+    const double dkk = L[k * LDS + k];
+    __syncthreads();
+    bad |= !(dkk > 0.0);
+    const double sk = dkk > 0.0 ? sqrt(dkk) : 1.0;
+    if (tid < 64) {
+      if (tid > k) L[k * LDS + tid] /= sk;
+      else if (tid == k) L[k * LDS + k] = sk;
+    }
+    __syncthreads();
+    for (int e = tid; e < 64 * 64; e += GEMM_THREADS) {
+      const int r = e & 63, c = e >> 6;
+      if (c > k && r >= c) L[c * LDS + r] -= L[k * LDS + r] * L[k * LDS + c];
+    }
+    __syncthreads();
+    if (bad && tid == 0 && i == j) atomicCAS(d.info, 0, j * kTile + k + 1);
+    if (bad) break;
+  }
+  if (bad) return;
+  if (i == j) {
+    // Dinv = L^{-1}.  The diagonal tile itself is never read again (solves and
+    // later updates touch only off-diagonal tiles), and other CTAs of this
+    // launch still read the unfactored C_jj, so it is not written back.
+    // Thread r forms row r of L^{-T} by forward substitution: x L^T = e_r.
+    if (tid < 64) {
+      const int r = tid;
+      for (int c = 0; c < 64; ++c) {
+        double s = (c == r) ? 1.0 : 0.0;
+        for (int k = 0; k < c; ++k) s -= X[k * LDS + r] * L[k * LDS + c];
+        X[c * LDS + r] = s / L[c * LDS + c];
+      }
+    }
+    __syncthreads();
+    // X = L^{-T} (row-major view: X[c*LDS+r] = (L^{-T})[r][c]); Dinv = L^{-1} = X^T
+    double* dv = d.dinv + (size_t)j * 64 * 64;
+    for (int e = tid; e < 64 * 64; e += GEMM_THREADS) {
+      const int r = e & 63, c = e >> 6;     // Dinv[r][c] = (L^{-T})[c][r] = X[r*LDS + c]
+      dv[(size_t)c * 64 + r] = X[r * LDS + c];
+    }
+    return;
+  }
+  // off-diagonal: X = C L^{-T}; thread r solves row r: x L^T = c_r
+  const double* ct = d.a + (size_t)(j * kTile) * ld + i * kTile;
+  for (int e = tid; e < 64 * 64; e += GEMM_THREADS) X[(e >> 6) * LDS + (e & 63)] = ct[(size_t)(e >> 6) * ld + (e & 63)];
+  __syncthreads();
+  if (tid < 64) {
+    const int r = tid;
+    for (int c = 0; c < 64; ++c) {
+      double s0 = X[c * LDS + r], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int k = 0;
+      for (; k + 4 <= c; k += 4) {
+        s0 -= X[k * LDS + r] * L[k * LDS + c];
+        s1 -= X[(k + 1) * LDS + r] * L[(k + 1) * LDS + c];
+        s2 -= X[(k + 2) * LDS + r] * L[(k + 2) * LDS + c];
+        s3 -= X[(k + 3) * LDS + r] * L[(k + 3) * LDS + c];
+      }
+      for (; k < c; ++k) s0 -= X[k * LDS + r] * L[k * LDS + c];
+      X[c * LDS + r] = ((s0 + s1) + (s2 + s3)) / L[c * LDS + c];
+    }
+  }
+  __syncthreads();
+  double* out = d.a + (size_t)(j * kTile) * ld + i * kTile;
+  for (int e = tid; e < 64 * 64; e += GEMM_THREADS) out[(size_t)(e >> 6) * ld + (e & 63)] = X[(e >> 6) * LDS + (e & 63)];
+}
+
+// ---------------------------------------------------------------------------
+// Front solves: one CTA per front, vector staged in shared memory.
+// ---------------------------------------------------------------------------
+constexpr int SOLVE_THREADS = 256;
+
+__global__ void __launch_bounds__(SOLVE_THREADS) k_front_forward(const SolveDesc* ds, const int* done) {
+  if (done && *done) return;
+  const SolveDesc d = ds[blockIdx.x];
+  extern __shared__ double xs[];
+  double* z = xs + d.n;  // 64 scratch
+  const int tid = threadIdx.x;
+  for (int r = tid; r < d.n; r += SOLVE_THREADS) xs[r] = d.x[r];
+  __syncthreads();
+  const size_t ld = d.n;
+  for (int kb = 0; kb < d.p / kTile; ++kb) {
+    const int k0 = kb * kTile;
+    // z = Dinv_kb * x[k0:k0+64]: 4 threads per output row
+    {
+      const int row = tid >> 2, part = tid & 3;
+      const double* dv = d.dinv + (size_t)kb * 64 * 64;
+      double s = 0.0;
+      for (int c = part; c < 64; c += 4) s += dv[(size_t)c * 64 + row] * xs[k0 + c];
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (part == 0) z[row] = s;
+    }
+    __syncthreads();
+    if (tid < 64) xs[k0 + tid] = z[tid];
+    // x[r] -= sum_c L[r, k0+c] z[c] for rows below the block
+    for (int r = k0 + kTile + tid; r < d.n; r += SOLVE_THREADS) {
+      const double* col = d.a + (size_t)k0 * ld + r;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < 64; c += 2) {
+        s0 += col[(size_t)c * ld] * z[c];
+        s1 += col[(size_t)(c + 1) * ld] * z[c + 1];
+      }
+      xs[r] -= s0 + s1;
+    }
+    __syncthreads();
+  }
+  for (int r = tid; r < d.n; r += SOLVE_THREADS) d.x[r] = xs[r];
+}
+
+__global__ void __launch_bounds__(SOLVE_THREADS) k_front_backward(const SolveDesc* ds, const int* done) {
+  if (done && *done) return;
+  const SolveDesc d = ds[blockIdx.x];
+  extern __shared__ double xs[];
+  double* t = xs + d.n;  // 64 scratch
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int r = tid; r < d.n; r += SOLVE_THREADS) {
+    double v = d.x[r];
+    if (d.cmap && r >= d.p) {
+      const int k = d.cmap[r - d.p];
+      v = k >= 0 ? d.croot[k] : 0.0;
+    }
+    xs[r] = v;
+  }
+  __syncthreads();
+  const size_t ld = d.n;
+  for (int kb = d.p / kTile - 1; kb >= 0; --kb) {
+    const int k0 = kb * kTile;
+    // t[c] = x[k0+c] - sum_{r >= k0+64} L[r, k0+c] x[r]   (warp per column)
+    for (int c = warp; c < 64; c += SOLVE_THREADS / 32) {
+      const double* col = d.a + (size_t)(k0 + c) * ld;
+      double s = 0.0;
+      for (int r = k0 + kTile + lane; r < d.n; r += 32) s += col[r] * xs[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) t[c] = xs[k0 + c] - s;
+    }
+    __syncthreads();
+    // x[k0:k0+64] = Dinv^T t
+    {
+      const int row = tid >> 2, part = tid & 3;
+      const double* dv = d.dinv + (size_t)kb * 64 * 64 + (size_t)row * 64;  // column `row` of Dinv
+      double s = 0.0;
+      for (int c = part; c < 64; c += 4) s += dv[c] * t[c];
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      __syncthreads();
+      if (part == 0) xs[k0 + row] = s;
+    }
+    __syncthreads();
+  }
+  for (int r = tid; r < d.n; r += SOLVE_THREADS) d.x[r] = xs[r];
+}
+
+__global__ void k_copy_trailing(const TrailDesc* ds) {
+  const TrailDesc d = ds[blockIdx.y];
+  const int m = d.n - d.p;
+  const long total = (long)m * m;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(e % m), c = static_cast<int>(e / m);
+    const int rr = r >= c ? r : c, cc = r >= c ? c : r;  // read the lower triangle
+    d.s[e] = d.a[(size_t)(d.p + cc) * d.n + d.p + rr];
+  }
+}
+
+int g_smem_configured = 0;
+void configure() {
+  if (g_smem_configured) return;
+  const int gemm_smem = 4 * KC * LDS * sizeof(double);
+  cudaFuncSetAttribute(k_syrk_column, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
+  cudaFuncSetAttribute(k_syrk_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
+  cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
+  cudaFuncSetAttribute(k_front_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  g_smem_configured = 1;
+}
+
+}  // namespace
+
+void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p, int max_m,
+                      cudaStream_t stream) {
+  if (batch == 0) return;
+  configure();
+  const int gemm_smem = 4 * KC * LDS * sizeof(double);
+  const int panel_smem = 2 * 64 * LDS * sizeof(double);
+  const int nt = max_n / kTile, pt = max_p / kTile;
+  for (int j = 0; j < pt; ++j) {
+    if (j > 0) k_syrk_column<<<dim3(nt - j, batch), GEMM_THREADS, gemm_smem, stream>>>(d_descs, j);
+    k_panel<<<dim3(nt - j, batch), GEMM_THREADS, panel_smem, stream>>>(d_descs, j);
+  }
+  // trailing tiles: worst case over the batch is bounded by the largest trailing block
+  const long mt = max_m / kTile;
+  const long max_tr = mt * (mt + 1) / 2;
+  if (max_p > 0 && max_tr > 0) k_syrk_trailing<<<dim3(static_cast<unsigned>(max_tr), batch), GEMM_THREADS, gemm_smem, stream>>>(d_descs);
+}
+
+void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
+  if (batch == 0) return;
+  configure();
+  k_front_forward<<<batch, SOLVE_THREADS, (max_n + 64) * sizeof(double), stream>>>(d_descs, done);
+}
+
+void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
+  if (batch == 0) return;
+  configure();
+  k_front_backward<<<batch, SOLVE_THREADS, (max_n + 64) * sizeof(double), stream>>>(d_descs, done);
+}
+
+void copy_trailing_full(const TrailDesc* d_descs, int batch, int max_m, cudaStream_t stream) {
+  if (batch == 0) return;
+  const long total = (long)max_m * max_m;
+  const int blocks = static_cast<int>(std::min<long>((total + 255) / 256, 1024));
+  k_copy_trailing<<<dim3(blocks, batch), 256, 0, stream>>>(d_descs);
+}
+
+}  // namespace b200

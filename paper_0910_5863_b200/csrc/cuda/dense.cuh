@@ -1,0 +1,65 @@
+// Batched dense FP64 kernels for the adaptive-BDDC fronts (sm_100a).
+//
+// A "front" is a dense symmetric matrix, column-major, padded to a multiple of
+// 64, whose first p columns are eliminated by Cholesky (partial factorization):
+//
+//      [ A_ee  .   ]      [ L_ee   .  ]  [ L_ee^T  L_ce^T ]
+//      [ A_ce A_cc ]  ->  [ L_ce   I  ]  [   0     S_cc   ]
+//
+// leaving the Schur complement S_cc = A_cc - L_ce L_ce^T in the trailing block
+// (lower tiles; diagonal tiles full).  The same kernels factor the substructure
+// leaves (A_II eliminated -> interface Schur S_s), the transformed leaf fronts of
+// the preconditioner, the root front, and the pair reductions of the adaptive
+// eigenproblems.  Tile updates run on FP64 tensor cores (DMMA,
+// mma.sync.m16n8k16.f64); see DESIGN.md "Kernels".
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace b200 {
+
+constexpr int kTile = 64;
+
+struct FrontDesc {
+  double* a;      // n x n column-major (ld = n)
+  double* dinv;   // (p/64) inverses of the diagonal L tiles, 64x64 column-major each
+  int n;          // padded dimension (multiple of 64)
+  int p;          // eliminated columns (multiple of 64, <= n)
+  int* info;      // 0, or 1 + first failing pivot column
+  int pad_;
+};
+
+struct SolveDesc {
+  const double* a;
+  const double* dinv;
+  double* x;      // length n
+  int n;
+  int p;
+  const int* cmap;      // optional (backward): x[p+c] = cmap[c] >= 0 ? croot[cmap[c]] : 0
+  const double* croot;
+};
+
+/// Partial Cholesky of a batch of fronts (device descriptor array).
+/// max_n/max_p bound the descriptors' n/p.  Launches on `stream`.
+/// max_m bounds the trailing dimension n - p.
+void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p, int max_m,
+                      cudaStream_t stream);
+
+/// Forward sweep x <- [L_ee^{-1} x_e ; x_c - L_ce L_ee^{-1} x_e] per front.
+void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream,
+                   const int* done = nullptr);
+/// Backward sweep x_e <- L_ee^{-T} (x_e - L_ce^T x_c) per front (x_c given).
+void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream,
+                    const int* done = nullptr);
+
+/// Symmetric copy of each front's trailing block into a dense full matrix.
+struct TrailDesc {
+  const double* a;  // front (ld = n)
+  double* s;        // output m x m, ld = m, where m = n - p
+  int n;
+  int p;
+};
+void copy_trailing_full(const TrailDesc* d_descs, int batch, int max_m, cudaStream_t stream);
+
+}  // namespace b200

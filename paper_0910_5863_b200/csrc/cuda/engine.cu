@@ -1,0 +1,1090 @@
+// Device engine: analysis (leaf factorization + interface Schur), the
+// transformed preconditioner (leaf fronts + dense root), and a device-resident
+// PCG whose iteration is one captured CUDA graph.  See engine.hpp and
+// DESIGN.md "Data layout" for the arenas used below.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "pairs.cuh"
+
+namespace b200 {
+
+void cuda_check(cudaError_t e, const char* file, int line) {
+  if (e != cudaSuccess)
+    throw Error(kCudaError, std::string("CUDA error ") + cudaGetErrorString(e) + " at " + file + ":" +
+                                std::to_string(line));
+}
+#define CK(x) ::b200::cuda_check((x), __FILE__, __LINE__)
+
+namespace {
+
+constexpr int kRed = 256;  // blocks of the deterministic dot-product reductions
+
+inline int rup(int v, int m) { return (v + m - 1) / m * m; }
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  std::size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(std::size_t k) {
+    release();
+    n = k;
+    if (k) CK(cudaMalloc(&p, k * sizeof(T)));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    if (v.size() != n) alloc(v.size());
+    if (n) CK(cudaMemcpyAsync(p, v.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void zero(cudaStream_t s) {
+    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+struct PcgState {
+  double rz, pq, alpha, beta, bnorm, ref, relres, tol;
+  int it, max_it, done, precond_residual;
+};
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+struct ScatterDesc {
+  const int* ptr;
+  const int* idx;
+  const double* val;
+  const int* pos;   // local dof -> dense position
+  double* a;
+  int n, ld, nI, PI, nB;
+};
+
+__global__ void k_scatter_csr(const ScatterDesc* ds) {
+  const ScatterDesc d = ds[blockIdx.y];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < d.ld; r += gridDim.x * blockDim.x) {
+    if (r < d.n) {
+      const int pr = d.pos[r];
+      for (int t = d.ptr[r]; t < d.ptr[r + 1]; ++t) d.a[(size_t)d.pos[d.idx[t]] * d.ld + pr] = d.val[t];
+    }
+    const bool pad = (r >= d.nI && r < d.PI) || (r >= d.PI + d.nB);
+    if (pad) d.a[(size_t)r * d.ld + r] = 1.0;
+  }
+}
+
+struct SubDesc {        // per-subdomain pointers used by the PCG kernels
+  const double* S;      // PB x PB full interface Schur
+  double* F;            // transformed leaf front
+  double* FV;           // F-layout vector
+  const int* biface;    // nB: interface index of each boundary dof
+  const double* bw;     // nB: averaging weights
+  const int* posF;      // nB: F position
+  const int* bglob;     // nB: transform instance or -1
+  const int* bslot;     // nB: slot within the glob
+  double* WB;           // nB: boundary scratch
+  int nB, PB, NF, PE;
+};
+
+struct XformDesc {      // glob transforms, flat
+  const int* inst_tr;
+  const int* inst_pos;  // per instance: offset into tpos
+  const int* tpos;      // glob slot -> boundary position
+  const int* tr_n;
+  const int* tr_r;
+  const int* tr_off_perm;
+  const int* tr_off_d;
+  const int* perm;
+  const int* iperm;
+  const double* D;      // r x n row-major per transform (= t_perm rows 0..r-1)
+};
+
+// y = T^T v on the glob blocks of one boundary position b (transform.cpp:94-149)
+__device__ __forceinline__ double xform_T_t(const XformDesc& x, int inst, int j, const double* v) {
+  const int tr = x.inst_tr[inst];
+  const int* pos = x.tpos + x.inst_pos[inst];
+  const int n = x.tr_n[tr], r = x.tr_r[tr];
+  const int* perm = x.perm + x.tr_off_perm[tr];
+  const double* D = x.D + x.tr_off_d[tr];
+  double s = j >= r ? v[pos[perm[j]]] : 0.0;
+  for (int i = 0; i < r; ++i) s += D[i * n + j] * v[pos[perm[i]]];
+  return s;
+}
+// x_orig = T x_new at glob slot a
+__device__ __forceinline__ double xform_T(const XformDesc& x, int inst, int a, const double* xn) {
+  const int tr = x.inst_tr[inst];
+  const int* pos = x.tpos + x.inst_pos[inst];
+  const int n = x.tr_n[tr], r = x.tr_r[tr];
+  const int i = x.iperm[x.tr_off_perm[tr] + a];
+  if (i >= r) return xn[pos[i]];
+  const double* D = x.D + x.tr_off_d[tr] + i * n;
+  double s = 0.0;
+  for (int jj = 0; jj < n; ++jj) s += D[jj] * xn[pos[jj]];
+  return s;
+}
+
+// Schur apply, step 1: WB_s = S_s * p[biface]   (schur.cpp:12-36 with S_s dense)
+__global__ void __launch_bounds__(256) k_schur_gemv(const SubDesc* sd, const double* __restrict__ p, const int* done) {
+  if (done && *done) return;
+  const SubDesc d = sd[blockIdx.x];
+  extern __shared__ double xs[];
+  for (int c = threadIdx.x; c < d.nB; c += blockDim.x) xs[c] = p[d.biface[c]];
+  __syncthreads();
+  for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
+    const double* col = d.S + b;
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    int c = 0;
+    for (; c + 4 <= d.nB; c += 4) {
+      s0 += col[(size_t)c * d.PB] * xs[c];
+      s1 += col[(size_t)(c + 1) * d.PB] * xs[c + 1];
+      s2 += col[(size_t)(c + 2) * d.PB] * xs[c + 2];
+      s3 += col[(size_t)(c + 3) * d.PB] * xs[c + 3];
+    }
+    for (; c < d.nB; ++c) s0 += col[(size_t)c * d.PB] * xs[c];
+    d.WB[b] = (s0 + s1) + (s2 + s3);
+  }
+}
+
+__device__ __forceinline__ void block_partial(double v, double* partials) {
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < (blockDim.x >> 5) ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) partials[blockIdx.x] = v;
+  }
+}
+
+__device__ __forceinline__ double sum_partials(const double* partials) {
+  // fixed-order tree over kRed partials by one block of kRed threads
+  __shared__ double red[kRed];
+  red[threadIdx.x] = partials[threadIdx.x];
+  __syncthreads();
+  for (int s = kRed / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  return red[0];
+}
+
+// out[i] = sum over the copies of interface dof i of src[pos]; optional dot with `other`
+__global__ void __launch_bounds__(256) k_sum_copies(i64 n, const int* __restrict__ ptr, const int* __restrict__ pos,
+                                                    const double* __restrict__ src, double* out,
+                                                    const double* other, double* partials, const int* done) {
+  if (done && *done) return;
+  double acc = 0.0;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int t = ptr[i]; t < ptr[i + 1]; ++t) s += src[pos[t]];
+    out[i] = s;
+    if (other) acc += s * other[i];
+  }
+  if (partials) block_partial(acc, partials);
+}
+
+__global__ void k_dot(i64 n, const double* a, const double* b, double* partials) {
+  double acc = 0.0;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) acc += a[i] * b[i];
+  block_partial(acc, partials);
+}
+
+__global__ void k_alpha(PcgState* st, const double* partials, double* alphas) {
+  if (st->done) return;
+  const double pq = sum_partials(partials);
+  if (threadIdx.x == 0) {
+    st->pq = pq;
+    st->alpha = st->rz / pq;
+    alphas[st->it] = st->alpha;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_axpy(i64 n, PcgState* st, double* x, double* r, const double* p,
+                                              const double* q, double* partials) {
+  if (st->done) return;
+  const double a = st->alpha;
+  double acc = 0.0;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    x[i] += a * p[i];
+    const double ri = r[i] - a * q[i];
+    r[i] = ri;
+    acc += ri * ri;
+  }
+  block_partial(acc, partials);
+}
+
+__global__ void k_beta(PcgState* st, const double* prz, const double* prr, double* betas) {
+  if (st->done) return;
+  const double rz_next = sum_partials(prz);
+  __syncthreads();
+  const double rr = sum_partials(prr);
+  if (threadIdx.x == 0) {
+    const double beta = rz_next / st->rz;
+    st->beta = beta;
+    betas[st->it] = beta;
+    st->rz = rz_next;
+    st->it += 1;
+    const double cur = st->precond_residual ? sqrt(fmax(rz_next, 0.0)) : sqrt(rr);
+    st->relres = cur / st->ref;
+    if (st->relres <= st->tol || st->it >= st->max_it) st->done = 1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_update_p(i64 n, const PcgState* st, double* p, const double* z) {
+  if (st->done) return;
+  const double b = st->beta;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) p[i] = z[i] + b * p[i];
+}
+
+// restrict_residual (bddc_operator.cpp:52-68) restricted to the interface:
+// FV_s = P_F T_s^T (w_s * r|_s), pads zero.
+__global__ void __launch_bounds__(256) k_restrict(const SubDesc* sd, XformDesc x, const double* __restrict__ r, const int* done) {
+  if (done && *done) return;
+  const SubDesc d = sd[blockIdx.x];
+  extern __shared__ double sm[];
+  double* v = sm;
+  for (int b = threadIdx.x; b < d.nB; b += blockDim.x) v[b] = d.bw[b] * r[d.biface[b]];
+  for (int q = threadIdx.x; q < d.NF; q += blockDim.x) d.FV[q] = 0.0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
+    const int inst = d.bglob[b];
+    const double y = inst < 0 ? v[b] : xform_T_t(x, inst, d.bslot[b], v);
+    d.FV[d.posF[b]] = y;
+  }
+}
+
+// prolong (bddc_operator.cpp:87-99): WB_s = w_s * T_s x_s   (then summed over copies)
+__global__ void __launch_bounds__(256) k_prolong(const SubDesc* sd, XformDesc x, const int* done) {
+  if (done && *done) return;
+  const SubDesc d = sd[blockIdx.x];
+  extern __shared__ double sm[];
+  double* xn = sm;
+  for (int b = threadIdx.x; b < d.nB; b += blockDim.x) xn[b] = d.FV[d.posF[b]];
+  __syncthreads();
+  for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
+    const int inst = d.bglob[b];
+    const double xo = inst < 0 ? xn[b] : xform_T(x, inst, d.bslot[b], xn);
+    d.WB[b] = d.bw[b] * xo;
+  }
+}
+
+// root right-hand side: sum of the leaves' coarse residuals (deterministic CSR)
+__global__ void k_root_gather(int n_root, int NR, const int* __restrict__ ptr, const long long* __restrict__ src,
+                              const double* __restrict__ fv, double* xr, const int* done) {
+  if (done && *done) return;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < NR; k += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    if (k < n_root)
+      for (int t = ptr[k]; t < ptr[k + 1]; ++t) s += fv[src[t]];
+    xr[k] = s;
+  }
+}
+
+// Guarded wrappers around the front solves (skip when PCG is done)
+__global__ void k_noop() {}
+
+// F_s column transform: X = S T (glob columns), other columns copied
+__global__ void k_colxform(const SubDesc* sd, XformDesc x, double* Xarena, const long long* xoff) {
+  const SubDesc d = sd[blockIdx.y];
+  double* X = Xarena + xoff[blockIdx.y];
+  const int c = blockIdx.x;
+  if (c >= d.PB) return;
+  const int inst = c < d.nB ? d.bglob[c] : -1;
+  if (inst < 0) {
+    for (int b = threadIdx.x; b < d.PB; b += blockDim.x) X[(size_t)c * d.PB + b] = d.S[(size_t)c * d.PB + b];
+    return;
+  }
+  const int j = d.bslot[c];
+  const int tr = x.inst_tr[inst];
+  const int* pos = x.tpos + x.inst_pos[inst];
+  const int n = x.tr_n[tr], r = x.tr_r[tr];
+  const int* perm = x.perm + x.tr_off_perm[tr];
+  const double* D = x.D + x.tr_off_d[tr];
+  for (int b = threadIdx.x; b < d.PB; b += blockDim.x) {
+    double s = j >= r ? d.S[(size_t)pos[perm[j]] * d.PB + b] : 0.0;
+    for (int i = 0; i < r; ++i) s += D[i * n + j] * d.S[(size_t)pos[perm[i]] * d.PB + b];
+    X[(size_t)c * d.PB + b] = s;
+  }
+}
+
+// F = P_F (T^T X) P_F^T with identity pads
+__global__ void k_rowxform_scatter(const SubDesc* sd, XformDesc x, const double* Xarena, const long long* xoff) {
+  const SubDesc d = sd[blockIdx.y];
+  const double* X = Xarena + xoff[blockIdx.y];
+  const int c = blockIdx.x;
+  if (c < d.nB) {
+    const double* col = X + (size_t)c * d.PB;
+    const size_t fc = (size_t)d.posF[c] * d.NF;
+    for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
+      const int inst = d.bglob[b];
+      const double v = inst < 0 ? col[b] : xform_T_t(x, inst, d.bslot[b], col);
+      d.F[fc + d.posF[b]] = v;
+    }
+  }
+  // the padding positions of F get identity entries in k_pad_identity
+}
+
+__global__ void k_pad_identity(double* F, int NF, const int* pads, int npads) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < npads; t += gridDim.x * blockDim.x) {
+    const int q = pads[t];
+    F[(size_t)q * NF + q] = 1.0;
+  }
+}
+
+struct RootAsm {
+  const int* ptr;          // root dof -> [ptr, ptr+1) entries
+  const int* sub;          // subdomain of the entry (ascending)
+  const int* cidx;         // coarse index within that leaf
+  const long long* foff;   // per subdomain: F arena offset
+  const int* NF;
+  const int* PE;
+};
+
+__global__ void k_root_assemble(int n_root, int NR, RootAsm ra, const double* Farena, double* R) {
+  const long total = (long)n_root * (n_root + 1) / 2;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
+    int k1 = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((long)k1 * (k1 + 1) / 2 > t) --k1;
+    while ((long)(k1 + 1) * (k1 + 2) / 2 <= t) ++k1;
+    const int k2 = static_cast<int>(t - (long)k1 * (k1 + 1) / 2);
+    double s = 0.0;
+    int a = ra.ptr[k1], b = ra.ptr[k2];
+    const int ae = ra.ptr[k1 + 1], be = ra.ptr[k2 + 1];
+    while (a < ae && b < be) {
+      const int sa = ra.sub[a], sb = ra.sub[b];
+      if (sa < sb) {
+        ++a;
+      } else if (sb < sa) {
+        ++b;
+      } else {
+        const int c1 = ra.cidx[a], c2 = ra.cidx[b];
+        const int hi = c1 >= c2 ? c1 : c2, lo = c1 >= c2 ? c2 : c1;
+        const int NF = ra.NF[sa], PE = ra.PE[sa];
+        s += Farena[ra.foff[sa] + (size_t)(PE + lo) * NF + PE + hi];
+        ++a;
+        ++b;
+      }
+    }
+    R[(size_t)k2 * NR + k1] = s;
+  }
+  for (long q = n_root + blockIdx.x * (long)blockDim.x + threadIdx.x; q < NR; q += (long)gridDim.x * blockDim.x)
+    R[(size_t)q * NR + q] = 1.0;
+}
+
+__global__ void k_extract_boundary(const SubDesc* sd, const double* MV, const long long* mvoff, const int* PI) {
+  const SubDesc d = sd[blockIdx.x];
+  for (int b = threadIdx.x; b < d.nB; b += blockDim.x) d.WB[b] = MV[mvoff[blockIdx.x] + PI[blockIdx.x] + b];
+}
+
+__global__ void k_insert_boundary(const SubDesc* sd, double* MV, const long long* mvoff, const int* PI,
+                                  const double* u_iface) {
+  const SubDesc d = sd[blockIdx.x];
+  for (int b = threadIdx.x; b < d.nB; b += blockDim.x) MV[mvoff[blockIdx.x] + PI[blockIdx.x] + b] = u_iface[d.biface[b]];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Device state
+// ---------------------------------------------------------------------------
+struct DeviceState {
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int nsub = 0;
+  i64 niface = 0;
+  std::vector<int> nI, nB, PI, PB, NM;
+  std::vector<long long> m_off, dm_off, s_off, wb_off, mv_off;
+  int max_NM = 0, max_PI = 0, max_PB = 0, max_nB = 0;
+  DBuf<double> M, DinvM, S, MV, WB;
+  DBuf<int> minfo;
+  DBuf<FrontDesc> mfront;
+  DBuf<SolveDesc> msolve;
+  DBuf<long long> d_mvoff;
+  DBuf<int> d_PI;
+  // interface maps
+  DBuf<int> biface, bposF, bglob, bslot, icopy_ptr, icopy_pos;
+  DBuf<double> bw;
+  DBuf<double> rhs;  // condensed rhs (interface)
+  // preconditioner
+  bool have_prec = false;
+  std::vector<int> NF, PE, nE, nC;
+  std::vector<long long> f_off, df_off, fv_off;
+  int max_NF = 0, max_PE = 0, max_M = 0;
+  DBuf<double> F, DinvF, FV, Xtmp;
+  DBuf<long long> d_xoff;
+  DBuf<int> finfo;
+  DBuf<FrontDesc> ffront;
+  DBuf<SolveDesc> fsolve_fwd, fsolve_bwd;
+  DBuf<SubDesc> subdesc;
+  // transforms
+  DBuf<int> inst_tr, inst_pos, tpos, tr_n, tr_r, tr_off_perm, tr_off_d, perm, iperm, cmap;
+  DBuf<double> trD;
+  XformDesc xf{};
+  // root
+  int n_root = 0, NR = 0;
+  DBuf<double> R, DinvR, xroot;
+  DBuf<int> rinfo, root_ptr, root_sub, root_c, d_NF, d_PE;
+  DBuf<long long> root_src, d_foff;
+  DBuf<FrontDesc> rfront;
+  DBuf<SolveDesc> rsolve;
+  // pcg
+  DBuf<double> vx, vr, vz, vp, vq, vb, part_a, part_b, alphas, betas;
+  DBuf<PcgState> pst;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int graph_max_it = -1;
+  // adaptive pair machinery
+  PairEngine pairs;
+
+  ~DeviceState() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+Engine::Engine(const Model& m) : m_(m), d_(new DeviceState) {
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+    throw Error(kCudaError, "no CUDA device: the B200 path has no CPU fallback");
+  CK(cudaStreamCreateWithFlags(&d_->st, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&d_->e0));
+  CK(cudaEventCreate(&d_->e1));
+}
+
+Engine::~Engine() = default;
+
+cudaStream_t Engine::stream() const { return d_->st; }
+i64 Engine::interface_size() const { return static_cast<i64>(m_.maps.interface_dofs.size()); }
+int Engine::root_size() const { return d_->n_root; }
+
+namespace {
+double elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  CK(cudaEventSynchronize(b));
+  CK(cudaEventElapsedTime(&ms, a, b));
+  return ms * 1e-3;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// analysis: A_s -> dense fronts -> partial Cholesky (eliminate interior)
+// ---------------------------------------------------------------------------
+void Engine::analysis() {
+  DeviceState& D = *d_;
+  const Model& m = m_;
+  D.nsub = static_cast<int>(m.subs.size());
+  D.niface = interface_size();
+  const int ns = D.nsub;
+  D.nI.resize(ns);
+  D.nB.resize(ns);
+  D.PI.resize(ns);
+  D.PB.resize(ns);
+  D.NM.resize(ns);
+  D.m_off.resize(ns);
+  D.dm_off.resize(ns);
+  D.s_off.resize(ns);
+  D.wb_off.resize(ns);
+  D.mv_off.resize(ns);
+  long long mo = 0, dmo = 0, so = 0, wbo = 0, mvo = 0;
+  for (int s = 0; s < ns; ++s) {
+    const Subdomain& S = m.subs[s];
+    D.nI[s] = static_cast<int>(S.interior.size());
+    D.nB[s] = static_cast<int>(S.boundary.size());
+    D.PI[s] = rup(D.nI[s], kTile);
+    D.PB[s] = rup(std::max(D.nB[s], 1), kTile);
+    D.NM[s] = D.PI[s] + D.PB[s];
+    D.m_off[s] = mo;
+    mo += (long long)D.NM[s] * D.NM[s];
+    D.dm_off[s] = dmo;
+    dmo += (long long)(D.PI[s] / kTile) * kTile * kTile;
+    D.s_off[s] = so;
+    so += (long long)D.PB[s] * D.PB[s];
+    D.wb_off[s] = wbo;
+    wbo += D.nB[s];
+    D.mv_off[s] = mvo;
+    mvo += D.NM[s];
+    D.max_NM = std::max(D.max_NM, D.NM[s]);
+    D.max_PI = std::max(D.max_PI, D.PI[s]);
+    D.max_PB = std::max(D.max_PB, D.PB[s]);
+    D.max_nB = std::max(D.max_nB, D.nB[s]);
+  }
+  cudaStream_t st = D.st;
+  CK(cudaEventRecord(D.e0, st));
+  D.M.alloc(mo);
+  D.M.zero(st);
+  D.DinvM.alloc(std::max<long long>(dmo, 1));
+  D.S.alloc(so);
+  D.MV.alloc(mvo);
+  D.WB.alloc(std::max<long long>(wbo, 1));
+  // CSR upload with dense positions
+  std::vector<int> ptr, idx, pos;
+  std::vector<double> val;
+  std::vector<long long> ptr_off(ns), idx_off(ns), pos_off(ns);
+  for (int s = 0; s < ns; ++s) {
+    const Subdomain& S = m.subs[s];
+    ptr_off[s] = ptr.size();
+    idx_off[s] = idx.size();
+    pos_off[s] = pos.size();
+    ptr.insert(ptr.end(), S.A.ptr.begin(), S.A.ptr.end());
+    idx.insert(idx.end(), S.A.idx.begin(), S.A.idx.end());
+    val.insert(val.end(), S.A.val.begin(), S.A.val.end());
+    std::vector<int> p(S.dim());
+    for (int r = 0; r < D.nI[s]; ++r) p[S.interior[r]] = r;
+    for (int b = 0; b < D.nB[s]; ++b) p[S.boundary[b]] = D.PI[s] + b;
+    pos.insert(pos.end(), p.begin(), p.end());
+  }
+  DBuf<int> dptr, didx, dpos;
+  DBuf<double> dval;
+  dptr.upload(ptr, st);
+  didx.upload(idx, st);
+  dpos.upload(pos, st);
+  dval.upload(val, st);
+  std::vector<ScatterDesc> sc(ns);
+  std::vector<FrontDesc> fd(ns);
+  std::vector<SolveDesc> sv(ns);
+  std::vector<TrailDesc> td(ns);
+  D.minfo.alloc(ns);
+  D.minfo.zero(st);
+  for (int s = 0; s < ns; ++s) {
+    sc[s] = ScatterDesc{dptr.p + ptr_off[s], didx.p + idx_off[s], dval.p + idx_off[s], dpos.p + pos_off[s],
+                        D.M.p + D.m_off[s], m.subs[s].dim(), D.NM[s], D.nI[s], D.PI[s], D.nB[s]};
+    fd[s] = FrontDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.NM[s], D.PI[s], D.minfo.p + s, 0};
+    sv[s] = SolveDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.MV.p + D.mv_off[s], D.NM[s], D.PI[s],
+                      nullptr, nullptr};
+    td[s] = TrailDesc{D.M.p + D.m_off[s], D.S.p + D.s_off[s], D.NM[s], D.PI[s]};
+  }
+  DBuf<ScatterDesc> dsc;
+  DBuf<TrailDesc> dtd;
+  dsc.upload(sc, st);
+  D.mfront.upload(fd, st);
+  D.msolve.upload(sv, st);
+  dtd.upload(td, st);
+  k_scatter_csr<<<dim3(8, ns), 256, 0, st>>>(dsc.p);
+  CK(cudaGetLastError());
+  partial_cholesky(D.mfront.p, ns, D.max_NM, D.max_PI, D.max_PB, st);
+  CK(cudaGetLastError());
+  copy_trailing_full(dtd.p, ns, D.max_PB, st);
+  CK(cudaGetLastError());
+  // interface maps
+  std::vector<int> biface(wbo), icp(D.niface + 1, 0), icpos;
+  std::vector<double> bw(wbo);
+  for (int s = 0; s < ns; ++s) {
+    const Subdomain& S = m.subs[s];
+    for (int b = 0; b < D.nB[s]; ++b) {
+      const i64 g = S.global_dof[S.boundary[b]];
+      biface[D.wb_off[s] + b] = static_cast<int>(m.maps.global_to_interface[g]);
+      // averaging weight: A_s(l,l) / sum over copies (spaces.cpp:71-86)
+      double tot = 0.0;
+      for (i64 t = m.maps.copy_ptr[g]; t < m.maps.copy_ptr[g + 1]; ++t)
+        tot += m.subs[m.maps.copy_sub[t]].A.diag(m.maps.copy_local[t]);
+      bw[D.wb_off[s] + b] = S.A.diag(S.boundary[b]) / tot;
+    }
+  }
+  // interface dof -> WB positions of its copies, ascending subdomain
+  std::vector<std::vector<int>> lists(D.niface);
+  for (int s = 0; s < ns; ++s)
+    for (int b = 0; b < D.nB[s]; ++b) lists[biface[D.wb_off[s] + b]].push_back(static_cast<int>(D.wb_off[s] + b));
+  for (i64 i = 0; i < D.niface; ++i) {
+    icp[i + 1] = icp[i] + static_cast<int>(lists[i].size());
+    icpos.insert(icpos.end(), lists[i].begin(), lists[i].end());
+  }
+  D.biface.upload(biface, st);
+  D.bw.upload(bw, st);
+  D.icopy_ptr.upload(icp, st);
+  D.icopy_pos.upload(icpos, st);
+  // condensed rhs: forward sweep on [f_I; f_B] then sum the boundary rows
+  std::vector<double> mv(mvo, 0.0);
+  for (int s = 0; s < ns; ++s) {
+    const Subdomain& S = m.subs[s];
+    for (int r = 0; r < D.nI[s]; ++r) mv[D.mv_off[s] + r] = S.load[S.interior[r]];
+    for (int b = 0; b < D.nB[s]; ++b) mv[D.mv_off[s] + D.PI[s] + b] = S.load[S.boundary[b]];
+  }
+  D.MV.upload(mv, st);
+  front_forward(D.msolve.p, ns, D.max_NM, st);
+  // per-subdomain descriptors (partial, preconditioner fields filled later)
+  std::vector<SubDesc> sd(ns);
+  for (int s = 0; s < ns; ++s)
+    sd[s] = SubDesc{D.S.p + D.s_off[s], nullptr, nullptr, D.biface.p + D.wb_off[s], D.bw.p + D.wb_off[s],
+                    nullptr, nullptr, nullptr, D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], 0, 0};
+  D.subdesc.upload(sd, st);
+  D.d_mvoff.upload(D.mv_off, st);
+  D.d_PI.upload(D.PI, st);
+  k_extract_boundary<<<ns, 256, 0, st>>>(D.subdesc.p, D.MV.p, D.d_mvoff.p, D.d_PI.p);
+  D.rhs.alloc(std::max<i64>(D.niface, 1));
+  k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, D.rhs.p, nullptr, nullptr, nullptr);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(D.e1, st));
+  times_.analysis = elapsed(D.e0, D.e1);
+  std::vector<int> info(ns);
+  CK(cudaMemcpy(info.data(), D.minfo.p, ns * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int s = 0; s < ns; ++s)
+    if (info[s]) throw Error(kNotPositiveDefinite, "factorize: A_II of substructure " + std::to_string(s) +
+                                                       " is not positive definite");
+  double fl = 0;
+  for (int s = 0; s < ns; ++s) {
+    const double ni = D.nI[s], nb = D.nB[s];
+    fl += ni * ni * ni / 3.0 + ni * ni * nb + ni * nb * nb;
+  }
+  times_.flops_leaf = fl;
+  // pair engine needs the interface Schur complements
+  D.pairs.attach(m, D.S.p, D.s_off, D.PB, D.nB, st);
+}
+
+double Engine::schur_bytes() const {
+  double b = 0;
+  for (int s = 0; s < d_->nsub; ++s) b += double(d_->nB[s]) * d_->nB[s] * 8.0;
+  return b;
+}
+
+double Engine::leaf_front_bytes() const {
+  const DeviceState& D = *d_;
+  double b = 0;
+  for (int s = 0; s < D.nsub && s < (int)D.NF.size(); ++s) {
+    const double e = D.nE[s], c = D.nC[s];
+    b += (e * (e + 1) / 2 + c * e) * 8.0;
+  }
+  b += double(D.n_root) * (D.n_root + 1) / 2 * 8.0;
+  return b;
+}
+
+// ---------------------------------------------------------------------------
+// set_constraints: change of variables, transformed leaf fronts, dense root
+// ---------------------------------------------------------------------------
+void Engine::set_constraints(const ConstraintSet& cs) {
+  DeviceState& D = *d_;
+  const Model& m = m_;
+  const int ns = D.nsub;
+  cudaStream_t st = D.st;
+  CK(cudaEventRecord(D.e0, st));
+  const ChangeOfVariables cov = change_of_variables(cs, m);
+  // boundary position of each local dof
+  std::vector<std::vector<int>> bpos_of(ns);
+  for (int s = 0; s < ns; ++s) {
+    bpos_of[s].assign(m.subs[s].dim(), -1);
+    for (int b = 0; b < D.nB[s]; ++b) bpos_of[s][m.subs[s].boundary[b]] = b;
+  }
+  // transforms (flat) and per-subdomain instances
+  std::vector<int> tr_n, tr_r, tr_off_perm, tr_off_d, perm, iperm, inst_tr, inst_pos, tpos;
+  std::vector<double> trD;
+  std::vector<long long> wbo(D.wb_off);
+  std::vector<int> bglob(D.WB.n, -1), bslot(D.WB.n, -1);
+  for (std::size_t k = 0; k < cov.transforms.size(); ++k) {
+    const GlobTransform& gt = cov.transforms[k];
+    const int n = gt.n, r = gt.rank;
+    tr_n.push_back(n);
+    tr_r.push_back(r);
+    tr_off_perm.push_back(static_cast<int>(perm.size()));
+    tr_off_d.push_back(static_cast<int>(trD.size()));
+    std::vector<int> ip(n);
+    for (int i = 0; i < n; ++i) ip[gt.perm[i]] = i;
+    perm.insert(perm.end(), gt.perm.begin(), gt.perm.end());
+    iperm.insert(iperm.end(), ip.begin(), ip.end());
+    for (int i = 0; i < r; ++i)  // D[i][j] = t_perm[i][j] = t[perm[i]][j]
+      for (int j = 0; j < n; ++j) trD.push_back(gt.t[std::size_t(gt.perm[i]) * n + j]);
+    const auto dofs = m.glob_free_dofs(gt.glob);
+    for (int s : m.globs[gt.glob].subdomains) {
+      const int inst = static_cast<int>(inst_tr.size());
+      inst_tr.push_back(static_cast<int>(k));
+      inst_pos.push_back(static_cast<int>(tpos.size()));
+      for (int a = 0; a < n; ++a) {
+        const int b = bpos_of[s][m.maps.local_of(dofs[a], s)];
+        tpos.push_back(b);
+        bglob[D.wb_off[s] + b] = inst;
+        bslot[D.wb_off[s] + b] = a;
+      }
+    }
+  }
+  // coarse dofs per subdomain: corners (ascending corner id), then explicit dofs (group order)
+  std::vector<std::vector<int>> coarse_b(ns), coarse_root(ns);
+  const i64 ncd = m.maps.corner_dof_count;
+  for (int s = 0; s < ns; ++s) {
+    const Subdomain& S = m.subs[s];
+    std::vector<std::pair<i64, int>> cors;
+    for (int b = 0; b < D.nB[s]; ++b) {
+      const i64 cid = m.maps.corner_dof_of_global[S.global_dof[S.boundary[b]]];
+      if (cid >= 0) cors.emplace_back(cid, b);
+    }
+    std::sort(cors.begin(), cors.end());
+    for (auto& [cid, b] : cors) {
+      coarse_b[s].push_back(b);
+      coarse_root[s].push_back(static_cast<int>(cid));
+    }
+  }
+  for (std::size_t g = 0; g < cov.groups.size(); ++g)
+    for (std::size_t t = 0; t < cov.group_subs[g].size(); ++t) {
+      const int s = cov.group_subs[g][t];
+      coarse_b[s].push_back(bpos_of[s][cov.group_local[g][t]]);
+      coarse_root[s].push_back(static_cast<int>(ncd + g));
+    }
+  D.n_root = static_cast<int>(ncd + cov.groups.size());
+  D.NR = rup(std::max(D.n_root, 1), kTile);
+  // F layout
+  D.NF.assign(ns, 0);
+  D.PE.assign(ns, 0);
+  D.nE.assign(ns, 0);
+  D.nC.assign(ns, 0);
+  D.f_off.assign(ns, 0);
+  D.df_off.assign(ns, 0);
+  D.fv_off.assign(ns, 0);
+  std::vector<int> posF(D.WB.n, 0), cmap, pads;
+  std::vector<long long> cmap_off(ns), pad_off(ns + 1), xoff(ns);
+  long long fo = 0, dfo = 0, fvo = 0, xo = 0;
+  D.max_NF = D.max_PE = D.max_M = 0;
+  std::vector<int> root_cnt(D.n_root + 1, 0);
+  for (int s = 0; s < ns; ++s) {
+    const int nB = D.nB[s], nC = static_cast<int>(coarse_b[s].size()), nE = nB - nC;
+    D.nE[s] = nE;
+    D.nC[s] = nC;
+    D.PE[s] = rup(nE, kTile);
+    D.NF[s] = D.PE[s] + rup(std::max(nC, 1), kTile);
+    D.f_off[s] = fo;
+    fo += (long long)D.NF[s] * D.NF[s];
+    D.df_off[s] = dfo;
+    dfo += (long long)(D.PE[s] / kTile) * kTile * kTile;
+    D.fv_off[s] = fvo;
+    fvo += D.NF[s];
+    xoff[s] = xo;
+    xo += (long long)D.PB[s] * D.PB[s];
+    D.max_NF = std::max(D.max_NF, D.NF[s]);
+    D.max_PE = std::max(D.max_PE, D.PE[s]);
+    D.max_M = std::max(D.max_M, D.NF[s] - D.PE[s]);
+    std::vector<int> is_coarse(nB, -1);
+    for (int c = 0; c < nC; ++c) is_coarse[coarse_b[s][c]] = c;
+    int e = 0;
+    for (int b = 0; b < nB; ++b)
+      posF[D.wb_off[s] + b] = is_coarse[b] >= 0 ? D.PE[s] + is_coarse[b] : e++;
+    cmap_off[s] = cmap.size();
+    for (int c = 0; c < D.NF[s] - D.PE[s]; ++c) cmap.push_back(c < nC ? coarse_root[s][c] : -1);
+    pad_off[s] = pads.size();
+    for (int q = nE; q < D.PE[s]; ++q) pads.push_back(q);
+    for (int q = D.PE[s] + nC; q < D.NF[s]; ++q) pads.push_back(q);
+    for (int c = 0; c < nC; ++c) ++root_cnt[coarse_root[s][c] + 1];
+  }
+  pad_off[ns] = pads.size();
+  // root CSR (entries ascending by subdomain)
+  std::vector<int> rptr(D.n_root + 1, 0);
+  for (int k = 0; k < D.n_root; ++k) rptr[k + 1] = rptr[k] + root_cnt[k + 1];
+  std::vector<int> rsub(rptr.back()), rc(rptr.back());
+  std::vector<long long> rsrc(rptr.back());
+  {
+    std::vector<int> fill(rptr.begin(), rptr.end() - 1);
+    for (int s = 0; s < ns; ++s)
+      for (int c = 0; c < D.nC[s]; ++c) {
+        const int k = coarse_root[s][c];
+        rsub[fill[k]] = s;
+        rc[fill[k]] = c;
+        rsrc[fill[k]] = D.fv_off[s] + D.PE[s] + c;
+        ++fill[k];
+      }
+  }
+  // uploads
+  D.bposF.upload(posF, st);
+  D.bglob.upload(bglob, st);
+  D.bslot.upload(bslot, st);
+  auto up_i = [&](DBuf<int>& b, const std::vector<int>& v) {
+    if (v.empty()) b.alloc(1); else b.upload(v, st);
+  };
+  up_i(D.inst_tr, inst_tr);
+  up_i(D.inst_pos, inst_pos);
+  up_i(D.tpos, tpos);
+  up_i(D.tr_n, tr_n);
+  up_i(D.tr_r, tr_r);
+  up_i(D.tr_off_perm, tr_off_perm);
+  up_i(D.tr_off_d, tr_off_d);
+  up_i(D.perm, perm);
+  up_i(D.iperm, iperm);
+  up_i(D.cmap, cmap);
+  if (trD.empty()) D.trD.alloc(1); else D.trD.upload(trD, st);
+  D.xf = XformDesc{D.inst_tr.p, D.inst_pos.p, D.tpos.p, D.tr_n.p, D.tr_r.p, D.tr_off_perm.p, D.tr_off_d.p,
+                   D.perm.p, D.iperm.p, D.trD.p};
+  D.F.alloc(fo);
+  D.F.zero(st);
+  D.DinvF.alloc(std::max<long long>(dfo, 1));
+  D.FV.alloc(fvo);
+  D.Xtmp.alloc(xo);
+  D.d_xoff.upload(xoff, st);
+  D.finfo.alloc(ns);
+  D.finfo.zero(st);
+  std::vector<SubDesc> sd(ns);
+  std::vector<FrontDesc> fd(ns);
+  std::vector<SolveDesc> fw(ns), bw(ns);
+  for (int s = 0; s < ns; ++s) {
+    sd[s] = SubDesc{D.S.p + D.s_off[s], D.F.p + D.f_off[s], D.FV.p + D.fv_off[s], D.biface.p + D.wb_off[s],
+                    D.bw.p + D.wb_off[s], D.bposF.p + D.wb_off[s], D.bglob.p + D.wb_off[s],
+                    D.bslot.p + D.wb_off[s], D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], D.NF[s], D.PE[s]};
+    fd[s] = FrontDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.NF[s], D.PE[s], D.finfo.p + s, 0};
+    fw[s] = SolveDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.FV.p + D.fv_off[s], D.NF[s], D.PE[s],
+                      nullptr, nullptr};
+  }
+  D.subdesc.upload(sd, st);
+  D.ffront.upload(fd, st);
+  D.fsolve_fwd.upload(fw, st);
+  // root front
+  D.R.alloc((size_t)D.NR * D.NR);
+  D.R.zero(st);
+  D.DinvR.alloc((size_t)D.NR * kTile);
+  D.xroot.alloc(D.NR);
+  D.rinfo.alloc(1);
+  D.rinfo.zero(st);
+  for (int s = 0; s < ns; ++s) {
+    bw[s] = fw[s];
+    bw[s].cmap = D.cmap.p + cmap_off[s];
+    bw[s].croot = D.xroot.p;
+  }
+  D.fsolve_bwd.upload(bw, st);
+  up_i(D.root_ptr, rptr);
+  up_i(D.root_sub, rsub);
+  up_i(D.root_c, rc);
+  if (rsrc.empty()) D.root_src.alloc(1); else D.root_src.upload(rsrc, st);
+  D.d_foff.upload(D.f_off, st);
+  up_i(D.d_NF, D.NF);
+  up_i(D.d_PE, D.PE);
+  DBuf<int> dpads;
+  up_i(dpads, pads);
+  // F = P (T^T S T) P^T, pads identity
+  k_colxform<<<dim3(D.max_PB, ns), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
+  k_rowxform_scatter<<<dim3(D.max_PB, ns), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
+  for (int s = 0; s < ns; ++s) {
+    const int np = static_cast<int>(pad_off[s + 1] - pad_off[s]);
+    if (np) k_pad_identity<<<1, 128, 0, st>>>(D.F.p + D.f_off[s], D.NF[s], dpads.p + pad_off[s], np);
+  }
+  CK(cudaGetLastError());
+  partial_cholesky(D.ffront.p, ns, D.max_NF, D.max_PE, D.max_M, st);
+  CK(cudaGetLastError());
+  RootAsm ra{D.root_ptr.p, D.root_sub.p, D.root_c.p, D.d_foff.p, D.d_NF.p, D.d_PE.p};
+  k_root_assemble<<<1024, 256, 0, st>>>(D.n_root, D.NR, ra, D.F.p, D.R.p);
+  std::vector<FrontDesc> rf{FrontDesc{D.R.p, D.DinvR.p, D.NR, D.NR, D.rinfo.p, 0}};
+  D.rfront.upload(rf, st);
+  partial_cholesky(D.rfront.p, 1, D.NR, D.NR, 0, st);
+  std::vector<SolveDesc> rs{SolveDesc{D.R.p, D.DinvR.p, D.xroot.p, D.NR, D.NR, nullptr, nullptr}};
+  D.rsolve.upload(rs, st);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(D.e1, st));
+  times_.preconditioner = elapsed(D.e0, D.e1);
+  std::vector<int> info(ns);
+  CK(cudaMemcpy(info.data(), D.finfo.p, ns * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int s = 0; s < ns; ++s)
+    if (info[s]) throw Error(kNotPositiveDefinite, "factorize: transformed leaf front " + std::to_string(s) +
+                                                       " is not positive definite");
+  int rinfo = 0;
+  CK(cudaMemcpy(&rinfo, D.rinfo.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (rinfo) throw Error(kNotPositiveDefinite, "factorize: root front is not positive definite");
+  D.have_prec = true;
+  // invalidate a captured PCG graph (pointers changed)
+  if (D.gexec) {
+    cudaGraphExecDestroy(D.gexec);
+    D.gexec = nullptr;
+  }
+  if (D.graph) {
+    cudaGraphDestroy(D.graph);
+    D.graph = nullptr;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// operator applications
+// ---------------------------------------------------------------------------
+namespace {
+void launch_precond(DeviceState& D, const double* r, double* z, const double* dot_with, double* partials,
+                    const int* done) {
+  cudaStream_t st = D.st;
+  const int ns = D.nsub;
+  const int smem_b = D.max_nB * sizeof(double);
+  k_restrict<<<ns, 256, smem_b, st>>>(D.subdesc.p, D.xf, r, done);
+  front_forward(D.fsolve_fwd.p, ns, D.max_NF, st, done);
+  k_root_gather<<<std::max(1, std::min(1024, (D.NR + 255) / 256)), 256, 0, st>>>(D.n_root, D.NR, D.root_ptr.p,
+                                                                             D.root_src.p, D.FV.p, D.xroot.p, done);
+  front_forward(D.rsolve.p, 1, D.NR, st, done);
+  front_backward(D.rsolve.p, 1, D.NR, st, done);
+  front_backward(D.fsolve_bwd.p, ns, D.max_NF, st, done);
+  k_prolong<<<ns, 256, smem_b, st>>>(D.subdesc.p, D.xf, done);
+  k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, z, dot_with, partials, done);
+}
+
+void launch_schur(DeviceState& D, const double* x, double* y, const double* dot_with, double* partials,
+                  const int* done) {
+  cudaStream_t st = D.st;
+  k_schur_gemv<<<D.nsub, 256, D.max_nB * sizeof(double), st>>>(D.subdesc.p, x, done);
+  k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, y, dot_with, partials, done);
+}
+
+void ensure_vectors(DeviceState& D) {
+  const i64 n = std::max<i64>(D.niface, 1);
+  if (D.vx.n == std::size_t(n)) return;
+  D.vx.alloc(n);
+  D.vr.alloc(n);
+  D.vz.alloc(n);
+  D.vp.alloc(n);
+  D.vq.alloc(n);
+  D.vb.alloc(n);
+  D.part_a.alloc(kRed);
+  D.part_b.alloc(kRed);
+  D.pst.alloc(1);
+}
+}  // namespace
+
+void Engine::schur_apply(const double* x, double* y) {
+  DeviceState& D = *d_;
+  ensure_vectors(D);
+  const std::size_t bytes = D.niface * sizeof(double);
+  CK(cudaMemcpyAsync(D.vp.p, x, bytes, cudaMemcpyHostToDevice, D.st));
+  launch_schur(D, D.vp.p, D.vq.p, nullptr, nullptr, nullptr);
+  CK(cudaMemcpyAsync(y, D.vq.p, bytes, cudaMemcpyDeviceToHost, D.st));
+  CK(cudaStreamSynchronize(D.st));
+  CK(cudaGetLastError());
+}
+
+void Engine::precond_apply(const double* r, double* z) {
+  DeviceState& D = *d_;
+  if (!D.have_prec) throw Error(kError, "preconditioner not set up");
+  ensure_vectors(D);
+  const std::size_t bytes = D.niface * sizeof(double);
+  CK(cudaMemcpyAsync(D.vr.p, r, bytes, cudaMemcpyHostToDevice, D.st));
+  launch_precond(D, D.vr.p, D.vz.p, nullptr, nullptr, nullptr);
+  CK(cudaMemcpyAsync(z, D.vz.p, bytes, cudaMemcpyDeviceToHost, D.st));
+  CK(cudaStreamSynchronize(D.st));
+  CK(cudaGetLastError());
+}
+
+void Engine::rhs(double* out) {
+  DeviceState& D = *d_;
+  CK(cudaMemcpyAsync(out, D.rhs.p, D.niface * sizeof(double), cudaMemcpyDeviceToHost, D.st));
+  CK(cudaStreamSynchronize(D.st));
+}
+
+void Engine::recover(const double* u_interface, double* u_free) {
+  DeviceState& D = *d_;
+  const Model& m = m_;
+  const int ns = D.nsub;
+  ensure_vectors(D);
+  // forward sweep on the loads again (MV holds L_II^{-1} f_I in the interior rows)
+  std::vector<double> mv(D.MV.n, 0.0);
+  for (int s = 0; s < ns; ++s) {
+    const Subdomain& S = m.subs[s];
+    for (int r = 0; r < D.nI[s]; ++r) mv[D.mv_off[s] + r] = S.load[S.interior[r]];
+  }
+  D.MV.upload(mv, D.st);
+  front_forward(D.msolve.p, ns, D.max_NM, D.st);
+  CK(cudaMemcpyAsync(D.vx.p, u_interface, D.niface * sizeof(double), cudaMemcpyHostToDevice, D.st));
+  k_insert_boundary<<<ns, 256, 0, D.st>>>(D.subdesc.p, D.MV.p, D.d_mvoff.p, D.d_PI.p, D.vx.p);
+  front_backward(D.msolve.p, ns, D.max_NM, D.st);
+  CK(cudaMemcpyAsync(mv.data(), D.MV.p, mv.size() * sizeof(double), cudaMemcpyDeviceToHost, D.st));
+  CK(cudaStreamSynchronize(D.st));
+  CK(cudaGetLastError());
+  for (i64 i = 0; i < D.niface; ++i) u_free[m.maps.interface_dofs[i]] = u_interface[i];
+  for (int s = 0; s < ns; ++s) {
+    const Subdomain& S = m.subs[s];
+    for (int r = 0; r < D.nI[s]; ++r) u_free[S.global_dof[S.interior[r]]] = mv[D.mv_off[s] + r];
+  }
+}
+
+PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool precond_residual) {
+  DeviceState& D = *d_;
+  if (!D.have_prec) throw Error(kError, "preconditioner not set up");
+  ensure_vectors(D);
+  cudaStream_t st = D.st;
+  const i64 n = D.niface;
+  const std::size_t bytes = n * sizeof(double);
+  if (D.alphas.n < std::size_t(max_it + 1)) {
+    D.alphas.alloc(max_it + 1);
+    D.betas.alloc(max_it + 1);
+  }
+  CK(cudaEventRecord(D.e0, st));
+  if (b)
+    CK(cudaMemcpyAsync(D.vb.p, b, bytes, cudaMemcpyHostToDevice, st));
+  else
+    CK(cudaMemcpyAsync(D.vb.p, D.rhs.p, bytes, cudaMemcpyDeviceToDevice, st));
+  // r = b, x = 0, z = M r, p = z, rz = r.z   (pcg.cpp:32-41)
+  CK(cudaMemcpyAsync(D.vr.p, D.vb.p, bytes, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(D.vx.p, 0, bytes, st));
+  launch_precond(D, D.vr.p, D.vz.p, D.vr.p, D.part_a.p, nullptr);
+  CK(cudaMemcpyAsync(D.vp.p, D.vz.p, bytes, cudaMemcpyDeviceToDevice, st));
+  k_dot<<<kRed, 256, 0, st>>>(n, D.vb.p, D.vb.p, D.part_b.p);
+  std::vector<double> pa(kRed), pb(kRed);
+  CK(cudaMemcpyAsync(pa.data(), D.part_a.p, kRed * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(pb.data(), D.part_b.p, kRed * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // same fixed-order tree as sum_partials
+  auto tree = [](std::vector<double> v) {
+    for (int s = kRed / 2; s > 0; s >>= 1)
+      for (int i = 0; i < s; ++i) v[i] += v[i + s];
+    return v[0];
+  };
+  const double rz = tree(pa), bb = tree(pb);
+  PcgState h{};
+  h.rz = rz;
+  h.bnorm = std::sqrt(bb);
+  h.ref = precond_residual ? std::sqrt(std::max(rz, 0.0)) : h.bnorm;
+  h.tol = tol;
+  h.max_it = max_it;
+  h.precond_residual = precond_residual ? 1 : 0;
+  h.it = 0;
+  h.relres = 1.0;
+  h.done = (h.ref == 0.0 || h.relres <= tol || max_it <= 0) ? 1 : 0;
+  PcgOut out;
+  if (h.ref == 0.0) {  // zero right hand side
+    out.relative_residual = 0.0;
+    if (x) std::memset(x, 0, bytes);
+    return out;
+  }
+  CK(cudaMemcpyAsync(D.pst.p, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  // capture one iteration as a graph (pcg.cpp:49-70)
+  if (!D.gexec) {
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    const int* done = &D.pst.p->done;
+    launch_schur(D, D.vp.p, D.vq.p, D.vp.p, D.part_a.p, done);
+    k_alpha<<<1, kRed, 0, st>>>(D.pst.p, D.part_a.p, D.alphas.p);
+    k_axpy<<<kRed, 256, 0, st>>>(n, D.pst.p, D.vx.p, D.vr.p, D.vp.p, D.vq.p, D.part_b.p);
+    launch_precond(D, D.vr.p, D.vz.p, D.vr.p, D.part_a.p, done);
+    k_beta<<<1, kRed, 0, st>>>(D.pst.p, D.part_a.p, D.part_b.p, D.betas.p);
+    k_update_p<<<kRed, 256, 0, st>>>(n, D.pst.p, D.vp.p, D.vz.p);
+    CK(cudaStreamEndCapture(st, &D.graph));
+    CK(cudaGraphInstantiate(&D.gexec, D.graph, 0));
+  }
+  PcgState hs = h;
+  const int chunk = 8;
+  while (!hs.done) {
+    for (int c = 0; c < chunk; ++c) CK(cudaGraphLaunch(D.gexec, st));
+    CK(cudaMemcpyAsync(&hs, D.pst.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  CK(cudaEventRecord(D.e1, st));
+  times_.pcg = elapsed(D.e0, D.e1);
+  CK(cudaGetLastError());
+  out.iterations = hs.it;
+  out.relative_residual = hs.relres;
+  out.converged = hs.relres <= tol;
+  out.alphas.resize(hs.it);
+  out.betas.resize(hs.it);
+  if (hs.it) {
+    CK(cudaMemcpy(out.alphas.data(), D.alphas.p, hs.it * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out.betas.data(), D.betas.p, hs.it * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  out.condition_estimate = lanczos_condition_estimate(out.alphas, out.betas);
+  if (x) CK(cudaMemcpy(x, D.vx.p, bytes, cudaMemcpyDeviceToHost));
+  return out;
+}
+
+EnrichOutcome Engine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
+  CK(cudaEventRecord(d_->e0, d_->st));
+  EnrichOutcome out = d_->pairs.enrich(cs, o);
+  CK(cudaEventRecord(d_->e1, d_->st));
+  times_.eigen = elapsed(d_->e0, d_->e1);
+  return out;
+}
+
+}  // namespace b200

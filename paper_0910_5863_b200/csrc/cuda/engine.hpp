@@ -1,0 +1,95 @@
+// Device engine of the B200 adaptive-BDDC path.
+//
+// Owns all device state of one problem instance (one GPU, one stream) and
+// implements the hot path of SURVEY.md section 8(a):
+//   analysis()          HarmonicExtension ctor (spaces.cpp:108-147) + dense
+//                       interface Schur complements S_s (pair.cpp:32-63)
+//   set_constraints()   change_of_variables + BddcPreconditioner ctor
+//                       (transform.cpp:94-149, bddc_operator.cpp:38-50)
+//   schur_apply()       InterfaceProblem::apply (schur.cpp:12-36)
+//   precond_apply()     BddcPreconditioner::apply (bddc_operator.cpp:52-103)
+//   pcg()               pcg + lanczos_condition_estimate (pcg.cpp:11-77)
+//   rhs(), recover()    InterfaceProblem::rhs / recover (schur.cpp:38-75)
+//   enrich()            enrich_constraints / pair_indicator (adaptive.cpp:66-144)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "../host/host.hpp"
+#include "dense.cuh"
+
+namespace b200 {
+
+struct PcgOut {
+  int iterations = 0;
+  double relative_residual = 0;
+  bool converged = true;
+  std::vector<double> alphas, betas;
+  double condition_estimate = 1.0;
+};
+
+struct EnrichOptions {  // adaptive.hpp:24-29
+  double tau = 10.0;
+  int max_vectors = 15;
+  bool keep_edge_constraints = false;
+  int fixed_count = -1;
+  bool indicator_only = false;  // pair_indicator (no rows added)
+};
+
+struct PairReport {  // adaptive.hpp:14-22
+  int si = 0, sj = 0;
+  std::vector<double> eigenvalues;
+  int enforced = 0;
+  double omega_next = 0;
+  bool saturated = false;
+  int kept = 0, dropped = 0;
+};
+
+struct EnrichOutcome {
+  std::vector<PairReport> pairs;
+  double omega_tilde = 0;
+  i64 kept = 0, dropped = 0;
+};
+
+struct PhaseTimes {  // device-timed seconds (CUDA events) of the last calls
+  double analysis = 0, eigen = 0, preconditioner = 0, pcg = 0;
+  double flops_leaf = 0;   // algorithmic FP64 flops of the last leaf factorization
+};
+
+struct DeviceState;
+
+class Engine {
+ public:
+  explicit Engine(const Model& m);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  void analysis();
+  void set_constraints(const ConstraintSet& cs);
+  EnrichOutcome enrich(ConstraintSet& cs, const EnrichOptions& o);
+
+  void schur_apply(const double* x, double* y);      // host vectors, interface size
+  void precond_apply(const double* r, double* z);
+  void rhs(double* out);
+  void recover(const double* u_interface, double* u_free);
+  /// b == nullptr: use the condensed rhs on the device.  x may be nullptr.
+  PcgOut pcg(const double* b, double* x, double tol, int max_it, bool precond_residual = false);
+
+  i64 interface_size() const;
+  int root_size() const;
+  const PhaseTimes& times() const { return times_; }
+  double leaf_front_bytes() const;   // bytes of the preconditioner's leaf factors (+root)
+  double schur_bytes() const;        // bytes of the dense S_s read per Schur apply
+  cudaStream_t stream() const;
+
+ private:
+  const Model& m_;
+  std::unique_ptr<DeviceState> d_;
+  PhaseTimes times_;
+};
+
+}  // namespace b200
