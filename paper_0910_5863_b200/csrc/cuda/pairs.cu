@@ -1,9 +1,392 @@
-// Adaptive face eigenproblems on the device.
+// Adaptive face eigenproblems on the device (adaptive.cpp:30-125, pair.cpp:32-209).
+//
+// The reference forms, per face pair, the dense pencil (J^T S J, Z^T S Z) of
+// dimension ~2 n_B and eigendecomposes it twice on the host (dense_eig.cpp:77-126).
+// Here the same pencil is reduced exactly before any eigensolve:
+//   * lhs = J^T S J only involves the jump coordinates alpha of the shared globs
+//     (J = Z - avg Z vanishes on corner, continuous and outer columns), and
+//     lhs = K^T M K with M = 4 (D_{1-rho} S_i,ff D_{1-rho} + D_rho S_j,ff D_rho);
+//   * the Rayleigh quotient is maximized over the other coordinates, so rhs is
+//     replaced by its Schur complement B onto alpha: outer dofs of each side are
+//     eliminated from S_i, S_j (batched DMMA partial Cholesky), the two sides are
+//     glued in [corner | continuous | alpha] coordinates (Q), and corner +
+//     continuous are eliminated (partial Cholesky); the rigid-body null space of
+//     floating pairs is deflated exactly by a rank-nm shift sigma N N^T;
+//   * C = L^{-1} lhs L^{-T} (B = L L^T) is formed by two augmented partial
+//     factorizations and diagonalized by a parallel cyclic Jacobi sweep per pair;
+//   * eigenvectors map back by alpha = L^{-T} y, and the jump functional
+//     a = (1 - rho) d_i - rho d_j (adaptive.cpp:51-58) equals 1/2 M K alpha.
+// Eigenvalues, their count and the functionals match generalized_eig_sym
+// (modulo null(rhs)) in exact arithmetic; the host then runs the reference's
+// selection, splitting, normalization and rank filter unchanged.
 #include "pairs.cuh"
 
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "dense.cuh"
 #include "engine.hpp"
 
 namespace b200 {
+
+void cuda_check(cudaError_t e, const char* file, int line);
+#define CK(x) ::b200::cuda_check((x), __FILE__, __LINE__)
+
+namespace {
+
+inline int rup(int v, int m) { return (v + m - 1) / m * m; }
+
+template <class T>
+struct Buf {
+  T* p = nullptr;
+  std::size_t n = 0;
+  Buf() = default;
+  Buf(const Buf&) = delete;
+  ~Buf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(std::size_t k) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = k;
+    if (k) CK(cudaMalloc(&p, k * sizeof(T)));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    alloc(std::max<std::size_t>(v.size(), 1));
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+struct PairDev {
+  // sides
+  const double* S[2];   // interface Schur of each side (PB x PB)
+  int PB[2];
+  const int* pos[2];    // front index -> boundary position: [outer | corner | shared]
+  double* G[2];         // side fronts
+  int NG[2], PO[2], no[2];
+  int nc, nf, nj, nm, PQ, PJ, k;
+  double* Q;            // NQ = PQ + PJ
+  double* F3;           // 2 PJ
+  double* F4;           // 2 PJ
+  double* M;            // nf x nf
+  const double* K;      // nf x nj (column-major)
+  double* H;            // nf x nj scratch
+  const double* N;      // nm x (nc + nf) row-major, orthonormal
+  const double* rho;    // nf
+  double* A;            // Jacobi matrix (n2 x n2), n2 = even(nj)
+  double* V;            // Jacobi vectors
+  double* evals;        // k
+  double* vecs;         // 2PJ x k (solve vectors, column m at m*2PJ)
+  double* func;         // nf x k
+};
+
+// (a) side fronts: G_s[a][b] = S_s[pos a, pos b] with identity pads
+__global__ void k_gather_G(const PairDev* pd) {
+  const PairDev d = pd[blockIdx.y >> 1];
+  const int side = blockIdx.y & 1;
+  const int NG = d.NG[side], PO = d.PO[side], no = d.no[side], m1 = d.nc + d.nf;
+  const int col = blockIdx.x;
+  if (col >= NG) return;
+  auto valid = [&](int a) { return a < no || (a >= PO && a < PO + m1); };
+  auto bidx = [&](int a) { return a < no ? a : no + (a - PO); };
+  const int* pos = d.pos[side];
+  double* G = d.G[side] + (size_t)col * NG;
+  const bool vc = valid(col);
+  const double* Sc = vc ? d.S[side] + (size_t)pos[bidx(col)] * d.PB[side] : nullptr;
+  for (int r = threadIdx.x; r < NG; r += blockDim.x) {
+    double v;
+    if (vc && valid(r))
+      v = Sc[pos[bidx(r)]];
+    else
+      v = (r == col) ? 1.0 : 0.0;
+    G[r] = v;
+  }
+}
+
+__device__ __forceinline__ double hat(const PairDev& d, int side, int a, int b) {
+  // condensed side matrix (lower triangle of the trailing block)
+  const int hi = a >= b ? a : b, lo = a >= b ? b : a;
+  const int PO = d.PO[side], NG = d.NG[side];
+  return d.G[side][(size_t)(PO + lo) * NG + PO + hi];
+}
+
+// (c) M = 4 (D_{1-rho} C_i D_{1-rho} + D_rho C_j D_rho), C = original S on shared slots
+__global__ void k_build_M(const PairDev* pd) {
+  const PairDev d = pd[blockIdx.y];
+  const int nf = d.nf;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nf * nf; e += gridDim.x * blockDim.x) {
+    const int t = e % nf, u = e / nf;
+    const int base_i = d.no[0] + d.nc, base_j = d.no[1] + d.nc;
+    const double ci = d.S[0][(size_t)d.pos[0][base_i + u] * d.PB[0] + d.pos[0][base_i + t]];
+    const double cj = d.S[1][(size_t)d.pos[1][base_j + u] * d.PB[1] + d.pos[1][base_j + t]];
+    const double rt = d.rho[t], ru = d.rho[u];
+    d.M[(size_t)u * nf + t] = 4.0 * ((1.0 - rt) * (1.0 - ru) * ci + rt * ru * cj);
+  }
+}
+
+// (d1) H = (hat_i + hat_j)_ff K   (nf x nj)
+__global__ void k_build_H(const PairDev* pd) {
+  const PairDev d = pd[blockIdx.y];
+  const int nf = d.nf, nj = d.nj, nc = d.nc;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nf * nj; e += gridDim.x * blockDim.x) {
+    const int t = e % nf, b = e / nf;
+    double s = 0.0;
+    for (int u = 0; u < nf; ++u) {
+      const double kv = d.K[(size_t)b * nf + u];
+      if (kv != 0.0) s += (hat(d, 0, nc + t, nc + u) + hat(d, 1, nc + t, nc + u)) * kv;
+    }
+    d.H[(size_t)b * nf + t] = s;
+  }
+}
+
+// (d2) Q in [corner | continuous | pad | alpha | pad] coordinates (lower part + pads)
+__global__ void k_assemble_Q(const PairDev* pd) {
+  const PairDev d = pd[blockIdx.y];
+  const int nc = d.nc, nf = d.nf, nj = d.nj, m1 = nc + nf, PQ = d.PQ, NQ = d.PQ + d.PJ;
+  __shared__ double sig;
+  if (threadIdx.x == 0) sig = 0.0;
+  __syncthreads();
+  if (d.nm > 0) {  // sigma = max diagonal of the glued corner/continuous block
+    double mx = 0.0;
+    for (int a = threadIdx.x; a < m1; a += blockDim.x) mx = fmax(mx, hat(d, 0, a, a) + hat(d, 1, a, a));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ double wm[32];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, wm[w]);
+      sig = m;
+    }
+    __syncthreads();
+  }
+  const long total = (long)NQ * NQ;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(e % NQ), c = static_cast<int>(e / NQ);
+    if (r < c) continue;
+    double v = 0.0;
+    if (r < m1 && c < m1) {
+      v = hat(d, 0, r, c) + hat(d, 1, r, c);
+      for (int k = 0; k < d.nm; ++k) v += sig * d.N[(size_t)k * m1 + r] * d.N[(size_t)k * m1 + c];
+    } else if (r >= PQ && r < PQ + nj && c < m1) {
+      const int al = r - PQ;
+      for (int t = 0; t < nf; ++t) {
+        const double kv = d.K[(size_t)al * nf + t];
+        if (kv != 0.0) v += kv * (hat(d, 0, nc + t, c) - hat(d, 1, nc + t, c));
+      }
+    } else if (r >= PQ && r < PQ + nj && c >= PQ && c < PQ + nj) {
+      const int al = r - PQ, be = c - PQ;
+      for (int t = 0; t < nf; ++t) v += d.K[(size_t)al * nf + t] * d.H[(size_t)be * nf + t];
+    } else if (r == c) {
+      v = 1.0;  // pads
+    }
+    d.Q[(size_t)c * NQ + r] = v;
+  }
+}
+
+// (f) F3 = [[B, .], [lhs, 0]]  with lhs = K^T M K
+__global__ void k_build_F3(const PairDev* pd) {
+  const PairDev d = pd[blockIdx.y];
+  const int nj = d.nj, nf = d.nf, PJ = d.PJ, N2 = 2 * PJ, PQ = d.PQ, NQ = d.PQ + d.PJ;
+  const long total = (long)N2 * N2;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(e % N2), c = static_cast<int>(e / N2);
+    double v = 0.0;
+    if (r < PJ && c < PJ) {
+      if (r < nj && c < nj) {
+        const int hi = r >= c ? r : c, lo = r >= c ? c : r;
+        v = d.Q[(size_t)(PQ + lo) * NQ + PQ + hi];
+      } else {
+        v = r == c ? 1.0 : 0.0;
+      }
+    } else if (r >= PJ && c < PJ) {
+      const int al = r - PJ;
+      if (al < nj && c < nj) {  // (K^T M K)[al][c] = sum_t K[t][al] (M K)[t][c]; H holds M K here
+        for (int t = 0; t < nf; ++t) v += d.K[(size_t)al * nf + t] * d.H[(size_t)c * nf + t];
+      }
+    }
+    d.F3[(size_t)c * N2 + r] = v;
+  }
+}
+
+// H = M K (reuses the scratch after Q is assembled)
+__global__ void k_build_MK(const PairDev* pd) {
+  const PairDev d = pd[blockIdx.y];
+  const int nf = d.nf, nj = d.nj;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nf * nj; e += gridDim.x * blockDim.x) {
+    const int t = e % nf, b = e / nf;
+    double s = 0.0;
+    for (int u = 0; u < nf; ++u) {
+      const double kv = d.K[(size_t)b * nf + u];
+      if (kv != 0.0) s += d.M[(size_t)u * nf + t] * kv;
+    }
+    d.H[(size_t)b * nf + t] = s;
+  }
+}
+
+// (h) F4 = [[B, .], [W^T, 0]],  W = lhs L^{-T} from F3's factor
+__global__ void k_build_F4(const PairDev* pd) {
+  const PairDev d = pd[blockIdx.y];
+  const int nj = d.nj, PJ = d.PJ, N2 = 2 * PJ, PQ = d.PQ, NQ = d.PQ + d.PJ;
+  const long total = (long)N2 * N2;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(e % N2), c = static_cast<int>(e / N2);
+    double v = 0.0;
+    if (r < PJ && c < PJ) {
+      if (r < nj && c < nj) {
+        const int hi = r >= c ? r : c, lo = r >= c ? c : r;
+        v = d.Q[(size_t)(PQ + lo) * NQ + PQ + hi];
+      } else {
+        v = r == c ? 1.0 : 0.0;
+      }
+    } else if (r >= PJ && c < PJ) {
+      const int al = r - PJ;
+      if (al < nj && c < nj) v = d.F3[(size_t)al * N2 + PJ + c];  // W^T[al][c] = W[c][al]
+    }
+    d.F4[(size_t)c * N2 + r] = v;
+  }
+}
+
+// (j) parallel cyclic Jacobi on C (n2 x n2, even): A <- J^T A J, V <- V J.
+// Round-robin ordering: in each of the n2-1 rounds the n2/2 index pairs are
+// disjoint, so all rotations of a round are applied at once (rows, then columns).
+__device__ __forceinline__ void rr_pair(int k, int round, int n2, int& p, int& q) {
+  const int m = n2 - 1;
+  p = k == 0 ? 0 : 1 + (k - 1 + round) % m;
+  q = 1 + (n2 - 2 - k + round) % m;
+  if (p > q) {
+    const int t = p;
+    p = q;
+    q = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_jacobi(const PairDev* pd, int smem_cap) {
+  const PairDev d = pd[blockIdx.x];
+  const int nj = d.nj, n2 = nj + (nj & 1), PJ = d.PJ, N2 = 2 * PJ;
+  extern __shared__ double sm[];
+  const bool in_smem = 2 * n2 * n2 <= smem_cap;
+  double* A = in_smem ? sm : d.A;
+  double* V = in_smem ? sm + n2 * n2 : d.V;
+  double* cs = in_smem ? sm + 2 * n2 * n2 : sm;  // n2/2 cosines then n2/2 sines
+  const int tid = threadIdx.x;
+  for (int e = tid; e < n2 * n2; e += blockDim.x) {
+    const int r = e % n2, c = e / n2;
+    double v = 0.0;
+    if (r < nj && c < nj) {
+      const int hi = r >= c ? r : c, lo = r >= c ? c : r;
+      v = d.F4[(size_t)lo * N2 + PJ + hi];
+    }
+    A[e] = v;
+    V[e] = r == c ? 1.0 : 0.0;
+  }
+  __shared__ double red[256];
+  __shared__ int rotated;
+  double part = 0.0;
+  for (int e = tid; e < n2 * n2; e += blockDim.x) part += A[e] * A[e];
+  red[tid] = part;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (tid < s) red[tid] += red[tid + s];
+    __syncthreads();
+  }
+  const double fro = sqrt(red[0]);
+  const double tiny = 1e-15 * fro / (n2 > 0 ? n2 : 1);
+  const int half = n2 / 2;
+  for (int sweep = 0; sweep < 40 && n2 > 1; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < n2 - 1; ++round) {
+      for (int k = tid; k < half; k += blockDim.x) {
+        int p, q;
+        rr_pair(k, round, n2, p, q);
+        const double apq = A[(size_t)q * n2 + p];
+        const double app = A[(size_t)p * n2 + p], aqq = A[(size_t)q * n2 + q];
+        double c = 1.0, s = 0.0;
+        if (fabs(apq) > tiny && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq))) {
+          const double theta = (aqq - app) / (2.0 * apq);
+          const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+          c = 1.0 / sqrt(t * t + 1.0);
+          s = t * c;
+          rotated = 1;
+        }
+        cs[k] = c;
+        cs[half + k] = s;
+      }
+      __syncthreads();
+      for (int e = tid; e < half * n2; e += blockDim.x) {  // rows p, q
+        const int k = e / n2, col = e % n2;
+        const double c = cs[k], s = cs[half + k];
+        if (s == 0.0) continue;
+        int p, q;
+        rr_pair(k, round, n2, p, q);
+        const double ap = A[(size_t)col * n2 + p], aq = A[(size_t)col * n2 + q];
+        A[(size_t)col * n2 + p] = c * ap - s * aq;
+        A[(size_t)col * n2 + q] = s * ap + c * aq;
+      }
+      __syncthreads();
+      for (int e = tid; e < half * n2; e += blockDim.x) {  // columns p, q of A and V
+        const int k = e / n2, row = e % n2;
+        const double c = cs[k], s = cs[half + k];
+        if (s == 0.0) continue;
+        int p, q;
+        rr_pair(k, round, n2, p, q);
+        const double ap = A[(size_t)p * n2 + row], aq = A[(size_t)q * n2 + row];
+        A[(size_t)p * n2 + row] = c * ap - s * aq;
+        A[(size_t)q * n2 + row] = s * ap + c * aq;
+        const double vp = V[(size_t)p * n2 + row], vq = V[(size_t)q * n2 + row];
+        V[(size_t)p * n2 + row] = c * vp - s * vq;
+        V[(size_t)q * n2 + row] = s * vp + c * vq;
+      }
+      __syncthreads();
+    }
+    const int any = rotated;
+    __syncthreads();
+    if (!any) break;
+  }
+  // top-k eigenvalues, descending (one thread; k <= 64)
+  __shared__ int order[64];
+  if (tid == 0) {
+    for (int m = 0; m < d.k; ++m) {
+      int best = -1;
+      double bv = -1e300;
+      for (int i = 0; i < nj; ++i) {
+        bool used = false;
+        for (int q = 0; q < m; ++q) used |= order[q] == i;
+        const double v = A[(size_t)i * n2 + i];
+        if (!used && v > bv) {
+          bv = v;
+          best = i;
+        }
+      }
+      order[m] = best;
+      d.evals[m] = best >= 0 ? fmax(bv, 0.0) : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < d.k * N2; e += blockDim.x) {  // solve vectors [y; 0]
+    const int m = e / N2, r = e % N2;
+    const int col = order[m];
+    d.vecs[e] = (col >= 0 && r < nj) ? V[(size_t)col * n2 + r] : 0.0;
+  }
+}
+
+// (l) functional a_m = 1/2 M K alpha_m (alpha = first nj entries of vecs after the back solve)
+__global__ void k_functional(const PairDev* pd) {
+  const PairDev d = pd[blockIdx.y];
+  const int nf = d.nf, nj = d.nj, N2 = 2 * d.PJ;
+  const int m = blockIdx.x;
+  if (m >= d.k) return;
+  const double* al = d.vecs + (size_t)m * N2;
+  for (int t = threadIdx.x; t < nf; t += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nj; ++b) s += d.H[(size_t)b * nf + t] * al[b];  // H = M K
+    d.func[(size_t)m * nf + t] = 0.5 * s;
+  }
+}
+
+}  // namespace
 
 void PairEngine::attach(const Model& m, const double* S, const std::vector<long long>& s_off,
                         const std::vector<int>& PB, const std::vector<int>& nB, cudaStream_t st) {
@@ -15,8 +398,373 @@ void PairEngine::attach(const Model& m, const double* S, const std::vector<long 
   st_ = st;
 }
 
-EnrichOutcome PairEngine::enrich(ConstraintSet&, const EnrichOptions&) {
-  throw Error(kUnsupported, "adaptive enrichment not built yet");
+namespace {
+struct HostPair {
+  PairIndex idx;
+  std::vector<int> pos[2];   // [outer | corner | shared] boundary positions per side
+  std::vector<double> K;     // nf x nj column-major
+  std::vector<double> N;     // nm x m1 row-major
+  std::vector<int> glob_off, glob_n;  // shared glob slot offsets
+  int nj = 0, nm = 0, r_total = 0;    // r_total = admissible columns - nullity
+};
+
+int count_above(const std::vector<double>& v, double tau) {
+  int k = 0;
+  while (k < static_cast<int>(v.size()) && v[k] > tau) ++k;
+  return k;
+}
+}  // namespace
+
+EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
+  const Model& m = *m_;
+  const ConstraintSet base = cs;  // adaptive.cpp:133: every pair sees the same base
+  const auto bg = base.by_glob(m.globs.size());
+  const int request = o.indicator_only ? 1 : (o.fixed_count >= 0 ? o.fixed_count : o.max_vectors) + 1;
+  const auto pairs = face_pairs(m);
+  const int np = static_cast<int>(pairs.size());
+  std::vector<HostPair> hp(np);
+  // boundary position of each local dof, per subdomain
+  std::vector<std::vector<int>> bpos(m.subs.size());
+  for (std::size_t s = 0; s < m.subs.size(); ++s) {
+    bpos[s].assign(m.subs[s].dim(), -1);
+    for (std::size_t b = 0; b < m.subs[s].boundary.size(); ++b) bpos[s][m.subs[s].boundary[b]] = static_cast<int>(b);
+  }
+  for (int p = 0; p < np; ++p) {
+    HostPair& h = hp[p];
+    h.idx = build_pair_index(m, pairs[p].first, pairs[p].second);
+    const PairIndex& x = h.idx;
+    const int nf = static_cast<int>(x.noncorner_globals.size());
+    for (int side = 0; side < 2; ++side) {
+      const int s = side == 0 ? x.si : x.sj;
+      const auto& outer = side == 0 ? x.outer_i : x.outer_j;
+      auto& pos = h.pos[side];
+      for (i64 g : outer) pos.push_back(bpos[s][m.maps.local_of(g, s)]);
+      for (i64 g : x.corner_globals) pos.push_back(bpos[s][m.maps.local_of(g, s)]);
+      for (i64 g : x.noncorner_globals) pos.push_back(bpos[s][m.maps.local_of(g, s)]);
+    }
+    // kernel blocks of the installed averages (pair.cpp:167-188)
+    std::vector<std::vector<double>> blocks;
+    std::vector<int> bcols;
+    int nj = 0;
+    for (std::size_t gi = 0; gi < x.shared_globs.size(); ++gi) {
+      const int g = x.shared_globs[gi];
+      const int n = x.glob_size[gi];
+      int cols = 0;
+      std::vector<double> k;
+      if (bg[g].empty()) {
+        k = glob_kernel(nullptr, 0, n, &cols);
+      } else {
+        std::vector<double> rows(bg[g].size() * std::size_t(n));
+        for (std::size_t a = 0; a < bg[g].size(); ++a)
+          for (int t = 0; t < n; ++t) rows[a * n + t] = base.averages[bg[g][a]].weights[t];
+        k = glob_kernel(&rows, static_cast<int>(bg[g].size()), n, &cols);
+      }
+      blocks.push_back(std::move(k));
+      bcols.push_back(cols);
+      nj += cols;
+    }
+    h.nj = nj;
+    h.K.assign(std::size_t(nf) * nj, 0.0);
+    int coff = 0;
+    for (std::size_t gi = 0; gi < blocks.size(); ++gi) {
+      const int n = x.glob_size[gi], off = x.glob_offset[gi], cols = bcols[gi];
+      for (int t = 0; t < n; ++t)
+        for (int c = 0; c < cols; ++c) h.K[std::size_t(coff + c) * nf + off + t] = blocks[gi][std::size_t(t) * cols + c];
+      coff += cols;
+    }
+    const int m1 = static_cast<int>(x.corner_globals.size()) + nf;
+    if (x.floating) {
+      std::vector<i64> dofs(x.corner_globals);
+      dofs.insert(dofs.end(), x.noncorner_globals.begin(), x.noncorner_globals.end());
+      h.N = rigid_modes(m, dofs, &h.nm);
+    }
+    const int n_adm = m1 + nj + static_cast<int>(x.outer_i.size() + x.outer_j.size());
+    h.r_total = n_adm - h.nm;
+    (void)m1;
+  }
+  // device buffers, processed in chunks bounded by a memory budget
+  EnrichOutcome out;
+  std::vector<std::vector<double>> all_evals(np), all_funcs(np);
+  std::vector<int> all_k(np);
+  const double budget = 24e9;  // bytes of pair fronts per chunk
+  int p0 = 0;
+  while (p0 < np) {
+    // choose chunk
+    std::vector<PairDev> pd;
+    std::vector<long long> offG0, offG1, offQ, offF3, offF4, offM, offK, offH, offN, offR, offA, offV, offE, offW, offFu,
+        offD0, offD1, offDQ, offD3, offD4, offP0, offP1;
+    long long nG = 0, nQ = 0, nF = 0, nM = 0, nK = 0, nH = 0, nN = 0, nR = 0, nA = 0, nE = 0, nW = 0, nFu = 0, nD = 0,
+              nP = 0;
+    int p1 = p0;
+    double bytes = 0;
+    struct Dims { int no[2], PO[2], NG[2], nc, nf, nj, PQ, PJ, k, nm; };
+    std::vector<Dims> dims;
+    while (p1 < np) {
+      const HostPair& h = hp[p1];
+      Dims dm{};
+      dm.nc = static_cast<int>(h.idx.corner_globals.size());
+      dm.nf = static_cast<int>(h.idx.noncorner_globals.size());
+      dm.nj = h.nj;
+      dm.nm = h.nm;
+      const int m1 = dm.nc + dm.nf;
+      for (int side = 0; side < 2; ++side) {
+        dm.no[side] = static_cast<int>((side == 0 ? h.idx.outer_i : h.idx.outer_j).size());
+        dm.PO[side] = rup(dm.no[side], kTile);
+        dm.NG[side] = dm.PO[side] + rup(std::max(m1, 1), kTile);
+      }
+      dm.PQ = rup(std::max(m1, 1), kTile);
+      dm.PJ = rup(std::max(dm.nj, 1), kTile);
+      dm.k = std::min(request, std::min(h.nj, std::max(h.r_total, 0)));
+      dm.k = std::min(dm.k, 64);
+      const double b = 8.0 * (double(dm.NG[0]) * dm.NG[0] + double(dm.NG[1]) * dm.NG[1] +
+                              double(dm.PQ + dm.PJ) * (dm.PQ + dm.PJ) + 8.0 * dm.PJ * dm.PJ);
+      if (p1 > p0 && bytes + b > budget) break;
+      bytes += b;
+      dims.push_back(dm);
+      ++p1;
+    }
+    const int nb = p1 - p0;
+    std::vector<int> posv;
+    std::vector<double> Kv, Nv, Rv;
+    pd.resize(nb);
+    std::vector<long long> oG(2 * nb), oQ(nb), oF3(nb), oF4(nb), oM(nb), oK(nb), oH(nb), oN(nb), oR(nb), oA(nb),
+        oE(nb), oW(nb), oFu(nb), oDG(2 * nb), oDQ(nb), oD3(nb), oD4(nb), oP(2 * nb);
+    for (int b = 0; b < nb; ++b) {
+      const Dims& dm = dims[b];
+      const HostPair& h = hp[p0 + b];
+      for (int side = 0; side < 2; ++side) {
+        oG[2 * b + side] = nG;
+        nG += (long long)dm.NG[side] * dm.NG[side];
+        oDG[2 * b + side] = nD;
+        nD += (long long)(dm.PO[side] / kTile) * kTile * kTile;
+        oP[2 * b + side] = posv.size();
+        posv.insert(posv.end(), h.pos[side].begin(), h.pos[side].end());
+      }
+      const int NQ = dm.PQ + dm.PJ, N2 = 2 * dm.PJ, n2 = dm.nj + (dm.nj & 1);
+      oQ[b] = nQ;
+      nQ += (long long)NQ * NQ;
+      oDQ[b] = nD;
+      nD += (long long)(dm.PQ / kTile) * kTile * kTile;
+      oF3[b] = nF;
+      nF += (long long)N2 * N2;
+      oF4[b] = nF;
+      nF += (long long)N2 * N2;
+      oD3[b] = nD;
+      nD += (long long)(dm.PJ / kTile) * kTile * kTile;
+      oD4[b] = nD;
+      nD += (long long)(dm.PJ / kTile) * kTile * kTile;
+      oM[b] = nM;
+      nM += (long long)dm.nf * dm.nf;
+      oK[b] = Kv.size();
+      Kv.insert(Kv.end(), h.K.begin(), h.K.end());
+      oH[b] = nH;
+      nH += (long long)dm.nf * std::max(dm.nj, 1);
+      oN[b] = Nv.size();
+      Nv.insert(Nv.end(), h.N.begin(), h.N.end());
+      oR[b] = Rv.size();
+      Rv.insert(Rv.end(), h.idx.rho_i.begin(), h.idx.rho_i.end());
+      oA[b] = nA;
+      nA += 2LL * n2 * n2;
+      oE[b] = nE;
+      nE += std::max(dm.k, 1);
+      oW[b] = nW;
+      nW += (long long)N2 * std::max(dm.k, 1);
+      oFu[b] = nFu;
+      nFu += (long long)dm.nf * std::max(dm.k, 1);
+    }
+    Buf<double> G, Q, F, Dv, M, K, H, N, R, A, E, W, Fu;
+    Buf<int> Pv, info;
+    G.alloc(nG);
+    Q.alloc(nQ);
+    F.alloc(nF);
+    Dv.alloc(std::max<long long>(nD, 1));
+    M.alloc(std::max<long long>(nM, 1));
+    K.upload(Kv, st_);
+    H.alloc(std::max<long long>(nH, 1));
+    N.upload(Nv, st_);
+    R.upload(Rv, st_);
+    A.alloc(std::max<long long>(nA, 1));
+    E.alloc(nE);
+    W.alloc(nW);
+    Fu.alloc(std::max<long long>(nFu, 1));
+    Pv.upload(posv, st_);
+    info.alloc(4 * nb);
+    CK(cudaMemsetAsync(info.p, 0, 4 * nb * sizeof(int), st_));
+    std::vector<FrontDesc> fG(2 * nb), fQ(nb), f3(nb), f4(nb);
+    int maxNG = 0, maxPO = 0, maxM1 = 0, maxNQ = 0, maxPQ = 0, maxPJ = 0, maxk = 0, maxnf = 0, maxn2 = 0;
+    for (int b = 0; b < nb; ++b) {
+      const Dims& dm = dims[b];
+      const HostPair& h = hp[p0 + b];
+      PairDev& d = pd[b];
+      for (int side = 0; side < 2; ++side) {
+        const int s = side == 0 ? h.idx.si : h.idx.sj;
+        d.S[side] = S_ + s_off_[s];
+        d.PB[side] = PB_[s];
+        d.pos[side] = Pv.p + oP[2 * b + side];
+        d.G[side] = G.p + oG[2 * b + side];
+        d.NG[side] = dm.NG[side];
+        d.PO[side] = dm.PO[side];
+        d.no[side] = dm.no[side];
+        fG[2 * b + side] = FrontDesc{d.G[side], Dv.p + oDG[2 * b + side], dm.NG[side], dm.PO[side], info.p + 4 * b + side, 0};
+        maxNG = std::max(maxNG, dm.NG[side]);
+        maxPO = std::max(maxPO, dm.PO[side]);
+        maxM1 = std::max(maxM1, dm.NG[side] - dm.PO[side]);
+      }
+      d.nc = dm.nc;
+      d.nf = dm.nf;
+      d.nj = dm.nj;
+      d.nm = dm.nm;
+      d.PQ = dm.PQ;
+      d.PJ = dm.PJ;
+      d.k = dm.k;
+      d.Q = Q.p + oQ[b];
+      d.F3 = F.p + oF3[b];
+      d.F4 = F.p + oF4[b];
+      d.M = M.p + oM[b];
+      d.K = K.p + oK[b];
+      d.H = H.p + oH[b];
+      d.N = N.p + oN[b];
+      d.rho = R.p + oR[b];
+      const int n2 = dm.nj + (dm.nj & 1);
+      d.A = A.p + oA[b];
+      d.V = A.p + oA[b] + (long long)n2 * n2;
+      d.evals = E.p + oE[b];
+      d.vecs = W.p + oW[b];
+      d.func = Fu.p + oFu[b];
+      const int NQ = dm.PQ + dm.PJ, N2 = 2 * dm.PJ;
+      fQ[b] = FrontDesc{d.Q, Dv.p + oDQ[b], NQ, dm.PQ, info.p + 4 * b + 2, 0};
+      f3[b] = FrontDesc{d.F3, Dv.p + oD3[b], N2, dm.PJ, info.p + 4 * b + 3, 0};
+      f4[b] = FrontDesc{d.F4, Dv.p + oD4[b], N2, dm.PJ, info.p + 4 * b + 3, 0};
+      maxNQ = std::max(maxNQ, NQ);
+      maxPQ = std::max(maxPQ, dm.PQ);
+      maxPJ = std::max(maxPJ, dm.PJ);
+      maxk = std::max(maxk, dm.k);
+      maxnf = std::max(maxnf, dm.nf);
+      maxn2 = std::max(maxn2, n2);
+    }
+    Buf<PairDev> dpd;
+    Buf<FrontDesc> dG, dQ, d3, d4;
+    dpd.upload(pd, st_);
+    dG.upload(fG, st_);
+    dQ.upload(fQ, st_);
+    d3.upload(f3, st_);
+    d4.upload(f4, st_);
+    // (a)-(b) side fronts, eliminate the outer skeleton
+    k_gather_G<<<dim3(maxNG, 2 * nb), 128, 0, st_>>>(dpd.p);
+    CK(cudaGetLastError());
+    partial_cholesky(dG.p, 2 * nb, maxNG, maxPO, maxM1, st_);
+    // (c) M from the original shared block
+    k_build_M<<<dim3(16, nb), 256, 0, st_>>>(dpd.p);
+    // (d) Q and its elimination onto alpha
+    k_build_H<<<dim3(32, nb), 256, 0, st_>>>(dpd.p);
+    k_assemble_Q<<<dim3(64, nb), 256, 0, st_>>>(dpd.p);
+    CK(cudaGetLastError());
+    partial_cholesky(dQ.p, nb, maxNQ, maxPQ, maxPJ, st_);
+    // (f)-(i) C = L^{-1} lhs L^{-T}
+    k_build_MK<<<dim3(32, nb), 256, 0, st_>>>(dpd.p);
+    k_build_F3<<<dim3(64, nb), 256, 0, st_>>>(dpd.p);
+    partial_cholesky(d3.p, nb, 2 * maxPJ, maxPJ, maxPJ, st_);
+    k_build_F4<<<dim3(64, nb), 256, 0, st_>>>(dpd.p);
+    partial_cholesky(d4.p, nb, 2 * maxPJ, maxPJ, maxPJ, st_);
+    CK(cudaGetLastError());
+    // (j) Jacobi
+    const int cap = 200 * 1024 / 8 - 4 * maxn2 - 64;
+    const bool smem_ok = 2 * maxn2 * maxn2 <= cap;
+    const int jsm = (smem_ok ? 2 * maxn2 * maxn2 : 0) * 8 + 3 * maxn2 * 8 + 64;
+    CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    k_jacobi<<<nb, 256, jsm, st_>>>(dpd.p, smem_ok ? 2 * maxn2 * maxn2 : 0);
+    CK(cudaGetLastError());
+    // (k) alpha = L^{-T} y via F3's factor; (l) functionals
+    std::vector<SolveDesc> sv;
+    for (int b = 0; b < nb; ++b)
+      for (int mm = 0; mm < dims[b].k; ++mm)
+        sv.push_back(SolveDesc{pd[b].F3, Dv.p + oD3[b], pd[b].vecs + (size_t)mm * 2 * dims[b].PJ, 2 * dims[b].PJ,
+                               dims[b].PJ, nullptr, nullptr});
+    Buf<SolveDesc> dsv;
+    dsv.upload(sv, st_);
+    front_backward(dsv.p, static_cast<int>(sv.size()), 2 * maxPJ, st_);
+    k_functional<<<dim3(std::max(maxk, 1), nb), 128, 0, st_>>>(dpd.p);
+    CK(cudaGetLastError());
+    std::vector<double> ev(E.n), fu(Fu.n);
+    std::vector<int> inf(4 * nb);
+    CK(cudaMemcpyAsync(ev.data(), E.p, E.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(fu.data(), Fu.p, Fu.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(inf.data(), info.p, 4 * nb * sizeof(int), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    for (int b = 0; b < nb; ++b) {
+      for (int q = 0; q < 4; ++q)
+        if (inf[4 * b + q])
+          throw Error(kNotPositiveDefinite, "pair eigenproblem " + std::to_string(hp[p0 + b].idx.si) + "," +
+                                                std::to_string(hp[p0 + b].idx.sj) + ": reduction not positive definite");
+      const Dims& dm = dims[b];
+      const HostPair& h = hp[p0 + b];
+      // eigenvalue list of generalized_eig_sym: top min(request, r) with zeros beyond rank(lhs)
+      const int take = std::min(request, std::max(h.r_total, 0));
+      std::vector<double> lam(take, 0.0);
+      for (int q = 0; q < std::min(dm.k, take); ++q) lam[q] = ev[oE[b] + q];
+      all_evals[p0 + b] = lam;
+      all_funcs[p0 + b].assign(fu.begin() + oFu[b], fu.begin() + oFu[b] + (long long)dm.nf * dm.k);
+      all_k[p0 + b] = dm.k;
+    }
+    p0 = p1;
+  }
+  // host selection, splitting and rank filter (adaptive.cpp:66-125)
+  for (int p = 0; p < np; ++p) {
+    const HostPair& h = hp[p];
+    PairReport rep;
+    rep.si = h.idx.si;
+    rep.sj = h.idx.sj;
+    rep.eigenvalues = all_evals[p];
+    const auto& lam = rep.eigenvalues;
+    const int L = static_cast<int>(lam.size());
+    if (!o.indicator_only) {
+      if (o.fixed_count >= 0)
+        rep.enforced = std::min(o.fixed_count, L);
+      else
+        rep.enforced = std::min(count_above(lam, o.tau), o.max_vectors);
+      rep.omega_next = rep.enforced < L ? lam[rep.enforced] : 0.0;
+      rep.saturated = rep.omega_next > o.tau && o.fixed_count < 0;
+      const int nf = static_cast<int>(h.idx.noncorner_globals.size());
+      for (int mm = 0; mm < rep.enforced; ++mm) {
+        std::vector<double> func(nf, 0.0);
+        if (mm < all_k[p])
+          std::copy(all_funcs[p].begin() + (long long)mm * nf, all_funcs[p].begin() + (long long)(mm + 1) * nf, func.begin());
+        double scale = 0;
+        for (double v : func) scale += v * v;
+        scale = std::sqrt(scale);
+        for (std::size_t gi = 0; gi < h.idx.shared_globs.size(); ++gi) {
+          const int g = h.idx.shared_globs[gi];
+          const int off = h.idx.glob_offset[gi], n = h.idx.glob_size[gi];
+          std::vector<double> piece(func.begin() + off, func.begin() + off + n);
+          double pn = 0;
+          for (double v : piece) pn += v * v;
+          pn = std::sqrt(pn);
+          if (pn <= 1e-12 * scale) continue;
+          if (m.globs[g].kind == kEdge && !o.keep_edge_constraints) continue;
+          int top = 0;
+          for (int t = 1; t < n; ++t)
+            if (std::abs(piece[t]) > std::abs(piece[top])) top = t;
+          const double div = piece[top] < 0 ? -pn : pn;
+          for (double& v : piece) v /= div;
+          Average av;
+          av.glob = g;
+          av.weights = std::move(piece);
+          av.adaptive = 1;
+          if (add_average(cs, std::move(av)))
+            ++rep.kept;
+          else
+            ++rep.dropped;
+        }
+      }
+    } else {
+      rep.omega_next = L > 0 ? lam[0] : 0.0;
+    }
+    out.omega_tilde = std::max(out.omega_tilde, rep.omega_next);
+    out.kept += rep.kept;
+    out.dropped += rep.dropped;
+    out.pairs.push_back(std::move(rep));
+  }
+  return out;
 }
 
 }  // namespace b200
