@@ -1,0 +1,296 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 adaptive-BDDC hot path (one JSON line on rank 0).
+
+A *step* is one pass of the hot path over one instance of the workload:
+leaf factorization + interface Schur complements, adaptive face
+eigenproblems, constraint selection, transformed preconditioner (leaf fronts +
+root) and the PCG solve to 1e-8 -- i.e. the metric's "setup + solve".  The
+workload defaults to BASELINE.json configs[1] (24^3 Poisson, 3x3x3
+substructures, 1e6 z-channels, adaptive tau=10, <=10 vectors per face); the
+host-side input (mesh, assembly, globs) is built once and uploaded before
+timing.  `value` is free dofs / device seconds per step, summed over ranks;
+`e2e` repeats the step through the C ABI with the host->device upload of the
+inputs and the device->host copy of the solution inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+N > 1 (torchrun, one process per GPU) runs N independent replicas ("weak"
+scaling); the sharded multi-GPU path is future work.
+`--impl reference` times the CPU oracle (oracle/, the reference restated; the
+C++ reference itself needs Eigen and cannot be built here) on the same config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIG_MODES = {1: ("c+e+f", 10.0, 15, False), 2: ("adaptive", 10.0, 10, False),
+                3: ("adaptive", 5.0, 15, False), 4: ("adaptive", 10.0, 15, True),
+                5: ("adaptive", 10.0, 15, False)}
+CONFIG_NAMES = {1: "cfg1: Poisson 24^3, 3^3 subdomains, c+e+f",
+                2: "cfg2: Poisson 24^3, 3^3 subdomains, 1e6 z-channels p=0.1, adaptive tau=10 max 10",
+                3: "cfg3: Poisson 80^3, 8^3 subdomains, k=exp(2z), adaptive tau=5 max 15",
+                4: "cfg4: elasticity 48^3, 6^3 subdomains, 20 spheres E=1e4, c+e+f + adaptive tau=10 max 15",
+                5: "cfg5: elasticity 96^3, 12^3 subdomains, layered E 1/1e5, adaptive tau=10 max 15"}
+METRIC = "adaptive-BDDC setup+solve throughput (free DOF/s)"
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+FP64_PEAK_TFLOPS = 35.47  # cuBLAS DGEMM 8192^3 on this pool's B200 (profiles/r01_fp64_peak.txt)
+FP64_DMMA_PEAK_TFLOPS = 36.9  # mma.sync m16n8k16 f64 microbenchmark, same file
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                bits = int(parts[2], 16) if parts[2].startswith("0x") else int(parts[2])
+            except ValueError:
+                continue
+            mx = max(mx, m)
+            if bits & 0x1:  # idle sample
+                continue
+            sm.append(s)
+            for b, name in REASONS.items():
+                if bits & b and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist_mod
+        backend = "nccl" if args.impl != "reference" else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist_mod.init_process_group(backend=backend)
+        dist = dist_mod
+    return world, rank, local, dist
+
+
+def max_over_ranks(dist, value: float, device=None) -> float:
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist, device=None):
+    if dist is not None:
+        if device is not None:
+            dist.barrier(device_ids=[device])
+        else:
+            dist.barrier()
+
+
+def run_oracle_step(cfg_id, seed):
+    from oracle.experiment import baseline_config, build_pipeline, solve_item
+    cfg = baseline_config(cfg_id, seed)
+    p = build_pipeline(cfg.spec)
+    t0 = time.perf_counter()
+    row = solve_item(p, cfg.mode, cfg.tau, cfg.max_vectors, base_faces=cfg.base_faces)
+    dt = time.perf_counter() - t0
+    return dt, p.dmap.free_count, row
+
+
+def reference_arm(args):
+    world, rank, local, dist = dist_setup(args)
+    if rank != 0:
+        return 0
+    cfg_id = args.config
+    times = []
+    row = None
+    for i in range(args.warmup + args.steps):
+        dt, free, row = run_oracle_step(cfg_id, args.seed)
+        if i >= args.warmup:
+            times.append(dt)
+    sec = sum(times) / len(times)
+    value = free / sec
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+        "config": {"workload": CONFIG_NAMES[cfg_id], "config": cfg_id, "seed": args.seed,
+                   "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
+                         "sample": "full %s setup+solve per step (numpy/scipy oracle, LAPACK on %d threads)"
+                                   % ("cfg%d" % cfg_id, cores)},
+        "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "iterations": row.iterations, "kappa": row.kappa, "constraint_rows": row.constraint_rows,
+        "omega_tilde": None if math.isnan(row.omega_tilde) else row.omega_tilde,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--seed", type=int, default=20091030)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    world, rank, local, dist = dist_setup(args)
+    import paper_0910_5863_b200 as pb
+    lib = pb.load_library()
+    if lib.bddc_b200_device_count() < 1:
+        raise SystemExit("no CUDA device visible: the B200 path has no CPU fallback")
+    pb._check(lib.bddc_b200_set_device(local))
+    import torch
+    torch.cuda.set_device(local)
+    mode, tau, maxv, base_faces = CONFIG_MODES[args.config]
+    t_in = time.perf_counter()
+    b = pb.BDDC(config=args.config, seed=args.seed)
+    input_seconds = time.perf_counter() - t_in
+    st = b.structure()
+    free = st["free_dofs"]
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+
+    def do_step(e2e=False, u=None):
+        flush.zero_()
+        torch.cuda.synchronize()
+        return b.step(mode, tau, maxv, base_faces=base_faces, e2e=e2e, u_free=u)
+
+    for _ in range(args.warmup):
+        do_step()
+    barrier(dist, local)
+    torch.cuda.synchronize()
+    steps = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            steps.append(do_step())
+    torch.cuda.synchronize()
+    barrier(dist, local)
+    dev_seconds = sum(s["seconds"] for s in steps)
+    dev_seconds = max_over_ranks(dist, dev_seconds, "cuda")
+    sec_per_step = dev_seconds / args.steps
+    value = world * free / sec_per_step
+    # end to end through the C ABI with host buffers
+    u = np.empty(free)
+    for _ in range(max(1, args.warmup // 2)):
+        do_step(True, u)
+    barrier(dist, local)
+    e2e_steps = [do_step(True, u) for _ in range(args.steps)]
+    e2e_sec = max_over_ranks(dist, sum(s["seconds"] for s in e2e_steps), "cuda") / args.steps
+    if rank != 0:
+        return 0
+    last = steps[-1]
+    # roofline of the dominant tensor kernel: the batched leaf partial Cholesky
+    peaks, peak_kind = measured_peaks()
+    lf_t = statistics.median(s["leaf_factor_seconds"] for s in steps)
+    lf_flops = last["leaf_flops"]
+    achieved = lf_flops / lf_t / 1e12
+    roof = {"kernel": "partial_cholesky (leaf fronts: A_II eliminated, S_s formed)", "bound": "tensor",
+            "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+            "peak_source": "measured cuBLAS DGEMM (MEASURED_PEAKS.json has bf16 only)",
+            "flops_per_launch": lf_flops, "seconds_per_launch": lf_t,
+            "share_of_step": lf_t / sec_per_step}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1 and args.config <= 2:
+        dt, _, _ = run_oracle_step(args.config, args.seed)
+        cpu = {"value": free / dt, "unit": "DOF/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": "one full cfg%d setup+solve (numpy/scipy oracle, %.1f s)" % (args.config, dt)}
+    line = {
+        "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec_per_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded coefficient field)",
+        "config": {"workload": CONFIG_NAMES[args.config], "config": args.config, "seed": args.seed,
+                   "free_dofs": free, "subdomains": st["subdomains"], "interface_dofs": st["interface_dofs"],
+                   "l2": "flushed (256 MiB write) before every step",
+                   "parallelism": "replicas%d" % world if world > 1 else "single GPU"},
+        "setup_s": statistics.median(s["setup_seconds"] for s in steps),
+        "solve_s": statistics.median(s["solve_seconds"] for s in steps),
+        "iterations": last["iterations"], "kappa": last["kappa"], "constraint_rows": last["constraint_rows"],
+        "omega_tilde": last["omega_tilde"], "input_build_s": input_seconds,
+        "phases_s": {k: v for k, v in b.times().items() if k in ("analysis", "eigen", "preconditioner", "pcg",
+                                                                   "leaf_factor")},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": world * free / e2e_sec, "unit": "DOF/s",
+                "h2d_bytes_per_step": int(e2e_steps[-1]["h2d_bytes"]),
+                "d2h_bytes_per_step": int(e2e_steps[-1]["d2h_bytes"]), "ms_per_step": e2e_sec * 1e3},
+        "clocks": clk.summary(),
+        "gpu_launches": int(sum(s["launches"] for s in steps)),
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

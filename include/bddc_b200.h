@@ -95,6 +95,9 @@ typedef struct bddc_b200_row {
 
 const char* bddc_b200_last_error(void);
 int bddc_b200_device_count(void);
+/* Select the CUDA device used by handles created afterwards on this thread
+ * (one process per GPU). */
+int bddc_b200_set_device(int device);
 
 /* Build mesh, decomposition, Dirichlet map, substructure matrices, globs,
  * corners and embeddings (experiment.cpp:116-128; support.hpp:89-100). */
@@ -157,9 +160,30 @@ int bddc_b200_pcg(bddc_b200_t* h, const double* b, double* x, double tolerance, 
 int bddc_b200_run_item(bddc_b200_t* h, const char* mode, double tau, int max_vectors, int keep_edge,
                        int base_faces, bddc_b200_row* row);
 
+/* One pass of the hot path, timed on the device with CUDA events (bench
+ * "step"): analysis + constraints (+ enrichment) + preconditioner + PCG.
+ * e2e != 0 adds the host->device copies of the inputs (subdomain CSR, loads,
+ * maps) and the device->host copy of the recovered solution (u_free, length
+ * free_dofs) inside the timed region. */
+typedef struct bddc_b200_step_out {
+  double seconds, setup_seconds, solve_seconds;
+  double h2d_bytes, d2h_bytes;
+  int64_t launches;
+  int64_t constraint_rows;
+  double omega_tilde;
+  int64_t iterations;
+  double kappa;
+  int converged;
+  double leaf_factor_seconds, leaf_flops;
+} bddc_b200_step_out;
+int bddc_b200_step(bddc_b200_t* h, const char* mode, double tau, int max_vectors, int keep_edge,
+                   int base_faces, int e2e, double* u_free, bddc_b200_step_out* out);
+int64_t bddc_b200_launch_count(void);
+
 /* Device-timed phase seconds and work of the last calls:
- * [analysis, eigen, preconditioner, pcg, leaf_flops, leaf_front_bytes, schur_bytes, root_size] */
-int bddc_b200_times(const bddc_b200_t* h, double out[8]);
+ * [analysis, eigen, preconditioner, pcg, leaf_flops, leaf_front_bytes, schur_bytes, root_size,
+ *  leaf_factor] */
+int bddc_b200_times(const bddc_b200_t* h, double out[9]);
 
 #ifdef __cplusplus
 }

@@ -66,6 +66,14 @@ class _PcgResult(C.Structure):
                 ("condition_estimate", C.c_double), ("converged", C.c_int)]
 
 
+class _StepOut(C.Structure):
+    _fields_ = [("seconds", C.c_double), ("setup_seconds", C.c_double), ("solve_seconds", C.c_double),
+                ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double), ("launches", C.c_int64),
+                ("constraint_rows", C.c_int64), ("omega_tilde", C.c_double), ("iterations", C.c_int64),
+                ("kappa", C.c_double), ("converged", C.c_int), ("leaf_factor_seconds", C.c_double),
+                ("leaf_flops", C.c_double)]
+
+
 class _Row(C.Structure):
     _fields_ = [("omega_tilde", C.c_double), ("constraint_rows", C.c_int64), ("kappa", C.c_double),
                 ("iterations", C.c_int64), ("converged", C.c_int),
@@ -81,6 +89,7 @@ I64 = C.POINTER(C.c_int64)
 EXPORTS = {
     "bddc_b200_last_error": (C.c_char_p, []),
     "bddc_b200_device_count": (C.c_int, []),
+    "bddc_b200_set_device": (C.c_int, [C.c_int]),
     "bddc_b200_create": (C.c_int, [C.POINTER(_Problem), C.POINTER(P)]),
     "bddc_b200_create_config": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_int), C.c_int, C.POINTER(P)]),
     "bddc_b200_destroy": (None, [P]),
@@ -111,6 +120,9 @@ EXPORTS = {
     "bddc_b200_run_item": (C.c_int, [P, C.c_char_p, C.c_double, C.c_int, C.c_int, C.c_int,
                                      C.POINTER(_Row)]),
     "bddc_b200_times": (C.c_int, [P, D]),
+    "bddc_b200_step": (C.c_int, [P, C.c_char_p, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, D,
+                                 C.c_void_p]),
+    "bddc_b200_launch_count": (C.c_int64, []),
 }
 
 _lib = None
@@ -427,8 +439,21 @@ class BDDC:
                    r.seconds_eigen, r.seconds_preconditioner, r.root_size)
 
     def times(self) -> dict:
-        out = np.zeros(8)
+        out = np.zeros(9)
         _check(self._lib.bddc_b200_times(self._h, _dptr(out)))
         keys = ("analysis", "eigen", "preconditioner", "pcg", "leaf_flops", "leaf_front_bytes",
-                "schur_bytes", "root_size")
+                "schur_bytes", "root_size", "leaf_factor")
         return dict(zip(keys, out.tolist()))
+
+    def step(self, mode: str, tau: float = 10.0, max_vectors: int = 15, keep_edge=False,
+             base_faces=False, e2e=False, u_free: Optional[np.ndarray] = None) -> dict:
+        """One device-timed pass of the hot path (see `bddc_b200_step`)."""
+        o = _StepOut()
+        up = _dptr(u_free) if u_free is not None else None
+        _check(self._lib.bddc_b200_step(self._h, mode.encode(), tau, max_vectors, int(keep_edge),
+                                        int(base_faces), int(e2e), up, C.byref(o)))
+        return {n: getattr(o, n) for n, _ in _StepOut._fields_}
+
+    @staticmethod
+    def launch_count() -> int:
+        return load_library().bddc_b200_launch_count()

@@ -63,6 +63,13 @@ int bddc_b200_device_count(void) {
   return n;
 }
 
+int bddc_b200_set_device(int device) {
+  return guarded([&] {
+    const cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) throw Error(kCudaError, cudaGetErrorString(e));
+  });
+}
+
 int bddc_b200_create(const bddc_b200_problem* p, bddc_b200_t** out) {
   return guarded([&] {
     Problem pr;
@@ -352,7 +359,46 @@ int bddc_b200_run_item(bddc_b200_t* h, const char* mode_c, double tau, int max_v
   });
 }
 
-int bddc_b200_times(const bddc_b200_t* h, double out[8]) {
+int bddc_b200_step(bddc_b200_t* h, const char* mode_c, double tau, int max_vectors, int keep_edge,
+                   int base_faces, int e2e, double* u_free, bddc_b200_step_out* out) {
+  return guarded([&] {
+    const std::string mode(mode_c);
+    if (mode != "c" && mode != "c+e" && mode != "c+e+f" && mode != "c+e+f-3eigv" && mode != "adaptive")
+      throw Error(kBadProblemSpec, "unknown constraint mode '" + mode + "'");
+    if (e2e && !u_free) throw Error(kBadProblemSpec, "e2e step needs a u_free buffer");
+    StepSpec sp;
+    sp.edges = mode != "c";
+    sp.faces = mode == "c+e+f" || ((mode == "adaptive" || mode == "c+e+f-3eigv") && base_faces);
+    sp.adaptive = mode == "adaptive";
+    sp.fixed_count = mode == "c+e+f-3eigv" ? 3 : -1;
+    sp.tau = tau;
+    sp.max_vectors = max_vectors;
+    sp.keep_edge = keep_edge != 0;
+    sp.tol = h->model.spec.tolerance;
+    sp.max_it = h->model.spec.max_iterations;
+    sp.e2e = e2e != 0;
+    Engine& e = engine(h);
+    const StepOut o = e.step(sp, h->cs, u_free);
+    h->analysed = true;
+    out->seconds = o.seconds;
+    out->setup_seconds = o.setup_seconds;
+    out->solve_seconds = o.solve_seconds;
+    out->h2d_bytes = o.h2d_bytes;
+    out->d2h_bytes = o.d2h_bytes;
+    out->launches = o.launches;
+    out->constraint_rows = o.constraint_rows;
+    out->omega_tilde = o.omega_tilde;
+    out->iterations = o.pcg.iterations;
+    out->kappa = o.pcg.condition_estimate;
+    out->converged = o.pcg.converged ? 1 : 0;
+    out->leaf_factor_seconds = e.times().leaf_factor;
+    out->leaf_flops = e.times().flops_leaf;
+  });
+}
+
+int64_t bddc_b200_launch_count(void) { return launch_count(); }
+
+int bddc_b200_times(const bddc_b200_t* h, double out[9]) {
   return guarded([&] {
     if (!h->engine) throw Error(kError, "no engine yet");
     const PhaseTimes& t = h->engine->times();
@@ -364,6 +410,7 @@ int bddc_b200_times(const bddc_b200_t* h, double out[8]) {
     out[5] = h->engine->leaf_front_bytes();
     out[6] = h->engine->schur_bytes();
     out[7] = h->engine->root_size();
+    out[8] = t.leaf_factor;
   });
 }
 

@@ -11,6 +11,7 @@
 #include "dense.cuh"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 
 namespace b200 {
@@ -329,7 +330,12 @@ void configure() {
   g_smem_configured = 1;
 }
 
+std::atomic<long long> g_launches{0};
+
 }  // namespace
+
+void count_launch(long long n) { g_launches += n; }
+long long launch_count() { return g_launches.load(); }
 
 void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p, int max_m,
                       cudaStream_t stream) {
@@ -339,25 +345,34 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
   const int panel_smem = 2 * 64 * LDS * sizeof(double);
   const int nt = max_n / kTile, pt = max_p / kTile;
   for (int j = 0; j < pt; ++j) {
-    if (j > 0) k_syrk_column<<<dim3(nt - j, batch), GEMM_THREADS, gemm_smem, stream>>>(d_descs, j);
+    if (j > 0) {
+      k_syrk_column<<<dim3(nt - j, batch), GEMM_THREADS, gemm_smem, stream>>>(d_descs, j);
+      count_launch(1);
+    }
     k_panel<<<dim3(nt - j, batch), GEMM_THREADS, panel_smem, stream>>>(d_descs, j);
+    count_launch(1);
   }
   // trailing tiles: worst case over the batch is bounded by the largest trailing block
   const long mt = max_m / kTile;
   const long max_tr = mt * (mt + 1) / 2;
-  if (max_p > 0 && max_tr > 0) k_syrk_trailing<<<dim3(static_cast<unsigned>(max_tr), batch), GEMM_THREADS, gemm_smem, stream>>>(d_descs);
+  if (max_p > 0 && max_tr > 0) {
+    k_syrk_trailing<<<dim3(static_cast<unsigned>(max_tr), batch), GEMM_THREADS, gemm_smem, stream>>>(d_descs);
+    count_launch(1);
+  }
 }
 
 void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
   if (batch == 0) return;
   configure();
   k_front_forward<<<batch, SOLVE_THREADS, (max_n + 64) * sizeof(double), stream>>>(d_descs, done);
+  count_launch(1);
 }
 
 void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
   if (batch == 0) return;
   configure();
   k_front_backward<<<batch, SOLVE_THREADS, (max_n + 64) * sizeof(double), stream>>>(d_descs, done);
+  count_launch(1);
 }
 
 void copy_trailing_full(const TrailDesc* d_descs, int batch, int max_m, cudaStream_t stream) {
@@ -365,6 +380,7 @@ void copy_trailing_full(const TrailDesc* d_descs, int batch, int max_m, cudaStre
   const long total = (long)max_m * max_m;
   const int blocks = static_cast<int>(std::min<long>((total + 255) / 256, 1024));
   k_copy_trailing<<<dim3(blocks, batch), 256, 0, stream>>>(d_descs);
+  count_launch(1);
 }
 
 }  // namespace b200

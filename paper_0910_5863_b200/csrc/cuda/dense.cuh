@@ -40,6 +40,10 @@ struct SolveDesc {
   const double* croot;
 };
 
+/// Kernel-launch accounting (bench "gpu_launches").
+void count_launch(long long n);
+long long launch_count();
+
 /// Partial Cholesky of a batch of fronts (device descriptor array).
 /// max_n/max_p bound the descriptors' n/p.  Launches on `stream`.
 /// max_m bounds the trailing dimension n - p.

@@ -1,0 +1,88 @@
+// Device buffers (grow-only, so repeated setups reuse their arenas without
+// cudaMalloc/cudaFree inside timed steps) and an opt-in stage profiler
+// (BDDC_B200_PROFILE=1 prints CUDA-event stage times to stderr).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+namespace b200 {
+
+void cuda_check(cudaError_t e, const char* file, int line);
+#define CK(x) ::b200::cuda_check((x), __FILE__, __LINE__)
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  std::size_t n = 0, cap = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = cap = 0;
+  }
+  void alloc(std::size_t k) {
+    if (k > cap) {
+      if (p) CK(cudaFree(p));
+      p = nullptr;
+      CK(cudaMalloc(&p, k * sizeof(T)));
+      cap = k;
+    }
+    n = k;
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    alloc(v.empty() ? 1 : v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void zero(cudaStream_t s) {
+    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+class StageProfiler {
+ public:
+  StageProfiler(const char* what, cudaStream_t st) : what_(what), st_(st) {
+    const char* e = std::getenv("BDDC_B200_PROFILE");
+    on_ = e && *e && *e != '0';
+    if (on_) mark("start");
+  }
+  bool on() const { return on_; }
+  void mark(const char* name) {
+    if (!on_) return;
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, st_));
+    ev_.push_back(e);
+    names_.push_back(name);
+  }
+  ~StageProfiler() {
+    if (!on_) return;
+    cudaEventSynchronize(ev_.back());
+    std::string line = std::string("[profile] ") + what_;
+    for (std::size_t i = 1; i < ev_.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev_[i - 1], ev_[i]);
+      char buf[96];
+      std::snprintf(buf, sizeof(buf), " %s=%.3fms", names_[i].c_str(), ms);
+      line += buf;
+    }
+    std::fprintf(stderr, "%s\n", line.c_str());
+    for (auto e : ev_) cudaEventDestroy(e);
+  }
+
+ private:
+  const char* what_;
+  cudaStream_t st_;
+  bool on_ = false;
+  std::vector<cudaEvent_t> ev_;
+  std::vector<std::string> names_;
+};
+
+}  // namespace b200

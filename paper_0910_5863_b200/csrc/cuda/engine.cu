@@ -10,6 +10,7 @@
 #include <numeric>
 #include <string>
 
+#include "devbuf.cuh"
 #include "pairs.cuh"
 
 namespace b200 {
@@ -19,39 +20,13 @@ void cuda_check(cudaError_t e, const char* file, int line) {
     throw Error(kCudaError, std::string("CUDA error ") + cudaGetErrorString(e) + " at " + file + ":" +
                                 std::to_string(line));
 }
-#define CK(x) ::b200::cuda_check((x), __FILE__, __LINE__)
 
 namespace {
 
 constexpr int kRed = 256;  // blocks of the deterministic dot-product reductions
+constexpr int kRootInverseMax = 12288;  // explicit root inverse up to this padded size (2.4 GB front)
 
 inline int rup(int v, int m) { return (v + m - 1) / m * m; }
-
-template <class T>
-struct DBuf {
-  T* p = nullptr;
-  std::size_t n = 0;
-  DBuf() = default;
-  DBuf(const DBuf&) = delete;
-  ~DBuf() { release(); }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-  void alloc(std::size_t k) {
-    release();
-    n = k;
-    if (k) CK(cudaMalloc(&p, k * sizeof(T)));
-  }
-  void upload(const std::vector<T>& v, cudaStream_t s) {
-    if (v.size() != n) alloc(v.size());
-    if (n) CK(cudaMemcpyAsync(p, v.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
-  }
-  void zero(cudaStream_t s) {
-    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
-  }
-};
 
 struct PcgState {
   double rz, pq, alpha, beta, bnorm, ref, relres, tol;
@@ -152,6 +127,37 @@ __global__ void __launch_bounds__(256) k_schur_gemv(const SubDesc* sd, const dou
     for (; c < d.nB; ++c) s0 += col[(size_t)c * d.PB] * xs[c];
     d.WB[b] = (s0 + s1) + (s2 + s3);
   }
+}
+
+// Row-blocked variant: CTA (rb, s) forms rows [64 rb, 64 rb + 64) of S_s x_s;
+// the four 64-thread groups split the columns and are reduced in shared memory.
+__global__ void __launch_bounds__(256) k_schur_gemv_rows(const SubDesc* sd, const double* __restrict__ p,
+                                                         const int* done) {
+  if (done && *done) return;
+  const SubDesc d = sd[blockIdx.y];
+  const int r0 = blockIdx.x * 64;
+  if (r0 >= d.nB) return;
+  extern __shared__ double xs[];
+  __shared__ double part[4][64];
+  for (int c = threadIdx.x; c < d.nB; c += blockDim.x) xs[c] = p[d.biface[c]];
+  __syncthreads();
+  const int g = threadIdx.x >> 6, r = r0 + (threadIdx.x & 63);
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  if (r < d.PB) {
+    const double* row = d.S + r;
+    int c = g;
+    for (; c + 12 < d.nB; c += 16) {
+      s0 += row[(size_t)c * d.PB] * xs[c];
+      s1 += row[(size_t)(c + 4) * d.PB] * xs[c + 4];
+      s2 += row[(size_t)(c + 8) * d.PB] * xs[c + 8];
+      s3 += row[(size_t)(c + 12) * d.PB] * xs[c + 12];
+    }
+    for (; c < d.nB; c += 4) s0 += row[(size_t)c * d.PB] * xs[c];
+  }
+  part[g][threadIdx.x & 63] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (threadIdx.x < 64 && r < d.nB)
+    d.WB[r] = (part[0][threadIdx.x] + part[1][threadIdx.x]) + (part[2][threadIdx.x] + part[3][threadIdx.x]);
 }
 
 __device__ __forceinline__ void block_partial(double v, double* partials) {
@@ -335,10 +341,11 @@ __global__ void k_rowxform_scatter(const SubDesc* sd, XformDesc x, const double*
   // the padding positions of F get identity entries in k_pad_identity
 }
 
-__global__ void k_pad_identity(double* F, int NF, const int* pads, int npads) {
+__global__ void k_pad_identity(double* Farena, const long long* foff, const int* NF, const int* pad_sub,
+                               const int* pads, int npads) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < npads; t += gridDim.x * blockDim.x) {
-    const int q = pads[t];
-    F[(size_t)q * NF + q] = 1.0;
+    const int q = pads[t], s = pad_sub[t];
+    Farena[foff[s] + (size_t)q * NF[s] + q] = 1.0;
   }
 }
 
@@ -351,7 +358,9 @@ struct RootAsm {
   const int* PE;
 };
 
-__global__ void k_root_assemble(int n_root, int NR, RootAsm ra, const double* Farena, double* R) {
+// Root front R (NR x NR, leading dimension ld).  With ld == 2 NR the front is
+// augmented as [[R, .], [I, 0]]: eliminating R leaves -R^{-1} in the trailing block.
+__global__ void k_root_assemble(int n_root, int NR, long ld, RootAsm ra, const double* Farena, double* R) {
   const long total = (long)n_root * (n_root + 1) / 2;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
     int k1 = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
@@ -376,10 +385,35 @@ __global__ void k_root_assemble(int n_root, int NR, RootAsm ra, const double* Fa
         ++b;
       }
     }
-    R[(size_t)k2 * NR + k1] = s;
+    R[(size_t)k2 * ld + k1] = s;
   }
   for (long q = n_root + blockIdx.x * (long)blockDim.x + threadIdx.x; q < NR; q += (long)gridDim.x * blockDim.x)
-    R[(size_t)q * NR + q] = 1.0;
+    R[(size_t)q * ld + q] = 1.0;
+  if (ld > NR)
+    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < NR; q += (long)gridDim.x * blockDim.x)
+      R[(size_t)q * ld + NR + q] = 1.0;
+}
+
+// x = -T b with T = -R^{-1} (full symmetric, NR x NR): one warp per output, reading
+// one column of T (coalesced; symmetric so column == row).
+__global__ void __launch_bounds__(256) k_root_gemv(int NR, const double* __restrict__ T, const double* __restrict__ b,
+                                                   double* __restrict__ x, const int* done) {
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < NR; c += warps) {
+    const double* col = T + (size_t)c * NR;
+    double s0 = 0.0, s1 = 0.0;
+    int r = lane;
+    for (; r + 32 < NR; r += 64) {
+      s0 += col[r] * b[r];
+      s1 += col[r + 32] * b[r + 32];
+    }
+    if (r < NR) s0 += col[r] * b[r];
+    double s = s0 + s1;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) x[c] = -s;
+  }
 }
 
 __global__ void k_extract_boundary(const SubDesc* sd, const double* MV, const long long* mvoff, const int* PI) {
@@ -387,8 +421,16 @@ __global__ void k_extract_boundary(const SubDesc* sd, const double* MV, const lo
   for (int b = threadIdx.x; b < d.nB; b += blockDim.x) d.WB[b] = MV[mvoff[blockIdx.x] + PI[blockIdx.x] + b];
 }
 
+__global__ void k_scatter_solution(long long nmv, const long long* gdof, const double* MV, i64 niface,
+                                   const long long* igdof, const double* uiface, double* u) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nmv; t += (long long)gridDim.x * blockDim.x)
+    if (gdof[t] >= 0) u[gdof[t]] = MV[t];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < niface; i += (long long)gridDim.x * blockDim.x)
+    u[igdof[i]] = uiface[i];
+}
+
 __global__ void k_insert_boundary(const SubDesc* sd, double* MV, const long long* mvoff, const int* PI,
-                                  const double* u_iface) {
+                                  const double* __restrict__ u_iface) {
   const SubDesc d = sd[blockIdx.x];
   for (int b = threadIdx.x; b < d.nB; b += blockDim.x) MV[mvoff[blockIdx.x] + PI[blockIdx.x] + b] = u_iface[d.biface[b]];
 }
@@ -400,14 +442,23 @@ __global__ void k_insert_boundary(const SubDesc* sd, double* MV, const long long
 // ---------------------------------------------------------------------------
 struct DeviceState {
   cudaStream_t st = nullptr;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, ef0 = nullptr, ef1 = nullptr, s0 = nullptr, s1 = nullptr, s2 = nullptr;
+  DBuf<double> ufree;
   int nsub = 0;
   i64 niface = 0;
   std::vector<int> nI, nB, PI, PB, NM;
   std::vector<long long> m_off, dm_off, s_off, wb_off, mv_off;
   int max_NM = 0, max_PI = 0, max_PB = 0, max_nB = 0;
-  DBuf<double> M, DinvM, S, MV, WB;
-  DBuf<int> minfo;
+  bool prepared = false;
+  struct HostStage {
+    std::vector<int> ptr, idx, pos, biface, icp, icpos;
+    std::vector<double> val, mv, bw;
+  } h;
+  DBuf<double> M, DinvM, S, MV, MV0, WB;
+  DBuf<int> minfo, csr_ptr, csr_idx, csr_pos;
+  DBuf<double> csr_val;
+  DBuf<ScatterDesc> scatter;
+  DBuf<TrailDesc> mtrail;
   DBuf<FrontDesc> mfront;
   DBuf<SolveDesc> msolve;
   DBuf<long long> d_mvoff;
@@ -416,6 +467,7 @@ struct DeviceState {
   DBuf<int> biface, bposF, bglob, bslot, icopy_ptr, icopy_pos;
   DBuf<double> bw;
   DBuf<double> rhs;  // condensed rhs (interface)
+  DBuf<long long> sol_gdof, iface_gdof;
   // preconditioner
   bool have_prec = false;
   std::vector<int> NF, PE, nE, nC;
@@ -433,8 +485,10 @@ struct DeviceState {
   XformDesc xf{};
   // root
   int n_root = 0, NR = 0;
-  DBuf<double> R, DinvR, xroot;
-  DBuf<int> rinfo, root_ptr, root_sub, root_c, d_NF, d_PE;
+  DBuf<double> R, DinvR, xroot, xroot2, Rinv;
+  bool root_inv = false;
+  DBuf<TrailDesc> rtrail;
+  DBuf<int> rinfo, root_ptr, root_sub, root_c, d_NF, d_PE, pads, pad_sub;
   DBuf<long long> root_src, d_foff;
   DBuf<FrontDesc> rfront;
   DBuf<SolveDesc> rsolve;
@@ -443,7 +497,7 @@ struct DeviceState {
   DBuf<PcgState> pst;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
-  int graph_max_it = -1;
+  long long graph_kernels = 0;
   // adaptive pair machinery
   PairEngine pairs;
 
@@ -452,6 +506,8 @@ struct DeviceState {
     if (graph) cudaGraphDestroy(graph);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
+    for (cudaEvent_t e : {ef0, ef1, s0, s1, s2})
+      if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -463,6 +519,11 @@ Engine::Engine(const Model& m) : m_(m), d_(new DeviceState) {
   CK(cudaStreamCreateWithFlags(&d_->st, cudaStreamNonBlocking));
   CK(cudaEventCreate(&d_->e0));
   CK(cudaEventCreate(&d_->e1));
+  CK(cudaEventCreate(&d_->ef0));
+  CK(cudaEventCreate(&d_->ef1));
+  CK(cudaEventCreate(&d_->s0));
+  CK(cudaEventCreate(&d_->s1));
+  CK(cudaEventCreate(&d_->s2));
 }
 
 Engine::~Engine() = default;
@@ -481,10 +542,14 @@ double elapsed(cudaEvent_t a, cudaEvent_t b) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// analysis: A_s -> dense fronts -> partial Cholesky (eliminate interior)
+// prepare: host staging of the inputs (CSR, positions, maps, loads) and device
+// allocations; upload_inputs: the host->device copies of those inputs;
+// analysis: A_s -> dense fronts -> partial Cholesky (eliminate the interior),
+// interface Schur complements, condensed rhs (spaces.cpp:108-147, schur.cpp:38-55).
 // ---------------------------------------------------------------------------
-void Engine::analysis() {
+void Engine::prepare() {
   DeviceState& D = *d_;
+  if (D.prepared) return;
   const Model& m = m_;
   D.nsub = static_cast<int>(m.subs.size());
   D.niface = interface_size();
@@ -523,112 +588,149 @@ void Engine::analysis() {
     D.max_nB = std::max(D.max_nB, D.nB[s]);
   }
   cudaStream_t st = D.st;
-  CK(cudaEventRecord(D.e0, st));
   D.M.alloc(mo);
-  D.M.zero(st);
   D.DinvM.alloc(std::max<long long>(dmo, 1));
   D.S.alloc(so);
   D.MV.alloc(mvo);
+  D.MV0.alloc(mvo);
   D.WB.alloc(std::max<long long>(wbo, 1));
-  // CSR upload with dense positions
-  std::vector<int> ptr, idx, pos;
-  std::vector<double> val;
+  // host staging: CSR with dense positions, loads in front layout
   std::vector<long long> ptr_off(ns), idx_off(ns), pos_off(ns);
+  auto& H = D.h;
+  H.ptr.clear();
+  H.idx.clear();
+  H.pos.clear();
+  H.val.clear();
   for (int s = 0; s < ns; ++s) {
     const Subdomain& S = m.subs[s];
-    ptr_off[s] = ptr.size();
-    idx_off[s] = idx.size();
-    pos_off[s] = pos.size();
-    ptr.insert(ptr.end(), S.A.ptr.begin(), S.A.ptr.end());
-    idx.insert(idx.end(), S.A.idx.begin(), S.A.idx.end());
-    val.insert(val.end(), S.A.val.begin(), S.A.val.end());
+    ptr_off[s] = H.ptr.size();
+    idx_off[s] = H.idx.size();
+    pos_off[s] = H.pos.size();
+    H.ptr.insert(H.ptr.end(), S.A.ptr.begin(), S.A.ptr.end());
+    H.idx.insert(H.idx.end(), S.A.idx.begin(), S.A.idx.end());
+    H.val.insert(H.val.end(), S.A.val.begin(), S.A.val.end());
     std::vector<int> p(S.dim());
     for (int r = 0; r < D.nI[s]; ++r) p[S.interior[r]] = r;
     for (int b = 0; b < D.nB[s]; ++b) p[S.boundary[b]] = D.PI[s] + b;
-    pos.insert(pos.end(), p.begin(), p.end());
+    H.pos.insert(H.pos.end(), p.begin(), p.end());
   }
-  DBuf<int> dptr, didx, dpos;
-  DBuf<double> dval;
-  dptr.upload(ptr, st);
-  didx.upload(idx, st);
-  dpos.upload(pos, st);
-  dval.upload(val, st);
-  std::vector<ScatterDesc> sc(ns);
-  std::vector<FrontDesc> fd(ns);
-  std::vector<SolveDesc> sv(ns);
-  std::vector<TrailDesc> td(ns);
-  D.minfo.alloc(ns);
-  D.minfo.zero(st);
+  H.mv.assign(mvo, 0.0);
   for (int s = 0; s < ns; ++s) {
-    sc[s] = ScatterDesc{dptr.p + ptr_off[s], didx.p + idx_off[s], dval.p + idx_off[s], dpos.p + pos_off[s],
-                        D.M.p + D.m_off[s], m.subs[s].dim(), D.NM[s], D.nI[s], D.PI[s], D.nB[s]};
-    fd[s] = FrontDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.NM[s], D.PI[s], D.minfo.p + s, 0};
-    sv[s] = SolveDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.MV.p + D.mv_off[s], D.NM[s], D.PI[s],
-                      nullptr, nullptr};
-    td[s] = TrailDesc{D.M.p + D.m_off[s], D.S.p + D.s_off[s], D.NM[s], D.PI[s]};
+    const Subdomain& S = m.subs[s];
+    for (int r = 0; r < D.nI[s]; ++r) H.mv[D.mv_off[s] + r] = S.load[S.interior[r]];
+    for (int b = 0; b < D.nB[s]; ++b) H.mv[D.mv_off[s] + D.PI[s] + b] = S.load[S.boundary[b]];
   }
-  DBuf<ScatterDesc> dsc;
-  DBuf<TrailDesc> dtd;
-  dsc.upload(sc, st);
-  D.mfront.upload(fd, st);
-  D.msolve.upload(sv, st);
-  dtd.upload(td, st);
-  k_scatter_csr<<<dim3(8, ns), 256, 0, st>>>(dsc.p);
-  CK(cudaGetLastError());
-  partial_cholesky(D.mfront.p, ns, D.max_NM, D.max_PI, D.max_PB, st);
-  CK(cudaGetLastError());
-  copy_trailing_full(dtd.p, ns, D.max_PB, st);
-  CK(cudaGetLastError());
-  // interface maps
-  std::vector<int> biface(wbo), icp(D.niface + 1, 0), icpos;
-  std::vector<double> bw(wbo);
+  // interface maps and averaging weights (spaces.cpp:71-86)
+  H.biface.assign(wbo, 0);
+  H.bw.assign(wbo, 0.0);
   for (int s = 0; s < ns; ++s) {
     const Subdomain& S = m.subs[s];
     for (int b = 0; b < D.nB[s]; ++b) {
       const i64 g = S.global_dof[S.boundary[b]];
-      biface[D.wb_off[s] + b] = static_cast<int>(m.maps.global_to_interface[g]);
-      // averaging weight: A_s(l,l) / sum over copies (spaces.cpp:71-86)
+      H.biface[D.wb_off[s] + b] = static_cast<int>(m.maps.global_to_interface[g]);
       double tot = 0.0;
       for (i64 t = m.maps.copy_ptr[g]; t < m.maps.copy_ptr[g + 1]; ++t)
         tot += m.subs[m.maps.copy_sub[t]].A.diag(m.maps.copy_local[t]);
-      bw[D.wb_off[s] + b] = S.A.diag(S.boundary[b]) / tot;
+      H.bw[D.wb_off[s] + b] = S.A.diag(S.boundary[b]) / tot;
     }
   }
-  // interface dof -> WB positions of its copies, ascending subdomain
   std::vector<std::vector<int>> lists(D.niface);
   for (int s = 0; s < ns; ++s)
-    for (int b = 0; b < D.nB[s]; ++b) lists[biface[D.wb_off[s] + b]].push_back(static_cast<int>(D.wb_off[s] + b));
+    for (int b = 0; b < D.nB[s]; ++b) lists[H.biface[D.wb_off[s] + b]].push_back(static_cast<int>(D.wb_off[s] + b));
+  H.icp.assign(D.niface + 1, 0);
+  H.icpos.clear();
   for (i64 i = 0; i < D.niface; ++i) {
-    icp[i + 1] = icp[i] + static_cast<int>(lists[i].size());
-    icpos.insert(icpos.end(), lists[i].begin(), lists[i].end());
+    H.icp[i + 1] = H.icp[i] + static_cast<int>(lists[i].size());
+    H.icpos.insert(H.icpos.end(), lists[i].begin(), lists[i].end());
   }
-  D.biface.upload(biface, st);
-  D.bw.upload(bw, st);
-  D.icopy_ptr.upload(icp, st);
-  D.icopy_pos.upload(icpos, st);
-  // condensed rhs: forward sweep on [f_I; f_B] then sum the boundary rows
-  std::vector<double> mv(mvo, 0.0);
-  for (int s = 0; s < ns; ++s) {
-    const Subdomain& S = m.subs[s];
-    for (int r = 0; r < D.nI[s]; ++r) mv[D.mv_off[s] + r] = S.load[S.interior[r]];
-    for (int b = 0; b < D.nB[s]; ++b) mv[D.mv_off[s] + D.PI[s] + b] = S.load[S.boundary[b]];
-  }
-  D.MV.upload(mv, st);
-  front_forward(D.msolve.p, ns, D.max_NM, st);
-  // per-subdomain descriptors (partial, preconditioner fields filled later)
+  D.csr_ptr.alloc(H.ptr.size());
+  D.csr_idx.alloc(std::max<std::size_t>(H.idx.size(), 1));
+  D.csr_pos.alloc(std::max<std::size_t>(H.pos.size(), 1));
+  D.csr_val.alloc(std::max<std::size_t>(H.val.size(), 1));
+  D.biface.alloc(std::max<long long>(wbo, 1));
+  D.bw.alloc(std::max<long long>(wbo, 1));
+  D.icopy_ptr.alloc(H.icp.size());
+  D.icopy_pos.alloc(std::max<std::size_t>(H.icpos.size(), 1));
+  D.minfo.alloc(ns);
+  D.rhs.alloc(std::max<i64>(D.niface, 1));
+  std::vector<ScatterDesc> sc(ns);
+  std::vector<FrontDesc> fd(ns);
+  std::vector<SolveDesc> sv(ns);
+  std::vector<TrailDesc> td(ns);
   std::vector<SubDesc> sd(ns);
-  for (int s = 0; s < ns; ++s)
+  for (int s = 0; s < ns; ++s) {
+    sc[s] = ScatterDesc{D.csr_ptr.p + ptr_off[s], D.csr_idx.p + idx_off[s], D.csr_val.p + idx_off[s],
+                        D.csr_pos.p + pos_off[s], D.M.p + D.m_off[s], m.subs[s].dim(), D.NM[s], D.nI[s], D.PI[s],
+                        D.nB[s]};
+    fd[s] = FrontDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.NM[s], D.PI[s], D.minfo.p + s, 0};
+    sv[s] = SolveDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.MV.p + D.mv_off[s], D.NM[s], D.PI[s],
+                      nullptr, nullptr};
+    td[s] = TrailDesc{D.M.p + D.m_off[s], D.S.p + D.s_off[s], D.NM[s], D.PI[s]};
     sd[s] = SubDesc{D.S.p + D.s_off[s], nullptr, nullptr, D.biface.p + D.wb_off[s], D.bw.p + D.wb_off[s],
                     nullptr, nullptr, nullptr, D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], 0, 0};
+  }
+  D.scatter.upload(sc, st);
+  D.mfront.upload(fd, st);
+  D.msolve.upload(sv, st);
+  D.mtrail.upload(td, st);
   D.subdesc.upload(sd, st);
   D.d_mvoff.upload(D.mv_off, st);
   D.d_PI.upload(D.PI, st);
+  D.pairs.attach(m, D.S.p, D.s_off, D.PB, D.nB, st);
+  D.prepared = true;
+  upload_inputs();
+  CK(cudaStreamSynchronize(st));
+}
+
+double Engine::upload_inputs() {
+  DeviceState& D = *d_;
+  auto& H = D.h;
+  cudaStream_t st = D.st;
+  double bytes = 0;
+  auto cp = [&](void* dst, const void* src, std::size_t n) {
+    if (n) CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
+    bytes += double(n);
+  };
+  cp(D.csr_ptr.p, H.ptr.data(), H.ptr.size() * sizeof(int));
+  cp(D.csr_idx.p, H.idx.data(), H.idx.size() * sizeof(int));
+  cp(D.csr_pos.p, H.pos.data(), H.pos.size() * sizeof(int));
+  cp(D.csr_val.p, H.val.data(), H.val.size() * sizeof(double));
+  cp(D.MV0.p, H.mv.data(), H.mv.size() * sizeof(double));
+  cp(D.biface.p, H.biface.data(), H.biface.size() * sizeof(int));
+  cp(D.bw.p, H.bw.data(), H.bw.size() * sizeof(double));
+  cp(D.icopy_ptr.p, H.icp.data(), H.icp.size() * sizeof(int));
+  cp(D.icopy_pos.p, H.icpos.data(), H.icpos.size() * sizeof(int));
+  return bytes;
+}
+
+void Engine::analysis() {
+  prepare();
+  DeviceState& D = *d_;
+  const int ns = D.nsub;
+  cudaStream_t st = D.st;
+  CK(cudaEventRecord(D.e0, st));
+  D.M.zero(st);
+  D.minfo.zero(st);
+  k_scatter_csr<<<dim3(8, ns), 256, 0, st>>>(D.scatter.p);
+  count_launch(1);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(D.ef0, st));
+  partial_cholesky(D.mfront.p, ns, D.max_NM, D.max_PI, D.max_PB, st);
+  CK(cudaEventRecord(D.ef1, st));
+  CK(cudaGetLastError());
+  copy_trailing_full(D.mtrail.p, ns, D.max_PB, st);
+  count_launch(1);
+  CK(cudaGetLastError());
+  // condensed rhs: forward sweep on [f_I; f_B], then sum the boundary rows over copies
+  CK(cudaMemcpyAsync(D.MV.p, D.MV0.p, D.MV.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  front_forward(D.msolve.p, ns, D.max_NM, st);
   k_extract_boundary<<<ns, 256, 0, st>>>(D.subdesc.p, D.MV.p, D.d_mvoff.p, D.d_PI.p);
-  D.rhs.alloc(std::max<i64>(D.niface, 1));
   k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, D.rhs.p, nullptr, nullptr, nullptr);
+  count_launch(3);
   CK(cudaGetLastError());
   CK(cudaEventRecord(D.e1, st));
   times_.analysis = elapsed(D.e0, D.e1);
+  times_.leaf_factor = elapsed(D.ef0, D.ef1);
   std::vector<int> info(ns);
   CK(cudaMemcpy(info.data(), D.minfo.p, ns * sizeof(int), cudaMemcpyDeviceToHost));
   for (int s = 0; s < ns; ++s)
@@ -640,8 +742,6 @@ void Engine::analysis() {
     fl += ni * ni * ni / 3.0 + ni * ni * nb + ni * nb * nb;
   }
   times_.flops_leaf = fl;
-  // pair engine needs the interface Schur complements
-  D.pairs.attach(m, D.S.p, D.s_off, D.PB, D.nB, st);
 }
 
 double Engine::schur_bytes() const {
@@ -740,7 +840,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   D.f_off.assign(ns, 0);
   D.df_off.assign(ns, 0);
   D.fv_off.assign(ns, 0);
-  std::vector<int> posF(D.WB.n, 0), cmap, pads;
+  std::vector<int> posF(D.WB.n, 0), cmap, pads, pad_sub;
   std::vector<long long> cmap_off(ns), pad_off(ns + 1), xoff(ns);
   long long fo = 0, dfo = 0, fvo = 0, xo = 0;
   D.max_NF = D.max_PE = D.max_M = 0;
@@ -770,8 +870,14 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     cmap_off[s] = cmap.size();
     for (int c = 0; c < D.NF[s] - D.PE[s]; ++c) cmap.push_back(c < nC ? coarse_root[s][c] : -1);
     pad_off[s] = pads.size();
-    for (int q = nE; q < D.PE[s]; ++q) pads.push_back(q);
-    for (int q = D.PE[s] + nC; q < D.NF[s]; ++q) pads.push_back(q);
+    for (int q = nE; q < D.PE[s]; ++q) {
+      pads.push_back(q);
+      pad_sub.push_back(s);
+    }
+    for (int q = D.PE[s] + nC; q < D.NF[s]; ++q) {
+      pads.push_back(q);
+      pad_sub.push_back(s);
+    }
     for (int c = 0; c < nC; ++c) ++root_cnt[coarse_root[s][c] + 1];
   }
   pad_off[ns] = pads.size();
@@ -833,17 +939,22 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   D.subdesc.upload(sd, st);
   D.ffront.upload(fd, st);
   D.fsolve_fwd.upload(fw, st);
-  // root front
-  D.R.alloc((size_t)D.NR * D.NR);
+  // root front; up to kRootInverseMax rows it is augmented to [[R, .], [I, 0]] so
+  // that the factorization leaves -R^{-1} and every apply is one parallel GEMV
+  D.root_inv = D.NR <= kRootInverseMax;
+  const long ldR = D.root_inv ? 2L * D.NR : D.NR;
+  D.R.alloc((size_t)ldR * ldR);
   D.R.zero(st);
   D.DinvR.alloc((size_t)D.NR * kTile);
   D.xroot.alloc(D.NR);
+  D.xroot2.alloc(D.NR);
+  if (D.root_inv) D.Rinv.alloc((size_t)D.NR * D.NR);
   D.rinfo.alloc(1);
   D.rinfo.zero(st);
   for (int s = 0; s < ns; ++s) {
     bw[s] = fw[s];
     bw[s].cmap = D.cmap.p + cmap_off[s];
-    bw[s].croot = D.xroot.p;
+    bw[s].croot = D.root_inv ? D.xroot2.p : D.xroot.p;
   }
   D.fsolve_bwd.upload(bw, st);
   up_i(D.root_ptr, rptr);
@@ -853,23 +964,34 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   D.d_foff.upload(D.f_off, st);
   up_i(D.d_NF, D.NF);
   up_i(D.d_PE, D.PE);
-  DBuf<int> dpads;
-  up_i(dpads, pads);
+  up_i(D.pads, pads);
+  up_i(D.pad_sub, pad_sub);
+  StageProfiler prof("set_constraints", st);
   // F = P (T^T S T) P^T, pads identity
   k_colxform<<<dim3(D.max_PB, ns), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
   k_rowxform_scatter<<<dim3(D.max_PB, ns), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
-  for (int s = 0; s < ns; ++s) {
-    const int np = static_cast<int>(pad_off[s + 1] - pad_off[s]);
-    if (np) k_pad_identity<<<1, 128, 0, st>>>(D.F.p + D.f_off[s], D.NF[s], dpads.p + pad_off[s], np);
-  }
+  if (!pads.empty())
+    k_pad_identity<<<std::min<int>(1024, (static_cast<int>(pads.size()) + 255) / 256), 256, 0, st>>>(
+        D.F.p, D.d_foff.p, D.d_NF.p, D.pad_sub.p, D.pads.p, static_cast<int>(pads.size()));
+  count_launch(3);
   CK(cudaGetLastError());
+  prof.mark("xform");
   partial_cholesky(D.ffront.p, ns, D.max_NF, D.max_PE, D.max_M, st);
   CK(cudaGetLastError());
+  prof.mark("cholF");
   RootAsm ra{D.root_ptr.p, D.root_sub.p, D.root_c.p, D.d_foff.p, D.d_NF.p, D.d_PE.p};
-  k_root_assemble<<<1024, 256, 0, st>>>(D.n_root, D.NR, ra, D.F.p, D.R.p);
-  std::vector<FrontDesc> rf{FrontDesc{D.R.p, D.DinvR.p, D.NR, D.NR, D.rinfo.p, 0}};
+  k_root_assemble<<<1024, 256, 0, st>>>(D.n_root, D.NR, ldR, ra, D.F.p, D.R.p);
+  count_launch(1);
+  std::vector<FrontDesc> rf{FrontDesc{D.R.p, D.DinvR.p, static_cast<int>(ldR), D.NR, D.rinfo.p, 0}};
   D.rfront.upload(rf, st);
-  partial_cholesky(D.rfront.p, 1, D.NR, D.NR, 0, st);
+  prof.mark("root_asm");
+  partial_cholesky(D.rfront.p, 1, static_cast<int>(ldR), D.NR, D.root_inv ? D.NR : 0, st);
+  if (D.root_inv) {
+    std::vector<TrailDesc> rt{TrailDesc{D.R.p, D.Rinv.p, static_cast<int>(ldR), D.NR}};
+    D.rtrail.upload(rt, st);
+    copy_trailing_full(D.rtrail.p, 1, D.NR, st);
+  }
+  prof.mark(D.root_inv ? "cholR+inverse" : "cholR");
   std::vector<SolveDesc> rs{SolveDesc{D.R.p, D.DinvR.p, D.xroot.p, D.NR, D.NR, nullptr, nullptr}};
   D.rsolve.upload(rs, st);
   CK(cudaGetLastError());
@@ -900,25 +1022,45 @@ void Engine::set_constraints(const ConstraintSet& cs) {
 // ---------------------------------------------------------------------------
 namespace {
 void launch_precond(DeviceState& D, const double* r, double* z, const double* dot_with, double* partials,
-                    const int* done) {
+                    const int* done, StageProfiler* prof = nullptr) {
   cudaStream_t st = D.st;
   const int ns = D.nsub;
   const int smem_b = D.max_nB * sizeof(double);
+  auto mark = [&](const char* s) {
+    if (prof) prof->mark(s);
+  };
   k_restrict<<<ns, 256, smem_b, st>>>(D.subdesc.p, D.xf, r, done);
+  count_launch(4);
+  mark("restrict");
   front_forward(D.fsolve_fwd.p, ns, D.max_NF, st, done);
+  mark("leaf_fwd");
   k_root_gather<<<std::max(1, std::min(1024, (D.NR + 255) / 256)), 256, 0, st>>>(D.n_root, D.NR, D.root_ptr.p,
                                                                              D.root_src.p, D.FV.p, D.xroot.p, done);
-  front_forward(D.rsolve.p, 1, D.NR, st, done);
-  front_backward(D.rsolve.p, 1, D.NR, st, done);
+  mark("root_gather");
+  if (D.root_inv) {
+    k_root_gemv<<<std::min(1184, (D.NR + 7) / 8), 256, 0, st>>>(D.NR, D.Rinv.p, D.xroot.p, D.xroot2.p, done);
+    count_launch(1);
+    mark("root_gemv");
+  } else {
+    front_forward(D.rsolve.p, 1, D.NR, st, done);
+    mark("root_fwd");
+    front_backward(D.rsolve.p, 1, D.NR, st, done);
+    mark("root_bwd");
+  }
   front_backward(D.fsolve_bwd.p, ns, D.max_NF, st, done);
+  mark("leaf_bwd");
   k_prolong<<<ns, 256, smem_b, st>>>(D.subdesc.p, D.xf, done);
+  mark("prolong");
   k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, z, dot_with, partials, done);
+  mark("sum_copies");
 }
 
 void launch_schur(DeviceState& D, const double* x, double* y, const double* dot_with, double* partials,
                   const int* done) {
   cudaStream_t st = D.st;
-  k_schur_gemv<<<D.nsub, 256, D.max_nB * sizeof(double), st>>>(D.subdesc.p, x, done);
+  k_schur_gemv_rows<<<dim3((D.max_nB + 63) / 64, D.nsub), 256, D.max_nB * sizeof(double), st>>>(D.subdesc.p, x,
+                                                                                               done);
+  count_launch(2);
   k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, y, dot_with, partials, done);
 }
 
@@ -966,30 +1108,42 @@ void Engine::rhs(double* out) {
   CK(cudaStreamSynchronize(D.st));
 }
 
-void Engine::recover(const double* u_interface, double* u_free) {
+// InterfaceProblem::recover (schur.cpp:57-75): x_I = A_II^{-1}(f_I - A_IB x_B),
+// as the forward sweep of the loads followed by the backward sweep with x_B.
+void Engine::recover_device(const double* d_uiface, double* d_ufree) {
   DeviceState& D = *d_;
   const Model& m = m_;
   const int ns = D.nsub;
-  ensure_vectors(D);
-  // forward sweep on the loads again (MV holds L_II^{-1} f_I in the interior rows)
-  std::vector<double> mv(D.MV.n, 0.0);
-  for (int s = 0; s < ns; ++s) {
-    const Subdomain& S = m.subs[s];
-    for (int r = 0; r < D.nI[s]; ++r) mv[D.mv_off[s] + r] = S.load[S.interior[r]];
+  cudaStream_t st = D.st;
+  if (D.sol_gdof.n == 0) {
+    std::vector<long long> g(D.MV.n, -1), ig(m.maps.interface_dofs.begin(), m.maps.interface_dofs.end());
+    for (int s = 0; s < ns; ++s) {
+      const Subdomain& S = m.subs[s];
+      for (int r = 0; r < D.nI[s]; ++r) g[D.mv_off[s] + r] = S.global_dof[S.interior[r]];
+    }
+    D.sol_gdof.upload(g, st);
+    if (ig.empty()) ig.push_back(0);
+    D.iface_gdof.upload(ig, st);
   }
-  D.MV.upload(mv, D.st);
-  front_forward(D.msolve.p, ns, D.max_NM, D.st);
-  CK(cudaMemcpyAsync(D.vx.p, u_interface, D.niface * sizeof(double), cudaMemcpyHostToDevice, D.st));
-  k_insert_boundary<<<ns, 256, 0, D.st>>>(D.subdesc.p, D.MV.p, D.d_mvoff.p, D.d_PI.p, D.vx.p);
-  front_backward(D.msolve.p, ns, D.max_NM, D.st);
-  CK(cudaMemcpyAsync(mv.data(), D.MV.p, mv.size() * sizeof(double), cudaMemcpyDeviceToHost, D.st));
-  CK(cudaStreamSynchronize(D.st));
+  CK(cudaMemcpyAsync(D.MV.p, D.MV0.p, D.MV.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  front_forward(D.msolve.p, ns, D.max_NM, st);
+  k_insert_boundary<<<ns, 256, 0, st>>>(D.subdesc.p, D.MV.p, D.d_mvoff.p, D.d_PI.p, d_uiface);
+  front_backward(D.msolve.p, ns, D.max_NM, st);
+  k_scatter_solution<<<256, 256, 0, st>>>(static_cast<long long>(D.MV.n), D.sol_gdof.p, D.MV.p, D.niface,
+                                          D.iface_gdof.p, d_uiface, d_ufree);
+  count_launch(2);
   CK(cudaGetLastError());
-  for (i64 i = 0; i < D.niface; ++i) u_free[m.maps.interface_dofs[i]] = u_interface[i];
-  for (int s = 0; s < ns; ++s) {
-    const Subdomain& S = m.subs[s];
-    for (int r = 0; r < D.nI[s]; ++r) u_free[S.global_dof[S.interior[r]]] = mv[D.mv_off[s] + r];
-  }
+}
+
+void Engine::recover(const double* u_interface, double* u_free) {
+  DeviceState& D = *d_;
+  ensure_vectors(D);
+  DBuf<double> uf;
+  uf.alloc(std::max<i64>(m_.free_count, 1));
+  CK(cudaMemcpyAsync(D.vx.p, u_interface, D.niface * sizeof(double), cudaMemcpyHostToDevice, D.st));
+  recover_device(D.vx.p, uf.p);
+  CK(cudaMemcpyAsync(u_free, uf.p, m_.free_count * sizeof(double), cudaMemcpyDeviceToHost, D.st));
+  CK(cudaStreamSynchronize(D.st));
 }
 
 PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool precond_residual) {
@@ -1011,9 +1165,18 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
   // r = b, x = 0, z = M r, p = z, rz = r.z   (pcg.cpp:32-41)
   CK(cudaMemcpyAsync(D.vr.p, D.vb.p, bytes, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(D.vx.p, 0, bytes, st));
-  launch_precond(D, D.vr.p, D.vz.p, D.vr.p, D.part_a.p, nullptr);
+  {
+    StageProfiler prof("precond_apply", st);
+    launch_precond(D, D.vr.p, D.vz.p, D.vr.p, D.part_a.p, nullptr, &prof);
+    if (prof.on()) {
+      StageProfiler prof2("schur_apply", st);
+      launch_schur(D, D.vz.p, D.vq.p, nullptr, nullptr, nullptr);
+      prof2.mark("schur");
+    }
+  }
   CK(cudaMemcpyAsync(D.vp.p, D.vz.p, bytes, cudaMemcpyDeviceToDevice, st));
   k_dot<<<kRed, 256, 0, st>>>(n, D.vb.p, D.vb.p, D.part_b.p);
+  count_launch(1);
   std::vector<double> pa(kRed), pb(kRed);
   CK(cudaMemcpyAsync(pa.data(), D.part_a.p, kRed * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(pb.data(), D.part_b.p, kRed * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1044,6 +1207,7 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
   CK(cudaMemcpyAsync(D.pst.p, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   // capture one iteration as a graph (pcg.cpp:49-70)
   if (!D.gexec) {
+    const long long before = launch_count();
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     const int* done = &D.pst.p->done;
     launch_schur(D, D.vp.p, D.vq.p, D.vp.p, D.part_a.p, done);
@@ -1054,11 +1218,14 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
     k_update_p<<<kRed, 256, 0, st>>>(n, D.pst.p, D.vp.p, D.vz.p);
     CK(cudaStreamEndCapture(st, &D.graph));
     CK(cudaGraphInstantiate(&D.gexec, D.graph, 0));
+    D.graph_kernels = launch_count() - before + 4;  // + k_alpha, k_axpy, k_beta, k_update_p
+    count_launch(-(launch_count() - before));
   }
   PcgState hs = h;
   const int chunk = 8;
   while (!hs.done) {
     for (int c = 0; c < chunk; ++c) CK(cudaGraphLaunch(D.gexec, st));
+    count_launch(chunk * D.graph_kernels);
     CK(cudaMemcpyAsync(&hs, D.pst.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   }
@@ -1076,6 +1243,43 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
   }
   out.condition_estimate = lanczos_condition_estimate(out.alphas, out.betas);
   if (x) CK(cudaMemcpy(x, D.vx.p, bytes, cudaMemcpyDeviceToHost));
+  return out;
+}
+
+StepOut Engine::step(const StepSpec& sp, ConstraintSet& cs, double* u_free_host) {
+  DeviceState& D = *d_;
+  prepare();
+  StepOut out;
+  const long long l0 = launch_count();
+  cudaStream_t st = D.st;
+  CK(cudaStreamSynchronize(st));
+  CK(cudaEventRecord(D.s0, st));
+  if (sp.e2e) out.h2d_bytes = upload_inputs();
+  analysis();
+  cs = arithmetic_constraints(m_, sp.edges, sp.faces);
+  if (sp.adaptive || sp.fixed_count >= 0) {
+    EnrichOptions o;
+    o.tau = sp.tau;
+    o.max_vectors = sp.max_vectors;
+    o.keep_edge_constraints = sp.keep_edge;
+    o.fixed_count = sp.fixed_count;
+    out.omega_tilde = enrich(cs, o).omega_tilde;
+  }
+  out.constraint_rows = cs.row_count(m_);
+  set_constraints(cs);
+  CK(cudaEventRecord(D.s1, st));
+  out.pcg = pcg(nullptr, nullptr, sp.tol, sp.max_it, false);
+  if (sp.e2e) {
+    if (D.ufree.n == 0) D.ufree.alloc(std::max<i64>(m_.free_count, 1));
+    recover_device(D.vx.p, D.ufree.p);
+    CK(cudaMemcpyAsync(u_free_host, D.ufree.p, m_.free_count * sizeof(double), cudaMemcpyDeviceToHost, st));
+    out.d2h_bytes = double(m_.free_count) * sizeof(double);
+  }
+  CK(cudaEventRecord(D.s2, st));
+  out.seconds = elapsed(D.s0, D.s2);
+  out.setup_seconds = elapsed(D.s0, D.s1);
+  out.solve_seconds = elapsed(D.s1, D.s2);
+  out.launches = launch_count() - l0;
   return out;
 }
 

@@ -56,7 +56,29 @@ struct EnrichOutcome {
 
 struct PhaseTimes {  // device-timed seconds (CUDA events) of the last calls
   double analysis = 0, eigen = 0, preconditioner = 0, pcg = 0;
+  double leaf_factor = 0;  // the batched partial Cholesky of the substructure leaves
   double flops_leaf = 0;   // algorithmic FP64 flops of the last leaf factorization
+};
+
+/// One pass of the hot path (bench "step"): analysis + constraint selection
+/// (+ adaptive enrichment) + transformed preconditioner + PCG [+ recovery].
+struct StepSpec {
+  bool edges = true, faces = false, adaptive = false;
+  int fixed_count = -1;
+  double tau = 10.0;
+  int max_vectors = 15;
+  bool keep_edge = false;
+  double tol = 1e-8;
+  int max_it = 500;
+  bool e2e = false;          // host->device inputs and device->host solution inside the step
+};
+struct StepOut {
+  double seconds = 0, setup_seconds = 0, solve_seconds = 0;
+  double h2d_bytes = 0, d2h_bytes = 0;
+  long long launches = 0;
+  i64 constraint_rows = 0;
+  double omega_tilde = 0;
+  PcgOut pcg;
 };
 
 struct DeviceState;
@@ -68,8 +90,12 @@ class Engine {
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
 
+  void prepare();              // host staging + device allocation + first upload
+  double upload_inputs();      // host->device copies of the inputs; returns bytes
   void analysis();
   void set_constraints(const ConstraintSet& cs);
+  StepOut step(const StepSpec& spec, ConstraintSet& cs, double* u_free_host);
+  void recover_device(const double* d_uiface, double* d_ufree);
   EnrichOutcome enrich(ConstraintSet& cs, const EnrichOptions& o);
 
   void schur_apply(const double* x, double* y);      // host vectors, interface size

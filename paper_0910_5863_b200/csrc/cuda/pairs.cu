@@ -22,41 +22,21 @@
 #include "pairs.cuh"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "dense.cuh"
+#include "devbuf.cuh"
 #include "engine.hpp"
 
 namespace b200 {
 
-void cuda_check(cudaError_t e, const char* file, int line);
-#define CK(x) ::b200::cuda_check((x), __FILE__, __LINE__)
-
 namespace {
 
 inline int rup(int v, int m) { return (v + m - 1) / m * m; }
-
-template <class T>
-struct Buf {
-  T* p = nullptr;
-  std::size_t n = 0;
-  Buf() = default;
-  Buf(const Buf&) = delete;
-  ~Buf() {
-    if (p) cudaFree(p);
-  }
-  void alloc(std::size_t k) {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = k;
-    if (k) CK(cudaMalloc(&p, k * sizeof(T)));
-  }
-  void upload(const std::vector<T>& v, cudaStream_t s) {
-    alloc(std::max<std::size_t>(v.size(), 1));
-    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
-  }
-};
 
 struct PairDev {
   // sides
@@ -70,7 +50,10 @@ struct PairDev {
   double* F3;           // 2 PJ
   double* F4;           // 2 PJ
   double* M;            // nf x nf
-  const double* K;      // nf x nj (column-major)
+  // kernel basis K (nf x nj), compact: column b = e_{unit} + sum_a kvals[vals+a] e_{krows[rows+a]}
+  const int4* kc;       // per column: (unit row, r, rows offset, vals offset)
+  const int* krows;
+  const double* kvals;
   double* H;            // nf x nj scratch
   const double* N;      // nm x (nc + nf) row-major, orthonormal
   const double* rho;    // nf
@@ -80,6 +63,32 @@ struct PairDev {
   double* vecs;         // 2PJ x k (solve vectors, column m at m*2PJ)
   double* func;         // nf x k
 };
+
+// sum_u f(u) K[u][b] for the compact kernel basis
+template <class F>
+__device__ __forceinline__ double kdot(const PairDev& d, int b, F f) {
+  const int4 c = d.kc[b];
+  double s = f(c.x);
+  for (int a = 0; a < c.y; ++a) s += d.kvals[c.w + a] * f(d.krows[c.z + a]);
+  return s;
+}
+
+}  // namespace
+
+// Grow-only arenas of the pair reductions, reused across enrich() calls.
+struct PairBuffers {
+  DBuf<double> G, Q, F, Dv, M, KV, H, N, R, A, E, W, Fu;
+  DBuf<int> Pv, info, KR;
+  DBuf<int4> KC;
+  DBuf<PairDev> dpd;
+  DBuf<FrontDesc> dG, dQ, d3, d4;
+  DBuf<SolveDesc> dsv;
+};
+
+PairEngine::PairEngine() : bufs_(new PairBuffers) {}
+PairEngine::~PairEngine() = default;
+
+namespace {
 
 // (a) side fronts: G_s[a][b] = S_s[pos a, pos b] with identity pads
 __global__ void k_gather_G(const PairDev* pd) {
@@ -131,12 +140,8 @@ __global__ void k_build_H(const PairDev* pd) {
   const int nf = d.nf, nj = d.nj, nc = d.nc;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nf * nj; e += gridDim.x * blockDim.x) {
     const int t = e % nf, b = e / nf;
-    double s = 0.0;
-    for (int u = 0; u < nf; ++u) {
-      const double kv = d.K[(size_t)b * nf + u];
-      if (kv != 0.0) s += (hat(d, 0, nc + t, nc + u) + hat(d, 1, nc + t, nc + u)) * kv;
-    }
-    d.H[(size_t)b * nf + t] = s;
+    d.H[(size_t)b * nf + t] =
+        kdot(d, b, [&](int u) { return hat(d, 0, nc + t, nc + u) + hat(d, 1, nc + t, nc + u); });
   }
 }
 
@@ -171,13 +176,11 @@ __global__ void k_assemble_Q(const PairDev* pd) {
       for (int k = 0; k < d.nm; ++k) v += sig * d.N[(size_t)k * m1 + r] * d.N[(size_t)k * m1 + c];
     } else if (r >= PQ && r < PQ + nj && c < m1) {
       const int al = r - PQ;
-      for (int t = 0; t < nf; ++t) {
-        const double kv = d.K[(size_t)al * nf + t];
-        if (kv != 0.0) v += kv * (hat(d, 0, nc + t, c) - hat(d, 1, nc + t, c));
-      }
+      v = kdot(d, al, [&](int t) { return hat(d, 0, nc + t, c) - hat(d, 1, nc + t, c); });
     } else if (r >= PQ && r < PQ + nj && c >= PQ && c < PQ + nj) {
       const int al = r - PQ, be = c - PQ;
-      for (int t = 0; t < nf; ++t) v += d.K[(size_t)al * nf + t] * d.H[(size_t)be * nf + t];
+      const double* hcol = d.H + (size_t)be * nf;
+      v = kdot(d, al, [&](int t) { return hcol[t]; });
     } else if (r == c) {
       v = 1.0;  // pads
     }
@@ -203,7 +206,8 @@ __global__ void k_build_F3(const PairDev* pd) {
     } else if (r >= PJ && c < PJ) {
       const int al = r - PJ;
       if (al < nj && c < nj) {  // (K^T M K)[al][c] = sum_t K[t][al] (M K)[t][c]; H holds M K here
-        for (int t = 0; t < nf; ++t) v += d.K[(size_t)al * nf + t] * d.H[(size_t)c * nf + t];
+        const double* hcol = d.H + (size_t)c * nf;
+        v = kdot(d, al, [&](int t) { return hcol[t]; });
       }
     }
     d.F3[(size_t)c * N2 + r] = v;
@@ -216,12 +220,7 @@ __global__ void k_build_MK(const PairDev* pd) {
   const int nf = d.nf, nj = d.nj;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nf * nj; e += gridDim.x * blockDim.x) {
     const int t = e % nf, b = e / nf;
-    double s = 0.0;
-    for (int u = 0; u < nf; ++u) {
-      const double kv = d.K[(size_t)b * nf + u];
-      if (kv != 0.0) s += d.M[(size_t)u * nf + t] * kv;
-    }
-    d.H[(size_t)b * nf + t] = s;
+    d.H[(size_t)b * nf + t] = kdot(d, b, [&](int u) { return d.M[(size_t)u * nf + t]; });
   }
 }
 
@@ -292,7 +291,11 @@ __global__ void __launch_bounds__(256) k_jacobi(const PairDev* pd, int smem_cap)
     __syncthreads();
   }
   const double fro = sqrt(red[0]);
-  const double tiny = 1e-15 * fro / (n2 > 0 ? n2 : 1);
+  // Rotations below `tiny` are skipped; a sweep whose rotations are all below
+  // `settle` counts as converged (off-diagonal mass at roundoff level, so the
+  // eigenvalue error is O(eps * ||C||_F)).
+  const double tiny = 1e-17 * fro / (n2 > 0 ? n2 : 1);
+  const double settle = 1e-14 * fro / (n2 > 0 ? n2 : 1);
   const int half = n2 / 2;
   for (int sweep = 0; sweep < 40 && n2 > 1; ++sweep) {
     if (tid == 0) rotated = 0;
@@ -309,7 +312,7 @@ __global__ void __launch_bounds__(256) k_jacobi(const PairDev* pd, int smem_cap)
           const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
           c = 1.0 / sqrt(t * t + 1.0);
           s = t * c;
-          rotated = 1;
+          if (fabs(apq) > settle) rotated = 1;
         }
         cs[k] = c;
         cs[half + k] = s;
@@ -372,6 +375,254 @@ __global__ void __launch_bounds__(256) k_jacobi(const PairDev* pd, int smem_cap)
   }
 }
 
+// (j') Top-k symmetric eigensolver (the default; k_jacobi is kept for
+// cross-checks, BDDC_B200_EIG=jacobi).  One CTA per pair:
+//   1. Householder tridiagonalization of C, packed lower storage in shared
+//      memory (global memory beyond 236 rows), reflectors kept in place;
+//   2. the k largest eigenvalues of the tridiagonal by 16-way multisection on
+//      Sturm counts (16 threads per eigenvalue);
+//   3. eigenvectors of the tridiagonal by inverse iteration (one thread per
+//      vector, partial-pivoting LU of T - lambda I, distinct start vectors),
+//      modified Gram-Schmidt inside clusters;
+//   4. back-transformation y = H_0 ... H_{n-3} z (one warp per vector).
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+  return s;
+}
+
+__device__ __forceinline__ size_t pk(int r, int c) { return (size_t)r * (r + 1) / 2 + c; }  // c <= r
+
+__device__ int sturm_count(const double* d, const double* e, int n, double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (q < 0) ++cnt;
+  for (int j = 1; j < n; ++j) {
+    if (fabs(q) < pivmin) q = -pivmin;
+    q = d[j] - x - e[j - 1] * e[j - 1] / q;
+    if (q < 0) ++cnt;
+  }
+  return cnt;
+}
+
+__global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) {
+  const PairDev dd = pd[blockIdx.x];
+  const int n = dd.nj, k = dd.k, N2 = 2 * dd.PJ, PJ = dd.PJ;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ double sm[];
+  const size_t np = (size_t)n * (n + 1) / 2;
+  const bool in_smem = (long)np + 6L * n <= smem_cap;
+  double* L = in_smem ? sm : dd.A;  // packed lower
+  double* vec = in_smem ? sm + np : sm;  // v, p, d, e, tau, lam (6n)
+  double* v = vec;
+  double* p = vec + n;
+  double* dg = vec + 2 * n;
+  double* eg = vec + 3 * n;
+  double* tau = vec + 4 * n;
+  double* lam = vec + 5 * n;
+  __shared__ double red[32];
+  if (n == 0 || k == 0) return;
+  for (int r = 0; r < n; ++r)
+    for (int c = tid; c <= r; c += blockDim.x) L[pk(r, c)] = dd.F4[(size_t)c * N2 + PJ + r];
+  __syncthreads();
+  // 1. tridiagonalization (dsytd2, lower)
+  for (int kk = 0; kk + 2 < n; ++kk) {
+    const int m0 = kk + 1;
+    double part = 0.0;
+    for (int i = m0 + tid; i < n; i += blockDim.x) {
+      const double x = L[pk(i, kk)];
+      part += x * x;
+    }
+    const double ss = block_sum(part, red);
+    const double x0 = L[pk(m0, kk)];
+    const double alpha = (x0 >= 0 ? -1.0 : 1.0) * sqrt(ss);
+    const double v0 = x0 - alpha;
+    const double vtv = ss - x0 * x0 + v0 * v0;
+    const double t = (ss > 0.0 && vtv > 0.0) ? 2.0 / vtv : 0.0;
+    for (int i = m0 + tid; i < n; i += blockDim.x) v[i] = (i == m0) ? v0 : L[pk(i, kk)];
+    if (tid == 0) {
+      dg[kk] = L[pk(kk, kk)];
+      eg[kk] = t != 0.0 ? alpha : x0;
+      tau[kk] = t;
+    }
+    __syncthreads();
+    if (t == 0.0) continue;
+    // p = t * A22 v
+    for (int r = m0 + tid; r < n; r += blockDim.x) {
+      double s0 = 0.0, s1 = 0.0;
+      const double* row = L + pk(r, 0);
+      int c = m0;
+      for (; c + 1 <= r; c += 2) {
+        s0 += row[c] * v[c];
+        s1 += row[c + 1] * v[c + 1];
+      }
+      for (; c <= r; ++c) s0 += row[c] * v[c];
+      for (int c2 = r + 1; c2 < n; ++c2) s1 += L[pk(c2, r)] * v[c2];
+      p[r] = t * (s0 + s1);
+    }
+    __syncthreads();
+    double pv = 0.0;
+    for (int i = m0 + tid; i < n; i += blockDim.x) pv += p[i] * v[i];
+    const double K = 0.5 * t * block_sum(pv, red);
+    for (int i = m0 + tid; i < n; i += blockDim.x) p[i] -= K * v[i];  // p becomes w
+    __syncthreads();
+    for (int r = m0 + tid; r < n; r += blockDim.x) {
+      double* row = L + pk(r, 0);
+      const double vr = v[r], wr = p[r];
+      for (int c = m0; c <= r; ++c) row[c] -= vr * p[c] + wr * v[c];
+    }
+    // keep the reflector in the eliminated column (for the back-transformation)
+    for (int i = m0 + tid; i < n; i += blockDim.x) L[pk(i, kk)] = v[i];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (n >= 2) {
+      dg[n - 2] = L[pk(n - 2, n - 2)];
+      eg[n - 2] = L[pk(n - 1, n - 2)];
+      tau[n - 2] = 0.0;
+    }
+    dg[n - 1] = L[pk(n - 1, n - 1)];
+    tau[n - 1] = 0.0;
+  }
+  __syncthreads();
+  // 2. top-k eigenvalues by multisection (16 threads per eigenvalue)
+  double tnorm = 0.0, emax2 = 0.0, glo = 1e300, ghi = -1e300;
+  for (int i = 0; i < n; ++i) {
+    const double a = i > 0 ? fabs(eg[i - 1]) : 0.0, b = i + 1 < n ? fabs(eg[i]) : 0.0;
+    glo = fmin(glo, dg[i] - a - b);
+    ghi = fmax(ghi, dg[i] + a + b);
+    tnorm = fmax(tnorm, fabs(dg[i]) + a + b);
+    if (i + 1 < n) emax2 = fmax(emax2, eg[i] * eg[i]);
+  }
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax2);
+  glo -= 2.2e-16 * tnorm + 2 * pivmin;
+  ghi += 2.2e-16 * tnorm + 2 * pivmin;
+  const int G = 16;
+  for (int base = 0; base < k; base += (int)blockDim.x / G) {
+    const int m = base + tid / G, j = tid % G;
+    const bool active = m < k;
+    const int target = n - 1 - (active ? m : 0);  // ascending index
+    double lo = glo, hi = ghi;
+    for (int it = 0; it < 30; ++it) {
+      const double x = lo + (hi - lo) * (j + 1) / (G + 1);
+      const int ok = active ? (sturm_count(dg, eg, n, x, pivmin) <= target) : 1;
+      // lo = largest x with count <= target; hi = smallest x with count > target
+      const unsigned mask = __ballot_sync(0xffffffffu, ok);
+      const unsigned sub = (mask >> ((lane / G) * G)) & 0xffffu;
+      const int nok = __popc(sub);  // points j < nok are <= target (count is monotone)
+      const double nlo = nok > 0 ? lo + (hi - lo) * nok / (G + 1) : lo;
+      const double nhi = nok < G ? lo + (hi - lo) * (nok + 1) / (G + 1) : hi;
+      lo = nlo;
+      hi = nhi;
+      const bool conv = hi - lo <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) + pivmin;
+      if (__all_sync(0xffffffffu, conv)) break;  // both 16-lane groups of the warp
+    }
+    if (active && j == 0) lam[m] = 0.5 * (lo + hi);
+  }
+  __syncthreads();
+  // 3. inverse iteration on T (thread m), scratch in global memory
+  if (tid < k) {
+    const int m = tid;
+    double* work = dd.A + (in_smem ? 0 : np) + (size_t)m * 4 * n;
+    double* xd = work;          // diagonal of the LU
+    double* xu = work + n;      // first superdiagonal
+    double* xu2 = work + 2 * n; // second superdiagonal
+    double* b = work + 3 * n;   // rhs / solution
+    double* z = dd.vecs + (size_t)m * N2;
+    const double shift = lam[m] + 4.0 * 2.2e-16 * tnorm * ((m & 1) ? 1.0 : -1.0);
+    unsigned long long seed = 0x9E3779B97F4A7C15ULL * (m + 1);
+    for (int i = 0; i < n; ++i) {
+      seed ^= seed << 13; seed ^= seed >> 7; seed ^= seed << 17;
+      z[i] = 0.5 + (double)(seed >> 11) * (1.0 / 9007199254740992.0);
+    }
+    for (int it = 0; it < 3; ++it) {
+      for (int i = 0; i < n; ++i) {
+        xd[i] = dg[i] - shift;
+        xu[i] = i + 1 < n ? eg[i] : 0.0;
+        xu2[i] = 0.0;
+        b[i] = z[i];
+      }
+      const double tiny = 2.2e-16 * tnorm + pivmin;
+      for (int i = 0; i + 1 < n; ++i) {
+        const double sub = eg[i];
+        if (fabs(xd[i]) >= fabs(sub)) {
+          if (xd[i] == 0.0) xd[i] = tiny;
+          const double f = sub / xd[i];
+          xd[i + 1] -= f * xu[i];
+          b[i + 1] -= f * b[i];
+        } else {
+          const double f = xd[i] / sub;
+          xd[i] = sub;
+          const double tmp = xd[i + 1];
+          xd[i + 1] = xu[i] - f * tmp;
+          if (i + 2 < n) {
+            xu2[i] = xu[i + 1];
+            xu[i + 1] = -f * xu[i + 1];
+          }
+          xu[i] = tmp;
+          const double tb = b[i];
+          b[i] = b[i + 1];
+          b[i + 1] = tb - f * b[i + 1];
+        }
+      }
+      if (xd[n - 1] == 0.0) xd[n - 1] = tiny;
+      b[n - 1] /= xd[n - 1];
+      if (n >= 2) b[n - 2] = (b[n - 2] - xu[n - 2] * b[n - 1]) / xd[n - 2];
+      for (int i = n - 3; i >= 0; --i) b[i] = (b[i] - xu[i] * b[i + 1] - xu2[i] * b[i + 2]) / xd[i];
+      double nn = 0.0;
+      for (int i = 0; i < n; ++i) nn += b[i] * b[i];
+      nn = 1.0 / sqrt(nn);
+      for (int i = 0; i < n; ++i) z[i] = b[i] * nn;
+    }
+  }
+  __syncthreads();
+  // modified Gram-Schmidt inside clusters (eigenvalues closer than 1e-7 ||T||)
+  if (warp == 0) {
+    for (int m = 1; m < k; ++m) {
+      int c0 = m;
+      while (c0 > 0 && fabs(lam[c0 - 1] - lam[c0]) <= 1e-7 * tnorm) --c0;
+      double* zm = dd.vecs + (size_t)m * N2;
+      for (int q = c0; q < m; ++q) {
+        const double* zq = dd.vecs + (size_t)q * N2;
+        double s = 0.0;
+        for (int i = lane; i < n; i += 32) s += zq[i] * zm[i];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        for (int i = lane; i < n; i += 32) zm[i] -= s * zq[i];
+      }
+      if (c0 < m) {
+        double s = 0.0;
+        for (int i = lane; i < n; i += 32) s += zm[i] * zm[i];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        s = 1.0 / sqrt(s);
+        for (int i = lane; i < n; i += 32) zm[i] *= s;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // 4. back-transformation (warp per vector), then zero the solve padding
+  for (int m = warp; m < k; m += blockDim.x / 32) {
+    double* y = dd.vecs + (size_t)m * N2;
+    for (int kk = n - 3; kk >= 0; --kk) {
+      const double t = tau[kk];
+      if (t == 0.0) continue;
+      double s = 0.0;
+      for (int i = kk + 1 + lane; i < n; i += 32) s += L[pk(i, kk)] * y[i];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      s *= t;
+      for (int i = kk + 1 + lane; i < n; i += 32) y[i] -= s * L[pk(i, kk)];
+      __syncwarp();
+    }
+    for (int i = n + lane; i < N2; i += 32) y[i] = 0.0;
+    if (lane == 0) dd.evals[m] = fmax(lam[m], 0.0);
+  }
+}
+
 // (l) functional a_m = 1/2 M K alpha_m (alpha = first nj entries of vecs after the back solve)
 __global__ void k_functional(const PairDev* pd) {
   const PairDev d = pd[blockIdx.y];
@@ -402,7 +653,9 @@ namespace {
 struct HostPair {
   PairIndex idx;
   std::vector<int> pos[2];   // [outer | corner | shared] boundary positions per side
-  std::vector<double> K;     // nf x nj column-major
+  std::vector<int4> kc;      // compact kernel columns (unit row, r, rows off, vals off), pair-local offsets
+  std::vector<int> krows;
+  std::vector<double> kvals;
   std::vector<double> N;     // nm x m1 row-major
   std::vector<int> glob_off, glob_n;  // shared glob slot offsets
   int nj = 0, nm = 0, r_total = 0;    // r_total = admissible columns - nullity
@@ -416,6 +669,8 @@ int count_above(const std::vector<double>& v, double tau) {
 }  // namespace
 
 EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
+  using clk = std::chrono::steady_clock;
+  const auto h0 = clk::now();
   const Model& m = *m_;
   const ConstraintSet base = cs;  // adaptive.cpp:133: every pair sees the same base
   const auto bg = base.by_glob(m.globs.size());
@@ -429,6 +684,8 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
     bpos[s].assign(m.subs[s].dim(), -1);
     for (std::size_t b = 0; b < m.subs[s].boundary.size(); ++b) bpos[s][m.subs[s].boundary[b]] = static_cast<int>(b);
   }
+  std::vector<KernelCompact> kern(m.globs.size());
+  std::vector<char> kern_done(m.globs.size(), 0);
   for (int p = 0; p < np; ++p) {
     HostPair& h = hp[p];
     h.idx = build_pair_index(m, pairs[p].first, pairs[p].second);
@@ -443,35 +700,33 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
       for (i64 g : x.noncorner_globals) pos.push_back(bpos[s][m.maps.local_of(g, s)]);
     }
     // kernel blocks of the installed averages (pair.cpp:167-188)
-    std::vector<std::vector<double>> blocks;
-    std::vector<int> bcols;
     int nj = 0;
     for (std::size_t gi = 0; gi < x.shared_globs.size(); ++gi) {
       const int g = x.shared_globs[gi];
-      const int n = x.glob_size[gi];
-      int cols = 0;
-      std::vector<double> k;
-      if (bg[g].empty()) {
-        k = glob_kernel(nullptr, 0, n, &cols);
-      } else {
-        std::vector<double> rows(bg[g].size() * std::size_t(n));
-        for (std::size_t a = 0; a < bg[g].size(); ++a)
-          for (int t = 0; t < n; ++t) rows[a * n + t] = base.averages[bg[g][a]].weights[t];
-        k = glob_kernel(&rows, static_cast<int>(bg[g].size()), n, &cols);
+      const int n = x.glob_size[gi], off = x.glob_offset[gi];
+      if (!kern_done[g]) {  // one QR per glob, shared by the pairs it touches
+        if (bg[g].empty()) {
+          kern[g] = glob_kernel_compact(nullptr, 0, n);
+        } else {
+          std::vector<double> rows(bg[g].size() * std::size_t(n));
+          for (std::size_t a = 0; a < bg[g].size(); ++a)
+            for (int t = 0; t < n; ++t) rows[a * n + t] = base.averages[bg[g][a]].weights[t];
+          kern[g] = glob_kernel_compact(&rows, static_cast<int>(bg[g].size()), n);
+        }
+        kern_done[g] = 1;
       }
-      blocks.push_back(std::move(k));
-      bcols.push_back(cols);
+      const KernelCompact& kc = kern[g];
+      const int r = kc.r, cols = n - r;
+      const int rows_off = static_cast<int>(h.krows.size());
+      for (int a = 0; a < r; ++a) h.krows.push_back(off + kc.perm[a]);
+      for (int c = 0; c < cols; ++c) {
+        const int vals_off = static_cast<int>(h.kvals.size());
+        for (int a = 0; a < r; ++a) h.kvals.push_back(kc.neg_top[std::size_t(a) * cols + c]);
+        h.kc.push_back(make_int4(off + kc.perm[r + c], r, rows_off, vals_off));
+      }
       nj += cols;
     }
     h.nj = nj;
-    h.K.assign(std::size_t(nf) * nj, 0.0);
-    int coff = 0;
-    for (std::size_t gi = 0; gi < blocks.size(); ++gi) {
-      const int n = x.glob_size[gi], off = x.glob_offset[gi], cols = bcols[gi];
-      for (int t = 0; t < n; ++t)
-        for (int c = 0; c < cols; ++c) h.K[std::size_t(coff + c) * nf + off + t] = blocks[gi][std::size_t(t) * cols + c];
-      coff += cols;
-    }
     const int m1 = static_cast<int>(x.corner_globals.size()) + nf;
     if (x.floating) {
       std::vector<i64> dofs(x.corner_globals);
@@ -482,6 +737,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
     h.r_total = n_adm - h.nm;
     (void)m1;
   }
+  const auto h1 = clk::now();
   // device buffers, processed in chunks bounded by a memory budget
   EnrichOutcome out;
   std::vector<std::vector<double>> all_evals(np), all_funcs(np);
@@ -524,11 +780,12 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
       ++p1;
     }
     const int nb = p1 - p0;
-    std::vector<int> posv;
-    std::vector<double> Kv, Nv, Rv;
+    std::vector<int> posv, krv;
+    std::vector<int4> kcv;
+    std::vector<double> kvv, Nv, Rv;
     pd.resize(nb);
-    std::vector<long long> oG(2 * nb), oQ(nb), oF3(nb), oF4(nb), oM(nb), oK(nb), oH(nb), oN(nb), oR(nb), oA(nb),
-        oE(nb), oW(nb), oFu(nb), oDG(2 * nb), oDQ(nb), oD3(nb), oD4(nb), oP(2 * nb);
+    std::vector<long long> oG(2 * nb), oQ(nb), oF3(nb), oF4(nb), oM(nb), oKC(nb), oKR(nb), oKV(nb), oH(nb), oN(nb),
+        oR(nb), oA(nb), oE(nb), oW(nb), oFu(nb), oDG(2 * nb), oDQ(nb), oD3(nb), oD4(nb), oP(2 * nb);
     for (int b = 0; b < nb; ++b) {
       const Dims& dm = dims[b];
       const HostPair& h = hp[p0 + b];
@@ -555,8 +812,12 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
       nD += (long long)(dm.PJ / kTile) * kTile * kTile;
       oM[b] = nM;
       nM += (long long)dm.nf * dm.nf;
-      oK[b] = Kv.size();
-      Kv.insert(Kv.end(), h.K.begin(), h.K.end());
+      oKC[b] = kcv.size();
+      kcv.insert(kcv.end(), h.kc.begin(), h.kc.end());
+      oKR[b] = krv.size();
+      krv.insert(krv.end(), h.krows.begin(), h.krows.end());
+      oKV[b] = kvv.size();
+      kvv.insert(kvv.end(), h.kvals.begin(), h.kvals.end());
       oH[b] = nH;
       nH += (long long)dm.nf * std::max(dm.nj, 1);
       oN[b] = Nv.size();
@@ -564,7 +825,8 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
       oR[b] = Rv.size();
       Rv.insert(Rv.end(), h.idx.rho_i.begin(), h.idx.rho_i.end());
       oA[b] = nA;
-      nA += 2LL * n2 * n2;
+      // Jacobi: A and V (2 n2^2); tridiagonal path: packed C + 4 n k LU scratch
+      nA += std::max(2LL * n2 * n2, (long long)dm.nj * (dm.nj + 1) / 2 + 4LL * dm.nj * std::max(dm.k, 1)) + 64;
       oE[b] = nE;
       nE += std::max(dm.k, 1);
       oW[b] = nW;
@@ -572,14 +834,19 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
       oFu[b] = nFu;
       nFu += (long long)dm.nf * std::max(dm.k, 1);
     }
-    Buf<double> G, Q, F, Dv, M, K, H, N, R, A, E, W, Fu;
-    Buf<int> Pv, info;
+    PairBuffers& B_ = *bufs_;
+    auto& G = B_.G; auto& Q = B_.Q; auto& F = B_.F; auto& Dv = B_.Dv; auto& M = B_.M;
+    auto& H = B_.H; auto& N = B_.N; auto& R = B_.R; auto& A = B_.A; auto& E = B_.E; auto& W = B_.W;
+    auto& Fu = B_.Fu;
+    auto& Pv = B_.Pv; auto& info = B_.info;
     G.alloc(nG);
     Q.alloc(nQ);
     F.alloc(nF);
     Dv.alloc(std::max<long long>(nD, 1));
     M.alloc(std::max<long long>(nM, 1));
-    K.upload(Kv, st_);
+    B_.KC.upload(kcv, st_);
+    B_.KR.upload(krv, st_);
+    B_.KV.upload(kvv, st_);
     H.alloc(std::max<long long>(nH, 1));
     N.upload(Nv, st_);
     R.upload(Rv, st_);
@@ -621,7 +888,9 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
       d.F3 = F.p + oF3[b];
       d.F4 = F.p + oF4[b];
       d.M = M.p + oM[b];
-      d.K = K.p + oK[b];
+      d.kc = B_.KC.p + oKC[b];
+      d.krows = B_.KR.p + oKR[b];
+      d.kvals = B_.KV.p + oKV[b];
       d.H = H.p + oH[b];
       d.N = N.p + oN[b];
       d.rho = R.p + oR[b];
@@ -642,24 +911,29 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
       maxnf = std::max(maxnf, dm.nf);
       maxn2 = std::max(maxn2, n2);
     }
-    Buf<PairDev> dpd;
-    Buf<FrontDesc> dG, dQ, d3, d4;
+    auto& dpd = B_.dpd;
+    auto& dG = B_.dG; auto& dQ = B_.dQ; auto& d3 = B_.d3; auto& d4 = B_.d4;
     dpd.upload(pd, st_);
     dG.upload(fG, st_);
     dQ.upload(fQ, st_);
     d3.upload(f3, st_);
     d4.upload(f4, st_);
+    StageProfiler prof("enrich", st_);
     // (a)-(b) side fronts, eliminate the outer skeleton
     k_gather_G<<<dim3(maxNG, 2 * nb), 128, 0, st_>>>(dpd.p);
     CK(cudaGetLastError());
+    prof.mark("gatherG");
     partial_cholesky(dG.p, 2 * nb, maxNG, maxPO, maxM1, st_);
+    prof.mark("cholG");
     // (c) M from the original shared block
     k_build_M<<<dim3(16, nb), 256, 0, st_>>>(dpd.p);
     // (d) Q and its elimination onto alpha
     k_build_H<<<dim3(32, nb), 256, 0, st_>>>(dpd.p);
     k_assemble_Q<<<dim3(64, nb), 256, 0, st_>>>(dpd.p);
     CK(cudaGetLastError());
+    prof.mark("buildQ");
     partial_cholesky(dQ.p, nb, maxNQ, maxPQ, maxPJ, st_);
+    prof.mark("cholQ");
     // (f)-(i) C = L^{-1} lhs L^{-T}
     k_build_MK<<<dim3(32, nb), 256, 0, st_>>>(dpd.p);
     k_build_F3<<<dim3(64, nb), 256, 0, st_>>>(dpd.p);
@@ -667,12 +941,28 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
     k_build_F4<<<dim3(64, nb), 256, 0, st_>>>(dpd.p);
     partial_cholesky(d4.p, nb, 2 * maxPJ, maxPJ, maxPJ, st_);
     CK(cudaGetLastError());
+    prof.mark("reduceC");
     // (j) Jacobi
-    const int cap = 200 * 1024 / 8 - 4 * maxn2 - 64;
-    const bool smem_ok = 2 * maxn2 * maxn2 <= cap;
-    const int jsm = (smem_ok ? 2 * maxn2 * maxn2 : 0) * 8 + 3 * maxn2 * 8 + 64;
-    CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    k_jacobi<<<nb, 256, jsm, st_>>>(dpd.p, smem_ok ? 2 * maxn2 * maxn2 : 0);
+    // A and V in shared memory when they fit next to the kernel's static
+    // arrays (~2.5 KB of the 227 KB per CTA), else in global memory (L2).
+    const char* eig_env = std::getenv("BDDC_B200_EIG");
+    if (eig_env && std::strcmp(eig_env, "jacobi") == 0) {
+      const int cap = (224 * 1024) / 8 - maxn2 - 16;
+      const bool smem_ok = 2 * maxn2 * maxn2 <= cap;
+      const int jsm = (smem_ok ? 2 * maxn2 * maxn2 : 0) * 8 + maxn2 * 8 + 64;
+      CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+      k_jacobi<<<nb, 256, jsm, st_>>>(dpd.p, smem_ok ? 2 * maxn2 * maxn2 : 0);
+      prof.mark(smem_ok ? "jacobi_smem" : "jacobi_gmem");
+    } else {
+      const int maxn = maxn2;  // >= every nj
+      const long need = (long)maxn * (maxn + 1) / 2 + 6L * maxn;
+      const long cap = (224 * 1024) / 8 - 32;
+      const bool smem_ok = need <= cap;
+      const int ssm = static_cast<int>((smem_ok ? need : 6L * maxn) * 8);
+      CK(cudaFuncSetAttribute(k_syevx, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+      k_syevx<<<nb, 256, ssm, st_>>>(dpd.p, smem_ok ? static_cast<int>(need) : 0);
+      prof.mark(smem_ok ? "syevx_smem" : "syevx_gmem");
+    }
     CK(cudaGetLastError());
     // (k) alpha = L^{-T} y via F3's factor; (l) functionals
     std::vector<SolveDesc> sv;
@@ -680,11 +970,13 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
       for (int mm = 0; mm < dims[b].k; ++mm)
         sv.push_back(SolveDesc{pd[b].F3, Dv.p + oD3[b], pd[b].vecs + (size_t)mm * 2 * dims[b].PJ, 2 * dims[b].PJ,
                                dims[b].PJ, nullptr, nullptr});
-    Buf<SolveDesc> dsv;
+    auto& dsv = B_.dsv;
     dsv.upload(sv, st_);
     front_backward(dsv.p, static_cast<int>(sv.size()), 2 * maxPJ, st_);
     k_functional<<<dim3(std::max(maxk, 1), nb), 128, 0, st_>>>(dpd.p);
+    count_launch(9);
     CK(cudaGetLastError());
+    prof.mark("vectors");
     std::vector<double> ev(E.n), fu(Fu.n);
     std::vector<int> inf(4 * nb);
     CK(cudaMemcpyAsync(ev.data(), E.p, E.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
@@ -708,6 +1000,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
     }
     p0 = p1;
   }
+  const auto h2 = clk::now();
   // host selection, splitting and rank filter (adaptive.cpp:66-125)
   for (int p = 0; p < np; ++p) {
     const HostPair& h = hp[p];
@@ -763,6 +1056,14 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
     out.kept += rep.kept;
     out.dropped += rep.dropped;
     out.pairs.push_back(std::move(rep));
+  }
+  const char* prof_env = std::getenv("BDDC_B200_PROFILE");
+  if (prof_env && *prof_env && *prof_env != '0') {
+    const auto h3 = clk::now();
+    std::fprintf(stderr, "[profile] enrich host: pairs=%d prep=%.3fms device+copy=%.3fms select=%.3fms\n", np,
+                 std::chrono::duration<double, std::milli>(h1 - h0).count(),
+                 std::chrono::duration<double, std::milli>(h2 - h1).count(),
+                 std::chrono::duration<double, std::milli>(h3 - h2).count());
   }
   return out;
 }

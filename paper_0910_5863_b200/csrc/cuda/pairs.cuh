@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <memory>
 #include <vector>
 
 #include "../host/host.hpp"
@@ -12,8 +13,12 @@ namespace b200 {
 struct EnrichOptions;
 struct EnrichOutcome;
 
+struct PairBuffers;
+
 class PairEngine {
  public:
+  PairEngine();
+  ~PairEngine();
   void attach(const Model& m, const double* S, const std::vector<long long>& s_off,
               const std::vector<int>& PB, const std::vector<int>& nB, cudaStream_t st);
   EnrichOutcome enrich(ConstraintSet& cs, const EnrichOptions& o);
@@ -24,6 +29,7 @@ class PairEngine {
   std::vector<long long> s_off_;
   std::vector<int> PB_, nB_;
   cudaStream_t st_ = nullptr;
+  std::unique_ptr<PairBuffers> bufs_;
 };
 
 }  // namespace b200

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <deque>
 #include <limits>
+#include <iterator>
 #include <numeric>
 #include <unordered_set>
 
@@ -706,6 +707,17 @@ void Model::build(const Problem& p) {
   assemble(*this);
   classify_and_select(*this);
   embeddings(*this);
+  // per-glob free dofs, per-subdomain glob lists and Dirichlet flags (pair index support)
+  glob_dofs.resize(globs.size());
+  sub_globs.assign(subs.size(), {});
+  for (std::size_t gi = 0; gi < globs.size(); ++gi) {
+    glob_dofs[gi] = glob_free_dofs(static_cast<int>(gi));
+    for (int s : globs[gi].subdomains) sub_globs[s].push_back(static_cast<int>(gi));
+  }
+  sub_constrained.assign(subs.size(), 0);
+  for (std::size_t s = 0; s < subs.size(); ++s)
+    for (int node : subs[s].nodes)
+      for (int c = 0; c < nc; ++c) sub_constrained[s] |= dof[i64(node) * nc + c] < 0;
 }
 
 std::vector<i64> Model::glob_free_dofs(int gi) const {
@@ -952,6 +964,32 @@ std::vector<double> glob_kernel(const std::vector<double>* rows, int r_in, int n
   return k;
 }
 
+KernelCompact glob_kernel_compact(const std::vector<double>* rows, int r_in, int n) {
+  KernelCompact kc;
+  kc.n = n;
+  if (!rows) {
+    kc.r = 0;
+    kc.perm.resize(n);
+    std::iota(kc.perm.begin(), kc.perm.end(), 0);
+    return kc;
+  }
+  const PivotedQr qr = pivoted_qr(*rows, r_in, n);
+  const int r = qr.rank;
+  kc.r = r;
+  kc.perm = qr.perm;
+  kc.neg_top.assign(std::size_t(r) * (n - r), 0.0);
+  if (n > r && r > 0) {
+    std::vector<double> u(std::size_t(r) * r), top(std::size_t(r) * (n - r));
+    for (int i = 0; i < r; ++i) {
+      for (int j = 0; j < r; ++j) u[std::size_t(i) * r + j] = qr.r[std::size_t(i) * n + j];
+      for (int j = r; j < n; ++j) top[std::size_t(i) * (n - r) + j - r] = qr.r[std::size_t(i) * n + j];
+    }
+    upper_solve(u, r, top, n - r);
+    for (std::size_t t = 0; t < top.size(); ++t) kc.neg_top[t] = -top[t];
+  }
+  return kc;
+}
+
 ChangeOfVariables change_of_variables(const ConstraintSet& cs, const Model& md) {
   ChangeOfVariables cov;
   const auto bg = cs.by_glob(md.globs.size());
@@ -1000,11 +1038,18 @@ PairIndex build_pair_index(const Model& md, int si, int sj) {
   PairIndex p;
   p.si = si;
   p.sj = sj;
-  for (std::size_t gi = 0; gi < md.globs.size(); ++gi) {
+  // globs touching either side, ascending (the reference scans all globs in
+  // order, pair.cpp:80-108; only these can contribute)
+  const auto& gi_list = md.sub_globs[si];
+  const auto& gj_list = md.sub_globs[sj];
+  std::vector<int> touched;
+  std::merge(gi_list.begin(), gi_list.end(), gj_list.begin(), gj_list.end(), std::back_inserter(touched));
+  touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+  for (int gi : touched) {
     const Glob& g = md.globs[gi];
     const bool hi = std::binary_search(g.subdomains.begin(), g.subdomains.end(), si);
     const bool hj = std::binary_search(g.subdomains.begin(), g.subdomains.end(), sj);
-    const auto dofs = md.glob_free_dofs(static_cast<int>(gi));
+    const auto& dofs = md.glob_dofs[gi];
     if (hi && hj) {
       if (g.kind == kCorner) {
         p.corner_globals.insert(p.corner_globals.end(), dofs.begin(), dofs.end());
@@ -1030,12 +1075,7 @@ PairIndex build_pair_index(const Model& md, int si, int sj) {
     p.rho_i.push_back(di / (di + dj));
   }
   // floating: neither side holds a Dirichlet-eliminated node-component
-  const int nc = md.mesh.ncomp;
-  bool constrained = false;
-  for (int s : {si, sj})
-    for (int node : md.subs[s].nodes)
-      for (int c = 0; c < nc; ++c) constrained |= md.dof[i64(node) * nc + c] < 0;
-  p.floating = !constrained;
+  p.floating = !md.sub_constrained[si] && !md.sub_constrained[sj];
   return p;
 }
 

@@ -178,6 +178,9 @@ struct Model {
   std::vector<Glob> globs;
   int classification_corners = 0;
   Maps maps;
+  std::vector<std::vector<i64>> glob_dofs;   // glob_free_dofs per glob (cached)
+  std::vector<std::vector<int>> sub_globs;   // globs containing each subdomain, ascending
+  std::vector<char> sub_constrained;         // subdomain holds a Dirichlet dof
 
   void build(const Problem& p);  // experiment.cpp:116-128
   std::vector<i64> glob_free_dofs(int gi) const;  // constraints.cpp:25-32
@@ -197,6 +200,14 @@ GlobTransform build_glob_transform(int glob, const std::vector<double>& rows, in
                                    int n);  // transform.cpp:51-90
 /// Kernel basis of a glob's averages, n x (n-rank) row-major (pair.cpp:167-188).
 std::vector<double> glob_kernel(const std::vector<double>* rows, int r_in, int n, int* cols);
+/// The same basis in compact form: column c has a unit entry at row perm[r+c]
+/// and the values neg_top[a*(n-r)+c] at rows perm[a], a < r.
+struct KernelCompact {
+  int n = 0, r = 0;
+  std::vector<int> perm;
+  std::vector<double> neg_top;
+};
+KernelCompact glob_kernel_compact(const std::vector<double>* rows, int r_in, int n);
 
 /// Change of variables restricted to the interface: per subdomain the
 /// constrained glob blocks (local boundary positions + t), and per
