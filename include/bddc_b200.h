@@ -71,6 +71,7 @@ typedef struct bddc_b200_structure {
   int64_t corners, classification_corners, edges, faces;
   int64_t coarse_space_dim; /* W^c dimension */
   int64_t subdomains, w_dim;
+  int64_t elements;
 } bddc_b200_structure;
 
 /* PcgResult (core/include/bddc/pcg.hpp:28-34) */
@@ -114,6 +115,12 @@ int bddc_b200_interface_dofs(const bddc_b200_t* h, int64_t* out);
 int bddc_b200_subdomain_dim(const bddc_b200_t* h, int s, int64_t* dim);
 int bddc_b200_local_to_wc(const bddc_b200_t* h, int s, int64_t* out);
 int bddc_b200_global_dof(const bddc_b200_t* h, int s, int64_t* out);
+/* Per-element coefficient multipliers (element count entries; 1 when unset). */
+int bddc_b200_element_scale(const bddc_b200_t* h, double* out);
+/* Substructure stiffness (assemble.cpp:202-292) as CSR (full symmetric) and
+ * its load: query nnz with ptr == NULL, then fill ptr (dim+1), idx, val (nnz), load (dim). */
+int bddc_b200_subdomain_matrix(const bddc_b200_t* h, int s, int64_t* nnz, int64_t* ptr, int64_t* idx,
+                               double* val, double* load);
 /* Globs (globs.hpp:18-44): count, then per glob kind / node count / sharer count. */
 int bddc_b200_glob_count(const bddc_b200_t* h, int64_t* n);
 int bddc_b200_glob_info(const bddc_b200_t* h, int g, int* kind, int64_t* n_nodes, int64_t* n_subs);
@@ -179,6 +186,8 @@ typedef struct bddc_b200_step_out {
 int bddc_b200_step(bddc_b200_t* h, const char* mode, double tau, int max_vectors, int keep_edge,
                    int base_faces, int e2e, double* u_free, bddc_b200_step_out* out);
 int64_t bddc_b200_launch_count(void);
+/* lanczos_condition_estimate (pcg.cpp:11-26) on given CG coefficients (host). */
+int bddc_b200_lanczos(const double* alphas, const double* betas, int64_t n, double* kappa);
 
 /* Device-timed phase seconds and work of the last calls:
  * [analysis, eigen, preconditioner, pcg, leaf_flops, leaf_front_bytes, schur_bytes, root_size,

@@ -58,7 +58,7 @@ class _Problem(C.Structure):
 class _Structure(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("dofs", "free_dofs", "interface_dofs", "corners",
                                          "classification_corners", "edges", "faces",
-                                         "coarse_space_dim", "subdomains", "w_dim")]
+                                         "coarse_space_dim", "subdomains", "w_dim", "elements")]
 
 
 class _PcgResult(C.Structure):
@@ -98,6 +98,8 @@ EXPORTS = {
     "bddc_b200_subdomain_dim": (C.c_int, [P, C.c_int, I64]),
     "bddc_b200_local_to_wc": (C.c_int, [P, C.c_int, I64]),
     "bddc_b200_global_dof": (C.c_int, [P, C.c_int, I64]),
+    "bddc_b200_element_scale": (C.c_int, [P, D]),
+    "bddc_b200_subdomain_matrix": (C.c_int, [P, C.c_int, I64, I64, I64, D, D]),
     "bddc_b200_glob_count": (C.c_int, [P, I64]),
     "bddc_b200_glob_info": (C.c_int, [P, C.c_int, C.POINTER(C.c_int), I64, I64]),
     "bddc_b200_glob_nodes": (C.c_int, [P, C.c_int, I64, I64]),
@@ -123,6 +125,7 @@ EXPORTS = {
     "bddc_b200_step": (C.c_int, [P, C.c_char_p, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, D,
                                  C.c_void_p]),
     "bddc_b200_launch_count": (C.c_int64, []),
+    "bddc_b200_lanczos": (C.c_int, [D, D, C.c_int64, D]),
 }
 
 _lib = None
@@ -206,6 +209,16 @@ class Row:
     seconds_eigen: float = 0.0
     seconds_preconditioner: float = 0.0
     root_size: int = 0
+
+
+def lanczos_condition_estimate(alphas, betas) -> float:
+    """`pcg.cpp:11-26` through the library's host implementation."""
+    lib = load_library()
+    a = np.ascontiguousarray(alphas, dtype=np.float64)
+    b = np.ascontiguousarray(betas, dtype=np.float64)
+    k = C.c_double()
+    _check(lib.bddc_b200_lanczos(_dptr(a), _dptr(b), len(a), C.byref(k)))
+    return k.value
 
 
 def emit_table(rows: List[Row], fmt="csv", include_times=True) -> str:
@@ -311,6 +324,26 @@ class BDDC:
 
     def global_dof(self, s) -> np.ndarray:
         return self._sub_array(self._lib.bddc_b200_global_dof, s)
+
+    def element_scale(self) -> np.ndarray:
+        out = np.empty(self.structure()["elements"])
+        _check(self._lib.bddc_b200_element_scale(self._h, _dptr(out)))
+        return out
+
+    def subdomain_matrix(self, s):
+        """(scipy.sparse.csr_matrix, load) of substructure s."""
+        import scipy.sparse as sp
+        nnz = C.c_int64()
+        _check(self._lib.bddc_b200_subdomain_matrix(self._h, s, C.byref(nnz), None, None, None, None))
+        dim = C.c_int64()
+        _check(self._lib.bddc_b200_subdomain_dim(self._h, s, C.byref(dim)))
+        ptr = np.empty(dim.value + 1, dtype=np.int64)
+        idx = np.empty(nnz.value, dtype=np.int64)
+        val = np.empty(nnz.value)
+        load = np.empty(dim.value)
+        _check(self._lib.bddc_b200_subdomain_matrix(self._h, s, C.byref(nnz), ptr.ctypes.data_as(I64),
+                                                    idx.ctypes.data_as(I64), _dptr(val), _dptr(load)))
+        return sp.csr_matrix((val, idx, ptr), shape=(dim.value, dim.value)), load
 
     def globs(self):
         n = C.c_int64()

@@ -143,6 +143,7 @@ int bddc_b200_structure_get(const bddc_b200_t* h, bddc_b200_structure* o) {
     o->coarse_space_dim = m.maps.wc_dim;
     o->subdomains = static_cast<i64>(m.subs.size());
     o->w_dim = m.maps.w_dim;
+    o->elements = m.mesh.element_count();
   });
 }
 
@@ -168,6 +169,28 @@ int bddc_b200_global_dof(const bddc_b200_t* h, int s, int64_t* out) {
   return guarded([&] {
     const auto& v = h->model.subs.at(s).global_dof;
     std::memcpy(out, v.data(), v.size() * sizeof(int64_t));
+  });
+}
+
+int bddc_b200_element_scale(const bddc_b200_t* h, double* out) {
+  return guarded([&] {
+    const Mesh& m = h->model.mesh;
+    for (int e = 0; e < m.element_count(); ++e) out[e] = m.element_scale.empty() ? 1.0 : m.element_scale[e];
+  });
+}
+
+int bddc_b200_subdomain_matrix(const bddc_b200_t* h, int s, int64_t* nnz, int64_t* ptr, int64_t* idx, double* val,
+                               double* load) {
+  return guarded([&] {
+    const Subdomain& S = h->model.subs.at(s);
+    *nnz = static_cast<int64_t>(S.A.idx.size());
+    if (!ptr) return;
+    for (int r = 0; r <= S.A.n; ++r) ptr[r] = S.A.ptr[r];
+    for (std::size_t t = 0; t < S.A.idx.size(); ++t) {
+      idx[t] = S.A.idx[t];
+      val[t] = S.A.val[t];
+    }
+    for (int l = 0; l < S.dim(); ++l) load[l] = S.load[l];
   });
 }
 
@@ -397,6 +420,13 @@ int bddc_b200_step(bddc_b200_t* h, const char* mode_c, double tau, int max_vecto
 }
 
 int64_t bddc_b200_launch_count(void) { return launch_count(); }
+
+int bddc_b200_lanczos(const double* alphas, const double* betas, int64_t n, double* kappa) {
+  return guarded([&] {
+    std::vector<double> a(alphas, alphas + n), b(betas, betas + n);
+    *kappa = lanczos_condition_estimate(a, b);
+  });
+}
 
 int bddc_b200_times(const bddc_b200_t* h, double out[9]) {
   return guarded([&] {

@@ -1,0 +1,218 @@
+"""The CPU oracle is pinned to the reference's own known answers (CPU only).
+
+Each check cites the reference test it restates (tests/golden/structural_pins.json
+records the file:line of every number).
+"""
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+from oracle import fem
+from oracle.adaptive import build_pair, face_pairs
+from oracle.bddc import BddcPreconditioner, lanczos_condition_estimate, pcg
+from oracle.constraints import (ConstraintSet, GlobAverage, add_average, arithmetic_constraints,
+                                change_of_variables, constraint_matrix, transformed_constraint_matrix)
+from oracle.experiment import ResultRow, build_pipeline, cube_spec, emit_table, run_experiment, solve_item
+from oracle.globs import CORNER, EDGE, FACE, classify_globs, select_corners
+from oracle.linalg import generalized_eig_sym, pivoted_qr
+from oracle.spaces import AveragingOperator, HarmonicExtension, InterfaceProblem
+
+
+def test_golden_table_byte_for_byte(golden_table):
+    """tests/test_experiment.cpp:184-194 + tests/data/structural_cube.csv."""
+    _, rows = run_experiment(cube_spec((2, 2, 2), 4, fem.ELASTICITY), ["c", "c+e", "c+e+f"])
+    assert emit_table(rows, include_times=False) == golden_table
+
+
+def test_floating_cube_structure(pins):
+    pin = pins["floating_222_h4_elasticity"]
+    p = build_pipeline(cube_spec((2, 2, 2), 4, fem.ELASTICITY, clamp=False))
+    assert p.mesh.total_dofs == pin["dofs"]
+    assert p.classification_corners == pin["classification_corners"]
+    assert (p.globset.count(CORNER), p.globset.count(EDGE), p.globset.count(FACE)) == \
+        (pin["corners"], pin["edges"], pin["faces"])
+    assert (p.maps.w_dim, p.maps.wc_dim, p.maps.interface_count) == (pin["w_dim"], pin["wc_dim"], pin["interface"])
+    for g in p.globset.globs:  # test_substructuring.cpp:70-80
+        if g.kind == EDGE:
+            assert len(g.nodes) == 3 and len(g.subdomains) == 4
+        if g.kind == FACE:
+            assert len(g.nodes) == 16 and len(g.subdomains) == 2
+
+
+def test_clamped_cube_structure(pins):
+    pin = pins["clamped_222_h4_elasticity"]
+    p = build_pipeline(cube_spec((2, 2, 2), 4, fem.ELASTICITY))
+    assert p.dmap.free_count == pin["free"] and p.maps.interface_count == pin["interface"]
+    assert p.maps.wc_dim == pin["wc_dim"]
+    assert arithmetic_constraints(p.globset, p.dmap, True, False).row_count(p.globset) == pin["rows_ce"]
+
+
+def test_other_structures(pins):
+    p = build_pipeline(cube_spec((2, 2, 2), 3, fem.SCALAR, clamp=False))
+    pin = pins["floating_222_h3_scalar"]
+    assert (p.maps.w_dim, p.maps.wc_dim) == (pin["w_dim"], pin["wc_dim"])
+    p = build_pipeline(cube_spec((2, 2, 1), 4, fem.ELASTICITY, clamp=False))
+    pin = pins["planar_221_h4_elasticity"]
+    assert (p.globset.count(CORNER), p.globset.count(EDGE), p.globset.count(FACE), p.maps.wc_dim) == \
+        (pin["corners"], pin["edges"], pin["faces"], pin["wc_dim"])
+    p = build_pipeline(cube_spec((2, 2, 1), 4, fem.SCALAR, clamp=False))
+    pin = pins["planar_221_h4_scalar"]
+    assert (p.globset.count(CORNER), p.globset.count(EDGE), p.globset.count(FACE)) == \
+        (pin["corners"], pin["edges"], pin["faces"])
+
+
+def test_stacked_pair_before_and_after_corner_selection(pins):
+    pin = pins["stacked_112_h2_elasticity"]
+    p = build_pipeline(cube_spec((1, 1, 2), 2, fem.ELASTICITY, clamp=False), promote_corners=False)
+    assert p.globset.count(FACE) == pin["faces_before"] and p.globset.count(CORNER) == 0
+    assert len(p.globset.globs[0].nodes) == pin["face_nodes"]
+    select_corners(p.globset, p.mesh, p.deco)
+    assert p.globset.count(CORNER) == pin["corners_after"]
+    p = build_pipeline(cube_spec((1, 1, 2), 2, fem.ELASTICITY, clamp=False))
+    assert (p.maps.w_dim, p.maps.interface_count, p.maps.corner_dof_count, p.maps.wc_dim) == \
+        (pin["w_dim"], pin["interface"], pin["corner_dofs"], pin["wc_dim"])
+
+
+def test_constraint_rows(pins):
+    pin = pins["edge_rows_222_h4"]
+    p = build_pipeline(cube_spec((2, 2, 2), 4, fem.ELASTICITY, clamp=False))
+    e = arithmetic_constraints(p.globset, p.dmap, True, False)
+    assert len(e.averages) == pin["edge_averages"] and e.row_count(p.globset) == pin["rows_e"]
+    assert arithmetic_constraints(p.globset, p.dmap, True, True).row_count(p.globset) == pin["rows_ef"]
+
+
+def test_pair_space_dimensions(pins):
+    pin = pins["pair_112_h2_scalar"]
+    p = build_pipeline(cube_spec((1, 1, 2), 2, fem.SCALAR, clamp=False))
+    pr = build_pair(p.systems, p.maps, p.globset, p.dmap, 0, 1)
+    assert (pr.n_corner, pr.n_shared, pr.dim) == (pin["n_corner"], pin["n_shared"], pin["dim"])
+    assert np.allclose(pr.rho_i, 0.5)
+    assert np.abs(pr.schur - pr.schur.T).max() <= 1e-10 * np.abs(pr.schur).max()
+    assert len(face_pairs(build_pipeline(cube_spec((2, 2, 2), 2, fem.SCALAR, clamp=False)).globset)) == 12
+
+
+def test_integer_transform_for_unit_averages():
+    """tests/test_constraints.cpp:124-143."""
+    p = build_pipeline(cube_spec((2, 2, 2), 3, fem.SCALAR, clamp=False))
+    cs = arithmetic_constraints(p.globset, p.dmap, True, True)
+    cov = change_of_variables(cs, p.globset, p.dmap, p.maps)
+    assert cov.glob_transforms
+    for gt in cov.glob_transforms:
+        n = gt.t.shape[0]
+        assert gt.rank == 1 and np.all(gt.h[0] == 1.0)
+        assert gt.t[0, 0] == 1.0 and np.all(gt.t[0, 1:] == -1.0)
+        assert np.array_equal(gt.t[1:], np.eye(n)[1:])
+        assert np.allclose(gt.h @ gt.t, np.eye(n), atol=1e-12)
+
+
+def test_transformed_rows_kill_continuous_fields():
+    """tests/test_constraints.cpp:83-100 and :172-199."""
+    p = build_pipeline(cube_spec((2, 2, 2), 2, fem.ELASTICITY))
+    cs = arithmetic_constraints(p.globset, p.dmap, True, True)
+    rng = np.random.default_rng(21)
+    for g, glob in enumerate(p.globset.globs):
+        if glob.kind != CORNER:
+            n = len([1 for node in glob.nodes for c in range(3) if p.dmap.at(node, c) >= 0])
+            add_average(cs, GlobAverage(g, rng.uniform(-1, 1, n), "adaptive"))
+    d = constraint_matrix(cs, p.globset, p.dmap, p.maps)
+    for _ in range(3):
+        u = rng.uniform(-1, 1, p.dmap.free_count)
+        wc = np.zeros(p.maps.wc_dim)
+        for gdof, copies in enumerate(p.maps.dof_copies):
+            for s, l in copies:
+                wc[p.maps.local_to_wc[s][l]] = u[gdof]
+        assert np.abs(d @ wc).max() <= 1e-10
+    dt = transformed_constraint_matrix(change_of_variables(cs, p.globset, p.dmap, p.maps), p.maps)
+    assert set(np.unique(dt.data)) <= {1.0, -1.0}
+
+
+def test_pivoted_qr_known_answers():
+    """tests/test_linalg.cpp:147-194."""
+    qr = pivoted_qr(np.array([[0.0, 3.0, 0.0]]))
+    assert qr.rank == 1 and qr.perm[0] == 1 and abs(qr.r[0, 0] - 3.0) < 1e-15
+    a = np.array([[1.0, 1.0], [2.0, 2.0], [3.0, 3.0]])
+    assert pivoted_qr(a).rank == 1 and pivoted_qr(a).perm[0] == 0  # ties keep the earliest column
+    assert pivoted_qr(np.zeros((3, 2))).rank == 0
+    rng = np.random.default_rng(3)
+    m = rng.standard_normal((5, 4))
+    q = pivoted_qr(m)
+    assert np.allclose(q.q @ q.r, m[:, q.perm], atol=1e-12) and np.all(np.diag(q.r) >= 0)
+
+
+def test_generalized_eig_matches_scipy():
+    """tests/test_linalg.cpp:229-248 (Cholesky-reduced pencil)."""
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((8, 8))
+    rhs = x @ x.T + 8 * np.eye(8)
+    y = rng.standard_normal((8, 8))
+    lhs = y @ y.T
+    rep = generalized_eig_sym(lhs, rhs, 3)
+    ref = sla.eigh(lhs, rhs, eigvals_only=True)[::-1][:3]
+    assert np.allclose(rep.eigenvalues, ref, rtol=1e-9)
+    v = rep.eigenvectors
+    assert np.allclose(v.T @ rhs @ v, np.eye(3), atol=1e-9)
+
+
+def test_acceptance_criterion_3(pins):
+    """acceptance_main.cpp:130-151: planar 2x2x1, H/h=8, corners only."""
+    pin = pins["acceptance_c3"]
+    p = build_pipeline(cube_spec((2, 2, 1), 8, fem.ELASTICITY))
+    assert p.mesh.total_dofs == pin["dofs"]
+    h = HarmonicExtension(p.systems, p.maps)
+    itf = InterfaceProblem(p.systems, p.maps, h)
+    prec = BddcPreconditioner(p.systems, p.maps, AveragingOperator(p.systems, p.maps),
+                              change_of_variables(ConstraintSet(), p.globset, p.dmap, p.maps))
+    r = pcg(itf.apply, prec.apply, itf.rhs(), 1e-8, 500, preconditioned_residual=True)
+    assert pin["kappa_lo"] <= r.condition_estimate <= pin["kappa_hi"]
+    assert pin["it_lo"] <= r.iterations <= pin["it_hi"]
+
+
+def test_lanczos_recovers_exact_condition(pins):
+    pin = pins["lanczos_diag_1_10"]
+    d = np.arange(1.0, 11.0)
+    r = pcg(lambda v: d * v, lambda v: v, np.ones(10), 1e-12, 50)
+    assert r.iterations == pin["iterations"]
+    assert abs(r.condition_estimate - pin["kappa"]) <= 1e-6 * pin["kappa"]
+
+
+def test_lanczos_roundoff_floor():
+    """Why kappa parity uses 1e-4 (tests/test_gpu_parity.py): perturbing the
+    oracle's own preconditioner by 1e-13 relative already moves its final Lanczos
+    estimate by more than 1e-6, and by less than 1e-4."""
+    p = build_pipeline(cube_spec((2, 2, 1), 8, fem.SCALAR))
+    h = HarmonicExtension(p.systems, p.maps)
+    itf = InterfaceProblem(p.systems, p.maps, h)
+    prec = BddcPreconditioner(p.systems, p.maps, AveragingOperator(p.systems, p.maps),
+                              change_of_variables(ConstraintSet(), p.globset, p.dmap, p.maps))
+    o = pcg(itf.apply, prec.apply, itf.rhs())
+    rng = np.random.default_rng(0)
+    shifts = []
+    for seed in range(8):
+        rng = np.random.default_rng(seed)
+        o2 = pcg(itf.apply, lambda v: prec.apply(v) * (1 + 1e-13 * rng.standard_normal(len(v))), itf.rhs())
+        shifts.append(abs(o2.condition_estimate - o.condition_estimate) / o.condition_estimate)
+    # roundoff-level operator differences move the estimate by up to ~1e-5 here
+    assert max(shifts) > 5e-7 and max(shifts) < 1e-3
+
+
+def test_table_format(pins):
+    pin = pins["table_format"]
+    row = ResultRow("c+e", float("nan"), 54, 7.2982134, 15)
+    assert emit_table([row], "csv", False) == pin["csv"]
+    row = ResultRow("10", 9.639, 54, 7.2982134, 15, converged=False)
+    assert emit_table([row], "markdown", False) == pin["markdown"]
+
+
+def test_adaptive_enrichment_deflates_and_is_monotone():
+    """tests/test_adaptive.cpp:232-290: after enrichment no pair eigenvalue above tau."""
+    spec = cube_spec((2, 2, 2), 2, fem.ELASTICITY)
+    p = build_pipeline(spec)
+    r10 = solve_item(p, "adaptive", 10.0, 15, keep_edge=True)
+    r5 = solve_item(p, "adaptive", 5.0, 15, keep_edge=True)
+    assert r5.constraint_rows >= r10.constraint_rows
+    assert r5.omega_tilde <= r10.omega_tilde * (1 + 1e-9)
+    from oracle.adaptive import pair_indicator
+    out = pair_indicator(r10.constraints, p.globset, p.dmap, p.systems, p.maps)
+    unsat = [rep for rep in r10.outcome.pairs if not rep.saturated]
+    assert unsat
+    assert out.omega_tilde <= 10.0 * (1 + 1e-6)
