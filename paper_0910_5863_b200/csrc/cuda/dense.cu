@@ -140,83 +140,146 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_syrk_trailing(const FrontDesc*
 
 // Panel step: every CTA of tile column j factors the diagonal tile in shared
 // memory (redundantly, avoiding a launch), then solves its own tile.
+//   POTRF: 16-wide blocked; warp 0 factors each 16x16 diagonal block with warp
+//          synchronization only, the panel below is solved row-parallel and the
+//          trailing 48x48 (or smaller) block updated by the whole CTA (12 barriers).
+//   L^{-1}: 16x16 diagonal-block inverses (one warp each), off-diagonal blocks by
+//          block diagonals: Linv_ij = -Linv_ii sum_k L_ik Linv_kj.
+//   TRSM:  X = C L^{-T} = C Linv^T as one 64x64x64 DMMA tile product.
 __global__ void __launch_bounds__(GEMM_THREADS) k_panel(const FrontDesc* ds, int j) {
   const FrontDesc d = ds[blockIdx.y];
   const int i = j + blockIdx.x;
   if (j * kTile >= d.p || i * kTile >= d.n) return;
   extern __shared__ __align__(16) double smem[];
-  double* L = smem;               // 64 x LDS, column-major: L[c*LDS + r]
-  double* X = smem + 64 * LDS;    // 64 x LDS
-  const int tid = threadIdx.x;
+  double* L = smem;                 // 64 x LDS, column-major: L[c*LDS + r]
+  double* V = smem + 64 * LDS;      // L^{-1}
+  double* C = smem + 2 * 64 * LDS;  // target tile (off-diagonal CTAs)
+  __shared__ double T[3][16][17];   // block products of the inverse
+  __shared__ int bad_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t ld = d.n;
   const double* diag = d.a + (size_t)(j * kTile) * ld + j * kTile;
-  for (int e = tid; e < 64 * 64; e += GEMM_THREADS) L[(e >> 6) * LDS + (e & 63)] = diag[(size_t)(e >> 6) * ld + (e & 63)];
-  __syncthreads();
-  // POTRF (lower), right-looking within the tile
-  bool bad = false;
-  for (int k = 0; k < 64; ++k) {
-    const double dkk = L[k * LDS + k];
-    __syncthreads();
-    bad |= !(dkk > 0.0);
-    const double sk = dkk > 0.0 ? sqrt(dkk) : 1.0;
-    if (tid < 64) {
-      if (tid > k) L[k * LDS + tid] /= sk;
-      else if (tid == k) L[k * LDS + k] = sk;
-    }
-    __syncthreads();
-    for (int e = tid; e < 64 * 64; e += GEMM_THREADS) {
-      const int r = e & 63, c = e >> 6;
-      if (c > k && r >= c) L[c * LDS + r] -= L[k * LDS + r] * L[k * LDS + c];
-    }
-    __syncthreads();
-    if (bad && tid == 0 && i == j) atomicCAS(d.info, 0, j * kTile + k + 1);
-    if (bad) break;
+  const double* ct = d.a + (size_t)(j * kTile) * ld + i * kTile;
+  for (int e = tid; e < 64 * 64; e += GEMM_THREADS) {
+    const int r = e & 63, c = e >> 6;
+    L[c * LDS + r] = diag[(size_t)c * ld + r];
+    V[c * LDS + r] = 0.0;
+    if (i != j) C[c * LDS + r] = ct[(size_t)c * ld + r];
   }
-  if (bad) return;
+  if (tid == 0) bad_s = 0;
+  __syncthreads();
+  // ---- blocked POTRF ----
+  for (int kb = 0; kb < 4; ++kb) {
+    const int o = kb * 16;
+    if (warp == 0) {
+      for (int k = 0; k < 16; ++k) {
+        const double dkk = L[(o + k) * LDS + o + k];
+        __syncwarp();
+        const bool ok = dkk > 0.0;
+        if (!ok && lane == 0) bad_s = o + k + 1;
+        const double sk = ok ? sqrt(dkk) : 1.0;
+        if (lane == k) L[(o + k) * LDS + o + k] = sk;
+        if (lane > k && lane < 16) L[(o + k) * LDS + o + lane] /= sk;
+        __syncwarp();
+        if (lane > k && lane < 16) {
+          const double lr = L[(o + k) * LDS + o + lane];
+          for (int c = k + 1; c <= lane; ++c) L[(o + c) * LDS + o + lane] -= lr * L[(o + k) * LDS + o + c];
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // panel rows below: x L_kk^T = a  (thread per row)
+    const int r = o + 16 + tid;
+    if (r < 64) {
+      double x[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        double s = L[(o + c) * LDS + r];
+#pragma unroll
+        for (int k = 0; k < c; ++k) s -= x[k] * L[(o + k) * LDS + o + c];
+        x[c] = s / L[(o + c) * LDS + o + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) L[(o + c) * LDS + r] = x[c];
+    }
+    __syncthreads();
+    // trailing update of the tile: rows/cols >= o + 16
+    const int m = 48 - o;
+    for (int e = tid; e < m * m; e += GEMM_THREADS) {
+      const int rr = o + 16 + e % m, cc = o + 16 + e / m;
+      if (rr < cc) continue;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) s += L[(o + k) * LDS + rr] * L[(o + k) * LDS + cc];
+      L[cc * LDS + rr] -= s;
+    }
+    __syncthreads();
+  }
+  if (bad_s) {
+    if (tid == 0 && i == j) atomicCAS(d.info, 0, j * kTile + bad_s);
+    return;
+  }
+  // ---- L^{-1}: diagonal 16x16 blocks (warp w inverts block w) ----
+  {
+    const int o = warp * 16;
+    if (lane < 16) {
+      const int c = lane;
+      double x[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        double s = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < r; ++k) s -= L[(o + k) * LDS + o + r] * x[k];
+        x[r] = (r >= c) ? s / L[(o + r) * LDS + o + r] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < 16; ++r) V[(o + c) * LDS + o + r] = x[r];
+    }
+  }
+  __syncthreads();
+  // ---- off-diagonal blocks by block diagonal dd = bi - bj ----
+  for (int dd = 1; dd < 4; ++dd) {
+    const int nblk = 4 - dd;
+    // T_b = sum_{k=bj}^{bi-1} L_{bi,k} Linv_{k,bj}
+    for (int e = tid; e < nblk * 256; e += GEMM_THREADS) {
+      const int b = e >> 8, r = (e >> 4) & 15, c = e & 15;
+      const int bj = b, bi = b + dd;
+      double s = 0.0;
+      for (int k = bj * 16; k < bi * 16; ++k) s += L[k * LDS + bi * 16 + r] * V[(bj * 16 + c) * LDS + k];
+      T[b][r][c] = s;
+    }
+    __syncthreads();
+    // Linv_{bi,bj} = -Linv_{bi,bi} T_b
+    for (int e = tid; e < nblk * 256; e += GEMM_THREADS) {
+      const int b = e >> 8, r = (e >> 4) & 15, c = e & 15;
+      const int bj = b, bi = b + dd;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) s += V[(bi * 16 + k) * LDS + bi * 16 + r] * T[b][k][c];
+      V[(bj * 16 + c) * LDS + bi * 16 + r] = -s;
+    }
+    __syncthreads();
+  }
   if (i == j) {
     // Dinv = L^{-1}.  The diagonal tile itself is never read again (solves and
     // later updates touch only off-diagonal tiles), and other CTAs of this
     // launch still read the unfactored C_jj, so it is not written back.
-    // Thread r forms row r of L^{-T} by forward substitution: x L^T = e_r.
-    if (tid < 64) {
-      const int r = tid;
-      for (int c = 0; c < 64; ++c) {
-        double s = (c == r) ? 1.0 : 0.0;
-        for (int k = 0; k < c; ++k) s -= X[k * LDS + r] * L[k * LDS + c];
-        X[c * LDS + r] = s / L[c * LDS + c];
-      }
-    }
-    __syncthreads();
-    // X = L^{-T} (row-major view: X[c*LDS+r] = (L^{-T})[r][c]); Dinv = L^{-1} = X^T
     double* dv = d.dinv + (size_t)j * 64 * 64;
-    for (int e = tid; e < 64 * 64; e += GEMM_THREADS) {
-      const int r = e & 63, c = e >> 6;     // Dinv[r][c] = (L^{-T})[c][r] = X[r*LDS + c]
-      dv[(size_t)c * 64 + r] = X[r * LDS + c];
-    }
+    for (int e = tid; e < 64 * 64; e += GEMM_THREADS) dv[(size_t)(e >> 6) * 64 + (e & 63)] = V[(e >> 6) * LDS + (e & 63)];
     return;
   }
-  // off-diagonal: X = C L^{-T}; thread r solves row r: x L^T = c_r
-  const double* ct = d.a + (size_t)(j * kTile) * ld + i * kTile;
-  for (int e = tid; e < 64 * 64; e += GEMM_THREADS) X[(e >> 6) * LDS + (e & 63)] = ct[(size_t)(e >> 6) * ld + (e & 63)];
-  __syncthreads();
-  if (tid < 64) {
-    const int r = tid;
-    for (int c = 0; c < 64; ++c) {
-      double s0 = X[c * LDS + r], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int k = 0;
-      for (; k + 4 <= c; k += 4) {
-        s0 -= X[k * LDS + r] * L[k * LDS + c];
-        s1 -= X[(k + 1) * LDS + r] * L[(k + 1) * LDS + c];
-        s2 -= X[(k + 2) * LDS + r] * L[(k + 2) * LDS + c];
-        s3 -= X[(k + 3) * LDS + r] * L[(k + 3) * LDS + c];
-      }
-      for (; k < c; ++k) s0 -= X[k * LDS + r] * L[k * LDS + c];
-      X[c * LDS + r] = ((s0 + s1) + (s2 + s3)) / L[c * LDS + c];
-    }
-  }
-  __syncthreads();
+  // ---- off-diagonal tile: X = C L^{-T} on the tensor cores ----
+  double acc[2][4][4];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[mi][ni][v] = 0.0;
+  warp_mma(C, V, 64, acc);
   double* out = d.a + (size_t)(j * kTile) * ld + i * kTile;
-  for (int e = tid; e < 64 * 64; e += GEMM_THREADS) out[(size_t)(e >> 6) * ld + (e & 63)] = X[(e >> 6) * LDS + (e & 63)];
+  for_acc(acc, [&](int m, int n, double v) { out[(size_t)n * ld + m] = v; });
 }
 
 // ---------------------------------------------------------------------------
@@ -250,13 +313,15 @@ __global__ void __launch_bounds__(SOLVE_THREADS) k_front_forward(const SolveDesc
     // x[r] -= sum_c L[r, k0+c] z[c] for rows below the block
     for (int r = k0 + kTile + tid; r < d.n; r += SOLVE_THREADS) {
       const double* col = d.a + (size_t)k0 * ld + r;
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll 8
-      for (int c = 0; c < 64; c += 2) {
-        s0 += col[(size_t)c * ld] * z[c];
-        s1 += col[(size_t)(c + 1) * ld] * z[c + 1];
+      double s[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s[q] = 0.0;
+#pragma unroll 2
+      for (int c = 0; c < 64; c += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s[q] += col[(size_t)(c + q) * ld] * z[c + q];
       }
-      xs[r] -= s0 + s1;
+      xs[r] -= ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
     }
     __syncthreads();
   }
@@ -281,14 +346,26 @@ __global__ void __launch_bounds__(SOLVE_THREADS) k_front_backward(const SolveDes
   const size_t ld = d.n;
   for (int kb = d.p / kTile - 1; kb >= 0; --kb) {
     const int k0 = kb * kTile;
-    // t[c] = x[k0+c] - sum_{r >= k0+64} L[r, k0+c] x[r]   (warp per column)
-    for (int c = warp; c < 64; c += SOLVE_THREADS / 32) {
-      const double* col = d.a + (size_t)(k0 + c) * ld;
-      double s = 0.0;
-      for (int r = k0 + kTile + lane; r < d.n; r += 32) s += col[r] * xs[r];
+    // t[c] = x[k0+c] - sum_{r >= k0+64} L[r, k0+c] x[r]: warp w owns columns
+    // w, w+8, ..., w+56 and streams all eight at once (eight independent loads
+    // in flight per lane), then reduces across lanes
+    {
+      double acc[8];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) t[c] = xs[k0 + c] - s;
+      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+      const double* base = d.a + (size_t)(k0 + warp) * ld;
+      for (int r = k0 + kTile + lane; r < d.n; r += 32) {
+        const double xr = xs[r];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += base[(size_t)(8 * q) * ld + r] * xr;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double s = acc[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) t[warp + 8 * q] = xs[k0 + warp + 8 * q] - s;
+      }
     }
     __syncthreads();
     // x[k0:k0+64] = Dinv^T t
@@ -324,7 +401,7 @@ void configure() {
   const int gemm_smem = 4 * KC * LDS * sizeof(double);
   cudaFuncSetAttribute(k_syrk_column, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
   cudaFuncSetAttribute(k_syrk_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
-  cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
+  cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 64 * LDS * (int)sizeof(double));
   cudaFuncSetAttribute(k_front_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   g_smem_configured = 1;
@@ -342,7 +419,7 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
   if (batch == 0) return;
   configure();
   const int gemm_smem = 4 * KC * LDS * sizeof(double);
-  const int panel_smem = 2 * 64 * LDS * sizeof(double);
+  const int panel_smem = 3 * 64 * LDS * sizeof(double);
   const int nt = max_n / kTile, pt = max_p / kTile;
   for (int j = 0; j < pt; ++j) {
     if (j > 0) {
