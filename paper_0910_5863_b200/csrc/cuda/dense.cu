@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_syrk_trailing(const FrontDesc*
 //   TRSM:  X = C L^{-T} = C Linv^T as one 64x64x64 DMMA tile product.
 __global__ void __launch_bounds__(GEMM_THREADS) k_panel(const FrontDesc* ds, int j) {
   const FrontDesc d = ds[blockIdx.y];
-  const int i = j + blockIdx.x;
+  const int i = j;  // one CTA per front: the diagonal tile only (k_trsm solves the rest)
   if (j * kTile >= d.p || i * kTile >= d.n) return;
   extern __shared__ __align__(16) double smem[];
   double* L = smem;                 // 64 x LDS, column-major: L[c*LDS + r]
@@ -261,15 +261,34 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_panel(const FrontDesc* ds, int
     }
     __syncthreads();
   }
-  if (i == j) {
-    // Dinv = L^{-1}.  The diagonal tile itself is never read again (solves and
-    // later updates touch only off-diagonal tiles), and other CTAs of this
-    // launch still read the unfactored C_jj, so it is not written back.
-    double* dv = d.dinv + (size_t)j * 64 * 64;
-    for (int e = tid; e < 64 * 64; e += GEMM_THREADS) dv[(size_t)(e >> 6) * 64 + (e & 63)] = V[(e >> 6) * LDS + (e & 63)];
-    return;
+  // Dinv = L^{-1}.  The diagonal tile itself is never read again (solves and
+  // later updates touch only off-diagonal tiles), so it is not written back.
+  (void)C;
+  (void)ct;
+  double* dv = d.dinv + (size_t)j * 64 * 64;
+  for (int e = tid; e < 64 * 64; e += GEMM_THREADS) dv[(size_t)(e >> 6) * 64 + (e & 63)] = V[(e >> 6) * LDS + (e & 63)];
+}
+
+// Off-diagonal tiles of column j: X = C_ij L_jj^{-T} = C_ij Dinv_j^T as one
+// 64x64x64 DMMA tile product (Dinv_j written by k_panel).
+__global__ void __launch_bounds__(GEMM_THREADS) k_trsm(const FrontDesc* ds, int j) {
+  const FrontDesc d = ds[blockIdx.y];
+  const int i = j + 1 + blockIdx.x;
+  if (j * kTile >= d.p || i * kTile >= d.n) return;
+  extern __shared__ __align__(16) double smem[];
+  double* V = smem;
+  double* C = smem + 64 * LDS;
+  const size_t ld = d.n;
+  const double* dv = d.dinv + (size_t)j * 64 * 64;
+  const double* ct = d.a + (size_t)(j * kTile) * ld + i * kTile;
+  for (int q = threadIdx.x; q < 64 * 32; q += GEMM_THREADS) {
+    const int col = q >> 5, part = q & 31;
+    cp_async16(V + col * LDS + part * 2, dv + (size_t)col * 64 + part * 2);
+    cp_async16(C + col * LDS + part * 2, ct + (size_t)col * ld + part * 2);
   }
-  // ---- off-diagonal tile: X = C L^{-T} on the tensor cores ----
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
   double acc[2][4][4];
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
@@ -402,6 +421,7 @@ void configure() {
   cudaFuncSetAttribute(k_syrk_column, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
   cudaFuncSetAttribute(k_syrk_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
   cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 64 * LDS * (int)sizeof(double));
+  cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
   cudaFuncSetAttribute(k_front_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   g_smem_configured = 1;
@@ -426,8 +446,12 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
       k_syrk_column<<<dim3(nt - j, batch), GEMM_THREADS, gemm_smem, stream>>>(d_descs, j);
       count_launch(1);
     }
-    k_panel<<<dim3(nt - j, batch), GEMM_THREADS, panel_smem, stream>>>(d_descs, j);
+    k_panel<<<dim3(1, batch), GEMM_THREADS, panel_smem, stream>>>(d_descs, j);
     count_launch(1);
+    if (nt - j - 1 > 0) {
+      k_trsm<<<dim3(nt - j - 1, batch), GEMM_THREADS, 2 * 64 * LDS * (int)sizeof(double), stream>>>(d_descs, j);
+      count_launch(1);
+    }
   }
   // trailing tiles: worst case over the batch is bounded by the largest trailing block
   const long mt = max_m / kTile;
