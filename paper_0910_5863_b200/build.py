@@ -17,7 +17,7 @@ LIB = HERE / "libbddc_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
-          "-I", str(HERE.parent / "include")]
+          "-Xcompiler", "-fopenmp", "-I", str(HERE.parent / "include")]
 
 
 def sources():
@@ -59,7 +59,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if failed:
         raise RuntimeError("CUDA build failed")
     tmp = LIB.with_suffix(".so.tmp")
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs),
+                           "-lgomp"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -44,6 +45,33 @@ struct DBuf {
   void zero(cudaStream_t s) {
     if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
   }
+};
+
+/// Host-side stage timer (printed with BDDC_B200_PROFILE=1).
+class HostTimer {
+ public:
+  explicit HostTimer(const char* what) : what_(what), t0_(std::chrono::steady_clock::now()), last_(t0_) {
+    const char* e = std::getenv("BDDC_B200_PROFILE");
+    on_ = e && *e && *e != '0';
+  }
+  void mark(const char* name) {
+    if (!on_) return;
+    const auto now = std::chrono::steady_clock::now();
+    char buf[96];
+    std::snprintf(buf, sizeof(buf), " %s=%.3fms", name,
+                  std::chrono::duration<double, std::milli>(now - last_).count());
+    line_ += buf;
+    last_ = now;
+  }
+  ~HostTimer() {
+    if (on_) std::fprintf(stderr, "[profile] %s host:%s\n", what_, line_.c_str());
+  }
+
+ private:
+  const char* what_;
+  std::chrono::steady_clock::time_point t0_, last_;
+  bool on_ = false;
+  std::string line_;
 };
 
 class StageProfiler {

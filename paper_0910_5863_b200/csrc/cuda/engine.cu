@@ -770,7 +770,9 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   const int ns = D.nsub;
   cudaStream_t st = D.st;
   CK(cudaEventRecord(D.e0, st));
+  HostTimer ht("set_constraints");
   const ChangeOfVariables cov = change_of_variables(cs, m);
+  ht.mark("change_of_variables");
   // boundary position of each local dof
   std::vector<std::vector<int>> bpos_of(ns);
   for (int s = 0; s < ns; ++s) {
@@ -794,8 +796,8 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     perm.insert(perm.end(), gt.perm.begin(), gt.perm.end());
     iperm.insert(iperm.end(), ip.begin(), ip.end());
     for (int i = 0; i < r; ++i)  // D[i][j] = t_perm[i][j] = t[perm[i]][j]
-      for (int j = 0; j < n; ++j) trD.push_back(gt.t[std::size_t(gt.perm[i]) * n + j]);
-    const auto dofs = m.glob_free_dofs(gt.glob);
+      for (int j = 0; j < n; ++j) trD.push_back(gt.D[std::size_t(i) * n + j]);
+    const auto& dofs = m.glob_dofs[gt.glob];
     for (int s : m.globs[gt.glob].subdomains) {
       const int inst = static_cast<int>(inst_tr.size());
       inst_tr.push_back(static_cast<int>(k));
@@ -897,6 +899,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
         ++fill[k];
       }
   }
+  ht.mark("index_build");
   // uploads
   D.bposF.upload(posF, st);
   D.bglob.upload(bglob, st);
@@ -966,6 +969,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   up_i(D.d_PE, D.PE);
   up_i(D.pads, pads);
   up_i(D.pad_sub, pad_sub);
+  ht.mark("uploads");
   StageProfiler prof("set_constraints", st);
   // F = P (T^T S T) P^T, pads identity
   k_colxform<<<dim3(D.max_PB, ns), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);

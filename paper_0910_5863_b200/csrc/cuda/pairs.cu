@@ -684,11 +684,34 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
     bpos[s].assign(m.subs[s].dim(), -1);
     for (std::size_t b = 0; b < m.subs[s].boundary.size(); ++b) bpos[s][m.subs[s].boundary[b]] = static_cast<int>(b);
   }
+  // pass 1: pair index spaces (independent per pair)
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int p = 0; p < np; ++p) hp[p].idx = build_pair_index(m, pairs[p].first, pairs[p].second);
+  // pass 2: one kernel basis (QR) per shared glob
   std::vector<KernelCompact> kern(m.globs.size());
-  std::vector<char> kern_done(m.globs.size(), 0);
+  std::vector<char> kern_need(m.globs.size(), 0);
+  for (int p = 0; p < np; ++p)
+    for (int g : hp[p].idx.shared_globs) kern_need[g] = 1;
+  std::vector<int> kern_list;
+  for (std::size_t g = 0; g < m.globs.size(); ++g)
+    if (kern_need[g]) kern_list.push_back(static_cast<int>(g));
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int q = 0; q < static_cast<int>(kern_list.size()); ++q) {
+    const int g = kern_list[q];
+    const int n = static_cast<int>(m.glob_dofs[g].size());
+    if (bg[g].empty()) {
+      kern[g] = glob_kernel_compact(nullptr, 0, n);
+    } else {
+      std::vector<double> rows(bg[g].size() * std::size_t(n));
+      for (std::size_t a = 0; a < bg[g].size(); ++a)
+        for (int t = 0; t < n; ++t) rows[a * n + t] = base.averages[bg[g][a]].weights[t];
+      kern[g] = glob_kernel_compact(&rows, static_cast<int>(bg[g].size()), n);
+    }
+  }
+  // pass 3: positions, compact kernel columns, rigid modes
+#pragma omp parallel for schedule(dynamic, 8)
   for (int p = 0; p < np; ++p) {
     HostPair& h = hp[p];
-    h.idx = build_pair_index(m, pairs[p].first, pairs[p].second);
     const PairIndex& x = h.idx;
     const int nf = static_cast<int>(x.noncorner_globals.size());
     for (int side = 0; side < 2; ++side) {
@@ -704,17 +727,6 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
     for (std::size_t gi = 0; gi < x.shared_globs.size(); ++gi) {
       const int g = x.shared_globs[gi];
       const int n = x.glob_size[gi], off = x.glob_offset[gi];
-      if (!kern_done[g]) {  // one QR per glob, shared by the pairs it touches
-        if (bg[g].empty()) {
-          kern[g] = glob_kernel_compact(nullptr, 0, n);
-        } else {
-          std::vector<double> rows(bg[g].size() * std::size_t(n));
-          for (std::size_t a = 0; a < bg[g].size(); ++a)
-            for (int t = 0; t < n; ++t) rows[a * n + t] = base.averages[bg[g][a]].weights[t];
-          kern[g] = glob_kernel_compact(&rows, static_cast<int>(bg[g].size()), n);
-        }
-        kern_done[g] = 1;
-      }
       const KernelCompact& kc = kern[g];
       const int r = kc.r, cols = n - r;
       const int rows_off = static_cast<int>(h.krows.size());

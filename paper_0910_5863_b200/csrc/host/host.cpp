@@ -746,13 +746,15 @@ i64 Model::count(int kind) const {
 // ============================================================================
 // Dense QR (dense_eig.cpp:17-75), row-major storage
 // ============================================================================
-PivotedQr pivoted_qr(const std::vector<double>& a, int m, int n, double rel_drop_tol) {
+PivotedQr pivoted_qr(const std::vector<double>& a, int m, int n, double rel_drop_tol, bool want_q) {
   PivotedQr o;
   o.m = m;
   o.n = n;
   o.r = a;
-  o.q.assign(std::size_t(m) * m, 0.0);
-  for (int i = 0; i < m; ++i) o.q[std::size_t(i) * m + i] = 1.0;
+  if (want_q) {
+    o.q.assign(std::size_t(m) * m, 0.0);
+    for (int i = 0; i < m; ++i) o.q[std::size_t(i) * m + i] = 1.0;
+  }
   o.perm.resize(n);
   std::iota(o.perm.begin(), o.perm.end(), 0);
   auto R = [&](int i, int j) -> double& { return o.r[std::size_t(i) * n + j]; };
@@ -794,7 +796,7 @@ PivotedQr pivoted_qr(const std::vector<double>& a, int m, int n, double rel_drop
         for (int i = k; i < m; ++i) s += v[i] * R(i, j);
         for (int i = k; i < m; ++i) R(i, j) -= f * v[i] * s;
       }
-      for (int i = 0; i < m; ++i) {  // qblock -= (qblock v)(f v)^T
+      for (int i = 0; want_q && i < m; ++i) {  // qblock -= (qblock v)(f v)^T
         double s = 0;
         for (int j = k; j < m; ++j) s += Q(i, j) * v[j];
         for (int j = k; j < m; ++j) Q(i, j) -= s * f * v[j];
@@ -804,7 +806,7 @@ PivotedQr pivoted_qr(const std::vector<double>& a, int m, int n, double rel_drop
     for (int i = k + 1; i < m; ++i) R(i, k) = 0.0;
     if (R(k, k) < 0) {
       for (int j = k; j < n; ++j) R(k, j) = -R(k, j);
-      for (int i = 0; i < m; ++i) Q(i, k) = -Q(i, k);
+      for (int i = 0; want_q && i < m; ++i) Q(i, k) = -Q(i, k);
     }
   }
   const double d0 = (m && n) ? std::abs(R(0, 0)) : 0.0;
@@ -877,7 +879,7 @@ bool add_average(ConstraintSet& cs, Average avg) {
       for (int c = 0; c + 1 < n; ++c) stack[std::size_t(i) * n + c] = (*existing[c])[i];
       stack[std::size_t(i) * n + n - 1] = avg.weights[i];
     }
-    if (pivoted_qr(stack, m, n).rank <= n - 1) return false;
+    if (pivoted_qr(stack, m, n, 1e-8, false).rank <= n - 1) return false;
   }
   cs.averages.push_back(std::move(avg));
   return true;
@@ -896,7 +898,7 @@ void upper_solve(const std::vector<double>& U, int r, std::vector<double>& B, in
 }  // namespace
 
 GlobTransform build_glob_transform(int glob, const std::vector<double>& rows, int r_in, int n) {
-  const PivotedQr qr = pivoted_qr(rows, r_in, n);
+  const PivotedQr qr = pivoted_qr(rows, r_in, n, 1e-8, false);
   if (qr.rank < r_in) throw Error(kSingularGram, "dependent averages slipped past the rank filter");
   const int r = qr.rank;
   std::vector<double> u(std::size_t(r) * r), v(std::size_t(r) * (n - r));
@@ -907,35 +909,23 @@ GlobTransform build_glob_transform(int glob, const std::vector<double>& rows, in
   std::vector<double> uinv(std::size_t(r) * r, 0.0);
   for (int i = 0; i < r; ++i) uinv[std::size_t(i) * r + i] = 1.0;
   upper_solve(u, r, uinv, r);
-  std::vector<double> hp(std::size_t(n) * n, 0.0), tp(std::size_t(n) * n, 0.0);
-  for (int i = 0; i < r; ++i) {
-    for (int j = 0; j < r; ++j) {
-      hp[std::size_t(i) * n + j] = u[std::size_t(i) * r + j];
-      tp[std::size_t(i) * n + j] = uinv[std::size_t(i) * r + j];
-    }
-    for (int j = r; j < n; ++j) {
-      hp[std::size_t(i) * n + j] = v[std::size_t(i) * (n - r) + j - r];
-      double s = 0;
-      for (int k = 0; k < r; ++k) s += uinv[std::size_t(i) * r + k] * v[std::size_t(k) * (n - r) + j - r];
-      tp[std::size_t(i) * n + j] = -s;
-    }
-  }
-  for (int i = r; i < n; ++i) {
-    hp[std::size_t(i) * n + i] = 1.0;
-    tp[std::size_t(i) * n + i] = 1.0;
-  }
+  // Compact form: t.row(perm[i]) = t_perm.row(i) with t_perm rows i >= r equal
+  // to unit rows, so t is the permutation plus the r dense rows
+  // D = [U^{-1} | -U^{-1} V] (transform.cpp:51-90).
   GlobTransform gt;
   gt.glob = glob;
   gt.rank = r;
   gt.n = n;
   gt.perm = qr.perm;
-  gt.h.assign(std::size_t(n) * n, 0.0);
-  gt.t.assign(std::size_t(n) * n, 0.0);
-  for (int i = 0; i < n; ++i)
-    for (int a = 0; a < n; ++a) {
-      gt.h[std::size_t(a) * n + qr.perm[i]] = hp[std::size_t(a) * n + i];   // h.col(perm[i]) = hp.col(i)
-      gt.t[std::size_t(qr.perm[i]) * n + a] = tp[std::size_t(i) * n + a];   // t.row(perm[i]) = tp.row(i)
+  gt.D.assign(std::size_t(r) * n, 0.0);
+  for (int i = 0; i < r; ++i) {
+    for (int j = 0; j < r; ++j) gt.D[std::size_t(i) * n + j] = uinv[std::size_t(i) * r + j];
+    for (int j = r; j < n; ++j) {
+      double acc = 0;
+      for (int k = 0; k < r; ++k) acc += uinv[std::size_t(i) * r + k] * v[std::size_t(k) * (n - r) + j - r];
+      gt.D[std::size_t(i) * n + j] = -acc;
     }
+  }
   return gt;
 }
 
@@ -964,6 +954,14 @@ std::vector<double> glob_kernel(const std::vector<double>* rows, int r_in, int n
   return k;
 }
 
+std::vector<double> GlobTransform::dense_t() const {
+  std::vector<double> t(std::size_t(n) * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      t[std::size_t(perm[i]) * n + j] = i < rank ? D[std::size_t(i) * n + j] : (i == j ? 1.0 : 0.0);
+  return t;
+}
+
 KernelCompact glob_kernel_compact(const std::vector<double>* rows, int r_in, int n) {
   KernelCompact kc;
   kc.n = n;
@@ -973,7 +971,7 @@ KernelCompact glob_kernel_compact(const std::vector<double>* rows, int r_in, int
     std::iota(kc.perm.begin(), kc.perm.end(), 0);
     return kc;
   }
-  const PivotedQr qr = pivoted_qr(*rows, r_in, n);
+  const PivotedQr qr = pivoted_qr(*rows, r_in, n, 1e-8, false);
   const int r = qr.rank;
   kc.r = r;
   kc.perm = qr.perm;
@@ -993,17 +991,26 @@ KernelCompact glob_kernel_compact(const std::vector<double>* rows, int r_in, int
 ChangeOfVariables change_of_variables(const ConstraintSet& cs, const Model& md) {
   ChangeOfVariables cov;
   const auto bg = cs.by_glob(md.globs.size());
-  for (std::size_t gi = 0; gi < md.globs.size(); ++gi) {
-    if (bg[gi].empty()) continue;
-    const Glob& g = md.globs[gi];
-    const auto dofs = md.glob_free_dofs(static_cast<int>(gi));
-    const int n = static_cast<int>(dofs.size());
+  std::vector<int> constrained;
+  for (std::size_t gi = 0; gi < md.globs.size(); ++gi)
+    if (!bg[gi].empty()) constrained.push_back(static_cast<int>(gi));
+  // the per-glob QRs are independent; groups keep glob order
+  cov.transforms.resize(constrained.size());
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int q = 0; q < static_cast<int>(constrained.size()); ++q) {
+    const int gi = constrained[q];
+    const int n = static_cast<int>(md.glob_dofs[gi].size());
     const int r_in = static_cast<int>(bg[gi].size());
     std::vector<double> rows(std::size_t(r_in) * n);
     for (int a = 0; a < r_in; ++a)
       for (int t = 0; t < n; ++t) rows[std::size_t(a) * n + t] = cs.averages[bg[gi][a]].weights[t];
-    cov.transforms.push_back(build_glob_transform(static_cast<int>(gi), rows, r_in, n));
-    const GlobTransform& gt = cov.transforms.back();
+    cov.transforms[q] = build_glob_transform(gi, rows, r_in, n);
+  }
+  for (std::size_t q = 0; q < constrained.size(); ++q) {
+    const int gi = constrained[q];
+    const Glob& g = md.globs[gi];
+    const auto& dofs = md.glob_dofs[gi];
+    const GlobTransform& gt = cov.transforms[q];
     for (int k = 0; k < gt.rank; ++k) {  // explicit_slots[k] == k
       const i64 gdof = dofs[k];
       std::vector<i64> grp;

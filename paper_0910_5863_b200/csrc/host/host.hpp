@@ -151,13 +151,14 @@ struct Average {  // constraints.hpp:23-27
   int adaptive = 0;
 };
 
-struct GlobTransform {  // transform.hpp:20-27
+struct GlobTransform {  // transform.hpp:20-27, compact form
   int glob = 0;
   int rank = 0;
   int n = 0;
-  std::vector<double> t;   // n x n row-major: t[a*n+b]
-  std::vector<double> h;   // n x n row-major
   std::vector<int> perm;   // QR column pivots: t.row(perm[i]) = t_perm.row(i)
+  std::vector<double> D;   // rank x n row-major: the dense rows t_perm[0:rank, :]
+  /// Full basis change t (n x n row-major), for checks: unit rows t[perm[i]][i], i >= rank.
+  std::vector<double> dense_t() const;
 };
 
 struct PivotedQr {  // dense_eig.hpp:20-29 (row-major m x n r, m x m q)
@@ -166,7 +167,7 @@ struct PivotedQr {  // dense_eig.hpp:20-29 (row-major m x n r, m x m q)
   std::vector<int> perm;
 };
 PivotedQr pivoted_qr(const std::vector<double>& a_rowmajor, int m, int n,
-                     double rel_drop_tol = 1e-8);
+                     double rel_drop_tol = 1e-8, bool want_q = true);
 
 /// Everything the host knows about one problem instance.
 struct Model {
