@@ -81,7 +81,17 @@ __device__ __forceinline__ void for_acc(double (&acc)[2][4][4], F f) {
 }
 
 // C[i0:i0+64, j0:j0+64] -= A[i0:i0+64, 0:K] * A[j0:j0+64, 0:K]^T  (A column-major, ld)
+// out == nullptr: C[i0:,j0:] -= A[i0:, kb:ke] A[j0:, kb:ke]^T in place;
+// otherwise the product over [kb, ke) is stored to out (64x64, ld 64).
+__device__ void tile_update_range(double* a, int ld, int i0, int j0, int kb, int ke, double* out);
+
 __device__ void tile_update(double* a, int ld, int i0, int j0, int K) {
+  tile_update_range(a, ld, i0, j0, 0, K, nullptr);
+}
+
+__device__ void tile_update_range(double* a, int ld, int i0, int j0, int kb, int ke, double* out) {
+  const int K = ke - kb;
+  a += (size_t)kb * ld;  // column offset of the K range
   extern __shared__ __align__(16) double smem[];
   double* As = smem;                       // [2][KC*LDS]
   double* Bs = smem + 2 * KC * LDS;        // [2][KC*LDS]
@@ -116,7 +126,45 @@ __device__ void tile_update(double* a, int ld, int i0, int j0, int K) {
     warp_mma(As + (c & 1) * KC * LDS, Bs + (c & 1) * KC * LDS, KC, acc);
     __syncthreads();
   }
-  for_acc(acc, [&](int m, int n, double v) { a[(size_t)(j0 + n) * ld + i0 + m] -= v; });
+  if (out) {
+    for_acc(acc, [&](int m, int n, double v) { out[n * 64 + m] = v; });
+  } else {
+    a -= (size_t)kb * ld;
+    for_acc(acc, [&](int m, int n, double v) { a[(size_t)(j0 + n) * ld + i0 + m] -= v; });
+  }
+}
+
+// Split-K column update for fronts with little tile parallelism (single large
+// root): CTA (t, b, s) forms the partial product of tile (j + t, j) over the
+// K slice s into a workspace; k_splitk_reduce subtracts the slices in a fixed
+// order (deterministic).
+__global__ void __launch_bounds__(GEMM_THREADS) k_syrk_column_splitk(const FrontDesc* ds, int j, int nsplit,
+                                                                    int tiles, double* work) {
+  const FrontDesc d = ds[blockIdx.y];
+  const int i = j + blockIdx.x;
+  if (j * kTile >= d.p || i * kTile >= d.n) return;
+  const int K = j * kTile;
+  const int chunk = ((K / nsplit + KC - 1) / KC) * KC;
+  const int kb = blockIdx.z * chunk, ke = min(K, kb + chunk);
+  double* out = work + (((size_t)blockIdx.y * tiles + blockIdx.x) * nsplit + blockIdx.z) * 64 * 64;
+  if (kb >= ke) {
+    for (int e = threadIdx.x; e < 64 * 64; e += GEMM_THREADS) out[e] = 0.0;
+    return;
+  }
+  tile_update_range(d.a, d.n, i * kTile, j * kTile, kb, ke, out);
+}
+
+__global__ void k_splitk_reduce(const FrontDesc* ds, int j, int nsplit, int tiles, const double* work) {
+  const FrontDesc d = ds[blockIdx.y];
+  const int i = j + blockIdx.x;
+  if (j * kTile >= d.p || i * kTile >= d.n) return;
+  const double* w = work + ((size_t)blockIdx.y * tiles + blockIdx.x) * nsplit * 64 * 64;
+  double* c = d.a + (size_t)(j * kTile) * d.n + i * kTile;
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < nsplit; ++q) s += w[(size_t)q * 64 * 64 + e];
+    c[(size_t)(e >> 6) * d.n + (e & 63)] -= s;
+  }
 }
 
 __global__ void __launch_bounds__(GEMM_THREADS) k_syrk_column(const FrontDesc* ds, int j) {
@@ -420,6 +468,7 @@ void configure() {
   const int gemm_smem = 4 * KC * LDS * sizeof(double);
   cudaFuncSetAttribute(k_syrk_column, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
   cudaFuncSetAttribute(k_syrk_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
+  cudaFuncSetAttribute(k_syrk_column_splitk, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
   cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 64 * LDS * (int)sizeof(double));
   cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
   cudaFuncSetAttribute(k_front_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -428,6 +477,34 @@ void configure() {
 }
 
 std::atomic<long long> g_launches{0};
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// Grow-only split-K workspace (engine entry points synchronize before
+// returning, so consecutive factorizations never overlap on it).
+double* splitk_workspace(size_t doubles) {
+  static double* p = nullptr;
+  static size_t cap = 0;
+  if (doubles > cap) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    if (cudaMalloc(&p, doubles * sizeof(double)) != cudaSuccess) {
+      cap = 0;
+      return nullptr;
+    }
+    cap = doubles;
+  }
+  return p;
+}
 
 }  // namespace
 
@@ -443,8 +520,22 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
   const int nt = max_n / kTile, pt = max_p / kTile;
   for (int j = 0; j < pt; ++j) {
     if (j > 0) {
-      k_syrk_column<<<dim3(nt - j, batch), GEMM_THREADS, gemm_smem, stream>>>(d_descs, j);
-      count_launch(1);
+      const int tiles = nt - j;
+      const long ctas = (long)tiles * batch;
+      const int K = j * kTile;
+      int nsplit = 1;
+      if (ctas < 2L * sm_count() && K >= 8 * KC)
+        nsplit = static_cast<int>(std::min<long>({16L, K / (4 * KC), (2L * sm_count() + ctas - 1) / ctas}));
+      double* work = nsplit > 1 ? splitk_workspace((size_t)ctas * nsplit * 64 * 64) : nullptr;
+      if (nsplit > 1 && work) {
+        k_syrk_column_splitk<<<dim3(tiles, batch, nsplit), GEMM_THREADS, gemm_smem, stream>>>(d_descs, j, nsplit,
+                                                                                             tiles, work);
+        k_splitk_reduce<<<dim3(tiles, batch), 256, 0, stream>>>(d_descs, j, nsplit, tiles, work);
+        count_launch(2);
+      } else {
+        k_syrk_column<<<dim3(tiles, batch), GEMM_THREADS, gemm_smem, stream>>>(d_descs, j);
+        count_launch(1);
+      }
     }
     k_panel<<<dim3(1, batch), GEMM_THREADS, panel_smem, stream>>>(d_descs, j);
     count_launch(1);

@@ -528,54 +528,75 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
   // 3. inverse iteration on T (thread m), scratch in global memory
   if (tid < k) {
     const int m = tid;
-    double* work = dd.A + (in_smem ? 0 : np) + (size_t)m * 4 * n;
-    double* xd = work;          // diagonal of the LU
-    double* xu = work + n;      // first superdiagonal
-    double* xu2 = work + 2 * n; // second superdiagonal
-    double* b = work + 3 * n;   // rhs / solution
+    double* work = dd.A + (in_smem ? 0 : np) + (size_t)m * 6 * n;
+    double* xd = work;           // U diagonal
+    double* xu = work + n;       // U first superdiagonal
+    double* xu2 = work + 2 * n;  // U second superdiagonal (row interchanges)
+    double* fm = work + 3 * n;   // multipliers
+    double* b = work + 4 * n;    // rhs / solution
+    double* sw = work + 5 * n;   // 1.0 where rows i, i+1 were interchanged
     double* z = dd.vecs + (size_t)m * N2;
     const double shift = lam[m] + 4.0 * 2.2e-16 * tnorm * ((m & 1) ? 1.0 : -1.0);
+    const double tiny = 2.2e-16 * tnorm + pivmin;
+    // LU of T - shift I with partial pivoting, factored once; the running row
+    // is carried in registers so the recurrence never waits on memory
+    double cd = dg[0] - shift, cu = n > 1 ? eg[0] : 0.0;
+    for (int i = 0; i + 1 < n; ++i) {
+      const double sub = eg[i];
+      const double nd = dg[i + 1] - shift;
+      const double nu = i + 2 < n ? eg[i + 1] : 0.0;
+      if (fabs(cd) >= fabs(sub)) {
+        if (cd == 0.0) cd = tiny;
+        const double f = sub / cd;
+        xd[i] = cd;
+        xu[i] = cu;
+        xu2[i] = 0.0;
+        fm[i] = f;
+        sw[i] = 0.0;
+        cd = nd - f * cu;
+        cu = nu;
+      } else {  // interchange rows i and i+1
+        const double f = cd / sub;
+        xd[i] = sub;
+        xu[i] = nd;
+        xu2[i] = nu;
+        fm[i] = f;
+        sw[i] = 1.0;
+        cd = cu - f * nd;
+        cu = -f * nu;
+      }
+    }
+    xd[n - 1] = cd == 0.0 ? tiny : cd;
     unsigned long long seed = 0x9E3779B97F4A7C15ULL * (m + 1);
     for (int i = 0; i < n; ++i) {
       seed ^= seed << 13; seed ^= seed >> 7; seed ^= seed << 17;
       z[i] = 0.5 + (double)(seed >> 11) * (1.0 / 9007199254740992.0);
     }
     for (int it = 0; it < 3; ++it) {
-      for (int i = 0; i < n; ++i) {
-        xd[i] = dg[i] - shift;
-        xu[i] = i + 1 < n ? eg[i] : 0.0;
-        xu2[i] = 0.0;
-        b[i] = z[i];
-      }
-      const double tiny = 2.2e-16 * tnorm + pivmin;
+      double cb = z[0];
+#pragma unroll 4
       for (int i = 0; i + 1 < n; ++i) {
-        const double sub = eg[i];
-        if (fabs(xd[i]) >= fabs(sub)) {
-          if (xd[i] == 0.0) xd[i] = tiny;
-          const double f = sub / xd[i];
-          xd[i + 1] -= f * xu[i];
-          b[i + 1] -= f * b[i];
+        const double nb = z[i + 1];
+        if (sw[i] == 0.0) {
+          b[i] = cb;
+          cb = nb - fm[i] * cb;
         } else {
-          const double f = xd[i] / sub;
-          xd[i] = sub;
-          const double tmp = xd[i + 1];
-          xd[i + 1] = xu[i] - f * tmp;
-          if (i + 2 < n) {
-            xu2[i] = xu[i + 1];
-            xu[i + 1] = -f * xu[i + 1];
-          }
-          xu[i] = tmp;
-          const double tb = b[i];
-          b[i] = b[i + 1];
-          b[i + 1] = tb - f * b[i + 1];
+          b[i] = nb;
+          cb = cb - fm[i] * nb;
         }
       }
-      if (xd[n - 1] == 0.0) xd[n - 1] = tiny;
-      b[n - 1] /= xd[n - 1];
-      if (n >= 2) b[n - 2] = (b[n - 2] - xu[n - 2] * b[n - 1]) / xd[n - 2];
-      for (int i = n - 3; i >= 0; --i) b[i] = (b[i] - xu[i] * b[i + 1] - xu2[i] * b[i + 2]) / xd[i];
-      double nn = 0.0;
-      for (int i = 0; i < n; ++i) nn += b[i] * b[i];
+      b[n - 1] = cb;
+      double x1 = b[n - 1] / xd[n - 1], x2 = 0.0;
+      b[n - 1] = x1;
+      double nn = x1 * x1;
+#pragma unroll 4
+      for (int i = n - 2; i >= 0; --i) {
+        const double xi = (b[i] - xu[i] * x1 - xu2[i] * x2) / xd[i];
+        b[i] = xi;
+        nn += xi * xi;
+        x2 = x1;
+        x1 = xi;
+      }
       nn = 1.0 / sqrt(nn);
       for (int i = 0; i < n; ++i) z[i] = b[i] * nn;
     }
@@ -838,7 +859,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
       Rv.insert(Rv.end(), h.idx.rho_i.begin(), h.idx.rho_i.end());
       oA[b] = nA;
       // Jacobi: A and V (2 n2^2); tridiagonal path: packed C + 4 n k LU scratch
-      nA += std::max(2LL * n2 * n2, (long long)dm.nj * (dm.nj + 1) / 2 + 4LL * dm.nj * std::max(dm.k, 1)) + 64;
+      nA += std::max(2LL * n2 * n2, (long long)dm.nj * (dm.nj + 1) / 2 + 6LL * dm.nj * std::max(dm.k, 1)) + 64;
       oE[b] = nE;
       nE += std::max(dm.k, 1);
       oW[b] = nW;

@@ -1,0 +1,141 @@
+"""Multi-rank (N > 1) logic on CPU with torch.distributed/gloo, world_size 2.
+
+Covers the sharding plan of the path (paper_0910_5863_b200/shard.py: block
+partition, pair ownership, interface halo exchange, owned-dof dot products,
+root sums) against the single-process oracle, and bench.py's multi-rank
+harness (barrier, max over ranks).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_0910_5863_b200 import shard
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_partition_shapes():
+    assert shard.process_grid((12, 12, 12), 8) == (2, 2, 2)
+    own = shard.partition((12, 12, 12), 8)
+    assert np.all(np.bincount(own) == 216)  # 6^3 subdomains per GPU
+    own = shard.partition((6, 6, 6), 8)
+    assert np.all(np.bincount(own) == 27)
+    own = shard.partition((8, 8, 8), 4)
+    assert np.all(np.bincount(own) == 128)
+    own = shard.partition((3, 3, 3), 2)
+    assert sorted(np.bincount(own)) in ([9, 18], [12, 15], [13, 14])
+    # blocks are contiguous boxes: every rank's subdomains form one lattice box
+    own = shard.partition((6, 4, 2), 4)
+    for r in range(4):
+        ids = np.nonzero(own == r)[0]
+        i, j, k = ids % 6, (ids // 6) % 4, ids // 24
+        assert len(ids) == (i.max() - i.min() + 1) * (j.max() - j.min() + 1) * (k.max() - k.min() + 1)
+
+
+def _subdomain_contribution(itf, s, x):
+    """InterfaceProblem::apply (schur.cpp:12-36) restricted to substructure s."""
+    sys = itf.systems[s]
+    h = itf.h
+    out = np.zeros(itf.size)
+    xl = np.zeros(sys.dim)
+    bnd, inn = h.boundary[s], h.interior[s]
+    xl[bnd] = x[itf.bidx[s]]
+    if len(inn):
+        xl[inn] = h.interior_solve(s, -(h.coupling[s] @ xl[bnd]))
+    y = sys.stiffness @ xl
+    np.add.at(out, itf.bidx[s], y[bnd])
+    return out
+
+
+def _worker(rank, world, port, errors):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle import fem
+        from oracle.adaptive import face_pairs
+        from oracle.experiment import build_pipeline, cube_spec
+        from oracle.spaces import HarmonicExtension, InterfaceProblem
+        sub = (3, 2, 2)
+        p = build_pipeline(cube_spec(sub, 3, fem.SCALAR))
+        h = HarmonicExtension(p.systems, p.maps)
+        itf = InterfaceProblem(p.systems, p.maps, h)
+        owner = shard.partition(sub, world)
+        copy_ranks = [[int(owner[s]) for s, _ in p.maps.dof_copies[g]] for g in p.maps.interface_dofs]
+        plan = shard.HaloPlan.build(rank, copy_ranks)
+        x = np.random.default_rng(7).standard_normal(itf.size)
+        # each rank applies only its substructures, then the halo exchange sums copies
+        part = np.zeros(itf.size)
+        for s in np.nonzero(owner == rank)[0]:
+            part += _subdomain_contribution(itf, int(s), x)
+        local = torch.from_numpy(part[plan.local_iface].copy())
+        plan.exchange(local, dist)
+        ref = itf.apply(x)
+        got = local.numpy()
+        assert np.allclose(got, ref[plan.local_iface], rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+        # shared dofs are bitwise identical on both ranks after the exchange
+        sums = torch.from_numpy(np.zeros(itf.size))
+        sums[torch.from_numpy(plan.local_iface)] = local
+        other = sums.clone()
+        dist.all_reduce(other, op=dist.ReduceOp.MAX)
+        mine = sums.clone()
+        dist.all_reduce(mine, op=dist.ReduceOp.MIN)
+        for r, idx in plan.shared.items():
+            g = plan.local_iface[idx]
+            assert torch.equal(other[g], mine[g])
+        # owned-dof dot product equals the global one
+        xl = torch.from_numpy(x[plan.local_iface].copy())
+        d = plan.owned_dot(local, xl, dist)
+        assert abs(d - float(ref @ x)) <= 1e-12 * abs(float(ref @ x))
+        # every face pair has exactly one owner rank
+        pairs = face_pairs(p.globset)
+        po = shard.pair_owner(pairs, owner)
+        mine_pairs = torch.tensor([int(np.sum(po == rank))], dtype=torch.int64)
+        dist.all_reduce(mine_pairs)
+        assert int(mine_pairs.item()) == len(pairs)
+        # root sum: per-rank coarse contributions (corner-dof incidence) add to the global count
+        root = np.zeros(p.maps.corner_dof_count)
+        for s in np.nonzero(owner == rank)[0]:
+            for l, cid in enumerate(p.maps.local_to_wc[int(s)]):
+                if p.maps.local_is_corner[int(s)][l]:
+                    root[cid] += 1.0
+        rt = shard.root_sum(torch.from_numpy(root), dist)
+        glob = np.zeros(p.maps.corner_dof_count)
+        for s in range(len(p.systems)):
+            for l, cid in enumerate(p.maps.local_to_wc[s]):
+                if p.maps.local_is_corner[s][l]:
+                    glob[cid] += 1.0
+        assert np.array_equal(rt.numpy(), glob)
+        # bench.py's multi-rank harness
+        import bench
+        bench.barrier(dist)
+        assert bench.max_over_ranks(dist, float(rank + 1)) == float(world)
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        errors.put("rank %d: %s\n%s" % (rank, e, traceback.format_exc()))
+
+
+def test_sharded_interface_operations_gloo():
+    ctx = mp.get_context("spawn")
+    errors = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, errors)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=300)
+    msgs = []
+    while not errors.empty():
+        msgs.append(errors.get())
+    assert not msgs, "\n".join(msgs)
+    assert all(pr.exitcode == 0 for pr in procs)
