@@ -186,55 +186,75 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_syrk_trailing(const FrontDesc*
   tile_update(d.a, d.n, (pt + ii) * kTile, (pt + jj) * kTile, d.p);
 }
 
-// Panel step: every CTA of tile column j factors the diagonal tile in shared
-// memory (redundantly, avoiding a launch), then solves its own tile.
-//   POTRF: 16-wide blocked; warp 0 factors each 16x16 diagonal block with warp
-//          synchronization only, the panel below is solved row-parallel and the
-//          trailing 48x48 (or smaller) block updated by the whole CTA (12 barriers).
+// Panel step (one CTA per front): L_jj = chol(C_jj) and Dinv_j = L_jj^{-1}.
+//   POTRF: 16-wide blocked.  Warp 0 factors each 16x16 diagonal block in
+//          registers (lane r holds row r; pivots and column entries move by
+//          shuffles), the panel rows below are solved row-parallel and the
+//          trailing block updated by the whole CTA.
 //   L^{-1}: 16x16 diagonal-block inverses (one warp each), off-diagonal blocks by
 //          block diagonals: Linv_ij = -Linv_ii sum_k L_ik Linv_kj.
-//   TRSM:  X = C L^{-T} = C Linv^T as one 64x64x64 DMMA tile product.
-__global__ void __launch_bounds__(GEMM_THREADS) k_panel(const FrontDesc* ds, int j) {
+// k_trsm then forms X = C L^{-T} = C Linv^T as one 64x64x64 DMMA tile product.
+// Cholesky of the 16x16 diagonal block at Lo (ld LDS, lower triangle) by one
+// warp: lane r holds row r in registers; pivots and column entries move by
+// shuffles; selects (not branches) keep the row in registers.  Kept out of line
+// so the unrolled row stays in registers inside the caller's block loop.
+// Writes 1/L_kk to rd[k].  Returns 1 + the first non-positive pivot, or 0.
+__device__ __noinline__ int chol16(double* Lo, double* rd, int lane) {
+  const int r = lane & 15;
+  double a[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) a[c] = Lo[c * LDS + r];
+  int bad = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const double dkk = __shfl_sync(0xffffffffu, a[k], k);
+    if (!(dkk > 0.0) && !bad) bad = k + 1;
+    const double inv = dkk > 0.0 ? rsqrt(dkk) : 1.0;
+    const double sk = dkk > 0.0 ? dkk * inv : 1.0;
+    if (lane == k) rd[k] = inv;
+    a[k] = (r == k) ? sk : (r > k ? a[k] * inv : a[k]);
+#pragma unroll
+    for (int c = k + 1; c < 16; ++c) {
+      const double lc = __shfl_sync(0xffffffffu, a[k], c);  // L[c][k]
+      a[c] = (r >= c) ? a[c] - a[k] * lc : a[c];
+    }
+  }
+  if (lane < 16) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c <= r) Lo[c * LDS + r] = a[c];
+  }
+  return bad;
+}
+
+constexpr int PANEL_THREADS = 256;
+
+__global__ void __launch_bounds__(PANEL_THREADS) k_panel(const FrontDesc* ds, int j) {
   const FrontDesc d = ds[blockIdx.y];
-  const int i = j;  // one CTA per front: the diagonal tile only (k_trsm solves the rest)
-  if (j * kTile >= d.p || i * kTile >= d.n) return;
+  if (j * kTile >= d.p) return;
   extern __shared__ __align__(16) double smem[];
-  double* L = smem;                 // 64 x LDS, column-major: L[c*LDS + r]
-  double* V = smem + 64 * LDS;      // L^{-1}
-  double* C = smem + 2 * 64 * LDS;  // target tile (off-diagonal CTAs)
-  __shared__ double T[3][16][17];   // block products of the inverse
+  double* L = smem;             // 64 x LDS, column-major: L[c*LDS + r]
+  double* V = smem + 64 * LDS;  // L^{-1} (lower block triangle only)
+  __shared__ double T[3][16][17];  // block products of the inverse
+  __shared__ double rd[64];        // reciprocal diagonal of L_jj
   __shared__ int bad_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t ld = d.n;
   const double* diag = d.a + (size_t)(j * kTile) * ld + j * kTile;
-  const double* ct = d.a + (size_t)(j * kTile) * ld + i * kTile;
-  for (int e = tid; e < 64 * 64; e += GEMM_THREADS) {
-    const int r = e & 63, c = e >> 6;
-    L[c * LDS + r] = diag[(size_t)c * ld + r];
-    V[c * LDS + r] = 0.0;
-    if (i != j) C[c * LDS + r] = ct[(size_t)c * ld + r];
+  for (int q = tid; q < 64 * 32; q += PANEL_THREADS) {
+    const int col = q >> 5, part = q & 31;
+    cp_async16(L + col * LDS + part * 2, diag + (size_t)col * ld + part * 2);
   }
+  cp_async_commit();
   if (tid == 0) bad_s = 0;
+  cp_async_wait<0>();
   __syncthreads();
   // ---- blocked POTRF ----
   for (int kb = 0; kb < 4; ++kb) {
     const int o = kb * 16;
     if (warp == 0) {
-      for (int k = 0; k < 16; ++k) {
-        const double dkk = L[(o + k) * LDS + o + k];
-        __syncwarp();
-        const bool ok = dkk > 0.0;
-        if (!ok && lane == 0) bad_s = o + k + 1;
-        const double sk = ok ? sqrt(dkk) : 1.0;
-        if (lane == k) L[(o + k) * LDS + o + k] = sk;
-        if (lane > k && lane < 16) L[(o + k) * LDS + o + lane] /= sk;
-        __syncwarp();
-        if (lane > k && lane < 16) {
-          const double lr = L[(o + k) * LDS + o + lane];
-          for (int c = k + 1; c <= lane; ++c) L[(o + c) * LDS + o + lane] -= lr * L[(o + k) * LDS + o + c];
-        }
-        __syncwarp();
-      }
+      const int bad = chol16(L + o * LDS + o, rd + o, lane);
+      if (lane == 0 && bad && !bad_s) bad_s = o + bad;
     }
     __syncthreads();
     // panel rows below: x L_kk^T = a  (thread per row)
@@ -246,15 +266,15 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_panel(const FrontDesc* ds, int
         double s = L[(o + c) * LDS + r];
 #pragma unroll
         for (int k = 0; k < c; ++k) s -= x[k] * L[(o + k) * LDS + o + c];
-        x[c] = s / L[(o + c) * LDS + o + c];
+        x[c] = s * rd[o + c];
       }
 #pragma unroll
       for (int c = 0; c < 16; ++c) L[(o + c) * LDS + r] = x[c];
     }
     __syncthreads();
-    // trailing update of the tile: rows/cols >= o + 16
+    // trailing update of the tile: rows/cols >= o + 16 (lower triangle)
     const int m = 48 - o;
-    for (int e = tid; e < m * m; e += GEMM_THREADS) {
+    for (int e = tid; e < m * m; e += PANEL_THREADS) {
       const int rr = o + 16 + e % m, cc = o + 16 + e / m;
       if (rr < cc) continue;
       double s = 0.0;
@@ -265,32 +285,29 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_panel(const FrontDesc* ds, int
     __syncthreads();
   }
   if (bad_s) {
-    if (tid == 0 && i == j) atomicCAS(d.info, 0, j * kTile + bad_s);
+    if (tid == 0) atomicCAS(d.info, 0, j * kTile + bad_s);
     return;
   }
-  // ---- L^{-1}: diagonal 16x16 blocks (warp w inverts block w) ----
-  {
-    const int o = warp * 16;
-    if (lane < 16) {
-      const int c = lane;
-      double x[16];
+  // ---- L^{-1}: diagonal 16x16 blocks (warp w < 4 inverts block w) ----
+  if (warp < 4 && lane < 16) {
+    const int o = warp * 16, c = lane;
+    double x[16];
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        double s = (r == c) ? 1.0 : 0.0;
+    for (int r = 0; r < 16; ++r) {
+      double s = (r == c) ? 1.0 : 0.0;
 #pragma unroll
-        for (int k = 0; k < r; ++k) s -= L[(o + k) * LDS + o + r] * x[k];
-        x[r] = (r >= c) ? s / L[(o + r) * LDS + o + r] : 0.0;
-      }
-#pragma unroll
-      for (int r = 0; r < 16; ++r) V[(o + c) * LDS + o + r] = x[r];
+      for (int k = 0; k < r; ++k) s -= L[(o + k) * LDS + o + r] * x[k];
+      x[r] = (r >= c) ? s * rd[o + r] : 0.0;
     }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) V[(o + c) * LDS + o + r] = x[r];
   }
   __syncthreads();
   // ---- off-diagonal blocks by block diagonal dd = bi - bj ----
   for (int dd = 1; dd < 4; ++dd) {
     const int nblk = 4 - dd;
     // T_b = sum_{k=bj}^{bi-1} L_{bi,k} Linv_{k,bj}
-    for (int e = tid; e < nblk * 256; e += GEMM_THREADS) {
+    for (int e = tid; e < nblk * 256; e += PANEL_THREADS) {
       const int b = e >> 8, r = (e >> 4) & 15, c = e & 15;
       const int bj = b, bi = b + dd;
       double s = 0.0;
@@ -299,7 +316,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_panel(const FrontDesc* ds, int
     }
     __syncthreads();
     // Linv_{bi,bj} = -Linv_{bi,bi} T_b
-    for (int e = tid; e < nblk * 256; e += GEMM_THREADS) {
+    for (int e = tid; e < nblk * 256; e += PANEL_THREADS) {
       const int b = e >> 8, r = (e >> 4) & 15, c = e & 15;
       const int bj = b, bi = b + dd;
       double s = 0.0;
@@ -309,12 +326,17 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_panel(const FrontDesc* ds, int
     }
     __syncthreads();
   }
-  // Dinv = L^{-1}.  The diagonal tile itself is never read again (solves and
-  // later updates touch only off-diagonal tiles), so it is not written back.
-  (void)C;
-  (void)ct;
-  double* dv = d.dinv + (size_t)j * 64 * 64;
-  for (int e = tid; e < 64 * 64; e += GEMM_THREADS) dv[(size_t)(e >> 6) * 64 + (e & 63)] = V[(e >> 6) * LDS + (e & 63)];
+  // Dinv = L^{-1} (zero above the block diagonal).  The diagonal tile itself is
+  // never read again (solves and later updates touch only off-diagonal tiles),
+  // so it is not written back.
+  double2* dv = reinterpret_cast<double2*>(d.dinv + (size_t)j * 64 * 64);
+  for (int q = tid; q < 64 * 32; q += PANEL_THREADS) {
+    const int c = q >> 5, r = (q & 31) * 2;
+    double2 v;
+    v.x = (r >> 4) >= (c >> 4) ? V[c * LDS + r] : 0.0;
+    v.y = (r >> 4) >= (c >> 4) ? V[c * LDS + r + 1] : 0.0;
+    dv[q] = v;
+  }
 }
 
 // Off-diagonal tiles of column j: X = C_ij L_jj^{-T} = C_ij Dinv_j^T as one
@@ -469,7 +491,7 @@ void configure() {
   cudaFuncSetAttribute(k_syrk_column, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
   cudaFuncSetAttribute(k_syrk_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
   cudaFuncSetAttribute(k_syrk_column_splitk, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
-  cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 64 * LDS * (int)sizeof(double));
+  cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
   cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
   cudaFuncSetAttribute(k_front_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -477,17 +499,6 @@ void configure() {
 }
 
 std::atomic<long long> g_launches{0};
-
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
 
 // Grow-only split-K workspace (engine entry points synchronize before
 // returning, so consecutive factorizations never overlap on it).
@@ -508,6 +519,17 @@ double* splitk_workspace(size_t doubles) {
 
 }  // namespace
 
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 void count_launch(long long n) { g_launches += n; }
 long long launch_count() { return g_launches.load(); }
 
@@ -516,7 +538,7 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
   if (batch == 0) return;
   configure();
   const int gemm_smem = 4 * KC * LDS * sizeof(double);
-  const int panel_smem = 3 * 64 * LDS * sizeof(double);
+  const int panel_smem = 2 * 64 * LDS * sizeof(double);
   const int nt = max_n / kTile, pt = max_p / kTile;
   for (int j = 0; j < pt; ++j) {
     if (j > 0) {
@@ -537,7 +559,7 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
         count_launch(1);
       }
     }
-    k_panel<<<dim3(1, batch), GEMM_THREADS, panel_smem, stream>>>(d_descs, j);
+    k_panel<<<dim3(1, batch), PANEL_THREADS, panel_smem, stream>>>(d_descs, j);
     count_launch(1);
     if (nt - j - 1 > 0) {
       k_trsm<<<dim3(nt - j - 1, batch), GEMM_THREADS, 2 * 64 * LDS * (int)sizeof(double), stream>>>(d_descs, j);

@@ -40,6 +40,9 @@ struct SolveDesc {
   const double* croot;
 };
 
+/// Streaming multiprocessors of the current device.
+int sm_count();
+
 /// Kernel-launch accounting (bench "gpu_launches").
 void count_launch(long long n);
 long long launch_count();

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -68,6 +69,7 @@ struct SubDesc {        // per-subdomain pointers used by the PCG kernels
   const int* bslot;     // nB: slot within the glob
   double* WB;           // nB: boundary scratch
   int nB, PB, NF, PE;
+  int ldF;              // leading dimension of F (NF, or NF + PE for the augmented front)
 };
 
 struct XformDesc {      // glob transforms, flat
@@ -129,8 +131,10 @@ __global__ void __launch_bounds__(256) k_schur_gemv(const SubDesc* sd, const dou
   }
 }
 
-// Row-blocked variant: CTA (rb, s) forms rows [64 rb, 64 rb + 64) of S_s x_s;
-// the four 64-thread groups split the columns and are reduced in shared memory.
+// Row-blocked variant: CTA (rb, s) forms rows [64 rb, 64 rb + 64) of S_s x_s.
+// Lane l of warp w owns rows (2l, 2l+1) (one 16-byte load per column) and the
+// columns w, w+8, ...; eight columns are in flight per thread, the eight warp
+// partials are reduced in shared memory in a fixed order.
 __global__ void __launch_bounds__(256) k_schur_gemv_rows(const SubDesc* sd, const double* __restrict__ p,
                                                          const int* done) {
   if (done && *done) return;
@@ -138,26 +142,44 @@ __global__ void __launch_bounds__(256) k_schur_gemv_rows(const SubDesc* sd, cons
   const int r0 = blockIdx.x * 64;
   if (r0 >= d.nB) return;
   extern __shared__ double xs[];
-  __shared__ double part[4][64];
+  __shared__ double2 part[8][32];
   for (int c = threadIdx.x; c < d.nB; c += blockDim.x) xs[c] = p[d.biface[c]];
   __syncthreads();
-  const int g = threadIdx.x >> 6, r = r0 + (threadIdx.x & 63);
-  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-  if (r < d.PB) {
-    const double* row = d.S + r;
-    int c = g;
-    for (; c + 12 < d.nB; c += 16) {
-      s0 += row[(size_t)c * d.PB] * xs[c];
-      s1 += row[(size_t)(c + 4) * d.PB] * xs[c + 4];
-      s2 += row[(size_t)(c + 8) * d.PB] * xs[c + 8];
-      s3 += row[(size_t)(c + 12) * d.PB] * xs[c + 12];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double2* col0 = reinterpret_cast<const double2*>(d.S + r0) + lane;  // rows r0 + 2 lane, +1
+  const size_t ld2 = d.PB / 2;
+  double2 acc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
+  int c = w;
+  for (; c + 56 < d.nB; c += 64) {
+    double2 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldg(col0 + (size_t)(c + 8 * q) * ld2);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double x = xs[c + 8 * q];
+      acc[q & 3].x += v[q].x * x;
+      acc[q & 3].y += v[q].y * x;
     }
-    for (; c < d.nB; c += 4) s0 += row[(size_t)c * d.PB] * xs[c];
   }
-  part[g][threadIdx.x & 63] = (s0 + s1) + (s2 + s3);
+  for (; c < d.nB; c += 8) {
+    const double2 v = __ldg(col0 + (size_t)c * ld2);
+    const double x = xs[c];
+    acc[0].x += v.x * x;
+    acc[0].y += v.y * x;
+  }
+  part[w][lane] = make_double2((acc[0].x + acc[1].x) + (acc[2].x + acc[3].x),
+                               (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
   __syncthreads();
-  if (threadIdx.x < 64 && r < d.nB)
-    d.WB[r] = (part[0][threadIdx.x] + part[1][threadIdx.x]) + (part[2][threadIdx.x] + part[3][threadIdx.x]);
+  if (threadIdx.x < 64) {
+    const int l = threadIdx.x >> 1, h = threadIdx.x & 1;
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += h ? part[q][l].y : part[q][l].x;
+    const int r = r0 + threadIdx.x;
+    if (r < d.nB) d.WB[r] = s;
+  }
 }
 
 __device__ __forceinline__ void block_partial(double v, double* partials) {
@@ -331,7 +353,7 @@ __global__ void k_rowxform_scatter(const SubDesc* sd, XformDesc x, const double*
   const int c = blockIdx.x;
   if (c < d.nB) {
     const double* col = X + (size_t)c * d.PB;
-    const size_t fc = (size_t)d.posF[c] * d.NF;
+    const size_t fc = (size_t)d.posF[c] * d.ldF;
     for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
       const int inst = d.bglob[b];
       const double v = inst < 0 ? col[b] : xform_T_t(x, inst, d.bslot[b], col);
@@ -347,6 +369,104 @@ __global__ void k_pad_identity(double* Farena, const long long* foff, const int*
     const int q = pads[t], s = pad_sub[t];
     Farena[foff[s] + (size_t)q * NF[s] + q] = 1.0;
   }
+}
+
+// Explicit leaf mode (few leaf fronts: the sweeps would leave most SMs idle).
+// The transformed leaf front is augmented to [[F_ee, F_ec, I], [F_ce, F_cc, 0],
+// [I, 0, 0]] and only the e block is eliminated; the trailing block then holds
+//   [[S_cc, -W^T], [-W, -F_ee^{-1}]],  W = F_ee^{-1} F_ec,
+// and both leaf sweeps of the preconditioner become parallel GEMVs with
+// E = [-F_ee^{-1} | -W]  (PE x (PE + M), column-major, ld PE).
+struct LeafX {
+  const double* a;  // augmented front (ld n)
+  double* E;
+  double* FV;       // F-layout vector: right-hand side in, solution out
+  double* FV2;      // forward result: [u = F_ee^{-1} b_e | y_c = b_c - W^T b_e]
+  const int* cmap;  // M: root index of each coarse slot or -1
+  int n, PE, M;
+};
+
+__global__ void k_aug_identity(const LeafX* ds) {
+  const LeafX d = ds[blockIdx.y];
+  double* a = const_cast<double*>(d.a);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.PE; i += gridDim.x * blockDim.x)
+    a[(size_t)i * d.n + d.PE + d.M + i] = 1.0;
+}
+
+// E from the lower triangle of the trailing block (element (r, c), r >= c, at
+// a[(PE + c) n + PE + r]; trailing index: coarse slots [0, M), augmented [M, M + PE)).
+__global__ void k_leaf_explicit_copy(const LeafX* ds) {
+  const LeafX d = ds[blockIdx.y];
+  const long total = (long)d.PE * (d.PE + d.M);
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(t % d.PE), j = static_cast<int>(t / d.PE);
+    int r, c;
+    if (j < d.PE) {
+      r = d.M + max(i, j);
+      c = d.M + min(i, j);
+    } else {
+      r = d.M + i;
+      c = j - d.PE;
+    }
+    d.E[(size_t)j * d.PE + i] = d.a[(size_t)(d.PE + c) * d.n + d.PE + r];
+  }
+}
+
+// forward: warp per column j of E (symmetric -F_ee^{-1}: column == row), b_e staged in smem
+__global__ void __launch_bounds__(256) k_leaf_fwd_explicit(const LeafX* ds, const int* done) {
+  if (done && *done) return;
+  const LeafX d = ds[blockIdx.y];
+  const int cols = d.PE + d.M;
+  if (blockIdx.x * 8 >= cols) return;
+  extern __shared__ double bs[];
+  for (int k = threadIdx.x; k < d.PE; k += blockDim.x) bs[k] = d.FV[k];
+  __syncthreads();
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= cols) return;
+  const double* col = d.E + (size_t)j * d.PE;
+  double s0 = 0.0, s1 = 0.0;
+  for (int k = lane; k < d.PE; k += 64) {  // PE is a multiple of 64
+    s0 += col[k] * bs[k];
+    s1 += col[k + 32] * bs[k + 32];
+  }
+  double s = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) d.FV2[j] = j < d.PE ? -s : d.FV[j] + s;
+}
+
+// backward: x_e = u - W x_c.  CTA (rb, s): rows [64 rb, 64 rb + 64) of the
+// F-layout vector; the four 64-thread groups split the coarse slots, partials
+// reduced in a fixed order.  Coarse slots take the root values.
+__global__ void __launch_bounds__(256) k_leaf_bwd_explicit(const LeafX* ds, const double* __restrict__ croot,
+                                                           const int* done) {
+  if (done && *done) return;
+  const LeafX d = ds[blockIdx.y];
+  const int r0 = blockIdx.x * 64;
+  if (r0 >= d.PE + d.M) return;
+  extern __shared__ double xc[];
+  __shared__ double part[4][64];
+  for (int c = threadIdx.x; c < d.M; c += blockDim.x) xc[c] = d.cmap[c] >= 0 ? croot[d.cmap[c]] : 0.0;
+  __syncthreads();
+  const int g = threadIdx.x >> 6, i = r0 + (threadIdx.x & 63);
+  if (r0 >= d.PE) {  // coarse slots (PE is a multiple of 64)
+    if (g == 0) d.FV[i] = xc[i - d.PE];
+    return;
+  }
+  const double* w = d.E + (size_t)d.PE * d.PE + i;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int c = g;
+  for (; c + 12 < d.M; c += 16) {
+    s0 += w[(size_t)c * d.PE] * xc[c];
+    s1 += w[(size_t)(c + 4) * d.PE] * xc[c + 4];
+    s2 += w[(size_t)(c + 8) * d.PE] * xc[c + 8];
+    s3 += w[(size_t)(c + 12) * d.PE] * xc[c + 12];
+  }
+  for (; c < d.M; c += 4) s0 += w[(size_t)c * d.PE] * xc[c];
+  part[g][threadIdx.x & 63] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (g == 0)
+    d.FV[i] = d.FV2[i] + ((part[0][threadIdx.x] + part[1][threadIdx.x]) + (part[2][threadIdx.x] + part[3][threadIdx.x]));
 }
 
 struct RootAsm {
@@ -473,7 +593,11 @@ struct DeviceState {
   std::vector<int> NF, PE, nE, nC;
   std::vector<long long> f_off, df_off, fv_off;
   int max_NF = 0, max_PE = 0, max_M = 0;
-  DBuf<double> F, DinvF, FV, Xtmp;
+  bool leaf_explicit = false;  // explicit leaf mode (k_leaf_*_explicit)
+  std::vector<int> NA;         // F leading dimension (NF, or NF + PE augmented)
+  int max_NA = 0, max_MA = 0;
+  DBuf<double> F, DinvF, FV, FV2, Xtmp, E;
+  DBuf<LeafX> leafx;
   DBuf<long long> d_xoff;
   DBuf<int> finfo;
   DBuf<FrontDesc> ffront;
@@ -755,7 +879,7 @@ double Engine::leaf_front_bytes() const {
   double b = 0;
   for (int s = 0; s < D.nsub && s < (int)D.NF.size(); ++s) {
     const double e = D.nE[s], c = D.nC[s];
-    b += (e * (e + 1) / 2 + c * e) * 8.0;
+    b += (D.leaf_explicit ? e * e + c * e : e * (e + 1) / 2 + c * e) * 8.0;
   }
   b += double(D.n_root) * (D.n_root + 1) / 2 * 8.0;
   return b;
@@ -845,7 +969,17 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   std::vector<int> posF(D.WB.n, 0), cmap, pads, pad_sub;
   std::vector<long long> cmap_off(ns), pad_off(ns + 1), xoff(ns);
   long long fo = 0, dfo = 0, fvo = 0, xo = 0;
-  D.max_NF = D.max_PE = D.max_M = 0;
+  D.max_NF = D.max_PE = D.max_M = D.max_NA = D.max_MA = 0;
+  D.NA.assign(ns, 0);
+  std::vector<long long> e_off(ns);
+  long long eo = 0;
+  {
+    // explicit leaf mode when the leaf fronts cannot fill the SMs (BDDC_B200_LEAF
+    // = explicit | factor overrides)
+    const char* env = std::getenv("BDDC_B200_LEAF");
+    const std::string mode = env ? env : "";
+    D.leaf_explicit = mode == "explicit" || (mode != "factor" && ns < sm_count());
+  }
   std::vector<int> root_cnt(D.n_root + 1, 0);
   for (int s = 0; s < ns; ++s) {
     const int nB = D.nB[s], nC = static_cast<int>(coarse_b[s].size()), nE = nB - nC;
@@ -853,8 +987,11 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     D.nC[s] = nC;
     D.PE[s] = rup(nE, kTile);
     D.NF[s] = D.PE[s] + rup(std::max(nC, 1), kTile);
+    D.NA[s] = D.leaf_explicit ? D.NF[s] + D.PE[s] : D.NF[s];
     D.f_off[s] = fo;
-    fo += (long long)D.NF[s] * D.NF[s];
+    fo += (long long)D.NA[s] * D.NA[s];
+    e_off[s] = eo;
+    if (D.leaf_explicit) eo += (long long)D.PE[s] * D.NF[s];
     D.df_off[s] = dfo;
     dfo += (long long)(D.PE[s] / kTile) * kTile * kTile;
     D.fv_off[s] = fvo;
@@ -864,6 +1001,8 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     D.max_NF = std::max(D.max_NF, D.NF[s]);
     D.max_PE = std::max(D.max_PE, D.PE[s]);
     D.max_M = std::max(D.max_M, D.NF[s] - D.PE[s]);
+    D.max_NA = std::max(D.max_NA, D.NA[s]);
+    D.max_MA = std::max(D.max_MA, D.NA[s] - D.PE[s]);
     std::vector<int> is_coarse(nB, -1);
     for (int c = 0; c < nC; ++c) is_coarse[coarse_b[s][c]] = c;
     int e = 0;
@@ -924,6 +1063,12 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   D.F.zero(st);
   D.DinvF.alloc(std::max<long long>(dfo, 1));
   D.FV.alloc(fvo);
+  D.FV.zero(st);
+  if (D.leaf_explicit) {
+    D.FV2.alloc(fvo);
+    D.FV2.zero(st);
+    D.E.alloc(std::max<long long>(eo, 1));
+  }
   D.Xtmp.alloc(xo);
   D.d_xoff.upload(xoff, st);
   D.finfo.alloc(ns);
@@ -934,8 +1079,8 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   for (int s = 0; s < ns; ++s) {
     sd[s] = SubDesc{D.S.p + D.s_off[s], D.F.p + D.f_off[s], D.FV.p + D.fv_off[s], D.biface.p + D.wb_off[s],
                     D.bw.p + D.wb_off[s], D.bposF.p + D.wb_off[s], D.bglob.p + D.wb_off[s],
-                    D.bslot.p + D.wb_off[s], D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], D.NF[s], D.PE[s]};
-    fd[s] = FrontDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.NF[s], D.PE[s], D.finfo.p + s, 0};
+                    D.bslot.p + D.wb_off[s], D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], D.NF[s], D.PE[s], D.NA[s]};
+    fd[s] = FrontDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.NA[s], D.PE[s], D.finfo.p + s, 0};
     fw[s] = SolveDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.FV.p + D.fv_off[s], D.NF[s], D.PE[s],
                       nullptr, nullptr};
   }
@@ -960,12 +1105,19 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     bw[s].croot = D.root_inv ? D.xroot2.p : D.xroot.p;
   }
   D.fsolve_bwd.upload(bw, st);
+  if (D.leaf_explicit) {
+    std::vector<LeafX> lx(ns);
+    for (int s = 0; s < ns; ++s)
+      lx[s] = LeafX{D.F.p + D.f_off[s], D.E.p + e_off[s], D.FV.p + D.fv_off[s], D.FV2.p + D.fv_off[s],
+                    D.cmap.p + cmap_off[s], D.NA[s], D.PE[s], D.NF[s] - D.PE[s]};
+    D.leafx.upload(lx, st);
+  }
   up_i(D.root_ptr, rptr);
   up_i(D.root_sub, rsub);
   up_i(D.root_c, rc);
   if (rsrc.empty()) D.root_src.alloc(1); else D.root_src.upload(rsrc, st);
   D.d_foff.upload(D.f_off, st);
-  up_i(D.d_NF, D.NF);
+  up_i(D.d_NF, D.NA);  // leading dimensions of the F fronts
   up_i(D.d_PE, D.PE);
   up_i(D.pads, pads);
   up_i(D.pad_sub, pad_sub);
@@ -978,11 +1130,19 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     k_pad_identity<<<std::min<int>(1024, (static_cast<int>(pads.size()) + 255) / 256), 256, 0, st>>>(
         D.F.p, D.d_foff.p, D.d_NF.p, D.pad_sub.p, D.pads.p, static_cast<int>(pads.size()));
   count_launch(3);
+  if (D.leaf_explicit) {
+    k_aug_identity<<<dim3((D.max_PE + 255) / 256, ns), 256, 0, st>>>(D.leafx.p);
+    count_launch(1);
+  }
   CK(cudaGetLastError());
   prof.mark("xform");
-  partial_cholesky(D.ffront.p, ns, D.max_NF, D.max_PE, D.max_M, st);
+  partial_cholesky(D.ffront.p, ns, D.max_NA, D.max_PE, D.max_MA, st);
+  if (D.leaf_explicit) {
+    k_leaf_explicit_copy<<<dim3(256, ns), 256, 0, st>>>(D.leafx.p);
+    count_launch(1);
+  }
   CK(cudaGetLastError());
-  prof.mark("cholF");
+  prof.mark(D.leaf_explicit ? "cholF+explicit" : "cholF");
   RootAsm ra{D.root_ptr.p, D.root_sub.p, D.root_c.p, D.d_foff.p, D.d_NF.p, D.d_PE.p};
   k_root_assemble<<<1024, 256, 0, st>>>(D.n_root, D.NR, ldR, ra, D.F.p, D.R.p);
   count_launch(1);
@@ -1036,10 +1196,15 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
   k_restrict<<<ns, 256, smem_b, st>>>(D.subdesc.p, D.xf, r, done);
   count_launch(4);
   mark("restrict");
-  front_forward(D.fsolve_fwd.p, ns, D.max_NF, st, done);
+  if (D.leaf_explicit) {
+    k_leaf_fwd_explicit<<<dim3((D.max_NF + 7) / 8, ns), 256, D.max_PE * sizeof(double), st>>>(D.leafx.p, done);
+    count_launch(1);
+  } else {
+    front_forward(D.fsolve_fwd.p, ns, D.max_NF, st, done);
+  }
   mark("leaf_fwd");
-  k_root_gather<<<std::max(1, std::min(1024, (D.NR + 255) / 256)), 256, 0, st>>>(D.n_root, D.NR, D.root_ptr.p,
-                                                                             D.root_src.p, D.FV.p, D.xroot.p, done);
+  k_root_gather<<<std::max(1, std::min(1024, (D.NR + 255) / 256)), 256, 0, st>>>(
+      D.n_root, D.NR, D.root_ptr.p, D.root_src.p, D.leaf_explicit ? D.FV2.p : D.FV.p, D.xroot.p, done);
   mark("root_gather");
   if (D.root_inv) {
     k_root_gemv<<<std::min(1184, (D.NR + 7) / 8), 256, 0, st>>>(D.NR, D.Rinv.p, D.xroot.p, D.xroot2.p, done);
@@ -1051,7 +1216,13 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     front_backward(D.rsolve.p, 1, D.NR, st, done);
     mark("root_bwd");
   }
-  front_backward(D.fsolve_bwd.p, ns, D.max_NF, st, done);
+  if (D.leaf_explicit) {
+    k_leaf_bwd_explicit<<<dim3(D.max_NF / kTile, ns), 256, D.max_M * sizeof(double), st>>>(
+        D.leafx.p, D.root_inv ? D.xroot2.p : D.xroot.p, done);
+    count_launch(1);
+  } else {
+    front_backward(D.fsolve_bwd.p, ns, D.max_NF, st, done);
+  }
   mark("leaf_bwd");
   k_prolong<<<ns, 256, smem_b, st>>>(D.subdesc.p, D.xf, done);
   mark("prolong");
