@@ -442,11 +442,15 @@ __global__ void __launch_bounds__(SOLVE_THREADS) k_front_backward(const SolveDes
       double acc[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+      // lane reads row pairs (16-byte loads)
       const double* base = d.a + (size_t)(k0 + warp) * ld;
-      for (int r = k0 + kTile + lane; r < d.n; r += 32) {
-        const double xr = xs[r];
+      for (int r = k0 + kTile + 2 * lane; r < d.n; r += 64) {
+        const double x0 = xs[r], x1 = xs[r + 1];
+        double2 v[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] += base[(size_t)(8 * q) * ld + r] * xr;
+        for (int q = 0; q < 8; ++q) v[q] = __ldg(reinterpret_cast<const double2*>(base + (size_t)(8 * q) * ld + r));
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += v[q].x * x0 + v[q].y * x1;
       }
 #pragma unroll
       for (int q = 0; q < 8; ++q) {

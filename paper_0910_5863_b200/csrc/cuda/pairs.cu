@@ -416,9 +416,15 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   extern __shared__ double sm[];
   const size_t np = (size_t)n * (n + 1) / 2;
-  const bool in_smem = (long)np + 6L * n <= smem_cap;
+  // shared-memory placement, most to least: packed L, the 6n vectors, the
+  // inverse-iteration scratch (6n per vector) and the vectors Z (n per vector)
+  const long wk = 7L * n * (k > 0 ? k : 1);
+  const bool in_smem = (long)np + 6L * n + wk <= smem_cap;
+  const bool work_smem = in_smem || 6L * n + wk <= smem_cap;
   double* L = in_smem ? sm : dd.A;  // packed lower
   double* vec = in_smem ? sm + np : sm;  // v, p, d, e, tau, lam (6n)
+  double* wbase = work_smem ? vec + 6 * n : dd.A + (in_smem ? 0 : np);
+  double* Z = wbase + (size_t)6 * n * k;  // k x n eigenvectors of T, then of C
   double* v = vec;
   double* p = vec + n;
   double* dg = vec + 2 * n;
@@ -426,6 +432,7 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
   double* tau = vec + 4 * n;
   double* lam = vec + 5 * n;
   __shared__ double red[32];
+  __shared__ double pg[256];  // column-group partials of A22 v
   if (n == 0 || k == 0) return;
   for (int r = 0; r < n; ++r)
     for (int c = tid; c <= r; c += blockDim.x) L[pk(r, c)] = dd.F4[(size_t)c * N2 + PJ + r];
@@ -452,30 +459,78 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
     }
     __syncthreads();
     if (t == 0.0) continue;
-    // p = t * A22 v
-    for (int r = m0 + tid; r < n; r += blockDim.x) {
-      double s0 = 0.0, s1 = 0.0;
-      const double* row = L + pk(r, 0);
-      int c = m0;
-      for (; c + 1 <= r; c += 2) {
-        s0 += row[c] * v[c];
-        s1 += row[c + 1] * v[c + 1];
+    // p = t * A22 v.  Packed L in global memory: thread per row (sequential
+    // row reads stay in L1 lines).  In shared memory: thread (row, column
+    // group), four column groups reduced in a fixed order.
+    if (!in_smem) {
+      for (int r = m0 + tid; r < n; r += blockDim.x) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        const double* row = L + pk(r, 0);
+        int c = m0;
+        for (; c + 3 <= r; c += 4) {
+          s0 += row[c] * v[c];
+          s1 += row[c + 1] * v[c + 1];
+          s2 += row[c + 2] * v[c + 2];
+          s3 += row[c + 3] * v[c + 3];
+        }
+        for (; c <= r; ++c) s0 += row[c] * v[c];
+        int c2 = r + 1;
+        size_t q = pk(c2, r);  // column r below the diagonal: stride grows by one per row
+        for (; c2 + 3 < n; c2 += 4) {
+          s1 += L[q] * v[c2];
+          s2 += L[q + c2 + 1] * v[c2 + 1];
+          s3 += L[q + 2 * c2 + 3] * v[c2 + 2];
+          s0 += L[q + 3 * c2 + 6] * v[c2 + 3];
+          q += 4 * c2 + 10;
+        }
+        for (; c2 < n; ++c2) {
+          s1 += L[q] * v[c2];
+          q += c2 + 1;
+        }
+        p[r] = t * ((s0 + s1) + (s2 + s3));
       }
-      for (; c <= r; ++c) s0 += row[c] * v[c];
-      for (int c2 = r + 1; c2 < n; ++c2) s1 += L[pk(c2, r)] * v[c2];
-      p[r] = t * (s0 + s1);
+      __syncthreads();
+    } else {
+      const int g = tid >> 6;
+      for (int r0 = m0; r0 < n; r0 += 64) {
+        const int r = r0 + (tid & 63);
+        double s0 = 0.0, s1 = 0.0;
+        if (r < n) {
+          int c = m0 + g;
+          for (; c + 4 < n; c += 8) {
+            s0 += L[c <= r ? pk(r, c) : pk(c, r)] * v[c];
+            s1 += L[c + 4 <= r ? pk(r, c + 4) : pk(c + 4, r)] * v[c + 4];
+          }
+          if (c < n) s0 += L[c <= r ? pk(r, c) : pk(c, r)] * v[c];
+        }
+        pg[g * 64 + (tid & 63)] = s0 + s1;
+        __syncthreads();
+        if (tid < 64 && r < n) p[r] = t * ((pg[tid] + pg[64 + tid]) + (pg[128 + tid] + pg[192 + tid]));
+        __syncthreads();
+      }
     }
-    __syncthreads();
     double pv = 0.0;
     for (int i = m0 + tid; i < n; i += blockDim.x) pv += p[i] * v[i];
     const double K = 0.5 * t * block_sum(pv, red);
     for (int i = m0 + tid; i < n; i += blockDim.x) p[i] -= K * v[i];  // p becomes w
     __syncthreads();
-    for (int r = m0 + tid; r < n; r += blockDim.x) {
+    // rank-2 update of the trailing lower triangle: warp per row, lanes over columns
+    for (int r = m0 + warp; r < n; r += 8) {
       double* row = L + pk(r, 0);
       const double vr = v[r], wr = p[r];
-      for (int c = m0; c <= r; ++c) row[c] -= vr * p[c] + wr * v[c];
+      for (int c = m0 + lane; c <= r; c += 128) {  // four independent elements in flight
+        double x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (c + 32 * q <= r) x[q] = row[c + 32 * q];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int cc = c + 32 * q;
+          if (cc <= r) row[cc] = x[q] - (vr * p[cc] + wr * v[cc]);
+        }
+      }
     }
+    __syncthreads();
     // keep the reflector in the eliminated column (for the back-transformation)
     for (int i = m0 + tid; i < n; i += blockDim.x) L[pk(i, kk)] = v[i];
     __syncthreads();
@@ -528,14 +583,14 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
   // 3. inverse iteration on T (thread m), scratch in global memory
   if (tid < k) {
     const int m = tid;
-    double* work = dd.A + (in_smem ? 0 : np) + (size_t)m * 6 * n;
+    double* work = wbase + (size_t)m * 6 * n;
     double* xd = work;           // U diagonal
     double* xu = work + n;       // U first superdiagonal
     double* xu2 = work + 2 * n;  // U second superdiagonal (row interchanges)
     double* fm = work + 3 * n;   // multipliers
     double* b = work + 4 * n;    // rhs / solution
     double* sw = work + 5 * n;   // 1.0 where rows i, i+1 were interchanged
-    double* z = dd.vecs + (size_t)m * N2;
+    double* z = Z + (size_t)m * n;
     const double shift = lam[m] + 4.0 * 2.2e-16 * tnorm * ((m & 1) ? 1.0 : -1.0);
     const double tiny = 2.2e-16 * tnorm + pivmin;
     // LU of T - shift I with partial pivoting, factored once; the running row
@@ -607,9 +662,9 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
     for (int m = 1; m < k; ++m) {
       int c0 = m;
       while (c0 > 0 && fabs(lam[c0 - 1] - lam[c0]) <= 1e-7 * tnorm) --c0;
-      double* zm = dd.vecs + (size_t)m * N2;
+      double* zm = Z + (size_t)m * n;
       for (int q = c0; q < m; ++q) {
-        const double* zq = dd.vecs + (size_t)q * N2;
+        const double* zq = Z + (size_t)q * n;
         double s = 0.0;
         for (int i = lane; i < n; i += 32) s += zq[i] * zm[i];
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -626,22 +681,44 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
     }
   }
   __syncthreads();
-  // 4. back-transformation (warp per vector), then zero the solve padding
-  for (int m = warp; m < k; m += blockDim.x / 32) {
-    double* y = dd.vecs + (size_t)m * N2;
+  // 4. back-transformation y = H_0 ... H_{n-3} z: warp w carries vectors w and
+  // w + 8 through the reflectors together (their reductions interleave), then
+  // the vectors are written out with the solve padding zeroed
+  for (int m0 = warp; m0 < k; m0 += 16) {
+    const int m1 = m0 + 8;
+    const bool two = m1 < k;
+    double* y0 = Z + (size_t)m0 * n;
+    double* y1 = Z + (size_t)(two ? m1 : m0) * n;
     for (int kk = n - 3; kk >= 0; --kk) {
       const double t = tau[kk];
       if (t == 0.0) continue;
-      double s = 0.0;
-      for (int i = kk + 1 + lane; i < n; i += 32) s += L[pk(i, kk)] * y[i];
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      s *= t;
-      for (int i = kk + 1 + lane; i < n; i += 32) y[i] -= s * L[pk(i, kk)];
+      double s0 = 0.0, s1 = 0.0;
+      for (int i = kk + 1 + lane; i < n; i += 32) {
+        const double h = L[pk(i, kk)];
+        s0 += h * y0[i];
+        s1 += h * y1[i];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      }
+      s0 *= t;
+      s1 *= t;
+      for (int i = kk + 1 + lane; i < n; i += 32) {
+        const double h = L[pk(i, kk)];
+        y0[i] -= s0 * h;
+        if (two) y1[i] -= s1 * h;
+      }
       __syncwarp();
     }
-    for (int i = n + lane; i < N2; i += 32) y[i] = 0.0;
-    if (lane == 0) dd.evals[m] = fmax(lam[m], 0.0);
   }
+  __syncthreads();
+  for (int e = tid; e < k * N2; e += blockDim.x) {
+    const int m = e / N2, i = e % N2;
+    dd.vecs[e] = i < n ? Z[(size_t)m * n + i] : 0.0;
+  }
+  for (int m = tid; m < k; m += blockDim.x) dd.evals[m] = fmax(lam[m], 0.0);
 }
 
 // (l) functional a_m = 1/2 M K alpha_m (alpha = first nj entries of vecs after the back solve)
@@ -859,7 +936,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
       Rv.insert(Rv.end(), h.idx.rho_i.begin(), h.idx.rho_i.end());
       oA[b] = nA;
       // Jacobi: A and V (2 n2^2); tridiagonal path: packed C + 4 n k LU scratch
-      nA += std::max(2LL * n2 * n2, (long long)dm.nj * (dm.nj + 1) / 2 + 6LL * dm.nj * std::max(dm.k, 1)) + 64;
+      nA += std::max(2LL * n2 * n2, (long long)dm.nj * (dm.nj + 1) / 2 + 7LL * dm.nj * std::max(dm.k, 1)) + 64;
       oE[b] = nE;
       nE += std::max(dm.k, 1);
       oW[b] = nW;
@@ -988,12 +1065,14 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
       prof.mark(smem_ok ? "jacobi_smem" : "jacobi_gmem");
     } else {
       const int maxn = maxn2;  // >= every nj
-      const long need = (long)maxn * (maxn + 1) / 2 + 6L * maxn;
-      const long cap = (224 * 1024) / 8 - 32;
+      const long need = (long)maxn * (maxn + 1) / 2 + 6L * maxn + 7L * maxn * std::max(maxk, 1);
+      const long cap = (220 * 1024) / 8;  // leaves room for the kernel's static arrays
       const bool smem_ok = need <= cap;
-      const int ssm = static_cast<int>((smem_ok ? need : 6L * maxn) * 8);
+      // all in shared memory when it fits; otherwise only the 6n vectors, so that
+      // several CTAs share an SM and hide the L2 latency of the packed matrix
+      const long dyn = smem_ok ? need : 6L * maxn;
       CK(cudaFuncSetAttribute(k_syevx, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
-      k_syevx<<<nb, 256, ssm, st_>>>(dpd.p, smem_ok ? static_cast<int>(need) : 0);
+      k_syevx<<<nb, 256, static_cast<int>(dyn * 8), st_>>>(dpd.p, static_cast<int>(dyn));
       prof.mark(smem_ok ? "syevx_smem" : "syevx_gmem");
     }
     CK(cudaGetLastError());
