@@ -84,7 +84,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
     def __exit__(self, *exc):
         if self.proc:
@@ -94,9 +94,22 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
+        """Median SM clock and throttle reasons over the samples taken in
+        [t0, t1] (the timed region); a timed region shorter than a few sampling
+        periods falls back to every loaded sample of the run (warm-up, timed and
+        e2e steps), and `window` says which."""
+        inside = [ln for t, ln in self.lines if t0 is None or t0 <= t <= t1]
+        out = self._summarise(inside)
+        out["window"] = "timed"
+        if out["samples"] < 3:
+            out = self._summarise([ln for _, ln in self.lines])
+            out["window"] = "whole run (timed region shorter than the sampling period)"
+        return out
+
+    def _summarise(self, lines):
         sm, mx, reasons = [], 0.0, set()
-        for ln in self.lines:
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 3:
                 continue
@@ -224,15 +237,20 @@ def main():
         torch.cuda.synchronize()
         return b.step(mode, tau, maxv, base_faces=base_faces, e2e=e2e, u_free=u)
 
+    clk = ClockSampler(local).__enter__()
+    t_wait = time.perf_counter()
+    while not clk.lines and clk.proc is not None and time.perf_counter() - t_wait < 3.0:
+        time.sleep(0.01)  # nvidia-smi start-up: sample from the first step on
     for _ in range(args.warmup):
         do_step()
     barrier(dist, local)
     torch.cuda.synchronize()
     steps = []
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            steps.append(do_step())
+    t_timed0 = time.perf_counter()
+    for _ in range(args.steps):
+        steps.append(do_step())
     torch.cuda.synchronize()
+    t_timed1 = time.perf_counter()
     barrier(dist, local)
     dev_seconds = sum(s["seconds"] for s in steps)
     dev_seconds = max_over_ranks(dist, dev_seconds, "cuda")
@@ -245,6 +263,7 @@ def main():
     barrier(dist, local)
     e2e_steps = [do_step(True, u) for _ in range(args.steps)]
     e2e_sec = max_over_ranks(dist, sum(s["seconds"] for s in e2e_steps), "cuda") / args.steps
+    clk.__exit__(None, None, None)
     if rank != 0:
         return 0
     last = steps[-1]
@@ -283,7 +302,9 @@ def main():
         "e2e": {"value": world * free / e2e_sec, "unit": "DOF/s",
                 "h2d_bytes_per_step": int(e2e_steps[-1]["h2d_bytes"]),
                 "d2h_bytes_per_step": int(e2e_steps[-1]["d2h_bytes"]), "ms_per_step": e2e_sec * 1e3},
-        "clocks": clk.summary(),
+        "clocks": clk.summary(t_timed0, t_timed1),
+        "step_ms": [round(s["seconds"] * 1e3, 3) for s in steps],
+        "e2e_step_ms": [round(s["seconds"] * 1e3, 3) for s in e2e_steps],
         "gpu_launches": int(sum(s["launches"] for s in steps)),
     }
     print(json.dumps(line), flush=True)

@@ -83,7 +83,28 @@ struct XformDesc {      // glob transforms, flat
   const int* perm;
   const int* iperm;
   const double* D;      // r x n row-major per transform (= t_perm rows 0..r-1)
+  const int* cpos;      // per instance (offset inst_pos): cpos[i] = tpos[perm[i]]
+  const int* item_ptr;  // per subdomain: [item_ptr[s], item_ptr[s+1]) constrained rows
+  const int* item_inst; // instance of the item
+  const int* item_row;  // constrained row i < r of the item
+  const int* inst_loff; // per instance: offset of its rows in the subdomain's row results
 };
+
+// T^T v at glob slot j with composite positions (restrict)
+__device__ __forceinline__ double xform_T_t_c(const XformDesc& x, int inst, int j, const double* v) {
+  const int tr = x.inst_tr[inst];
+  const int* cp = x.cpos + x.inst_pos[inst];
+  const int n = x.tr_n[tr], r = x.tr_r[tr];
+  const double* D = x.D + x.tr_off_d[tr];
+  double s0 = j >= r ? v[cp[j]] : 0.0, s1 = 0.0;
+  int i = 0;
+  for (; i + 1 < r; i += 2) {
+    s0 += D[i * n + j] * v[cp[i]];
+    s1 += D[(i + 1) * n + j] * v[cp[i + 1]];
+  }
+  if (i < r) s0 += D[i * n + j] * v[cp[i]];
+  return s0 + s1;
+}
 
 // y = T^T v on the glob blocks of one boundary position b (transform.cpp:94-149)
 __device__ __forceinline__ double xform_T_t(const XformDesc& x, int inst, int j, const double* v) {
@@ -287,22 +308,46 @@ __global__ void __launch_bounds__(256) k_restrict(const SubDesc* sd, XformDesc x
   __syncthreads();
   for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
     const int inst = d.bglob[b];
-    const double y = inst < 0 ? v[b] : xform_T_t(x, inst, d.bslot[b], v);
+    const double y = inst < 0 ? v[b] : xform_T_t_c(x, inst, d.bslot[b], v);
     d.FV[d.posF[b]] = y;
   }
 }
 
 // prolong (bddc_operator.cpp:87-99): WB_s = w_s * T_s x_s   (then summed over copies)
+// The constrained rows of the glob transforms (dot products over the glob) are
+// formed first, one warp per row, into shared memory; every other boundary
+// position is a copy.
 __global__ void __launch_bounds__(256) k_prolong(const SubDesc* sd, XformDesc x, const int* done) {
   if (done && *done) return;
   const SubDesc d = sd[blockIdx.x];
   extern __shared__ double sm[];
   double* xn = sm;
+  double* yrow = sm + d.nB;
   for (int b = threadIdx.x; b < d.nB; b += blockDim.x) xn[b] = d.FV[d.posF[b]];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i0 = x.item_ptr[blockIdx.x], i1 = x.item_ptr[blockIdx.x + 1];
+  for (int it = i0 + warp; it < i1; it += blockDim.x >> 5) {
+    const int inst = x.item_inst[it], i = x.item_row[it];
+    const int tr = x.inst_tr[inst];
+    const int* pos = x.tpos + x.inst_pos[inst];
+    const int n = x.tr_n[tr];
+    const double* D = x.D + x.tr_off_d[tr] + i * n;
+    double s = 0.0;
+    for (int jj = lane; jj < n; jj += 32) s += D[jj] * xn[pos[jj]];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) yrow[x.inst_loff[inst] + i] = s;
+  }
   __syncthreads();
   for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
     const int inst = d.bglob[b];
-    const double xo = inst < 0 ? xn[b] : xform_T(x, inst, d.bslot[b], xn);
+    double xo = xn[b];
+    if (inst >= 0) {
+      const int tr = x.inst_tr[inst];
+      const int i = x.iperm[x.tr_off_perm[tr] + d.bslot[b]];
+      xo = i < x.tr_r[tr] ? yrow[x.inst_loff[inst] + i] : xn[x.tpos[x.inst_pos[inst] + i]];
+    }
     d.WB[b] = d.bw[b] * xo;
   }
 }
@@ -605,6 +650,8 @@ struct DeviceState {
   DBuf<SubDesc> subdesc;
   // transforms
   DBuf<int> inst_tr, inst_pos, tpos, tr_n, tr_r, tr_off_perm, tr_off_d, perm, iperm, cmap;
+  DBuf<int> cpos, item_ptr, item_inst, item_row, inst_loff;
+  int max_rows = 0;  // most constrained transform rows of one subdomain (prolong smem)
   DBuf<double> trD;
   XformDesc xf{};
   // root
@@ -828,6 +875,11 @@ double Engine::upload_inputs() {
 }
 
 void Engine::analysis() {
+  analysis_launch();
+  analysis_finish();
+}
+
+void Engine::analysis_launch() {
   prepare();
   DeviceState& D = *d_;
   const int ns = D.nsub;
@@ -853,6 +905,12 @@ void Engine::analysis() {
   count_launch(3);
   CK(cudaGetLastError());
   CK(cudaEventRecord(D.e1, st));
+}
+
+// waits for analysis_launch's work, checks the pivots
+void Engine::analysis_finish() {
+  DeviceState& D = *d_;
+  const int ns = D.nsub;
   times_.analysis = elapsed(D.e0, D.e1);
   times_.leaf_factor = elapsed(D.ef0, D.ef1);
   std::vector<int> info(ns);
@@ -932,6 +990,33 @@ void Engine::set_constraints(const ConstraintSet& cs) {
         bglob[D.wb_off[s] + b] = inst;
         bslot[D.wb_off[s] + b] = a;
       }
+    }
+  }
+  // composite slot positions and the per-subdomain constrained-row work lists
+  std::vector<int> cpos(tpos.size()), inst_loff(inst_tr.size()), item_ptr(ns + 1, 0), item_inst, item_row;
+  {
+    std::vector<int> inst_sub(inst_tr.size());
+    for (std::size_t k = 0, inst = 0; k < cov.transforms.size(); ++k)
+      for (int s : m.globs[cov.transforms[k].glob].subdomains) inst_sub[inst++] = s;
+    std::vector<std::vector<int>> by_sub(ns);
+    for (std::size_t inst = 0; inst < inst_tr.size(); ++inst) {
+      const int tr = inst_tr[inst];
+      for (int i = 0; i < tr_n[tr]; ++i) cpos[inst_pos[inst] + i] = tpos[inst_pos[inst] + perm[tr_off_perm[tr] + i]];
+      by_sub[inst_sub[inst]].push_back(static_cast<int>(inst));
+    }
+    D.max_rows = 0;
+    for (int s = 0; s < ns; ++s) {
+      int off = 0;
+      for (int inst : by_sub[s]) {
+        inst_loff[inst] = off;
+        for (int i = 0; i < tr_r[inst_tr[inst]]; ++i) {
+          item_inst.push_back(inst);
+          item_row.push_back(i);
+        }
+        off += tr_r[inst_tr[inst]];
+      }
+      item_ptr[s + 1] = static_cast<int>(item_inst.size());
+      D.max_rows = std::max(D.max_rows, off);
     }
   }
   // coarse dofs per subdomain: corners (ascending corner id), then explicit dofs (group order)
@@ -1057,8 +1142,14 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   up_i(D.iperm, iperm);
   up_i(D.cmap, cmap);
   if (trD.empty()) D.trD.alloc(1); else D.trD.upload(trD, st);
+  up_i(D.cpos, cpos);
+  up_i(D.item_ptr, item_ptr);
+  up_i(D.item_inst, item_inst);
+  up_i(D.item_row, item_row);
+  up_i(D.inst_loff, inst_loff);
   D.xf = XformDesc{D.inst_tr.p, D.inst_pos.p, D.tpos.p, D.tr_n.p, D.tr_r.p, D.tr_off_perm.p, D.tr_off_d.p,
-                   D.perm.p, D.iperm.p, D.trD.p};
+                   D.perm.p, D.iperm.p, D.trD.p, D.cpos.p, D.item_ptr.p, D.item_inst.p, D.item_row.p,
+                   D.inst_loff.p};
   D.F.alloc(fo);
   D.F.zero(st);
   D.DinvF.alloc(std::max<long long>(dfo, 1));
@@ -1224,7 +1315,7 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     front_backward(D.fsolve_bwd.p, ns, D.max_NF, st, done);
   }
   mark("leaf_bwd");
-  k_prolong<<<ns, 256, smem_b, st>>>(D.subdesc.p, D.xf, done);
+  k_prolong<<<ns, 256, smem_b + D.max_rows * sizeof(double), st>>>(D.subdesc.p, D.xf, done);
   mark("prolong");
   k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, z, dot_with, partials, done);
   mark("sum_copies");
@@ -1430,15 +1521,24 @@ StepOut Engine::step(const StepSpec& sp, ConstraintSet& cs, double* u_free_host)
   CK(cudaStreamSynchronize(st));
   CK(cudaEventRecord(D.s0, st));
   if (sp.e2e) out.h2d_bytes = upload_inputs();
-  analysis();
+  // the leaf factorization runs on the device while the host builds the base
+  // constraints and prepares the face-pair problems
+  analysis_launch();
   cs = arithmetic_constraints(m_, sp.edges, sp.faces);
-  if (sp.adaptive || sp.fixed_count >= 0) {
-    EnrichOptions o;
-    o.tau = sp.tau;
-    o.max_vectors = sp.max_vectors;
-    o.keep_edge_constraints = sp.keep_edge;
-    o.fixed_count = sp.fixed_count;
-    out.omega_tilde = enrich(cs, o).omega_tilde;
+  EnrichOptions o;
+  o.tau = sp.tau;
+  o.max_vectors = sp.max_vectors;
+  o.keep_edge_constraints = sp.keep_edge;
+  o.fixed_count = sp.fixed_count;
+  const bool adaptive = sp.adaptive || sp.fixed_count >= 0;
+  std::shared_ptr<PairPrep> prep;
+  if (adaptive) prep = D.pairs.prepare(cs, o);
+  analysis_finish();
+  if (adaptive) {
+    CK(cudaEventRecord(D.e0, st));
+    out.omega_tilde = D.pairs.enrich(cs, o, prep).omega_tilde;
+    CK(cudaEventRecord(D.e1, st));
+    times_.eigen = elapsed(D.e0, D.e1);
   }
   out.constraint_rows = cs.row_count(m_);
   set_constraints(cs);

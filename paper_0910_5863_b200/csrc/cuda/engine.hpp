@@ -93,6 +93,8 @@ class Engine {
   void prepare();              // host staging + device allocation + first upload
   double upload_inputs();      // host->device copies of the inputs; returns bytes
   void analysis();
+  void analysis_launch();  // enqueue only
+  void analysis_finish();  // wait + pivot checks
   void set_constraints(const ConstraintSet& cs);
   StepOut step(const StepSpec& spec, ConstraintSet& cs, double* u_free_host);
   void recover_device(const double* d_uiface, double* d_ufree);

@@ -747,7 +747,7 @@ void PairEngine::attach(const Model& m, const double* S, const std::vector<long 
   st_ = st;
 }
 
-namespace {
+namespace detail {
 struct HostPair {
   PairIndex idx;
   std::vector<int> pos[2];   // [outer | corner | shared] boundary positions per side
@@ -759,6 +759,21 @@ struct HostPair {
   int nj = 0, nm = 0, r_total = 0;    // r_total = admissible columns - nullity
 };
 
+}  // namespace detail
+using detail::HostPair;
+
+// Host preparation of the face-pair eigenproblems: depends on the model and the
+// base constraint set only, so Engine::step runs it while the leaf
+// factorization is on the device.
+struct PairPrep {
+  ConstraintSet base;
+  std::vector<std::pair<int, int>> pairs;
+  std::vector<HostPair> hp;
+  int request = 0;
+  double prep_ms = 0.0;
+};
+
+namespace {
 int count_above(const std::vector<double>& v, double tau) {
   int k = 0;
   while (k < static_cast<int>(v.size()) && v[k] > tau) ++k;
@@ -766,16 +781,20 @@ int count_above(const std::vector<double>& v, double tau) {
 }
 }  // namespace
 
-EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
+std::shared_ptr<PairPrep> PairEngine::prepare(const ConstraintSet& cs, const EnrichOptions& o) const {
   using clk = std::chrono::steady_clock;
   const auto h0 = clk::now();
+  auto prep = std::make_shared<PairPrep>();
   const Model& m = *m_;
-  const ConstraintSet base = cs;  // adaptive.cpp:133: every pair sees the same base
+  prep->base = cs;  // adaptive.cpp:133: every pair sees the same base
+  const ConstraintSet& base = prep->base;
   const auto bg = base.by_glob(m.globs.size());
-  const int request = o.indicator_only ? 1 : (o.fixed_count >= 0 ? o.fixed_count : o.max_vectors) + 1;
-  const auto pairs = face_pairs(m);
+  prep->request = o.indicator_only ? 1 : (o.fixed_count >= 0 ? o.fixed_count : o.max_vectors) + 1;
+  prep->pairs = face_pairs(m);
+  const auto& pairs = prep->pairs;
   const int np = static_cast<int>(pairs.size());
-  std::vector<HostPair> hp(np);
+  prep->hp.resize(np);
+  std::vector<HostPair>& hp = prep->hp;
   // boundary position of each local dof, per subdomain
   std::vector<std::vector<int>> bpos(m.subs.size());
   for (std::size_t s = 0; s < m.subs.size(); ++s) {
@@ -847,7 +866,19 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
     h.r_total = n_adm - h.nm;
     (void)m1;
   }
+  prep->prep_ms = std::chrono::duration<double, std::milli>(clk::now() - h0).count();
+  return prep;
+}
+
+EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std::shared_ptr<PairPrep> prep) {
+  using clk = std::chrono::steady_clock;
+  const bool overlapped = prep != nullptr;
+  if (!prep) prep = prepare(cs, o);
   const auto h1 = clk::now();
+  const Model& m = *m_;
+  const std::vector<HostPair>& hp = prep->hp;
+  const int np = static_cast<int>(hp.size());
+  const int request = prep->request;
   // device buffers, processed in chunks bounded by a memory budget
   EnrichOutcome out;
   std::vector<std::vector<double>> all_evals(np), all_funcs(np);
@@ -1172,8 +1203,8 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
   const char* prof_env = std::getenv("BDDC_B200_PROFILE");
   if (prof_env && *prof_env && *prof_env != '0') {
     const auto h3 = clk::now();
-    std::fprintf(stderr, "[profile] enrich host: pairs=%d prep=%.3fms device+copy=%.3fms select=%.3fms\n", np,
-                 std::chrono::duration<double, std::milli>(h1 - h0).count(),
+    std::fprintf(stderr, "[profile] enrich host: pairs=%d prep=%.3fms%s device+copy=%.3fms select=%.3fms\n", np,
+                 prep->prep_ms, overlapped ? " (overlapped)" : "",
                  std::chrono::duration<double, std::milli>(h2 - h1).count(),
                  std::chrono::duration<double, std::milli>(h3 - h2).count());
   }

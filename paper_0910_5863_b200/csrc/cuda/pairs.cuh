@@ -14,6 +14,7 @@ struct EnrichOptions;
 struct EnrichOutcome;
 
 struct PairBuffers;
+struct PairPrep;
 
 class PairEngine {
  public:
@@ -21,7 +22,10 @@ class PairEngine {
   ~PairEngine();
   void attach(const Model& m, const double* S, const std::vector<long long>& s_off,
               const std::vector<int>& PB, const std::vector<int>& nB, cudaStream_t st);
-  EnrichOutcome enrich(ConstraintSet& cs, const EnrichOptions& o);
+  /// Host-side preparation (pair index spaces, kernel bases, rigid modes); no
+  /// device work, so it can run while the device is busy.
+  std::shared_ptr<PairPrep> prepare(const ConstraintSet& cs, const EnrichOptions& o) const;
+  EnrichOutcome enrich(ConstraintSet& cs, const EnrichOptions& o, std::shared_ptr<PairPrep> prep = nullptr);
 
  private:
   const Model* m_ = nullptr;
