@@ -85,10 +85,6 @@ __device__ __forceinline__ void for_acc(double (&acc)[2][4][4], F f) {
 // otherwise the product over [kb, ke) is stored to out (64x64, ld 64).
 __device__ void tile_update_range(double* a, int ld, int i0, int j0, int kb, int ke, double* out);
 
-__device__ void tile_update(double* a, int ld, int i0, int j0, int K) {
-  tile_update_range(a, ld, i0, j0, 0, K, nullptr);
-}
-
 __device__ void tile_update_range(double* a, int ld, int i0, int j0, int kb, int ke, double* out) {
   const int K = ke - kb;
   a += (size_t)kb * ld;  // column offset of the K range
@@ -134,6 +130,9 @@ __device__ void tile_update_range(double* a, int ld, int i0, int j0, int kb, int
   }
 }
 
+// First K column with a nonzero factor entry in tile row i0 (see FrontDesc::aug).
+__device__ __forceinline__ int aug_k0(const FrontDesc& d, int i0) { return d.aug && i0 >= d.aug ? i0 - d.aug : 0; }
+
 // Split-K column update for fronts with little tile parallelism (single large
 // root): CTA (t, b, s) forms the partial product of tile (j + t, j) over the
 // K slice s into a workspace; k_splitk_reduce subtracts the slices in a fixed
@@ -143,9 +142,10 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_syrk_column_splitk(const Front
   const FrontDesc d = ds[blockIdx.y];
   const int i = j + blockIdx.x;
   if (j * kTile >= d.p || i * kTile >= d.n) return;
-  const int K = j * kTile;
+  const int K0 = aug_k0(d, i * kTile), K1 = j * kTile;  // K0 > K1: zero tile
+  const int K = max(K1 - K0, 0);
   const int chunk = ((K / nsplit + KC - 1) / KC) * KC;
-  const int kb = blockIdx.z * chunk, ke = min(K, kb + chunk);
+  const int kb = K0 + blockIdx.z * chunk, ke = min(K1, kb + chunk);
   double* out = work + (((size_t)blockIdx.y * tiles + blockIdx.x) * nsplit + blockIdx.z) * 64 * 64;
   if (kb >= ke) {
     for (int e = threadIdx.x; e < 64 * 64; e += GEMM_THREADS) out[e] = 0.0;
@@ -171,7 +171,9 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_syrk_column(const FrontDesc* d
   const FrontDesc d = ds[blockIdx.y];
   const int i = j + blockIdx.x;
   if (j * kTile >= d.p || i * kTile >= d.n) return;
-  tile_update(d.a, d.n, i * kTile, j * kTile, j * kTile);
+  const int k0 = aug_k0(d, i * kTile);
+  if (k0 > j * kTile) return;  // zero tile of the augmented block
+  tile_update_range(d.a, d.n, i * kTile, j * kTile, k0, j * kTile, nullptr);
 }
 
 __global__ void __launch_bounds__(GEMM_THREADS) k_syrk_trailing(const FrontDesc* ds) {
@@ -183,7 +185,8 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_syrk_trailing(const FrontDesc*
   while ((long)ii * (ii + 1) / 2 > t) --ii;
   while ((long)(ii + 1) * (ii + 2) / 2 <= t) ++ii;
   const int jj = static_cast<int>(t - (long)ii * (ii + 1) / 2);
-  tile_update(d.a, d.n, (pt + ii) * kTile, (pt + jj) * kTile, d.p);
+  tile_update_range(d.a, d.n, (pt + ii) * kTile, (pt + jj) * kTile, min(aug_k0(d, (pt + ii) * kTile), d.p), d.p,
+                    nullptr);
 }
 
 // Panel step (one CTA per front): L_jj = chol(C_jj) and Dinv_j = L_jj^{-1}.
@@ -345,6 +348,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_trsm(const FrontDesc* ds, int 
   const FrontDesc d = ds[blockIdx.y];
   const int i = j + 1 + blockIdx.x;
   if (j * kTile >= d.p || i * kTile >= d.n) return;
+  if (aug_k0(d, i * kTile) > j * kTile) return;  // zero tile of the augmented block
   extern __shared__ __align__(16) double smem[];
   double* V = smem;
   double* C = smem + 64 * LDS;

@@ -27,7 +27,11 @@ struct FrontDesc {
   int n;          // padded dimension (multiple of 64)
   int p;          // eliminated columns (multiple of 64, <= n)
   int* info;      // 0, or 1 + first failing pivot column
-  int pad_;
+  // 0, or the first row (multiple of 64, >= p) of an identity-augmented block:
+  // rows aug + q hold e_q in the eliminated columns (fronts [[A, .], [I, 0]]).
+  // Their factor rows are L^{-T} (upper triangular), so augmented tile (a, k)
+  // is zero for a > k and the updates skip those tiles and K ranges.
+  int aug;
 };
 
 struct SolveDesc {

@@ -1171,7 +1171,8 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     sd[s] = SubDesc{D.S.p + D.s_off[s], D.F.p + D.f_off[s], D.FV.p + D.fv_off[s], D.biface.p + D.wb_off[s],
                     D.bw.p + D.wb_off[s], D.bposF.p + D.wb_off[s], D.bglob.p + D.wb_off[s],
                     D.bslot.p + D.wb_off[s], D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], D.NF[s], D.PE[s], D.NA[s]};
-    fd[s] = FrontDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.NA[s], D.PE[s], D.finfo.p + s, 0};
+    fd[s] = FrontDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.NA[s], D.PE[s], D.finfo.p + s,
+                      D.leaf_explicit ? D.NF[s] : 0};
     fw[s] = SolveDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.FV.p + D.fv_off[s], D.NF[s], D.PE[s],
                       nullptr, nullptr};
   }
@@ -1237,7 +1238,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   RootAsm ra{D.root_ptr.p, D.root_sub.p, D.root_c.p, D.d_foff.p, D.d_NF.p, D.d_PE.p};
   k_root_assemble<<<1024, 256, 0, st>>>(D.n_root, D.NR, ldR, ra, D.F.p, D.R.p);
   count_launch(1);
-  std::vector<FrontDesc> rf{FrontDesc{D.R.p, D.DinvR.p, static_cast<int>(ldR), D.NR, D.rinfo.p, 0}};
+  std::vector<FrontDesc> rf{FrontDesc{D.R.p, D.DinvR.p, static_cast<int>(ldR), D.NR, D.rinfo.p, D.root_inv ? D.NR : 0}};
   D.rfront.upload(rf, st);
   prof.mark("root_asm");
   partial_cholesky(D.rfront.p, 1, static_cast<int>(ldR), D.NR, D.root_inv ? D.NR : 0, st);
