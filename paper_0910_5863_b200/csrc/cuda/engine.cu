@@ -957,41 +957,59 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   ht.mark("change_of_variables");
   // boundary position of each local dof
   std::vector<std::vector<int>> bpos_of(ns);
+#pragma omp parallel for schedule(dynamic, 4)
   for (int s = 0; s < ns; ++s) {
     bpos_of[s].assign(m.subs[s].dim(), -1);
     for (int b = 0; b < D.nB[s]; ++b) bpos_of[s][m.subs[s].boundary[b]] = b;
   }
+  ht.mark("bpos");
   // transforms (flat) and per-subdomain instances
-  std::vector<int> tr_n, tr_r, tr_off_perm, tr_off_d, perm, iperm, inst_tr, inst_pos, tpos;
-  std::vector<double> trD;
-  std::vector<long long> wbo(D.wb_off);
+  // sizes and offsets first (sequential, cheap), then the fill in parallel
+  const int ntr = static_cast<int>(cov.transforms.size());
+  std::vector<int> tr_n(ntr), tr_r(ntr), tr_off_perm(ntr), tr_off_d(ntr), tr_inst0(ntr + 1, 0);
+  std::vector<int> inst_tr, inst_pos;
+  int np_total = 0, nd_total = 0, ntpos = 0;
+  for (int k = 0; k < ntr; ++k) {
+    const GlobTransform& gt = cov.transforms[k];
+    tr_n[k] = gt.n;
+    tr_r[k] = gt.rank;
+    tr_off_perm[k] = np_total;
+    tr_off_d[k] = nd_total;
+    np_total += gt.n;
+    nd_total += gt.rank * gt.n;
+    tr_inst0[k + 1] = tr_inst0[k] + static_cast<int>(m.globs[gt.glob].subdomains.size());
+    for (std::size_t q = 0; q < m.globs[gt.glob].subdomains.size(); ++q) {
+      inst_tr.push_back(k);
+      inst_pos.push_back(ntpos);
+      ntpos += gt.n;
+    }
+  }
+  std::vector<int> perm(np_total), iperm(np_total), tpos(ntpos);
+  std::vector<double> trD(nd_total);
   std::vector<int> bglob(D.WB.n, -1), bslot(D.WB.n, -1);
-  for (std::size_t k = 0; k < cov.transforms.size(); ++k) {
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int k = 0; k < ntr; ++k) {
     const GlobTransform& gt = cov.transforms[k];
     const int n = gt.n, r = gt.rank;
-    tr_n.push_back(n);
-    tr_r.push_back(r);
-    tr_off_perm.push_back(static_cast<int>(perm.size()));
-    tr_off_d.push_back(static_cast<int>(trD.size()));
-    std::vector<int> ip(n);
-    for (int i = 0; i < n; ++i) ip[gt.perm[i]] = i;
-    perm.insert(perm.end(), gt.perm.begin(), gt.perm.end());
-    iperm.insert(iperm.end(), ip.begin(), ip.end());
+    for (int i = 0; i < n; ++i) {
+      perm[tr_off_perm[k] + i] = gt.perm[i];
+      iperm[tr_off_perm[k] + gt.perm[i]] = i;
+    }
     for (int i = 0; i < r; ++i)  // D[i][j] = t_perm[i][j] = t[perm[i]][j]
-      for (int j = 0; j < n; ++j) trD.push_back(gt.D[std::size_t(i) * n + j]);
+      for (int j = 0; j < n; ++j) trD[tr_off_d[k] + std::size_t(i) * n + j] = gt.D[std::size_t(i) * n + j];
     const auto& dofs = m.glob_dofs[gt.glob];
+    int inst = tr_inst0[k];
     for (int s : m.globs[gt.glob].subdomains) {
-      const int inst = static_cast<int>(inst_tr.size());
-      inst_tr.push_back(static_cast<int>(k));
-      inst_pos.push_back(static_cast<int>(tpos.size()));
       for (int a = 0; a < n; ++a) {
         const int b = bpos_of[s][m.maps.local_of(dofs[a], s)];
-        tpos.push_back(b);
+        tpos[inst_pos[inst] + a] = b;
         bglob[D.wb_off[s] + b] = inst;
         bslot[D.wb_off[s] + b] = a;
       }
+      ++inst;
     }
   }
+  ht.mark("transforms");
   // composite slot positions and the per-subdomain constrained-row work lists
   std::vector<int> cpos(tpos.size()), inst_loff(inst_tr.size()), item_ptr(ns + 1, 0), item_inst, item_row;
   {
@@ -1019,9 +1037,11 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       D.max_rows = std::max(D.max_rows, off);
     }
   }
+  ht.mark("items");
   // coarse dofs per subdomain: corners (ascending corner id), then explicit dofs (group order)
   std::vector<std::vector<int>> coarse_b(ns), coarse_root(ns);
   const i64 ncd = m.maps.corner_dof_count;
+#pragma omp parallel for schedule(dynamic, 4)
   for (int s = 0; s < ns; ++s) {
     const Subdomain& S = m.subs[s];
     std::vector<std::pair<i64, int>> cors;
@@ -1043,6 +1063,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     }
   D.n_root = static_cast<int>(ncd + cov.groups.size());
   D.NR = rup(std::max(D.n_root, 1), kTile);
+  ht.mark("coarse");
   // F layout
   D.NF.assign(ns, 0);
   D.PE.assign(ns, 0);
@@ -1107,6 +1128,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     for (int c = 0; c < nC; ++c) ++root_cnt[coarse_root[s][c] + 1];
   }
   pad_off[ns] = pads.size();
+  ht.mark("f_layout");
   // root CSR (entries ascending by subdomain)
   std::vector<int> rptr(D.n_root + 1, 0);
   for (int k = 0; k < D.n_root; ++k) rptr[k + 1] = rptr[k] + root_cnt[k + 1];

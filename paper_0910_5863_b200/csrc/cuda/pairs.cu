@@ -1144,10 +1144,20 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     p0 = p1;
   }
   const auto h2 = clk::now();
-  // host selection, splitting and rank filter (adaptive.cpp:66-125)
+  // host selection, splitting and rank filter (adaptive.cpp:66-125).  The
+  // candidate averages are enumerated in the sequential order; whether one is
+  // kept depends only on the earlier ones of its glob, so the rank tests run per
+  // glob in parallel and the kept averages are appended in the original order.
+  struct Cand {
+    int p, glob;
+    std::vector<double> w;
+    char ok;
+  };
+  std::vector<Cand> cands;
+  std::vector<PairReport> reps(np);
   for (int p = 0; p < np; ++p) {
     const HostPair& h = hp[p];
-    PairReport rep;
+    PairReport& rep = reps[p];
     rep.si = h.idx.si;
     rep.sj = h.idx.sj;
     rep.eigenvalues = all_evals[p];
@@ -1182,23 +1192,48 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
             if (std::abs(piece[t]) > std::abs(piece[top])) top = t;
           const double div = piece[top] < 0 ? -pn : pn;
           for (double& v : piece) v /= div;
-          Average av;
-          av.glob = g;
-          av.weights = std::move(piece);
-          av.adaptive = 1;
-          if (add_average(cs, std::move(av)))
-            ++rep.kept;
-          else
-            ++rep.dropped;
+          cands.push_back(Cand{p, g, std::move(piece), 0});
         }
       }
     } else {
       rep.omega_next = L > 0 ? lam[0] : 0.0;
     }
-    out.omega_tilde = std::max(out.omega_tilde, rep.omega_next);
-    out.kept += rep.kept;
-    out.dropped += rep.dropped;
-    out.pairs.push_back(std::move(rep));
+  }
+  {
+    std::vector<std::vector<int>> by_g(m.globs.size());
+    for (std::size_t c = 0; c < cands.size(); ++c) by_g[cands[c].glob].push_back(static_cast<int>(c));
+    const auto existing_idx = cs.by_glob(m.globs.size());
+    std::vector<int> glist;
+    for (std::size_t g = 0; g < by_g.size(); ++g)
+      if (!by_g[g].empty()) glist.push_back(static_cast<int>(g));
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int q = 0; q < static_cast<int>(glist.size()); ++q) {
+      const int g = glist[q];
+      std::vector<const std::vector<double>*> ex;
+      for (int a : existing_idx[g]) ex.push_back(&cs.averages[a].weights);
+      for (int c : by_g[g]) {
+        cands[c].ok = average_admissible(ex, cands[c].w) ? 1 : 0;
+        if (cands[c].ok) ex.push_back(&cands[c].w);
+      }
+    }
+  }
+  for (Cand& c : cands) {
+    if (c.ok) {
+      Average av;
+      av.glob = c.glob;
+      av.weights = std::move(c.w);
+      av.adaptive = 1;
+      cs.averages.push_back(std::move(av));
+      ++reps[c.p].kept;
+    } else {
+      ++reps[c.p].dropped;
+    }
+  }
+  for (int p = 0; p < np; ++p) {
+    out.omega_tilde = std::max(out.omega_tilde, reps[p].omega_next);
+    out.kept += reps[p].kept;
+    out.dropped += reps[p].dropped;
+    out.pairs.push_back(std::move(reps[p]));
   }
   const char* prof_env = std::getenv("BDDC_B200_PROFILE");
   if (prof_env && *prof_env && *prof_env != '0') {

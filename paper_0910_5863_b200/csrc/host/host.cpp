@@ -864,23 +864,28 @@ ConstraintSet arithmetic_constraints(const Model& md, bool edges, bool faces) {
   return cs;
 }
 
-bool add_average(ConstraintSet& cs, Average avg) {
+bool average_admissible(const std::vector<const std::vector<double>*>& existing, const std::vector<double>& w) {
   bool nz = false;
-  for (double w : avg.weights) nz |= (w != 0.0);
+  for (double x : w) nz |= (x != 0.0);
   if (!nz) return false;
-  std::vector<const std::vector<double>*> existing;
-  for (const auto& a : cs.averages)
-    if (a.glob == avg.glob) existing.push_back(&a.weights);
   if (!existing.empty()) {
-    const int m = static_cast<int>(avg.weights.size());
+    const int m = static_cast<int>(w.size());
     const int n = static_cast<int>(existing.size()) + 1;
     std::vector<double> stack(std::size_t(m) * n);
     for (int i = 0; i < m; ++i) {
       for (int c = 0; c + 1 < n; ++c) stack[std::size_t(i) * n + c] = (*existing[c])[i];
-      stack[std::size_t(i) * n + n - 1] = avg.weights[i];
+      stack[std::size_t(i) * n + n - 1] = w[i];
     }
     if (pivoted_qr(stack, m, n, 1e-8, false).rank <= n - 1) return false;
   }
+  return true;
+}
+
+bool add_average(ConstraintSet& cs, Average avg) {
+  std::vector<const std::vector<double>*> existing;
+  for (const auto& a : cs.averages)
+    if (a.glob == avg.glob) existing.push_back(&a.weights);
+  if (!average_admissible(existing, avg.weights)) return false;
   cs.averages.push_back(std::move(avg));
   return true;
 }

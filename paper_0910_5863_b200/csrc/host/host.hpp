@@ -197,6 +197,9 @@ struct ConstraintSet {
 };
 ConstraintSet arithmetic_constraints(const Model& m, bool edges, bool faces);  // :34-59
 bool add_average(ConstraintSet& cs, Average avg);                              // :61-76
+/// The rank test of add_average: `w` is nonzero and independent of `existing`
+/// (same glob); pivoted QR, tolerance 1e-8 (constraints.cpp:61-76).
+bool average_admissible(const std::vector<const std::vector<double>*>& existing, const std::vector<double>& w);
 GlobTransform build_glob_transform(int glob, const std::vector<double>& rows, int r_in,
                                    int n);  // transform.cpp:51-90
 /// Kernel basis of a glob's averages, n x (n-rank) row-major (pair.cpp:167-188).
