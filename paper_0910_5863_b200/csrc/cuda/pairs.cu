@@ -759,8 +759,21 @@ struct HostPair {
   int nj = 0, nm = 0, r_total = 0;    // r_total = admissible columns - nullity
 };
 
+struct Dims { int no[2], PO[2], NG[2], nc, nf, nj, PQ, PJ, k, nm; };
+struct ChunkHost {
+  int p0 = 0, p1 = 0;
+  std::vector<Dims> dims;
+  std::vector<int> posv, krv;
+  std::vector<int4> kcv;
+  std::vector<double> kvv, Nv, Rv;
+  std::vector<long long> oG, oQ, oF3, oF4, oM, oKC, oKR, oKV, oH, oN, oR, oA, oE, oW, oFu, oDG, oDQ, oD3, oD4, oP;
+  long long nG = 0, nQ = 0, nF = 0, nM = 0, nH = 0, nA = 0, nE = 0, nW = 0, nFu = 0, nD = 0;
+};
+ChunkHost build_chunk(const std::vector<HostPair>& hp, int p0, int request);
 }  // namespace detail
 using detail::HostPair;
+using detail::ChunkHost;
+using detail::Dims;
 
 // Host preparation of the face-pair eigenproblems: depends on the model and the
 // base constraint set only, so Engine::step runs it while the leaf
@@ -769,6 +782,7 @@ struct PairPrep {
   ConstraintSet base;
   std::vector<std::pair<int, int>> pairs;
   std::vector<HostPair> hp;
+  std::vector<ChunkHost> chunks;
   int request = 0;
   double prep_ms = 0.0;
 };
@@ -780,6 +794,108 @@ int count_above(const std::vector<double>& v, double tau) {
   return k;
 }
 }  // namespace
+
+namespace detail {
+// One chunk of pair problems (bounded by a device-memory budget): dimensions,
+// arena offsets and the concatenated host inputs, built in PairEngine::prepare.
+ChunkHost build_chunk(const std::vector<HostPair>& hp, int p0, int request) {
+  const int np = static_cast<int>(hp.size());
+  const double budget = 24e9;  // bytes of pair fronts per chunk
+  ChunkHost ch;
+  ch.p0 = p0;
+  long long& nG = ch.nG; long long& nQ = ch.nQ; long long& nF = ch.nF; long long& nM = ch.nM;
+  long long& nH = ch.nH; long long& nA = ch.nA; long long& nE = ch.nE; long long& nW = ch.nW;
+  long long& nFu = ch.nFu; long long& nD = ch.nD;
+  int p1 = p0;
+  double bytes = 0;
+  std::vector<Dims>& dims = ch.dims;
+  while (p1 < np) {
+    const HostPair& h = hp[p1];
+    Dims dm{};
+    dm.nc = static_cast<int>(h.idx.corner_globals.size());
+    dm.nf = static_cast<int>(h.idx.noncorner_globals.size());
+    dm.nj = h.nj;
+    dm.nm = h.nm;
+    const int m1 = dm.nc + dm.nf;
+    for (int side = 0; side < 2; ++side) {
+      dm.no[side] = static_cast<int>((side == 0 ? h.idx.outer_i : h.idx.outer_j).size());
+      dm.PO[side] = rup(dm.no[side], kTile);
+      dm.NG[side] = dm.PO[side] + rup(std::max(m1, 1), kTile);
+    }
+    dm.PQ = rup(std::max(m1, 1), kTile);
+    dm.PJ = rup(std::max(dm.nj, 1), kTile);
+    dm.k = std::min(request, std::min(h.nj, std::max(h.r_total, 0)));
+    dm.k = std::min(dm.k, 64);
+    const double b = 8.0 * (double(dm.NG[0]) * dm.NG[0] + double(dm.NG[1]) * dm.NG[1] +
+                            double(dm.PQ + dm.PJ) * (dm.PQ + dm.PJ) + 8.0 * dm.PJ * dm.PJ);
+    if (p1 > p0 && bytes + b > budget) break;
+    bytes += b;
+    dims.push_back(dm);
+    ++p1;
+  }
+  ch.p1 = p1;
+  const int nb = p1 - p0;
+  auto& posv = ch.posv; auto& krv = ch.krv; auto& kcv = ch.kcv;
+  auto& kvv = ch.kvv; auto& Nv = ch.Nv; auto& Rv = ch.Rv;
+  auto sized = [](std::vector<long long>& v, int n) -> std::vector<long long>& { v.assign(n, 0); return v; };
+  auto& oG = sized(ch.oG, 2 * nb); auto& oQ = sized(ch.oQ, nb); auto& oF3 = sized(ch.oF3, nb);
+  auto& oF4 = sized(ch.oF4, nb); auto& oM = sized(ch.oM, nb); auto& oKC = sized(ch.oKC, nb);
+  auto& oKR = sized(ch.oKR, nb); auto& oKV = sized(ch.oKV, nb); auto& oH = sized(ch.oH, nb);
+  auto& oN = sized(ch.oN, nb); auto& oR = sized(ch.oR, nb); auto& oA = sized(ch.oA, nb);
+  auto& oE = sized(ch.oE, nb); auto& oW = sized(ch.oW, nb); auto& oFu = sized(ch.oFu, nb);
+  auto& oDG = sized(ch.oDG, 2 * nb); auto& oDQ = sized(ch.oDQ, nb); auto& oD3 = sized(ch.oD3, nb);
+  auto& oD4 = sized(ch.oD4, nb); auto& oP = sized(ch.oP, 2 * nb);
+  for (int b = 0; b < nb; ++b) {
+    const Dims& dm = dims[b];
+    const HostPair& h = hp[p0 + b];
+    for (int side = 0; side < 2; ++side) {
+      oG[2 * b + side] = nG;
+      nG += (long long)dm.NG[side] * dm.NG[side];
+      oDG[2 * b + side] = nD;
+      nD += (long long)(dm.PO[side] / kTile) * kTile * kTile;
+      oP[2 * b + side] = posv.size();
+      posv.insert(posv.end(), h.pos[side].begin(), h.pos[side].end());
+    }
+    const int NQ = dm.PQ + dm.PJ, N2 = 2 * dm.PJ, n2 = dm.nj + (dm.nj & 1);
+    oQ[b] = nQ;
+    nQ += (long long)NQ * NQ;
+    oDQ[b] = nD;
+    nD += (long long)(dm.PQ / kTile) * kTile * kTile;
+    oF3[b] = nF;
+    nF += (long long)N2 * N2;
+    oF4[b] = nF;
+    nF += (long long)N2 * N2;
+    oD3[b] = nD;
+    nD += (long long)(dm.PJ / kTile) * kTile * kTile;
+    oD4[b] = nD;
+    nD += (long long)(dm.PJ / kTile) * kTile * kTile;
+    oM[b] = nM;
+    nM += (long long)dm.nf * dm.nf;
+    oKC[b] = kcv.size();
+    kcv.insert(kcv.end(), h.kc.begin(), h.kc.end());
+    oKR[b] = krv.size();
+    krv.insert(krv.end(), h.krows.begin(), h.krows.end());
+    oKV[b] = kvv.size();
+    kvv.insert(kvv.end(), h.kvals.begin(), h.kvals.end());
+    oH[b] = nH;
+    nH += (long long)dm.nf * std::max(dm.nj, 1);
+    oN[b] = Nv.size();
+    Nv.insert(Nv.end(), h.N.begin(), h.N.end());
+    oR[b] = Rv.size();
+    Rv.insert(Rv.end(), h.idx.rho_i.begin(), h.idx.rho_i.end());
+    oA[b] = nA;
+    // Jacobi: A and V (2 n2^2); tridiagonal path: packed C + 4 n k LU scratch
+    nA += std::max(2LL * n2 * n2, (long long)dm.nj * (dm.nj + 1) / 2 + 7LL * dm.nj * std::max(dm.k, 1)) + 64;
+    oE[b] = nE;
+    nE += std::max(dm.k, 1);
+    oW[b] = nW;
+    nW += (long long)N2 * std::max(dm.k, 1);
+    oFu[b] = nFu;
+    nFu += (long long)dm.nf * std::max(dm.k, 1);
+  }
+  return ch;
+}
+}  // namespace detail
 
 std::shared_ptr<PairPrep> PairEngine::prepare(const ConstraintSet& cs, const EnrichOptions& o) const {
   using clk = std::chrono::steady_clock;
@@ -866,6 +982,10 @@ std::shared_ptr<PairPrep> PairEngine::prepare(const ConstraintSet& cs, const Enr
     h.r_total = n_adm - h.nm;
     (void)m1;
   }
+  for (int p0 = 0; p0 < np;) {
+    prep->chunks.push_back(detail::build_chunk(hp, p0, prep->request));
+    p0 = prep->chunks.back().p1;
+  }
   prep->prep_ms = std::chrono::duration<double, std::milli>(clk::now() - h0).count();
   return prep;
 }
@@ -883,98 +1003,24 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
   EnrichOutcome out;
   std::vector<std::vector<double>> all_evals(np), all_funcs(np);
   std::vector<int> all_k(np);
-  const double budget = 24e9;  // bytes of pair fronts per chunk
   int p0 = 0;
+  std::size_t chunk_id = 0;
   while (p0 < np) {
-    // choose chunk
-    std::vector<PairDev> pd;
-    std::vector<long long> offG0, offG1, offQ, offF3, offF4, offM, offK, offH, offN, offR, offA, offV, offE, offW, offFu,
-        offD0, offD1, offDQ, offD3, offD4, offP0, offP1;
-    long long nG = 0, nQ = 0, nF = 0, nM = 0, nK = 0, nH = 0, nN = 0, nR = 0, nA = 0, nE = 0, nW = 0, nFu = 0, nD = 0,
-              nP = 0;
-    int p1 = p0;
-    double bytes = 0;
-    struct Dims { int no[2], PO[2], NG[2], nc, nf, nj, PQ, PJ, k, nm; };
-    std::vector<Dims> dims;
-    while (p1 < np) {
-      const HostPair& h = hp[p1];
-      Dims dm{};
-      dm.nc = static_cast<int>(h.idx.corner_globals.size());
-      dm.nf = static_cast<int>(h.idx.noncorner_globals.size());
-      dm.nj = h.nj;
-      dm.nm = h.nm;
-      const int m1 = dm.nc + dm.nf;
-      for (int side = 0; side < 2; ++side) {
-        dm.no[side] = static_cast<int>((side == 0 ? h.idx.outer_i : h.idx.outer_j).size());
-        dm.PO[side] = rup(dm.no[side], kTile);
-        dm.NG[side] = dm.PO[side] + rup(std::max(m1, 1), kTile);
-      }
-      dm.PQ = rup(std::max(m1, 1), kTile);
-      dm.PJ = rup(std::max(dm.nj, 1), kTile);
-      dm.k = std::min(request, std::min(h.nj, std::max(h.r_total, 0)));
-      dm.k = std::min(dm.k, 64);
-      const double b = 8.0 * (double(dm.NG[0]) * dm.NG[0] + double(dm.NG[1]) * dm.NG[1] +
-                              double(dm.PQ + dm.PJ) * (dm.PQ + dm.PJ) + 8.0 * dm.PJ * dm.PJ);
-      if (p1 > p0 && bytes + b > budget) break;
-      bytes += b;
-      dims.push_back(dm);
-      ++p1;
-    }
-    const int nb = p1 - p0;
-    std::vector<int> posv, krv;
-    std::vector<int4> kcv;
-    std::vector<double> kvv, Nv, Rv;
-    pd.resize(nb);
-    std::vector<long long> oG(2 * nb), oQ(nb), oF3(nb), oF4(nb), oM(nb), oKC(nb), oKR(nb), oKV(nb), oH(nb), oN(nb),
-        oR(nb), oA(nb), oE(nb), oW(nb), oFu(nb), oDG(2 * nb), oDQ(nb), oD3(nb), oD4(nb), oP(2 * nb);
-    for (int b = 0; b < nb; ++b) {
-      const Dims& dm = dims[b];
-      const HostPair& h = hp[p0 + b];
-      for (int side = 0; side < 2; ++side) {
-        oG[2 * b + side] = nG;
-        nG += (long long)dm.NG[side] * dm.NG[side];
-        oDG[2 * b + side] = nD;
-        nD += (long long)(dm.PO[side] / kTile) * kTile * kTile;
-        oP[2 * b + side] = posv.size();
-        posv.insert(posv.end(), h.pos[side].begin(), h.pos[side].end());
-      }
-      const int NQ = dm.PQ + dm.PJ, N2 = 2 * dm.PJ, n2 = dm.nj + (dm.nj & 1);
-      oQ[b] = nQ;
-      nQ += (long long)NQ * NQ;
-      oDQ[b] = nD;
-      nD += (long long)(dm.PQ / kTile) * kTile * kTile;
-      oF3[b] = nF;
-      nF += (long long)N2 * N2;
-      oF4[b] = nF;
-      nF += (long long)N2 * N2;
-      oD3[b] = nD;
-      nD += (long long)(dm.PJ / kTile) * kTile * kTile;
-      oD4[b] = nD;
-      nD += (long long)(dm.PJ / kTile) * kTile * kTile;
-      oM[b] = nM;
-      nM += (long long)dm.nf * dm.nf;
-      oKC[b] = kcv.size();
-      kcv.insert(kcv.end(), h.kc.begin(), h.kc.end());
-      oKR[b] = krv.size();
-      krv.insert(krv.end(), h.krows.begin(), h.krows.end());
-      oKV[b] = kvv.size();
-      kvv.insert(kvv.end(), h.kvals.begin(), h.kvals.end());
-      oH[b] = nH;
-      nH += (long long)dm.nf * std::max(dm.nj, 1);
-      oN[b] = Nv.size();
-      Nv.insert(Nv.end(), h.N.begin(), h.N.end());
-      oR[b] = Rv.size();
-      Rv.insert(Rv.end(), h.idx.rho_i.begin(), h.idx.rho_i.end());
-      oA[b] = nA;
-      // Jacobi: A and V (2 n2^2); tridiagonal path: packed C + 4 n k LU scratch
-      nA += std::max(2LL * n2 * n2, (long long)dm.nj * (dm.nj + 1) / 2 + 7LL * dm.nj * std::max(dm.k, 1)) + 64;
-      oE[b] = nE;
-      nE += std::max(dm.k, 1);
-      oW[b] = nW;
-      nW += (long long)N2 * std::max(dm.k, 1);
-      oFu[b] = nFu;
-      nFu += (long long)dm.nf * std::max(dm.k, 1);
-    }
+    const ChunkHost& ch = prep->chunks[chunk_id++];
+    HostTimer ht("enrich chunk");
+    const int p1 = ch.p1, nb = p1 - p0;
+    const auto& dims = ch.dims;
+    const auto& posv = ch.posv; const auto& krv = ch.krv; const auto& kcv = ch.kcv;
+    const auto& kvv = ch.kvv; const auto& Nv = ch.Nv; const auto& Rv = ch.Rv;
+    const auto& oG = ch.oG; const auto& oQ = ch.oQ; const auto& oF3 = ch.oF3; const auto& oF4 = ch.oF4;
+    const auto& oM = ch.oM; const auto& oKC = ch.oKC; const auto& oKR = ch.oKR; const auto& oKV = ch.oKV;
+    const auto& oH = ch.oH; const auto& oN = ch.oN; const auto& oR = ch.oR; const auto& oA = ch.oA;
+    const auto& oE = ch.oE; const auto& oW = ch.oW; const auto& oFu = ch.oFu; const auto& oDG = ch.oDG;
+    const auto& oDQ = ch.oDQ; const auto& oD3 = ch.oD3; const auto& oD4 = ch.oD4; const auto& oP = ch.oP;
+    const long long nG = ch.nG, nQ = ch.nQ, nF = ch.nF, nM = ch.nM, nH = ch.nH, nA = ch.nA, nE = ch.nE, nW = ch.nW,
+                    nFu = ch.nFu, nD = ch.nD;
+    std::vector<PairDev> pd(nb);
+    ht.mark("host_arrays");
     PairBuffers& B_ = *bufs_;
     auto& G = B_.G; auto& Q = B_.Q; auto& F = B_.F; auto& Dv = B_.Dv; auto& M = B_.M;
     auto& H = B_.H; auto& N = B_.N; auto& R = B_.R; auto& A = B_.A; auto& E = B_.E; auto& W = B_.W;
@@ -998,6 +1044,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     Pv.upload(posv, st_);
     info.alloc(4 * nb);
     CK(cudaMemsetAsync(info.p, 0, 4 * nb * sizeof(int), st_));
+    ht.mark("alloc_upload");
     std::vector<FrontDesc> fG(2 * nb), fQ(nb), f3(nb), f4(nb);
     int maxNG = 0, maxPO = 0, maxM1 = 0, maxNQ = 0, maxPQ = 0, maxPJ = 0, maxk = 0, maxnf = 0, maxn2 = 0;
     for (int b = 0; b < nb; ++b) {
@@ -1059,6 +1106,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     dQ.upload(fQ, st_);
     d3.upload(f3, st_);
     d4.upload(f4, st_);
+    ht.mark("descriptors");
     StageProfiler prof("enrich", st_);
     // (a)-(b) side fronts, eliminate the outer skeleton
     k_gather_G<<<dim3(maxNG, 2 * nb), 128, 0, st_>>>(dpd.p);
