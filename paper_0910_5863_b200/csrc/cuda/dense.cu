@@ -378,21 +378,22 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_trsm(const FrontDesc* ds, int 
 // ---------------------------------------------------------------------------
 // Front solves: one CTA per front, vector staged in shared memory.
 // ---------------------------------------------------------------------------
-constexpr int SOLVE_THREADS = 256;
-
-__global__ void __launch_bounds__(SOLVE_THREADS) k_front_forward(const SolveDesc* ds, const int* done) {
+// THREADS = 256, or 1024 when the fronts are too few to fill the GPU (more
+// rows, hence more loads, in flight per front).
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_front_forward(const SolveDesc* ds, const int* done) {
   if (done && *done) return;
   const SolveDesc d = ds[blockIdx.x];
   extern __shared__ double xs[];
   double* z = xs + d.n;  // 64 scratch
   const int tid = threadIdx.x;
-  for (int r = tid; r < d.n; r += SOLVE_THREADS) xs[r] = d.x[r];
+  for (int r = tid; r < d.n; r += THREADS) xs[r] = d.x[r];
   __syncthreads();
   const size_t ld = d.n;
   for (int kb = 0; kb < d.p / kTile; ++kb) {
     const int k0 = kb * kTile;
     // z = Dinv_kb * x[k0:k0+64]: 4 threads per output row
-    {
+    if (tid < 256) {
       const int row = tid >> 2, part = tid & 3;
       const double* dv = d.dinv + (size_t)kb * 64 * 64;
       double s = 0.0;
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) k_front_forward(const SolveDesc
     __syncthreads();
     if (tid < 64) xs[k0 + tid] = z[tid];
     // x[r] -= sum_c L[r, k0+c] z[c] for rows below the block
-    for (int r = k0 + kTile + tid; r < d.n; r += SOLVE_THREADS) {
+    for (int r = k0 + kTile + tid; r < d.n; r += THREADS) {
       const double* col = d.a + (size_t)k0 * ld + r;
       double s[8];
 #pragma unroll
@@ -418,16 +419,19 @@ __global__ void __launch_bounds__(SOLVE_THREADS) k_front_forward(const SolveDesc
     }
     __syncthreads();
   }
-  for (int r = tid; r < d.n; r += SOLVE_THREADS) d.x[r] = xs[r];
+  for (int r = tid; r < d.n; r += THREADS) d.x[r] = xs[r];
 }
 
-__global__ void __launch_bounds__(SOLVE_THREADS) k_front_backward(const SolveDesc* ds, const int* done) {
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_front_backward(const SolveDesc* ds, const int* done) {
+  constexpr int G = THREADS / 256;  // row groups per column set
   if (done && *done) return;
   const SolveDesc d = ds[blockIdx.x];
   extern __shared__ double xs[];
   double* t = xs + d.n;  // 64 scratch
+  __shared__ double part[G][64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int r = tid; r < d.n; r += SOLVE_THREADS) {
+  for (int r = tid; r < d.n; r += THREADS) {
     double v = d.x[r];
     if (d.cmap && r >= d.p) {
       const int k = d.cmap[r - d.p];
@@ -437,18 +441,19 @@ __global__ void __launch_bounds__(SOLVE_THREADS) k_front_backward(const SolveDes
   }
   __syncthreads();
   const size_t ld = d.n;
+  const int cw = warp & 7, rg = warp >> 3;  // column set, row group
   for (int kb = d.p / kTile - 1; kb >= 0; --kb) {
     const int k0 = kb * kTile;
-    // t[c] = x[k0+c] - sum_{r >= k0+64} L[r, k0+c] x[r]: warp w owns columns
-    // w, w+8, ..., w+56 and streams all eight at once (eight independent loads
-    // in flight per lane), then reduces across lanes
+    // t[c] = x[k0+c] - sum_{r >= k0+64} L[r, k0+c] x[r]: warp (cw, rg) owns
+    // columns cw, cw+8, ..., cw+56 and row pairs rg, rg+G, ... (16-byte loads,
+    // eight columns in flight), reduced across lanes, then over the G row
+    // groups in a fixed order
     {
       double acc[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-      // lane reads row pairs (16-byte loads)
-      const double* base = d.a + (size_t)(k0 + warp) * ld;
-      for (int r = k0 + kTile + 2 * lane; r < d.n; r += 64) {
+      const double* base = d.a + (size_t)(k0 + cw) * ld;
+      for (int r = k0 + kTile + 64 * rg + 2 * lane; r < d.n; r += 64 * G) {
         const double x0 = xs[r], x1 = xs[r + 1];
         double2 v[8];
 #pragma unroll
@@ -461,24 +466,30 @@ __global__ void __launch_bounds__(SOLVE_THREADS) k_front_backward(const SolveDes
         double s = acc[q];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) t[warp + 8 * q] = xs[k0 + warp + 8 * q] - s;
+        if (lane == 0) part[rg][cw + 8 * q] = s;
       }
     }
     __syncthreads();
+    if (tid < 64) {
+      double s = 0.0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) s += part[g][tid];
+      t[tid] = xs[k0 + tid] - s;
+    }
+    __syncthreads();
     // x[k0:k0+64] = Dinv^T t
-    {
-      const int row = tid >> 2, part = tid & 3;
+    if (tid < 256) {
+      const int row = tid >> 2, prt = tid & 3;
       const double* dv = d.dinv + (size_t)kb * 64 * 64 + (size_t)row * 64;  // column `row` of Dinv
       double s = 0.0;
-      for (int c = part; c < 64; c += 4) s += dv[c] * t[c];
+      for (int c = prt; c < 64; c += 4) s += dv[c] * t[c];
       s += __shfl_xor_sync(0xffffffffu, s, 1);
       s += __shfl_xor_sync(0xffffffffu, s, 2);
-      __syncthreads();
-      if (part == 0) xs[k0 + row] = s;
+      if (prt == 0) xs[k0 + row] = s;
     }
     __syncthreads();
   }
-  for (int r = tid; r < d.n; r += SOLVE_THREADS) d.x[r] = xs[r];
+  for (int r = tid; r < d.n; r += THREADS) d.x[r] = xs[r];
 }
 
 __global__ void k_copy_trailing(const TrailDesc* ds) {
@@ -501,8 +512,12 @@ void configure() {
   cudaFuncSetAttribute(k_syrk_column_splitk, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
   cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
   cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
-  cudaFuncSetAttribute(k_front_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_front_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_forward<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_backward<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_forward<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_backward<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_forward<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_backward<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   g_smem_configured = 1;
 }
 
@@ -583,17 +598,33 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
   }
 }
 
+namespace {
+// Threads per front.  256: measured faster than 512/1024-thread fronts on
+// configs 3-4 (the per-block barriers dominate once more warps share a front).
+int solve_threads(int) { return 256; }
+}  // namespace
+
 void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
   if (batch == 0) return;
   configure();
-  k_front_forward<<<batch, SOLVE_THREADS, (max_n + 64) * sizeof(double), stream>>>(d_descs, done);
+  const size_t smem = (max_n + 64) * sizeof(double);
+  switch (solve_threads(batch)) {
+    case 1024: k_front_forward<1024><<<batch, 1024, smem, stream>>>(d_descs, done); break;
+    case 512: k_front_forward<512><<<batch, 512, smem, stream>>>(d_descs, done); break;
+    default: k_front_forward<256><<<batch, 256, smem, stream>>>(d_descs, done); break;
+  }
   count_launch(1);
 }
 
 void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
   if (batch == 0) return;
   configure();
-  k_front_backward<<<batch, SOLVE_THREADS, (max_n + 64) * sizeof(double), stream>>>(d_descs, done);
+  const size_t smem = (max_n + 64) * sizeof(double);
+  switch (solve_threads(batch)) {
+    case 1024: k_front_backward<1024><<<batch, 1024, smem, stream>>>(d_descs, done); break;
+    case 512: k_front_backward<512><<<batch, 512, smem, stream>>>(d_descs, done); break;
+    default: k_front_backward<256><<<batch, 256, smem, stream>>>(d_descs, done); break;
+  }
   count_launch(1);
 }
 
