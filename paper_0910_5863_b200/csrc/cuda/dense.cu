@@ -208,19 +208,31 @@ __device__ __noinline__ int chol16(double* Lo, double* rd, int lane) {
 #pragma unroll
   for (int c = 0; c < 16; ++c) a[c] = Lo[c * LDS + r];
   int bad = 0;
+  // software-pipelined: column k+1 is updated first and pivot k+1 (shuffle +
+  // rsqrt) is started before the remaining updates of step k, which fill its
+  // latency
+  double dkk = __shfl_sync(0xffffffffu, a[0], 0);
+  double inv = dkk > 0.0 ? rsqrt(dkk) : 1.0;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
-    const double dkk = __shfl_sync(0xffffffffu, a[k], k);
     if (!(dkk > 0.0) && !bad) bad = k + 1;
-    const double inv = dkk > 0.0 ? rsqrt(dkk) : 1.0;
     const double sk = dkk > 0.0 ? dkk * inv : 1.0;
     if (lane == k) rd[k] = inv;
     a[k] = (r == k) ? sk : (r > k ? a[k] * inv : a[k]);
+    double dkk_n = 1.0, inv_n = 1.0;
+    if (k + 1 < 16) {
+      const double l1 = __shfl_sync(0xffffffffu, a[k], k + 1);  // L[k+1][k]
+      a[k + 1] = (r >= k + 1) ? a[k + 1] - a[k] * l1 : a[k + 1];
+      dkk_n = __shfl_sync(0xffffffffu, a[k + 1], k + 1);
+      inv_n = dkk_n > 0.0 ? rsqrt(dkk_n) : 1.0;
+    }
 #pragma unroll
-    for (int c = k + 1; c < 16; ++c) {
+    for (int c = k + 2; c < 16; ++c) {
       const double lc = __shfl_sync(0xffffffffu, a[k], c);  // L[c][k]
       a[c] = (r >= c) ? a[c] - a[k] * lc : a[c];
     }
+    dkk = dkk_n;
+    inv = inv_n;
   }
   if (lane < 16) {
 #pragma unroll

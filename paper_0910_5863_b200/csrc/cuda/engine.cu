@@ -32,6 +32,7 @@ inline int rup(int v, int m) { return (v + m - 1) / m * m; }
 struct PcgState {
   double rz, pq, alpha, beta, bnorm, ref, relres, tol;
   int it, max_it, done, precond_residual;
+  unsigned int arrive;  // CTAs of k_beta_update that finished this iteration
 };
 
 // ---------------------------------------------------------------------------
@@ -249,20 +250,14 @@ __global__ void k_dot(i64 n, const double* a, const double* b, double* partials)
   block_partial(acc, partials);
 }
 
-__global__ void k_alpha(PcgState* st, const double* partials, double* alphas) {
+// alpha = rz / (p.q) (every CTA reduces the partials in the same fixed order),
+// x += alpha p, r -= alpha q, partials of r.r.  Only CTA 0 writes the state
+// fields nobody else reads here.
+__global__ void __launch_bounds__(kRed) k_alpha_axpy(i64 n, PcgState* st, double* x, double* r, const double* p,
+                                                     const double* q, const double* ppq, double* prr, double* alphas) {
   if (st->done) return;
-  const double pq = sum_partials(partials);
-  if (threadIdx.x == 0) {
-    st->pq = pq;
-    st->alpha = st->rz / pq;
-    alphas[st->it] = st->alpha;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_axpy(i64 n, PcgState* st, double* x, double* r, const double* p,
-                                              const double* q, double* partials) {
-  if (st->done) return;
-  const double a = st->alpha;
+  const double pq = sum_partials(ppq);
+  const double a = st->rz / pq;
   double acc = 0.0;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     x[i] += a * p[i];
@@ -270,30 +265,40 @@ __global__ void __launch_bounds__(256) k_axpy(i64 n, PcgState* st, double* x, do
     r[i] = ri;
     acc += ri * ri;
   }
-  block_partial(acc, partials);
+  block_partial(acc, prr);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->pq = pq;
+    st->alpha = a;
+    alphas[st->it] = a;
+  }
 }
 
-__global__ void k_beta(PcgState* st, const double* prz, const double* prr, double* betas) {
+// beta = rz_next / rz, p = z + beta p; the last CTA to finish commits the
+// iteration (rz, it, residual, done), after every CTA has read the old state.
+__global__ void __launch_bounds__(kRed) k_beta_update(i64 n, PcgState* st, double* p, const double* z,
+                                                      const double* prz, const double* prr, double* betas) {
   if (st->done) return;
   const double rz_next = sum_partials(prz);
   __syncthreads();
   const double rr = sum_partials(prr);
+  const double beta = rz_next / st->rz;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const double beta = rz_next / st->rz;
-    st->beta = beta;
-    betas[st->it] = beta;
-    st->rz = rz_next;
-    st->it += 1;
-    const double cur = st->precond_residual ? sqrt(fmax(rz_next, 0.0)) : sqrt(rr);
-    st->relres = cur / st->ref;
-    if (st->relres <= st->tol || st->it >= st->max_it) st->done = 1;
+    __threadfence();
+    if (atomicAdd(&st->arrive, 1u) == gridDim.x - 1) {
+      st->arrive = 0;
+      st->beta = beta;
+      betas[st->it] = beta;
+      st->rz = rz_next;
+      st->it += 1;
+      const double cur = st->precond_residual ? sqrt(fmax(rz_next, 0.0)) : sqrt(rr);
+      st->relres = cur / st->ref;
+      if (st->relres <= st->tol || st->it >= st->max_it) st->done = 1;
+      __threadfence();
+    }
   }
-}
-
-__global__ void __launch_bounds__(256) k_update_p(i64 n, const PcgState* st, double* p, const double* z) {
-  if (st->done) return;
-  const double b = st->beta;
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) p[i] = z[i] + b * p[i];
 }
 
 // restrict_residual (bddc_operator.cpp:52-68) restricted to the interface:
@@ -1500,14 +1505,13 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     const int* done = &D.pst.p->done;
     launch_schur(D, D.vp.p, D.vq.p, D.vp.p, D.part_a.p, done);
-    k_alpha<<<1, kRed, 0, st>>>(D.pst.p, D.part_a.p, D.alphas.p);
-    k_axpy<<<kRed, 256, 0, st>>>(n, D.pst.p, D.vx.p, D.vr.p, D.vp.p, D.vq.p, D.part_b.p);
+    k_alpha_axpy<<<kRed, kRed, 0, st>>>(n, D.pst.p, D.vx.p, D.vr.p, D.vp.p, D.vq.p, D.part_a.p, D.part_b.p,
+                                         D.alphas.p);
     launch_precond(D, D.vr.p, D.vz.p, D.vr.p, D.part_a.p, done);
-    k_beta<<<1, kRed, 0, st>>>(D.pst.p, D.part_a.p, D.part_b.p, D.betas.p);
-    k_update_p<<<kRed, 256, 0, st>>>(n, D.pst.p, D.vp.p, D.vz.p);
+    k_beta_update<<<kRed, kRed, 0, st>>>(n, D.pst.p, D.vp.p, D.vz.p, D.part_a.p, D.part_b.p, D.betas.p);
     CK(cudaStreamEndCapture(st, &D.graph));
     CK(cudaGraphInstantiate(&D.gexec, D.graph, 0));
-    D.graph_kernels = launch_count() - before + 4;  // + k_alpha, k_axpy, k_beta, k_update_p
+    D.graph_kernels = launch_count() - before + 2;  // + k_alpha_axpy, k_beta_update
     count_launch(-(launch_count() - before));
   }
   PcgState hs = h;
