@@ -121,6 +121,12 @@ int bddc_b200_element_scale(const bddc_b200_t* h, double* out);
  * its load: query nnz with ptr == NULL, then fill ptr (dim+1), idx, val (nnz), load (dim). */
 int bddc_b200_subdomain_matrix(const bddc_b200_t* h, int s, int64_t* nnz, int64_t* ptr, int64_t* idx,
                                double* val, double* load);
+/* Dense leaf front of substructure s as assembled on the device (assemble.cpp:
+ * 202-258 evaluated per entry from the reference element matrices), column-major
+ * ld x ld in [interior | boundary] order: query ld with front == NULL, then fill
+ * front (ld*ld) and pos (dim: local dof -> front position).  Does not disturb an
+ * analysis (the next analysis re-assembles). */
+int bddc_b200_leaf_front(bddc_b200_t* h, int s, int64_t* ld, double* front, int64_t* pos);
 /* Globs (globs.hpp:18-44): count, then per glob kind / node count / sharer count. */
 int bddc_b200_glob_count(const bddc_b200_t* h, int64_t* n);
 int bddc_b200_glob_info(const bddc_b200_t* h, int g, int* kind, int64_t* n_nodes, int64_t* n_subs);

@@ -100,6 +100,7 @@ EXPORTS = {
     "bddc_b200_global_dof": (C.c_int, [P, C.c_int, I64]),
     "bddc_b200_element_scale": (C.c_int, [P, D]),
     "bddc_b200_subdomain_matrix": (C.c_int, [P, C.c_int, I64, I64, I64, D, D]),
+    "bddc_b200_leaf_front": (C.c_int, [P, C.c_int, I64, D, I64]),
     "bddc_b200_glob_count": (C.c_int, [P, I64]),
     "bddc_b200_glob_info": (C.c_int, [P, C.c_int, C.POINTER(C.c_int), I64, I64]),
     "bddc_b200_glob_nodes": (C.c_int, [P, C.c_int, I64, I64]),
@@ -344,6 +345,17 @@ class BDDC:
         _check(self._lib.bddc_b200_subdomain_matrix(self._h, s, C.byref(nnz), ptr.ctypes.data_as(I64),
                                                     idx.ctypes.data_as(I64), _dptr(val), _dptr(load)))
         return sp.csr_matrix((val, idx, ptr), shape=(dim.value, dim.value)), load
+
+    def leaf_front(self, s):
+        """(dense front ld x ld as assembled on the device, position of each local dof)."""
+        ld = C.c_int64()
+        _check(self._lib.bddc_b200_leaf_front(self._h, s, C.byref(ld), None, None))
+        dim = C.c_int64()
+        _check(self._lib.bddc_b200_subdomain_dim(self._h, s, C.byref(dim)))
+        front = np.empty(ld.value * ld.value)
+        pos = np.empty(dim.value, dtype=np.int64)
+        _check(self._lib.bddc_b200_leaf_front(self._h, s, C.byref(ld), _dptr(front), pos.ctypes.data_as(I64)))
+        return front.reshape(ld.value, ld.value).T, pos
 
     def globs(self):
         n = C.c_int64()

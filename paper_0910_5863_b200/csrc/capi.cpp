@@ -183,14 +183,29 @@ int bddc_b200_subdomain_matrix(const bddc_b200_t* h, int s, int64_t* nnz, int64_
                                double* load) {
   return guarded([&] {
     const Subdomain& S = h->model.subs.at(s);
-    *nnz = static_cast<int64_t>(S.A.idx.size());
+    const CSR& A = h->model.matrix(s);
+    *nnz = static_cast<int64_t>(A.idx.size());
     if (!ptr) return;
-    for (int r = 0; r <= S.A.n; ++r) ptr[r] = S.A.ptr[r];
-    for (std::size_t t = 0; t < S.A.idx.size(); ++t) {
-      idx[t] = S.A.idx[t];
-      val[t] = S.A.val[t];
+    for (int r = 0; r <= A.n; ++r) ptr[r] = A.ptr[r];
+    for (std::size_t t = 0; t < A.idx.size(); ++t) {
+      idx[t] = A.idx[t];
+      val[t] = A.val[t];
     }
     for (int l = 0; l < S.dim(); ++l) load[l] = S.load[l];
+  });
+}
+
+int bddc_b200_leaf_front(bddc_b200_t* h, int s, int64_t* ld, double* front, int64_t* pos) {
+  return guarded([&] {
+    if (s < 0 || s >= static_cast<int>(h->model.subs.size())) throw Error(kError, "substructure out of range");
+    std::vector<double> f;
+    std::vector<int> p;
+    int n = 0;
+    engine(h).leaf_front(s, front ? &f : nullptr, &p, &n);
+    *ld = n;
+    if (!front) return;
+    std::memcpy(front, f.data(), f.size() * sizeof(double));
+    for (std::size_t i = 0; i < p.size(); ++i) pos[i] = p[i];
   });
 }
 

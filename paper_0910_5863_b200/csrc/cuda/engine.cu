@@ -38,24 +38,64 @@ struct PcgState {
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
-struct ScatterDesc {
-  const int* ptr;
-  const int* idx;
-  const double* val;
-  const int* pos;   // local dof -> dense position
-  double* a;
-  int n, ld, nI, PI, nB;
+// Device assembly of the dense leaf fronts (assemble.cpp:202-258; SURVEY
+// 8(f) row 1).  Elements are congruent: K_e = scale_e * K_ref[material_e].
+struct AsmDesc {
+  double* a;         // dense front [interior | boundary], ld x ld
+  const int* lnode;  // local node grid (x fastest) * nc + c -> local dof or -1
+  const int* pos;    // local dof -> front position
+  int ld, nI, PI, nB, i0, j0, k0;
+};
+struct AsmMesh {
+  const double* ke;      // reference element matrices, ed x ed row-major each
+  const int* eke;        // element -> reference matrix
+  const double* escale;  // element scale, or nullptr (all 1)
+  int ne0, ne1, epe, nc;
 };
 
-__global__ void k_scatter_csr(const ScatterDesc* ds) {
-  const ScatterDesc d = ds[blockIdx.y];
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < d.ld; r += gridDim.x * blockDim.x) {
-    if (r < d.n) {
-      const int pr = d.pos[r];
-      for (int t = d.ptr[r]; t < d.ptr[r + 1]; ++t) d.a[(size_t)d.pos[d.idx[t]] * d.ld + pr] = d.val[t];
+// Thread per stiffness entry (node, component, neighbour slot, component): the
+// entry of the (lower, higher) local dof pair summed over the elements holding
+// both nodes in the host's element order (k, j, i), multiply and add rounded
+// separately, so the front equals the host CSR bitwise.  Padding rows get a
+// unit diagonal.
+__global__ void k_assemble_front(const AsmDesc* ds, AsmMesh mm) {
+  const AsmDesc d = ds[blockIdx.y];
+  const int nc = mm.nc, ln = mm.epe + 1, ed = 8 * nc;
+  const long nent = (long)ln * ln * ln * nc * 27 * nc;
+  const int vtx[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // (dx + 2 dy + 4 dz) -> VTK vertex
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < nent + d.ld; t += (long)gridDim.x * blockDim.x) {
+    if (t >= nent) {
+      const int r = static_cast<int>(t - nent);
+      if ((r >= d.nI && r < d.PI) || r >= d.PI + d.nB) d.a[(size_t)r * d.ld + r] = 1.0;
+      continue;
     }
-    const bool pad = (r >= d.nI && r < d.PI) || (r >= d.PI + d.nB);
-    if (pad) d.a[(size_t)r * d.ld + r] = 1.0;
+    const int cb = static_cast<int>(t % nc);
+    long u = t / nc;
+    const int slot = static_cast<int>(u % 27);
+    u /= 27;
+    const int ca = static_cast<int>(u % nc);
+    const int q = static_cast<int>(u / nc);
+    const int li = q % ln, lj = (q / ln) % ln, lk = q / (ln * ln);
+    const int ci = li + slot % 3 - 1, cj = lj + (slot / 3) % 3 - 1, ck = lk + slot / 9 - 1;
+    if (ci < 0 || cj < 0 || ck < 0 || ci >= ln || cj >= ln || ck >= ln) continue;
+    const int r = d.lnode[q * nc + ca];
+    const int c = d.lnode[((ck * ln + cj) * ln + ci) * nc + cb];
+    if (r < 0 || c < 0) continue;
+    const bool lo = r <= c;
+    const int pi = lo ? li : ci, pj = lo ? lj : cj, pk = lo ? lk : ck, pc = lo ? ca : cb;
+    const int qi = lo ? ci : li, qj = lo ? cj : lj, qk = lo ? ck : lk, qc = lo ? cb : ca;
+    double s = 0.0;
+    for (int ek = max(max(pk, qk) - 1, 0); ek <= min(min(pk, qk), mm.epe - 1); ++ek)
+      for (int ej = max(max(pj, qj) - 1, 0); ej <= min(min(pj, qj), mm.epe - 1); ++ej)
+        for (int ei = max(max(pi, qi) - 1, 0); ei <= min(min(pi, qi), mm.epe - 1); ++ei) {
+          const int e = ((d.k0 + ek) * mm.ne1 + d.j0 + ej) * mm.ne0 + d.i0 + ei;
+          const int va = vtx[(pi - ei) + 2 * (pj - ej) + 4 * (pk - ek)];
+          const int vb = vtx[(qi - ei) + 2 * (qj - ej) + 4 * (qk - ek)];
+          const double kv = mm.ke[(size_t)mm.eke[e] * ed * ed + (va * nc + pc) * ed + vb * nc + qc];
+          const double sc = mm.escale ? mm.escale[e] : 1.0;
+          s = __dadd_rn(s, sc == 1.0 ? kv : __dmul_rn(sc, kv));
+        }
+    d.a[(size_t)d.pos[c] * d.ld + d.pos[r]] = s;
   }
 }
 
@@ -621,13 +661,14 @@ struct DeviceState {
   int max_NM = 0, max_PI = 0, max_PB = 0, max_nB = 0;
   bool prepared = false;
   struct HostStage {
-    std::vector<int> ptr, idx, pos, biface, icp, icpos;
-    std::vector<double> val, mv, bw;
+    std::vector<int> lnode, pos, eke, biface, icp, icpos;
+    std::vector<double> ke, escale, mv, bw;
   } h;
   DBuf<double> M, DinvM, S, MV, MV0, WB;
-  DBuf<int> minfo, csr_ptr, csr_idx, csr_pos;
-  DBuf<double> csr_val;
-  DBuf<ScatterDesc> scatter;
+  DBuf<int> minfo, asm_lnode, asm_pos, asm_eke;
+  DBuf<double> asm_ke, asm_escale;
+  DBuf<AsmDesc> asmdesc;
+  AsmMesh asm_mesh{};
   DBuf<TrailDesc> mtrail;
   DBuf<FrontDesc> mfront;
   DBuf<SolveDesc> msolve;
@@ -770,26 +811,26 @@ void Engine::prepare() {
   D.MV.alloc(mvo);
   D.MV0.alloc(mvo);
   D.WB.alloc(std::max<long long>(wbo, 1));
-  // host staging: CSR with dense positions, loads in front layout
-  std::vector<long long> ptr_off(ns), idx_off(ns), pos_off(ns);
+  // host staging of the assembly inputs: element data, local numbering and
+  // dense positions per substructure, loads in front layout
+  std::vector<long long> lnode_off(ns), pos_off(ns);
   auto& H = D.h;
-  H.ptr.clear();
-  H.idx.clear();
+  H.lnode.clear();
   H.pos.clear();
-  H.val.clear();
   for (int s = 0; s < ns; ++s) {
     const Subdomain& S = m.subs[s];
-    ptr_off[s] = H.ptr.size();
-    idx_off[s] = H.idx.size();
+    lnode_off[s] = H.lnode.size();
     pos_off[s] = H.pos.size();
-    H.ptr.insert(H.ptr.end(), S.A.ptr.begin(), S.A.ptr.end());
-    H.idx.insert(H.idx.end(), S.A.idx.begin(), S.A.idx.end());
-    H.val.insert(H.val.end(), S.A.val.begin(), S.A.val.end());
+    H.lnode.insert(H.lnode.end(), S.lnode.begin(), S.lnode.end());
     std::vector<int> p(S.dim());
     for (int r = 0; r < D.nI[s]; ++r) p[S.interior[r]] = r;
     for (int b = 0; b < D.nB[s]; ++b) p[S.boundary[b]] = D.PI[s] + b;
     H.pos.insert(H.pos.end(), p.begin(), p.end());
   }
+  H.ke.clear();
+  for (const auto& k : m.ke_ref) H.ke.insert(H.ke.end(), k.begin(), k.end());
+  H.eke = m.element_ke;
+  H.escale = m.mesh.element_scale;
   H.mv.assign(mvo, 0.0);
   for (int s = 0; s < ns; ++s) {
     const Subdomain& S = m.subs[s];
@@ -806,8 +847,8 @@ void Engine::prepare() {
       H.biface[D.wb_off[s] + b] = static_cast<int>(m.maps.global_to_interface[g]);
       double tot = 0.0;
       for (i64 t = m.maps.copy_ptr[g]; t < m.maps.copy_ptr[g + 1]; ++t)
-        tot += m.subs[m.maps.copy_sub[t]].A.diag(m.maps.copy_local[t]);
-      H.bw[D.wb_off[s] + b] = S.A.diag(S.boundary[b]) / tot;
+        tot += m.subs[m.maps.copy_sub[t]].diag[m.maps.copy_local[t]];
+      H.bw[D.wb_off[s] + b] = S.diag[S.boundary[b]] / tot;
     }
   }
   std::vector<std::vector<int>> lists(D.niface);
@@ -819,25 +860,28 @@ void Engine::prepare() {
     H.icp[i + 1] = H.icp[i] + static_cast<int>(lists[i].size());
     H.icpos.insert(H.icpos.end(), lists[i].begin(), lists[i].end());
   }
-  D.csr_ptr.alloc(H.ptr.size());
-  D.csr_idx.alloc(std::max<std::size_t>(H.idx.size(), 1));
-  D.csr_pos.alloc(std::max<std::size_t>(H.pos.size(), 1));
-  D.csr_val.alloc(std::max<std::size_t>(H.val.size(), 1));
+  D.asm_lnode.alloc(std::max<std::size_t>(H.lnode.size(), 1));
+  D.asm_pos.alloc(std::max<std::size_t>(H.pos.size(), 1));
+  D.asm_eke.alloc(std::max<std::size_t>(H.eke.size(), 1));
+  D.asm_ke.alloc(std::max<std::size_t>(H.ke.size(), 1));
+  D.asm_escale.alloc(std::max<std::size_t>(H.escale.size(), 1));
+  D.asm_mesh = AsmMesh{D.asm_ke.p, D.asm_eke.p, H.escale.empty() ? nullptr : D.asm_escale.p, m.mesh.ne[0],
+                       m.mesh.ne[1], m.mesh.epe, m.mesh.ncomp};
   D.biface.alloc(std::max<long long>(wbo, 1));
   D.bw.alloc(std::max<long long>(wbo, 1));
   D.icopy_ptr.alloc(H.icp.size());
   D.icopy_pos.alloc(std::max<std::size_t>(H.icpos.size(), 1));
   D.minfo.alloc(ns);
   D.rhs.alloc(std::max<i64>(D.niface, 1));
-  std::vector<ScatterDesc> sc(ns);
+  std::vector<AsmDesc> ad(ns);
   std::vector<FrontDesc> fd(ns);
   std::vector<SolveDesc> sv(ns);
   std::vector<TrailDesc> td(ns);
   std::vector<SubDesc> sd(ns);
   for (int s = 0; s < ns; ++s) {
-    sc[s] = ScatterDesc{D.csr_ptr.p + ptr_off[s], D.csr_idx.p + idx_off[s], D.csr_val.p + idx_off[s],
-                        D.csr_pos.p + pos_off[s], D.M.p + D.m_off[s], m.subs[s].dim(), D.NM[s], D.nI[s], D.PI[s],
-                        D.nB[s]};
+    const Subdomain& S = m.subs[s];
+    ad[s] = AsmDesc{D.M.p + D.m_off[s], D.asm_lnode.p + lnode_off[s], D.asm_pos.p + pos_off[s], D.NM[s], D.nI[s],
+                    D.PI[s], D.nB[s], S.origin[0], S.origin[1], S.origin[2]};
     fd[s] = FrontDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.NM[s], D.PI[s], D.minfo.p + s, 0};
     sv[s] = SolveDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.MV.p + D.mv_off[s], D.NM[s], D.PI[s],
                       nullptr, nullptr};
@@ -845,7 +889,7 @@ void Engine::prepare() {
     sd[s] = SubDesc{D.S.p + D.s_off[s], nullptr, nullptr, D.biface.p + D.wb_off[s], D.bw.p + D.wb_off[s],
                     nullptr, nullptr, nullptr, D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], 0, 0};
   }
-  D.scatter.upload(sc, st);
+  D.asmdesc.upload(ad, st);
   D.mfront.upload(fd, st);
   D.msolve.upload(sv, st);
   D.mtrail.upload(td, st);
@@ -867,10 +911,11 @@ double Engine::upload_inputs() {
     if (n) CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
     bytes += double(n);
   };
-  cp(D.csr_ptr.p, H.ptr.data(), H.ptr.size() * sizeof(int));
-  cp(D.csr_idx.p, H.idx.data(), H.idx.size() * sizeof(int));
-  cp(D.csr_pos.p, H.pos.data(), H.pos.size() * sizeof(int));
-  cp(D.csr_val.p, H.val.data(), H.val.size() * sizeof(double));
+  cp(D.asm_ke.p, H.ke.data(), H.ke.size() * sizeof(double));
+  cp(D.asm_eke.p, H.eke.data(), H.eke.size() * sizeof(int));
+  cp(D.asm_escale.p, H.escale.data(), H.escale.size() * sizeof(double));
+  cp(D.asm_lnode.p, H.lnode.data(), H.lnode.size() * sizeof(int));
+  cp(D.asm_pos.p, H.pos.data(), H.pos.size() * sizeof(int));
   cp(D.MV0.p, H.mv.data(), H.mv.size() * sizeof(double));
   cp(D.biface.p, H.biface.data(), H.biface.size() * sizeof(int));
   cp(D.bw.p, H.bw.data(), H.bw.size() * sizeof(double));
@@ -892,7 +937,7 @@ void Engine::analysis_launch() {
   CK(cudaEventRecord(D.e0, st));
   D.M.zero(st);
   D.minfo.zero(st);
-  k_scatter_csr<<<dim3(8, ns), 256, 0, st>>>(D.scatter.p);
+  k_assemble_front<<<dim3(64, ns), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
   count_launch(1);
   CK(cudaGetLastError());
   CK(cudaEventRecord(D.ef0, st));
@@ -1372,6 +1417,25 @@ void ensure_vectors(DeviceState& D) {
   D.pst.alloc(1);
 }
 }  // namespace
+
+void Engine::leaf_front(int s, std::vector<double>* out, std::vector<int>* pos, int* ld) {
+  prepare();
+  DeviceState& D = *d_;
+  *ld = D.NM[s];
+  const Subdomain& S = m_.subs[s];
+  std::size_t off = 0;
+  for (int q = 0; q < s; ++q) off += m_.subs[q].dim();
+  pos->assign(D.h.pos.begin() + off, D.h.pos.begin() + off + S.dim());
+  if (!out) return;
+  cudaStream_t st = D.st;
+  D.M.zero(st);
+  k_assemble_front<<<dim3(64, D.nsub), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
+  count_launch(1);
+  CK(cudaGetLastError());
+  out->resize((size_t)D.NM[s] * D.NM[s]);
+  CK(cudaMemcpyAsync(out->data(), D.M.p + D.m_off[s], out->size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
 
 void Engine::schur_apply(const double* x, double* y) {
   DeviceState& D = *d_;

@@ -101,6 +101,9 @@ class Engine {
   EnrichOutcome enrich(ConstraintSet& cs, const EnrichOptions& o);
 
   void schur_apply(const double* x, double* y);      // host vectors, interface size
+  /// Device-assembled dense front of substructure s (before factorization);
+  /// out == nullptr returns only ld and the position map.
+  void leaf_front(int s, std::vector<double>* out, std::vector<int>* pos, int* ld);
   void precond_apply(const double* r, double* z);
   void rhs(double* out);
   void recover(const double* u_interface, double* u_free);

@@ -3,6 +3,9 @@
 #include "host.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <deque>
 #include <limits>
@@ -303,33 +306,46 @@ int Maps::local_of(i64 g, int s) const {
 // ============================================================================
 namespace {
 
+// VTK vertex order of the Q1 element: local grid offsets, and the inverse map
+const int kVertexOff[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0},
+                              {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
+
+// assemble_subdomains, structural part (assemble.cpp:202-269): local numbering,
+// loads and the stiffness diagonal.  Values are summed element by element in
+// the element loop order (k, j, i), which the device assembly and
+// assemble_values reproduce entry by entry.
 void assemble(Model& md) {
   const Mesh& m = md.mesh;
   const Problem& p = md.spec;
   const int nc = m.ncomp, epe = m.epe, ed = 8 * nc;
-  std::map<int, std::vector<double>> cache;  // assemble.cpp:145-169
-  for (int mat : m.element_material)
-    if (!cache.count(mat)) {
+  std::map<int, int> mat_index;  // assemble.cpp:145-169
+  md.ke_ref.clear();
+  md.element_ke.resize(m.element_material.size());
+  for (std::size_t e = 0; e < m.element_material.size(); ++e) {
+    const int mat = m.element_material[e];
+    auto f = mat_index.find(mat);
+    if (f == mat_index.end()) {
       auto it = p.materials.find(mat);
       if (it == p.materials.end()) throw Error(kBadProblemSpec, "element references unknown material");
-      cache[mat] = element_stiffness(m.h, it->second, m.physics);
+      f = mat_index.emplace(mat, static_cast<int>(md.ke_ref.size())).first;
+      md.ke_ref.push_back(element_stiffness(m.h, it->second, m.physics));
     }
+    md.element_ke[e] = f->second;
+  }
   const int nsub = m.sub[0] * m.sub[1] * m.sub[2];
-  md.subs.resize(nsub);
+  md.subs.assign(nsub, Subdomain{});
   const int ln = epe + 1;  // local node grid per axis
-  const int slots = 27 * nc;
-  std::vector<double> acc;
-  std::vector<int> lnode_local;  // local node grid index -> first local dof (or -1 per comp)
+#pragma omp parallel for schedule(dynamic, 4)
   for (int s = 0; s < nsub; ++s) {
     Subdomain& S = md.subs[s];
     S.id = s;
     const int si = s % m.sub[0], sj = (s / m.sub[0]) % m.sub[1], sk = s / (m.sub[0] * m.sub[1]);
     const int i0 = si * epe, j0 = sj * epe, k0 = sk * epe;
+    S.origin[0] = i0;
+    S.origin[1] = j0;
+    S.origin[2] = k0;
     // nodes ascending by global id == (lk, lj, li) lexicographic
-    S.nodes.clear();
-    S.global_dof.clear();
-    lnode_local.assign(std::size_t(ln) * ln * ln * nc, -1);
-    std::vector<i64> node_comp;
+    S.lnode.assign(std::size_t(ln) * ln * ln * nc, -1);
     for (int lk = 0; lk < ln; ++lk)
       for (int lj = 0; lj < ln; ++lj)
         for (int li = 0; li < ln; ++li) {
@@ -338,41 +354,28 @@ void assemble(Model& md) {
           for (int c = 0; c < nc; ++c) {
             const i64 g = md.dof[i64(node) * nc + c];
             if (g < 0) continue;
-            lnode_local[((std::size_t(lk) * ln + lj) * ln + li) * nc + c] = S.dim();
+            S.lnode[((std::size_t(lk) * ln + lj) * ln + li) * nc + c] = S.dim();
             S.global_dof.push_back(g);
           }
         }
     const int n = S.dim();
-    acc.assign(std::size_t(n) * slots, 0.0);
     S.load.assign(n, 0.0);
+    S.diag.assign(n, 0.0);
     const double cell = m.h * m.h * m.h / 8.0;
     for (int lk = 0; lk < epe; ++lk)
       for (int lj = 0; lj < epe; ++lj)
         for (int li = 0; li < epe; ++li) {
           const int gi = i0 + li, gj = j0 + lj, gk = k0 + lk;
           const int e = (gk * m.ne[1] + gj) * m.ne[0] + gi;
-          const std::vector<double>& ke = cache[m.element_material[e]];
+          const std::vector<double>& ke = md.ke_ref[md.element_ke[e]];
           const double sc = m.element_scale.empty() ? 1.0 : m.element_scale[e];
-          // element-local nodes in VTK order -> local grid offsets
-          static const int off[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0},
-                                        {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
           int local[24];
           for (int a = 0; a < 8; ++a)
             for (int c = 0; c < nc; ++c)
-              local[a * nc + c] = lnode_local[((std::size_t(lk + off[a][2]) * ln + lj + off[a][1]) * ln +
-                                               li + off[a][0]) * nc + c];
-          for (int a = 0; a < ed; ++a) {
-            if (local[a] < 0) continue;
-            const int na = a / nc;
-            for (int b = 0; b < ed; ++b) {
-              if (local[b] < 0 || local[b] < local[a]) continue;
-              const int nb = b / nc, cb = b % nc;
-              const int slot = ((off[nb][2] - off[na][2] + 1) * 3 + (off[nb][1] - off[na][1] + 1)) * 3 +
-                               (off[nb][0] - off[na][0] + 1);
-              const double v = sc == 1.0 ? ke[a * ed + b] : sc * ke[a * ed + b];
-              acc[std::size_t(local[a]) * slots + slot * nc + cb] += v;
-            }
-          }
+              local[a * nc + c] = S.lnode[((std::size_t(lk + kVertexOff[a][2]) * ln + lj + kVertexOff[a][1]) * ln +
+                                           li + kVertexOff[a][0]) * nc + c];
+          for (int a = 0; a < ed; ++a)
+            if (local[a] >= 0) S.diag[local[a]] += sc == 1.0 ? ke[a * ed + a] : sc * ke[a * ed + a];
           for (int a = 0; a < 8; ++a)  // assemble.cpp:260-269
             for (int c = 0; c < nc; ++c) {
               const int l = local[a * nc + c];
@@ -392,50 +395,83 @@ void assemble(Model& md) {
               }
           }
         }
-    // CSR of the full symmetric matrix: columns ascending = slot order.
-    CSR& A = S.A;
-    A.n = n;
-    A.ptr.assign(n + 1, 0);
-    A.idx.clear();
-    A.val.clear();
-    std::vector<int> row_node(n), row_comp(n);
-    for (int lk = 0; lk < ln; ++lk)
-      for (int lj = 0; lj < ln; ++lj)
-        for (int li = 0; li < ln; ++li)
+  }
+}
+
+// assemble_subdomains, values (assemble.cpp:202-258): upper entries accumulated
+// per element in loop order, the full symmetric CSR mirrored from them.
+void assemble_values(const Model& md, const Subdomain& S, CSR& A) {
+  const Mesh& m = md.mesh;
+  const int nc = m.ncomp, epe = m.epe, ed = 8 * nc, ln = epe + 1, slots = 27 * nc;
+  const int n = S.dim();
+  const int i0 = S.origin[0], j0 = S.origin[1], k0 = S.origin[2];
+  std::vector<double> acc(std::size_t(n) * slots, 0.0);
+  for (int lk = 0; lk < epe; ++lk)
+    for (int lj = 0; lj < epe; ++lj)
+      for (int li = 0; li < epe; ++li) {
+        const int e = ((k0 + lk) * m.ne[1] + j0 + lj) * m.ne[0] + i0 + li;
+        const std::vector<double>& ke = md.ke_ref[md.element_ke[e]];
+        const double sc = m.element_scale.empty() ? 1.0 : m.element_scale[e];
+        int local[24];
+        for (int a = 0; a < 8; ++a)
+          for (int c = 0; c < nc; ++c)
+            local[a * nc + c] = S.lnode[((std::size_t(lk + kVertexOff[a][2]) * ln + lj + kVertexOff[a][1]) * ln + li +
+                                         kVertexOff[a][0]) * nc + c];
+        for (int a = 0; a < ed; ++a) {
+          if (local[a] < 0) continue;
+          const int na = a / nc;
+          for (int b = 0; b < ed; ++b) {
+            if (local[b] < 0 || local[b] < local[a]) continue;
+            const int nb = b / nc, cb = b % nc;
+            const int slot = ((kVertexOff[nb][2] - kVertexOff[na][2] + 1) * 3 + (kVertexOff[nb][1] - kVertexOff[na][1] + 1)) * 3 +
+                             (kVertexOff[nb][0] - kVertexOff[na][0] + 1);
+            const double v = sc == 1.0 ? ke[a * ed + b] : sc * ke[a * ed + b];
+            acc[std::size_t(local[a]) * slots + slot * nc + cb] += v;
+          }
+        }
+      }
+  // CSR of the full symmetric matrix: columns ascending = slot order.
+  A.n = n;
+  A.ptr.assign(n + 1, 0);
+  A.idx.clear();
+  A.val.clear();
+  std::vector<int> row_node(n), row_comp(n);
+  for (int lk = 0; lk < ln; ++lk)
+    for (int lj = 0; lj < ln; ++lj)
+      for (int li = 0; li < ln; ++li)
+        for (int c = 0; c < nc; ++c) {
+          const int l = S.lnode[((std::size_t(lk) * ln + lj) * ln + li) * nc + c];
+          if (l >= 0) {
+            row_node[l] = (lk * ln + lj) * ln + li;
+            row_comp[l] = c;
+          }
+        }
+  for (int r = 0; r < n; ++r) {
+    const int rn = row_node[r];
+    const int rl = rn % ln, rm = (rn / ln) % ln, rk = rn / (ln * ln);
+    const int ra = row_comp[r];
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int ci = rl + dx, cj = rm + dy, ck = rk + dz;
+          if (ci < 0 || cj < 0 || ck < 0 || ci >= ln || cj >= ln || ck >= ln) continue;
           for (int c = 0; c < nc; ++c) {
-            const int l = lnode_local[((std::size_t(lk) * ln + lj) * ln + li) * nc + c];
-            if (l >= 0) {
-              row_node[l] = (lk * ln + lj) * ln + li;
-              row_comp[l] = c;
+            const int col = S.lnode[((std::size_t(ck) * ln + cj) * ln + ci) * nc + c];
+            if (col < 0) continue;
+            // upper entries were accumulated at (min, max)
+            double v;
+            if (col >= r) {
+              const int slot = ((dz + 1) * 3 + (dy + 1)) * 3 + (dx + 1);
+              v = acc[std::size_t(r) * slots + slot * nc + c];
+            } else {
+              const int slot = ((-dz + 1) * 3 + (-dy + 1)) * 3 + (-dx + 1);
+              v = acc[std::size_t(col) * slots + slot * nc + ra];
             }
+            A.idx.push_back(col);
+            A.val.push_back(v);
           }
-    for (int r = 0; r < n; ++r) {
-      const int rn = row_node[r];
-      const int rl = rn % ln, rm = (rn / ln) % ln, rk = rn / (ln * ln);
-      const int ra = row_comp[r];
-      for (int dz = -1; dz <= 1; ++dz)
-        for (int dy = -1; dy <= 1; ++dy)
-          for (int dx = -1; dx <= 1; ++dx) {
-            const int ci = rl + dx, cj = rm + dy, ck = rk + dz;
-            if (ci < 0 || cj < 0 || ck < 0 || ci >= ln || cj >= ln || ck >= ln) continue;
-            for (int c = 0; c < nc; ++c) {
-              const int col = lnode_local[((std::size_t(ck) * ln + cj) * ln + ci) * nc + c];
-              if (col < 0) continue;
-              // upper entries were accumulated at (min, max)
-              double v;
-              if (col >= r) {
-                const int slot = ((dz + 1) * 3 + (dy + 1)) * 3 + (dx + 1);
-                v = acc[std::size_t(r) * slots + slot * nc + c];
-              } else {
-                const int slot = ((-dz + 1) * 3 + (-dy + 1)) * 3 + (-dx + 1);
-                v = acc[std::size_t(col) * slots + slot * nc + ra];
-              }
-              A.idx.push_back(col);
-              A.val.push_back(v);
-            }
-          }
-      A.ptr[r + 1] = static_cast<int>(A.idx.size());
-    }
+        }
+    A.ptr[r + 1] = static_cast<int>(A.idx.size());
   }
 }
 
@@ -662,7 +698,33 @@ void embeddings(Model& md) {  // spaces.cpp:9-56
 
 }  // namespace
 
+namespace {
+// BDDC_B200_PROFILE=1: host phase times of Model::build on stderr
+struct BuildTimer {
+  using clk = std::chrono::steady_clock;
+  bool on;
+  clk::time_point t = clk::now();
+  std::string line;
+  BuildTimer() {
+    const char* e = std::getenv("BDDC_B200_PROFILE");
+    on = e && *e && *e != '0';
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = clk::now();
+    char buf[96];
+    std::snprintf(buf, sizeof buf, " %s=%.3fms", what, std::chrono::duration<double, std::milli>(now - t).count());
+    line += buf;
+    t = now;
+  }
+  ~BuildTimer() {
+    if (on) std::fprintf(stderr, "[profile] model build:%s\n", line.c_str());
+  }
+};
+}  // namespace
+
 void Model::build(const Problem& p) {
+  BuildTimer bt;
   spec = p;
   if (p.elements_per_edge < 1) throw Error(kBadProblemSpec, "elements per subdomain edge must be >= 1");
   for (int a = 0; a < 3; ++a)
@@ -704,9 +766,13 @@ void Model::build(const Problem& p) {
   free_count = 0;
   for (auto& d : dof)
     if (d == 0) d = free_count++;
+  bt.mark("mesh+dirichlet");
   assemble(*this);
+  bt.mark("assemble");
   classify_and_select(*this);
+  bt.mark("globs");
   embeddings(*this);
+  bt.mark("embeddings");
   // per-glob free dofs, per-subdomain glob lists and Dirichlet flags (pair index support)
   glob_dofs.resize(globs.size());
   sub_globs.assign(subs.size(), {});
@@ -718,6 +784,16 @@ void Model::build(const Problem& p) {
   for (std::size_t s = 0; s < subs.size(); ++s)
     for (int node : subs[s].nodes)
       for (int c = 0; c < nc; ++c) sub_constrained[s] |= dof[i64(node) * nc + c] < 0;
+  bt.mark("glob_lists");
+}
+
+const CSR& Model::matrix(int s) const {
+  const Subdomain& S = subs.at(s);
+  if (!S.have_A) {
+    assemble_values(*this, S, S.A);
+    S.have_A = true;
+  }
+  return S.A;
 }
 
 std::vector<i64> Model::glob_free_dofs(int gi) const {
@@ -1079,11 +1155,11 @@ PairIndex build_pair_index(const Model& md, int si, int sj) {
   }
   if (p.corner_globals.empty() && p.noncorner_globals.empty())
     throw Error(kNotAdjacent, "substructures share no interface dofs");
-  const auto& Ai = md.subs[si].A;
-  const auto& Aj = md.subs[sj].A;
+  const auto& Ai = md.subs[si].diag;
+  const auto& Aj = md.subs[sj].diag;
   for (i64 g : p.noncorner_globals) {
-    const double di = Ai.diag(md.maps.local_of(g, si));
-    const double dj = Aj.diag(md.maps.local_of(g, sj));
+    const double di = Ai[md.maps.local_of(g, si)];
+    const double dj = Aj[md.maps.local_of(g, sj)];
     p.rho_i.push_back(di / (di + dj));
   }
   // floating: neither side holds a Dirichlet-eliminated node-component

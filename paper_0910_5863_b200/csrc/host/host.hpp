@@ -117,7 +117,11 @@ struct Subdomain {  // assemble.hpp:41-51
   int id = 0;
   std::vector<int> nodes;        // ascending global node ids
   std::vector<i64> global_dof;   // local dof -> global free dof
-  CSR A;                         // full symmetric local stiffness
+  int origin[3] = {0, 0, 0};     // first element (i, j, k) of the subdomain block
+  std::vector<int> lnode;        // local node grid (x fastest) * ncomp + c -> local dof, -1 if eliminated
+  std::vector<double> diag;      // diagonal of the local stiffness (same summation order as A)
+  mutable CSR A;                 // full symmetric local stiffness, built on demand (Model::matrix)
+  mutable bool have_A = false;
   std::vector<double> load;
   std::vector<int> interior, boundary;  // spaces.cpp:119-125 (local ids, ascending)
   int dim() const { return static_cast<int>(global_dof.size()); }
@@ -182,8 +186,15 @@ struct Model {
   std::vector<std::vector<i64>> glob_dofs;   // glob_free_dofs per glob (cached)
   std::vector<std::vector<int>> sub_globs;   // globs containing each subdomain, ascending
   std::vector<char> sub_constrained;         // subdomain holds a Dirichlet dof
+  // reference element matrices (one per material, ed x ed row-major, ed = 8 ncomp)
+  // and the per-element index into them (assemble.cpp:145-169: congruent elements)
+  std::vector<std::vector<double>> ke_ref;
+  std::vector<int> element_ke;
 
   void build(const Problem& p);  // experiment.cpp:116-128
+  /// Local stiffness of substructure s (assemble.cpp:202-292); the device path
+  /// assembles the dense fronts itself, the CSR is built only when asked for.
+  const CSR& matrix(int s) const;
   std::vector<i64> glob_free_dofs(int gi) const;  // constraints.cpp:25-32
   std::vector<int> corner_nodes() const;
   i64 count(int kind) const;
