@@ -1254,6 +1254,13 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   // root front; up to kRootInverseMax rows it is augmented to [[R, .], [I, 0]] so
   // that the factorization leaves -R^{-1} and every apply is one parallel GEMV
   D.root_inv = D.NR <= kRootInverseMax;
+  // Larger roots are solved by single-CTA sweeps whose vector lives in shared
+  // memory (front_forward/backward: (n + 64) doubles of at most 200 KB).  A
+  // dense root beyond that (cfg5: ~50k primal unknowns) needs a sparse or
+  // multilevel coarse solve, which this engine does not have.
+  if (!D.root_inv && (D.NR + 64) * 8 > 200 * 1024)
+    throw Error(kError, "dense root of " + std::to_string(D.n_root) +
+                            " primal unknowns exceeds the single-GPU root solver (limit 25536)");
   const long ldR = D.root_inv ? 2L * D.NR : D.NR;
   D.R.alloc((size_t)ldR * ldR);
   D.R.zero(st);
