@@ -1253,7 +1253,11 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   D.fsolve_fwd.upload(fw, st);
   // root front; up to kRootInverseMax rows it is augmented to [[R, .], [I, 0]] so
   // that the factorization leaves -R^{-1} and every apply is one parallel GEMV
-  D.root_inv = D.NR <= kRootInverseMax;
+  {
+    const char* env = std::getenv("BDDC_B200_ROOT");  // inverse | sweep (testing override)
+    const std::string mode = env ? env : "";
+    D.root_inv = mode == "inverse" || (mode != "sweep" && D.NR <= kRootInverseMax);
+  }
   // Larger roots are solved by single-CTA sweeps whose vector lives in shared
   // memory (front_forward/backward: (n + 64) doubles of at most 200 KB).  A
   // dense root beyond that (cfg5: ~50k primal unknowns) needs a sparse or
