@@ -100,6 +100,20 @@ int bddc_b200_device_count(void);
  * (one process per GPU). */
 int bddc_b200_set_device(int device);
 
+/* Sharding over GPUs (one process or host thread per shard).
+ * Call after create and before any device work.  owner[s] = rank owning
+ * substructure s (one entry per substructure, e.g. shard.partition); face
+ * pairs belong to the owner of their lower substructure.  Every rank then
+ * returns the complete interface vectors, constraint set, root and solution.
+ * NCCL: rank 0 makes the 128-byte id with bddc_b200_nccl_unique_id and shares
+ * it; loopback: ranks are host threads of this process (tests), `group`
+ * names the set of handles that exchange with each other. */
+int bddc_b200_nccl_unique_id(unsigned char* id128);
+int bddc_b200_shard_nccl(bddc_b200_t* h, const unsigned char* id128, int rank, int world, const int* owner);
+int bddc_b200_shard_loopback(bddc_b200_t* h, int group, int rank, int world, const int* owner);
+/* Substructure lattice (nx, ny, nz), substructure ids x-fastest (mesh.cpp:68-70). */
+int bddc_b200_subdomain_lattice(const bddc_b200_t* h, int64_t* dims3);
+
 /* Build mesh, decomposition, Dirichlet map, substructure matrices, globs,
  * corners and embeddings (experiment.cpp:116-128; support.hpp:89-100). */
 int bddc_b200_create(const bddc_b200_problem* problem, bddc_b200_t** out);

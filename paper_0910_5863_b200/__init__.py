@@ -101,6 +101,10 @@ EXPORTS = {
     "bddc_b200_element_scale": (C.c_int, [P, D]),
     "bddc_b200_subdomain_matrix": (C.c_int, [P, C.c_int, I64, I64, I64, D, D]),
     "bddc_b200_leaf_front": (C.c_int, [P, C.c_int, I64, D, I64]),
+    "bddc_b200_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "bddc_b200_shard_nccl": (C.c_int, [P, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "bddc_b200_shard_loopback": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "bddc_b200_subdomain_lattice": (C.c_int, [P, I64]),
     "bddc_b200_glob_count": (C.c_int, [P, I64]),
     "bddc_b200_glob_info": (C.c_int, [P, C.c_int, C.POINTER(C.c_int), I64, I64]),
     "bddc_b200_glob_nodes": (C.c_int, [P, C.c_int, I64, I64]),
@@ -242,6 +246,13 @@ def emit_table(rows: List[Row], fmt="csv", include_times=True) -> str:
     return line(header) + line(["---"] * len(header)) + "".join(line(c) for c in body)
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0), to be broadcast to the other ranks."""
+    buf = C.create_string_buffer(128)
+    _check(load_library().bddc_b200_nccl_unique_id(buf))
+    return buf.raw
+
+
 class BDDC:
     """One problem instance: host substructuring + the device engine."""
 
@@ -300,6 +311,33 @@ class BDDC:
         if h:
             self._lib.bddc_b200_destroy(h)
             self._h = None
+
+    # --- sharding over GPUs ------------------------------------
+    def lattice(self):
+        d = np.empty(3, dtype=np.int64)
+        _check(self._lib.bddc_b200_subdomain_lattice(self._h, d.ctypes.data_as(I64)))
+        return tuple(int(x) for x in d)
+
+    def shard(self, rank: int, world: int, owner=None, backend: str = "nccl", nccl_id: bytes = None,
+              group: int = 0):
+        """Shard this handle: `owner` (default shard.partition of the lattice)
+        assigns substructures to ranks.  backend "nccl" needs the id from
+        nccl_unique_id() on rank 0, shared by the caller (torch.distributed);
+        "loopback" pairs handles of one process driven by separate threads."""
+        from . import shard as _shard
+        if owner is None:
+            owner = _shard.partition(self.lattice(), world)
+        own = np.ascontiguousarray(np.asarray(owner, dtype=np.int32))
+        self._owner = own
+        ptr = own.ctypes.data_as(C.POINTER(C.c_int))
+        if backend == "nccl":
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("nccl backend needs the 128-byte id from nccl_unique_id()")
+            _check(self._lib.bddc_b200_shard_nccl(self._h, nccl_id, rank, world, ptr))
+        elif backend == "loopback":
+            _check(self._lib.bddc_b200_shard_loopback(self._h, group, rank, world, ptr))
+        else:
+            raise ValueError("backend must be 'nccl' or 'loopback'")
 
     # --- structure and index maps (host) -----------------------------------
     def structure(self) -> dict:

@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError("CUDA build failed")
     tmp = LIB.with_suffix(".so.tmp")
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs),
-                           "-lgomp"])
+                           "-lgomp", "-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

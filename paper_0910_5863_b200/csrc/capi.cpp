@@ -70,6 +70,30 @@ int bddc_b200_set_device(int device) {
   });
 }
 
+int bddc_b200_nccl_unique_id(unsigned char* id128) {
+  return guarded([&] { nccl_unique_id(id128); });
+}
+
+int bddc_b200_shard_nccl(bddc_b200_t* h, const unsigned char* id128, int rank, int world, const int* owner) {
+  return guarded([&] {
+    std::vector<int> own(owner, owner + h->model.subs.size());
+    engine(h).set_shard(make_nccl_comm(id128, rank, world), own);
+  });
+}
+
+int bddc_b200_shard_loopback(bddc_b200_t* h, int group, int rank, int world, const int* owner) {
+  return guarded([&] {
+    std::vector<int> own(owner, owner + h->model.subs.size());
+    engine(h).set_shard(make_loopback_comm(group, rank, world), own);
+  });
+}
+
+int bddc_b200_subdomain_lattice(const bddc_b200_t* h, int64_t* dims3) {
+  return guarded([&] {
+    for (int a = 0; a < 3; ++a) dims3[a] = h->model.mesh.sub[a];
+  });
+}
+
 int bddc_b200_create(const bddc_b200_problem* p, bddc_b200_t** out) {
   return guarded([&] {
     Problem pr;

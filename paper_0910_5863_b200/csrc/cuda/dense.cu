@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 namespace b200 {
 
@@ -535,21 +537,31 @@ void configure() {
 
 std::atomic<long long> g_launches{0};
 
-// Grow-only split-K workspace (engine entry points synchronize before
-// returning, so consecutive factorizations never overlap on it).
-double* splitk_workspace(size_t doubles) {
-  static double* p = nullptr;
-  static size_t cap = 0;
-  if (doubles > cap) {
-    if (p) cudaFree(p);
-    p = nullptr;
-    if (cudaMalloc(&p, doubles * sizeof(double)) != cudaSuccess) {
-      cap = 0;
+// Grow-only split-K workspace, one per stream: work on one stream is ordered,
+// and engines (one stream each, possibly driven by different host threads of
+// one process) never share a workspace.
+double* splitk_workspace(size_t doubles, cudaStream_t stream) {
+  struct Ws {
+    double* p = nullptr;
+    size_t cap = 0;
+  };
+  static std::mutex mu;
+  static std::map<cudaStream_t, Ws> ws;
+  std::lock_guard<std::mutex> lk(mu);
+  Ws& w = ws[stream];
+  if (doubles > w.cap) {
+    if (w.p) {
+      cudaStreamSynchronize(stream);  // the old buffer may still be in use on this stream
+      cudaFree(w.p);
+    }
+    w.p = nullptr;
+    if (cudaMalloc(&w.p, doubles * sizeof(double)) != cudaSuccess) {
+      w.cap = 0;
       return nullptr;
     }
-    cap = doubles;
+    w.cap = doubles;
   }
-  return p;
+  return w.p;
 }
 
 }  // namespace
@@ -583,7 +595,7 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
       int nsplit = 1;
       if (ctas < 2L * sm_count() && K >= 8 * KC)
         nsplit = static_cast<int>(std::min<long>({16L, K / (4 * KC), (2L * sm_count() + ctas - 1) / ctas}));
-      double* work = nsplit > 1 ? splitk_workspace((size_t)ctas * nsplit * 64 * 64) : nullptr;
+      double* work = nsplit > 1 ? splitk_workspace((size_t)ctas * nsplit * 64 * 64, stream) : nullptr;
       if (nsplit > 1 && work) {
         k_syrk_column_splitk<<<dim3(tiles, batch, nsplit), GEMM_THREADS, gemm_smem, stream>>>(d_descs, j, nsplit,
                                                                                              tiles, work);

@@ -570,7 +570,8 @@ struct RootAsm {
 
 // Root front R (NR x NR, leading dimension ld).  With ld == 2 NR the front is
 // augmented as [[R, .], [I, 0]]: eliminating R leaves -R^{-1} in the trailing block.
-__global__ void k_root_assemble(int n_root, int NR, long ld, RootAsm ra, const double* Farena, double* R) {
+__global__ void k_root_assemble(int n_root, int NR, long ld, RootAsm ra, const double* Farena, double* R,
+                                bool identity) {
   const long total = (long)n_root * (n_root + 1) / 2;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
     int k1 = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
@@ -597,6 +598,7 @@ __global__ void k_root_assemble(int n_root, int NR, long ld, RootAsm ra, const d
     }
     R[(size_t)k2 * ld + k1] = s;
   }
+  if (!identity) return;
   for (long q = n_root + blockIdx.x * (long)blockDim.x + threadIdx.x; q < NR; q += (long)gridDim.x * blockDim.x)
     R[(size_t)q * ld + q] = 1.0;
   if (ld > NR)
@@ -651,6 +653,12 @@ __global__ void k_insert_boundary(const SubDesc* sd, double* MV, const long long
 // Device state
 // ---------------------------------------------------------------------------
 struct DeviceState {
+  // sharding: comm == nullptr is the single-GPU engine
+  std::shared_ptr<Comm> comm;
+  std::vector<int> owner;       // rank per substructure
+  std::vector<int> act, own;    // active (owned + ghosts) and owned substructures, ascending
+  std::vector<char> is_act, is_own;
+  int n_act = 0, n_own = 0;
   cudaStream_t st = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr, ef0 = nullptr, ef1 = nullptr, s0 = nullptr, s1 = nullptr, s2 = nullptr;
   DBuf<double> ufree;
@@ -745,6 +753,18 @@ Engine::Engine(const Model& m) : m_(m), d_(new DeviceState) {
 
 Engine::~Engine() = default;
 
+void Engine::set_shard(std::shared_ptr<Comm> comm, const std::vector<int>& owner) {
+  DeviceState& D = *d_;
+  if (D.prepared) throw Error(kError, "set_shard must precede any device work");
+  if (owner.size() != m_.subs.size()) throw Error(kError, "owner: one rank per substructure");
+  for (int r : owner)
+    if (r < 0 || r >= comm->world()) throw Error(kError, "owner rank out of range");
+  D.comm = std::move(comm);
+  D.owner = owner;
+}
+
+bool Engine::sharded() const { return d_->comm != nullptr; }
+
 cudaStream_t Engine::stream() const { return d_->st; }
 i64 Engine::interface_size() const { return static_cast<i64>(m_.maps.interface_dofs.size()); }
 int Engine::root_size() const { return d_->n_root; }
@@ -771,6 +791,25 @@ void Engine::prepare() {
   D.nsub = static_cast<int>(m.subs.size());
   D.niface = interface_size();
   const int ns = D.nsub;
+  // shard sets: owned substructures, plus the ghosts this rank's face pairs
+  // need (a pair belongs to the owner of its lower substructure, shard.py)
+  D.is_own.assign(ns, 1);
+  D.is_act.assign(ns, 1);
+  if (D.comm) {
+    const int rank = D.comm->rank();
+    for (int s = 0; s < ns; ++s) D.is_own[s] = D.owner[s] == rank;
+    D.is_act = D.is_own;
+    for (const auto& pr : face_pairs(m))
+      if (D.owner[std::min(pr.first, pr.second)] == rank) D.is_act[pr.first] = D.is_act[pr.second] = 1;
+  }
+  D.act.clear();
+  D.own.clear();
+  for (int s = 0; s < ns; ++s) {
+    if (D.is_act[s]) D.act.push_back(s);
+    if (D.is_own[s]) D.own.push_back(s);
+  }
+  D.n_act = static_cast<int>(D.act.size());
+  D.n_own = static_cast<int>(D.own.size());
   D.nI.resize(ns);
   D.nB.resize(ns);
   D.PI.resize(ns);
@@ -779,15 +818,16 @@ void Engine::prepare() {
   D.m_off.resize(ns);
   D.dm_off.resize(ns);
   D.s_off.resize(ns);
-  D.wb_off.resize(ns);
+  D.wb_off.assign(ns, 0);
   D.mv_off.resize(ns);
   long long mo = 0, dmo = 0, so = 0, wbo = 0, mvo = 0;
   for (int s = 0; s < ns; ++s) {
     const Subdomain& S = m.subs[s];
     D.nI[s] = static_cast<int>(S.interior.size());
     D.nB[s] = static_cast<int>(S.boundary.size());
-    D.PI[s] = rup(D.nI[s], kTile);
-    D.PB[s] = rup(std::max(D.nB[s], 1), kTile);
+    const bool a = D.is_act[s];  // no storage for substructures this rank never touches
+    D.PI[s] = a ? rup(D.nI[s], kTile) : 0;
+    D.PB[s] = a ? rup(std::max(D.nB[s], 1), kTile) : 0;
     D.NM[s] = D.PI[s] + D.PB[s];
     D.m_off[s] = mo;
     mo += (long long)D.NM[s] * D.NM[s];
@@ -795,29 +835,32 @@ void Engine::prepare() {
     dmo += (long long)(D.PI[s] / kTile) * kTile * kTile;
     D.s_off[s] = so;
     so += (long long)D.PB[s] * D.PB[s];
-    D.wb_off[s] = wbo;
-    wbo += D.nB[s];
     D.mv_off[s] = mvo;
     mvo += D.NM[s];
+    if (D.is_own[s]) {
+      D.wb_off[s] = wbo;
+      wbo += D.nB[s];
+    }
+    if (!a) continue;
     D.max_NM = std::max(D.max_NM, D.NM[s]);
     D.max_PI = std::max(D.max_PI, D.PI[s]);
     D.max_PB = std::max(D.max_PB, D.PB[s]);
     D.max_nB = std::max(D.max_nB, D.nB[s]);
   }
   cudaStream_t st = D.st;
-  D.M.alloc(mo);
+  D.M.alloc(std::max<long long>(mo, 1));
   D.DinvM.alloc(std::max<long long>(dmo, 1));
-  D.S.alloc(so);
-  D.MV.alloc(mvo);
-  D.MV0.alloc(mvo);
+  D.S.alloc(std::max<long long>(so, 1));
+  D.MV.alloc(std::max<long long>(mvo, 1));
+  D.MV0.alloc(std::max<long long>(mvo, 1));
   D.WB.alloc(std::max<long long>(wbo, 1));
   // host staging of the assembly inputs: element data, local numbering and
   // dense positions per substructure, loads in front layout
-  std::vector<long long> lnode_off(ns), pos_off(ns);
+  std::vector<long long> lnode_off(ns, 0), pos_off(ns, 0);
   auto& H = D.h;
   H.lnode.clear();
   H.pos.clear();
-  for (int s = 0; s < ns; ++s) {
+  for (int s : D.act) {
     const Subdomain& S = m.subs[s];
     lnode_off[s] = H.lnode.size();
     pos_off[s] = H.pos.size();
@@ -831,16 +874,17 @@ void Engine::prepare() {
   for (const auto& k : m.ke_ref) H.ke.insert(H.ke.end(), k.begin(), k.end());
   H.eke = m.element_ke;
   H.escale = m.mesh.element_scale;
-  H.mv.assign(mvo, 0.0);
-  for (int s = 0; s < ns; ++s) {
+  H.mv.assign(std::max<long long>(mvo, 1), 0.0);
+  for (int s : D.act) {
     const Subdomain& S = m.subs[s];
     for (int r = 0; r < D.nI[s]; ++r) H.mv[D.mv_off[s] + r] = S.load[S.interior[r]];
     for (int b = 0; b < D.nB[s]; ++b) H.mv[D.mv_off[s] + D.PI[s] + b] = S.load[S.boundary[b]];
   }
-  // interface maps and averaging weights (spaces.cpp:71-86)
-  H.biface.assign(wbo, 0);
-  H.bw.assign(wbo, 0.0);
-  for (int s = 0; s < ns; ++s) {
+  // interface maps and averaging weights (spaces.cpp:71-86); the weights use
+  // every copy of a dof, the copy lists only this rank's copies
+  H.biface.assign(std::max<long long>(wbo, 1), 0);
+  H.bw.assign(std::max<long long>(wbo, 1), 0.0);
+  for (int s : D.own) {
     const Subdomain& S = m.subs[s];
     for (int b = 0; b < D.nB[s]; ++b) {
       const i64 g = S.global_dof[S.boundary[b]];
@@ -852,7 +896,7 @@ void Engine::prepare() {
     }
   }
   std::vector<std::vector<int>> lists(D.niface);
-  for (int s = 0; s < ns; ++s)
+  for (int s : D.own)
     for (int b = 0; b < D.nB[s]; ++b) lists[H.biface[D.wb_off[s] + b]].push_back(static_cast<int>(D.wb_off[s] + b));
   H.icp.assign(D.niface + 1, 0);
   H.icpos.clear();
@@ -871,32 +915,45 @@ void Engine::prepare() {
   D.bw.alloc(std::max<long long>(wbo, 1));
   D.icopy_ptr.alloc(H.icp.size());
   D.icopy_pos.alloc(std::max<std::size_t>(H.icpos.size(), 1));
-  D.minfo.alloc(ns);
+  D.minfo.alloc(std::max(D.n_act, 1));
   D.rhs.alloc(std::max<i64>(D.niface, 1));
-  std::vector<AsmDesc> ad(ns);
-  std::vector<FrontDesc> fd(ns);
-  std::vector<SolveDesc> sv(ns);
-  std::vector<TrailDesc> td(ns);
-  std::vector<SubDesc> sd(ns);
-  for (int s = 0; s < ns; ++s) {
+  // descriptors: leaf fronts over the active substructures, interface
+  // operators over the owned ones (compacted, in ascending order)
+  std::vector<AsmDesc> ad;
+  std::vector<FrontDesc> fd;
+  std::vector<SolveDesc> sv;
+  std::vector<TrailDesc> td;
+  for (int q = 0; q < D.n_act; ++q) {
+    const int s = D.act[q];
     const Subdomain& S = m.subs[s];
-    ad[s] = AsmDesc{D.M.p + D.m_off[s], D.asm_lnode.p + lnode_off[s], D.asm_pos.p + pos_off[s], D.NM[s], D.nI[s],
-                    D.PI[s], D.nB[s], S.origin[0], S.origin[1], S.origin[2]};
-    fd[s] = FrontDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.NM[s], D.PI[s], D.minfo.p + s, 0};
-    sv[s] = SolveDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.MV.p + D.mv_off[s], D.NM[s], D.PI[s],
-                      nullptr, nullptr};
-    td[s] = TrailDesc{D.M.p + D.m_off[s], D.S.p + D.s_off[s], D.NM[s], D.PI[s]};
-    sd[s] = SubDesc{D.S.p + D.s_off[s], nullptr, nullptr, D.biface.p + D.wb_off[s], D.bw.p + D.wb_off[s],
-                    nullptr, nullptr, nullptr, D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], 0, 0};
+    ad.push_back(AsmDesc{D.M.p + D.m_off[s], D.asm_lnode.p + lnode_off[s], D.asm_pos.p + pos_off[s], D.NM[s], D.nI[s],
+                         D.PI[s], D.nB[s], S.origin[0], S.origin[1], S.origin[2]});
+    fd.push_back(FrontDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.NM[s], D.PI[s], D.minfo.p + q, 0});
+    sv.push_back(SolveDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.MV.p + D.mv_off[s], D.NM[s], D.PI[s],
+                           nullptr, nullptr});
+    td.push_back(TrailDesc{D.M.p + D.m_off[s], D.S.p + D.s_off[s], D.NM[s], D.PI[s]});
   }
-  D.asmdesc.upload(ad, st);
-  D.mfront.upload(fd, st);
-  D.msolve.upload(sv, st);
-  D.mtrail.upload(td, st);
-  D.subdesc.upload(sd, st);
-  D.d_mvoff.upload(D.mv_off, st);
-  D.d_PI.upload(D.PI, st);
+  std::vector<SubDesc> sd;
+  std::vector<long long> mvo_own;
+  std::vector<int> pi_own;
+  for (int s : D.own) {
+    sd.push_back(SubDesc{D.S.p + D.s_off[s], nullptr, nullptr, D.biface.p + D.wb_off[s], D.bw.p + D.wb_off[s],
+                         nullptr, nullptr, nullptr, D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], 0, 0});
+    mvo_own.push_back(D.mv_off[s]);
+    pi_own.push_back(D.PI[s]);
+  }
+  auto up = [&](auto& buf, const auto& v) {
+    if (v.empty()) buf.alloc(1); else buf.upload(v, st);
+  };
+  up(D.asmdesc, ad);
+  up(D.mfront, fd);
+  up(D.msolve, sv);
+  up(D.mtrail, td);
+  up(D.subdesc, sd);
+  up(D.d_mvoff, mvo_own);
+  up(D.d_PI, pi_own);
   D.pairs.attach(m, D.S.p, D.s_off, D.PB, D.nB, st);
+  if (D.comm) D.pairs.set_shard(D.comm, D.owner);
   D.prepared = true;
   upload_inputs();
   CK(cudaStreamSynchronize(st));
@@ -932,44 +989,48 @@ void Engine::analysis() {
 void Engine::analysis_launch() {
   prepare();
   DeviceState& D = *d_;
-  const int ns = D.nsub;
+  const int na = D.n_act;
   cudaStream_t st = D.st;
   CK(cudaEventRecord(D.e0, st));
   D.M.zero(st);
   D.minfo.zero(st);
-  k_assemble_front<<<dim3(64, ns), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
-  count_launch(1);
+  if (na) {
+    k_assemble_front<<<dim3(64, na), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
+    count_launch(1);
+  }
   CK(cudaGetLastError());
   CK(cudaEventRecord(D.ef0, st));
-  partial_cholesky(D.mfront.p, ns, D.max_NM, D.max_PI, D.max_PB, st);
+  partial_cholesky(D.mfront.p, na, D.max_NM, D.max_PI, D.max_PB, st);
   CK(cudaEventRecord(D.ef1, st));
   CK(cudaGetLastError());
-  copy_trailing_full(D.mtrail.p, ns, D.max_PB, st);
-  count_launch(1);
+  copy_trailing_full(D.mtrail.p, na, D.max_PB, st);
   CK(cudaGetLastError());
   // condensed rhs: forward sweep on [f_I; f_B], then sum the boundary rows over copies
   CK(cudaMemcpyAsync(D.MV.p, D.MV0.p, D.MV.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  front_forward(D.msolve.p, ns, D.max_NM, st);
-  k_extract_boundary<<<ns, 256, 0, st>>>(D.subdesc.p, D.MV.p, D.d_mvoff.p, D.d_PI.p);
+  front_forward(D.msolve.p, na, D.max_NM, st);
+  if (D.n_own) {
+    k_extract_boundary<<<D.n_own, 256, 0, st>>>(D.subdesc.p, D.MV.p, D.d_mvoff.p, D.d_PI.p);
+    count_launch(1);
+  }
   k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, D.rhs.p, nullptr, nullptr, nullptr);
-  count_launch(3);
+  count_launch(1);
   CK(cudaGetLastError());
+  if (D.comm) D.comm->allreduce(D.rhs.p, D.niface, st);  // interface neighbour exchange
   CK(cudaEventRecord(D.e1, st));
 }
 
 // waits for analysis_launch's work, checks the pivots
 void Engine::analysis_finish() {
   DeviceState& D = *d_;
-  const int ns = D.nsub;
   times_.analysis = elapsed(D.e0, D.e1);
   times_.leaf_factor = elapsed(D.ef0, D.ef1);
-  std::vector<int> info(ns);
-  CK(cudaMemcpy(info.data(), D.minfo.p, ns * sizeof(int), cudaMemcpyDeviceToHost));
-  for (int s = 0; s < ns; ++s)
-    if (info[s]) throw Error(kNotPositiveDefinite, "factorize: A_II of substructure " + std::to_string(s) +
+  std::vector<int> info(std::max(D.n_act, 1));
+  CK(cudaMemcpy(info.data(), D.minfo.p, info.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int q = 0; q < D.n_act; ++q)
+    if (info[q]) throw Error(kNotPositiveDefinite, "factorize: A_II of substructure " + std::to_string(D.act[q]) +
                                                        " is not positive definite");
   double fl = 0;
-  for (int s = 0; s < ns; ++s) {
+  for (int s : D.act) {
     const double ni = D.nI[s], nb = D.nB[s];
     fl += ni * ni * ni / 3.0 + ni * ni * nb + ni * nb * nb;
   }
@@ -978,17 +1039,18 @@ void Engine::analysis_finish() {
 
 double Engine::schur_bytes() const {
   double b = 0;
-  for (int s = 0; s < d_->nsub; ++s) b += double(d_->nB[s]) * d_->nB[s] * 8.0;
+  for (int s : d_->own) b += double(d_->nB[s]) * d_->nB[s] * 8.0;
   return b;
 }
 
 double Engine::leaf_front_bytes() const {
   const DeviceState& D = *d_;
   double b = 0;
-  for (int s = 0; s < D.nsub && s < (int)D.NF.size(); ++s) {
-    const double e = D.nE[s], c = D.nC[s];
-    b += (D.leaf_explicit ? e * e + c * e : e * (e + 1) / 2 + c * e) * 8.0;
-  }
+  if (D.NF.size() == std::size_t(D.nsub))
+    for (int s : D.own) {
+      const double e = D.nE[s], c = D.nC[s];
+      b += (D.leaf_explicit ? e * e + c * e : e * (e + 1) / 2 + c * e) * 8.0;
+    }
   b += double(D.n_root) * (D.n_root + 1) / 2 * 8.0;
   return b;
 }
@@ -1005,10 +1067,12 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   HostTimer ht("set_constraints");
   const ChangeOfVariables cov = change_of_variables(cs, m);
   ht.mark("change_of_variables");
-  // boundary position of each local dof
+  // boundary position of each local dof (owned substructures)
   std::vector<std::vector<int>> bpos_of(ns);
+  const int no = D.n_own;
 #pragma omp parallel for schedule(dynamic, 4)
-  for (int s = 0; s < ns; ++s) {
+  for (int q = 0; q < no; ++q) {
+    const int s = D.own[q];
     bpos_of[s].assign(m.subs[s].dim(), -1);
     for (int b = 0; b < D.nB[s]; ++b) bpos_of[s][m.subs[s].boundary[b]] = b;
   }
@@ -1027,12 +1091,15 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     tr_off_d[k] = nd_total;
     np_total += gt.n;
     nd_total += gt.rank * gt.n;
-    tr_inst0[k + 1] = tr_inst0[k] + static_cast<int>(m.globs[gt.glob].subdomains.size());
-    for (std::size_t q = 0; q < m.globs[gt.glob].subdomains.size(); ++q) {
+    int ninst = 0;
+    for (int sq : m.globs[gt.glob].subdomains) {
+      if (!D.is_own[sq]) continue;  // instances of this rank's substructures only
       inst_tr.push_back(k);
       inst_pos.push_back(ntpos);
       ntpos += gt.n;
+      ++ninst;
     }
+    tr_inst0[k + 1] = tr_inst0[k] + ninst;
   }
   std::vector<int> perm(np_total), iperm(np_total), tpos(ntpos);
   std::vector<double> trD(nd_total);
@@ -1050,6 +1117,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     const auto& dofs = m.glob_dofs[gt.glob];
     int inst = tr_inst0[k];
     for (int s : m.globs[gt.glob].subdomains) {
+      if (!D.is_own[s]) continue;
       for (int a = 0; a < n; ++a) {
         const int b = bpos_of[s][m.maps.local_of(dofs[a], s)];
         tpos[inst_pos[inst] + a] = b;
@@ -1061,11 +1129,12 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   }
   ht.mark("transforms");
   // composite slot positions and the per-subdomain constrained-row work lists
-  std::vector<int> cpos(tpos.size()), inst_loff(inst_tr.size()), item_ptr(ns + 1, 0), item_inst, item_row;
+  std::vector<int> cpos(tpos.size()), inst_loff(inst_tr.size()), item_ptr(no + 1, 0), item_inst, item_row;
   {
     std::vector<int> inst_sub(inst_tr.size());
     for (std::size_t k = 0, inst = 0; k < cov.transforms.size(); ++k)
-      for (int s : m.globs[cov.transforms[k].glob].subdomains) inst_sub[inst++] = s;
+      for (int s : m.globs[cov.transforms[k].glob].subdomains)
+        if (D.is_own[s]) inst_sub[inst++] = s;
     std::vector<std::vector<int>> by_sub(ns);
     for (std::size_t inst = 0; inst < inst_tr.size(); ++inst) {
       const int tr = inst_tr[inst];
@@ -1073,7 +1142,8 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       by_sub[inst_sub[inst]].push_back(static_cast<int>(inst));
     }
     D.max_rows = 0;
-    for (int s = 0; s < ns; ++s) {
+    for (int q = 0; q < no; ++q) {  // compacted over the owned substructures (k_prolong's blocks)
+      const int s = D.own[q];
       int off = 0;
       for (int inst : by_sub[s]) {
         inst_loff[inst] = off;
@@ -1083,7 +1153,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
         }
         off += tr_r[inst_tr[inst]];
       }
-      item_ptr[s + 1] = static_cast<int>(item_inst.size());
+      item_ptr[q + 1] = static_cast<int>(item_inst.size());
       D.max_rows = std::max(D.max_rows, off);
     }
   }
@@ -1092,7 +1162,8 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   std::vector<std::vector<int>> coarse_b(ns), coarse_root(ns);
   const i64 ncd = m.maps.corner_dof_count;
 #pragma omp parallel for schedule(dynamic, 4)
-  for (int s = 0; s < ns; ++s) {
+  for (int q = 0; q < no; ++q) {
+    const int s = D.own[q];
     const Subdomain& S = m.subs[s];
     std::vector<std::pair<i64, int>> cors;
     for (int b = 0; b < D.nB[s]; ++b) {
@@ -1108,6 +1179,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   for (std::size_t g = 0; g < cov.groups.size(); ++g)
     for (std::size_t t = 0; t < cov.group_subs[g].size(); ++t) {
       const int s = cov.group_subs[g][t];
+      if (!D.is_own[s]) continue;
       coarse_b[s].push_back(bpos_of[s][cov.group_local[g][t]]);
       coarse_root[s].push_back(static_cast<int>(ncd + g));
     }
@@ -1123,7 +1195,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   D.df_off.assign(ns, 0);
   D.fv_off.assign(ns, 0);
   std::vector<int> posF(D.WB.n, 0), cmap, pads, pad_sub;
-  std::vector<long long> cmap_off(ns), pad_off(ns + 1), xoff(ns);
+  std::vector<long long> cmap_off(ns), pad_off(ns + 1), xoff;
   long long fo = 0, dfo = 0, fvo = 0, xo = 0;
   D.max_NF = D.max_PE = D.max_M = D.max_NA = D.max_MA = 0;
   D.NA.assign(ns, 0);
@@ -1134,10 +1206,10 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     // = explicit | factor overrides)
     const char* env = std::getenv("BDDC_B200_LEAF");
     const std::string mode = env ? env : "";
-    D.leaf_explicit = mode == "explicit" || (mode != "factor" && ns < sm_count());
+    D.leaf_explicit = mode == "explicit" || (mode != "factor" && no < sm_count());
   }
   std::vector<int> root_cnt(D.n_root + 1, 0);
-  for (int s = 0; s < ns; ++s) {
+  for (int s : D.own) {
     const int nB = D.nB[s], nC = static_cast<int>(coarse_b[s].size()), nE = nB - nC;
     D.nE[s] = nE;
     D.nC[s] = nC;
@@ -1152,7 +1224,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     dfo += (long long)(D.PE[s] / kTile) * kTile * kTile;
     D.fv_off[s] = fvo;
     fvo += D.NF[s];
-    xoff[s] = xo;
+    xoff.push_back(xo);  // compacted (k_colxform's blocks)
     xo += (long long)D.PB[s] * D.PB[s];
     D.max_NF = std::max(D.max_NF, D.NF[s]);
     D.max_PE = std::max(D.max_PE, D.PE[s]);
@@ -1186,7 +1258,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   std::vector<long long> rsrc(rptr.back());
   {
     std::vector<int> fill(rptr.begin(), rptr.end() - 1);
-    for (int s = 0; s < ns; ++s)
+    for (int s : D.own)
       for (int c = 0; c < D.nC[s]; ++c) {
         const int k = coarse_root[s][c];
         rsub[fill[k]] = s;
@@ -1222,35 +1294,39 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   D.xf = XformDesc{D.inst_tr.p, D.inst_pos.p, D.tpos.p, D.tr_n.p, D.tr_r.p, D.tr_off_perm.p, D.tr_off_d.p,
                    D.perm.p, D.iperm.p, D.trD.p, D.cpos.p, D.item_ptr.p, D.item_inst.p, D.item_row.p,
                    D.inst_loff.p};
-  D.F.alloc(fo);
+  D.F.alloc(std::max<long long>(fo, 1));
   D.F.zero(st);
   D.DinvF.alloc(std::max<long long>(dfo, 1));
-  D.FV.alloc(fvo);
+  D.FV.alloc(std::max<long long>(fvo, 1));
   D.FV.zero(st);
   if (D.leaf_explicit) {
-    D.FV2.alloc(fvo);
+    D.FV2.alloc(std::max<long long>(fvo, 1));
     D.FV2.zero(st);
     D.E.alloc(std::max<long long>(eo, 1));
   }
-  D.Xtmp.alloc(xo);
-  D.d_xoff.upload(xoff, st);
-  D.finfo.alloc(ns);
+  D.Xtmp.alloc(std::max<long long>(xo, 1));
+  if (xoff.empty()) D.d_xoff.alloc(1); else D.d_xoff.upload(xoff, st);
+  D.finfo.alloc(std::max(no, 1));
   D.finfo.zero(st);
-  std::vector<SubDesc> sd(ns);
-  std::vector<FrontDesc> fd(ns);
-  std::vector<SolveDesc> fw(ns), bw(ns);
-  for (int s = 0; s < ns; ++s) {
-    sd[s] = SubDesc{D.S.p + D.s_off[s], D.F.p + D.f_off[s], D.FV.p + D.fv_off[s], D.biface.p + D.wb_off[s],
+  std::vector<SubDesc> sd(no);
+  std::vector<FrontDesc> fd(no);
+  std::vector<SolveDesc> fw(no), bw(no);
+  for (int q = 0; q < no; ++q) {
+    const int s = D.own[q];
+    sd[q] = SubDesc{D.S.p + D.s_off[s], D.F.p + D.f_off[s], D.FV.p + D.fv_off[s], D.biface.p + D.wb_off[s],
                     D.bw.p + D.wb_off[s], D.bposF.p + D.wb_off[s], D.bglob.p + D.wb_off[s],
                     D.bslot.p + D.wb_off[s], D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], D.NF[s], D.PE[s], D.NA[s]};
-    fd[s] = FrontDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.NA[s], D.PE[s], D.finfo.p + s,
+    fd[q] = FrontDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.NA[s], D.PE[s], D.finfo.p + q,
                       D.leaf_explicit ? D.NF[s] : 0};
-    fw[s] = SolveDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.FV.p + D.fv_off[s], D.NF[s], D.PE[s],
+    fw[q] = SolveDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.FV.p + D.fv_off[s], D.NF[s], D.PE[s],
                       nullptr, nullptr};
   }
-  D.subdesc.upload(sd, st);
-  D.ffront.upload(fd, st);
-  D.fsolve_fwd.upload(fw, st);
+  auto up_v = [&](auto& b, const auto& v) {
+    if (v.empty()) b.alloc(1); else b.upload(v, st);
+  };
+  up_v(D.subdesc, sd);
+  up_v(D.ffront, fd);
+  up_v(D.fsolve_fwd, fw);
   // root front; up to kRootInverseMax rows it is augmented to [[R, .], [I, 0]] so
   // that the factorization leaves -R^{-1} and every apply is one parallel GEMV
   {
@@ -1274,18 +1350,20 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   if (D.root_inv) D.Rinv.alloc((size_t)D.NR * D.NR);
   D.rinfo.alloc(1);
   D.rinfo.zero(st);
-  for (int s = 0; s < ns; ++s) {
-    bw[s] = fw[s];
-    bw[s].cmap = D.cmap.p + cmap_off[s];
-    bw[s].croot = D.root_inv ? D.xroot2.p : D.xroot.p;
+  for (int q = 0; q < no; ++q) {
+    bw[q] = fw[q];
+    bw[q].cmap = D.cmap.p + cmap_off[D.own[q]];
+    bw[q].croot = D.root_inv ? D.xroot2.p : D.xroot.p;
   }
-  D.fsolve_bwd.upload(bw, st);
+  up_v(D.fsolve_bwd, bw);
   if (D.leaf_explicit) {
-    std::vector<LeafX> lx(ns);
-    for (int s = 0; s < ns; ++s)
-      lx[s] = LeafX{D.F.p + D.f_off[s], D.E.p + e_off[s], D.FV.p + D.fv_off[s], D.FV2.p + D.fv_off[s],
+    std::vector<LeafX> lx(no);
+    for (int q = 0; q < no; ++q) {
+      const int s = D.own[q];
+      lx[q] = LeafX{D.F.p + D.f_off[s], D.E.p + e_off[s], D.FV.p + D.fv_off[s], D.FV2.p + D.fv_off[s],
                     D.cmap.p + cmap_off[s], D.NA[s], D.PE[s], D.NF[s] - D.PE[s]};
-    D.leafx.upload(lx, st);
+    }
+    up_v(D.leafx, lx);
   }
   up_i(D.root_ptr, rptr);
   up_i(D.root_sub, rsub);
@@ -1299,28 +1377,34 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   ht.mark("uploads");
   StageProfiler prof("set_constraints", st);
   // F = P (T^T S T) P^T, pads identity
-  k_colxform<<<dim3(D.max_PB, ns), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
-  k_rowxform_scatter<<<dim3(D.max_PB, ns), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
+  if (no) {
+    k_colxform<<<dim3(D.max_PB, no), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
+    k_rowxform_scatter<<<dim3(D.max_PB, no), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
+  }
   if (!pads.empty())
     k_pad_identity<<<std::min<int>(1024, (static_cast<int>(pads.size()) + 255) / 256), 256, 0, st>>>(
         D.F.p, D.d_foff.p, D.d_NF.p, D.pad_sub.p, D.pads.p, static_cast<int>(pads.size()));
   count_launch(3);
-  if (D.leaf_explicit) {
-    k_aug_identity<<<dim3((D.max_PE + 255) / 256, ns), 256, 0, st>>>(D.leafx.p);
+  if (D.leaf_explicit && no) {
+    k_aug_identity<<<dim3((D.max_PE + 255) / 256, no), 256, 0, st>>>(D.leafx.p);
     count_launch(1);
   }
   CK(cudaGetLastError());
   prof.mark("xform");
-  partial_cholesky(D.ffront.p, ns, D.max_NA, D.max_PE, D.max_MA, st);
-  if (D.leaf_explicit) {
-    k_leaf_explicit_copy<<<dim3(256, ns), 256, 0, st>>>(D.leafx.p);
+  partial_cholesky(D.ffront.p, no, D.max_NA, D.max_PE, D.max_MA, st);
+  if (D.leaf_explicit && no) {
+    k_leaf_explicit_copy<<<dim3(256, no), 256, 0, st>>>(D.leafx.p);
     count_launch(1);
   }
   CK(cudaGetLastError());
   prof.mark(D.leaf_explicit ? "cholF+explicit" : "cholF");
   RootAsm ra{D.root_ptr.p, D.root_sub.p, D.root_c.p, D.d_foff.p, D.d_NF.p, D.d_PE.p};
-  k_root_assemble<<<1024, 256, 0, st>>>(D.n_root, D.NR, ldR, ra, D.F.p, D.R.p);
+  // this rank's leaf contributions (+ the identity blocks on rank 0), then the
+  // gather of the root front: an allreduce of its first N_R columns
+  const bool identity = !D.comm || D.comm->rank() == 0;
+  k_root_assemble<<<1024, 256, 0, st>>>(D.n_root, D.NR, ldR, ra, D.F.p, D.R.p, identity);
   count_launch(1);
+  if (D.comm) D.comm->allreduce(D.R.p, (size_t)ldR * D.NR, st);
   std::vector<FrontDesc> rf{FrontDesc{D.R.p, D.DinvR.p, static_cast<int>(ldR), D.NR, D.rinfo.p, D.root_inv ? D.NR : 0}};
   D.rfront.upload(rf, st);
   prof.mark("root_asm");
@@ -1336,10 +1420,10 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   CK(cudaGetLastError());
   CK(cudaEventRecord(D.e1, st));
   times_.preconditioner = elapsed(D.e0, D.e1);
-  std::vector<int> info(ns);
-  CK(cudaMemcpy(info.data(), D.finfo.p, ns * sizeof(int), cudaMemcpyDeviceToHost));
-  for (int s = 0; s < ns; ++s)
-    if (info[s]) throw Error(kNotPositiveDefinite, "factorize: transformed leaf front " + std::to_string(s) +
+  std::vector<int> info(std::max(no, 1));
+  CK(cudaMemcpy(info.data(), D.finfo.p, info.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int q = 0; q < no; ++q)
+    if (info[q]) throw Error(kNotPositiveDefinite, "factorize: transformed leaf front " + std::to_string(D.own[q]) +
                                                        " is not positive definite");
   int rinfo = 0;
   CK(cudaMemcpy(&rinfo, D.rinfo.p, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1360,26 +1444,41 @@ void Engine::set_constraints(const ConstraintSet& cs) {
 // operator applications
 // ---------------------------------------------------------------------------
 namespace {
+// Sharded: this rank's copies are summed, then the interface neighbour
+// exchange (allreduce of the interface vector) completes every dof, and the
+// dot product is taken on the complete vector.
+void finish_interface(DeviceState& D, double* y, const double* dot_with, double* partials, const int* done) {
+  cudaStream_t st = D.st;
+  if (!D.comm) return;
+  D.comm->allreduce(y, D.niface, st);
+  if (partials) {
+    k_dot<<<kRed, 256, 0, st>>>(D.niface, dot_with, y, partials);
+    count_launch(1);
+  }
+  (void)done;
+}
+
 void launch_precond(DeviceState& D, const double* r, double* z, const double* dot_with, double* partials,
                     const int* done, StageProfiler* prof = nullptr) {
   cudaStream_t st = D.st;
-  const int ns = D.nsub;
+  const int ns = D.n_own;
   const int smem_b = D.max_nB * sizeof(double);
   auto mark = [&](const char* s) {
     if (prof) prof->mark(s);
   };
-  k_restrict<<<ns, 256, smem_b, st>>>(D.subdesc.p, D.xf, r, done);
+  if (ns) k_restrict<<<ns, 256, smem_b, st>>>(D.subdesc.p, D.xf, r, done);
   count_launch(4);
   mark("restrict");
-  if (D.leaf_explicit) {
+  if (D.leaf_explicit && ns) {
     k_leaf_fwd_explicit<<<dim3((D.max_NF + 7) / 8, ns), 256, D.max_PE * sizeof(double), st>>>(D.leafx.p, done);
     count_launch(1);
-  } else {
+  } else if (!D.leaf_explicit) {
     front_forward(D.fsolve_fwd.p, ns, D.max_NF, st, done);
   }
   mark("leaf_fwd");
   k_root_gather<<<std::max(1, std::min(1024, (D.NR + 255) / 256)), 256, 0, st>>>(
       D.n_root, D.NR, D.root_ptr.p, D.root_src.p, D.leaf_explicit ? D.FV2.p : D.FV.p, D.xroot.p, done);
+  if (D.comm) D.comm->allreduce(D.xroot.p, D.NR, st);  // root right-hand side of every rank
   mark("root_gather");
   if (D.root_inv) {
     k_root_gemv<<<std::min(1184, (D.NR + 7) / 8), 256, 0, st>>>(D.NR, D.Rinv.p, D.xroot.p, D.xroot2.p, done);
@@ -1391,27 +1490,32 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     front_backward(D.rsolve.p, 1, D.NR, st, done);
     mark("root_bwd");
   }
-  if (D.leaf_explicit) {
+  if (D.leaf_explicit && ns) {
     k_leaf_bwd_explicit<<<dim3(D.max_NF / kTile, ns), 256, D.max_M * sizeof(double), st>>>(
         D.leafx.p, D.root_inv ? D.xroot2.p : D.xroot.p, done);
     count_launch(1);
-  } else {
+  } else if (!D.leaf_explicit) {
     front_backward(D.fsolve_bwd.p, ns, D.max_NF, st, done);
   }
   mark("leaf_bwd");
-  k_prolong<<<ns, 256, smem_b + D.max_rows * sizeof(double), st>>>(D.subdesc.p, D.xf, done);
+  if (ns) k_prolong<<<ns, 256, smem_b + D.max_rows * sizeof(double), st>>>(D.subdesc.p, D.xf, done);
   mark("prolong");
-  k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, z, dot_with, partials, done);
+  k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, z, D.comm ? nullptr : dot_with,
+                                     D.comm ? nullptr : partials, done);
+  finish_interface(D, z, dot_with, partials, done);
   mark("sum_copies");
 }
 
 void launch_schur(DeviceState& D, const double* x, double* y, const double* dot_with, double* partials,
                   const int* done) {
   cudaStream_t st = D.st;
-  k_schur_gemv_rows<<<dim3((D.max_nB + 63) / 64, D.nsub), 256, D.max_nB * sizeof(double), st>>>(D.subdesc.p, x,
-                                                                                               done);
+  if (D.n_own)
+    k_schur_gemv_rows<<<dim3((D.max_nB + 63) / 64, D.n_own), 256, D.max_nB * sizeof(double), st>>>(D.subdesc.p, x,
+                                                                                                  done);
   count_launch(2);
-  k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, y, dot_with, partials, done);
+  k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, y, D.comm ? nullptr : dot_with,
+                                     D.comm ? nullptr : partials, done);
+  finish_interface(D, y, dot_with, partials, done);
 }
 
 void ensure_vectors(DeviceState& D) {
@@ -1434,13 +1538,17 @@ void Engine::leaf_front(int s, std::vector<double>* out, std::vector<int>* pos, 
   DeviceState& D = *d_;
   *ld = D.NM[s];
   const Subdomain& S = m_.subs[s];
+  if (!D.is_act[s]) throw Error(kError, "substructure not held by this shard");
   std::size_t off = 0;
-  for (int q = 0; q < s; ++q) off += m_.subs[q].dim();
+  for (int q : D.act) {
+    if (q == s) break;
+    off += m_.subs[q].dim();
+  }
   pos->assign(D.h.pos.begin() + off, D.h.pos.begin() + off + S.dim());
   if (!out) return;
   cudaStream_t st = D.st;
   D.M.zero(st);
-  k_assemble_front<<<dim3(64, D.nsub), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
+  k_assemble_front<<<dim3(64, D.n_act), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
   count_launch(1);
   CK(cudaGetLastError());
   out->resize((size_t)D.NM[s] * D.NM[s]);
@@ -1482,11 +1590,13 @@ void Engine::rhs(double* out) {
 void Engine::recover_device(const double* d_uiface, double* d_ufree) {
   DeviceState& D = *d_;
   const Model& m = m_;
-  const int ns = D.nsub;
   cudaStream_t st = D.st;
+  // sharded: interiors of the owned substructures; the interface values from
+  // rank 0; the rest zero, summed over ranks
+  const bool iface_here = !D.comm || D.comm->rank() == 0;
   if (D.sol_gdof.n == 0) {
     std::vector<long long> g(D.MV.n, -1), ig(m.maps.interface_dofs.begin(), m.maps.interface_dofs.end());
-    for (int s = 0; s < ns; ++s) {
+    for (int s : D.own) {
       const Subdomain& S = m.subs[s];
       for (int r = 0; r < D.nI[s]; ++r) g[D.mv_off[s] + r] = S.global_dof[S.interior[r]];
     }
@@ -1494,14 +1604,16 @@ void Engine::recover_device(const double* d_uiface, double* d_ufree) {
     if (ig.empty()) ig.push_back(0);
     D.iface_gdof.upload(ig, st);
   }
+  if (D.comm) CK(cudaMemsetAsync(d_ufree, 0, m.free_count * sizeof(double), st));
   CK(cudaMemcpyAsync(D.MV.p, D.MV0.p, D.MV.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  front_forward(D.msolve.p, ns, D.max_NM, st);
-  k_insert_boundary<<<ns, 256, 0, st>>>(D.subdesc.p, D.MV.p, D.d_mvoff.p, D.d_PI.p, d_uiface);
-  front_backward(D.msolve.p, ns, D.max_NM, st);
-  k_scatter_solution<<<256, 256, 0, st>>>(static_cast<long long>(D.MV.n), D.sol_gdof.p, D.MV.p, D.niface,
-                                          D.iface_gdof.p, d_uiface, d_ufree);
+  front_forward(D.msolve.p, D.n_act, D.max_NM, st);
+  if (D.n_own) k_insert_boundary<<<D.n_own, 256, 0, st>>>(D.subdesc.p, D.MV.p, D.d_mvoff.p, D.d_PI.p, d_uiface);
+  front_backward(D.msolve.p, D.n_act, D.max_NM, st);
+  k_scatter_solution<<<256, 256, 0, st>>>(static_cast<long long>(D.MV.n), D.sol_gdof.p, D.MV.p,
+                                          iface_here ? D.niface : 0, D.iface_gdof.p, d_uiface, d_ufree);
   count_launch(2);
   CK(cudaGetLastError());
+  if (D.comm) D.comm->allreduce(d_ufree, m.free_count, st);
 }
 
 void Engine::recover(const double* u_interface, double* u_free) {
@@ -1574,28 +1686,44 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
     return out;
   }
   CK(cudaMemcpyAsync(D.pst.p, &h, sizeof(h), cudaMemcpyHostToDevice, st));
-  // capture one iteration as a graph (pcg.cpp:49-70)
-  if (!D.gexec) {
-    const long long before = launch_count();
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    const int* done = &D.pst.p->done;
-    launch_schur(D, D.vp.p, D.vq.p, D.vp.p, D.part_a.p, done);
-    k_alpha_axpy<<<kRed, kRed, 0, st>>>(n, D.pst.p, D.vx.p, D.vr.p, D.vp.p, D.vq.p, D.part_a.p, D.part_b.p,
-                                         D.alphas.p);
-    launch_precond(D, D.vr.p, D.vz.p, D.vr.p, D.part_a.p, done);
-    k_beta_update<<<kRed, kRed, 0, st>>>(n, D.pst.p, D.vp.p, D.vz.p, D.part_a.p, D.part_b.p, D.betas.p);
-    CK(cudaStreamEndCapture(st, &D.graph));
-    CK(cudaGraphInstantiate(&D.gexec, D.graph, 0));
-    D.graph_kernels = launch_count() - before + 2;  // + k_alpha_axpy, k_beta_update
-    count_launch(-(launch_count() - before));
-  }
   PcgState hs = h;
-  const int chunk = 8;
-  while (!hs.done) {
-    for (int c = 0; c < chunk; ++c) CK(cudaGraphLaunch(D.gexec, st));
-    count_launch(chunk * D.graph_kernels);
-    CK(cudaMemcpyAsync(&hs, D.pst.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+  if (D.comm) {
+    // sharded: the iteration runs eagerly (its exchanges may synchronize the
+    // host); every rank holds the same complete vectors and scalars, so the
+    // iterations stay in lockstep
+    while (!hs.done) {
+      launch_schur(D, D.vp.p, D.vq.p, D.vp.p, D.part_a.p, nullptr);
+      k_alpha_axpy<<<kRed, kRed, 0, st>>>(n, D.pst.p, D.vx.p, D.vr.p, D.vp.p, D.vq.p, D.part_a.p, D.part_b.p,
+                                           D.alphas.p);
+      launch_precond(D, D.vr.p, D.vz.p, D.vr.p, D.part_a.p, nullptr);
+      k_beta_update<<<kRed, kRed, 0, st>>>(n, D.pst.p, D.vp.p, D.vz.p, D.part_a.p, D.part_b.p, D.betas.p);
+      count_launch(2);
+      CK(cudaMemcpyAsync(&hs, D.pst.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+  } else {
+    // capture one iteration as a graph (pcg.cpp:49-70)
+    if (!D.gexec) {
+      const long long before = launch_count();
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      const int* done = &D.pst.p->done;
+      launch_schur(D, D.vp.p, D.vq.p, D.vp.p, D.part_a.p, done);
+      k_alpha_axpy<<<kRed, kRed, 0, st>>>(n, D.pst.p, D.vx.p, D.vr.p, D.vp.p, D.vq.p, D.part_a.p, D.part_b.p,
+                                           D.alphas.p);
+      launch_precond(D, D.vr.p, D.vz.p, D.vr.p, D.part_a.p, done);
+      k_beta_update<<<kRed, kRed, 0, st>>>(n, D.pst.p, D.vp.p, D.vz.p, D.part_a.p, D.part_b.p, D.betas.p);
+      CK(cudaStreamEndCapture(st, &D.graph));
+      CK(cudaGraphInstantiate(&D.gexec, D.graph, 0));
+      D.graph_kernels = launch_count() - before + 2;  // + k_alpha_axpy, k_beta_update
+      count_launch(-(launch_count() - before));
+    }
+    const int chunk = 8;
+    while (!hs.done) {
+      for (int c = 0; c < chunk; ++c) CK(cudaGraphLaunch(D.gexec, st));
+      count_launch(chunk * D.graph_kernels);
+      CK(cudaMemcpyAsync(&hs, D.pst.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
   }
   CK(cudaEventRecord(D.e1, st));
   times_.pcg = elapsed(D.e0, D.e1);

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../host/host.hpp"
+#include "comm.hpp"
 #include "dense.cuh"
 
 namespace b200 {
@@ -90,6 +91,12 @@ class Engine {
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
 
+  /// Shard this engine (before any device work): `owner[s]` is the rank that
+  /// owns substructure s; this rank assembles and factors its substructures
+  /// plus the neighbours its face pairs need (ghosts), runs its pairs, and
+  /// exchanges through `comm` (interface sums, root, selected constraints).
+  void set_shard(std::shared_ptr<Comm> comm, const std::vector<int>& owner);
+  bool sharded() const;
   void prepare();              // host staging + device allocation + first upload
   double upload_inputs();      // host->device copies of the inputs; returns bytes
   void analysis();

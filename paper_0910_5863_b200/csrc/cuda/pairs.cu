@@ -398,13 +398,23 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 
 __device__ __forceinline__ size_t pk(int r, int c) { return (size_t)r * (r + 1) / 2 + c; }  // c <= r
 
-__device__ int sturm_count(const double* d, const double* e, int n, double x, double pivmin) {
+// 1/q: hardware approximation refined by two Newton steps (full double
+// precision; only the sign of the Sturm recurrence matters downstream).
+__device__ __forceinline__ double fast_rcp(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  r = fma(r, fma(-q, r, 1.0), r);
+  return fma(r, fma(-q, r, 1.0), r);
+}
+
+// Sturm count with the squared off-diagonal precomputed (e2[j] = e[j]^2)
+__device__ int sturm_count_sq(const double* d, const double* e2, int n, double x, double pivmin) {
   int cnt = 0;
   double q = d[0] - x;
   if (q < 0) ++cnt;
   for (int j = 1; j < n; ++j) {
     if (fabs(q) < pivmin) q = -pivmin;
-    q = d[j] - x - e[j - 1] * e[j - 1] / q;
+    q = (d[j] - x) - e2[j - 1] * fast_rcp(q);
     if (q < 0) ++cnt;
   }
   return cnt;
@@ -555,6 +565,9 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
     if (i + 1 < n) emax2 = fmax(emax2, eg[i] * eg[i]);
   }
   const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax2);
+  double* e2g = v;  // the reflector scratch is free after the tridiagonalization
+  for (int i = tid; i + 1 < n; i += blockDim.x) e2g[i] = eg[i] * eg[i];
+  __syncthreads();
   glo -= 2.2e-16 * tnorm + 2 * pivmin;
   ghi += 2.2e-16 * tnorm + 2 * pivmin;
   const int G = 16;
@@ -565,7 +578,7 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
     double lo = glo, hi = ghi;
     for (int it = 0; it < 30; ++it) {
       const double x = lo + (hi - lo) * (j + 1) / (G + 1);
-      const int ok = active ? (sturm_count(dg, eg, n, x, pivmin) <= target) : 1;
+      const int ok = active ? (sturm_count_sq(dg, e2g, n, x, pivmin) <= target) : 1;
       // lo = largest x with count <= target; hi = smallest x with count > target
       const unsigned mask = __ballot_sync(0xffffffffu, ok);
       const unsigned sub = (mask >> ((lane / G) * G)) & 0xffffu;
@@ -622,6 +635,7 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
       }
     }
     xd[n - 1] = cd == 0.0 ? tiny : cd;
+    for (int i = 0; i < n; ++i) xd[i] = 1.0 / xd[i];  // reciprocals: the solves below multiply
     unsigned long long seed = 0x9E3779B97F4A7C15ULL * (m + 1);
     for (int i = 0; i < n; ++i) {
       seed ^= seed << 13; seed ^= seed >> 7; seed ^= seed << 17;
@@ -641,12 +655,12 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
         }
       }
       b[n - 1] = cb;
-      double x1 = b[n - 1] / xd[n - 1], x2 = 0.0;
+      double x1 = b[n - 1] * xd[n - 1], x2 = 0.0;
       b[n - 1] = x1;
       double nn = x1 * x1;
 #pragma unroll 4
       for (int i = n - 2; i >= 0; --i) {
-        const double xi = (b[i] - xu[i] * x1 - xu2[i] * x2) / xd[i];
+        const double xi = (b[i] - xu[i] * x1 - xu2[i] * x2) * xd[i];
         b[i] = xi;
         nn += xi * xi;
         x2 = x1;
@@ -737,6 +751,11 @@ __global__ void k_functional(const PairDev* pd) {
 
 }  // namespace
 
+void PairEngine::set_shard(std::shared_ptr<Comm> comm, const std::vector<int>& owner) {
+  comm_ = std::move(comm);
+  owner_ = owner;
+}
+
 void PairEngine::attach(const Model& m, const double* S, const std::vector<long long>& s_off,
                         const std::vector<int>& PB, const std::vector<int>& nB, cudaStream_t st) {
   m_ = &m;
@@ -780,7 +799,8 @@ using detail::Dims;
 // factorization is on the device.
 struct PairPrep {
   ConstraintSet base;
-  std::vector<std::pair<int, int>> pairs;
+  std::vector<std::pair<int, int>> pairs;  // this rank's face pairs
+  std::vector<int> gidx;                    // their positions in face_pairs(m)
   std::vector<HostPair> hp;
   std::vector<ChunkHost> chunks;
   int request = 0;
@@ -788,6 +808,44 @@ struct PairPrep {
 };
 
 namespace {
+// flat byte records for the constraint exchange of the sharded engine
+struct ByteWriter {
+  std::vector<char> buf;
+  template <class T>
+  void put(const T& x) {
+    const char* p = reinterpret_cast<const char*>(&x);
+    buf.insert(buf.end(), p, p + sizeof(T));
+  }
+  void i(int x) { put(x); }
+  void d(double x) { put(x); }
+  void v(const std::vector<double>& x) {
+    i(static_cast<int>(x.size()));
+    const char* p = reinterpret_cast<const char*>(x.data());
+    buf.insert(buf.end(), p, p + x.size() * sizeof(double));
+  }
+};
+struct ByteReader {
+  const std::vector<char>& buf;
+  std::size_t at = 0;
+  explicit ByteReader(const std::vector<char>& b) : buf(b) {}
+  template <class T>
+  T get() {
+    T x;
+    std::memcpy(&x, buf.data() + at, sizeof(T));
+    at += sizeof(T);
+    return x;
+  }
+  int i() { return get<int>(); }
+  double d() { return get<double>(); }
+  std::vector<double> v() {
+    const int n = i();
+    std::vector<double> x(n);
+    std::memcpy(x.data(), buf.data() + at, n * sizeof(double));
+    at += n * sizeof(double);
+    return x;
+  }
+};
+
 int count_above(const std::vector<double>& v, double tau) {
   int k = 0;
   while (k < static_cast<int>(v.size()) && v[k] > tau) ++k;
@@ -906,7 +964,15 @@ std::shared_ptr<PairPrep> PairEngine::prepare(const ConstraintSet& cs, const Enr
   const ConstraintSet& base = prep->base;
   const auto bg = base.by_glob(m.globs.size());
   prep->request = o.indicator_only ? 1 : (o.fixed_count >= 0 ? o.fixed_count : o.max_vectors) + 1;
-  prep->pairs = face_pairs(m);
+  {
+    // a face pair belongs to the owner of its lower substructure (shard.py)
+    const auto all = face_pairs(m);
+    for (std::size_t g = 0; g < all.size(); ++g)
+      if (!comm_ || owner_[std::min(all[g].first, all[g].second)] == comm_->rank()) {
+        prep->pairs.push_back(all[g]);
+        prep->gidx.push_back(static_cast<int>(g));
+      }
+  }
   const auto& pairs = prep->pairs;
   const int np = static_cast<int>(pairs.size());
   prep->hp.resize(np);
@@ -1247,6 +1313,55 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       rep.omega_next = L > 0 ? lam[0] : 0.0;
     }
   }
+  if (comm_) {
+    // every rank's reports and candidates, in the global pair order, so that all
+    // ranks apply the same rank filter and end with the same constraint set
+    ByteWriter w;
+    w.i(static_cast<int>(reps.size()));
+    for (int p = 0; p < static_cast<int>(reps.size()); ++p) {
+      const PairReport& r = reps[p];
+      w.i(prep->gidx[p]); w.i(r.si); w.i(r.sj); w.i(r.enforced); w.i(r.saturated ? 1 : 0);
+      w.d(r.omega_next);
+      w.v(r.eigenvalues);
+    }
+    w.i(static_cast<int>(cands.size()));
+    for (const Cand& c : cands) {
+      w.i(prep->gidx[c.p]); w.i(c.glob);
+      w.v(c.w);
+    }
+    const auto all = comm_->allgather(w.buf);
+    std::vector<std::pair<int, PairReport>> greps;
+    std::vector<Cand> gc;
+    for (const auto& blob : all) {
+      ByteReader rd(blob);
+      const int nr = rd.i();
+      for (int t = 0; t < nr; ++t) {
+        PairReport r;
+        const int g = rd.i();
+        r.si = rd.i(); r.sj = rd.i(); r.enforced = rd.i(); r.saturated = rd.i() != 0;
+        r.omega_next = rd.d();
+        r.eigenvalues = rd.v();
+        greps.emplace_back(g, std::move(r));
+      }
+      const int nc = rd.i();
+      for (int t = 0; t < nc; ++t) {
+        Cand c;
+        c.p = rd.i(); c.glob = rd.i(); c.w = rd.v(); c.ok = 0;
+        gc.push_back(std::move(c));
+      }
+    }
+    std::stable_sort(greps.begin(), greps.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::stable_sort(gc.begin(), gc.end(), [](const Cand& a, const Cand& b) { return a.p < b.p; });
+    // reports indexed by global pair, candidates pointing at them
+    reps.clear();
+    std::vector<int> where(greps.empty() ? 0 : greps.back().first + 1, -1);
+    for (auto& gr : greps) {
+      where[gr.first] = static_cast<int>(reps.size());
+      reps.push_back(std::move(gr.second));
+    }
+    for (Cand& c : gc) c.p = where[c.p];
+    cands = std::move(gc);
+  }
   {
     std::vector<std::vector<int>> by_g(m.globs.size());
     for (std::size_t c = 0; c < cands.size(); ++c) by_g[cands[c].glob].push_back(static_cast<int>(c));
@@ -1277,7 +1392,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       ++reps[c.p].dropped;
     }
   }
-  for (int p = 0; p < np; ++p) {
+  for (int p = 0; p < static_cast<int>(reps.size()); ++p) {
     out.omega_tilde = std::max(out.omega_tilde, reps[p].omega_next);
     out.kept += reps[p].kept;
     out.dropped += reps[p].dropped;

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../host/host.hpp"
+#include "comm.hpp"
 
 namespace b200 {
 
@@ -20,6 +21,9 @@ class PairEngine {
  public:
   PairEngine();
   ~PairEngine();
+  /// Pairs are owned by the rank of their lower substructure; the selected
+  /// constraints are exchanged so that every rank ends with the same set.
+  void set_shard(std::shared_ptr<Comm> comm, const std::vector<int>& owner);
   void attach(const Model& m, const double* S, const std::vector<long long>& s_off,
               const std::vector<int>& PB, const std::vector<int>& nB, cudaStream_t st);
   /// Host-side preparation (pair index spaces, kernel bases, rigid modes); no
@@ -34,6 +38,8 @@ class PairEngine {
   std::vector<int> PB_, nB_;
   cudaStream_t st_ = nullptr;
   std::unique_ptr<PairBuffers> bufs_;
+  std::shared_ptr<Comm> comm_;
+  std::vector<int> owner_;
 };
 
 }  // namespace b200

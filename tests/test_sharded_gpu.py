@@ -1,0 +1,127 @@
+"""Sharded engine on one GPU: R ranks as host threads of this
+process, exchanging through the loopback backend (each rank synchronizes its
+own stream before a host-side exchange, so no kernel waits on another rank).
+The sharded results must equal the single-engine results: operators to
+roundoff, identical constraint selection and pair reports, PCG iterations
+within +-1, kappa to the KAPPA_RTOL of test_gpu_parity, the solution to 1e-8
+in the energy norm, and every rank must hold the same complete result.
+"""
+import itertools
+import threading
+
+import numpy as np
+import pytest
+
+import paper_0910_5863_b200 as pb
+from paper_0910_5863_b200 import shard
+
+pytestmark = pytest.mark.gpu
+
+_group = itertools.count(100)
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def run_ranks(make, world, fn, owner=None, timeout=600):
+    group = next(_group)
+    handles = [make() for _ in range(world)]
+    for r, b in enumerate(handles):
+        b.shard(r, world, owner=owner, backend="loopback", group=group)
+    out, errors = [None] * world, []
+
+    def work(r):
+        try:
+            out[r] = fn(handles[r])
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append("rank %d: %r" % (r, e))
+
+    threads = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout)
+    assert not errors, errors
+    assert all(not t.is_alive() for t in threads), "a rank did not finish"
+    return out
+
+
+def pipeline(mode, tau, maxv, base_faces=False, seed=3):
+    def fn(b):
+        b.analysis()
+        if mode == "adaptive":
+            b.arithmetic_constraints(True, base_faces)
+            b.enrich(tau, maxv)
+        else:
+            b.arithmetic_constraints(mode != "c", mode == "c+e+f")
+        b.setup_preconditioner()
+        n = b.structure()["interface_dofs"]
+        x = np.random.default_rng(seed).standard_normal(n)
+        g = b.pcg()
+        return {"rows": b.constraint_rows(), "reports": b.pair_reports() if mode == "adaptive" else [],
+                "schur": b.schur_apply(x), "prec": b.precond_apply(x), "rhs": b.rhs(), "pcg": g,
+                "u": b.recover(g["x"])}
+    return fn
+
+
+def energy(b, e):
+    import scipy.sparse as sp
+    st = b.structure()
+    rows, cols, vals = [], [], []
+    for s in range(st["subdomains"]):
+        a, _ = b.subdomain_matrix(s)
+        g = b.global_dof(s)
+        c = a.tocoo()
+        rows.append(g[c.row]); cols.append(g[c.col]); vals.append(c.data)
+    A = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=(st["free_dofs"], st["free_dofs"]))
+    return float(e @ (A @ e))
+
+
+CASES = [
+    ("el222h4 adaptive w2", lambda: pb.BDDC(pb.Problem.cube((2, 2, 2), 4, "elasticity")), 2, ("adaptive", 10.0, 15)),
+    ("cfg2 w3", lambda: pb.BDDC(config=2), 3, ("adaptive", 10.0, 10)),
+    ("cfg4 3x3x3 H/h=4 w2", lambda: pb.BDDC(config=4, subdomains=(3, 3, 3), elements_per_edge=4), 2,
+     ("adaptive", 10.0, 15)),
+    ("sc221h8 c+e+f w2", lambda: pb.BDDC(pb.Problem.cube((2, 2, 1), 8, "scalar")), 2, ("c+e+f", 0.0, 0)),
+]
+
+
+@pytest.mark.parametrize("name,make,world,mode", CASES, ids=[c[0] for c in CASES])
+def test_sharded_equals_single(name, make, world, mode):
+    fn = pipeline(*mode)
+    ref_b = make()
+    ref = fn(ref_b)
+    got = run_ranks(make, world, fn)
+    for r in range(world):
+        g = got[r]
+        # every rank holds the same complete result
+        for key in ("schur", "prec", "rhs", "u"):
+            assert np.array_equal(g[key], got[0][key]), (r, key)
+        assert g["rows"] == ref["rows"]
+        assert len(g["reports"]) == len(ref["reports"])
+        for a, o in zip(g["reports"], ref["reports"]):
+            assert (a["si"], a["sj"], a["enforced"], a["saturated"]) == (o["si"], o["sj"], o["enforced"], o["saturated"])
+            assert np.allclose(a["eigenvalues"], o["eigenvalues"], rtol=1e-9, atol=0)
+            assert abs(a["omega_next"] - o["omega_next"]) <= 1e-9 * max(o["omega_next"], 1e-12)
+        assert rel(g["schur"], ref["schur"]) <= 1e-11
+        assert rel(g["rhs"], ref["rhs"]) <= 1e-11
+        # the root is summed per rank and then across ranks: a different rounding
+        # of R, amplified by the root inverse (cfg2: 1e6 coefficient contrast)
+        assert rel(g["prec"], ref["prec"]) <= 1e-8
+        assert abs(g["pcg"]["iterations"] - ref["pcg"]["iterations"]) <= 1
+        n = min(len(g["pcg"]["alphas"]), len(ref["pcg"]["alphas"]))
+        kg = pb.lanczos_condition_estimate(g["pcg"]["alphas"][:n], g["pcg"]["betas"][:n])
+        ko = pb.lanczos_condition_estimate(ref["pcg"]["alphas"][:n], ref["pcg"]["betas"][:n])
+        assert abs(kg - ko) <= 1e-3 * ko
+    e = got[0]["u"] - ref["u"]
+    assert energy(ref_b, e) <= 1e-16 * energy(ref_b, ref["u"])
+
+
+def test_sharded_partition_covers_every_pair_once():
+    """The ghost layer: every face pair is solved by exactly one rank, on a rank
+    that holds both of its substructures (owned or ghost)."""
+    b = pb.BDDC(config=2)
+    owner = shard.partition(b.lattice(), 3)
+    assert sorted(np.bincount(owner)) == [9, 9, 9]
