@@ -14,8 +14,13 @@ inputs and the device->host copy of the solution inside the timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
 
-N > 1 (torchrun, one process per GPU) runs N independent replicas ("weak"
-scaling); the sharded multi-GPU path is future work.
+N > 1 (torchrun, one process per GPU) runs the sharded engine: one problem
+whose substructure lattice grows with N along x (the config's lattice per GPU,
+same per-element coefficient rule), substructures and face pairs partitioned
+over the ranks (paper_0910_5863_b200/shard.py), NCCL for the interface
+exchange, the dot products (complete vectors on every rank) and the root
+("weak" scaling: per-GPU work fixed).  `--replicas` runs N independent copies
+of the N=1 workload instead.
 `--impl reference` times the CPU oracle (oracle/, the reference restated; the
 C++ reference itself needs Eigen and cannot be built here) on the same config.
 """
@@ -193,8 +198,9 @@ def reference_arm(args):
         "config": {"workload": CONFIG_NAMES[cfg_id], "config": cfg_id, "seed": args.seed,
                    "l2": "n/a (CPU)"},
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
-                         "sample": "full %s setup+solve per step (numpy/scipy oracle, LAPACK on %d threads)"
-                                   % ("cfg%d" % cfg_id, cores)},
+                         "sample": ("full %s setup+solve per step (numpy/scipy oracle, LAPACK on %d threads)"
+                                    % ("cfg%d" % cfg_id, cores)) + (
+                             "; one GPU's share of the %d-GPU weak-scaled job" % world if world > 1 else "")},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "iterations": row.iterations, "kappa": row.kappa, "constraint_rows": row.constraint_rows,
         "omega_tilde": None if math.isnan(row.omega_tilde) else row.omega_tilde,
@@ -212,6 +218,7 @@ def main():
     ap.add_argument("--seed", type=int, default=20091030)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent copies instead of sharding")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -225,8 +232,18 @@ def main():
     import torch
     torch.cuda.set_device(local)
     mode, tau, maxv, base_faces = CONFIG_MODES[args.config]
+    sharded = world > 1 and not args.replicas
     t_in = time.perf_counter()
-    b = pb.BDDC(config=args.config, seed=args.seed)
+    if sharded:
+        base = pb.BDDC(config=args.config, seed=args.seed).lattice()
+        lattice = (base[0] * world, base[1], base[2])
+        b = pb.BDDC(config=args.config, seed=args.seed, subdomains=lattice)
+        nid = [pb.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        b.shard(rank, world, backend="nccl", nccl_id=nid[0])
+    else:
+        b = pb.BDDC(config=args.config, seed=args.seed)
+        lattice = b.lattice()
     input_seconds = time.perf_counter() - t_in
     st = b.structure()
     free = st["free_dofs"]
@@ -255,7 +272,8 @@ def main():
     dev_seconds = sum(s["seconds"] for s in steps)
     dev_seconds = max_over_ranks(dist, dev_seconds, "cuda")
     sec_per_step = dev_seconds / args.steps
-    value = world * free / sec_per_step
+    jobs = 1 if sharded else world  # sharded: one problem over all ranks
+    value = jobs * free / sec_per_step
     # end to end through the C ABI with host buffers
     u = np.empty(free)
     for _ in range(max(1, args.warmup // 2)):
@@ -263,6 +281,7 @@ def main():
     barrier(dist, local)
     e2e_steps = [do_step(True, u) for _ in range(args.steps)]
     e2e_sec = max_over_ranks(dist, sum(s["seconds"] for s in e2e_steps), "cuda") / args.steps
+    launches = max_over_ranks(dist, float(sum(s["launches"] for s in steps)), "cuda")
     clk.__exit__(None, None, None)
     if rank != 0:
         return 0
@@ -287,10 +306,13 @@ def main():
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec_per_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded coefficient field)",
-        "config": {"workload": CONFIG_NAMES[args.config], "config": args.config, "seed": args.seed,
+        "config": {"workload": CONFIG_NAMES[args.config] + (
+                       " per GPU; lattice %dx%dx%d over %d GPUs" % (lattice + (world,)) if sharded else ""),
+                   "config": args.config, "seed": args.seed, "lattice": list(lattice),
                    "free_dofs": free, "subdomains": st["subdomains"], "interface_dofs": st["interface_dofs"],
                    "l2": "flushed (256 MiB write) before every step",
-                   "parallelism": "replicas%d" % world if world > 1 else "single GPU"},
+                   "parallelism": ("sharded%d (NCCL: interface exchange, dot products, root)" % world if sharded
+                                   else "replicas%d" % world if world > 1 else "single GPU")},
         "setup_s": statistics.median(s["setup_seconds"] for s in steps),
         "solve_s": statistics.median(s["solve_seconds"] for s in steps),
         "iterations": last["iterations"], "kappa": last["kappa"], "constraint_rows": last["constraint_rows"],
@@ -299,13 +321,13 @@ def main():
                                                                    "leaf_factor")},
         "roofline": roof,
         "cpu_baseline": cpu,
-        "e2e": {"value": world * free / e2e_sec, "unit": "DOF/s",
+        "e2e": {"value": jobs * free / e2e_sec, "unit": "DOF/s",
                 "h2d_bytes_per_step": int(e2e_steps[-1]["h2d_bytes"]),
                 "d2h_bytes_per_step": int(e2e_steps[-1]["d2h_bytes"]), "ms_per_step": e2e_sec * 1e3},
         "clocks": clk.summary(t_timed0, t_timed1),
         "step_ms": [round(s["seconds"] * 1e3, 3) for s in steps],
         "e2e_step_ms": [round(s["seconds"] * 1e3, 3) for s in e2e_steps],
-        "gpu_launches": int(sum(s["launches"] for s in steps)),
+        "gpu_launches": int(launches),  # max over ranks
     }
     print(json.dumps(line), flush=True)
     if dist is not None:

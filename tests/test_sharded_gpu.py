@@ -125,3 +125,20 @@ def test_sharded_partition_covers_every_pair_once():
     b = pb.BDDC(config=2)
     owner = shard.partition(b.lattice(), 3)
     assert sorted(np.bincount(owner)) == [9, 9, 9]
+
+
+def test_nccl_backend_world1():
+    """The NCCL backend on one GPU (world 1): communicator set-up, the host
+    allgather of the selected constraints and the sharded code paths (eager
+    PCG, exchange points) give the single-engine results bit for bit."""
+    make = lambda: pb.BDDC(config=2)
+    fn = pipeline("adaptive", 10.0, 10)
+    ref = fn(make())
+    b = make()
+    b.shard(0, 1, backend="nccl", nccl_id=pb.nccl_unique_id())
+    got = fn(b)
+    assert got["rows"] == ref["rows"]
+    for key in ("schur", "prec", "rhs"):
+        assert np.array_equal(got[key], ref[key]), key
+    assert got["pcg"]["iterations"] == ref["pcg"]["iterations"]
+    assert np.array_equal(got["u"], ref["u"])
