@@ -10,6 +10,8 @@
 // loads) and issue mma.sync.aligned.m16n8k16.f64 (FP64 tensor cores).
 #include "dense.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
@@ -506,6 +508,158 @@ __global__ void __launch_bounds__(THREADS) k_front_backward(const SolveDesc* ds,
   for (int r = tid; r < d.n; r += THREADS) d.x[r] = xs[r];
 }
 
+// ---------------------------------------------------------------------------
+// Front solves over a thread-block cluster of CL CTAs per front (few fronts:
+// more SMs and more loads in flight per front).  Row tile t (64 rows) belongs
+// to CTA t % CL.  Forward: the owner of block kb forms z = Dinv_kb x_kb and
+// the others read it through distributed shared memory; every CTA updates its
+// own rows.  Backward: every CTA forms the partial sums of its rows; the owner
+// adds them in rank order and solves the block.  One cluster barrier per block.
+// ---------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+
+template <int CL>
+__global__ void __launch_bounds__(256) k_front_forward_cl(const SolveDesc* ds, const int* done) {
+  if (done && *done) return;
+  cg::cluster_group cl = cg::this_cluster();
+  const int me = static_cast<int>(cl.block_rank());
+  const SolveDesc d = ds[blockIdx.x / CL];
+  extern __shared__ double xs[];
+  double* zb = xs + d.n;      // [2][64] double-buffered block solution (read remotely)
+  double* zl = zb + 128;      // local copy of a remote z
+  const int tid = threadIdx.x;
+  const int nt = d.n / kTile;
+  for (int r = tid; r < d.n; r += 256)
+    if ((r >> 6) % CL == me) xs[r] = d.x[r];
+  __syncthreads();
+  const size_t ld = d.n;
+  for (int kb = 0; kb < d.p / kTile; ++kb) {
+    const int k0 = kb * kTile, owner = kb % CL;
+    double* zc = zb + (kb & 1) * 64;
+    if (me == owner) {
+      const int row = tid >> 2, part = tid & 3;
+      const double* dv = d.dinv + (size_t)kb * 64 * 64;
+      double sum = 0.0;
+      for (int c = part; c < 64; c += 4) sum += dv[(size_t)c * 64 + row] * xs[k0 + c];
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      if (part == 0) zc[row] = sum;
+      __syncthreads();
+      if (tid < 64) xs[k0 + tid] = zc[tid];
+    }
+    cl.sync();
+    const double* z = zc;
+    if (me != owner) {
+      const double* rz = cl.map_shared_rank(zc, owner);
+      if (tid < 64) zl[tid] = rz[tid];
+      __syncthreads();
+      z = zl;
+    }
+    // own row tiles below the block: t = first, first + CL, ...
+    int first = kb + 1 + ((me - (kb + 1) % CL) + CL) % CL;
+    const int ntiles = first < nt ? (nt - 1 - first) / CL + 1 : 0;
+    for (int i = tid; i < 64 * ntiles; i += 256) {
+      const int r = (first + (i >> 6) * CL) * 64 + (i & 63);
+      const double* col = d.a + (size_t)k0 * ld + r;
+      double sq[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sq[q] = 0.0;
+#pragma unroll 2
+      for (int c = 0; c < 64; c += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sq[q] += col[(size_t)(c + q) * ld] * z[c + q];
+      }
+      xs[r] -= ((sq[0] + sq[1]) + (sq[2] + sq[3])) + ((sq[4] + sq[5]) + (sq[6] + sq[7]));
+    }
+    __syncthreads();
+  }
+  for (int r = tid; r < d.n; r += 256)
+    if ((r >> 6) % CL == me) d.x[r] = xs[r];
+  cl.sync();  // no CTA leaves while its shared memory may still be read
+}
+
+template <int CL>
+__global__ void __launch_bounds__(256) k_front_backward_cl(const SolveDesc* ds, const int* done) {
+  if (done && *done) return;
+  cg::cluster_group cl = cg::this_cluster();
+  const int me = static_cast<int>(cl.block_rank());
+  const SolveDesc d = ds[blockIdx.x / CL];
+  extern __shared__ double xs[];
+  double* pb = xs + d.n;       // [2][CL][64] partial sums, written by every rank into the owner
+  double* t = pb + 2 * CL * 64;  // 64
+  __shared__ double part[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nt = d.n / kTile;
+  for (int r = tid; r < d.n; r += 256) {
+    if ((r >> 6) % CL != me) continue;
+    double v = d.x[r];
+    if (d.cmap && r >= d.p) {
+      const int k = d.cmap[r - d.p];
+      v = k >= 0 ? d.croot[k] : 0.0;
+    }
+    xs[r] = v;
+  }
+  __syncthreads();
+  const size_t ld = d.n;
+  for (int kb = d.p / kTile - 1; kb >= 0; --kb) {
+    const int k0 = kb * kTile, owner = kb % CL;
+    // partial t over this CTA's row tiles below the block: warp w owns columns
+    // w, w+8, ..., w+56; a lane reads a row pair (16-byte loads)
+    {
+      double acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+      const double* base = d.a + (size_t)(k0 + warp) * ld;
+      const int first = kb + 1 + ((me - (kb + 1) % CL) + CL) % CL;
+      for (int tt = first; tt < nt; tt += CL) {
+        const int r = tt * 64 + 2 * lane;
+        const double x0 = xs[r], x1 = xs[r + 1];
+        double2 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = __ldg(reinterpret_cast<const double2*>(base + (size_t)(8 * q) * ld + r));
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += v[q].x * x0 + v[q].y * x1;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double sum = acc[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) part[warp + 8 * q] = sum;
+      }
+    }
+    __syncthreads();
+    double* slot = pb + (kb & 1) * CL * 64 + me * 64;
+    if (tid < 64) {
+      double* dst = me == owner ? slot : cl.map_shared_rank(slot, owner);
+      dst[tid] = part[tid];
+    }
+    cl.sync();
+    if (me == owner) {
+      if (tid < 64) {
+        const double* ps = pb + (kb & 1) * CL * 64;
+        double sum = 0.0;
+#pragma unroll
+        for (int q = 0; q < CL; ++q) sum += ps[q * 64 + tid];
+        t[tid] = xs[k0 + tid] - sum;
+      }
+      __syncthreads();
+      // x[k0:k0+64] = Dinv^T t
+      const int row = tid >> 2, prt = tid & 3;
+      const double* dv = d.dinv + (size_t)kb * 64 * 64 + (size_t)row * 64;
+      double sum = 0.0;
+      for (int c = prt; c < 64; c += 4) sum += dv[c] * t[c];
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      if (prt == 0) xs[k0 + row] = sum;
+    }
+    __syncthreads();
+  }
+  for (int r = tid; r < d.n; r += 256)
+    if ((r >> 6) % CL == me) d.x[r] = xs[r];
+  cl.sync();
+}
+
 __global__ void k_copy_trailing(const TrailDesc* ds) {
   const TrailDesc d = ds[blockIdx.y];
   const int m = d.n - d.p;
@@ -528,6 +682,10 @@ void configure() {
   cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
   cudaFuncSetAttribute(k_front_forward<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_backward<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_forward_cl<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_forward_cl<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_backward_cl<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_backward_cl<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_forward<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_backward<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_forward<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -623,32 +781,57 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
 }
 
 namespace {
-// Threads per front.  256: measured faster than 512/1024-thread fronts on
-// configs 3-4 (the per-block barriers dominate once more warps share a front).
-int solve_threads(int) { return 256; }
+// CTAs per front: a cluster of 4 or 2 when the fronts alone cannot fill the
+// GPU (about three CTAs per SM), else one.  BDDC_B200_SWEEP_CL=1|2|4 overrides.
+int sweep_cluster(int batch) {
+  const char* env = std::getenv("BDDC_B200_SWEEP_CL");
+  if (env && *env) {
+    const int c = std::atoi(env);
+    if (c == 1 || c == 2 || c == 4) return c;
+  }
+  const long cap = 3L * sm_count();
+  if ((long)batch * 4 <= cap) return 4;
+  if ((long)batch * 2 <= cap) return 2;
+  return 1;
+}
+
+template <class K>
+void launch_cluster(K kern, int cl, int batch, size_t smem, cudaStream_t stream, const SolveDesc* d, const int* done) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(batch * cl);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, d, done);
+}
 }  // namespace
 
 void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
   if (batch == 0) return;
   configure();
-  const size_t smem = (max_n + 64) * sizeof(double);
-  switch (solve_threads(batch)) {
-    case 1024: k_front_forward<1024><<<batch, 1024, smem, stream>>>(d_descs, done); break;
-    case 512: k_front_forward<512><<<batch, 512, smem, stream>>>(d_descs, done); break;
-    default: k_front_forward<256><<<batch, 256, smem, stream>>>(d_descs, done); break;
-  }
+  const int cl = sweep_cluster(batch);
+  const size_t smem = (max_n + 64 * 3) * sizeof(double);
+  if (cl == 4) launch_cluster(k_front_forward_cl<4>, 4, batch, smem, stream, d_descs, done);
+  else if (cl == 2) launch_cluster(k_front_forward_cl<2>, 2, batch, smem, stream, d_descs, done);
+  else k_front_forward<256><<<batch, 256, (max_n + 64) * sizeof(double), stream>>>(d_descs, done);
   count_launch(1);
 }
 
 void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
   if (batch == 0) return;
   configure();
-  const size_t smem = (max_n + 64) * sizeof(double);
-  switch (solve_threads(batch)) {
-    case 1024: k_front_backward<1024><<<batch, 1024, smem, stream>>>(d_descs, done); break;
-    case 512: k_front_backward<512><<<batch, 512, smem, stream>>>(d_descs, done); break;
-    default: k_front_backward<256><<<batch, 256, smem, stream>>>(d_descs, done); break;
-  }
+  const int cl = sweep_cluster(batch);
+  const size_t smem = (max_n + 64 + 2 * 4 * 64) * sizeof(double);
+  if (cl == 4) launch_cluster(k_front_backward_cl<4>, 4, batch, smem, stream, d_descs, done);
+  else if (cl == 2) launch_cluster(k_front_backward_cl<2>, 2, batch, smem, stream, d_descs, done);
+  else k_front_backward<256><<<batch, 256, (max_n + 64) * sizeof(double), stream>>>(d_descs, done);
   count_launch(1);
 }
 
