@@ -391,11 +391,8 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_trsm(const FrontDesc* ds, int 
   for_acc(acc, [&](int m, int n, double v) { out[(size_t)n * ld + m] = v; });
 }
 
-// ---------------------------------------------------------------------------
-// Front solves: one CTA per front, vector staged in shared memory.
-// ---------------------------------------------------------------------------
-// THREADS = 256, or 1024 when the fronts are too few to fill the GPU (more
-// rows, hence more loads, in flight per front).
+// Forward sweep, one CTA per front (fronts that fill the GPU on their own):
+// measured faster than the cluster kernel with CL = 1.
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_front_forward(const SolveDesc* ds, const int* done) {
   if (done && *done) return;
@@ -438,78 +435,8 @@ __global__ void __launch_bounds__(THREADS) k_front_forward(const SolveDesc* ds, 
   for (int r = tid; r < d.n; r += THREADS) d.x[r] = xs[r];
 }
 
-template <int THREADS>
-__global__ void __launch_bounds__(THREADS) k_front_backward(const SolveDesc* ds, const int* done) {
-  constexpr int G = THREADS / 256;  // row groups per column set
-  if (done && *done) return;
-  const SolveDesc d = ds[blockIdx.x];
-  extern __shared__ double xs[];
-  double* t = xs + d.n;  // 64 scratch
-  __shared__ double part[G][64];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int r = tid; r < d.n; r += THREADS) {
-    double v = d.x[r];
-    if (d.cmap && r >= d.p) {
-      const int k = d.cmap[r - d.p];
-      v = k >= 0 ? d.croot[k] : 0.0;
-    }
-    xs[r] = v;
-  }
-  __syncthreads();
-  const size_t ld = d.n;
-  const int cw = warp & 7, rg = warp >> 3;  // column set, row group
-  for (int kb = d.p / kTile - 1; kb >= 0; --kb) {
-    const int k0 = kb * kTile;
-    // t[c] = x[k0+c] - sum_{r >= k0+64} L[r, k0+c] x[r]: warp (cw, rg) owns
-    // columns cw, cw+8, ..., cw+56 and row pairs rg, rg+G, ... (16-byte loads,
-    // eight columns in flight), reduced across lanes, then over the G row
-    // groups in a fixed order
-    {
-      double acc[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-      const double* base = d.a + (size_t)(k0 + cw) * ld;
-      for (int r = k0 + kTile + 64 * rg + 2 * lane; r < d.n; r += 64 * G) {
-        const double x0 = xs[r], x1 = xs[r + 1];
-        double2 v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = __ldg(reinterpret_cast<const double2*>(base + (size_t)(8 * q) * ld + r));
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] += v[q].x * x0 + v[q].y * x1;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        double s = acc[q];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) part[rg][cw + 8 * q] = s;
-      }
-    }
-    __syncthreads();
-    if (tid < 64) {
-      double s = 0.0;
-#pragma unroll
-      for (int g = 0; g < G; ++g) s += part[g][tid];
-      t[tid] = xs[k0 + tid] - s;
-    }
-    __syncthreads();
-    // x[k0:k0+64] = Dinv^T t
-    if (tid < 256) {
-      const int row = tid >> 2, prt = tid & 3;
-      const double* dv = d.dinv + (size_t)kb * 64 * 64 + (size_t)row * 64;  // column `row` of Dinv
-      double s = 0.0;
-      for (int c = prt; c < 64; c += 4) s += dv[c] * t[c];
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      if (prt == 0) xs[k0 + row] = s;
-    }
-    __syncthreads();
-  }
-  for (int r = tid; r < d.n; r += THREADS) d.x[r] = xs[r];
-}
-
 // ---------------------------------------------------------------------------
-// Front solves over a thread-block cluster of CL CTAs per front (few fronts:
+// Front solves: one CTA, or a thread-block cluster of CL CTAs, per front (few fronts:
 // more SMs and more loads in flight per front).  Row tile t (64 rows) belongs
 // to CTA t % CL.  Forward: the owner of block kb forms z = Dinv_kb x_kb and
 // the others read it through distributed shared memory; every CTA updates its
@@ -584,12 +511,24 @@ __global__ void __launch_bounds__(256) k_front_backward_cl(const SolveDesc* ds, 
   cg::cluster_group cl = cg::this_cluster();
   const int me = static_cast<int>(cl.block_rank());
   const SolveDesc d = ds[blockIdx.x / CL];
-  extern __shared__ double xs[];
-  double* pb = xs + d.n;       // [2][CL][64] partial sums, written by every rank into the owner
-  double* t = pb + 2 * CL * 64;  // 64
+  extern __shared__ __align__(16) double xs_[];
+  double* dvs = xs_;                 // 64 x LDS: Dinv of this CTA's next block (cp.async prefetch)
+  double* pb = xs_ + 64 * LDS;       // [2][CL][64] partial sums, written by every rank into the owner
+  double* t = pb + 2 * CL * 64;      // 64
+  double* xs = t + 64;               // the vector (own row tiles)
   __shared__ double part[64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nt = d.n / kTile;
+  const int nt = d.n / kTile, nb = d.p / kTile;
+  auto prefetch = [&](int kb) {
+    const double* dv = d.dinv + (size_t)kb * 64 * 64;
+    for (int q = tid; q < 64 * 32; q += 256) cp_async16(dvs + (q >> 5) * LDS + (q & 31) * 2, dv + (q >> 5) * 64 + (q & 31) * 2);
+    cp_async_commit();
+  };
+  {
+    // the last block this CTA owns comes first in the backward order
+    int kl = nb - 1 - ((nb - 1 - me) % CL + CL) % CL;
+    if (kl >= 0 && kl % CL == me) prefetch(kl);
+  }
   for (int r = tid; r < d.n; r += 256) {
     if ((r >> 6) % CL != me) continue;
     double v = d.x[r];
@@ -636,6 +575,7 @@ __global__ void __launch_bounds__(256) k_front_backward_cl(const SolveDesc* ds, 
     }
     cl.sync();
     if (me == owner) {
+      cp_async_wait<0>();
       if (tid < 64) {
         const double* ps = pb + (kb & 1) * CL * 64;
         double sum = 0.0;
@@ -644,14 +584,15 @@ __global__ void __launch_bounds__(256) k_front_backward_cl(const SolveDesc* ds, 
         t[tid] = xs[k0 + tid] - sum;
       }
       __syncthreads();
-      // x[k0:k0+64] = Dinv^T t
+      // x[k0:k0+64] = Dinv^T t  (column `row` of Dinv)
       const int row = tid >> 2, prt = tid & 3;
-      const double* dv = d.dinv + (size_t)kb * 64 * 64 + (size_t)row * 64;
       double sum = 0.0;
-      for (int c = prt; c < 64; c += 4) sum += dv[c] * t[c];
+      for (int c = prt; c < 64; c += 4) sum += dvs[row * LDS + c] * t[c];
       sum += __shfl_xor_sync(0xffffffffu, sum, 1);
       sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      __syncthreads();
       if (prt == 0) xs[k0 + row] = sum;
+      if (kb - CL >= 0) prefetch(kb - CL);  // overlaps the partial sums of the next CL blocks
     }
     __syncthreads();
   }
@@ -681,15 +622,11 @@ void configure() {
   cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
   cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
   cudaFuncSetAttribute(k_front_forward<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_front_backward<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_backward_cl<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_forward_cl<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_forward_cl<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_backward_cl<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_backward_cl<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_front_forward<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_front_backward<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_front_forward<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_front_backward<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   g_smem_configured = 1;
 }
 
@@ -828,10 +765,10 @@ void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t
   if (batch == 0) return;
   configure();
   const int cl = sweep_cluster(batch);
-  const size_t smem = (max_n + 64 + 2 * 4 * 64) * sizeof(double);
+  const size_t smem = (64 * LDS + max_n + 64 + 2 * 4 * 64) * sizeof(double);
   if (cl == 4) launch_cluster(k_front_backward_cl<4>, 4, batch, smem, stream, d_descs, done);
   else if (cl == 2) launch_cluster(k_front_backward_cl<2>, 2, batch, smem, stream, d_descs, done);
-  else k_front_backward<256><<<batch, 256, (max_n + 64) * sizeof(double), stream>>>(d_descs, done);
+  else k_front_backward_cl<1><<<batch, 256, smem, stream>>>(d_descs, done);
   count_launch(1);
 }
 
