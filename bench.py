@@ -297,6 +297,16 @@ def main():
             "peak_source": "measured cuBLAS DGEMM (MEASURED_PEAKS.json has bf16 only)",
             "flops_per_launch": lf_flops, "seconds_per_launch": lf_t,
             "share_of_step": lf_t / sec_per_step}
+    # second roofline: the HBM-bound PCG iteration (Schur apply + both leaf
+    # sweeps + root apply), algorithmic bytes over the device-timed PCG phase
+    tm = b.times()
+    pcg_it = max(int(tm["pcg_iterations"]), 1)
+    pcg_achieved = tm["pcg_bytes_per_iteration"] * pcg_it / max(tm["pcg"], 1e-12) / 1e9
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    roof_pcg = {"kernel": "PCG iteration (S_s GEMV + leaf sweeps + root apply)", "bound": "hbm",
+                "achieved": pcg_achieved, "peak": hbm_peak, "unit": "GB/s", "frac": pcg_achieved / hbm_peak,
+                "traffic": None, "bytes_per_iteration": tm["pcg_bytes_per_iteration"], "iterations": pcg_it,
+                "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind}
     cpu = None
     if not args.no_cpu_baseline and world == 1 and args.config <= 2:
         dt, _, _ = run_oracle_step(args.config, args.seed)
@@ -320,6 +330,7 @@ def main():
         "phases_s": {k: v for k, v in b.times().items() if k in ("analysis", "eigen", "preconditioner", "pcg",
                                                                    "leaf_factor")},
         "roofline": roof,
+        "roofline_pcg": roof_pcg,
         "cpu_baseline": cpu,
         "e2e": {"value": jobs * free / e2e_sec, "unit": "DOF/s",
                 "h2d_bytes_per_step": int(e2e_steps[-1]["h2d_bytes"]),

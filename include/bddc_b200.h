@@ -211,8 +211,8 @@ int bddc_b200_lanczos(const double* alphas, const double* betas, int64_t n, doub
 
 /* Device-timed phase seconds and work of the last calls:
  * [analysis, eigen, preconditioner, pcg, leaf_flops, leaf_front_bytes, schur_bytes, root_size,
- *  leaf_factor] */
-int bddc_b200_times(const bddc_b200_t* h, double out[9]);
+ *  leaf_factor, pcg_iterations, pcg_bytes_per_iteration] */
+int bddc_b200_times(const bddc_b200_t* h, double out[11]);
 
 #ifdef __cplusplus
 }

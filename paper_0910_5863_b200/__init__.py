@@ -522,10 +522,10 @@ class BDDC:
                    r.seconds_eigen, r.seconds_preconditioner, r.root_size)
 
     def times(self) -> dict:
-        out = np.zeros(9)
+        out = np.zeros(11)
         _check(self._lib.bddc_b200_times(self._h, _dptr(out)))
         keys = ("analysis", "eigen", "preconditioner", "pcg", "leaf_flops", "leaf_front_bytes",
-                "schur_bytes", "root_size", "leaf_factor")
+                "schur_bytes", "root_size", "leaf_factor", "pcg_iterations", "pcg_bytes_per_iteration")
         return dict(zip(keys, out.tolist()))
 
     def step(self, mode: str, tau: float = 10.0, max_vectors: int = 15, keep_edge=False,

@@ -467,7 +467,7 @@ int bddc_b200_lanczos(const double* alphas, const double* betas, int64_t n, doub
   });
 }
 
-int bddc_b200_times(const bddc_b200_t* h, double out[9]) {
+int bddc_b200_times(const bddc_b200_t* h, double out[11]) {
   return guarded([&] {
     if (!h->engine) throw Error(kError, "no engine yet");
     const PhaseTimes& t = h->engine->times();
@@ -480,6 +480,8 @@ int bddc_b200_times(const bddc_b200_t* h, double out[9]) {
     out[6] = h->engine->schur_bytes();
     out[7] = h->engine->root_size();
     out[8] = t.leaf_factor;
+    out[9] = t.pcg_iterations;
+    out[10] = h->engine->pcg_bytes_per_iteration();
   });
 }
 

@@ -1043,6 +1043,19 @@ double Engine::schur_bytes() const {
   return b;
 }
 
+double Engine::pcg_bytes_per_iteration() const {
+  const DeviceState& D = *d_;
+  double b = schur_bytes();
+  if (D.NF.size() == std::size_t(D.nsub))
+    for (int s : D.own) {
+      const double e = D.nE[s], c = D.nC[s];
+      // explicit: E = [-F_ee^{-1} | -W] forward, W backward; factor: L twice
+      b += (D.leaf_explicit ? e * (e + c) + e * c : 2.0 * (e * (e + 1) / 2 + e * c)) * 8.0;
+    }
+  b += double(D.n_root) * D.n_root * 8.0;  // R^{-1} GEMV, or both triangular root sweeps
+  return b;
+}
+
 double Engine::leaf_front_bytes() const {
   const DeviceState& D = *d_;
   double b = 0;
@@ -1727,6 +1740,7 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
   }
   CK(cudaEventRecord(D.e1, st));
   times_.pcg = elapsed(D.e0, D.e1);
+  times_.pcg_iterations = hs.it;
   CK(cudaGetLastError());
   out.iterations = hs.it;
   out.relative_residual = hs.relres;

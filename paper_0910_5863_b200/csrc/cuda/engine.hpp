@@ -59,6 +59,7 @@ struct PhaseTimes {  // device-timed seconds (CUDA events) of the last calls
   double analysis = 0, eigen = 0, preconditioner = 0, pcg = 0;
   double leaf_factor = 0;  // the batched partial Cholesky of the substructure leaves
   double flops_leaf = 0;   // algorithmic FP64 flops of the last leaf factorization
+  int pcg_iterations = 0;  // of the last pcg()
 };
 
 /// One pass of the hot path (bench "step"): analysis + constraint selection
@@ -122,6 +123,9 @@ class Engine {
   const PhaseTimes& times() const { return times_; }
   double leaf_front_bytes() const;   // bytes of the preconditioner's leaf factors (+root)
   double schur_bytes() const;        // bytes of the dense S_s read per Schur apply
+  /// Algorithmic bytes of one PCG iteration: the dense S_s of the Schur apply,
+  /// the leaf operators of both preconditioner sweeps and the root apply.
+  double pcg_bytes_per_iteration() const;
   cudaStream_t stream() const;
 
  private:
