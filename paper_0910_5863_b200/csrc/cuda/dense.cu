@@ -296,10 +296,13 @@ __global__ void __launch_bounds__(PANEL_THREADS) k_panel(const FrontDesc* ds, in
     for (int e = tid; e < m * m; e += PANEL_THREADS) {
       const int rr = o + 16 + e % m, cc = o + 16 + e / m;
       if (rr < cc) continue;
-      double s = 0.0;
+      double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) s += L[(o + k) * LDS + rr] * L[(o + k) * LDS + cc];
-      L[cc * LDS + rr] -= s;
+      for (int k = 0; k < 16; k += 2) {
+        s0 += L[(o + k) * LDS + rr] * L[(o + k) * LDS + cc];
+        s1 += L[(o + k + 1) * LDS + rr] * L[(o + k + 1) * LDS + cc];
+      }
+      L[cc * LDS + rr] -= s0 + s1;
     }
     __syncthreads();
   }
@@ -329,9 +332,14 @@ __global__ void __launch_bounds__(PANEL_THREADS) k_panel(const FrontDesc* ds, in
     for (int e = tid; e < nblk * 256; e += PANEL_THREADS) {
       const int b = e >> 8, r = (e >> 4) & 15, c = e & 15;
       const int bj = b, bi = b + dd;
-      double s = 0.0;
-      for (int k = bj * 16; k < bi * 16; ++k) s += L[k * LDS + bi * 16 + r] * V[(bj * 16 + c) * LDS + k];
-      T[b][r][c] = s;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      for (int k = bj * 16; k < bi * 16; k += 4) {
+        s0 += L[k * LDS + bi * 16 + r] * V[(bj * 16 + c) * LDS + k];
+        s1 += L[(k + 1) * LDS + bi * 16 + r] * V[(bj * 16 + c) * LDS + k + 1];
+        s2 += L[(k + 2) * LDS + bi * 16 + r] * V[(bj * 16 + c) * LDS + k + 2];
+        s3 += L[(k + 3) * LDS + bi * 16 + r] * V[(bj * 16 + c) * LDS + k + 3];
+      }
+      T[b][r][c] = (s0 + s1) + (s2 + s3);
     }
     __syncthreads();
     // Linv_{bi,bj} = -Linv_{bi,bi} T_b
