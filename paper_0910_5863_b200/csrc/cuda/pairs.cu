@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 
 #include "dense.cuh"
 #include "devbuf.cuh"
@@ -42,7 +43,7 @@ struct PairDev {
   // sides
   const double* S[2];   // interface Schur of each side (PB x PB)
   int PB[2];
-  const int* pos[2];    // front index -> boundary position: [outer | corner | shared]
+  const int* pos[2];    // kept slots [corner | shared] -> boundary position in S_s
   double* G[2];         // side fronts
   int NG[2], PO[2], no[2];
   int nc, nf, nj, nm, PQ, PJ, k;
@@ -76,9 +77,21 @@ __device__ __forceinline__ double kdot(const PairDev& d, int b, F f) {
 }  // namespace
 
 // Grow-only arenas of the pair reductions, reused across enrich() calls.
+// Gather of a front [outer | kept] from a symmetric source (lower triangle
+// read), identity on the padding: the hub fronts from S_s and the side fronts
+// from the hubs' Schur complements.
+struct GatherDesc {
+  const double* src;
+  const int* pos;  // front index (outer, then kept) -> source index
+  double* dst;
+  int ld, N, PO, no, m1;
+};
+
 struct PairBuffers {
-  DBuf<double> G, Q, F, Dv, M, KV, H, N, R, A, E, W, Fu;
-  DBuf<int> Pv, info, KR;
+  DBuf<double> G, Q, F, Dv, M, KV, H, N, R, A, E, W, Fu, Hub, DvH;
+  DBuf<int> Pv, info, KR, Gpos, Hpos, hinfo;
+  DBuf<GatherDesc> ghub, gside;
+  DBuf<FrontDesc> dHub;
   DBuf<int4> KC;
   DBuf<PairDev> dpd;
   DBuf<FrontDesc> dG, dQ, d3, d4;
@@ -90,26 +103,25 @@ PairEngine::~PairEngine() = default;
 
 namespace {
 
-// (a) side fronts: G_s[a][b] = S_s[pos a, pos b] with identity pads
-__global__ void k_gather_G(const PairDev* pd) {
-  const PairDev d = pd[blockIdx.y >> 1];
-  const int side = blockIdx.y & 1;
-  const int NG = d.NG[side], PO = d.PO[side], no = d.no[side], m1 = d.nc + d.nf;
+__global__ void k_gather_front(const GatherDesc* gd) {
+  const GatherDesc d = gd[blockIdx.y];
   const int col = blockIdx.x;
-  if (col >= NG) return;
-  auto valid = [&](int a) { return a < no || (a >= PO && a < PO + m1); };
-  auto bidx = [&](int a) { return a < no ? a : no + (a - PO); };
-  const int* pos = d.pos[side];
-  double* G = d.G[side] + (size_t)col * NG;
+  if (col >= d.N) return;
+  auto valid = [&](int a) { return a < d.no || (a >= d.PO && a < d.PO + d.m1); };
+  auto bidx = [&](int a) { return a < d.no ? a : d.no + (a - d.PO); };
   const bool vc = valid(col);
-  const double* Sc = vc ? d.S[side] + (size_t)pos[bidx(col)] * d.PB[side] : nullptr;
-  for (int r = threadIdx.x; r < NG; r += blockDim.x) {
+  const int pc = vc ? d.pos[bidx(col)] : 0;
+  double* out = d.dst + (size_t)col * d.N;
+  for (int r = threadIdx.x; r < d.N; r += blockDim.x) {
     double v;
-    if (vc && valid(r))
-      v = Sc[pos[bidx(r)]];
-    else
+    if (vc && valid(r)) {
+      const int pr = d.pos[bidx(r)];
+      const int hi = pr >= pc ? pr : pc, lo = pr >= pc ? pc : pr;
+      v = d.src[(size_t)lo * d.ld + hi];
+    } else {
       v = (r == col) ? 1.0 : 0.0;
-    G[r] = v;
+    }
+    out[r] = v;
   }
 }
 
@@ -126,7 +138,7 @@ __global__ void k_build_M(const PairDev* pd) {
   const int nf = d.nf;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nf * nf; e += gridDim.x * blockDim.x) {
     const int t = e % nf, u = e / nf;
-    const int base_i = d.no[0] + d.nc, base_j = d.no[1] + d.nc;
+    const int base_i = d.nc, base_j = d.nc;  // pos points at the kept slots [corner | shared]
     const double ci = d.S[0][(size_t)d.pos[0][base_i + u] * d.PB[0] + d.pos[0][base_i + t]];
     const double cj = d.S[1][(size_t)d.pos[1][base_j + u] * d.PB[1] + d.pos[1][base_j + t]];
     const double rt = d.rho[t], ru = d.rho[u];
@@ -770,6 +782,9 @@ namespace detail {
 struct HostPair {
   PairIndex idx;
   std::vector<int> pos[2];   // [outer | corner | shared] boundary positions per side
+  int hub[2] = {-1, -1};     // two-level side fronts: the hub of each side
+  int nout[2] = {0, 0};      // hub slots eliminated in the side front (U \ K)
+  std::vector<int> gpos[2];  // [U \ K | corner | shared] as indices into the hub's U
   std::vector<int4> kc;      // compact kernel columns (unit row, r, rows off, vals off), pair-local offsets
   std::vector<int> krows;
   std::vector<double> kvals;
@@ -778,13 +793,22 @@ struct HostPair {
   int nj = 0, nm = 0, r_total = 0;    // r_total = admissible columns - nullity
 };
 
+// Hub of the two-level side-front elimination: substructure s, side g (1: its
+// faces towards higher neighbours, 0: towards lower), U = union of the pair
+// faces' closures (kept), rest = its other boundary slots (eliminated first).
+struct Hub {
+  int s = 0, g = 0;
+  std::vector<int> U, rest;  // boundary positions, ascending
+};
+
 struct Dims { int no[2], PO[2], NG[2], nc, nf, nj, PQ, PJ, k, nm; };
 struct ChunkHost {
   int p0 = 0, p1 = 0;
   std::vector<Dims> dims;
-  std::vector<int> posv, krv;
+  std::vector<int> posv, krv, gposv;
   std::vector<int4> kcv;
   std::vector<double> kvv, Nv, Rv;
+  std::vector<long long> oGp;  // per side: offset into gposv
   std::vector<long long> oG, oQ, oF3, oF4, oM, oKC, oKR, oKV, oH, oN, oR, oA, oE, oW, oFu, oDG, oDQ, oD3, oD4, oP;
   long long nG = 0, nQ = 0, nF = 0, nM = 0, nH = 0, nA = 0, nE = 0, nW = 0, nFu = 0, nD = 0;
 };
@@ -793,6 +817,7 @@ ChunkHost build_chunk(const std::vector<HostPair>& hp, int p0, int request);
 using detail::HostPair;
 using detail::ChunkHost;
 using detail::Dims;
+using detail::Hub;
 
 // Host preparation of the face-pair eigenproblems: depends on the model and the
 // base constraint set only, so Engine::step runs it while the leaf
@@ -803,6 +828,7 @@ struct PairPrep {
   std::vector<int> gidx;                    // their positions in face_pairs(m)
   std::vector<HostPair> hp;
   std::vector<ChunkHost> chunks;
+  std::vector<Hub> hubs;
   int request = 0;
   double prep_ms = 0.0;
 };
@@ -876,7 +902,7 @@ ChunkHost build_chunk(const std::vector<HostPair>& hp, int p0, int request) {
     dm.nm = h.nm;
     const int m1 = dm.nc + dm.nf;
     for (int side = 0; side < 2; ++side) {
-      dm.no[side] = static_cast<int>((side == 0 ? h.idx.outer_i : h.idx.outer_j).size());
+      dm.no[side] = h.nout[side];  // slots of the side's hub eliminated in its side front
       dm.PO[side] = rup(dm.no[side], kTile);
       dm.NG[side] = dm.PO[side] + rup(std::max(m1, 1), kTile);
     }
@@ -903,6 +929,8 @@ ChunkHost build_chunk(const std::vector<HostPair>& hp, int p0, int request) {
   auto& oE = sized(ch.oE, nb); auto& oW = sized(ch.oW, nb); auto& oFu = sized(ch.oFu, nb);
   auto& oDG = sized(ch.oDG, 2 * nb); auto& oDQ = sized(ch.oDQ, nb); auto& oD3 = sized(ch.oD3, nb);
   auto& oD4 = sized(ch.oD4, nb); auto& oP = sized(ch.oP, 2 * nb);
+  auto& oGp = sized(ch.oGp, 2 * nb);
+  auto& gposv = ch.gposv;
   for (int b = 0; b < nb; ++b) {
     const Dims& dm = dims[b];
     const HostPair& h = hp[p0 + b];
@@ -913,6 +941,8 @@ ChunkHost build_chunk(const std::vector<HostPair>& hp, int p0, int request) {
       nD += (long long)(dm.PO[side] / kTile) * kTile * kTile;
       oP[2 * b + side] = posv.size();
       posv.insert(posv.end(), h.pos[side].begin(), h.pos[side].end());
+      oGp[2 * b + side] = gposv.size();
+      gposv.insert(gposv.end(), h.gpos[side].begin(), h.gpos[side].end());
     }
     const int NQ = dm.PQ + dm.PJ, N2 = 2 * dm.PJ, n2 = dm.nj + (dm.nj & 1);
     oQ[b] = nQ;
@@ -1048,6 +1078,79 @@ std::shared_ptr<PairPrep> PairEngine::prepare(const ConstraintSet& cs, const Enr
     h.r_total = n_adm - h.nm;
     (void)m1;
   }
+  // pass 4: hubs of the two-level side fronts.  Side 0 of a pair is its lower
+  // substructure (the face is on that substructure's upper side, g = 1).  Used
+  // when the pairs fill the GPU (the extra stage costs latency on small runs);
+  // BDDC_B200_GTREE=0|1 overrides.
+  bool two_level = np >= sm_count();
+  if (const char* env = std::getenv("BDDC_B200_GTREE")) {
+    if (*env == '0') two_level = false;
+    if (*env == '1') two_level = true;
+  }
+  if (!two_level) {
+    // single level: the side front [outer | corner | shared] straight from S_s
+    for (int p = 0; p < np; ++p)
+      for (int side = 0; side < 2; ++side) {
+        HostPair& h = hp[p];
+        h.hub[side] = -1;
+        h.nout[side] = static_cast<int>((side == 0 ? h.idx.outer_i : h.idx.outer_j).size());
+        h.gpos[side] = h.pos[side];
+      }
+  } else {
+    std::map<std::pair<int, int>, int> hub_of;
+    auto& hubs = prep->hubs;
+    for (int p = 0; p < np; ++p)
+      for (int side = 0; side < 2; ++side) {
+        const int s = side == 0 ? hp[p].idx.si : hp[p].idx.sj, g = side == 0 ? 1 : 0;
+        auto it = hub_of.find({s, g});
+        if (it == hub_of.end()) {
+          it = hub_of.emplace(std::make_pair(s, g), static_cast<int>(hubs.size())).first;
+          Hub hb;
+          hb.s = s;
+          hb.g = g;
+          hubs.push_back(hb);
+        }
+        hp[p].hub[side] = it->second;
+      }
+    // U = union of the kept slots (corner + shared) of the hub's pair sides
+    std::vector<std::vector<char>> inU(hubs.size());
+    for (std::size_t q = 0; q < hubs.size(); ++q) inU[q].assign(m.subs[hubs[q].s].boundary.size(), 0);
+    for (int p = 0; p < np; ++p)
+      for (int side = 0; side < 2; ++side) {
+        const auto& pos = hp[p].pos[side];
+        const int no = static_cast<int>((side == 0 ? hp[p].idx.outer_i : hp[p].idx.outer_j).size());
+        for (std::size_t a = no; a < pos.size(); ++a) inU[hp[p].hub[side]][pos[a]] = 1;
+      }
+    std::vector<std::vector<int>> idxU(hubs.size());
+    for (std::size_t q = 0; q < hubs.size(); ++q) {
+      idxU[q].assign(inU[q].size(), -1);
+      for (int b = 0; b < static_cast<int>(inU[q].size()); ++b) {
+        if (inU[q][b]) {
+          idxU[q][b] = static_cast<int>(hubs[q].U.size());
+          hubs[q].U.push_back(b);
+        } else {
+          hubs[q].rest.push_back(b);
+        }
+      }
+    }
+    // side fronts from the hub: [U \ K | corner | shared] as indices into U
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int p = 0; p < np; ++p)
+      for (int side = 0; side < 2; ++side) {
+        HostPair& h = hp[p];
+        const int q = h.hub[side];
+        const auto& pos = h.pos[side];
+        const int no = static_cast<int>((side == 0 ? h.idx.outer_i : h.idx.outer_j).size());
+        std::vector<char> inK(hubs[q].U.size(), 0);
+        for (std::size_t a = no; a < pos.size(); ++a) inK[idxU[q][pos[a]]] = 1;
+        auto& gp = h.gpos[side];
+        gp.clear();
+        for (int u = 0; u < static_cast<int>(hubs[q].U.size()); ++u)
+          if (!inK[u]) gp.push_back(u);
+        h.nout[side] = static_cast<int>(gp.size());
+        for (std::size_t a = no; a < pos.size(); ++a) gp.push_back(idxU[q][pos[a]]);
+      }
+  }
   for (int p0 = 0; p0 < np;) {
     prep->chunks.push_back(detail::build_chunk(hp, p0, prep->request));
     p0 = prep->chunks.back().p1;
@@ -1069,6 +1172,60 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
   EnrichOutcome out;
   std::vector<std::vector<double>> all_evals(np), all_funcs(np);
   std::vector<int> all_k(np);
+  // hub stage of the two-level side fronts: [rest | U] gathered from S_s, the
+  // rest eliminated once per hub (Schur complement onto U in the trailing block)
+  const auto& hubs = prep->hubs;
+  const int nh = static_cast<int>(hubs.size());
+  std::vector<int> hubNH(nh), hubPH(nh);
+  std::vector<long long> hubOff(nh);
+  {
+    HostTimer hth("enrich hubs");
+    PairBuffers& B_ = *bufs_;
+    long long nH = 0, nDH = 0;
+    int maxNH = 0, maxPH = 0, maxMH = 0;
+    std::vector<int> hposv;
+    std::vector<GatherDesc> gh(nh);
+    std::vector<FrontDesc> fh(nh);
+    std::vector<long long> hposOff(nh), hubDOff(nh);
+    for (int q = 0; q < nh; ++q) {
+      const int nR = static_cast<int>(hubs[q].rest.size()), nU = static_cast<int>(hubs[q].U.size());
+      hubPH[q] = rup(nR, kTile);
+      hubNH[q] = hubPH[q] + rup(std::max(nU, 1), kTile);
+      hubOff[q] = nH;
+      nH += (long long)hubNH[q] * hubNH[q];
+      hubDOff[q] = nDH;
+      nDH += (long long)(hubPH[q] / kTile) * kTile * kTile;
+      hposOff[q] = hposv.size();
+      hposv.insert(hposv.end(), hubs[q].rest.begin(), hubs[q].rest.end());
+      hposv.insert(hposv.end(), hubs[q].U.begin(), hubs[q].U.end());
+      maxNH = std::max(maxNH, hubNH[q]);
+      maxPH = std::max(maxPH, hubPH[q]);
+      maxMH = std::max(maxMH, hubNH[q] - hubPH[q]);
+    }
+    if (nh) {
+      B_.Hub.alloc(nH);
+      B_.DvH.alloc(std::max<long long>(nDH, 1));
+      B_.Hpos.upload(hposv, st_);
+      B_.hinfo.alloc(nh);
+      CK(cudaMemsetAsync(B_.hinfo.p, 0, nh * sizeof(int), st_));
+      for (int q = 0; q < nh; ++q) {
+        const int sub = hubs[q].s;
+        gh[q] = GatherDesc{S_ + s_off_[sub], B_.Hpos.p + hposOff[q], B_.Hub.p + hubOff[q], PB_[sub], hubNH[q],
+                           hubPH[q], static_cast<int>(hubs[q].rest.size()), static_cast<int>(hubs[q].U.size())};
+        fh[q] = FrontDesc{B_.Hub.p + hubOff[q], B_.DvH.p + hubDOff[q], hubNH[q], hubPH[q], B_.hinfo.p + q, 0};
+      }
+      B_.ghub.upload(gh, st_);
+      B_.dHub.upload(fh, st_);
+      StageProfiler hprof("enrich", st_);
+      k_gather_front<<<dim3(maxNH, nh), 128, 0, st_>>>(B_.ghub.p);
+      count_launch(1);
+      CK(cudaGetLastError());
+      hprof.mark("gatherHub");
+      partial_cholesky(B_.dHub.p, nh, maxNH, maxPH, maxMH, st_);
+      CK(cudaGetLastError());
+      hprof.mark("cholHub");
+    }
+  }
   int p0 = 0;
   std::size_t chunk_id = 0;
   while (p0 < np) {
@@ -1108,6 +1265,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     W.alloc(nW);
     Fu.alloc(std::max<long long>(nFu, 1));
     Pv.upload(posv, st_);
+    if (ch.gposv.empty()) B_.Gpos.alloc(1); else B_.Gpos.upload(ch.gposv, st_);
     info.alloc(4 * nb);
     CK(cudaMemsetAsync(info.p, 0, 4 * nb * sizeof(int), st_));
     ht.mark("alloc_upload");
@@ -1121,7 +1279,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
         const int s = side == 0 ? h.idx.si : h.idx.sj;
         d.S[side] = S_ + s_off_[s];
         d.PB[side] = PB_[s];
-        d.pos[side] = Pv.p + oP[2 * b + side];
+        d.pos[side] = Pv.p + oP[2 * b + side] + (side == 0 ? h.idx.outer_i : h.idx.outer_j).size();
         d.G[side] = G.p + oG[2 * b + side];
         d.NG[side] = dm.NG[side];
         d.PO[side] = dm.PO[side];
@@ -1175,7 +1333,25 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     ht.mark("descriptors");
     StageProfiler prof("enrich", st_);
     // (a)-(b) side fronts, eliminate the outer skeleton
-    k_gather_G<<<dim3(maxNG, 2 * nb), 128, 0, st_>>>(dpd.p);
+    {
+      // side fronts [U \ K | corner | shared] from the hubs' Schur complements
+      std::vector<GatherDesc> gs(2 * nb);
+      for (int b = 0; b < nb; ++b)
+        for (int side = 0; side < 2; ++side) {
+          const HostPair& h = hp[p0 + b];
+          const int q = h.hub[side];
+          const int sub = side == 0 ? h.idx.si : h.idx.sj;
+          const double* src = q >= 0 ? B_.Hub.p + hubOff[q] + (size_t)hubPH[q] * hubNH[q] + hubPH[q]
+                                     : S_ + s_off_[sub];
+          const int lds = q >= 0 ? hubNH[q] : PB_[sub];
+          gs[2 * b + side] = GatherDesc{src, B_.Gpos.p + ch.oGp[2 * b + side], pd[b].G[side], lds,
+                                        dims[b].NG[side], dims[b].PO[side], dims[b].no[side],
+                                        dims[b].nc + dims[b].nf};
+        }
+      B_.gside.upload(gs, st_);
+      k_gather_front<<<dim3(maxNG, 2 * nb), 128, 0, st_>>>(B_.gside.p);
+      count_launch(1);
+    }
     CK(cudaGetLastError());
     prof.mark("gatherG");
     partial_cholesky(dG.p, 2 * nb, maxNG, maxPO, maxM1, st_);
@@ -1240,6 +1416,14 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     CK(cudaMemcpyAsync(fu.data(), Fu.p, Fu.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
     CK(cudaMemcpyAsync(inf.data(), info.p, 4 * nb * sizeof(int), cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
+    if (chunk_id == 1 && nh) {
+      std::vector<int> hinf(nh);
+      CK(cudaMemcpy(hinf.data(), B_.hinfo.p, nh * sizeof(int), cudaMemcpyDeviceToHost));
+      for (int q = 0; q < nh; ++q)
+        if (hinf[q])
+          throw Error(kNotPositiveDefinite, "pair eigenproblem hub of substructure " + std::to_string(hubs[q].s) +
+                                                ": reduction not positive definite");
+    }
     for (int b = 0; b < nb; ++b) {
       for (int q = 0; q < 4; ++q)
         if (inf[4 * b + q])

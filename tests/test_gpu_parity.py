@@ -205,3 +205,23 @@ def test_max_iterations_marks_rows_unconverged():
     row = b.run_item("c")
     assert not row.converged and row.iterations == 2
     assert "2*" in pb.emit_table([row], include_times=False)
+
+
+@pytest.mark.parametrize("gtree", ["0", "1"])
+def test_side_front_elimination_levels(gtree, monkeypatch):
+    """Single-level and two-level (hub) side-front eliminations give the
+    oracle's selection and spectrum (cfg4 3x3x3 H/h=4: both sides of every
+    face pair, corners + faces base)."""
+    monkeypatch.setenv("BDDC_B200_GTREE", gtree)
+    spec = baseline_config(4, subdomains=(3, 3, 3), elements_per_edge=4).spec
+    p = build_pipeline(spec)
+    ref = solve_item(p, "adaptive", 10.0, 15, base_faces=True)
+    b = pb.BDDC(config=4, subdomains=(3, 3, 3), elements_per_edge=4)
+    row = b.run_item("adaptive", 10.0, 15, base_faces=True)
+    assert row.constraint_rows == ref.constraint_rows
+    for rep, orep in zip(b.pair_reports(), ref.outcome.pairs):
+        assert rep["enforced"] == orep.enforced
+        e0 = np.asarray(orep.eigenvalues)
+        big = e0 > 1e-6 * max(e0.max(), 1e-300)
+        assert np.all(np.abs(rep["eigenvalues"][big] - e0[big]) <= 1e-6 * e0[big])
+    assert abs(row.iterations - ref.iterations) <= 1
