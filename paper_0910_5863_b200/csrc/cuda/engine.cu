@@ -158,42 +158,9 @@ __device__ __forceinline__ double xform_T_t(const XformDesc& x, int inst, int j,
   for (int i = 0; i < r; ++i) s += D[i * n + j] * v[pos[perm[i]]];
   return s;
 }
-// x_orig = T x_new at glob slot a
-__device__ __forceinline__ double xform_T(const XformDesc& x, int inst, int a, const double* xn) {
-  const int tr = x.inst_tr[inst];
-  const int* pos = x.tpos + x.inst_pos[inst];
-  const int n = x.tr_n[tr], r = x.tr_r[tr];
-  const int i = x.iperm[x.tr_off_perm[tr] + a];
-  if (i >= r) return xn[pos[i]];
-  const double* D = x.D + x.tr_off_d[tr] + i * n;
-  double s = 0.0;
-  for (int jj = 0; jj < n; ++jj) s += D[jj] * xn[pos[jj]];
-  return s;
-}
 
-// Schur apply, step 1: WB_s = S_s * p[biface]   (schur.cpp:12-36 with S_s dense)
-__global__ void __launch_bounds__(256) k_schur_gemv(const SubDesc* sd, const double* __restrict__ p, const int* done) {
-  if (done && *done) return;
-  const SubDesc d = sd[blockIdx.x];
-  extern __shared__ double xs[];
-  for (int c = threadIdx.x; c < d.nB; c += blockDim.x) xs[c] = p[d.biface[c]];
-  __syncthreads();
-  for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
-    const double* col = d.S + b;
-    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-    int c = 0;
-    for (; c + 4 <= d.nB; c += 4) {
-      s0 += col[(size_t)c * d.PB] * xs[c];
-      s1 += col[(size_t)(c + 1) * d.PB] * xs[c + 1];
-      s2 += col[(size_t)(c + 2) * d.PB] * xs[c + 2];
-      s3 += col[(size_t)(c + 3) * d.PB] * xs[c + 3];
-    }
-    for (; c < d.nB; ++c) s0 += col[(size_t)c * d.PB] * xs[c];
-    d.WB[b] = (s0 + s1) + (s2 + s3);
-  }
-}
-
-// Row-blocked variant: CTA (rb, s) forms rows [64 rb, 64 rb + 64) of S_s x_s.
+// Schur apply, step 1 (schur.cpp:12-36 with S_s dense): WB_s = S_s * p[biface].
+// Row-blocked: CTA (rb, s) forms rows [64 rb, 64 rb + 64) of S_s x_s.
 // Lane l of warp w owns rows (2l, 2l+1) (one 16-byte load per column) and the
 // columns w, w+8, ...; eight columns are in flight per thread, the eight warp
 // partials are reduced in shared memory in a fixed order.
@@ -408,9 +375,6 @@ __global__ void k_root_gather(int n_root, int NR, const int* __restrict__ ptr, c
     xr[k] = s;
   }
 }
-
-// Guarded wrappers around the front solves (skip when PCG is done)
-__global__ void k_noop() {}
 
 // F_s column transform: X = S T (glob columns), other columns copied
 __global__ void k_colxform(const SubDesc* sd, XformDesc x, double* Xarena, const long long* xoff) {

@@ -278,8 +278,6 @@ std::vector<int> grid_neighbors(const Mesh& m, int node) {  // globs.cpp:21-34
   return out;
 }
 
-int kind_rank(int k) { return k; }
-
 void sort_canonical(std::vector<Glob>& globs) {  // globs.cpp:38-44
   std::sort(globs.begin(), globs.end(), [](const Glob& a, const Glob& b) {
     if (a.kind != b.kind) return a.kind < b.kind;
