@@ -609,6 +609,144 @@ __global__ void __launch_bounds__(256) k_front_backward_cl(const SolveDesc* ds, 
   cl.sync();
 }
 
+// ---------------------------------------------------------------------------
+// One large front (the root when R^{-1} is not formed) over the whole GPU:
+// a cooperative grid of G CTAs, row tile t owned by CTA t % G, the CTA's own
+// rows kept in shared memory.  Forward: at block kb every CTA updates its rows
+// below with z_kb; the owner of tile kb+1 then forms z_{kb+1} (its rows are
+// final) -- one grid barrier per block.  Backward: every CTA writes the
+// partial sums of its rows, and after the barrier the owner of tile kb adds
+// them in CTA order and solves the block (deterministic).
+// ---------------------------------------------------------------------------
+// out = Dinv_kb * xb (64 values); the owner's copy of the block := out
+__device__ __forceinline__ void big_z(const SolveDesc& d, int kb, double* xb, double* out) {
+  const int tid = threadIdx.x, row = tid >> 2, part = tid & 3;
+  const double* dv = d.dinv + (size_t)kb * 64 * 64;
+  double sum = 0.0;
+  for (int c = part; c < 64; c += 4) sum += dv[(size_t)c * 64 + row] * xb[c];
+  sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+  sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+  __syncthreads();
+  if (part == 0) {
+    out[row] = sum;
+    xb[row] = sum;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_big_forward(const SolveDesc* ds, double* zbuf, const int* done) {
+  if (done && *done) return;
+  cg::grid_group grid = cg::this_grid();
+  const SolveDesc d = ds[0];
+  const int G = gridDim.x, me = blockIdx.x, tid = threadIdx.x;
+  const int nt = d.n / kTile, nb = d.p / kTile;
+  extern __shared__ double xs[];  // own tiles: tile t at (t / G) * 64
+  __shared__ double zs[64];
+  for (int t = me; t < nt; t += G)
+    for (int r = tid; r < 64; r += 256) xs[(t / G) * 64 + r] = d.x[(size_t)t * 64 + r];
+  __syncthreads();
+  const size_t ld = d.n;
+  if (nb > 0 && me == 0) big_z(d, 0, xs, zbuf);
+  grid.sync();
+  for (int kb = 0; kb < nb; ++kb) {
+    if (tid < 64) zs[tid] = zbuf[(kb & 1) * 64 + tid];
+    __syncthreads();
+    const int k0 = kb * kTile;
+    const int first = kb + 1 + ((me - (kb + 1) % G) % G + G) % G;  // own tiles below the block
+    const int ntl = first < nt ? (nt - 1 - first) / G + 1 : 0;
+    for (int i = tid; i < 64 * ntl; i += 256) {
+      const int t = first + (i >> 6) * G, r = t * 64 + (i & 63);
+      const double* col = d.a + (size_t)k0 * ld + r;
+      double sq[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sq[q] = 0.0;
+#pragma unroll 2
+      for (int c = 0; c < 64; c += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sq[q] += col[(size_t)(c + q) * ld] * zs[c + q];
+      }
+      xs[(t / G) * 64 + (i & 63)] -= ((sq[0] + sq[1]) + (sq[2] + sq[3])) + ((sq[4] + sq[5]) + (sq[6] + sq[7]));
+    }
+    __syncthreads();
+    if (kb + 1 < nb && (kb + 1) % G == me) big_z(d, kb + 1, xs + ((kb + 1) / G) * 64, zbuf + ((kb + 1) & 1) * 64);
+    grid.sync();
+  }
+  for (int t = me; t < nt; t += G)
+    for (int r = tid; r < 64; r += 256) d.x[(size_t)t * 64 + r] = xs[(t / G) * 64 + r];
+}
+
+__global__ void __launch_bounds__(256) k_big_backward(const SolveDesc* ds, double* pbuf, const int* done) {
+  if (done && *done) return;
+  cg::grid_group grid = cg::this_grid();
+  const SolveDesc d = ds[0];
+  const int G = gridDim.x, me = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nt = d.n / kTile, nb = d.p / kTile;
+  extern __shared__ double xs[];
+  __shared__ double part[64], tv[64];
+  for (int t = me; t < nt; t += G)
+    for (int r = tid; r < 64; r += 256) {
+      const int row = t * 64 + r;
+      double v = d.x[row];
+      if (d.cmap && row >= d.p) {
+        const int k = d.cmap[row - d.p];
+        v = k >= 0 ? d.croot[k] : 0.0;
+      }
+      xs[(t / G) * 64 + r] = v;
+    }
+  __syncthreads();
+  const size_t ld = d.n;
+  for (int kb = nb - 1; kb >= 0; --kb) {
+    const int k0 = kb * kTile;
+    {
+      double acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+      const double* base = d.a + (size_t)(k0 + warp) * ld;
+      const int first = kb + 1 + ((me - (kb + 1) % G) % G + G) % G;
+      for (int t = first; t < nt; t += G) {
+        const int r = t * 64 + 2 * lane;
+        const double x0 = xs[(t / G) * 64 + 2 * lane], x1 = xs[(t / G) * 64 + 2 * lane + 1];
+        double2 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = __ldg(reinterpret_cast<const double2*>(base + (size_t)(8 * q) * ld + r));
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += v[q].x * x0 + v[q].y * x1;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double sum = acc[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) part[warp + 8 * q] = sum;
+      }
+    }
+    __syncthreads();
+    if (tid < 64) pbuf[((size_t)(kb & 1) * G + me) * 64 + tid] = part[tid];
+    grid.sync();
+    if (kb % G == me) {
+      double* xb = xs + (kb / G) * 64;
+      if (tid < 64) {
+        const double* ps = pbuf + (size_t)(kb & 1) * G * 64 + tid;
+        double sum = 0.0;
+        for (int g = 0; g < G; ++g) sum += ps[(size_t)g * 64];
+        tv[tid] = xb[tid] - sum;
+      }
+      __syncthreads();
+      const int row = tid >> 2, prt = tid & 3;
+      const double* dv = d.dinv + (size_t)kb * 64 * 64 + (size_t)row * 64;
+      double sum = 0.0;
+      for (int c = prt; c < 64; c += 4) sum += dv[c] * tv[c];
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      __syncthreads();
+      if (prt == 0) xb[row] = sum;
+    }
+    __syncthreads();
+  }
+  for (int t = me; t < nt; t += G)
+    for (int r = tid; r < 64; r += 256) d.x[(size_t)t * 64 + r] = xs[(t / G) * 64 + r];
+}
+
 __global__ void k_copy_trailing(const TrailDesc* ds) {
   const TrailDesc d = ds[blockIdx.y];
   const int m = d.n - d.p;
@@ -631,6 +769,8 @@ void configure() {
   cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * LDS * (int)sizeof(double));
   cudaFuncSetAttribute(k_front_forward<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_backward_cl<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_big_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_big_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_forward_cl<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_forward_cl<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_backward_cl<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -643,15 +783,15 @@ std::atomic<long long> g_launches{0};
 // Grow-only split-K workspace, one per stream: work on one stream is ordered,
 // and engines (one stream each, possibly driven by different host threads of
 // one process) never share a workspace.
-double* splitk_workspace(size_t doubles, cudaStream_t stream) {
+double* stream_workspace(int slot, size_t doubles, cudaStream_t stream) {
   struct Ws {
     double* p = nullptr;
     size_t cap = 0;
   };
   static std::mutex mu;
-  static std::map<cudaStream_t, Ws> ws;
+  static std::map<std::pair<cudaStream_t, int>, Ws> ws;
   std::lock_guard<std::mutex> lk(mu);
-  Ws& w = ws[stream];
+  Ws& w = ws[{stream, slot}];
   if (doubles > w.cap) {
     if (w.p) {
       cudaStreamSynchronize(stream);  // the old buffer may still be in use on this stream
@@ -666,6 +806,9 @@ double* splitk_workspace(size_t doubles, cudaStream_t stream) {
   }
   return w.p;
 }
+// slot 0: split-K partial tiles; slot 1: the large-front sweeps (small, never
+// reallocated once sized, so captured PCG graphs keep a valid pointer)
+double* splitk_workspace(size_t doubles, cudaStream_t stream) { return stream_workspace(0, doubles, stream); }
 
 }  // namespace
 
@@ -758,9 +901,45 @@ void launch_cluster(K kern, int cl, int batch, size_t smem, cudaStream_t stream,
 }
 }  // namespace
 
+namespace {
+// one front spread over the GPU when it is large (BDDC_B200_BIGSWEEP=0|1 overrides)
+bool big_sweep(int batch, int max_n) {
+  if (batch != 1) return false;
+  if (const char* env = std::getenv("BDDC_B200_BIGSWEEP")) {
+    if (*env == '0') return false;
+    if (*env == '1') return true;
+  }
+  return max_n >= 8192;
+}
+
+template <class K>
+void launch_big(K kern, int max_n, size_t ws_per_cta, cudaStream_t stream, const SolveDesc* d, const int* done) {
+  const int G = sm_count();
+  const int tiles = (max_n / kTile + G - 1) / G;
+  const size_t smem = (size_t)tiles * 64 * sizeof(double);
+  double* buf = stream_workspace(1, std::max<size_t>(ws_per_cta, 2 * 64) * G, stream);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, d, buf, done);
+}
+}  // namespace
+
 void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
   if (batch == 0) return;
   configure();
+  if (big_sweep(batch, max_n)) {
+    launch_big(k_big_forward, max_n, 2, stream, d_descs, done);  // z double buffer (2 x 64 <= 2 G)
+    count_launch(1);
+    return;
+  }
   const int cl = sweep_cluster(batch);
   const size_t smem = (max_n + 64 * 3) * sizeof(double);
   if (cl == 4) launch_cluster(k_front_forward_cl<4>, 4, batch, smem, stream, d_descs, done);
@@ -772,6 +951,11 @@ void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t 
 void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
   if (batch == 0) return;
   configure();
+  if (big_sweep(batch, max_n)) {
+    launch_big(k_big_backward, max_n, 2 * 64, stream, d_descs, done);  // partials: 2 x G x 64
+    count_launch(1);
+    return;
+  }
   const int cl = sweep_cluster(batch);
   const size_t smem = (64 * LDS + max_n + 64 + 2 * 4 * 64) * sizeof(double);
   if (cl == 4) launch_cluster(k_front_backward_cl<4>, 4, batch, smem, stream, d_descs, done);

@@ -91,14 +91,17 @@ OPS = [("el222h4 c+e", cube_spec((2, 2, 2), 4, fem.ELASTICITY), lambda: pb.BDDC(
        ("cfg1", baseline_config(1).spec, lambda: pb.BDDC(config=1), "c+e+f")]
 
 
-@pytest.mark.parametrize("leaf,root", [("explicit", "inverse"), ("factor", "inverse"), ("factor", "sweep")])
+@pytest.mark.parametrize("leaf,root,big", [("explicit", "inverse", "0"), ("factor", "inverse", "0"),
+                                            ("factor", "sweep", "0"), ("factor", "sweep", "1")])
 @pytest.mark.parametrize("name,spec,make,mode", OPS, ids=[o[0] for o in OPS])
-def test_operators_pcg_and_solution(name, spec, make, mode, leaf, root, monkeypatch):
+def test_operators_pcg_and_solution(name, spec, make, mode, leaf, root, big, monkeypatch):
     """Both leaf modes of the preconditioner (explicit F_ee^{-1} GEMVs
-    for small batches, front sweeps otherwise) and both root solvers (explicit
-    R^{-1} GEMV, triangular sweeps for large roots) against the oracle."""
+    for small batches, front sweeps otherwise) and the root solvers (explicit
+    R^{-1} GEMV; triangular sweeps on a cluster, or over the whole GPU with a
+    cooperative grid as for roots too large for R^{-1}) against the oracle."""
     monkeypatch.setenv("BDDC_B200_LEAF", leaf)
     monkeypatch.setenv("BDDC_B200_ROOT", root)
+    monkeypatch.setenv("BDDC_B200_BIGSWEEP", big)
     p = build_pipeline(spec)
     h = HarmonicExtension(p.systems, p.maps)
     itf = InterfaceProblem(p.systems, p.maps, h)
