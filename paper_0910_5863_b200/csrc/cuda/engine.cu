@@ -734,6 +734,13 @@ i64 Engine::interface_size() const { return static_cast<i64>(m_.maps.interface_d
 int Engine::root_size() const { return d_->n_root; }
 
 namespace {
+// device memory is tight (large runs): stage arenas are released after use
+bool memory_tight() {
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || tot == 0) return false;
+  return double(fr) < 0.35 * double(tot);
+}
+
 double elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
   CK(cudaEventSynchronize(b));
@@ -1311,14 +1318,17 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     const std::string mode = env ? env : "";
     D.root_inv = mode == "inverse" || (mode != "sweep" && D.NR <= kRootInverseMax);
   }
-  // Larger roots are solved by single-CTA sweeps whose vector lives in shared
-  // memory (front_forward/backward: (n + 64) doubles of at most 200 KB).  A
-  // dense root beyond that (cfg5: ~50k primal unknowns) needs a sparse or
-  // multilevel coarse solve, which this engine does not have.
-  if (!D.root_inv && (D.NR + 64) * 8 > 200 * 1024)
-    throw Error(kError, "dense root of " + std::to_string(D.n_root) +
-                            " primal unknowns exceeds the single-GPU root solver (limit 25536)");
+  // Larger roots are factored in place and solved by triangular sweeps (over
+  // the whole GPU for the largest ones).  The dense root must fit in memory.
   const long ldR = D.root_inv ? 2L * D.NR : D.NR;
+  {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const double need = double(ldR) * ldR * 8.0;  // the current root arena is freed before growing
+    if (need > double(fr) + double(D.R.cap) * 8.0)
+      throw Error(kError, "dense root of " + std::to_string(D.n_root) + " primal unknowns needs " +
+                              std::to_string(need / 1e9) + " GB; " + std::to_string(fr / 1e9) + " GB free");
+  }
   D.R.alloc((size_t)ldR * ldR);
   D.R.zero(st);
   D.DinvR.alloc((size_t)D.NR * kTile);
@@ -1367,6 +1377,10 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     count_launch(1);
   }
   CK(cudaGetLastError());
+  if (memory_tight()) {  // the transform scratch is dead once F is formed
+    CK(cudaStreamSynchronize(st));
+    D.Xtmp.release();
+  }
   prof.mark("xform");
   partial_cholesky(D.ffront.p, no, D.max_NA, D.max_PE, D.max_MA, st);
   if (D.leaf_explicit && no) {
@@ -1745,6 +1759,7 @@ StepOut Engine::step(const StepSpec& sp, ConstraintSet& cs, double* u_free_host)
   if (adaptive) {
     CK(cudaEventRecord(D.e0, st));
     out.omega_tilde = D.pairs.enrich(cs, o, prep).omega_tilde;
+    if (memory_tight()) D.pairs.release_buffers();
     CK(cudaEventRecord(D.e1, st));
     times_.eigen = elapsed(D.e0, D.e1);
   }
@@ -1769,6 +1784,7 @@ StepOut Engine::step(const StepSpec& sp, ConstraintSet& cs, double* u_free_host)
 EnrichOutcome Engine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
   CK(cudaEventRecord(d_->e0, d_->st));
   EnrichOutcome out = d_->pairs.enrich(cs, o);
+  if (memory_tight()) d_->pairs.release_buffers();
   CK(cudaEventRecord(d_->e1, d_->st));
   times_.eigen = elapsed(d_->e0, d_->e1);
   return out;

@@ -763,6 +763,11 @@ __global__ void k_functional(const PairDev* pd) {
 
 }  // namespace
 
+void PairEngine::release_buffers() {
+  if (st_) CK(cudaStreamSynchronize(st_));
+  bufs_.reset(new PairBuffers);
+}
+
 void PairEngine::set_shard(std::shared_ptr<Comm> comm, const std::vector<int>& owner) {
   comm_ = std::move(comm);
   owner_ = owner;

@@ -24,6 +24,9 @@ class PairEngine {
   /// Pairs are owned by the rank of their lower substructure; the selected
   /// constraints are exchanged so that every rank ends with the same set.
   void set_shard(std::shared_ptr<Comm> comm, const std::vector<int>& owner);
+  /// Frees the pair-stage arenas (large runs: the memory goes to the
+  /// preconditioner's fronts and root; the next enrich reallocates).
+  void release_buffers();
   void attach(const Model& m, const double* S, const std::vector<long long>& s_off,
               const std::vector<int>& PB, const std::vector<int>& nB, cudaStream_t st);
   /// Host-side preparation (pair index spaces, kernel bases, rigid modes); no
