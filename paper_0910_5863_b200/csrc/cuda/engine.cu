@@ -592,6 +592,38 @@ __global__ void __launch_bounds__(256) k_root_gemv(int NR, const double* __restr
   }
 }
 
+// Small roots: every CTA gathers the whole root right-hand side (deterministic
+// CSR sums, as k_root_gather) into shared memory, then applies -R^{-1}.
+__global__ void __launch_bounds__(256) k_root_gather_gemv(int n_root, int NR, const int* __restrict__ ptr,
+                                                          const long long* __restrict__ src,
+                                                          const double* __restrict__ fv, const double* __restrict__ T,
+                                                          double* __restrict__ x, const int* done) {
+  if (done && *done) return;
+  extern __shared__ double bs[];
+  for (int k = threadIdx.x; k < NR; k += blockDim.x) {
+    double s = 0.0;
+    if (k < n_root)
+      for (int t = ptr[k]; t < ptr[k + 1]; ++t) s += fv[src[t]];
+    bs[k] = s;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < NR; c += warps) {
+    const double* col = T + (size_t)c * NR;
+    double s0 = 0.0, s1 = 0.0;
+    int r = lane;
+    for (; r + 32 < NR; r += 64) {
+      s0 += col[r] * bs[r];
+      s1 += col[r + 32] * bs[r + 32];
+    }
+    if (r < NR) s0 += col[r] * bs[r];
+    double s = s0 + s1;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) x[c] = -s;
+  }
+}
+
 __global__ void k_extract_boundary(const SubDesc* sd, const double* MV, const long long* mvoff, const int* PI) {
   const SubDesc d = sd[blockIdx.x];
   for (int b = threadIdx.x; b < d.nB; b += blockDim.x) d.WB[b] = MV[mvoff[blockIdx.x] + PI[blockIdx.x] + b];
@@ -1458,7 +1490,7 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     if (prof) prof->mark(s);
   };
   if (ns) k_restrict<<<ns, 256, smem_b, st>>>(D.subdesc.p, D.xf, r, done);
-  count_launch(4);
+  count_launch(3);  // restrict, prolong, copy sum
   mark("restrict");
   if (D.leaf_explicit && ns) {
     k_leaf_fwd_explicit<<<dim3((D.max_NF + 7) / 8, ns), 256, D.max_PE * sizeof(double), st>>>(D.leafx.p, done);
@@ -1467,8 +1499,18 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     front_forward(D.fsolve_fwd.p, ns, D.max_NF, st, done);
   }
   mark("leaf_fwd");
+  const double* fvsrc = D.leaf_explicit ? D.FV2.p : D.FV.p;
+  if (D.root_inv && !D.comm && D.NR <= 1024) {
+    // small root, one GPU: gather and apply in one launch
+    k_root_gather_gemv<<<(D.NR + 7) / 8, 256, D.NR * sizeof(double), st>>>(D.n_root, D.NR, D.root_ptr.p,
+                                                                         D.root_src.p, fvsrc, D.Rinv.p,
+                                                                         D.xroot2.p, done);
+    count_launch(1);
+    mark("root_gemv");
+  } else {
   k_root_gather<<<std::max(1, std::min(1024, (D.NR + 255) / 256)), 256, 0, st>>>(
-      D.n_root, D.NR, D.root_ptr.p, D.root_src.p, D.leaf_explicit ? D.FV2.p : D.FV.p, D.xroot.p, done);
+      D.n_root, D.NR, D.root_ptr.p, D.root_src.p, fvsrc, D.xroot.p, done);
+  count_launch(1);
   if (D.comm) D.comm->allreduce(D.xroot.p, D.NR, st);  // root right-hand side of every rank
   mark("root_gather");
   if (D.root_inv) {
@@ -1480,6 +1522,7 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     mark("root_fwd");
     front_backward(D.rsolve.p, 1, D.NR, st, done);
     mark("root_bwd");
+  }
   }
   if (D.leaf_explicit && ns) {
     k_leaf_bwd_explicit<<<dim3(D.max_NF / kTile, ns), 256, D.max_M * sizeof(double), st>>>(
