@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(256) k_big_backward(const SolveDesc* ds, doubl
   const int G = gridDim.x, me = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt = d.n / kTile, nb = d.p / kTile;
   extern __shared__ double xs[];
-  __shared__ double part[64], tv[64];
+  __shared__ double part[64], tv[64], red4[4][64];
   for (int t = me; t < nt; t += G)
     for (int r = tid; r < 64; r += 256) {
       const int row = t * 64 + r;
@@ -725,12 +725,21 @@ __global__ void __launch_bounds__(256) k_big_backward(const SolveDesc* ds, doubl
     grid.sync();
     if (kb % G == me) {
       double* xb = xs + (kb / G) * 64;
-      if (tid < 64) {
-        const double* ps = pbuf + (size_t)(kb & 1) * G * 64 + tid;
-        double sum = 0.0;
-        for (int g = 0; g < G; ++g) sum += ps[(size_t)g * 64];
-        tv[tid] = xb[tid] - sum;
+      {
+        // sum of the CTAs' partials: four fixed-order strands, then combined
+        const int c = tid & 63, q = tid >> 6;
+        const double* ps = pbuf + (size_t)(kb & 1) * G * 64 + c;
+        double s0 = 0.0, s1 = 0.0;
+        int g = q;
+        for (; g + 4 < G; g += 8) {
+          s0 += ps[(size_t)g * 64];
+          s1 += ps[(size_t)(g + 4) * 64];
+        }
+        if (g < G) s0 += ps[(size_t)g * 64];
+        red4[q][c] = s0 + s1;
       }
+      __syncthreads();
+      if (tid < 64) tv[tid] = xb[tid] - ((red4[0][tid] + red4[1][tid]) + (red4[2][tid] + red4[3][tid]));
       __syncthreads();
       const int row = tid >> 2, prt = tid & 3;
       const double* dv = d.dinv + (size_t)kb * 64 * 64 + (size_t)row * 64;
