@@ -20,23 +20,31 @@ template <class T>
 struct DBuf {
   T* p = nullptr;
   std::size_t n = 0, cap = 0;
+  bool owned = true;  // false: a view into another allocation (a stage arena region)
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
     p = nullptr;
     n = cap = 0;
+    owned = true;
   }
   void alloc(std::size_t k) {
     if (k > cap) {
-      if (p) CK(cudaFree(p));
-      p = nullptr;
+      release();
       CK(cudaMalloc(&p, k * sizeof(T)));
       cap = k;
     }
     n = k;
+  }
+  /// Use [ptr, ptr + k) of an allocation owned elsewhere.
+  void view(T* ptr, std::size_t k) {
+    release();
+    p = ptr;
+    n = cap = k;
+    owned = false;
   }
   void upload(const std::vector<T>& v, cudaStream_t s) {
     alloc(v.empty() ? 1 : v.size());
@@ -44,6 +52,58 @@ struct DBuf {
   }
   void zero(cudaStream_t s) {
     if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+/// Grow-only device arena shared by the two scratch-heavy stages of a setup:
+/// the pair stage (face eigenproblems) and the preconditioner (transform
+/// scratch, transformed leaf fronts, primal tree, root).  The preconditioner
+/// region starts at 0; the pair region follows it when the device holds both,
+/// else it overlays it (the pair stage then clobbers the preconditioner, which
+/// the next set_constraints rebuilds).  No cudaMalloc/cudaFree in steady state.
+class StageArena {
+ public:
+  /// Base of a region of n doubles.  *clobbers_prec: the region overlays the
+  /// preconditioner's (or the arena moved), so its contents are lost.
+  double* region(bool pair, std::size_t n, bool* clobbers_prec) {
+    *clobbers_prec = false;
+    std::size_t& mine = pair ? pair_ : prec_;
+    if (n > mine) mine = n;
+    std::size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 0;
+    const double room = double(buf_.cap) * sizeof(double) + double(fr) - 1.5e9;
+    const bool split = double(prec_ + pair_) * sizeof(double) <= room;
+    const std::size_t total = split ? prec_ + pair_ : (prec_ > pair_ ? prec_ : pair_);
+    if (total > buf_.cap) {
+      buf_.release();
+      buf_.alloc(total);
+      *clobbers_prec = true;
+    }
+    if (pair && !split) *clobbers_prec = true;
+    return buf_.p + (pair && split ? prec_ : 0);
+  }
+  std::size_t capacity() const { return buf_.cap; }
+
+ private:
+  DBuf<double> buf_;
+  std::size_t prec_ = 0, pair_ = 0;  // largest request of each region so far
+};
+
+/// Consecutive views into one region (256-byte aligned parts).
+struct RegionPlan {
+  std::vector<std::pair<DBuf<double>*, std::size_t>> parts;
+  void add(DBuf<double>& b, std::size_t n) { parts.emplace_back(&b, n < 1 ? 1 : n); }
+  std::size_t total() const {
+    std::size_t t = 0;
+    for (const auto& q : parts) t += (q.second + 31) / 32 * 32;
+    return t;
+  }
+  void place(double* base) const {
+    std::size_t off = 0;
+    for (const auto& q : parts) {
+      q.first->view(base + off, q.second);
+      off += (q.second + 31) / 32 * 32;
+    }
   }
 };
 

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "devbuf.cuh"
+#include "../host/coarse_tree.hpp"
 #include "pairs.cuh"
 
 namespace b200 {
@@ -26,6 +27,7 @@ namespace {
 
 constexpr int kRed = 256;  // blocks of the deterministic dot-product reductions
 constexpr int kRootInverseMax = 12288;  // explicit root inverse up to this padded size (2.4 GB front)
+constexpr int kTreeApplies = 60;      // preconditioner applies assumed when choosing the primal tree depth
 
 inline int rup(int v, int m) { return (v + m - 1) / m * m; }
 
@@ -523,51 +525,70 @@ __global__ void __launch_bounds__(256) k_leaf_bwd_explicit(const LeafX* ds, cons
     d.FV[i] = d.FV2[i] + ((part[0][threadIdx.x] + part[1][threadIdx.x]) + (part[2][threadIdx.x] + part[3][threadIdx.x]));
 }
 
-struct RootAsm {
-  const int* ptr;          // root dof -> [ptr, ptr+1) entries
-  const int* sub;          // subdomain of the entry (ascending)
-  const int* cidx;         // coarse index within that leaf
-  const long long* foff;   // per subdomain: F arena offset
-  const int* NF;
-  const int* PE;
+// A child of a coarse front: its Schur complement onto its coarse slots is the
+// lower triangle of the trailing block, a[(p + lo) ld + p + hi], hi >= lo.
+struct AsmChild {
+  const double* a;
+  int ld;
+  int p;
 };
 
-// Root front R (NR x NR, leading dimension ld).  With ld == 2 NR the front is
-// augmented as [[R, .], [I, 0]]: eliminating R leaves -R^{-1} in the trailing block.
-__global__ void k_root_assemble(int n_root, int NR, long ld, RootAsm ra, const double* Farena, double* R,
-                                bool identity) {
-  const long total = (long)n_root * (n_root + 1) / 2;
+// A coarse front (a box of the primal tree, or the root): logical slots are the
+// rows [0, ne) (eliminated here) and [PE, PE + nc) (passed up); rows are padded
+// to NF.  Entry lists of row r: [ptr[pos0 + r], ptr[pos0 + r + 1]), ascending by child.
+struct AsmFront {
+  double* out;
+  long ld;  // NF, or 2 NF for the augmented root [[R, .], [I, 0]]
+  int ne, nc, PE, NF;
+  long long pos0;
+};
+
+// Extend-add of the children's Schur complements into the lower triangle of
+// each front (the reference's sparse assembly of the stabilized operator,
+// bddc_operator.cpp:7-36, restricted to the primal unknowns):
+// one thread per entry, the two rows' entry lists merged by child in a fixed
+// order (deterministic, no atomics).
+__global__ void k_front_assemble(const AsmFront* fr, const int* __restrict__ ptr, const int* __restrict__ child,
+                                 const int* __restrict__ cidx, const AsmChild* __restrict__ kids) {
+  const AsmFront f = fr[blockIdx.y];
+  const int n = f.ne + f.nc;
+  const long total = (long)n * (n + 1) / 2;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
-    int k1 = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while ((long)k1 * (k1 + 1) / 2 > t) --k1;
-    while ((long)(k1 + 1) * (k1 + 2) / 2 <= t) ++k1;
-    const int k2 = static_cast<int>(t - (long)k1 * (k1 + 1) / 2);
+    int i1 = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((long)i1 * (i1 + 1) / 2 > t) --i1;
+    while ((long)(i1 + 1) * (i1 + 2) / 2 <= t) ++i1;
+    const int i2 = static_cast<int>(t - (long)i1 * (i1 + 1) / 2);
+    const int r1 = i1 < f.ne ? i1 : f.PE + i1 - f.ne, r2 = i2 < f.ne ? i2 : f.PE + i2 - f.ne;
     double s = 0.0;
-    int a = ra.ptr[k1], b = ra.ptr[k2];
-    const int ae = ra.ptr[k1 + 1], be = ra.ptr[k2 + 1];
+    int a = ptr[f.pos0 + r1], b = ptr[f.pos0 + r2];
+    const int ae = ptr[f.pos0 + r1 + 1], be = ptr[f.pos0 + r2 + 1];
     while (a < ae && b < be) {
-      const int sa = ra.sub[a], sb = ra.sub[b];
-      if (sa < sb) {
+      const int ca = child[a], cb = child[b];
+      if (ca < cb) {
         ++a;
-      } else if (sb < sa) {
+      } else if (cb < ca) {
         ++b;
       } else {
-        const int c1 = ra.cidx[a], c2 = ra.cidx[b];
+        const int c1 = cidx[a], c2 = cidx[b];
         const int hi = c1 >= c2 ? c1 : c2, lo = c1 >= c2 ? c2 : c1;
-        const int NF = ra.NF[sa], PE = ra.PE[sa];
-        s += Farena[ra.foff[sa] + (size_t)(PE + lo) * NF + PE + hi];
+        const AsmChild k = kids[ca];
+        s += k.a[(size_t)(k.p + lo) * k.ld + k.p + hi];
         ++a;
         ++b;
       }
     }
-    R[(size_t)k2 * ld + k1] = s;
+    f.out[(size_t)r2 * f.ld + r1] = s;
   }
-  if (!identity) return;
-  for (long q = n_root + blockIdx.x * (long)blockDim.x + threadIdx.x; q < NR; q += (long)gridDim.x * blockDim.x)
-    R[(size_t)q * ld + q] = 1.0;
-  if (ld > NR)
-    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < NR; q += (long)gridDim.x * blockDim.x)
-      R[(size_t)q * ld + NR + q] = 1.0;
+}
+
+// Identity on the padding rows; with ld > NF also the augmented identity block
+// (eliminating R then leaves -R^{-1} in the trailing block).
+__global__ void k_front_pads(const AsmFront* fr) {
+  const AsmFront f = fr[blockIdx.y];
+  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < f.NF; q += (long)gridDim.x * blockDim.x) {
+    if ((q >= f.ne && q < f.PE) || q >= f.PE + f.nc) f.out[(size_t)q * f.ld + q] = 1.0;
+    if (f.ld > f.NF) f.out[(size_t)q * f.ld + f.NF + q] = 1.0;
+  }
 }
 
 // x = -T b with T = -R^{-1} (full symmetric, NR x NR): one warp per output, reading
@@ -691,7 +712,8 @@ struct DeviceState {
   bool leaf_explicit = false;  // explicit leaf mode (k_leaf_*_explicit)
   std::vector<int> NA;         // F leading dimension (NF, or NF + PE augmented)
   int max_NA = 0, max_MA = 0;
-  DBuf<double> F, DinvF, FV, FV2, Xtmp, E;
+  DBuf<double> F, DinvF, FV, FV2, Xtmp, E;  // F, DinvF, E, Xtmp: views into `stage`
+  StageArena stage;
   DBuf<LeafX> leafx;
   DBuf<long long> d_xoff;
   DBuf<int> finfo;
@@ -704,15 +726,35 @@ struct DeviceState {
   int max_rows = 0;  // most constrained transform rows of one subdomain (prolong smem)
   DBuf<double> trD;
   XformDesc xf{};
-  // root
-  int n_root = 0, NR = 0;
+  // root: the top front of the primal tree (all primal unknowns when the tree
+  // has depth 0)
+  int n_root = 0, NR = 0, n_primal = 0;
   DBuf<double> R, DinvR, xroot, xroot2, Rinv;
   bool root_inv = false;
   DBuf<TrailDesc> rtrail;
-  DBuf<int> rinfo, root_ptr, root_sub, root_c, d_NF, d_PE, pads, pad_sub;
+  DBuf<int> rinfo, root_ptr, root_child, root_c, d_NF, d_PE, pads, pad_sub;
   DBuf<long long> root_src, d_foff;
+  DBuf<AsmChild> root_kids;
+  DBuf<AsmFront> root_afront;
   DBuf<FrontDesc> rfront;
   DBuf<SolveDesc> rsolve;
+  // primal tree levels below the root (coarse_tree.hpp), deepest first
+  struct TreeLevel {
+    DBuf<double> A, Dinv, V;  // fronts, diagonal-tile inverses, vectors
+    DBuf<FrontDesc> fronts;
+    DBuf<SolveDesc> fwd, bwd;
+    DBuf<AsmFront> afronts;
+    DBuf<AsmChild> kids;
+    DBuf<int> info, ptr, child, cidx, cmap;
+    DBuf<long long> src;
+    int nfr = 0, max_NF = 0, max_PE = 0, max_M = 0, max_slots = 0;
+    long long arena = 0;
+    std::vector<int> NF, PE, nown, nupd;
+  };
+  std::vector<std::unique_ptr<TreeLevel>> tree;
+  int tree_depth = 0;
+  double tree_apply_bytes = 0, tree_factor_bytes = 0;
+  double* leaf_croot = nullptr;  // where the leaves' backward sweeps read their coarse values
   // pcg
   DBuf<double> vx, vr, vz, vp, vq, vb, part_a, part_b, alphas, betas;
   DBuf<PcgState> pst;
@@ -749,6 +791,7 @@ Engine::Engine(const Model& m) : m_(m), d_(new DeviceState) {
 
 Engine::~Engine() = default;
 
+
 void Engine::set_shard(std::shared_ptr<Comm> comm, const std::vector<int>& owner) {
   DeviceState& D = *d_;
   if (D.prepared) throw Error(kError, "set_shard must precede any device work");
@@ -767,11 +810,19 @@ int Engine::root_size() const { return d_->n_root; }
 
 namespace {
 // device memory is tight (large runs): stage arenas are released after use
-bool memory_tight() {
+double free_bytes() {
   size_t fr = 0, tot = 0;
-  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || tot == 0) return false;
-  return double(fr) < 0.35 * double(tot);
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 0.0;
+  return double(fr);
 }
+
+// bytes a grow-only buffer needs beyond its current capacity
+template <class T>
+double growth(const DBuf<T>& b, long long n) {
+  return n > (long long)b.cap ? double(n - (long long)b.cap) * sizeof(T) : 0.0;
+}
+
+constexpr double kMemMargin = 1.5e9;  // headroom kept free for small buffers and the runtime
 
 double elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
@@ -956,6 +1007,12 @@ void Engine::prepare() {
   up(D.d_mvoff, mvo_own);
   up(D.d_PI, pi_own);
   D.pairs.attach(m, D.S.p, D.s_off, D.PB, D.nB, st);
+  D.pairs.set_region([this](std::size_t n) {
+    bool lost = false;
+    double* base = d_->stage.region(true, n, &lost);
+    if (lost) invalidate_preconditioner();
+    return base;
+  });
   if (D.comm) D.pairs.set_shard(D.comm, D.owner);
   D.prepared = true;
   upload_inputs();
@@ -1056,6 +1113,7 @@ double Engine::pcg_bytes_per_iteration() const {
       b += (D.leaf_explicit ? e * (e + c) + e * c : 2.0 * (e * (e + 1) / 2 + e * c)) * 8.0;
     }
   b += double(D.n_root) * D.n_root * 8.0;  // R^{-1} GEMV, or both triangular root sweeps
+  b += D.tree_apply_bytes;                  // both sweeps of every primal tree front
   return b;
 }
 
@@ -1067,7 +1125,7 @@ double Engine::leaf_front_bytes() const {
       const double e = D.nE[s], c = D.nC[s];
       b += (D.leaf_explicit ? e * e + c * e : e * (e + 1) / 2 + c * e) * 8.0;
     }
-  b += double(D.n_root) * (D.n_root + 1) / 2 * 8.0;
+  b += double(D.n_root) * (D.n_root + 1) / 2 * 8.0 + D.tree_factor_bytes;
   return b;
 }
 
@@ -1199,8 +1257,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       coarse_b[s].push_back(bpos_of[s][cov.group_local[g][t]]);
       coarse_root[s].push_back(static_cast<int>(ncd + g));
     }
-  D.n_root = static_cast<int>(ncd + cov.groups.size());
-  D.NR = rup(std::max(D.n_root, 1), kTile);
+  D.n_primal = static_cast<int>(ncd + cov.groups.size());
   ht.mark("coarse");
   // F layout
   D.NF.assign(ns, 0);
@@ -1224,7 +1281,6 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     const std::string mode = env ? env : "";
     D.leaf_explicit = mode == "explicit" || (mode != "factor" && no < sm_count());
   }
-  std::vector<int> root_cnt(D.n_root + 1, 0);
   for (int s : D.own) {
     const int nB = D.nB[s], nC = static_cast<int>(coarse_b[s].size()), nE = nB - nC;
     D.nE[s] = nE;
@@ -1263,25 +1319,66 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       pads.push_back(q);
       pad_sub.push_back(s);
     }
-    for (int c = 0; c < nC; ++c) ++root_cnt[coarse_root[s][c] + 1];
   }
   pad_off[ns] = pads.size();
   ht.mark("f_layout");
-  // root CSR (entries ascending by subdomain)
-  std::vector<int> rptr(D.n_root + 1, 0);
-  for (int k = 0; k < D.n_root; ++k) rptr[k + 1] = rptr[k] + root_cnt[k + 1];
-  std::vector<int> rsub(rptr.back()), rc(rptr.back());
-  std::vector<long long> rsrc(rptr.back());
+  // primal tree over the substructure lattice (coarse_tree.hpp); its top front
+  // is the root.  Depth 0 = one dense root over all primal unknowns (always
+  // when sharded: the root is then gathered over the ranks).
+  CoarseTree plan;
   {
-    std::vector<int> fill(rptr.begin(), rptr.end() - 1);
-    for (int s : D.own)
-      for (int c = 0; c < D.nC[s]; ++c) {
-        const int k = coarse_root[s][c];
-        rsub[fill[k]] = s;
-        rc[fill[k]] = c;
-        rsrc[fill[k]] = D.fv_off[s] + D.PE[s] + c;
-        ++fill[k];
+    std::vector<CoarseLeaf> leaves(no);
+    for (int q = 0; q < no; ++q) {
+      const int s = D.own[q];
+      leaves[q].coarse = coarse_root[s];
+      for (int a = 0; a < 3; ++a) leaves[q].coord[a] = m.subs[s].origin[a] / m.mesh.epe;
+      leaves[q].src0 = D.fv_off[s] + D.PE[s];
+    }
+    int depth = 0;
+    if (!D.comm) {
+      const int maxd = coarse_tree_max_depth(m.mesh.sub);
+      const char* env = std::getenv("BDDC_B200_ROOT_DEPTH");
+      if (env && *env) {
+        depth = std::max(0, std::min(std::atoi(env), maxd));
+      } else {
+        double best = 0;
+        for (int d = 0; d <= maxd; ++d) {
+          const CoarseTree t = plan_coarse_tree(leaves, m.mesh.sub, D.n_primal, d, kRootInverseMax, true);
+          const double c = coarse_tree_cost(t, kTreeApplies, kRootInverseMax);
+          if (d == 0 || c < best) {
+            best = c;
+            depth = d;
+          }
+        }
       }
+    }
+    plan = plan_coarse_tree(leaves, m.mesh.sub, D.n_primal, depth, kRootInverseMax);
+    for (int q = 0; q < no; ++q) {
+      const int s = D.own[q];
+      for (int c = 0; c < D.nC[s]; ++c) cmap[cmap_off[s] + c] = plan.leaf_cmap[q][c];
+    }
+  }
+  D.tree_depth = plan.depth;
+  if (const char* e = std::getenv("BDDC_B200_PROFILE"); e && *e && *e != '0') {
+    std::string line = "[profile] primal tree: " + std::to_string(D.n_primal) + " unknowns, depth " +
+                       std::to_string(plan.depth);
+    for (const auto& L : plan.levels) {
+      long long own = 0;
+      for (const auto& f : L.fronts) own += static_cast<long long>(f.own.size());
+      line += ", " + std::to_string(L.fronts.size()) + " fronts (" + std::to_string(own) + " eliminated, max " +
+              std::to_string(L.max_NF) + " rows)";
+    }
+    line += ", top " + std::to_string(plan.top.size()) + ", est " + std::to_string(plan.flops / 1e9) + " GF";
+    std::fprintf(stderr, "%s\n", line.c_str());
+  }
+  D.n_root = static_cast<int>(plan.top.size());
+  D.NR = rup(std::max(D.n_root, 1), kTile);
+  // root front; up to kRootInverseMax rows it is augmented to [[R, .], [I, 0]] so
+  // that the factorization leaves -R^{-1} and every apply is one parallel GEMV
+  {
+    const char* env = std::getenv("BDDC_B200_ROOT");  // inverse | sweep (testing override)
+    const std::string mode = env ? env : "";
+    D.root_inv = mode == "inverse" || (mode != "sweep" && D.NR <= kRootInverseMax);
   }
   ht.mark("index_build");
   // uploads
@@ -1310,17 +1407,45 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   D.xf = XformDesc{D.inst_tr.p, D.inst_pos.p, D.tpos.p, D.tr_n.p, D.tr_r.p, D.tr_off_perm.p, D.tr_off_d.p,
                    D.perm.p, D.iperm.p, D.trD.p, D.cpos.p, D.item_ptr.p, D.item_inst.p, D.item_row.p,
                    D.inst_loff.p};
-  D.F.alloc(std::max<long long>(fo, 1));
+  // Preconditioner arenas: views into the stage arena (shared with the pair
+  // stage).  [F | DinvF | E | Xtmp], with the root and the primal tree over the
+  // transform scratch Xtmp (dead once F is formed).
+  D.tree.resize(plan.levels.size());
+  for (auto& T : D.tree)
+    if (!T) T.reset(new DeviceState::TreeLevel);
+  {
+    const long long ldR0 = D.root_inv ? 2LL * D.NR : D.NR;
+    RegionPlan lead, scratch, late;
+    lead.add(D.F, fo);
+    lead.add(D.DinvF, dfo);
+    if (D.leaf_explicit) lead.add(D.E, eo);
+    scratch.add(D.Xtmp, xo);
+    late.add(D.R, ldR0 * ldR0);
+    late.add(D.DinvR, (long long)D.NR * kTile);
+    if (D.root_inv) late.add(D.Rinv, (long long)D.NR * D.NR);
+    for (std::size_t l = 0; l < plan.levels.size(); ++l) {
+      late.add(D.tree[l]->A, plan.levels[l].a_size);
+      late.add(D.tree[l]->Dinv, plan.levels[l].d_size);
+    }
+    const std::size_t total = lead.total() + std::max(scratch.total(), late.total());
+    const double room = double(D.stage.capacity()) * 8.0 + free_bytes();
+    if (double(total) * 8.0 > room)
+      throw Error(kError, "preconditioner needs " + std::to_string(total * 8.0 / 1e9) + " GB (root " +
+                              std::to_string(D.n_root) + " primal unknowns); " + std::to_string(room / 1e9) +
+                              " GB available");
+    bool lost = false;
+    double* base = D.stage.region(false, total, &lost);
+    lead.place(base);
+    scratch.place(base + lead.total());
+    late.place(base + lead.total());
+  }
   D.F.zero(st);
-  D.DinvF.alloc(std::max<long long>(dfo, 1));
   D.FV.alloc(std::max<long long>(fvo, 1));
   D.FV.zero(st);
   if (D.leaf_explicit) {
     D.FV2.alloc(std::max<long long>(fvo, 1));
     D.FV2.zero(st);
-    D.E.alloc(std::max<long long>(eo, 1));
   }
-  D.Xtmp.alloc(std::max<long long>(xo, 1));
   if (xoff.empty()) D.d_xoff.alloc(1); else D.d_xoff.upload(xoff, st);
   D.finfo.alloc(std::max(no, 1));
   D.finfo.zero(st);
@@ -1343,36 +1468,103 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   up_v(D.subdesc, sd);
   up_v(D.ffront, fd);
   up_v(D.fsolve_fwd, fw);
-  // root front; up to kRootInverseMax rows it is augmented to [[R, .], [I, 0]] so
-  // that the factorization leaves -R^{-1} and every apply is one parallel GEMV
-  {
-    const char* env = std::getenv("BDDC_B200_ROOT");  // inverse | sweep (testing override)
-    const std::string mode = env ? env : "";
-    D.root_inv = mode == "inverse" || (mode != "sweep" && D.NR <= kRootInverseMax);
+  // primal tree levels (deepest first): fronts, vectors, gathers, backward maps
+  D.tree_apply_bytes = D.tree_factor_bytes = 0;
+  for (std::size_t l = 0; l < plan.levels.size(); ++l) {
+    DeviceState::TreeLevel& T = *D.tree[l];
+    const CoarseTree::Level& P = plan.levels[l];
+    T.nfr = static_cast<int>(P.fronts.size());
+    T.max_NF = P.max_NF;
+    T.max_PE = P.max_PE;
+    T.max_M = P.max_M;
+    T.arena = P.arena;
+    T.V.alloc(std::max<long long>(P.arena, 1));
+    T.info.alloc(T.nfr);
+    T.info.zero(st);
+    up_i(T.ptr, P.ptr);
+    up_i(T.child, P.child);
+    up_i(T.cidx, P.cidx);
+    up_i(T.cmap, P.cmap);
+    if (P.src.empty()) T.src.alloc(1); else T.src.upload(P.src, st);
+    T.NF.assign(T.nfr, 0);
+    T.PE.assign(T.nfr, 0);
+    T.nown.assign(T.nfr, 0);
+    T.nupd.assign(T.nfr, 0);
+    T.max_slots = 0;
+    for (int f = 0; f < T.nfr; ++f) {
+      const CoarseTree::Front& F = P.fronts[f];
+      T.NF[f] = F.NF;
+      T.PE[f] = F.PE;
+      T.nown[f] = static_cast<int>(F.own.size());
+      T.nupd[f] = static_cast<int>(F.upd.size());
+      T.max_slots = std::max(T.max_slots, T.nown[f] + T.nupd[f]);
+      const double e = T.nown[f], c = T.nupd[f];
+      D.tree_apply_bytes += 2.0 * (e * (e + 1) / 2 + e * c) * 8.0;
+      D.tree_factor_bytes += (e * (e + 1) / 2 + e * c) * 8.0;
+    }
   }
   // Larger roots are factored in place and solved by triangular sweeps (over
-  // the whole GPU for the largest ones).  The dense root must fit in memory.
+  // the whole GPU for the largest ones).
   const long ldR = D.root_inv ? 2L * D.NR : D.NR;
-  {
-    size_t fr = 0, tot = 0;
-    CK(cudaMemGetInfo(&fr, &tot));
-    const double need = double(ldR) * ldR * 8.0;  // the current root arena is freed before growing
-    if (need > double(fr) + double(D.R.cap) * 8.0)
-      throw Error(kError, "dense root of " + std::to_string(D.n_root) + " primal unknowns needs " +
-                              std::to_string(need / 1e9) + " GB; " + std::to_string(fr / 1e9) + " GB free");
-  }
-  D.R.alloc((size_t)ldR * ldR);
-  D.R.zero(st);
-  D.DinvR.alloc((size_t)D.NR * kTile);
   D.xroot.alloc(D.NR);
   D.xroot2.alloc(D.NR);
-  if (D.root_inv) D.Rinv.alloc((size_t)D.NR * D.NR);
   D.rinfo.alloc(1);
   D.rinfo.zero(st);
+  double* const top_x = D.root_inv ? D.xroot2.p : D.xroot.p;  // the root's solution
+  for (std::size_t l = 0; l < plan.levels.size(); ++l) {
+    DeviceState::TreeLevel& T = *D.tree[l];
+    const CoarseTree::Level& P = plan.levels[l];
+    double* const up = l + 1 < plan.levels.size() ? D.tree[l + 1]->V.p : top_x;
+    std::vector<FrontDesc> fdl(T.nfr);
+    std::vector<SolveDesc> fwl(T.nfr), bwl(T.nfr);
+    std::vector<AsmFront> afl(T.nfr);
+    for (int f = 0; f < T.nfr; ++f) {
+      const CoarseTree::Front& F = P.fronts[f];
+      fdl[f] = FrontDesc{T.A.p + F.a_off, T.Dinv.p + F.d_off, F.NF, F.PE, T.info.p + f, 0};
+      fwl[f] = SolveDesc{T.A.p + F.a_off, T.Dinv.p + F.d_off, T.V.p + F.fv_off, F.NF, F.PE, nullptr, nullptr};
+      bwl[f] = fwl[f];
+      bwl[f].cmap = T.cmap.p + F.cmap_off;
+      bwl[f].croot = up;
+      afl[f] = AsmFront{T.A.p + F.a_off, F.NF, T.nown[f], T.nupd[f], F.PE, F.NF, F.fv_off};
+    }
+    up_v(T.fronts, fdl);
+    up_v(T.fwd, fwl);
+    up_v(T.bwd, bwl);
+    up_v(T.afronts, afl);
+    std::vector<AsmChild> kids;
+    if (l == 0) {
+      for (int q = 0; q < no; ++q) {
+        const int s = D.own[q];
+        kids.push_back(AsmChild{D.F.p + D.f_off[s], D.NA[s], D.PE[s]});
+      }
+    } else {
+      const DeviceState::TreeLevel& C = *D.tree[l - 1];
+      for (const CoarseTree::Front& F : plan.levels[l - 1].fronts)
+        kids.push_back(AsmChild{C.A.p + F.a_off, F.NF, F.PE});
+    }
+    up_v(T.kids, kids);
+  }
+  {
+    std::vector<AsmChild> kids;
+    if (plan.levels.empty()) {
+      for (int q = 0; q < no; ++q) {
+        const int s = D.own[q];
+        kids.push_back(AsmChild{D.F.p + D.f_off[s], D.NA[s], D.PE[s]});
+      }
+    } else {
+      const DeviceState::TreeLevel& C = *D.tree.back();
+      for (const CoarseTree::Front& F : plan.levels.back().fronts)
+        kids.push_back(AsmChild{C.A.p + F.a_off, F.NF, F.PE});
+    }
+    up_v(D.root_kids, kids);
+    std::vector<AsmFront> af{AsmFront{D.R.p, ldR, D.n_root, 0, D.NR, D.NR, 0}};
+    up_v(D.root_afront, af);
+  }
+  D.leaf_croot = plan.levels.empty() ? top_x : D.tree[0]->V.p;
   for (int q = 0; q < no; ++q) {
     bw[q] = fw[q];
     bw[q].cmap = D.cmap.p + cmap_off[D.own[q]];
-    bw[q].croot = D.root_inv ? D.xroot2.p : D.xroot.p;
+    bw[q].croot = D.leaf_croot;
   }
   up_v(D.fsolve_bwd, bw);
   if (D.leaf_explicit) {
@@ -1384,10 +1576,10 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     }
     up_v(D.leafx, lx);
   }
-  up_i(D.root_ptr, rptr);
-  up_i(D.root_sub, rsub);
-  up_i(D.root_c, rc);
-  if (rsrc.empty()) D.root_src.alloc(1); else D.root_src.upload(rsrc, st);
+  up_i(D.root_ptr, plan.top_ptr);
+  up_i(D.root_child, plan.top_child);
+  up_i(D.root_c, plan.top_cidx);
+  if (plan.top_src.empty()) D.root_src.alloc(1); else D.root_src.upload(plan.top_src, st);
   D.d_foff.upload(D.f_off, st);
   up_i(D.d_NF, D.NA);  // leading dimensions of the F fronts
   up_i(D.d_PE, D.PE);
@@ -1409,10 +1601,6 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     count_launch(1);
   }
   CK(cudaGetLastError());
-  if (memory_tight()) {  // the transform scratch is dead once F is formed
-    CK(cudaStreamSynchronize(st));
-    D.Xtmp.release();
-  }
   prof.mark("xform");
   partial_cholesky(D.ffront.p, no, D.max_NA, D.max_PE, D.max_MA, st);
   if (D.leaf_explicit && no) {
@@ -1421,12 +1609,33 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   }
   CK(cudaGetLastError());
   prof.mark(D.leaf_explicit ? "cholF+explicit" : "cholF");
-  RootAsm ra{D.root_ptr.p, D.root_sub.p, D.root_c.p, D.d_foff.p, D.d_NF.p, D.d_PE.p};
-  // this rank's leaf contributions (+ the identity blocks on rank 0), then the
+  // primal tree, deepest level first: extend-add of the children's Schur
+  // complements, identity pads, batched partial Cholesky
+  for (std::size_t l = 0; l < D.tree.size(); ++l) {
+    DeviceState::TreeLevel& T = *D.tree[l];
+    T.A.zero(st);
+    const long pairs = (long)T.max_slots * (T.max_slots + 1) / 2;
+    k_front_assemble<<<dim3(static_cast<unsigned>(std::min<long>(1024, (pairs + 255) / 256)), T.nfr), 256, 0, st>>>(
+        T.afronts.p, T.ptr.p, T.child.p, T.cidx.p, T.kids.p);
+    k_front_pads<<<dim3(std::max(1, std::min(64, (T.max_NF + 255) / 256)), T.nfr), 256, 0, st>>>(T.afronts.p);
+    count_launch(2);
+    partial_cholesky(T.fronts.p, T.nfr, T.max_NF, T.max_PE, T.max_M, st);
+  }
+  if (!D.tree.empty()) prof.mark("tree");
+  // this rank's contributions (+ the identity blocks on rank 0), then the
   // gather of the root front: an allreduce of its first N_R columns
   const bool identity = !D.comm || D.comm->rank() == 0;
-  k_root_assemble<<<1024, 256, 0, st>>>(D.n_root, D.NR, ldR, ra, D.F.p, D.R.p, identity);
-  count_launch(1);
+  D.R.zero(st);
+  {
+    const long pairs = (long)D.n_root * (D.n_root + 1) / 2;
+    k_front_assemble<<<static_cast<unsigned>(std::max<long>(1, std::min<long>(1024, (pairs + 255) / 256))), 256, 0,
+                       st>>>(D.root_afront.p, D.root_ptr.p, D.root_child.p, D.root_c.p, D.root_kids.p);
+    count_launch(1);
+    if (identity) {
+      k_front_pads<<<std::max(1, std::min(1024, (D.NR + 255) / 256)), 256, 0, st>>>(D.root_afront.p);
+      count_launch(1);
+    }
+  }
   if (D.comm) D.comm->allreduce(D.R.p, (size_t)ldR * D.NR, st);
   std::vector<FrontDesc> rf{FrontDesc{D.R.p, D.DinvR.p, static_cast<int>(ldR), D.NR, D.rinfo.p, D.root_inv ? D.NR : 0}};
   D.rfront.upload(rf, st);
@@ -1451,6 +1660,12 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   int rinfo = 0;
   CK(cudaMemcpy(&rinfo, D.rinfo.p, sizeof(int), cudaMemcpyDeviceToHost));
   if (rinfo) throw Error(kNotPositiveDefinite, "factorize: root front is not positive definite");
+  for (auto& T : D.tree) {
+    std::vector<int> ti(T->nfr);
+    CK(cudaMemcpy(ti.data(), T->info.p, ti.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int v : ti)
+      if (v) throw Error(kNotPositiveDefinite, "factorize: primal tree front is not positive definite");
+  }
   D.have_prec = true;
   // invalidate a captured PCG graph (pointers changed)
   if (D.gexec) {
@@ -1500,6 +1715,16 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
   }
   mark("leaf_fwd");
   const double* fvsrc = D.leaf_explicit ? D.FV2.p : D.FV.p;
+  // primal tree, deepest level first: gather the children's coarse residuals,
+  // forward sweep
+  for (auto& T : D.tree) {
+    k_root_gather<<<std::max(1, std::min<int>(1024, static_cast<int>((T->arena + 255) / 256))), 256, 0, st>>>(
+        static_cast<int>(T->arena), static_cast<int>(T->arena), T->ptr.p, T->src.p, fvsrc, T->V.p, done);
+    count_launch(1);
+    front_forward(T->fwd.p, T->nfr, T->max_NF, st, done);
+    fvsrc = T->V.p;
+  }
+  if (!D.tree.empty()) mark("tree_fwd");
   if (D.root_inv && !D.comm && D.NR <= 1024) {
     // small root, one GPU: gather and apply in one launch
     k_root_gather_gemv<<<(D.NR + 7) / 8, 256, D.NR * sizeof(double), st>>>(D.n_root, D.NR, D.root_ptr.p,
@@ -1524,9 +1749,11 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     mark("root_bwd");
   }
   }
+  for (std::size_t l = D.tree.size(); l-- > 0;) front_backward(D.tree[l]->bwd.p, D.tree[l]->nfr, D.tree[l]->max_NF, st, done);
+  if (!D.tree.empty()) mark("tree_bwd");
   if (D.leaf_explicit && ns) {
-    k_leaf_bwd_explicit<<<dim3(D.max_NF / kTile, ns), 256, D.max_M * sizeof(double), st>>>(
-        D.leafx.p, D.root_inv ? D.xroot2.p : D.xroot.p, done);
+    k_leaf_bwd_explicit<<<dim3(D.max_NF / kTile, ns), 256, D.max_M * sizeof(double), st>>>(D.leafx.p, D.leaf_croot,
+                                                                                          done);
     count_launch(1);
   } else if (!D.leaf_explicit) {
     front_backward(D.fsolve_bwd.p, ns, D.max_NF, st, done);
@@ -1802,7 +2029,6 @@ StepOut Engine::step(const StepSpec& sp, ConstraintSet& cs, double* u_free_host)
   if (adaptive) {
     CK(cudaEventRecord(D.e0, st));
     out.omega_tilde = D.pairs.enrich(cs, o, prep).omega_tilde;
-    if (memory_tight()) D.pairs.release_buffers();
     CK(cudaEventRecord(D.e1, st));
     times_.eigen = elapsed(D.e0, D.e1);
   }
@@ -1827,10 +2053,23 @@ StepOut Engine::step(const StepSpec& sp, ConstraintSet& cs, double* u_free_host)
 EnrichOutcome Engine::enrich(ConstraintSet& cs, const EnrichOptions& o) {
   CK(cudaEventRecord(d_->e0, d_->st));
   EnrichOutcome out = d_->pairs.enrich(cs, o);
-  if (memory_tight()) d_->pairs.release_buffers();
   CK(cudaEventRecord(d_->e1, d_->st));
   times_.eigen = elapsed(d_->e0, d_->e1);
   return out;
+}
+
+
+void Engine::invalidate_preconditioner() {
+  DeviceState& D = *d_;
+  D.have_prec = false;
+  if (D.gexec) {
+    cudaGraphExecDestroy(D.gexec);
+    D.gexec = nullptr;
+  }
+  if (D.graph) {
+    cudaGraphDestroy(D.graph);
+    D.graph = nullptr;
+  }
 }
 
 }  // namespace b200

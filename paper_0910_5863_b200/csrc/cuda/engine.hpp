@@ -127,6 +127,9 @@ class Engine {
   /// the leaf operators of both preconditioner sweeps and the root apply.
   double pcg_bytes_per_iteration() const;
   cudaStream_t stream() const;
+  /// The pair stage reuses the preconditioner's memory (large runs): the next
+  /// set_constraints rebuilds it.
+  void invalidate_preconditioner();
 
  private:
   const Model& m_;

@@ -1177,6 +1177,34 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
   EnrichOutcome out;
   std::vector<std::vector<double>> all_evals(np), all_funcs(np);
   std::vector<int> all_k(np);
+  // Arenas sized once for the largest chunk: views into the engine's stage
+  // arena (no allocation between chunks or steps; see StageArena).
+  {
+    HostTimer hr("enrich reserve");
+    PairBuffers& B_ = *bufs_;
+    long long hH = 0, hD = 0;
+    for (const auto& h : prep->hubs) {
+      const long long PH = rup(static_cast<int>(h.rest.size()), kTile);
+      const long long NH = PH + rup(std::max(static_cast<int>(h.U.size()), 1), kTile);
+      hH += NH * NH;
+      hD += (PH / kTile) * kTile * kTile;
+    }
+    long long mx[10] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+    for (const ChunkHost& c : prep->chunks) {
+      const long long v[10] = {c.nG, c.nQ, c.nF, c.nD, c.nM, c.nH, c.nA, c.nE, c.nW, c.nFu};
+      for (int i = 0; i < 10; ++i) mx[i] = std::max(mx[i], v[i]);
+    }
+    DBuf<double>* bufs[12] = {&B_.G, &B_.Q, &B_.F, &B_.Dv, &B_.M, &B_.H, &B_.A, &B_.E, &B_.W, &B_.Fu, &B_.Hub, &B_.DvH};
+    const long long want[12] = {mx[0], mx[1], mx[2], mx[3], mx[4], mx[5], mx[6], mx[7], mx[8], mx[9],
+                                std::max(hH, 1LL), std::max(hD, 1LL)};
+    RegionPlan rp;
+    for (int i = 0; i < 12; ++i) rp.add(*bufs[i], want[i]);
+    if (region_)
+      rp.place(region_(rp.total()));
+    else
+      for (int i = 0; i < 12; ++i) bufs[i]->alloc(want[i]);
+    hr.mark("alloc");
+  }
   // hub stage of the two-level side fronts: [rest | U] gathered from S_s, the
   // rest eliminated once per hub (Schur complement onto U in the trailing block)
   const auto& hubs = prep->hubs;
@@ -1415,12 +1443,16 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     count_launch(9);
     CK(cudaGetLastError());
     prof.mark("vectors");
+    ht.mark("launch");
     std::vector<double> ev(E.n), fu(Fu.n);
     std::vector<int> inf(4 * nb);
+    CK(cudaStreamSynchronize(st_));
+    ht.mark("device_wait");
     CK(cudaMemcpyAsync(ev.data(), E.p, E.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
     CK(cudaMemcpyAsync(fu.data(), Fu.p, Fu.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
     CK(cudaMemcpyAsync(inf.data(), info.p, 4 * nb * sizeof(int), cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
+    ht.mark("copy");
     if (chunk_id == 1 && nh) {
       std::vector<int> hinf(nh);
       CK(cudaMemcpy(hinf.data(), B_.hinfo.p, nh * sizeof(int), cudaMemcpyDeviceToHost));

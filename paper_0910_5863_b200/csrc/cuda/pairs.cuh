@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -27,6 +28,8 @@ class PairEngine {
   /// Frees the pair-stage arenas (large runs: the memory goes to the
   /// preconditioner's fronts and root; the next enrich reallocates).
   void release_buffers();
+  /// Provider of the pair stage's device region (the engine's stage arena).
+  void set_region(std::function<double*(std::size_t)> f) { region_ = std::move(f); }
   void attach(const Model& m, const double* S, const std::vector<long long>& s_off,
               const std::vector<int>& PB, const std::vector<int>& nB, cudaStream_t st);
   /// Host-side preparation (pair index spaces, kernel bases, rigid modes); no
@@ -41,6 +44,7 @@ class PairEngine {
   std::vector<int> PB_, nB_;
   cudaStream_t st_ = nullptr;
   std::unique_ptr<PairBuffers> bufs_;
+  std::function<double*(std::size_t)> region_;
   std::shared_ptr<Comm> comm_;
   std::vector<int> owner_;
 };

@@ -230,3 +230,56 @@ def test_side_front_elimination_levels(gtree, monkeypatch):
         big = e0 > 1e-6 * max(e0.max(), 1e-300)
         assert np.all(np.abs(rep["eigenvalues"][big] - e0[big]) <= 1e-6 * e0[big])
     assert abs(row.iterations - ref.iterations) <= 1
+
+
+TREE = [("cfg1", baseline_config(1).spec, lambda: pb.BDDC(config=1), "c+e+f", 1),
+        ("sc444h3 c+e+f", cube_spec((4, 4, 4), 3, fem.SCALAR),
+         lambda: pb.BDDC(pb.Problem.cube((4, 4, 4), 3, "scalar")), "c+e+f", 1),
+        ("sc444h3 c+e+f d2", cube_spec((4, 4, 4), 3, fem.SCALAR),
+         lambda: pb.BDDC(pb.Problem.cube((4, 4, 4), 3, "scalar")), "c+e+f", 2),
+        ("el432h2 c+e d2", cube_spec((4, 3, 2), 2, fem.ELASTICITY),
+         lambda: pb.BDDC(pb.Problem.cube((4, 3, 2), 2, "elasticity")), "c+e", 2)]
+
+
+@pytest.mark.parametrize("leaf", ["explicit", "factor"])
+@pytest.mark.parametrize("name,spec,make,mode,depth", TREE, ids=[t[0] for t in TREE])
+def test_primal_tree(name, spec, make, mode, depth, leaf, monkeypatch):
+    """The primal (root) system factored as a nested-dissection tree of fronts
+    over the substructure lattice (coarse_tree.hpp) instead of one dense root:
+    preconditioner, PCG and solution against the oracle's single sparse
+    factorization of the stabilized operator (bddc_operator.cpp:38-103)."""
+    monkeypatch.setenv("BDDC_B200_ROOT_DEPTH", str(depth))
+    monkeypatch.setenv("BDDC_B200_LEAF", leaf)
+    p = build_pipeline(spec)
+    h = HarmonicExtension(p.systems, p.maps)
+    itf = InterfaceProblem(p.systems, p.maps, h)
+    cs = arithmetic_constraints(p.globset, p.dmap, mode != "c", mode == "c+e+f")
+    prec = BddcPreconditioner(p.systems, p.maps, AveragingOperator(p.systems, p.maps),
+                              change_of_variables(cs, p.globset, p.dmap, p.maps))
+    b = make()
+    b.analysis()
+    b.arithmetic_constraints(mode != "c", mode == "c+e+f")
+    b.setup_preconditioner()
+    x = np.random.default_rng(2).standard_normal(itf.size)
+    assert rel(b.precond_apply(x), prec.apply(x)) <= 1e-10
+    g = b.pcg()
+    o = pcg(itf.apply, prec.apply, itf.rhs())
+    assert abs(g["iterations"] - o.iterations) <= 1
+    kg, ko = kappa_common(g["alphas"], g["betas"], o.alphas, o.betas)
+    assert abs(kg - ko) <= KAPPA_RTOL * ko
+    assert energy_error(p.systems, p.dmap.free_count, b.recover(g["x"]), itf.recover(o.x)) <= 1e-8
+
+
+def test_primal_tree_adaptive(monkeypatch):
+    """Adaptive constraints (group unknowns on faces) through a depth-2 primal tree."""
+    monkeypatch.setenv("BDDC_B200_ROOT_DEPTH", "2")
+    spec = baseline_config(5, subdomains=(4, 4, 4), elements_per_edge=2).spec
+    p = build_pipeline(spec)
+    ref = solve_item(p, "adaptive", 10.0, 15)
+    b = pb.BDDC(config=5, subdomains=(4, 4, 4), elements_per_edge=2)
+    row = b.run_item("adaptive", 10.0, 15)
+    assert row.constraint_rows == ref.constraint_rows
+    assert abs(row.iterations - ref.iterations) <= 1
+    g = b.pcg()
+    kg, ko = kappa_common(g["alphas"], g["betas"], ref.pcg.alphas, ref.pcg.betas)
+    assert abs(kg - ko) <= KAPPA_RTOL * ko
