@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -69,10 +70,13 @@ class StageArena {
     *clobbers_prec = false;
     std::size_t& mine = pair ? pair_ : prec_;
     if (n > mine) mine = n;
-    std::size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 0;
-    const double room = double(buf_.cap) * sizeof(double) + double(fr) - 1.5e9;
-    const bool split = double(prec_ + pair_) * sizeof(double) <= room;
+    bool split = prec_ + pair_ <= buf_.cap;  // both fit already: no query
+    if (!split) {
+      std::size_t fr = 0, tot = 0;
+      if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 0;
+      const double room = double(buf_.cap) * sizeof(double) + double(fr) - 1.5e9;
+      split = double(prec_ + pair_) * sizeof(double) <= room;
+    }
     const std::size_t total = split ? prec_ + pair_ : (prec_ > pair_ ? prec_ : pair_);
     if (total > buf_.cap) {
       buf_.release();
@@ -105,6 +109,65 @@ struct RegionPlan {
       off += (q.second + 31) / 32 * 32;
     }
   }
+};
+
+/// Many small host->device uploads as one copy: the arrays are packed into a
+/// pinned host blob and copied with one cudaMemcpyAsync into a grow-only device
+/// blob; every target DBuf becomes a view into it.  Add every array of a setup
+/// to the same batch (a grown blob invalidates the previous views), then
+/// flush() before the first kernel that reads them.
+class UploadBatch {
+ public:
+  UploadBatch() = default;
+  UploadBatch(const UploadBatch&) = delete;
+  UploadBatch& operator=(const UploadBatch&) = delete;
+  ~UploadBatch() {
+    if (host_) cudaFreeHost(host_);
+    if (ev_) cudaEventDestroy(ev_);
+  }
+  template <class T>
+  void add(DBuf<T>& target, const std::vector<T>& v) {
+    const std::size_t n = v.empty() ? 1 : v.size();
+    const std::size_t off = stage_.size(), bytes = n * sizeof(T);
+    stage_.resize(off + (bytes + 255) / 256 * 256, 0);
+    if (!v.empty()) std::memcpy(stage_.data() + off, v.data(), bytes);
+    items_.push_back(Item{reinterpret_cast<void*>(&target), off, n, &UploadBatch::bind<T>});
+  }
+  void flush(cudaStream_t st) {
+    if (items_.empty()) return;
+    const std::size_t used = stage_.size();
+    if (ev_) CK(cudaEventSynchronize(ev_));  // the previous copy out of the host blob is done
+    if (used > host_cap_) {
+      if (host_) CK(cudaFreeHost(host_));
+      host_cap_ = used + used / 4;
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&host_), host_cap_, cudaHostAllocDefault));
+    }
+    dev_.alloc(used);
+    std::memcpy(host_, stage_.data(), used);
+    CK(cudaMemcpyAsync(dev_.p, host_, used, cudaMemcpyHostToDevice, st));
+    if (!ev_) CK(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev_, st));
+    for (const Item& it : items_) it.bind_fn(it.target, dev_.p + it.off, it.count);
+    items_.clear();
+    stage_.clear();
+  }
+
+ private:
+  template <class T>
+  static void bind(void* target, char* p, std::size_t n) {
+    static_cast<DBuf<T>*>(target)->view(reinterpret_cast<T*>(p), n);
+  }
+  struct Item {
+    void* target;
+    std::size_t off, count;
+    void (*bind_fn)(void*, char*, std::size_t);
+  };
+  std::vector<Item> items_;
+  std::vector<char> stage_;
+  std::size_t host_cap_ = 0;
+  char* host_ = nullptr;
+  cudaEvent_t ev_ = nullptr;
+  DBuf<char> dev_;
 };
 
 /// Host-side stage timer (printed with BDDC_B200_PROFILE=1).

@@ -11,6 +11,8 @@
 #include <numeric>
 #include <string>
 
+#include <cooperative_groups.h>
+
 #include "devbuf.cuh"
 #include "../host/coarse_tree.hpp"
 #include "pairs.cuh"
@@ -165,16 +167,12 @@ __device__ __forceinline__ double xform_T_t(const XformDesc& x, int inst, int j,
 // Row-blocked: CTA (rb, s) forms rows [64 rb, 64 rb + 64) of S_s x_s.
 // Lane l of warp w owns rows (2l, 2l+1) (one 16-byte load per column) and the
 // columns w, w+8, ...; eight columns are in flight per thread, the eight warp
-// partials are reduced in shared memory in a fixed order.
-__global__ void __launch_bounds__(256) k_schur_gemv_rows(const SubDesc* sd, const double* __restrict__ p,
-                                                         const int* done) {
-  if (done && *done) return;
-  const SubDesc d = sd[blockIdx.y];
-  const int r0 = blockIdx.x * 64;
-  if (r0 >= d.nB) return;
-  extern __shared__ double xs[];
+// partials are reduced in shared memory in a fixed order.  `in(i)` yields the
+// input at interface dof i; xs holds nB doubles of shared memory.
+template <class In>
+__device__ __forceinline__ void schur_rows_body(const SubDesc& d, int r0, In in, double* xs) {
   __shared__ double2 part[8][32];
-  for (int c = threadIdx.x; c < d.nB; c += blockDim.x) xs[c] = p[d.biface[c]];
+  for (int c = threadIdx.x; c < d.nB; c += blockDim.x) xs[c] = in(d.biface[c]);
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double2* col0 = reinterpret_cast<const double2*>(d.S + r0) + lane;  // rows r0 + 2 lane, +1
@@ -211,6 +209,17 @@ __global__ void __launch_bounds__(256) k_schur_gemv_rows(const SubDesc* sd, cons
     const int r = r0 + threadIdx.x;
     if (r < d.nB) d.WB[r] = s;
   }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_schur_gemv_rows(const SubDesc* sd, const double* __restrict__ p,
+                                                         const int* done) {
+  if (done && *done) return;
+  const SubDesc d = sd[blockIdx.y];
+  const int r0 = blockIdx.x * 64;
+  if (r0 >= d.nB) return;
+  extern __shared__ double xs[];
+  schur_rows_body(d, r0, [p](int i) { return p[i]; }, xs);
 }
 
 __device__ __forceinline__ void block_partial(double v, double* partials) {
@@ -311,13 +320,11 @@ __global__ void __launch_bounds__(kRed) k_beta_update(i64 n, PcgState* st, doubl
 }
 
 // restrict_residual (bddc_operator.cpp:52-68) restricted to the interface:
-// FV_s = P_F T_s^T (w_s * r|_s), pads zero.
-__global__ void __launch_bounds__(256) k_restrict(const SubDesc* sd, XformDesc x, const double* __restrict__ r, const int* done) {
-  if (done && *done) return;
-  const SubDesc d = sd[blockIdx.x];
-  extern __shared__ double sm[];
-  double* v = sm;
-  for (int b = threadIdx.x; b < d.nB; b += blockDim.x) v[b] = d.bw[b] * r[d.biface[b]];
+// FV_s = P_F T_s^T (w_s * r|_s), pads zero.  `in(i)` yields r at interface dof
+// i; v holds nB doubles of shared memory.
+template <class In>
+__device__ __forceinline__ void restrict_body(const SubDesc& d, const XformDesc& x, In in, double* v) {
+  for (int b = threadIdx.x; b < d.nB; b += blockDim.x) v[b] = d.bw[b] * in(d.biface[b]);
   for (int q = threadIdx.x; q < d.NF; q += blockDim.x) d.FV[q] = 0.0;
   __syncthreads();
   for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
@@ -325,22 +332,26 @@ __global__ void __launch_bounds__(256) k_restrict(const SubDesc* sd, XformDesc x
     const double y = inst < 0 ? v[b] : xform_T_t_c(x, inst, d.bslot[b], v);
     d.FV[d.posF[b]] = y;
   }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_restrict(const SubDesc* sd, XformDesc x, const double* __restrict__ r, const int* done) {
+  if (done && *done) return;
+  extern __shared__ double sm[];
+  restrict_body(sd[blockIdx.x], x, [r](int i) { return r[i]; }, sm);
 }
 
 // prolong (bddc_operator.cpp:87-99): WB_s = w_s * T_s x_s   (then summed over copies)
 // The constrained rows of the glob transforms (dot products over the glob) are
 // formed first, one warp per row, into shared memory; every other boundary
-// position is a copy.
-__global__ void __launch_bounds__(256) k_prolong(const SubDesc* sd, XformDesc x, const int* done) {
-  if (done && *done) return;
-  const SubDesc d = sd[blockIdx.x];
-  extern __shared__ double sm[];
+// position is a copy.  q: the substructure's index among the owned ones.
+__device__ __forceinline__ void prolong_body(const SubDesc& d, const XformDesc& x, int q, double* sm) {
   double* xn = sm;
   double* yrow = sm + d.nB;
   for (int b = threadIdx.x; b < d.nB; b += blockDim.x) xn[b] = d.FV[d.posF[b]];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i0 = x.item_ptr[blockIdx.x], i1 = x.item_ptr[blockIdx.x + 1];
+  const int i0 = x.item_ptr[q], i1 = x.item_ptr[q + 1];
   for (int it = i0 + warp; it < i1; it += blockDim.x >> 5) {
     const int inst = x.item_inst[it], i = x.item_row[it];
     const int tr = x.inst_tr[inst];
@@ -364,6 +375,13 @@ __global__ void __launch_bounds__(256) k_prolong(const SubDesc* sd, XformDesc x,
     }
     d.WB[b] = d.bw[b] * xo;
   }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_prolong(const SubDesc* sd, XformDesc x, const int* done) {
+  if (done && *done) return;
+  extern __shared__ double sm[];
+  prolong_body(sd[blockIdx.x], x, blockIdx.x, sm);
 }
 
 // root right-hand side: sum of the leaves' coarse residuals (deterministic CSR)
@@ -468,61 +486,89 @@ __global__ void k_leaf_explicit_copy(const LeafX* ds) {
   }
 }
 
-// forward: warp per column j of E (symmetric -F_ee^{-1}: column == row), b_e staged in smem
-__global__ void __launch_bounds__(256) k_leaf_fwd_explicit(const LeafX* ds, const int* done) {
-  if (done && *done) return;
-  const LeafX d = ds[blockIdx.y];
+// forward: warp per column j of E (symmetric -F_ee^{-1}: column == row), b_e
+// staged in smem (bs: PE doubles).  Column block cb = columns [8 cb, 8 cb + 8).
+__device__ __forceinline__ void leaf_fwd_body(const LeafX& d, int cb, double* bs) {
   const int cols = d.PE + d.M;
-  if (blockIdx.x * 8 >= cols) return;
-  extern __shared__ double bs[];
-  for (int k = threadIdx.x; k < d.PE; k += blockDim.x) bs[k] = d.FV[k];
-  __syncthreads();
-  const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (j >= cols) return;
-  const double* col = d.E + (size_t)j * d.PE;
-  double s0 = 0.0, s1 = 0.0;
-  for (int k = lane; k < d.PE; k += 64) {  // PE is a multiple of 64
-    s0 += col[k] * bs[k];
-    s1 += col[k + 32] * bs[k + 32];
-  }
-  double s = s0 + s1;
+  if (cb * 8 < cols) {
+    for (int k = threadIdx.x; k < d.PE; k += blockDim.x) bs[k] = d.FV[k];
+    __syncthreads();
+    const int j = cb * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (j < cols) {
+      // lane reads double2 k = lane + 32 t; eight loads in flight per lane
+      const double2* col = reinterpret_cast<const double2*>(d.E + (size_t)j * d.PE);
+      const double2* b2 = reinterpret_cast<const double2*>(bs);
+      const int half = d.PE / 2;  // PE is a multiple of 64
+      double s0 = 0.0, s1 = 0.0;
+      for (int k0 = 0; k0 < half; k0 += 256) {
+        double2 v[8];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) d.FV2[j] = j < d.PE ? -s : d.FV[j] + s;
+        for (int t = 0; t < 8; ++t) {
+          const int k = k0 + 32 * t + lane;
+          v[t] = k < half ? __ldg(col + k) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int k = k0 + 32 * t + lane;
+          if (k < half) {
+            const double2 bb = b2[k];
+            s0 += v[t].x * bb.x;
+            s1 += v[t].y * bb.y;
+          }
+        }
+      }
+      double s = s0 + s1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) d.FV2[j] = j < d.PE ? -s : d.FV[j] + s;
+    }
+  }
+  __syncthreads();
 }
 
-// backward: x_e = u - W x_c.  CTA (rb, s): rows [64 rb, 64 rb + 64) of the
+__global__ void __launch_bounds__(256) k_leaf_fwd_explicit(const LeafX* ds, const int* done) {
+  if (done && *done) return;
+  extern __shared__ double bs[];
+  leaf_fwd_body(ds[blockIdx.y], blockIdx.x, bs);
+}
+
+// backward: x_e = u - W x_c.  Row block rb: rows [64 rb, 64 rb + 64) of the
 // F-layout vector; the four 64-thread groups split the coarse slots, partials
-// reduced in a fixed order.  Coarse slots take the root values.
+// reduced in a fixed order.  Coarse slots take the root values (xc: M doubles).
+__device__ __forceinline__ void leaf_bwd_body(const LeafX& d, int rb, const double* __restrict__ croot, double* xc) {
+  __shared__ double part[4][64];
+  const int r0 = rb * 64;
+  if (r0 < d.PE + d.M) {
+    for (int c = threadIdx.x; c < d.M; c += blockDim.x) xc[c] = d.cmap[c] >= 0 ? croot[d.cmap[c]] : 0.0;
+    __syncthreads();
+    const int g = threadIdx.x >> 6, i = r0 + (threadIdx.x & 63);
+    if (r0 >= d.PE) {  // coarse slots (PE is a multiple of 64)
+      if (g == 0) d.FV[i] = xc[i - d.PE];
+    } else {
+      const double* w = d.E + (size_t)d.PE * d.PE + i;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int c = g;
+      for (; c + 12 < d.M; c += 16) {
+        s0 += w[(size_t)c * d.PE] * xc[c];
+        s1 += w[(size_t)(c + 4) * d.PE] * xc[c + 4];
+        s2 += w[(size_t)(c + 8) * d.PE] * xc[c + 8];
+        s3 += w[(size_t)(c + 12) * d.PE] * xc[c + 12];
+      }
+      for (; c < d.M; c += 4) s0 += w[(size_t)c * d.PE] * xc[c];
+      part[g][threadIdx.x & 63] = (s0 + s1) + (s2 + s3);
+      __syncthreads();
+      if (g == 0)
+        d.FV[i] = d.FV2[i] + ((part[0][threadIdx.x] + part[1][threadIdx.x]) + (part[2][threadIdx.x] + part[3][threadIdx.x]));
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(256) k_leaf_bwd_explicit(const LeafX* ds, const double* __restrict__ croot,
                                                            const int* done) {
   if (done && *done) return;
-  const LeafX d = ds[blockIdx.y];
-  const int r0 = blockIdx.x * 64;
-  if (r0 >= d.PE + d.M) return;
   extern __shared__ double xc[];
-  __shared__ double part[4][64];
-  for (int c = threadIdx.x; c < d.M; c += blockDim.x) xc[c] = d.cmap[c] >= 0 ? croot[d.cmap[c]] : 0.0;
-  __syncthreads();
-  const int g = threadIdx.x >> 6, i = r0 + (threadIdx.x & 63);
-  if (r0 >= d.PE) {  // coarse slots (PE is a multiple of 64)
-    if (g == 0) d.FV[i] = xc[i - d.PE];
-    return;
-  }
-  const double* w = d.E + (size_t)d.PE * d.PE + i;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int c = g;
-  for (; c + 12 < d.M; c += 16) {
-    s0 += w[(size_t)c * d.PE] * xc[c];
-    s1 += w[(size_t)(c + 4) * d.PE] * xc[c + 4];
-    s2 += w[(size_t)(c + 8) * d.PE] * xc[c + 8];
-    s3 += w[(size_t)(c + 12) * d.PE] * xc[c + 12];
-  }
-  for (; c < d.M; c += 4) s0 += w[(size_t)c * d.PE] * xc[c];
-  part[g][threadIdx.x & 63] = (s0 + s1) + (s2 + s3);
-  __syncthreads();
-  if (g == 0)
-    d.FV[i] = d.FV2[i] + ((part[0][threadIdx.x] + part[1][threadIdx.x]) + (part[2][threadIdx.x] + part[3][threadIdx.x]));
+  leaf_bwd_body(ds[blockIdx.y], blockIdx.x, croot, xc);
 }
 
 // A child of a coarse front: its Schur complement onto its coarse slots is the
@@ -664,6 +710,367 @@ __global__ void k_insert_boundary(const SubDesc* sd, double* MV, const long long
   for (int b = threadIdx.x; b < d.nB; b += blockDim.x) MV[mvoff[blockIdx.x] + PI[blockIdx.x] + b] = u_iface[d.biface[b]];
 }
 
+// restrict / prolong at one boundary position (s, b): the same arithmetic as
+// restrict_body / prolong_body, spread over every boundary copy instead of one
+// CTA per substructure (the persistent PCG's latency-bound regime).
+template <class In>
+__device__ __forceinline__ void restrict_at(const SubDesc& d, const XformDesc& x, int b, In in) {
+  const int inst = d.bglob[b];
+  double y;
+  if (inst < 0) {
+    y = d.bw[b] * in(d.biface[b]);
+  } else {
+    const int tr = x.inst_tr[inst];
+    const int* cp = x.cpos + x.inst_pos[inst];
+    const int n = x.tr_n[tr], r = x.tr_r[tr], j = d.bslot[b];
+    const double* D = x.D + x.tr_off_d[tr];
+    double s0 = j >= r ? d.bw[cp[j]] * in(d.biface[cp[j]]) : 0.0, s1 = 0.0;
+    int i = 0;
+    for (; i + 1 < r; i += 2) {
+      s0 += D[i * n + j] * (d.bw[cp[i]] * in(d.biface[cp[i]]));
+      s1 += D[(i + 1) * n + j] * (d.bw[cp[i + 1]] * in(d.biface[cp[i + 1]]));
+    }
+    if (i < r) s0 += D[i * n + j] * (d.bw[cp[i]] * in(d.biface[cp[i]]));
+    y = s0 + s1;
+  }
+  d.FV[d.posF[b]] = y;
+}
+
+// prolong, constrained rows: item k = row i of a glob instance of owned
+// substructure item_sub[k]; one warp per item (dot product over the glob).
+__device__ __forceinline__ void prolong_item(const SubDesc& d, const XformDesc& x, int k, double* yglob) {
+  const int lane = threadIdx.x & 31;
+  const int inst = x.item_inst[k], i = x.item_row[k];
+  const int tr = x.inst_tr[inst];
+  const int* pos = x.tpos + x.inst_pos[inst];
+  const int n = x.tr_n[tr];
+  const double* D = x.D + x.tr_off_d[tr] + i * n;
+  double s = 0.0;
+  for (int jj = lane; jj < n; jj += 32) s += D[jj] * d.FV[d.posF[pos[jj]]];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) yglob[k] = s;
+}
+
+// Position-parallel restrict / prolong (every boundary copy of the owned
+// substructures; wpos = (owned index, boundary position)).
+__global__ void __launch_bounds__(256) k_restrict_pos(const SubDesc* sd, XformDesc x, const int2* __restrict__ wpos,
+                                                      int nw, const double* __restrict__ r, const int* done) {
+  if (done && *done) return;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nw; e += gridDim.x * blockDim.x) {
+    const int2 sb = wpos[e];
+    restrict_at(sd[sb.x], x, sb.y, [r](int i) { return r[i]; });
+  }
+}
+
+__global__ void __launch_bounds__(256) k_prolong_items(const SubDesc* sd, XformDesc x, const int* __restrict__ item_sub,
+                                                       int nitems, double* yglob, const int* done) {
+  if (done && *done) return;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nitems; k += (gridDim.x * blockDim.x) >> 5)
+    prolong_item(sd[item_sub[k]], x, k, yglob);
+}
+
+__global__ void __launch_bounds__(256) k_prolong_copy(const SubDesc* sd, const int2* __restrict__ wpos,
+                                                      const int* __restrict__ wsrc, int nw,
+                                                      const double* __restrict__ fv, const double* __restrict__ yglob,
+                                                      const int* done) {
+  if (done && *done) return;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nw; e += gridDim.x * blockDim.x) {
+    const int2 sb = wpos[e];
+    const SubDesc& d = sd[sb.x];
+    const int src = wsrc[e];
+    d.WB[sb.y] = d.bw[sb.y] * (src >= 0 ? fv[src] : yglob[-1 - src]);
+  }
+}
+
+// Leaf forward, one 64-column tile of E per call: b_e staged once, each warp
+// owns eight columns and keeps two of them (up to 16 loads) in flight.
+__device__ __forceinline__ void leaf_fwd_tile(const LeafX& d, int t, double* bs) {
+  const int cols = d.PE + d.M;
+  if (t * 64 >= cols) return;  // uniform over the CTA
+  for (int k = threadIdx.x; k < d.PE; k += blockDim.x) bs[k] = d.FV[k];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = d.PE / 2;
+  const double2* b2 = reinterpret_cast<const double2*>(bs);
+  for (int u = 0; u < 8; u += 2) {
+    const int j0 = t * 64 + warp + 8 * u, j1 = j0 + 8;
+    const double2* c0 = reinterpret_cast<const double2*>(d.E + (size_t)min(j0, cols - 1) * d.PE);
+    const double2* c1 = reinterpret_cast<const double2*>(d.E + (size_t)min(j1, cols - 1) * d.PE);
+    double a0 = 0.0, a1 = 0.0, e0 = 0.0, e1 = 0.0;
+    for (int k0 = 0; k0 < half; k0 += 256) {
+      double2 v[8], w[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int k = k0 + 32 * q + lane;
+        v[q] = k < half ? __ldg(c0 + k) : make_double2(0.0, 0.0);
+        w[q] = k < half ? __ldg(c1 + k) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int k = k0 + 32 * q + lane;
+        if (k < half) {
+          const double2 bb = b2[k];
+          a0 += v[q].x * bb.x;
+          a1 += v[q].y * bb.y;
+          e0 += w[q].x * bb.x;
+          e1 += w[q].y * bb.y;
+        }
+      }
+    }
+    double s0 = a0 + a1, s1 = e0 + e1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (lane == 0) {
+      if (j0 < cols) d.FV2[j0] = j0 < d.PE ? -s0 : d.FV[j0] + s0;
+      if (j1 < cols) d.FV2[j1] = j1 < d.PE ? -s1 : d.FV[j1] + s1;
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Persistent PCG (pcg.cpp:28-77) for the latency-bound regime: explicit leaf
+// operators and a small root inverse on one GPU.  One cooperative launch runs
+// every iteration; grid barriers replace kernel boundaries and the scalars
+// (alpha, beta, rz, the stopping test) are formed redundantly by every CTA
+// from the same partials in the same order, so no CTA waits on another for
+// them.  p and r are double-buffered so that the updates p = z + beta p and
+// r -= alpha q fold into the phases that read them:
+//   A  q_s = S_s (z + beta p)                 (and p' = z + beta p)
+//   B  q = sum of copies, partial p'.q
+//   C  alpha; x += alpha p'; r' = r - alpha q (partials r'.r'); restrict(r')
+//   D  leaf forward   E  root gather + R^{-1}   F  leaf backward
+//   G  prolong        H  z = sum of copies, partial r'.z
+// ---------------------------------------------------------------------------
+struct PcgPersist {
+  const SubDesc* sd;
+  XformDesc xf;
+  const LeafX* lx;
+  const int2* wpos;  // every boundary copy: (owned substructure index, boundary position)
+  int nw;
+  const int* wsrc;   // per boundary copy: leaf-vector index, or -1 - constrained item
+  const int* item_sub;
+  int nitems;
+  double* yglob;     // constrained rows of the prolongation
+  double* FVall;     // leaf vectors (zeroed before the restriction writes them)
+  long long nfv;
+  int ns, nrb_schur, ncb_fwd, nrb_bwd;
+  // root
+  int n_root, NR;
+  const int* root_ptr;
+  const long long* root_src;
+  const double* Rinv;
+  const double* fvsrc;  // leaf forward results (root_src offsets)
+  double* xroot;
+  // interface
+  i64 n;
+  const int* icp;
+  const int* icpos;
+  const double* WB;
+  double *x, *z, *q;
+  double* p[2];
+  double* r[2];
+  double* part;  // 3 x G partials: p.q, r.r, r.z
+  PcgState* st;
+  double* alphas;
+  double* betas;
+  unsigned long long* trace;  // optional: %globaltimer at each phase end (CTA 0), 9 per iteration
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ double grid_sum(const double* part, int G) {
+  // every CTA: the same fixed-order sum of the G partials
+  __shared__ double red[256];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < G; i += blockDim.x) v += part[i];
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double out = red[0];
+  __syncthreads();
+  return out;
+}
+
+__device__ __forceinline__ void cta_partial(double v, double* slot) {
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < (blockDim.x >> 5) ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) *slot = v;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_pcg_persistent(PcgPersist P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  const int G = gridDim.x, me = blockIdx.x;
+  const i64 gt = (i64)me * blockDim.x + threadIdx.x, gs = (i64)G * blockDim.x;
+  double* part_pq = P.part;
+  double* part_rr = P.part + G;
+  double* part_rz = P.part + 2 * G;
+  // scalars: identical in every CTA
+  double rz = P.st->rz, beta = 0.0;
+  int it = P.st->it;
+  const int max_it = P.st->max_it, precond_residual = P.st->precond_residual;
+  const double ref = P.st->ref, tol = P.st->tol;
+  int done = P.st->done, cur = 0;
+  while (!done) {
+    const double* pold = P.p[cur];
+    double* pnew = P.p[cur ^ 1];
+    const double* rold = P.r[cur];
+    double* rnew = P.r[cur ^ 1];
+    if (P.trace && me == 0 && threadIdx.x == 0 && it < 64) P.trace[(size_t)it * 9 + 8] = gtimer();
+    // A
+    for (int vb = me; vb < P.nrb_schur * P.ns; vb += G) {
+      const SubDesc& d = P.sd[vb / P.nrb_schur];
+      const int r0 = (vb % P.nrb_schur) * 64;
+      if (r0 < d.nB) {
+        const double* z = P.z;
+        const double b = beta;
+        schur_rows_body(d, r0, [z, pold, b](int i) { return z[i] + b * pold[i]; }, sm);
+      }
+    }
+    for (i64 i = gt; i < P.n; i += gs) pnew[i] = P.z[i] + beta * pold[i];
+    for (i64 i = gt; i < P.nfv; i += gs) P.FVall[i] = 0.0;
+    grid.sync();
+    if (P.trace && me == 0 && threadIdx.x == 0 && it < 64) P.trace[(size_t)it * 9 + 0] = gtimer();
+    // B
+    {
+      double acc = 0.0;
+      for (i64 i = gt; i < P.n; i += gs) {
+        double s = 0.0;
+        for (int t = P.icp[i]; t < P.icp[i + 1]; ++t) s += P.WB[P.icpos[t]];
+        P.q[i] = s;
+        acc += s * pnew[i];
+      }
+      cta_partial(acc, part_pq + me);
+    }
+    grid.sync();
+    if (P.trace && me == 0 && threadIdx.x == 0 && it < 64) P.trace[(size_t)it * 9 + 1] = gtimer();
+    // C
+    const double alpha = rz / grid_sum(part_pq, G);
+    {
+      double acc = 0.0;
+      for (i64 i = gt; i < P.n; i += gs) {
+        P.x[i] += alpha * pnew[i];
+        const double ri = rold[i] - alpha * P.q[i];
+        rnew[i] = ri;
+        acc += ri * ri;
+      }
+      cta_partial(acc, part_rr + me);
+    }
+    {
+      const double* q = P.q;
+      const double a = alpha;
+      for (i64 w = gt; w < P.nw; w += gs) {
+        const int2 sb = P.wpos[w];
+        restrict_at(P.sd[sb.x], P.xf, sb.y, [rold, q, a](int i) { return rold[i] - a * q[i]; });
+      }
+    }
+    if (me == 0 && threadIdx.x == 0) P.alphas[it] = alpha;
+    grid.sync();
+    if (P.trace && me == 0 && threadIdx.x == 0 && it < 64) P.trace[(size_t)it * 9 + 2] = gtimer();
+    // D
+    for (int vb = me; vb < P.ncb_fwd * P.ns; vb += G) leaf_fwd_tile(P.lx[vb / P.ncb_fwd], vb % P.ncb_fwd, sm);
+    grid.sync();
+    if (P.trace && me == 0 && threadIdx.x == 0 && it < 64) P.trace[(size_t)it * 9 + 3] = gtimer();
+    // E: every CTA gathers the root right-hand side, then its columns of -R^{-1}
+    if (me * 8 < P.NR) {
+      for (int k = threadIdx.x; k < P.NR; k += blockDim.x) {
+        double s = 0.0;
+        if (k < P.n_root)
+          for (int t = P.root_ptr[k]; t < P.root_ptr[k + 1]; ++t) s += P.fvsrc[P.root_src[t]];
+        sm[k] = s;
+      }
+      __syncthreads();
+      const int lane = threadIdx.x & 31;
+      for (int c = (me * blockDim.x + threadIdx.x) >> 5; c < P.NR; c += (G * blockDim.x) >> 5) {
+        const double* col = P.Rinv + (size_t)c * P.NR;
+        double s0 = 0.0, s1 = 0.0;
+        int rr = lane;
+        for (; rr + 32 < P.NR; rr += 64) {
+          s0 += col[rr] * sm[rr];
+          s1 += col[rr + 32] * sm[rr + 32];
+        }
+        if (rr < P.NR) s0 += col[rr] * sm[rr];
+        double sum = s0 + s1;
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) P.xroot[c] = -sum;
+      }
+      __syncthreads();
+    }
+    grid.sync();
+    if (P.trace && me == 0 && threadIdx.x == 0 && it < 64) P.trace[(size_t)it * 9 + 4] = gtimer();
+    // F
+    for (int vb = me; vb < P.nrb_bwd * P.ns; vb += G) leaf_bwd_body(P.lx[vb / P.nrb_bwd], vb % P.nrb_bwd, P.xroot, sm);
+    grid.sync();
+    if (P.trace && me == 0 && threadIdx.x == 0 && it < 64) P.trace[(size_t)it * 9 + 5] = gtimer();
+    // G
+    for (int k = (me * blockDim.x + threadIdx.x) >> 5; k < P.nitems; k += (G * blockDim.x) >> 5)
+      prolong_item(P.sd[P.item_sub[k]], P.xf, k, P.yglob);
+    grid.sync();
+    for (i64 w = gt; w < P.nw; w += gs) {
+      const int2 sb = P.wpos[w];
+      const SubDesc& d = P.sd[sb.x];
+      const int src = P.wsrc[w];
+      d.WB[sb.y] = d.bw[sb.y] * (src >= 0 ? P.FVall[src] : P.yglob[-1 - src]);
+    }
+    grid.sync();
+    if (P.trace && me == 0 && threadIdx.x == 0 && it < 64) P.trace[(size_t)it * 9 + 6] = gtimer();
+    // H
+    {
+      double acc = 0.0;
+      for (i64 i = gt; i < P.n; i += gs) {
+        double s = 0.0;
+        for (int t = P.icp[i]; t < P.icp[i + 1]; ++t) s += P.WB[P.icpos[t]];
+        P.z[i] = s;
+        acc += s * rnew[i];
+      }
+      cta_partial(acc, part_rz + me);
+    }
+    grid.sync();
+    if (P.trace && me == 0 && threadIdx.x == 0 && it < 64) P.trace[(size_t)it * 9 + 7] = gtimer();
+    // beta and the stopping test (pcg.cpp:49-70)
+    const double rz_next = grid_sum(part_rz, G);
+    const double rr = grid_sum(part_rr, G);
+    beta = rz_next / rz;
+    rz = rz_next;
+    if (me == 0 && threadIdx.x == 0) P.betas[it] = beta;
+    ++it;
+    const double res = precond_residual ? sqrt(fmax(rz_next, 0.0)) : sqrt(rr);
+    const double relres = res / ref;
+    done = (relres <= tol || it >= max_it) ? 1 : 0;
+    cur ^= 1;
+    if (done && me == 0 && threadIdx.x == 0) {
+      P.st->rz = rz;
+      P.st->beta = beta;
+      P.st->alpha = alpha;
+      P.st->it = it;
+      P.st->relres = relres;
+      P.st->done = 1;
+    }
+  }
+  // the final iterate lives in x; p/r buffers need no copy back
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -757,9 +1164,18 @@ struct DeviceState {
   double* leaf_croot = nullptr;  // where the leaves' backward sweeps read their coarse values
   // pcg
   DBuf<double> vx, vr, vz, vp, vq, vb, part_a, part_b, alphas, betas;
+  DBuf<double> vp2, vr2, part3;  // persistent PCG: second p/r buffers, 3 x G partials
+  DBuf<int2> wpos;
+  UploadBatch up_index, up_desc;  // set_constraints' small uploads (one copy each)
+  int nw = 0;
+  DBuf<int> wsrc, item_sub;
+  DBuf<double> yglob;
+  int nitems = 0;
   DBuf<PcgState> pst;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  int pcg_grid = 0;
+  std::size_t pcg_smem = 0;
   long long graph_kernels = 0;
   // adaptive pair machinery
   PairEngine pairs;
@@ -1144,7 +1560,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   // boundary position of each local dof (owned substructures)
   std::vector<std::vector<int>> bpos_of(ns);
   const int no = D.n_own;
-#pragma omp parallel for schedule(dynamic, 4)
+#pragma omp parallel for schedule(dynamic, 4) if (no >= 64)
   for (int q = 0; q < no; ++q) {
     const int s = D.own[q];
     bpos_of[s].assign(m.subs[s].dim(), -1);
@@ -1178,7 +1594,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   std::vector<int> perm(np_total), iperm(np_total), tpos(ntpos);
   std::vector<double> trD(nd_total);
   std::vector<int> bglob(D.WB.n, -1), bslot(D.WB.n, -1);
-#pragma omp parallel for schedule(dynamic, 16)
+#pragma omp parallel for schedule(dynamic, 16) if (ntr >= 512)
   for (int k = 0; k < ntr; ++k) {
     const GlobTransform& gt = cov.transforms[k];
     const int n = gt.n, r = gt.rank;
@@ -1235,7 +1651,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   // coarse dofs per subdomain: corners (ascending corner id), then explicit dofs (group order)
   std::vector<std::vector<int>> coarse_b(ns), coarse_root(ns);
   const i64 ncd = m.maps.corner_dof_count;
-#pragma omp parallel for schedule(dynamic, 4)
+#pragma omp parallel for schedule(dynamic, 4) if (no >= 64)
   for (int q = 0; q < no; ++q) {
     const int s = D.own[q];
     const Subdomain& S = m.subs[s];
@@ -1381,13 +1797,14 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     D.root_inv = mode == "inverse" || (mode != "sweep" && D.NR <= kRootInverseMax);
   }
   ht.mark("index_build");
-  // uploads
-  D.bposF.upload(posF, st);
-  D.bglob.upload(bglob, st);
-  D.bslot.upload(bslot, st);
-  auto up_i = [&](DBuf<int>& b, const std::vector<int>& v) {
-    if (v.empty()) b.alloc(1); else b.upload(v, st);
-  };
+  // uploads: the index arrays in one copy (batch A), then the descriptors that
+  // point into them and into the arenas (batch B)
+  UploadBatch& UA = D.up_index;
+  UploadBatch& UB = D.up_desc;
+  UA.add(D.bposF, posF);
+  UA.add(D.bglob, bglob);
+  UA.add(D.bslot, bslot);
+  auto up_i = [&](DBuf<int>& b, const std::vector<int>& v) { UA.add(b, v); };
   up_i(D.inst_tr, inst_tr);
   up_i(D.inst_pos, inst_pos);
   up_i(D.tpos, tpos);
@@ -1398,21 +1815,74 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   up_i(D.perm, perm);
   up_i(D.iperm, iperm);
   up_i(D.cmap, cmap);
-  if (trD.empty()) D.trD.alloc(1); else D.trD.upload(trD, st);
+  UA.add(D.trD, trD);
   up_i(D.cpos, cpos);
   up_i(D.item_ptr, item_ptr);
   up_i(D.item_inst, item_inst);
   up_i(D.item_row, item_row);
   up_i(D.inst_loff, inst_loff);
+  {
+    // position-parallel restrict / prolong: per boundary copy of the owned
+    // substructures, the leaf-vector index it copies or the constrained item
+    // it takes (prolong_body's two cases)
+    std::vector<int2> wp;
+    std::vector<int> wsrc, isub(item_inst.size());
+    for (int q = 0; q < no; ++q) {
+      const int s = D.own[q];
+      for (int k = item_ptr[q]; k < item_ptr[q + 1]; ++k) isub[k] = q;
+      for (int b = 0; b < D.nB[s]; ++b) {
+        const long long w = D.wb_off[s] + b;
+        wp.push_back(make_int2(q, b));
+        const int inst = bglob[w];
+        int src = static_cast<int>(D.fv_off[s]) + posF[w];
+        if (inst >= 0) {
+          const int tr = inst_tr[inst];
+          const int i = iperm[tr_off_perm[tr] + bslot[w]];
+          if (i < tr_r[tr])
+            src = -1 - (item_ptr[q] + inst_loff[inst] + i);
+          else
+            src = static_cast<int>(D.fv_off[s]) + posF[D.wb_off[s] + tpos[inst_pos[inst] + i]];
+        }
+        wsrc.push_back(src);
+      }
+    }
+    UA.add(D.wpos, wp);
+    D.nw = static_cast<int>(wp.size());
+    up_i(D.wsrc, wsrc);
+    up_i(D.item_sub, isub);
+    D.nitems = static_cast<int>(item_inst.size());
+    D.yglob.alloc(std::max(D.nitems, 1));
+  }
+  UA.add(D.d_xoff, xoff);
+  D.tree.resize(plan.levels.size());
+  for (auto& T : D.tree)
+    if (!T) T.reset(new DeviceState::TreeLevel);
+  for (std::size_t l = 0; l < plan.levels.size(); ++l) {
+    DeviceState::TreeLevel& T = *D.tree[l];
+    const CoarseTree::Level& P = plan.levels[l];
+    up_i(T.ptr, P.ptr);
+    up_i(T.child, P.child);
+    up_i(T.cidx, P.cidx);
+    up_i(T.cmap, P.cmap);
+    UA.add(T.src, P.src);
+  }
+  up_i(D.root_ptr, plan.top_ptr);
+  up_i(D.root_child, plan.top_child);
+  up_i(D.root_c, plan.top_cidx);
+  UA.add(D.root_src, plan.top_src);
+  UA.add(D.d_foff, D.f_off);
+  up_i(D.d_NF, D.NA);  // leading dimensions of the F fronts
+  up_i(D.d_PE, D.PE);
+  up_i(D.pads, pads);
+  up_i(D.pad_sub, pad_sub);
+  UA.flush(st);
+  ht.mark("upload_index");
   D.xf = XformDesc{D.inst_tr.p, D.inst_pos.p, D.tpos.p, D.tr_n.p, D.tr_r.p, D.tr_off_perm.p, D.tr_off_d.p,
                    D.perm.p, D.iperm.p, D.trD.p, D.cpos.p, D.item_ptr.p, D.item_inst.p, D.item_row.p,
                    D.inst_loff.p};
   // Preconditioner arenas: views into the stage arena (shared with the pair
   // stage).  [F | DinvF | E | Xtmp], with the root and the primal tree over the
   // transform scratch Xtmp (dead once F is formed).
-  D.tree.resize(plan.levels.size());
-  for (auto& T : D.tree)
-    if (!T) T.reset(new DeviceState::TreeLevel);
   {
     const long long ldR0 = D.root_inv ? 2LL * D.NR : D.NR;
     RegionPlan lead, scratch, late;
@@ -1428,8 +1898,8 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       late.add(D.tree[l]->Dinv, plan.levels[l].d_size);
     }
     const std::size_t total = lead.total() + std::max(scratch.total(), late.total());
-    const double room = double(D.stage.capacity()) * 8.0 + free_bytes();
-    if (double(total) * 8.0 > room)
+    const double room = total <= D.stage.capacity() ? 0.0 : double(D.stage.capacity()) * 8.0 + free_bytes();
+    if (total > D.stage.capacity() && double(total) * 8.0 > room)
       throw Error(kError, "preconditioner needs " + std::to_string(total * 8.0 / 1e9) + " GB (root " +
                               std::to_string(D.n_root) + " primal unknowns); " + std::to_string(room / 1e9) +
                               " GB available");
@@ -1439,6 +1909,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     scratch.place(base + lead.total());
     late.place(base + lead.total());
   }
+  ht.mark("regions");
   D.F.zero(st);
   D.FV.alloc(std::max<long long>(fvo, 1));
   D.FV.zero(st);
@@ -1446,7 +1917,6 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     D.FV2.alloc(std::max<long long>(fvo, 1));
     D.FV2.zero(st);
   }
-  if (xoff.empty()) D.d_xoff.alloc(1); else D.d_xoff.upload(xoff, st);
   D.finfo.alloc(std::max(no, 1));
   D.finfo.zero(st);
   std::vector<SubDesc> sd(no);
@@ -1462,9 +1932,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     fw[q] = SolveDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.FV.p + D.fv_off[s], D.NF[s], D.PE[s],
                       nullptr, nullptr};
   }
-  auto up_v = [&](auto& b, const auto& v) {
-    if (v.empty()) b.alloc(1); else b.upload(v, st);
-  };
+  auto up_v = [&](auto& b, const auto& v) { UB.add(b, v); };
   up_v(D.subdesc, sd);
   up_v(D.ffront, fd);
   up_v(D.fsolve_fwd, fw);
@@ -1481,11 +1949,6 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     T.V.alloc(std::max<long long>(P.arena, 1));
     T.info.alloc(T.nfr);
     T.info.zero(st);
-    up_i(T.ptr, P.ptr);
-    up_i(T.child, P.child);
-    up_i(T.cidx, P.cidx);
-    up_i(T.cmap, P.cmap);
-    if (P.src.empty()) T.src.alloc(1); else T.src.upload(P.src, st);
     T.NF.assign(T.nfr, 0);
     T.PE.assign(T.nfr, 0);
     T.nown.assign(T.nfr, 0);
@@ -1576,16 +2039,18 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     }
     up_v(D.leafx, lx);
   }
-  up_i(D.root_ptr, plan.top_ptr);
-  up_i(D.root_child, plan.top_child);
-  up_i(D.root_c, plan.top_cidx);
-  if (plan.top_src.empty()) D.root_src.alloc(1); else D.root_src.upload(plan.top_src, st);
-  D.d_foff.upload(D.f_off, st);
-  up_i(D.d_NF, D.NA);  // leading dimensions of the F fronts
-  up_i(D.d_PE, D.PE);
-  up_i(D.pads, pads);
-  up_i(D.pad_sub, pad_sub);
-  ht.mark("uploads");
+  {
+    std::vector<FrontDesc> rf{
+        FrontDesc{D.R.p, D.DinvR.p, static_cast<int>(ldR), D.NR, D.rinfo.p, D.root_inv ? D.NR : 0}};
+    up_v(D.rfront, rf);
+    std::vector<TrailDesc> rt{TrailDesc{D.R.p, D.Rinv.p, static_cast<int>(ldR), D.NR}};
+    up_v(D.rtrail, rt);
+    std::vector<SolveDesc> rs{SolveDesc{D.R.p, D.DinvR.p, D.xroot.p, D.NR, D.NR, nullptr, nullptr}};
+    up_v(D.rsolve, rs);
+  }
+  ht.mark("descriptors");
+  UB.flush(st);
+  ht.mark("upload_desc");
   StageProfiler prof("set_constraints", st);
   // F = P (T^T S T) P^T, pads identity
   if (no) {
@@ -1637,18 +2102,12 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     }
   }
   if (D.comm) D.comm->allreduce(D.R.p, (size_t)ldR * D.NR, st);
-  std::vector<FrontDesc> rf{FrontDesc{D.R.p, D.DinvR.p, static_cast<int>(ldR), D.NR, D.rinfo.p, D.root_inv ? D.NR : 0}};
-  D.rfront.upload(rf, st);
   prof.mark("root_asm");
   partial_cholesky(D.rfront.p, 1, static_cast<int>(ldR), D.NR, D.root_inv ? D.NR : 0, st);
   if (D.root_inv) {
-    std::vector<TrailDesc> rt{TrailDesc{D.R.p, D.Rinv.p, static_cast<int>(ldR), D.NR}};
-    D.rtrail.upload(rt, st);
     copy_trailing_full(D.rtrail.p, 1, D.NR, st);
   }
   prof.mark(D.root_inv ? "cholR+inverse" : "cholR");
-  std::vector<SolveDesc> rs{SolveDesc{D.R.p, D.DinvR.p, D.xroot.p, D.NR, D.NR, nullptr, nullptr}};
-  D.rsolve.upload(rs, st);
   CK(cudaGetLastError());
   CK(cudaEventRecord(D.e1, st));
   times_.preconditioner = elapsed(D.e0, D.e1);
@@ -1704,7 +2163,9 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
   auto mark = [&](const char* s) {
     if (prof) prof->mark(s);
   };
-  if (ns) k_restrict<<<ns, 256, smem_b, st>>>(D.subdesc.p, D.xf, r, done);
+  const int nw = D.nw;
+  const int pos_blocks = std::max(1, std::min(4 * sm_count(), (nw + 255) / 256));
+  if (ns) k_restrict_pos<<<pos_blocks, 256, 0, st>>>(D.subdesc.p, D.xf, D.wpos.p, nw, r, done);
   count_launch(3);  // restrict, prolong, copy sum
   mark("restrict");
   if (D.leaf_explicit && ns) {
@@ -1759,7 +2220,14 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     front_backward(D.fsolve_bwd.p, ns, D.max_NF, st, done);
   }
   mark("leaf_bwd");
-  if (ns) k_prolong<<<ns, 256, smem_b + D.max_rows * sizeof(double), st>>>(D.subdesc.p, D.xf, done);
+  if (ns) {
+    if (D.nitems) {
+      k_prolong_items<<<std::max(1, std::min(4 * sm_count(), (D.nitems + 7) / 8)), 256, 0, st>>>(
+          D.subdesc.p, D.xf, D.item_sub.p, D.nitems, D.yglob.p, done);
+      count_launch(1);
+    }
+    k_prolong_copy<<<pos_blocks, 256, 0, st>>>(D.subdesc.p, D.wpos.p, D.wsrc.p, nw, D.FV.p, D.yglob.p, done);
+  }
   mark("prolong");
   k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, z, D.comm ? nullptr : dot_with,
                                      D.comm ? nullptr : partials, done);
@@ -1888,6 +2356,32 @@ void Engine::recover(const double* u_interface, double* u_free) {
   CK(cudaStreamSynchronize(D.st));
 }
 
+namespace {
+// The persistent PCG kernel covers the latency-bound layout: one GPU, explicit
+// leaf operators, a small root inverse, no primal tree (BDDC_B200_PCG=graph
+// keeps the per-iteration CUDA graph).
+bool persistent_pcg(DeviceState& D) {
+  if (D.comm || !D.leaf_explicit || !D.root_inv || D.NR > 1024 || !D.tree.empty() || D.n_own == 0) return false;
+  if (const char* e = std::getenv("BDDC_B200_PCG"); e && std::string(e) == "graph") return false;
+  const std::size_t words = std::max<std::size_t>({(std::size_t)D.max_nB + D.max_rows, (std::size_t)D.max_PE,
+                                                   (std::size_t)D.NR, (std::size_t)D.max_M, 1});
+  const std::size_t smem = words * sizeof(double);
+  if (smem > 200 * 1024) return false;
+  if (smem != D.pcg_smem || D.pcg_grid == 0) {  // occupancy queried once per shared-memory size
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_pcg_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_persistent, 256, smem));
+    D.pcg_smem = smem;
+    D.pcg_grid = per_sm < 1 ? -1 : sm_count() * std::min(per_sm, 2);
+  }
+  return D.pcg_grid > 0;
+}
+}  // namespace
+
 PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool precond_residual) {
   DeviceState& D = *d_;
   if (!D.have_prec) throw Error(kError, "preconditioner not set up");
@@ -1961,6 +2455,81 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
       count_launch(2);
       CK(cudaMemcpyAsync(&hs, D.pst.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+    }
+  } else if (persistent_pcg(D)) {
+    // one cooperative launch for the whole iteration (k_pcg_persistent)
+    const int G = D.pcg_grid;
+    D.vp2.alloc(n);
+    D.vr2.alloc(n);
+    D.part3.alloc(3 * (size_t)G);
+    PcgPersist P{};
+    P.sd = D.subdesc.p;
+    P.xf = D.xf;
+    P.lx = D.leafx.p;
+    P.wpos = D.wpos.p;
+    P.nw = D.nw;
+    P.FVall = D.FV.p;
+    P.nfv = static_cast<long long>(D.FV.n);
+    P.ns = D.n_own;
+    P.nrb_schur = (D.max_nB + 63) / 64;
+    P.ncb_fwd = (D.max_NF + 63) / 64;
+    P.wsrc = D.wsrc.p;
+    P.item_sub = D.item_sub.p;
+    P.nitems = D.nitems;
+    P.yglob = D.yglob.p;
+    P.nrb_bwd = D.max_NF / kTile;
+    P.n_root = D.n_root;
+    P.NR = D.NR;
+    P.root_ptr = D.root_ptr.p;
+    P.root_src = D.root_src.p;
+    P.Rinv = D.Rinv.p;
+    P.fvsrc = D.FV2.p;
+    P.xroot = D.xroot2.p;
+    P.n = n;
+    P.icp = D.icopy_ptr.p;
+    P.icpos = D.icopy_pos.p;
+    P.WB = D.WB.p;
+    P.x = D.vx.p;
+    P.z = D.vz.p;
+    P.q = D.vq.p;
+    P.p[0] = D.vp.p;
+    P.p[1] = D.vp2.p;
+    P.r[0] = D.vr.p;
+    P.r[1] = D.vr2.p;
+    P.part = D.part3.p;
+    P.st = D.pst.p;
+    P.alphas = D.alphas.p;
+    P.betas = D.betas.p;
+    const char* pe = std::getenv("BDDC_B200_PROFILE");
+    const bool trace = pe && *pe && *pe != '0';
+    DBuf<unsigned long long> tr;
+    if (trace) {
+      tr.alloc(64 * 9);
+      tr.zero(st);
+      P.trace = tr.p;
+    }
+    void* args[] = {&P};
+    CK(cudaLaunchCooperativeKernel((void*)k_pcg_persistent, dim3(G), dim3(256), args, D.pcg_smem, st));
+    count_launch(1);
+    CK(cudaMemcpyAsync(&hs, D.pst.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (trace) {
+      std::vector<unsigned long long> t(64 * 9);
+      CK(cudaMemcpy(t.data(), tr.p, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      const char* names[8] = {"schur", "copysum_q", "alpha_restrict", "leaf_fwd", "root", "leaf_bwd", "prolong",
+                              "copysum_z"};
+      double acc[8] = {0};
+      const int its = std::min(hs.it, 64);
+      for (int i = 0; i < its; ++i) {
+        unsigned long long prev = t[i * 9 + 8];
+        for (int k = 0; k < 8; ++k) {
+          acc[k] += double(t[i * 9 + k] - prev) * 1e-3;
+          prev = t[i * 9 + k];
+        }
+      }
+      std::string line = "[profile] persistent pcg grid=" + std::to_string(G) + " us/iteration:";
+      for (int k = 0; k < 8; ++k) line += std::string(" ") + names[k] + "=" + std::to_string(acc[k] / std::max(its, 1));
+      std::fprintf(stderr, "%s\n", line.c_str());
     }
   } else {
     // capture one iteration as a graph (pcg.cpp:49-70)

@@ -1019,7 +1019,7 @@ std::shared_ptr<PairPrep> PairEngine::prepare(const ConstraintSet& cs, const Enr
     for (std::size_t b = 0; b < m.subs[s].boundary.size(); ++b) bpos[s][m.subs[s].boundary[b]] = static_cast<int>(b);
   }
   // pass 1: pair index spaces (independent per pair)
-#pragma omp parallel for schedule(dynamic, 8)
+#pragma omp parallel for schedule(dynamic, 8) if (np >= 256)
   for (int p = 0; p < np; ++p) hp[p].idx = build_pair_index(m, pairs[p].first, pairs[p].second);
   // pass 2: one kernel basis (QR) per shared glob
   std::vector<KernelCompact> kern(m.globs.size());
@@ -1029,7 +1029,7 @@ std::shared_ptr<PairPrep> PairEngine::prepare(const ConstraintSet& cs, const Enr
   std::vector<int> kern_list;
   for (std::size_t g = 0; g < m.globs.size(); ++g)
     if (kern_need[g]) kern_list.push_back(static_cast<int>(g));
-#pragma omp parallel for schedule(dynamic, 8)
+#pragma omp parallel for schedule(dynamic, 8) if (kern_list.size() >= 256)
   for (int q = 0; q < static_cast<int>(kern_list.size()); ++q) {
     const int g = kern_list[q];
     const int n = static_cast<int>(m.glob_dofs[g].size());
@@ -1043,7 +1043,7 @@ std::shared_ptr<PairPrep> PairEngine::prepare(const ConstraintSet& cs, const Enr
     }
   }
   // pass 3: positions, compact kernel columns, rigid modes
-#pragma omp parallel for schedule(dynamic, 8)
+#pragma omp parallel for schedule(dynamic, 8) if (np >= 256)
   for (int p = 0; p < np; ++p) {
     HostPair& h = hp[p];
     const PairIndex& x = h.idx;
@@ -1139,7 +1139,7 @@ std::shared_ptr<PairPrep> PairEngine::prepare(const ConstraintSet& cs, const Enr
       }
     }
     // side fronts from the hub: [U \ K | corner | shared] as indices into U
-#pragma omp parallel for schedule(dynamic, 8)
+#pragma omp parallel for schedule(dynamic, 8) if (np >= 256)
     for (int p = 0; p < np; ++p)
       for (int side = 0; side < 2; ++side) {
         HostPair& h = hp[p];
@@ -1425,7 +1425,11 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       // all in shared memory when it fits; otherwise only the 6n vectors, so that
       // several CTAs share an SM and hide the L2 latency of the packed matrix
       const long dyn = smem_ok ? need : 6L * maxn;
-      CK(cudaFuncSetAttribute(k_syevx, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+      static bool syevx_attr = false;
+      if (!syevx_attr) {
+        CK(cudaFuncSetAttribute(k_syevx, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+        syevx_attr = true;
+      }
       k_syevx<<<nb, 256, static_cast<int>(dyn * 8), st_>>>(dpd.p, static_cast<int>(dyn));
       prof.mark(smem_ok ? "syevx_smem" : "syevx_gmem");
     }
@@ -1590,7 +1594,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     std::vector<int> glist;
     for (std::size_t g = 0; g < by_g.size(); ++g)
       if (!by_g[g].empty()) glist.push_back(static_cast<int>(g));
-#pragma omp parallel for schedule(dynamic, 4)
+#pragma omp parallel for schedule(dynamic, 4) if (glist.size() >= 64)
     for (int q = 0; q < static_cast<int>(glist.size()); ++q) {
       const int g = glist[q];
       std::vector<const std::vector<double>*> ex;

@@ -333,7 +333,7 @@ void assemble(Model& md) {
   const int nsub = m.sub[0] * m.sub[1] * m.sub[2];
   md.subs.assign(nsub, Subdomain{});
   const int ln = epe + 1;  // local node grid per axis
-#pragma omp parallel for schedule(dynamic, 4)
+#pragma omp parallel for schedule(dynamic, 4) if (nsub >= 64)
   for (int s = 0; s < nsub; ++s) {
     Subdomain& S = md.subs[s];
     S.id = s;
@@ -1075,7 +1075,7 @@ ChangeOfVariables change_of_variables(const ConstraintSet& cs, const Model& md) 
     if (!bg[gi].empty()) constrained.push_back(static_cast<int>(gi));
   // the per-glob QRs are independent; groups keep glob order
   cov.transforms.resize(constrained.size());
-#pragma omp parallel for schedule(dynamic, 16)
+#pragma omp parallel for schedule(dynamic, 16) if (constrained.size() >= 512)
   for (int q = 0; q < static_cast<int>(constrained.size()); ++q) {
     const int gi = constrained[q];
     const int n = static_cast<int>(md.glob_dofs[gi].size());
