@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <map>
 #include <mutex>
+#include <string>
 
 namespace b200 {
 
@@ -784,6 +785,12 @@ void configure() {
   cudaFuncSetAttribute(k_front_forward_cl<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_backward_cl<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_backward_cl<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_forward_cl<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_backward_cl<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_forward_cl<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_backward_cl<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_front_forward_cl<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_front_backward_cl<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   g_smem_configured = 1;
 }
 
@@ -878,15 +885,18 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
 }
 
 namespace {
-// CTAs per front: a cluster of 4 or 2 when the fronts alone cannot fill the
-// GPU (about three CTAs per SM), else one.  BDDC_B200_SWEEP_CL=1|2|4 overrides.
-int sweep_cluster(int batch) {
+// CTAs per front: a cluster of 16, 8, 4 or 2 when the fronts alone cannot fill
+// the GPU (about three CTAs per SM), else one.  BDDC_B200_SWEEP_CL=1|2|4|8|16
+// overrides.
+int sweep_cluster(int batch, int max_cl) {
   const char* env = std::getenv("BDDC_B200_SWEEP_CL");
   if (env && *env) {
     const int c = std::atoi(env);
-    if (c == 1 || c == 2 || c == 4) return c;
+    if (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) return c;
   }
   const long cap = 3L * sm_count();
+  if (max_cl >= 16 && (long)batch * 16 <= cap) return 16;
+  if (max_cl >= 8 && (long)batch * 8 <= cap) return 8;
   if ((long)batch * 4 <= cap) return 4;
   if ((long)batch * 2 <= cap) return 2;
   return 1;
@@ -949,9 +959,11 @@ void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t 
     count_launch(1);
     return;
   }
-  const int cl = sweep_cluster(batch);
+  const int cl = sweep_cluster(batch, 4);  // measured: wider forward clusters are slower
   const size_t smem = (max_n + 64 * 3) * sizeof(double);
-  if (cl == 4) launch_cluster(k_front_forward_cl<4>, 4, batch, smem, stream, d_descs, done);
+  if (cl == 16) launch_cluster(k_front_forward_cl<16>, 16, batch, smem, stream, d_descs, done);
+  else if (cl == 8) launch_cluster(k_front_forward_cl<8>, 8, batch, smem, stream, d_descs, done);
+  else if (cl == 4) launch_cluster(k_front_forward_cl<4>, 4, batch, smem, stream, d_descs, done);
   else if (cl == 2) launch_cluster(k_front_forward_cl<2>, 2, batch, smem, stream, d_descs, done);
   else k_front_forward<256><<<batch, 256, (max_n + 64) * sizeof(double), stream>>>(d_descs, done);
   count_launch(1);
@@ -965,9 +977,11 @@ void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t
     count_launch(1);
     return;
   }
-  const int cl = sweep_cluster(batch);
-  const size_t smem = (64 * LDS + max_n + 64 + 2 * 4 * 64) * sizeof(double);
-  if (cl == 4) launch_cluster(k_front_backward_cl<4>, 4, batch, smem, stream, d_descs, done);
+  const int cl = sweep_cluster(batch, 16);
+  const size_t smem = (64 * LDS + max_n + 64 + 2 * 16 * 64) * sizeof(double);
+  if (cl == 16) launch_cluster(k_front_backward_cl<16>, 16, batch, smem, stream, d_descs, done);
+  else if (cl == 8) launch_cluster(k_front_backward_cl<8>, 8, batch, smem, stream, d_descs, done);
+  else if (cl == 4) launch_cluster(k_front_backward_cl<4>, 4, batch, smem, stream, d_descs, done);
   else if (cl == 2) launch_cluster(k_front_backward_cl<2>, 2, batch, smem, stream, d_descs, done);
   else k_front_backward_cl<1><<<batch, 256, smem, stream>>>(d_descs, done);
   count_launch(1);

@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kRed = 256;  // blocks of the deterministic dot-product reductions
 constexpr int kRootInverseMax = 12288;  // explicit root inverse up to this padded size (2.4 GB front)
-constexpr int kTreeApplies = 60;      // preconditioner applies assumed when choosing the primal tree depth
+constexpr int kTreeApplies = 40;      // preconditioner applies assumed when choosing the primal tree depth
 
 inline int rup(int v, int m) { return (v + m - 1) / m * m; }
 

@@ -311,8 +311,12 @@ double coarse_tree_cost(const CoarseTree& t, int applies, int root_inverse_max) 
   for (const auto& L : t.levels) steps += L.max_PE / kT;
   const double setup = t.flops / 20e12 + steps * 3 * 6e-6;
   const double top_bytes = n * n * 8.0;
-  const double per_apply = (t.apply_bytes - top_bytes) / 3e12 + top_bytes / (inv ? 4e12 : 0.8e12) +
-                           static_cast<double>(t.levels.size()) * 3 * 6e-6;
+  // a level's two sweeps are a chain of 64-row block steps over few fronts:
+  // about 15 us per block step plus the gather (measured, cfg3-5)
+  double level_latency = 0;
+  for (const auto& L : t.levels) level_latency += 8e-6 + 15e-6 * (L.max_PE / kT);
+  const double per_apply =
+      (t.apply_bytes - top_bytes) / 3e12 + top_bytes / (inv ? 4e12 : 0.8e12) + level_latency;
   return setup + applies * per_apply;
 }
 
