@@ -67,6 +67,25 @@ FP64_PEAK_TFLOPS = 35.47  # cuBLAS DGEMM 8192^3 on this pool's B200 (profiles/r0
 FP64_DMMA_PEAK_TFLOPS = 36.9  # mma.sync m16n8k16 f64 microbenchmark, same file
 
 
+def measured_traffic(config):
+    """DRAM bytes (read + write) of one leaf factorization and of one Schur +
+    preconditioner apply, from the ncu capture committed under profiles/
+    (tools/ncu_traffic.py); {} when this config was not captured."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as f:
+            data = json.load(f)
+    except OSError:
+        return {}
+    out = {}
+    for phase in ("leaf", "apply"):
+        rec = data.get("cfg%d_%s" % (config, phase))
+        if rec:
+            out[phase] = rec["dram_bytes_read"] + rec["dram_bytes_write"]
+    if out:
+        out["source"] = "profiles/r01_traffic.json (ncu dram__bytes_{read,write}.sum over one phase)"
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region."""
 
@@ -293,9 +312,10 @@ def main():
     lf_t = statistics.median(s["leaf_factor_seconds"] for s in steps)
     lf_flops = last["leaf_flops"]
     achieved = lf_flops / lf_t / 1e12
+    traffic = measured_traffic(args.config) if world == 1 else {}
     roof = {"kernel": "partial_cholesky (leaf fronts: A_II eliminated, S_s formed)", "bound": "tensor",
             "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic.get("leaf"),
             "peak_source": "measured cuBLAS DGEMM (MEASURED_PEAKS.json has bf16 only)",
             "flops_per_launch": lf_flops, "seconds_per_launch": lf_t,
             "share_of_step": lf_t / sec_per_step}
@@ -307,8 +327,11 @@ def main():
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     roof_pcg = {"kernel": "PCG iteration (S_s GEMV + leaf sweeps + root apply)", "bound": "hbm",
                 "achieved": pcg_achieved, "peak": hbm_peak, "unit": "GB/s", "frac": pcg_achieved / hbm_peak,
-                "traffic": None, "bytes_per_iteration": tm["pcg_bytes_per_iteration"], "iterations": pcg_it,
+                "traffic": traffic.get("apply"), "bytes_per_iteration": tm["pcg_bytes_per_iteration"],
+                "iterations": pcg_it,
                 "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind}
+    if traffic:
+        roof["traffic_source"] = roof_pcg["traffic_source"] = traffic["source"]
     cpu = None
     if not args.no_cpu_baseline and world == 1 and args.config <= 2:
         dt, _, _ = run_oracle_step(args.config, args.seed)

@@ -2580,12 +2580,15 @@ StepOut Engine::step(const StepSpec& sp, ConstraintSet& cs, double* u_free_host)
   const long long l0 = launch_count();
   cudaStream_t st = D.st;
   CK(cudaStreamSynchronize(st));
+  HostTimer ht("step");
   CK(cudaEventRecord(D.s0, st));
   if (sp.e2e) out.h2d_bytes = upload_inputs();
   // the leaf factorization runs on the device while the host builds the base
   // constraints and prepares the face-pair problems
   analysis_launch();
+  ht.mark("launch");
   cs = arithmetic_constraints(m_, sp.edges, sp.faces);
+  ht.mark("base_constraints");
   EnrichOptions o;
   o.tau = sp.tau;
   o.max_vectors = sp.max_vectors;
@@ -2594,17 +2597,22 @@ StepOut Engine::step(const StepSpec& sp, ConstraintSet& cs, double* u_free_host)
   const bool adaptive = sp.adaptive || sp.fixed_count >= 0;
   std::shared_ptr<PairPrep> prep;
   if (adaptive) prep = D.pairs.prepare(cs, o);
+  ht.mark("pair_prep");
   analysis_finish();
+  ht.mark("analysis_wait");
   if (adaptive) {
     CK(cudaEventRecord(D.e0, st));
     out.omega_tilde = D.pairs.enrich(cs, o, prep).omega_tilde;
     CK(cudaEventRecord(D.e1, st));
     times_.eigen = elapsed(D.e0, D.e1);
   }
+  ht.mark("eigen");
   out.constraint_rows = cs.row_count(m_);
   set_constraints(cs);
+  ht.mark("set_constraints");
   CK(cudaEventRecord(D.s1, st));
   out.pcg = pcg(nullptr, nullptr, sp.tol, sp.max_it, false);
+  ht.mark("pcg");
   if (sp.e2e) {
     if (D.ufree.n == 0) D.ufree.alloc(std::max<i64>(m_.free_count, 1));
     recover_device(D.vx.p, D.ufree.p);
