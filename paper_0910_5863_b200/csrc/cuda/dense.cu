@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <map>
 #include <mutex>
+#include <stdexcept>
 #include <string>
 
 namespace b200 {
@@ -916,7 +917,12 @@ void launch_cluster(K kern, int cl, int batch, size_t smem, cudaStream_t stream,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, d, done);
+  if (cudaLaunchKernelEx(&cfg, kern, d, done) != cudaSuccess) {
+    // the device could not place a cluster this wide (large clusters are not
+    // portable): clear the error; the caller retries narrower
+    (void)cudaGetLastError();
+    throw std::runtime_error("cluster launch");
+  }
 }
 }  // namespace
 
@@ -977,11 +983,21 @@ void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t
     count_launch(1);
     return;
   }
-  const int cl = sweep_cluster(batch, 16);
+  static int max_cl = 16;  // lowered once if the device refuses a cluster width
+  int cl = sweep_cluster(batch, max_cl);
   const size_t smem = (64 * LDS + max_n + 64 + 2 * 16 * 64) * sizeof(double);
-  if (cl == 16) launch_cluster(k_front_backward_cl<16>, 16, batch, smem, stream, d_descs, done);
-  else if (cl == 8) launch_cluster(k_front_backward_cl<8>, 8, batch, smem, stream, d_descs, done);
-  else if (cl == 4) launch_cluster(k_front_backward_cl<4>, 4, batch, smem, stream, d_descs, done);
+  while (cl >= 8) {
+    try {
+      if (cl == 16) launch_cluster(k_front_backward_cl<16>, 16, batch, smem, stream, d_descs, done);
+      else launch_cluster(k_front_backward_cl<8>, 8, batch, smem, stream, d_descs, done);
+      count_launch(1);
+      return;
+    } catch (const std::runtime_error&) {
+      max_cl = cl / 2;
+      cl = sweep_cluster(batch, max_cl);
+    }
+  }
+  if (cl == 4) launch_cluster(k_front_backward_cl<4>, 4, batch, smem, stream, d_descs, done);
   else if (cl == 2) launch_cluster(k_front_backward_cl<2>, 2, batch, smem, stream, d_descs, done);
   else k_front_backward_cl<1><<<batch, 256, smem, stream>>>(d_descs, done);
   count_launch(1);

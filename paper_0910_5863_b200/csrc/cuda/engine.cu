@@ -49,6 +49,9 @@ struct AsmDesc {
   const int* lnode;  // local node grid (x fastest) * nc + c -> local dof or -1
   const int* pos;    // local dof -> front position
   int ld, nI, PI, nB, i0, j0, k0;
+  int* ipos;         // front position -> local dof, or -1 (padding)
+  int* dofq;         // local dof -> node grid index * nc + component
+  int lnode_n, dim;  // entries of lnode, local dofs
 };
 struct AsmMesh {
   const double* ke;      // reference element matrices, ed x ed row-major each
@@ -57,49 +60,88 @@ struct AsmMesh {
   int ne0, ne1, epe, nc;
 };
 
-// Thread per stiffness entry (node, component, neighbour slot, component): the
-// entry of the (lower, higher) local dof pair summed over the elements holding
-// both nodes in the host's element order (k, j, i), multiply and add rounded
-// separately, so the front equals the host CSR bitwise.  Padding rows get a
-// unit diagonal.
-__global__ void k_assemble_front(const AsmDesc* ds, AsmMesh mm) {
+// Inverse maps of the front layout (per substructure, blockIdx.y): position ->
+// local dof (ipos, preset to -1) and local dof -> node grid slot (dofq).
+__global__ void k_front_maps(const AsmDesc* ds) {
+  const AsmDesc d = ds[blockIdx.y];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < d.lnode_n + d.dim; t += gridDim.x * blockDim.x) {
+    if (t < d.lnode_n) {
+      const int l = d.lnode[t];
+      if (l >= 0) d.dofq[l] = t;
+    } else {
+      const int l = t - d.lnode_n;
+      d.ipos[d.pos[l]] = l;
+    }
+  }
+}
+
+// Dense leaf fronts (assemble.cpp:202-258): one thread per entry of the
+// block-lower triangle (tiles (a, b), a >= b, the diagonal tiles in full) --
+// the only part of a leaf front the factorization and the sweeps read.  Every
+// such entry is written (stiffness value, 0, or 1 on a padding diagonal), so
+// the arena needs no memset.  A stiffness entry is the sum over the elements
+// holding both nodes in the host's element order (k, j, i) of the reference
+// element matrix entry times the element scale, multiply and add rounded
+// separately: the front equals the host CSR bitwise.
+__global__ void __launch_bounds__(256) k_assemble_dense(const AsmDesc* ds, AsmMesh mm) {
   const AsmDesc d = ds[blockIdx.y];
   const int nc = mm.nc, ln = mm.epe + 1, ed = 8 * nc;
-  const long nent = (long)ln * ln * ln * nc * 27 * nc;
+  const long nt = d.ld / 64;
+  const long ntile = nt * (nt + 1) / 2;
   const int vtx[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // (dx + 2 dy + 4 dz) -> VTK vertex
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < nent + d.ld; t += (long)gridDim.x * blockDim.x) {
-    if (t >= nent) {
-      const int r = static_cast<int>(t - nent);
-      if ((r >= d.nI && r < d.PI) || r >= d.PI + d.nB) d.a[(size_t)r * d.ld + r] = 1.0;
-      continue;
+  // per tile: local dof and (i, j, k, component) of its 64 rows and 64 columns
+  __shared__ int dof_s[2][64];
+  __shared__ int4 crd_s[2][64];
+  for (long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    int ta = static_cast<int>((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
+    while ((long)ta * (ta + 1) / 2 > tile) --ta;
+    while ((long)(ta + 1) * (ta + 2) / 2 <= tile) ++ta;
+    const int tb = static_cast<int>(tile - (long)ta * (ta + 1) / 2);
+    if (threadIdx.x < 128) {
+      const int w = threadIdx.x >> 6, idx = threadIdx.x & 63;
+      const int l = d.ipos[(w ? tb : ta) * 64 + idx];
+      dof_s[w][idx] = l;
+      if (l >= 0) {
+        const int g = d.dofq[l], q = g / nc;
+        crd_s[w][idx] = make_int4(q % ln, (q / ln) % ln, q / (ln * ln), g % nc);
+      }
     }
-    const int cb = static_cast<int>(t % nc);
-    long u = t / nc;
-    const int slot = static_cast<int>(u % 27);
-    u /= 27;
-    const int ca = static_cast<int>(u % nc);
-    const int q = static_cast<int>(u / nc);
-    const int li = q % ln, lj = (q / ln) % ln, lk = q / (ln * ln);
-    const int ci = li + slot % 3 - 1, cj = lj + (slot / 3) % 3 - 1, ck = lk + slot / 9 - 1;
-    if (ci < 0 || cj < 0 || ck < 0 || ci >= ln || cj >= ln || ck >= ln) continue;
-    const int r = d.lnode[q * nc + ca];
-    const int c = d.lnode[((ck * ln + cj) * ln + ci) * nc + cb];
-    if (r < 0 || c < 0) continue;
-    const bool lo = r <= c;
-    const int pi = lo ? li : ci, pj = lo ? lj : cj, pk = lo ? lk : ck, pc = lo ? ca : cb;
-    const int qi = lo ? ci : li, qj = lo ? cj : lj, qk = lo ? ck : lk, qc = lo ? cb : ca;
-    double s = 0.0;
-    for (int ek = max(max(pk, qk) - 1, 0); ek <= min(min(pk, qk), mm.epe - 1); ++ek)
-      for (int ej = max(max(pj, qj) - 1, 0); ej <= min(min(pj, qj), mm.epe - 1); ++ej)
-        for (int ei = max(max(pi, qi) - 1, 0); ei <= min(min(pi, qi), mm.epe - 1); ++ei) {
-          const int e = ((d.k0 + ek) * mm.ne1 + d.j0 + ej) * mm.ne0 + d.i0 + ei;
-          const int va = vtx[(pi - ei) + 2 * (pj - ej) + 4 * (pk - ek)];
-          const int vb = vtx[(qi - ei) + 2 * (qj - ej) + 4 * (qk - ek)];
-          const double kv = mm.ke[(size_t)mm.eke[e] * ed * ed + (va * nc + pc) * ed + vb * nc + qc];
-          const double sc = mm.escale ? mm.escale[e] : 1.0;
-          s = __dadd_rn(s, sc == 1.0 ? kv : __dmul_rn(sc, kv));
+    __syncthreads();
+    double* out = d.a + (size_t)(tb * 64) * d.ld + ta * 64;
+    for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
+      const int i = e & 63, j = e >> 6;
+      const int dr = dof_s[0][i], dc = dof_s[1][j];
+      double s = 0.0;
+      if (dr < 0 || dc < 0) {
+        s = (ta == tb && i == j) ? 1.0 : 0.0;
+      } else {
+        const int4 a = crd_s[0][i], b = crd_s[1][j];
+        if (abs(a.x - b.x) <= 1 && abs(a.y - b.y) <= 1 && abs(a.z - b.z) <= 1) {
+          const bool lo = dr <= dc;
+          const int4 P = lo ? a : b, Q = lo ? b : a;
+          for (int ek = max(max(P.z, Q.z) - 1, 0); ek <= min(min(P.z, Q.z), mm.epe - 1); ++ek)
+            for (int ej = max(max(P.y, Q.y) - 1, 0); ej <= min(min(P.y, Q.y), mm.epe - 1); ++ej)
+              for (int ei = max(max(P.x, Q.x) - 1, 0); ei <= min(min(P.x, Q.x), mm.epe - 1); ++ei) {
+                const int el = ((d.k0 + ek) * mm.ne1 + d.j0 + ej) * mm.ne0 + d.i0 + ei;
+                const int va = vtx[(P.x - ei) + 2 * (P.y - ej) + 4 * (P.z - ek)];
+                const int vb = vtx[(Q.x - ei) + 2 * (Q.y - ej) + 4 * (Q.z - ek)];
+                const double kv = mm.ke[(size_t)mm.eke[el] * ed * ed + (va * nc + P.w) * ed + vb * nc + Q.w];
+                const double sc = mm.escale ? mm.escale[el] : 1.0;
+                s = __dadd_rn(s, sc == 1.0 ? kv : __dmul_rn(sc, kv));
+              }
         }
-    d.a[(size_t)d.pos[c] * d.ld + d.pos[r]] = s;
+      }
+      out[(size_t)j * d.ld + i] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// upper triangle := lower (leaf_front's full copy of one front for the tests)
+__global__ void k_mirror_upper(double* a, int ld) {
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < (long)ld * ld; t += (long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(t % ld), c = static_cast<int>(t / ld);
+    if (r < c) a[t] = a[(size_t)r * ld + c];
   }
 }
 
@@ -1097,7 +1139,7 @@ struct DeviceState {
     std::vector<double> ke, escale, mv, bw;
   } h;
   DBuf<double> M, DinvM, S, MV, MV0, WB;
-  DBuf<int> minfo, asm_lnode, asm_pos, asm_eke;
+  DBuf<int> minfo, asm_lnode, asm_pos, asm_eke, asm_ipos, asm_dofq;
   DBuf<double> asm_ke, asm_escale;
   DBuf<AsmDesc> asmdesc;
   AsmMesh asm_mesh{};
@@ -1326,7 +1368,8 @@ void Engine::prepare() {
   D.WB.alloc(std::max<long long>(wbo, 1));
   // host staging of the assembly inputs: element data, local numbering and
   // dense positions per substructure, loads in front layout
-  std::vector<long long> lnode_off(ns, 0), pos_off(ns, 0);
+  std::vector<long long> lnode_off(ns, 0), pos_off(ns, 0), ipos_off(ns, 0);
+  long long ipos_n = 0;
   auto& H = D.h;
   H.lnode.clear();
   H.pos.clear();
@@ -1339,6 +1382,8 @@ void Engine::prepare() {
     for (int r = 0; r < D.nI[s]; ++r) p[S.interior[r]] = r;
     for (int b = 0; b < D.nB[s]; ++b) p[S.boundary[b]] = D.PI[s] + b;
     H.pos.insert(H.pos.end(), p.begin(), p.end());
+    ipos_off[s] = ipos_n;
+    ipos_n += D.NM[s];
   }
   H.ke.clear();
   for (const auto& k : m.ke_ref) H.ke.insert(H.ke.end(), k.begin(), k.end());
@@ -1376,6 +1421,8 @@ void Engine::prepare() {
   }
   D.asm_lnode.alloc(std::max<std::size_t>(H.lnode.size(), 1));
   D.asm_pos.alloc(std::max<std::size_t>(H.pos.size(), 1));
+  D.asm_ipos.alloc(std::max<long long>(ipos_n, 1));
+  D.asm_dofq.alloc(std::max<std::size_t>(H.pos.size(), 1));
   D.asm_eke.alloc(std::max<std::size_t>(H.eke.size(), 1));
   D.asm_ke.alloc(std::max<std::size_t>(H.ke.size(), 1));
   D.asm_escale.alloc(std::max<std::size_t>(H.escale.size(), 1));
@@ -1397,7 +1444,8 @@ void Engine::prepare() {
     const int s = D.act[q];
     const Subdomain& S = m.subs[s];
     ad.push_back(AsmDesc{D.M.p + D.m_off[s], D.asm_lnode.p + lnode_off[s], D.asm_pos.p + pos_off[s], D.NM[s], D.nI[s],
-                         D.PI[s], D.nB[s], S.origin[0], S.origin[1], S.origin[2]});
+                         D.PI[s], D.nB[s], S.origin[0], S.origin[1], S.origin[2], D.asm_ipos.p + ipos_off[s],
+                         D.asm_dofq.p + pos_off[s], static_cast<int>(S.lnode.size()), S.dim()});
     fd.push_back(FrontDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.NM[s], D.PI[s], D.minfo.p + q, 0});
     sv.push_back(SolveDesc{D.M.p + D.m_off[s], D.DinvM.p + D.dm_off[s], D.MV.p + D.mv_off[s], D.NM[s], D.PI[s],
                            nullptr, nullptr});
@@ -1457,6 +1505,23 @@ double Engine::upload_inputs() {
   return bytes;
 }
 
+namespace {
+// Leaf fronts from the reference element matrices: the
+// inverse layout maps, then every block-lower entry of every front.
+void assemble_fronts(DeviceState& D) {
+  const int na = D.n_act;
+  if (!na) return;
+  cudaStream_t st = D.st;
+  CK(cudaMemsetAsync(D.asm_ipos.p, 0xff, D.asm_ipos.n * sizeof(int), st));
+  k_front_maps<<<dim3(16, na), 256, 0, st>>>(D.asmdesc.p);
+  long tiles = 0;
+  for (int s : D.act) tiles = std::max<long>(tiles, (long)(D.NM[s] / 64) * (D.NM[s] / 64 + 1) / 2);
+  const int bx = static_cast<int>(std::max<long>(1, std::min<long>(tiles, (16L * sm_count() + na - 1) / na)));
+  k_assemble_dense<<<dim3(bx, na), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
+  count_launch(2);
+}
+}  // namespace
+
 void Engine::analysis() {
   analysis_launch();
   analysis_finish();
@@ -1468,12 +1533,8 @@ void Engine::analysis_launch() {
   const int na = D.n_act;
   cudaStream_t st = D.st;
   CK(cudaEventRecord(D.e0, st));
-  D.M.zero(st);
   D.minfo.zero(st);
-  if (na) {
-    k_assemble_front<<<dim3(64, na), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
-    count_launch(1);
-  }
+  assemble_fronts(D);
   CK(cudaGetLastError());
   CK(cudaEventRecord(D.ef0, st));
   partial_cholesky(D.mfront.p, na, D.max_NM, D.max_PI, D.max_PB, st);
@@ -2276,8 +2337,8 @@ void Engine::leaf_front(int s, std::vector<double>* out, std::vector<int>* pos, 
   pos->assign(D.h.pos.begin() + off, D.h.pos.begin() + off + S.dim());
   if (!out) return;
   cudaStream_t st = D.st;
-  D.M.zero(st);
-  k_assemble_front<<<dim3(64, D.n_act), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
+  assemble_fronts(D);
+  k_mirror_upper<<<256, 256, 0, st>>>(D.M.p + D.m_off[s], D.NM[s]);
   count_launch(1);
   CK(cudaGetLastError());
   out->resize((size_t)D.NM[s] * D.NM[s]);
