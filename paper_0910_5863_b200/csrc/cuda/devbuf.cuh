@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -71,7 +72,8 @@ class StageArena {
     std::size_t& mine = pair ? pair_ : prec_;
     if (n > mine) mine = n;
     bool split = prec_ + pair_ <= buf_.cap;  // both fit already: no query
-    if (!split) {
+    const bool fits_overlaid = (prec_ > pair_ ? prec_ : pair_) <= buf_.cap;
+    if (!split && !fits_overlaid) {  // the arena must grow: side by side if the device holds both
       std::size_t fr = 0, tot = 0;
       if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 0;
       const double room = double(buf_.cap) * sizeof(double) + double(fr) - 1.5e9;
@@ -127,32 +129,55 @@ class UploadBatch {
   }
   template <class T>
   void add(DBuf<T>& target, const std::vector<T>& v) {
+    if (items_.empty() && ev_) CK(cudaEventSynchronize(ev_));  // the previous copy out of the host blob is done
     const std::size_t n = v.empty() ? 1 : v.size();
-    const std::size_t off = stage_.size(), bytes = n * sizeof(T);
-    stage_.resize(off + (bytes + 255) / 256 * 256, 0);
-    if (!v.empty()) std::memcpy(stage_.data() + off, v.data(), bytes);
-    items_.push_back(Item{reinterpret_cast<void*>(&target), off, n, &UploadBatch::bind<T>});
+    const std::size_t bytes = n * sizeof(T), span = (bytes + 255) / 256 * 256;
+    reserve(used_ + span);
+    if (v.empty())
+      std::memset(host_ + used_, 0, bytes);
+    else
+      copy(host_ + used_, v.data(), bytes);
+    items_.push_back(Item{reinterpret_cast<void*>(&target), used_, n, &UploadBatch::bind<T>});
+    used_ += span;
   }
   void flush(cudaStream_t st) {
     if (items_.empty()) return;
-    const std::size_t used = stage_.size();
-    if (ev_) CK(cudaEventSynchronize(ev_));  // the previous copy out of the host blob is done
-    if (used > host_cap_) {
-      if (host_) CK(cudaFreeHost(host_));
-      host_cap_ = used + used / 4;
-      CK(cudaHostAlloc(reinterpret_cast<void**>(&host_), host_cap_, cudaHostAllocDefault));
-    }
-    dev_.alloc(used);
-    std::memcpy(host_, stage_.data(), used);
-    CK(cudaMemcpyAsync(dev_.p, host_, used, cudaMemcpyHostToDevice, st));
+    dev_.alloc(used_);
+    CK(cudaMemcpyAsync(dev_.p, host_, used_, cudaMemcpyHostToDevice, st));
     if (!ev_) CK(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
     CK(cudaEventRecord(ev_, st));
     for (const Item& it : items_) it.bind_fn(it.target, dev_.p + it.off, it.count);
     items_.clear();
-    stage_.clear();
+    used_ = 0;
   }
 
  private:
+  void reserve(std::size_t need) {
+    if (need <= host_cap_) return;
+    const std::size_t cap = need + need / 2;
+    char* h = nullptr;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h), cap, cudaHostAllocDefault));
+    if (host_) {
+      std::memcpy(h, host_, used_);
+      CK(cudaFreeHost(host_));
+    }
+    host_ = h;
+    host_cap_ = cap;
+  }
+  // large arrays are copied by several threads (page-locked destination)
+  static void copy(char* dst, const void* src, std::size_t bytes) {
+    const std::size_t chunk = std::size_t(1) << 20;
+    if (bytes < 4 * chunk) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    const long nch = static_cast<long>((bytes + chunk - 1) / chunk);
+#pragma omp parallel for schedule(static)
+    for (long c = 0; c < nch; ++c) {
+      const std::size_t o = c * chunk, len = std::min(chunk, bytes - o);
+      std::memcpy(dst + o, static_cast<const char*>(src) + o, len);
+    }
+  }
   template <class T>
   static void bind(void* target, char* p, std::size_t n) {
     static_cast<DBuf<T>*>(target)->view(reinterpret_cast<T*>(p), n);
@@ -163,8 +188,7 @@ class UploadBatch {
     void (*bind_fn)(void*, char*, std::size_t);
   };
   std::vector<Item> items_;
-  std::vector<char> stage_;
-  std::size_t host_cap_ = 0;
+  std::size_t used_ = 0, host_cap_ = 0;
   char* host_ = nullptr;
   cudaEvent_t ev_ = nullptr;
   DBuf<char> dev_;

@@ -1818,18 +1818,25 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       if (env && *env) {
         depth = std::max(0, std::min(std::atoi(env), maxd));
       } else {
-        double best = 0;
+        // candidate depths planned symbolically in parallel, the cheapest kept
+        std::vector<double> cost(maxd + 1);
+        std::vector<CoarseTree> cand(maxd + 1);
+#pragma omp parallel for schedule(static, 1) if (no >= 256)
         for (int d = 0; d <= maxd; ++d) {
-          const CoarseTree t = plan_coarse_tree(leaves, m.mesh.sub, D.n_primal, d, kRootInverseMax, true);
-          const double c = coarse_tree_cost(t, kTreeApplies, kRootInverseMax);
-          if (d == 0 || c < best) {
-            best = c;
-            depth = d;
-          }
+          cand[d] = plan_coarse_tree(leaves, m.mesh.sub, D.n_primal, d, kRootInverseMax, true);
+          cost[d] = coarse_tree_cost(cand[d], kTreeApplies, kRootInverseMax);
         }
+        for (int d = 1; d <= maxd; ++d)
+          if (cost[d] < cost[depth]) depth = d;
+        plan = std::move(cand[depth]);
+        ht.mark("tree_depths");
       }
     }
-    plan = plan_coarse_tree(leaves, m.mesh.sub, D.n_primal, depth, kRootInverseMax);
+    if (plan.leaf_box.empty() && plan.top.empty())
+      plan = plan_coarse_tree(leaves, m.mesh.sub, D.n_primal, depth, kRootInverseMax);
+    else
+      complete_coarse_tree(plan, leaves);
+    ht.mark("tree_plan");
     for (int q = 0; q < no; ++q) {
       const int s = D.own[q];
       for (int c = 0; c < D.nC[s]; ++c) cmap[cmap_off[s] + c] = plan.leaf_cmap[q][c];
@@ -1886,14 +1893,25 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     // position-parallel restrict / prolong: per boundary copy of the owned
     // substructures, the leaf-vector index it copies or the constrained item
     // it takes (prolong_body's two cases)
-    std::vector<int2> wp;
-    std::vector<int> wsrc, isub(item_inst.size());
+    // boundary copies in owned order; the (substructure, position) list is
+    // fixed by the model, so it is uploaded once
+    std::vector<long long> w0(no + 1, 0);
+    for (int q = 0; q < no; ++q) w0[q + 1] = w0[q] + D.nB[D.own[q]];
+    if (D.nw != static_cast<int>(w0[no]) || D.wpos.n == 0 || !D.wpos.owned) {
+      std::vector<int2> wp(w0[no]);
+      for (int q = 0; q < no; ++q)
+        for (int b = 0; b < D.nB[D.own[q]]; ++b) wp[w0[q] + b] = make_int2(q, b);
+      D.wpos.release();
+      D.wpos.upload(wp, st);
+      D.nw = static_cast<int>(w0[no]);
+    }
+    std::vector<int> wsrc(std::max<long long>(w0[no], 1)), isub(item_inst.size());
+#pragma omp parallel for schedule(dynamic, 16) if (no >= 64)
     for (int q = 0; q < no; ++q) {
       const int s = D.own[q];
       for (int k = item_ptr[q]; k < item_ptr[q + 1]; ++k) isub[k] = q;
       for (int b = 0; b < D.nB[s]; ++b) {
         const long long w = D.wb_off[s] + b;
-        wp.push_back(make_int2(q, b));
         const int inst = bglob[w];
         int src = static_cast<int>(D.fv_off[s]) + posF[w];
         if (inst >= 0) {
@@ -1904,11 +1922,9 @@ void Engine::set_constraints(const ConstraintSet& cs) {
           else
             src = static_cast<int>(D.fv_off[s]) + posF[D.wb_off[s] + tpos[inst_pos[inst] + i]];
         }
-        wsrc.push_back(src);
+        wsrc[w0[q] + b] = src;
       }
     }
-    UA.add(D.wpos, wp);
-    D.nw = static_cast<int>(wp.size());
     up_i(D.wsrc, wsrc);
     up_i(D.item_sub, isub);
     D.nitems = static_cast<int>(item_inst.size());

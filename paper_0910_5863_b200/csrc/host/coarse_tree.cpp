@@ -70,20 +70,6 @@ bool inside(const Box& b, const int lo[3], const int hi[3]) {
   return true;
 }
 
-int row_of(const CoarseTree::Front& f, int k) {
-  auto it = std::lower_bound(f.own.begin(), f.own.end(), k);
-  if (it != f.own.end() && *it == k) return static_cast<int>(it - f.own.begin());
-  it = std::lower_bound(f.upd.begin(), f.upd.end(), k);
-  if (it != f.upd.end() && *it == k) return f.PE + static_cast<int>(it - f.upd.begin());
-  throw std::logic_error("coarse tree: unknown missing from its parent front");
-}
-
-int top_index(const std::vector<int>& top, int k) {
-  auto it = std::lower_bound(top.begin(), top.end(), k);
-  if (it == top.end() || *it != k) throw std::logic_error("coarse tree: unknown missing from the top front");
-  return static_cast<int>(it - top.begin());
-}
-
 // gather CSR from (position, child, cidx, src) tuples produced in child order
 void to_csr(std::size_t npos, const std::vector<long long>& pos, const std::vector<int>& ch,
             const std::vector<int>& ci, const std::vector<long long>& sr, std::vector<int>& ptr,
@@ -228,33 +214,78 @@ CoarseTree plan_coarse_tree(const std::vector<CoarseLeaf>& leaves, const int lat
     L.d_size = dof;
     L.cmap.assign(co, -1);
   }
-  if (symbolic) {  // sizes and costs only (depth selection)
+  {
     const double n = static_cast<double>(t.top.size());
     const bool inv = rup(std::max<int>(static_cast<int>(t.top.size()), 1)) <= root_inverse_max;
     t.flops += inv ? n * n * n : n * n * n / 3.0;
     t.apply_bytes += n * n * 8.0;
-    return t;
   }
-  // forward gathers (children in ascending order) and backward maps
-  auto leaf_parent_pos = [&](int i, int k) -> long long {
-    if (depth == 0) return top_index(t.top, k);
-    const CoarseTree::Front& f = t.levels[0].fronts[leaf_box[i]];
-    return f.fv_off + row_of(f, k);
+  t.leaf_box = std::move(leaf_box);
+  t.n_primal = n_primal;
+  if (!symbolic) complete_coarse_tree(t, leaves);
+  return t;
+}
+
+void complete_coarse_tree(CoarseTree& t, const std::vector<CoarseLeaf>& leaves) {
+  const int depth = t.depth, nl = static_cast<int>(leaves.size()), n_primal = t.n_primal;
+  const std::vector<int>& leaf_box = t.leaf_box;
+  // forward gathers and backward maps, parent by parent: the parent's rows are
+  // stamped into a direct map, then its children are visited in ascending
+  // order, so every position's entry list is ascending by child
+  std::vector<int> rowmap(n_primal, -1), rstamp(n_primal, -1);
+  int pstamp = 0;
+  auto stamp_front = [&](const CoarseTree::Front& f) {
+    ++pstamp;
+    for (std::size_t i = 0; i < f.own.size(); ++i) {
+      rowmap[f.own[i]] = static_cast<int>(i);
+      rstamp[f.own[i]] = pstamp;
+    }
+    for (std::size_t i = 0; i < f.upd.size(); ++i) {
+      rowmap[f.upd[i]] = f.PE + static_cast<int>(i);
+      rstamp[f.upd[i]] = pstamp;
+    }
+  };
+  auto stamp_top = [&]() {
+    ++pstamp;
+    for (std::size_t i = 0; i < t.top.size(); ++i) {
+      rowmap[t.top[i]] = static_cast<int>(i);
+      rstamp[t.top[i]] = pstamp;
+    }
+  };
+  auto row = [&](int k) {
+    if (rstamp[k] != pstamp) throw std::logic_error("coarse tree: unknown missing from its parent front");
+    return rowmap[k];
   };
   t.leaf_cmap.resize(nl);
   {
     std::vector<long long> pos, sr;
     std::vector<int> ch, ci;
-    for (int i = 0; i < nl; ++i) {
-      const auto& cs = leaves[i].coarse;
-      t.leaf_cmap[i].resize(cs.size());
-      for (std::size_t c = 0; c < cs.size(); ++c) {
-        const long long p = leaf_parent_pos(i, cs[c]);
-        t.leaf_cmap[i][c] = static_cast<int>(p);
-        pos.push_back(p);
-        ch.push_back(i);
-        ci.push_back(static_cast<int>(c));
-        sr.push_back(leaves[i].src0 + static_cast<long long>(c));
+    pos.reserve(nl * 64);
+    sr.reserve(nl * 64);
+    ch.reserve(nl * 64);
+    ci.reserve(nl * 64);
+    const int nparent = depth == 0 ? 1 : static_cast<int>(t.levels[0].fronts.size());
+    std::vector<std::vector<int>> kids(nparent);
+    for (int i = 0; i < nl; ++i) kids[depth == 0 ? 0 : leaf_box[i]].push_back(i);
+    for (int pf = 0; pf < nparent; ++pf) {
+      long long base = 0;
+      if (depth == 0) {
+        stamp_top();
+      } else {
+        stamp_front(t.levels[0].fronts[pf]);
+        base = t.levels[0].fronts[pf].fv_off;
+      }
+      for (int i : kids[pf]) {
+        const auto& cs = leaves[i].coarse;
+        t.leaf_cmap[i].resize(cs.size());
+        for (std::size_t c = 0; c < cs.size(); ++c) {
+          const long long p = base + row(cs[c]);
+          t.leaf_cmap[i][c] = static_cast<int>(p);
+          pos.push_back(p);
+          ch.push_back(i);
+          ci.push_back(static_cast<int>(c));
+          sr.push_back(leaves[i].src0 + static_cast<long long>(c));
+        }
       }
     }
     if (depth == 0)
@@ -268,22 +299,27 @@ CoarseTree plan_coarse_tree(const std::vector<CoarseLeaf>& leaves, const int lat
     const bool to_top = l + 1 == depth;
     std::vector<long long> pos, sr;
     std::vector<int> ch, ci;
-    for (int fi = 0; fi < static_cast<int>(C.fronts.size()); ++fi) {
-      const CoarseTree::Front& f = C.fronts[fi];
-      for (std::size_t c = 0; c < f.upd.size(); ++c) {
-        const int k = f.upd[c];
-        long long p;
-        if (to_top) {
-          p = top_index(t.top, k);
-        } else {
-          const CoarseTree::Front& par = t.levels[l + 1].fronts[f.parent];
-          p = par.fv_off + row_of(par, k);
+    const int nparent = to_top ? 1 : static_cast<int>(t.levels[l + 1].fronts.size());
+    std::vector<std::vector<int>> kids(nparent);
+    for (int fi = 0; fi < static_cast<int>(C.fronts.size()); ++fi) kids[to_top ? 0 : C.fronts[fi].parent].push_back(fi);
+    for (int pf = 0; pf < nparent; ++pf) {
+      long long base = 0;
+      if (to_top) {
+        stamp_top();
+      } else {
+        stamp_front(t.levels[l + 1].fronts[pf]);
+        base = t.levels[l + 1].fronts[pf].fv_off;
+      }
+      for (int fi : kids[pf]) {
+        const CoarseTree::Front& f = C.fronts[fi];
+        for (std::size_t c = 0; c < f.upd.size(); ++c) {
+          const long long p = base + row(f.upd[c]);
+          C.cmap[f.cmap_off + c] = static_cast<int>(p);
+          pos.push_back(p);
+          ch.push_back(fi);
+          ci.push_back(static_cast<int>(c));
+          sr.push_back(f.fv_off + f.PE + static_cast<long long>(c));
         }
-        C.cmap[f.cmap_off + c] = static_cast<int>(p);
-        pos.push_back(p);
-        ch.push_back(fi);
-        ci.push_back(static_cast<int>(c));
-        sr.push_back(f.fv_off + f.PE + static_cast<long long>(c));
       }
     }
     if (to_top)
@@ -292,11 +328,6 @@ CoarseTree plan_coarse_tree(const std::vector<CoarseLeaf>& leaves, const int lat
       to_csr(t.levels[l + 1].arena, pos, ch, ci, sr, t.levels[l + 1].ptr, t.levels[l + 1].child,
              t.levels[l + 1].cidx, t.levels[l + 1].src);
   }
-  const double n = static_cast<double>(t.top.size());
-  const bool inv = rup(std::max<int>(static_cast<int>(t.top.size()), 1)) <= root_inverse_max;
-  t.flops += inv ? n * n * n : n * n * n / 3.0;
-  t.apply_bytes += n * n * 8.0;
-  return t;
 }
 
 double coarse_tree_cost(const CoarseTree& t, int applies, int root_inverse_max) {

@@ -50,6 +50,8 @@ struct CoarseTree {
   std::vector<int> top_ptr, top_child, top_cidx;  // gather CSR of the top (children: levels.back() or leaves)
   std::vector<long long> top_src;
   std::vector<std::vector<int>> leaf_cmap;  // per leaf: position of each coarse slot in levels[0]'s vector (or top index)
+  std::vector<int> leaf_box;  // deepest box of each leaf
+  int n_primal = 0;
   double flops = 0;       // factorization flops (fronts + top)
   double apply_bytes = 0;  // bytes read per preconditioner apply (both sweeps of every front + top)
 };
@@ -61,6 +63,9 @@ int coarse_tree_max_depth(const int lattice[3]);
 /// `symbolic`: front sets, sizes and costs only (no gather or backward maps).
 CoarseTree plan_coarse_tree(const std::vector<CoarseLeaf>& leaves, const int lattice[3], int n_primal, int depth,
                             int root_inverse_max, bool symbolic = false);
+
+/// Adds the gather and backward maps to a symbolic plan.
+void complete_coarse_tree(CoarseTree& t, const std::vector<CoarseLeaf>& leaves);
 
 /// Estimated seconds of setup + `applies` preconditioner applies for a plan.
 double coarse_tree_cost(const CoarseTree& t, int applies, int root_inverse_max);
