@@ -157,6 +157,7 @@ struct SubDesc {        // per-subdomain pointers used by the PCG kernels
   double* WB;           // nB: boundary scratch
   int nB, PB, NF, PE;
   int ldF;              // leading dimension of F (NF, or NF + PE for the augmented front)
+  int nE;               // non-coarse boundary dofs (F rows [0, nE) and [PE, PE + nB - nE) are used)
 };
 
 struct XformDesc {      // glob transforms, flat
@@ -477,6 +478,51 @@ __global__ void k_rowxform_scatter(const SubDesc* sd, XformDesc x, const double*
     }
   }
   // the padding positions of F get identity entries in k_pad_identity
+}
+
+// F = P_F (T^T S T) P_F^T in one pass (factor mode: ld F = NF): CTA (c, s)
+// forms column c of S T in shared memory (the glob columns combine r + 1
+// columns of S), applies T^T on the rows and writes the whole F column,
+// padding rows included; CTAs beyond nB write the padding columns (unit
+// vectors).  Every entry of F is written: no scratch X, no memset.
+__global__ void __launch_bounds__(256) k_xform_fused(const SubDesc* sd, XformDesc x) {
+  const SubDesc d = sd[blockIdx.y];
+  extern __shared__ double y[];
+  const int c = blockIdx.x, nE = d.nE, nC = d.nB - d.nE;
+  const size_t ld = d.ldF;
+  if (c < d.nB) {
+    const int inst = d.bglob[c];
+    if (inst < 0) {
+      const double* sc = d.S + (size_t)c * d.PB;
+      for (int b = threadIdx.x; b < d.nB; b += blockDim.x) y[b] = sc[b];
+    } else {
+      const int j = d.bslot[c];
+      const int tr = x.inst_tr[inst];
+      const int* pos = x.tpos + x.inst_pos[inst];
+      const int n = x.tr_n[tr], r = x.tr_r[tr];
+      const int* perm = x.perm + x.tr_off_perm[tr];
+      const double* D = x.D + x.tr_off_d[tr];
+      for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
+        double s = j >= r ? d.S[(size_t)pos[perm[j]] * d.PB + b] : 0.0;
+        for (int i = 0; i < r; ++i) s += D[i * n + j] * d.S[(size_t)pos[perm[i]] * d.PB + b];
+        y[b] = s;
+      }
+    }
+    __syncthreads();
+    double* fcol = d.F + (size_t)d.posF[c] * ld;
+    for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
+      const int inst = d.bglob[b];
+      fcol[d.posF[b]] = inst < 0 ? y[b] : xform_T_t(x, inst, d.bslot[b], y);
+    }
+    for (int q = nE + threadIdx.x; q < d.PE; q += blockDim.x) fcol[q] = 0.0;
+    for (int q = d.PE + nC + threadIdx.x; q < d.NF; q += blockDim.x) fcol[q] = 0.0;
+  } else {
+    const int k = c - d.nB, npe = d.PE - nE;  // padding column k: [nE, PE) then [PE + nC, NF)
+    const int q = k < npe ? nE + k : d.PE + nC + (k - npe);
+    if (q >= d.NF) return;
+    double* fcol = d.F + (size_t)q * ld;
+    for (int r = threadIdx.x; r < d.NF; r += blockDim.x) fcol[r] = r == q ? 1.0 : 0.0;
+  }
 }
 
 __global__ void k_pad_identity(double* Farena, const long long* foff, const int* NF, const int* pad_sub,
@@ -1456,7 +1502,7 @@ void Engine::prepare() {
   std::vector<int> pi_own;
   for (int s : D.own) {
     sd.push_back(SubDesc{D.S.p + D.s_off[s], nullptr, nullptr, D.biface.p + D.wb_off[s], D.bw.p + D.wb_off[s],
-                         nullptr, nullptr, nullptr, D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], 0, 0});
+                         nullptr, nullptr, nullptr, D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], 0, 0, 0, 0});
     mvo_own.push_back(D.mv_off[s]);
     pi_own.push_back(D.PI[s]);
   }
@@ -1966,7 +2012,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     lead.add(D.F, fo);
     lead.add(D.DinvF, dfo);
     if (D.leaf_explicit) lead.add(D.E, eo);
-    scratch.add(D.Xtmp, xo);
+    if (D.leaf_explicit) scratch.add(D.Xtmp, xo);  // factor mode: k_xform_fused needs no scratch
     late.add(D.R, ldR0 * ldR0);
     late.add(D.DinvR, (long long)D.NR * kTile);
     if (D.root_inv) late.add(D.Rinv, (long long)D.NR * D.NR);
@@ -1987,7 +2033,6 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     late.place(base + lead.total());
   }
   ht.mark("regions");
-  D.F.zero(st);
   D.FV.alloc(std::max<long long>(fvo, 1));
   D.FV.zero(st);
   if (D.leaf_explicit) {
@@ -2003,7 +2048,8 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     const int s = D.own[q];
     sd[q] = SubDesc{D.S.p + D.s_off[s], D.F.p + D.f_off[s], D.FV.p + D.fv_off[s], D.biface.p + D.wb_off[s],
                     D.bw.p + D.wb_off[s], D.bposF.p + D.wb_off[s], D.bglob.p + D.wb_off[s],
-                    D.bslot.p + D.wb_off[s], D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], D.NF[s], D.PE[s], D.NA[s]};
+                    D.bslot.p + D.wb_off[s], D.WB.p + D.wb_off[s], D.nB[s], D.PB[s], D.NF[s], D.PE[s], D.NA[s],
+                    D.nE[s]};
     fd[q] = FrontDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.NA[s], D.PE[s], D.finfo.p + q,
                       D.leaf_explicit ? D.NF[s] : 0};
     fw[q] = SolveDesc{D.F.p + D.f_off[s], D.DinvF.p + D.df_off[s], D.FV.p + D.fv_off[s], D.NF[s], D.PE[s],
@@ -2130,14 +2176,22 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   ht.mark("upload_desc");
   StageProfiler prof("set_constraints", st);
   // F = P (T^T S T) P^T, pads identity
-  if (no) {
-    k_colxform<<<dim3(D.max_PB, no), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
-    k_rowxform_scatter<<<dim3(D.max_PB, no), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
+  if (!D.leaf_explicit) {
+    if (no) {
+      k_xform_fused<<<dim3(D.max_PB + 2 * kTile, no), 256, D.max_nB * sizeof(double), st>>>(D.subdesc.p, D.xf);
+      count_launch(1);
+    }
+  } else {
+    D.F.zero(st);
+    if (no) {
+      k_colxform<<<dim3(D.max_PB, no), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
+      k_rowxform_scatter<<<dim3(D.max_PB, no), 128, 0, st>>>(D.subdesc.p, D.xf, D.Xtmp.p, D.d_xoff.p);
+    }
+    if (!pads.empty())
+      k_pad_identity<<<std::min<int>(1024, (static_cast<int>(pads.size()) + 255) / 256), 256, 0, st>>>(
+          D.F.p, D.d_foff.p, D.d_NF.p, D.pad_sub.p, D.pads.p, static_cast<int>(pads.size()));
+    count_launch(3);
   }
-  if (!pads.empty())
-    k_pad_identity<<<std::min<int>(1024, (static_cast<int>(pads.size()) + 255) / 256), 256, 0, st>>>(
-        D.F.p, D.d_foff.p, D.d_NF.p, D.pad_sub.p, D.pads.p, static_cast<int>(pads.size()));
-  count_launch(3);
   if (D.leaf_explicit && no) {
     k_aug_identity<<<dim3((D.max_PE + 255) / 256, no), 256, 0, st>>>(D.leafx.p);
     count_launch(1);
