@@ -96,6 +96,7 @@ struct PairBuffers {
   DBuf<PairDev> dpd;
   DBuf<FrontDesc> dG, dQ, d3, d4;
   DBuf<SolveDesc> dsv;
+  UploadBatch up_index, up_desc;  // per chunk: index arrays, then descriptors (one copy each)
 };
 
 PairEngine::PairEngine() : bufs_(new PairBuffers) {}
@@ -1287,18 +1288,19 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     F.alloc(nF);
     Dv.alloc(std::max<long long>(nD, 1));
     M.alloc(std::max<long long>(nM, 1));
-    B_.KC.upload(kcv, st_);
-    B_.KR.upload(krv, st_);
-    B_.KV.upload(kvv, st_);
+    B_.up_index.add(B_.KC, kcv);
+    B_.up_index.add(B_.KR, krv);
+    B_.up_index.add(B_.KV, kvv);
     H.alloc(std::max<long long>(nH, 1));
-    N.upload(Nv, st_);
-    R.upload(Rv, st_);
+    B_.up_index.add(N, Nv);
+    B_.up_index.add(R, Rv);
     A.alloc(std::max<long long>(nA, 1));
     E.alloc(nE);
     W.alloc(nW);
     Fu.alloc(std::max<long long>(nFu, 1));
-    Pv.upload(posv, st_);
-    if (ch.gposv.empty()) B_.Gpos.alloc(1); else B_.Gpos.upload(ch.gposv, st_);
+    B_.up_index.add(Pv, posv);
+    B_.up_index.add(B_.Gpos, ch.gposv);
+    B_.up_index.flush(st_);
     info.alloc(4 * nb);
     CK(cudaMemsetAsync(info.p, 0, 4 * nb * sizeof(int), st_));
     ht.mark("alloc_upload");
@@ -1358,30 +1360,38 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     }
     auto& dpd = B_.dpd;
     auto& dG = B_.dG; auto& dQ = B_.dQ; auto& d3 = B_.d3; auto& d4 = B_.d4;
-    dpd.upload(pd, st_);
-    dG.upload(fG, st_);
-    dQ.upload(fQ, st_);
-    d3.upload(f3, st_);
-    d4.upload(f4, st_);
+    B_.up_desc.add(dpd, pd);
+    B_.up_desc.add(dG, fG);
+    B_.up_desc.add(dQ, fQ);
+    B_.up_desc.add(d3, f3);
+    B_.up_desc.add(d4, f4);
+    // side-front gathers and the back-substitution descriptors of (k)
+    std::vector<GatherDesc> gs(2 * nb);
+    for (int b = 0; b < nb; ++b)
+      for (int side = 0; side < 2; ++side) {
+        const HostPair& h = hp[p0 + b];
+        const int q = h.hub[side];
+        const int sub = side == 0 ? h.idx.si : h.idx.sj;
+        const double* src = q >= 0 ? B_.Hub.p + hubOff[q] + (size_t)hubPH[q] * hubNH[q] + hubPH[q]
+                                   : S_ + s_off_[sub];
+        const int lds = q >= 0 ? hubNH[q] : PB_[sub];
+        gs[2 * b + side] = GatherDesc{src, B_.Gpos.p + ch.oGp[2 * b + side], pd[b].G[side], lds,
+                                      dims[b].NG[side], dims[b].PO[side], dims[b].no[side],
+                                      dims[b].nc + dims[b].nf};
+      }
+    B_.up_desc.add(B_.gside, gs);
+    std::vector<SolveDesc> sv;
+    for (int b = 0; b < nb; ++b)
+      for (int mm = 0; mm < dims[b].k; ++mm)
+        sv.push_back(SolveDesc{pd[b].F3, Dv.p + oD3[b], pd[b].vecs + (size_t)mm * 2 * dims[b].PJ, 2 * dims[b].PJ,
+                               dims[b].PJ, nullptr, nullptr});
+    B_.up_desc.add(B_.dsv, sv);
+    B_.up_desc.flush(st_);
     ht.mark("descriptors");
     StageProfiler prof("enrich", st_);
     // (a)-(b) side fronts, eliminate the outer skeleton
     {
       // side fronts [U \ K | corner | shared] from the hubs' Schur complements
-      std::vector<GatherDesc> gs(2 * nb);
-      for (int b = 0; b < nb; ++b)
-        for (int side = 0; side < 2; ++side) {
-          const HostPair& h = hp[p0 + b];
-          const int q = h.hub[side];
-          const int sub = side == 0 ? h.idx.si : h.idx.sj;
-          const double* src = q >= 0 ? B_.Hub.p + hubOff[q] + (size_t)hubPH[q] * hubNH[q] + hubPH[q]
-                                     : S_ + s_off_[sub];
-          const int lds = q >= 0 ? hubNH[q] : PB_[sub];
-          gs[2 * b + side] = GatherDesc{src, B_.Gpos.p + ch.oGp[2 * b + side], pd[b].G[side], lds,
-                                        dims[b].NG[side], dims[b].PO[side], dims[b].no[side],
-                                        dims[b].nc + dims[b].nf};
-        }
-      B_.gside.upload(gs, st_);
       k_gather_front<<<dim3(maxNG, 2 * nb), 128, 0, st_>>>(B_.gside.p);
       count_launch(1);
     }
@@ -1435,13 +1445,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     }
     CK(cudaGetLastError());
     // (k) alpha = L^{-T} y via F3's factor; (l) functionals
-    std::vector<SolveDesc> sv;
-    for (int b = 0; b < nb; ++b)
-      for (int mm = 0; mm < dims[b].k; ++mm)
-        sv.push_back(SolveDesc{pd[b].F3, Dv.p + oD3[b], pd[b].vecs + (size_t)mm * 2 * dims[b].PJ, 2 * dims[b].PJ,
-                               dims[b].PJ, nullptr, nullptr});
     auto& dsv = B_.dsv;
-    dsv.upload(sv, st_);
     front_backward(dsv.p, static_cast<int>(sv.size()), 2 * maxPJ, st_);
     k_functional<<<dim3(std::max(maxk, 1), nb), 128, 0, st_>>>(dpd.p);
     count_launch(9);
