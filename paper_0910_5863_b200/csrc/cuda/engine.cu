@@ -636,6 +636,15 @@ __device__ __forceinline__ void leaf_bwd_body(const LeafX& d, int rb, const doub
       const double* w = d.E + (size_t)d.PE * d.PE + i;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       int c = g;
+      for (; c + 28 < d.M; c += 32) {  // eight loads in flight
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = __ldg(w + (size_t)(c + 4 * q) * d.PE);
+        s0 += v[0] * xc[c] + v[4] * xc[c + 16];
+        s1 += v[1] * xc[c + 4] + v[5] * xc[c + 20];
+        s2 += v[2] * xc[c + 8] + v[6] * xc[c + 24];
+        s3 += v[3] * xc[c + 12] + v[7] * xc[c + 28];
+      }
       for (; c + 12 < d.M; c += 16) {
         s0 += w[(size_t)c * d.PE] * xc[c];
         s1 += w[(size_t)(c + 4) * d.PE] * xc[c + 4];
@@ -721,7 +730,7 @@ __global__ void k_front_pads(const AsmFront* fr) {
   const AsmFront f = fr[blockIdx.y];
   for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < f.NF; q += (long)gridDim.x * blockDim.x) {
     if ((q >= f.ne && q < f.PE) || q >= f.PE + f.nc) f.out[(size_t)q * f.ld + q] = 1.0;
-    if (f.ld > f.NF) f.out[(size_t)q * f.ld + f.NF + q] = 1.0;
+    if (f.ld > f.NF && q < f.ld - f.NF) f.out[(size_t)q * f.ld + f.NF + q] = 1.0;
   }
 }
 
@@ -1245,6 +1254,15 @@ struct DeviceState {
     int nfr = 0, max_NF = 0, max_PE = 0, max_M = 0, max_slots = 0;
     long long arena = 0;
     std::vector<int> NF, PE, nown, nupd;
+    // explicit level (few fronts): augmented fronts [[F, I], [I, 0]] (ld NA =
+    // NF + PE) whose elimination leaves E = [-F_ee^{-1} | -W]; both sweeps of
+    // the level become GEMVs (k_leaf_*_explicit), forward results in V2
+    bool expl = false;
+    int max_NA = 0, max_MA = 0;
+    std::vector<long long> xa_off, xe_off;
+    long long xa_size = 0, xe_size = 0;
+    DBuf<double> E, V2;
+    DBuf<LeafX> lx;
   };
   std::vector<std::unique_ptr<TreeLevel>> tree;
   int tree_depth = 0;
@@ -2006,6 +2024,27 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   // Preconditioner arenas: views into the stage arena (shared with the pair
   // stage).  [F | DinvF | E | Xtmp], with the root and the primal tree over the
   // transform scratch Xtmp (dead once F is formed).
+  for (std::size_t l = 0; l < plan.levels.size(); ++l) {
+    DeviceState::TreeLevel& T = *D.tree[l];
+    const CoarseTree::Level& P = plan.levels[l];
+    const char* env = std::getenv("BDDC_B200_TREE");  // explicit | factor (testing override)
+    const std::string mode = env ? env : "";
+    T.expl = mode == "explicit" || (mode != "factor" && static_cast<int>(P.fronts.size()) < sm_count());
+    T.xa_off.assign(P.fronts.size(), 0);
+    T.xe_off.assign(P.fronts.size(), 0);
+    T.xa_size = T.xe_size = 0;
+    T.max_NA = T.max_MA = 0;
+    for (std::size_t f = 0; f < P.fronts.size(); ++f) {
+      const CoarseTree::Front& F = P.fronts[f];
+      const long long NA = T.expl ? (long long)F.NF + F.PE : F.NF;
+      T.xa_off[f] = T.xa_size;
+      T.xa_size += NA * NA;
+      T.xe_off[f] = T.xe_size;
+      if (T.expl) T.xe_size += (long long)F.PE * F.NF;
+      T.max_NA = std::max<int>(T.max_NA, static_cast<int>(NA));
+      T.max_MA = std::max<int>(T.max_MA, static_cast<int>(NA - F.PE));
+    }
+  }
   {
     const long long ldR0 = D.root_inv ? 2LL * D.NR : D.NR;
     RegionPlan lead, scratch, late;
@@ -2017,8 +2056,9 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     late.add(D.DinvR, (long long)D.NR * kTile);
     if (D.root_inv) late.add(D.Rinv, (long long)D.NR * D.NR);
     for (std::size_t l = 0; l < plan.levels.size(); ++l) {
-      late.add(D.tree[l]->A, plan.levels[l].a_size);
+      late.add(D.tree[l]->A, D.tree[l]->xa_size);
       late.add(D.tree[l]->Dinv, plan.levels[l].d_size);
+      if (D.tree[l]->expl) late.add(D.tree[l]->E, D.tree[l]->xe_size);
     }
     const std::size_t total = lead.total() + std::max(scratch.total(), late.total());
     const double room = total <= D.stage.capacity() ? 0.0 : double(D.stage.capacity()) * 8.0 + free_bytes();
@@ -2070,6 +2110,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     T.max_M = P.max_M;
     T.arena = P.arena;
     T.V.alloc(std::max<long long>(P.arena, 1));
+    if (T.expl) T.V2.alloc(std::max<long long>(P.arena, 1));
     T.info.alloc(T.nfr);
     T.info.zero(st);
     T.NF.assign(T.nfr, 0);
@@ -2085,8 +2126,9 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       T.nupd[f] = static_cast<int>(F.upd.size());
       T.max_slots = std::max(T.max_slots, T.nown[f] + T.nupd[f]);
       const double e = T.nown[f], c = T.nupd[f];
-      D.tree_apply_bytes += 2.0 * (e * (e + 1) / 2 + e * c) * 8.0;
-      D.tree_factor_bytes += (e * (e + 1) / 2 + e * c) * 8.0;
+      // explicit: E (e x (e + c)) forward, W (e x c) backward; else L twice
+      D.tree_apply_bytes += (T.expl ? e * (e + c) + e * c : 2.0 * (e * (e + 1) / 2 + e * c)) * 8.0;
+      D.tree_factor_bytes += (T.expl ? e * e + e * c : e * (e + 1) / 2 + e * c) * 8.0;
     }
   }
   // Larger roots are factored in place and solved by triangular sweeps (over
@@ -2104,19 +2146,26 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     std::vector<FrontDesc> fdl(T.nfr);
     std::vector<SolveDesc> fwl(T.nfr), bwl(T.nfr);
     std::vector<AsmFront> afl(T.nfr);
+    std::vector<LeafX> lxl;
     for (int f = 0; f < T.nfr; ++f) {
       const CoarseTree::Front& F = P.fronts[f];
-      fdl[f] = FrontDesc{T.A.p + F.a_off, T.Dinv.p + F.d_off, F.NF, F.PE, T.info.p + f, 0};
-      fwl[f] = SolveDesc{T.A.p + F.a_off, T.Dinv.p + F.d_off, T.V.p + F.fv_off, F.NF, F.PE, nullptr, nullptr};
+      const int NA = T.expl ? F.NF + F.PE : F.NF;
+      double* a = T.A.p + T.xa_off[f];
+      fdl[f] = FrontDesc{a, T.Dinv.p + F.d_off, NA, F.PE, T.info.p + f, T.expl ? F.NF : 0};
+      fwl[f] = SolveDesc{a, T.Dinv.p + F.d_off, T.V.p + F.fv_off, F.NF, F.PE, nullptr, nullptr};
       bwl[f] = fwl[f];
       bwl[f].cmap = T.cmap.p + F.cmap_off;
       bwl[f].croot = up;
-      afl[f] = AsmFront{T.A.p + F.a_off, F.NF, T.nown[f], T.nupd[f], F.PE, F.NF, F.fv_off};
+      afl[f] = AsmFront{a, NA, T.nown[f], T.nupd[f], F.PE, F.NF, F.fv_off};
+      if (T.expl)
+        lxl.push_back(LeafX{a, T.E.p + T.xe_off[f], T.V.p + F.fv_off, T.V2.p + F.fv_off, T.cmap.p + F.cmap_off, NA,
+                            F.PE, F.NF - F.PE});
     }
     up_v(T.fronts, fdl);
     up_v(T.fwd, fwl);
     up_v(T.bwd, bwl);
     up_v(T.afronts, afl);
+    if (T.expl) up_v(T.lx, lxl);
     std::vector<AsmChild> kids;
     if (l == 0) {
       for (int q = 0; q < no; ++q) {
@@ -2125,8 +2174,10 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       }
     } else {
       const DeviceState::TreeLevel& C = *D.tree[l - 1];
-      for (const CoarseTree::Front& F : plan.levels[l - 1].fronts)
-        kids.push_back(AsmChild{C.A.p + F.a_off, F.NF, F.PE});
+      for (std::size_t f = 0; f < plan.levels[l - 1].fronts.size(); ++f) {
+        const CoarseTree::Front& F = plan.levels[l - 1].fronts[f];
+        kids.push_back(AsmChild{C.A.p + C.xa_off[f], C.expl ? F.NF + F.PE : F.NF, F.PE});
+      }
     }
     up_v(T.kids, kids);
   }
@@ -2139,8 +2190,10 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       }
     } else {
       const DeviceState::TreeLevel& C = *D.tree.back();
-      for (const CoarseTree::Front& F : plan.levels.back().fronts)
-        kids.push_back(AsmChild{C.A.p + F.a_off, F.NF, F.PE});
+      for (std::size_t f = 0; f < plan.levels.back().fronts.size(); ++f) {
+        const CoarseTree::Front& F = plan.levels.back().fronts[f];
+        kids.push_back(AsmChild{C.A.p + C.xa_off[f], C.expl ? F.NF + F.PE : F.NF, F.PE});
+      }
     }
     up_v(D.root_kids, kids);
     std::vector<AsmFront> af{AsmFront{D.R.p, ldR, D.n_root, 0, D.NR, D.NR, 0}};
@@ -2215,7 +2268,11 @@ void Engine::set_constraints(const ConstraintSet& cs) {
         T.afronts.p, T.ptr.p, T.child.p, T.cidx.p, T.kids.p);
     k_front_pads<<<dim3(std::max(1, std::min(64, (T.max_NF + 255) / 256)), T.nfr), 256, 0, st>>>(T.afronts.p);
     count_launch(2);
-    partial_cholesky(T.fronts.p, T.nfr, T.max_NF, T.max_PE, T.max_M, st);
+    partial_cholesky(T.fronts.p, T.nfr, T.max_NA, T.max_PE, T.max_MA, st);
+    if (T.expl) {
+      k_leaf_explicit_copy<<<dim3(64, T.nfr), 256, 0, st>>>(T.lx.p);
+      count_launch(1);
+    }
   }
   if (!D.tree.empty()) prof.mark("tree");
   // this rank's contributions (+ the identity blocks on rank 0), then the
@@ -2313,8 +2370,14 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     k_root_gather<<<std::max(1, std::min<int>(1024, static_cast<int>((T->arena + 255) / 256))), 256, 0, st>>>(
         static_cast<int>(T->arena), static_cast<int>(T->arena), T->ptr.p, T->src.p, fvsrc, T->V.p, done);
     count_launch(1);
-    front_forward(T->fwd.p, T->nfr, T->max_NF, st, done);
-    fvsrc = T->V.p;
+    if (T->expl) {
+      k_leaf_fwd_explicit<<<dim3((T->max_NF + 7) / 8, T->nfr), 256, T->max_PE * sizeof(double), st>>>(T->lx.p, done);
+      count_launch(1);
+      fvsrc = T->V2.p;
+    } else {
+      front_forward(T->fwd.p, T->nfr, T->max_NF, st, done);
+      fvsrc = T->V.p;
+    }
   }
   if (!D.tree.empty()) mark("tree_fwd");
   if (D.root_inv && !D.comm && D.NR <= 1024) {
@@ -2341,7 +2404,17 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     mark("root_bwd");
   }
   }
-  for (std::size_t l = D.tree.size(); l-- > 0;) front_backward(D.tree[l]->bwd.p, D.tree[l]->nfr, D.tree[l]->max_NF, st, done);
+  for (std::size_t l = D.tree.size(); l-- > 0;) {
+    DeviceState::TreeLevel& T = *D.tree[l];
+    if (T.expl) {
+      double* up = l + 1 < D.tree.size() ? D.tree[l + 1]->V.p : (D.root_inv ? D.xroot2.p : D.xroot.p);
+      k_leaf_bwd_explicit<<<dim3(T.max_NF / kTile, T.nfr), 256, std::max(T.max_M, 1) * sizeof(double), st>>>(T.lx.p, up,
+                                                                                                          done);
+      count_launch(1);
+    } else {
+      front_backward(T.bwd.p, T.nfr, T.max_NF, st, done);
+    }
+  }
   if (!D.tree.empty()) mark("tree_bwd");
   if (D.leaf_explicit && ns) {
     k_leaf_bwd_explicit<<<dim3(D.max_NF / kTile, ns), 256, D.max_M * sizeof(double), st>>>(D.leafx.p, D.leaf_croot,

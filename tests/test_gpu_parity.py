@@ -241,15 +241,17 @@ TREE = [("cfg1", baseline_config(1).spec, lambda: pb.BDDC(config=1), "c+e+f", 1)
          lambda: pb.BDDC(pb.Problem.cube((4, 3, 2), 2, "elasticity")), "c+e", 2)]
 
 
-@pytest.mark.parametrize("leaf", ["explicit", "factor"])
+@pytest.mark.parametrize("leaf,tree", [("explicit", "explicit"), ("factor", "factor"), ("factor", "explicit")])
 @pytest.mark.parametrize("name,spec,make,mode,depth", TREE, ids=[t[0] for t in TREE])
-def test_primal_tree(name, spec, make, mode, depth, leaf, monkeypatch):
+def test_primal_tree(name, spec, make, mode, depth, leaf, tree, monkeypatch):
     """The primal (root) system factored as a nested-dissection tree of fronts
-    over the substructure lattice (coarse_tree.hpp) instead of one dense root:
-    preconditioner, PCG and solution against the oracle's single sparse
-    factorization of the stabilized operator (bddc_operator.cpp:38-103)."""
+    over the substructure lattice (coarse_tree.hpp) instead of one dense root,
+    its levels swept or applied through explicit inverses: preconditioner, PCG
+    and solution against the oracle's single sparse factorization of the
+    stabilized operator (bddc_operator.cpp:38-103)."""
     monkeypatch.setenv("BDDC_B200_ROOT_DEPTH", str(depth))
     monkeypatch.setenv("BDDC_B200_LEAF", leaf)
+    monkeypatch.setenv("BDDC_B200_TREE", tree)
     p = build_pipeline(spec)
     h = HarmonicExtension(p.systems, p.maps)
     itf = InterfaceProblem(p.systems, p.maps, h)
