@@ -433,6 +433,18 @@ __device__ int sturm_count_sq(const double* d, const double* e2, int n, double x
   return cnt;
 }
 
+// stage timestamps of block 0 (BDDC_B200_PROFILE=1): load, tridiagonalization,
+// multisection, inverse iteration, orthogonalization, back-transformation
+__device__ unsigned long long g_syevx_trace[8];
+__device__ int g_syevx_trace_on;
+__device__ __forceinline__ void syevx_mark(int i) {
+  if (g_syevx_trace_on && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_syevx_trace[i] = t;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) {
   const PairDev dd = pd[blockIdx.x];
   const int n = dd.nj, k = dd.k, N2 = 2 * dd.PJ, PJ = dd.PJ;
@@ -457,9 +469,11 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
   __shared__ double red[32];
   __shared__ double pg[256];  // column-group partials of A22 v
   if (n == 0 || k == 0) return;
+  syevx_mark(0);
   for (int r = 0; r < n; ++r)
     for (int c = tid; c <= r; c += blockDim.x) L[pk(r, c)] = dd.F4[(size_t)c * N2 + PJ + r];
   __syncthreads();
+  syevx_mark(1);
   // 1. tridiagonalization (dsytd2, lower)
   for (int kk = 0; kk + 2 < n; ++kk) {
     const int m0 = kk + 1;
@@ -568,6 +582,7 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
     tau[n - 1] = 0.0;
   }
   __syncthreads();
+  syevx_mark(2);
   // 2. top-k eigenvalues by multisection (16 threads per eigenvalue)
   double tnorm = 0.0, emax2 = 0.0, glo = 1e300, ghi = -1e300;
   for (int i = 0; i < n; ++i) {
@@ -606,6 +621,7 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
     if (active && j == 0) lam[m] = 0.5 * (lo + hi);
   }
   __syncthreads();
+  syevx_mark(3);
   // 3. inverse iteration on T (thread m), scratch in global memory
   if (tid < k) {
     const int m = tid;
@@ -684,6 +700,7 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
     }
   }
   __syncthreads();
+  syevx_mark(4);
   // modified Gram-Schmidt inside clusters (eigenvalues closer than 1e-7 ||T||)
   if (warp == 0) {
     for (int m = 1; m < k; ++m) {
@@ -708,6 +725,7 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
     }
   }
   __syncthreads();
+  syevx_mark(5);
   // 4. back-transformation y = H_0 ... H_{n-3} z: warp w carries vectors w and
   // w + 8 through the reflectors together (their reductions interleave), then
   // the vectors are written out with the solve padding zeroed
@@ -746,6 +764,7 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
     dd.vecs[e] = i < n ? Z[(size_t)m * n + i] : 0.0;
   }
   for (int m = tid; m < k; m += blockDim.x) dd.evals[m] = fmax(lam[m], 0.0);
+  syevx_mark(6);
 }
 
 // (l) functional a_m = 1/2 M K alpha_m (alpha = first nj entries of vecs after the back solve)
@@ -1440,7 +1459,19 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
         CK(cudaFuncSetAttribute(k_syevx, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
         syevx_attr = true;
       }
+      const char* pe = std::getenv("BDDC_B200_PROFILE");
+      const int tr_on = pe && *pe && *pe != '0';
+      CK(cudaMemcpyToSymbolAsync(g_syevx_trace_on, &tr_on, sizeof(int), 0, cudaMemcpyHostToDevice, st_));
       k_syevx<<<nb, 256, static_cast<int>(dyn * 8), st_>>>(dpd.p, static_cast<int>(dyn));
+      if (tr_on) {
+        unsigned long long t[8];
+        CK(cudaMemcpyFromSymbolAsync(t, g_syevx_trace, sizeof(t), 0, cudaMemcpyDeviceToHost, st_));
+        CK(cudaStreamSynchronize(st_));
+        std::fprintf(stderr, "[profile] syevx block 0 (n=%d k=%d): load=%.1fus tridiag=%.1fus multisection=%.1fus "
+                     "inverse_iteration=%.1fus mgs=%.1fus back_transform=%.1fus\n", dims[0].nj, dims[0].k,
+                     (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3,
+                     (t[5] - t[4]) * 1e-3, (t[6] - t[5]) * 1e-3);
+      }
       prof.mark(smem_ok ? "syevx_smem" : "syevx_gmem");
     }
     CK(cudaGetLastError());
