@@ -13,6 +13,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstdio>
 #include <map>
@@ -204,41 +205,41 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_syrk_trailing(const FrontDesc*
 //          block diagonals: Linv_ij = -Linv_ii sum_k L_ik Linv_kj.
 // k_trsm then forms X = C L^{-T} = C Linv^T as one 64x64x64 DMMA tile product.
 // Cholesky of the 16x16 diagonal block at Lo (ld LDS, lower triangle) by one
-// warp: lane r holds row r in registers; pivots and column entries move by
-// shuffles; selects (not branches) keep the row in registers.  Kept out of line
-// so the unrolled row stays in registers inside the caller's block loop.
+// warp: lane r holds row r in registers; column entries move by shuffles.  The
+// pivot chain is kept short: lane k+1 updates its own next pivot with its own
+// L[k+1][k] (no shuffle), so one step is shuffle -> rsqrt -> mul -> fma.
+// Kept out of line so the unrolled row stays in registers.
 // Writes 1/L_kk to rd[k].  Returns 1 + the first non-positive pivot, or 0.
 __device__ __noinline__ int chol16(double* Lo, double* rd, int lane) {
+  __shared__ __align__(16) double cb[2][16];  // column k of L, double-buffered (warp broadcast)
   const int r = lane & 15;
   double a[16];
 #pragma unroll
   for (int c = 0; c < 16; ++c) a[c] = Lo[c * LDS + r];
   int bad = 0;
-  // software-pipelined: column k+1 is updated first and pivot k+1 (shuffle +
-  // rsqrt) is started before the remaining updates of step k, which fill its
-  // latency
-  double dkk = __shfl_sync(0xffffffffu, a[0], 0);
-  double inv = dkk > 0.0 ? rsqrt(dkk) : 1.0;
+  double dk = __shfl_sync(0xffffffffu, a[0], 0);
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
-    if (!(dkk > 0.0) && !bad) bad = k + 1;
-    const double sk = dkk > 0.0 ? dkk * inv : 1.0;
+    const double inv = dk > 0.0 ? rsqrt(dk) : 1.0;
+    if (!(dk > 0.0) && !bad) bad = k + 1;
     if (lane == k) rd[k] = inv;
-    a[k] = (r == k) ? sk : (r > k ? a[k] * inv : a[k]);
-    double dkk_n = 1.0, inv_n = 1.0;
+    const double l = (r == k) ? (dk > 0.0 ? dk * inv : 1.0) : (r > k ? a[k] * inv : a[k]);
+    a[k] = l;
     if (k + 1 < 16) {
-      const double l1 = __shfl_sync(0xffffffffu, a[k], k + 1);  // L[k+1][k]
-      a[k + 1] = (r >= k + 1) ? a[k + 1] - a[k] * l1 : a[k + 1];
-      dkk_n = __shfl_sync(0xffffffffu, a[k + 1], k + 1);
-      inv_n = dkk_n > 0.0 ? rsqrt(dkk_n) : 1.0;
-    }
+      // next pivot first: lane k+1 owns L[k+1][k] = l
+      const double own = a[k + 1] - l * l;
+      const double dn = __shfl_sync(0xffffffffu, own, k + 1);
+      if (lane < 16) cb[k & 1][r] = l;
+      __syncwarp();
+      const double2* col = reinterpret_cast<const double2*>(cb[k & 1]);
 #pragma unroll
-    for (int c = k + 2; c < 16; ++c) {
-      const double lc = __shfl_sync(0xffffffffu, a[k], c);  // L[c][k]
-      a[c] = (r >= c) ? a[c] - a[k] * lc : a[c];
+      for (int q = (k + 1) / 2; q < 8; ++q) {
+        const double2 v = col[q];  // L[2q][k], L[2q+1][k]
+        if (2 * q > k) a[2 * q] = (r >= 2 * q) ? a[2 * q] - l * v.x : a[2 * q];
+        a[2 * q + 1] = (r >= 2 * q + 1) ? a[2 * q + 1] - l * v.y : a[2 * q + 1];
+      }
+      dk = dn;
     }
-    dkk = dkk_n;
-    inv = inv_n;
   }
   if (lane < 16) {
 #pragma unroll
@@ -248,29 +249,83 @@ __device__ __noinline__ int chol16(double* Lo, double* rd, int lane) {
   return bad;
 }
 
+// 16x16 block product on one warp (DMMA m16n8k16): acc += op(A) B with
+// A(m, k) = A[m * ars + k * acs], B(k, n) = B[k * brs + n * bcs], K a multiple
+// of 16; op negates A when NEG.  acc[ni][v] is C(g + 8 (v >> 1), 8 ni + 2 t0 + (v & 1)).
+template <bool NEG>
+__device__ __forceinline__ void mma16(double (&acc)[2][4], const double* A, int ars, int acs, const double* B,
+                                      int brs, int bcs, int K) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t0 = lane & 3;
+  for (int kk = 0; kk < K; kk += 16) {
+    double a[8], b[2][4];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double x = A[(g + 8 * (v & 1)) * ars + (kk + t0 + 4 * (v >> 1)) * acs];
+      a[v] = NEG ? -x : x;
+    }
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) b[ni][v] = B[(kk + t0 + 4 * v) * brs + (ni * 8 + g) * bcs];
+    dmma(acc[0], a, b[0]);
+    dmma(acc[1], a, b[1]);
+  }
+}
+
+template <class F>
+__device__ __forceinline__ void for_acc16(double (&acc)[2][4], F f) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t0 = lane & 3;
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) f(g + 8 * (v >> 1), ni * 8 + 2 * t0 + (v & 1), acc[ni][v]);
+}
+
 constexpr int PANEL_THREADS = 256;
 
-__global__ void __launch_bounds__(PANEL_THREADS) k_panel(const FrontDesc* ds, int j) {
-  const FrontDesc d = ds[blockIdx.y];
-  if (j * kTile >= d.p) return;
-  extern __shared__ __align__(16) double smem[];
-  double* L = smem;             // 64 x LDS, column-major: L[c*LDS + r]
-  double* V = smem + 64 * LDS;  // L^{-1} (lower block triangle only)
-  __shared__ double T[3][16][17];  // block products of the inverse
-  __shared__ double rd[64];        // reciprocal diagonal of L_jj
+// Timestamps of front 0's diagonal tasks (tools/chol_bench): [2j] accumulation
+// done, [2j+1] Dinv_j published.
+__device__ unsigned long long g_dag_trace[2 * 64];
+__device__ int g_dag_trace_on;
+__device__ unsigned long long g_pf_trace[16];
+__device__ __forceinline__ void pf_mark(int slot) {
+#ifndef DENSE_TRACE
+  return;
+#endif
+  if (g_dag_trace_on && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_pf_trace[slot] = t;
+  }
+}
+__device__ __forceinline__ void dag_mark(int b, int slot) {
+#ifndef DENSE_TRACE
+  return;
+#endif
+  if (g_dag_trace_on && b == 0 && threadIdx.x == 0 && slot < 128) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_dag_trace[slot] = t;
+  }
+}
+
+
+// POTRF of the 64x64 tile in L (shared, ld LDS, lower triangle) and its
+// inverse into V, by NT threads.  Returns 1 + the first non-positive pivot
+// (uniform over the CTA), or 0.  On success dinv_out (64x64, column-major)
+// receives L^{-1} with zeros above the block diagonal.
+template <int NT>
+__device__ int panel_factor(double* L, double* V, double* dinv_out) {
+  static_assert(NT >= 128, "four warps");
+  __shared__ double rd[64];  // reciprocal diagonal of L_jj
   __shared__ int bad_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const size_t ld = d.n;
-  const double* diag = d.a + (size_t)(j * kTile) * ld + j * kTile;
-  for (int q = tid; q < 64 * 32; q += PANEL_THREADS) {
-    const int col = q >> 5, part = q & 31;
-    cp_async16(L + col * LDS + part * 2, diag + (size_t)col * ld + part * 2);
-  }
-  cp_async_commit();
   if (tid == 0) bad_s = 0;
-  cp_async_wait<0>();
   __syncthreads();
-  // ---- blocked POTRF ----
+  pf_mark(0);
+  // ---- blocked POTRF, 16-wide: warp 0 factors the diagonal block; then warp 0
+  // inverts it (W_kk, into V) while warps 1-2 solve the rows below (thread per
+  // row); the trailing blocks are updated with DMMA, one 16x16 block per warp.
   for (int kb = 0; kb < 4; ++kb) {
     const int o = kb * 16;
     if (warp == 0) {
@@ -278,94 +333,111 @@ __global__ void __launch_bounds__(PANEL_THREADS) k_panel(const FrontDesc* ds, in
       if (lane == 0 && bad && !bad_s) bad_s = o + bad;
     }
     __syncthreads();
-    // panel rows below: x L_kk^T = a  (thread per row)
-    const int r = o + 16 + tid;
-    if (r < 64) {
+    pf_mark(1 + 3 * kb);
+    if (warp == 0) {
+      if (lane < 16) {  // column c of W_kk = L_kk^{-1}, right-looking (short dependency chains)
+        const int c = lane;
+        double x[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) x[r] = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          x[k] = (k >= c) ? x[k] * rd[o + k] : 0.0;
+#pragma unroll
+          for (int r = k + 1; r < 16; ++r) x[r] -= L[(o + k) * LDS + o + r] * x[k];
+        }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) V[(o + c) * LDS + o + r] = x[r];
+      }
+    } else if (tid - 32 < 48 - o) {  // panel rows below: x L_kk^T = a, right-looking
+      const int r = o + 16 + (tid - 32);
       double x[16];
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        double s = L[(o + c) * LDS + r];
+      for (int c = 0; c < 16; ++c) x[c] = L[(o + c) * LDS + r];
 #pragma unroll
-        for (int k = 0; k < c; ++k) s -= x[k] * L[(o + k) * LDS + o + c];
-        x[c] = s * rd[o + c];
+      for (int c = 0; c < 16; ++c) {
+        x[c] *= rd[o + c];
+#pragma unroll
+        for (int c2 = c + 1; c2 < 16; ++c2) x[c2] -= x[c] * L[(o + c) * LDS + o + c2];
       }
 #pragma unroll
       for (int c = 0; c < 16; ++c) L[(o + c) * LDS + r] = x[c];
     }
     __syncthreads();
-    // trailing update of the tile: rows/cols >= o + 16 (lower triangle)
-    const int m = 48 - o;
-    for (int e = tid; e < m * m; e += PANEL_THREADS) {
-      const int rr = o + 16 + e % m, cc = o + 16 + e / m;
-      if (rr < cc) continue;
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < 16; k += 2) {
-        s0 += L[(o + k) * LDS + rr] * L[(o + k) * LDS + cc];
-        s1 += L[(o + k + 1) * LDS + rr] * L[(o + k + 1) * LDS + cc];
+    pf_mark(2 + 3 * kb);
+    // trailing blocks (bi, bj), kb < bj <= bi < 4: C -= X_bi X_bj^T
+    const int nb = 3 - kb, nblk = nb * (nb + 1) / 2;
+    for (int q = warp; q < nblk; q += NT / 32) {
+      int bi = kb + 1, rem = q;
+      while (rem > bi - kb - 1) {
+        rem -= bi - kb;
+        ++bi;
       }
-      L[cc * LDS + rr] -= s0 + s1;
+      const int bj = kb + 1 + rem;
+      double acc[2][4];
+      double* Cb = L + (16 * bj) * LDS + 16 * bi;
+      for_acc16(acc, [&](int m, int n, double& v) { v = Cb[n * LDS + m]; });
+      mma16<true>(acc, L + o * LDS + 16 * bi, 1, LDS, L + o * LDS + 16 * bj, LDS, 1, 16);
+      for_acc16(acc, [&](int m, int n, double& v) { Cb[n * LDS + m] = v; });
     }
     __syncthreads();
+    pf_mark(3 + 3 * kb);
   }
-  if (bad_s) {
-    if (tid == 0) atomicCAS(d.info, 0, j * kTile + bad_s);
-    return;
-  }
-  // ---- L^{-1}: diagonal 16x16 blocks (warp w < 4 inverts block w) ----
-  if (warp < 4 && lane < 16) {
-    const int o = warp * 16, c = lane;
-    double x[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      double s = (r == c) ? 1.0 : 0.0;
-#pragma unroll
-      for (int k = 0; k < r; ++k) s -= L[(o + k) * LDS + o + r] * x[k];
-      x[r] = (r >= c) ? s * rd[o + r] : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < 16; ++r) V[(o + c) * LDS + o + r] = x[r];
-  }
-  __syncthreads();
-  // ---- off-diagonal blocks by block diagonal dd = bi - bj ----
+  const int bad = bad_s;
+  if (bad) return bad;
+  pf_mark(13);
+  // ---- off-diagonal blocks of L^{-1} by block diagonal dd = i - j:
+  //   T = sum_{k=j}^{i-1} L_ik W_kj ;  W_ij = -W_ii T   (one warp per block; T in
+  //   the strictly upper block (0, w + 1) of the tile, unused by the factor)
   for (int dd = 1; dd < 4; ++dd) {
-    const int nblk = 4 - dd;
-    // T_b = sum_{k=bj}^{bi-1} L_{bi,k} Linv_{k,bj}
-    for (int e = tid; e < nblk * 256; e += PANEL_THREADS) {
-      const int b = e >> 8, r = (e >> 4) & 15, c = e & 15;
-      const int bj = b, bi = b + dd;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      for (int k = bj * 16; k < bi * 16; k += 4) {
-        s0 += L[k * LDS + bi * 16 + r] * V[(bj * 16 + c) * LDS + k];
-        s1 += L[(k + 1) * LDS + bi * 16 + r] * V[(bj * 16 + c) * LDS + k + 1];
-        s2 += L[(k + 2) * LDS + bi * 16 + r] * V[(bj * 16 + c) * LDS + k + 2];
-        s3 += L[(k + 3) * LDS + bi * 16 + r] * V[(bj * 16 + c) * LDS + k + 3];
-      }
-      T[b][r][c] = (s0 + s1) + (s2 + s3);
-    }
-    __syncthreads();
-    // Linv_{bi,bj} = -Linv_{bi,bi} T_b
-    for (int e = tid; e < nblk * 256; e += PANEL_THREADS) {
-      const int b = e >> 8, r = (e >> 4) & 15, c = e & 15;
-      const int bj = b, bi = b + dd;
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) s += V[(bi * 16 + k) * LDS + bi * 16 + r] * T[b][k][c];
-      V[(bj * 16 + c) * LDS + bi * 16 + r] = -s;
+    for (int w = warp; w < 4 - dd; w += NT / 32) {
+      const int j = w, i = w + dd;
+      double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+      mma16<false>(acc, L + (16 * j) * LDS + 16 * i, 1, LDS, V + (16 * j) * LDS + 16 * j, 1, LDS, 16 * dd);
+      double* T = L + (16 * (w + 1)) * LDS;
+      for_acc16(acc, [&](int m, int n, double& v) { T[n * LDS + m] = v; });
+      __syncwarp();
+      double acc2[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+      mma16<true>(acc2, V + (16 * i) * LDS + 16 * i, 1, LDS, T, 1, LDS, 16);
+      for_acc16(acc2, [&](int m, int n, double& v) { V[(16 * j + n) * LDS + 16 * i + m] = v; });
     }
     __syncthreads();
   }
-  // Dinv = L^{-1} (zero above the block diagonal).  The diagonal tile itself is
-  // never read again (solves and later updates touch only off-diagonal tiles),
-  // so it is not written back.
-  double2* dv = reinterpret_cast<double2*>(d.dinv + (size_t)j * 64 * 64);
-  for (int q = tid; q < 64 * 32; q += PANEL_THREADS) {
+  pf_mark(14);
+  // Dinv = L^{-1} (zero above the block diagonal).
+  double2* dv = reinterpret_cast<double2*>(dinv_out);
+  for (int q = tid; q < 64 * 32; q += NT) {
     const int c = q >> 5, r = (q & 31) * 2;
     double2 v;
     v.x = (r >> 4) >= (c >> 4) ? V[c * LDS + r] : 0.0;
     v.y = (r >> 4) >= (c >> 4) ? V[c * LDS + r + 1] : 0.0;
     dv[q] = v;
+    V[c * LDS + r] = v.x;  // the dataflow worker multiplies by V directly
+    V[c * LDS + r + 1] = v.y;
   }
+  pf_mark(15);
+  return 0;
+}
+
+__global__ void __launch_bounds__(PANEL_THREADS) k_panel(const FrontDesc* ds, int j) {
+  const FrontDesc d = ds[blockIdx.y];
+  if (j * kTile >= d.p) return;
+  extern __shared__ __align__(16) double smem[];
+  double* L = smem;             // 64 x LDS, column-major: L[c*LDS + r]
+  double* V = smem + 64 * LDS;  // L^{-1} (lower block triangle only)
+  const int tid = threadIdx.x;
+  const size_t ld = d.n;
+  const double* diag = d.a + (size_t)(j * kTile) * ld + j * kTile;
+  for (int q = tid; q < 64 * 32; q += PANEL_THREADS) {
+    const int col = q >> 5, part = q & 31;
+    cp_async16(L + col * LDS + part * 2, diag + (size_t)col * ld + part * 2);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  // The diagonal tile itself is never read again (solves and later updates
+  // touch only off-diagonal tiles), so it is not written back.
+  const int bad = panel_factor<PANEL_THREADS>(L, V, d.dinv + (size_t)j * 64 * 64);
+  if (bad && tid == 0) atomicCAS(d.info, 0, j * kTile + bad);
 }
 
 // Off-diagonal tiles of column j: X = C_ij L_jj^{-T} = C_ij Dinv_j^T as one
@@ -399,6 +471,484 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_trsm(const FrontDesc* ds, int 
   warp_mma(C, V, 64, acc);
   double* out = d.a + (size_t)(j * kTile) * ld + i * kTile;
   for_acc(acc, [&](int m, int n, double v) { out[(size_t)n * ld + m] = v; });
+}
+
+// ---------------------------------------------------------------------------
+// Dataflow partial Cholesky for latency-bound batches: one persistent launch
+// instead of ~3 launches per tile column.  Task (b, i, j) is tile (i, j) of
+// front b; an atomic counter hands the tasks out in a fixed topological order
+// (column j major; within a column the diagonal tiles of every front first,
+// then the off-diagonal rows in increasing i):
+//   j <  p_b/64 : C_ij -= sum_{k<j} L_ik L_jk^T, accumulated as the columns k
+//                 become final; then i == j: L_jj = chol(C_jj), Dinv_j = L_jj^{-1}
+//                 (panel_factor), i > j: L_ij = C_ij Dinv_j^T (one DMMA tile product)
+//   j >= p_b/64 : trailing tile S_ij -= sum_{k<p} L_ik L_jk^T
+// prog[b][i] = 1 + the last column k whose tile (i, k) is final; it is stored
+// with release semantics after the tile (monotone: tile (i, k) is written only
+// after its task has read (i, k-1)).  A task waits only for tasks with smaller
+// indices, which were handed to CTAs that are already running, so the schedule
+// cannot deadlock for any grid size.  The arithmetic is the tiled path's
+// (same K order of the DMMA accumulation, same panel and trsm).
+// ---------------------------------------------------------------------------
+constexpr int DAG_THREADS = 128;
+constexpr int DAG_CTL = 288;  // ints before the progress counters: [0] tasks, [1] roles, [32..288) SM flags
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// acc = sum over K in [kb, ke) of A[i0:i0+64, K] A[j0:j0+64, K]^T, waiting for
+// column block k of rows i0/64 and j0/64 (prog pointers pi, pj) before reading it.
+__device__ void dag_accumulate(const double* a, int ld, int i0, int j0, int kb, int ke, const int* pi,
+                               const int* pj, double (&acc)[2][4][4], double* smem, int* s_ready) {
+  double* As = smem;                 // [2][KC*LDS]
+  double* Bs = smem + 2 * KC * LDS;  // [2][KC*LDS]
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[mi][ni][v] = 0.0;
+  const int nch = (ke - kb) / KC;
+  if (nch <= 0) return;
+  int ready = 0;  // column blocks [0, ready) final for both rows (uniform over the CTA)
+  auto blk = [&](int c) { return (kb + c * KC) >> 6; };
+  auto poll = [&](int need, bool block) {
+    __syncthreads();  // every thread has read the previous s_ready
+    if (threadIdx.x == 0) {
+      int v;
+      do {
+        v = min(ld_acquire(pi), ld_acquire(pj));
+      } while (block && v <= need);
+      *s_ready = v;
+    }
+    __syncthreads();
+    ready = *s_ready;
+  };
+  auto load = [&](int c, int buf) {
+    const int k0 = kb + c * KC;
+    for (int q = threadIdx.x; q < KC * 32; q += DAG_THREADS) {
+      const int col = q >> 5, part = q & 31;
+      const double* srcA = a + (size_t)(k0 + col) * ld + i0 + part * 2;
+      const double* srcB = a + (size_t)(k0 + col) * ld + j0 + part * 2;
+      cp_async16(As + buf * KC * LDS + col * LDS + part * 2, srcA);
+      cp_async16(Bs + buf * KC * LDS + col * LDS + part * 2, srcB);
+    }
+    cp_async_commit();
+  };
+  if (blk(0) >= ready) poll(blk(0), true);
+  load(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    bool pf = false;
+    if (c + 1 < nch) {
+      if (blk(c + 1) >= ready) poll(blk(c + 1), false);
+      pf = blk(c + 1) < ready;
+    }
+    if (pf) {
+      load(c + 1, (c + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    warp_mma(As + (c & 1) * KC * LDS, Bs + (c & 1) * KC * LDS, KC, acc);
+    __syncthreads();
+    if (c + 1 < nch && !pf) {
+      poll(blk(c + 1), true);
+      load(c + 1, (c + 1) & 1);
+    }
+  }
+}
+
+// Diagonal tile j of front b: C_jj -= sum_k L_jk L_jk^T (waiting for the
+// columns), L_jj = chol(C_jj), Dinv_j; publishes prog[j] = j + 1.
+__device__ void dag_diagonal(const FrontDesc& d, int b, int j, int* prog, double* smem, int* s_ready) {
+  const int tid = threadIdx.x, j0 = j * kTile;
+  const size_t ld = d.n;
+  double acc[2][4][4];
+  dag_accumulate(d.a, d.n, j0, j0, 0, j0, prog + j, prog + j, acc, smem, s_ready);
+  dag_mark(b, 2 * j);
+  double* tile = d.a + (size_t)j0 * ld + j0;
+  double* C = smem;
+  double* V = smem + 64 * LDS;
+  for (int q = tid; q < 64 * 32; q += DAG_THREADS) {
+    const int col = q >> 5, part = q & 31;
+    cp_async16(C + col * LDS + part * 2, tile + (size_t)col * ld + part * 2);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  for_acc(acc, [&](int m, int n, double v) { C[n * LDS + m] -= v; });
+  __syncthreads();
+  // keep the updated (unfactored) diagonal tile in the front, as the tiled path does
+  for (int q = tid; q < 64 * 32; q += DAG_THREADS) {
+    const int col = q >> 5, part = q & 31;
+    *reinterpret_cast<double2*>(tile + (size_t)col * ld + part * 2) =
+        *reinterpret_cast<const double2*>(C + col * LDS + part * 2);
+  }
+  const int bad = panel_factor<DAG_THREADS>(C, V, d.dinv + (size_t)j * 64 * 64);
+  if (bad && tid == 0) atomicCAS(d.info, 0, j0 + bad);
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(prog + j, j + 1);
+  }
+  dag_mark(b, 2 * j + 1);
+}
+
+// ctl: [0] task counter, [1] role counter, [DAG_CTL ...] prog[b][i].
+// The first `workers` CTAs to start (they are resident) own the eliminated
+// diagonal tiles of fronts b = role, role + workers, ... column by column,
+// accumulating each tile while its columns arrive; the others take the
+// remaining tasks from the queue.  workers == 0: every task from the queue.
+// Off-diagonal tile (i, j), j < p/64: L_ij = (C_ij - sum_{k<j} L_ik L_jk^T) Dinv_j^T;
+// publishes prog[i] = j + 1.
+__device__ void dag_offdiag(const FrontDesc& d, int i, int j, int* prog, double* smem, int* s_ready) {
+  const int tid = threadIdx.x, i0 = i * kTile, j0 = j * kTile;
+  const size_t ld = d.n;
+  const int kb = aug_k0(d, i0);
+  if (kb > j0) return;  // zero tile of the augmented block
+  double acc[2][4][4];
+  dag_accumulate(d.a, d.n, i0, j0, kb, j0, prog + i, prog + j, acc, smem, s_ready);
+  double* tile = d.a + (size_t)j0 * ld + i0;
+  double* C = smem;
+  double* V = smem + 64 * LDS;
+  for (int q = tid; q < 64 * 32; q += DAG_THREADS) {
+    const int col = q >> 5, part = q & 31;
+    cp_async16(C + col * LDS + part * 2, tile + (size_t)col * ld + part * 2);
+  }
+  cp_async_commit();
+  __syncthreads();
+  if (tid == 0)
+    while (ld_acquire(prog + j) <= j) {
+    }
+  __syncthreads();
+  const double* dv = d.dinv + (size_t)j * 64 * 64;
+  for (int q = tid; q < 64 * 32; q += DAG_THREADS) {
+    const int col = q >> 5, part = q & 31;
+    cp_async16(V + col * LDS + part * 2, dv + (size_t)col * 64 + part * 2);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  for_acc(acc, [&](int m, int n, double v) { C[n * LDS + m] -= v; });
+  __syncthreads();
+  double x[2][4][4];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) x[mi][ni][v] = 0.0;
+  warp_mma(C, V, 64, x);
+  for_acc(x, [&](int m, int n, double v) { tile[(size_t)n * ld + m] = v; });
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(prog + i, j + 1);
+  }
+}
+
+// tile (64x64 at t, ld) -= acc, staged through shared memory so that the
+// global read-modify-write is coalesced (16-byte accesses along columns).
+// Call after dag_accumulate (its trailing barrier frees the operand buffers).
+__device__ __forceinline__ void tile_sub_acc(double* t, size_t ld, double (&acc)[2][4][4], double* smem) {
+  for_acc(acc, [&](int m, int n, double v) { smem[n * LDS + m] = v; });
+  __syncthreads();
+  for (int q = threadIdx.x; q < 64 * 32; q += DAG_THREADS) {
+    const int col = q >> 5, part = q & 31;
+    double2* g = reinterpret_cast<double2*>(t + (size_t)col * ld + part * 2);
+    const double2 a = *reinterpret_cast<const double2*>(smem + col * LDS + part * 2);
+    double2 v = *g;
+    v.x -= a.x;
+    v.y -= a.y;
+    *g = v;
+  }
+}
+
+// Trailing tile (i, j), i >= j >= p/64: S_ij -= sum over K in [kb, ke) of L_iK L_jK^T.
+__device__ void dag_trailing(const FrontDesc& d, int i, int j, int kb, int ke, int* prog, double* smem,
+                             int* s_ready) {
+  const int i0 = i * kTile, j0 = j * kTile;
+  double acc[2][4][4];
+  dag_accumulate(d.a, d.n, i0, j0, kb, ke, prog + i, prog + j, acc, smem, s_ready);
+  tile_sub_acc(d.a + (size_t)j0 * d.n + i0, d.n, acc, smem);
+}
+
+__device__ __forceinline__ void wait_flag(const int* f, int v) {
+  __syncthreads();
+  if (threadIdx.x == 0)
+    while (ld_acquire(f) < v) {
+    }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void load_tile(double* dst, const double* src, size_t ld) {
+  for (int q = threadIdx.x; q < 64 * 32; q += DAG_THREADS) {
+    const int col = q >> 5, part = q & 31;
+    cp_async16(dst + col * LDS + part * 2, src + (size_t)col * ld + part * 2);
+  }
+  cp_async_commit();
+}
+
+// Diagonal worker of one front (chunked mode).  Iteration j, with
+// C = C_jj - sum_{k<j} L_jk L_jk^T already in shared memory:
+//   L_jj = chol(C), Dinv_j (panel_factor; V keeps L_jj^{-1})      -> prog[j] = j+1
+//   L_{j+1,j} = C'_{j+1,j} Dinv_j^T (C' prepared by a queue task)    -> prog[j+1] = j+1
+//   C = C'_{j+1,j+1} - L_{j+1,j} L_{j+1,j}^T                        (next pivot tile)
+// so the pivot chain never leaves the SM: the queue prepares the tiles
+// (every column but the last), the worker applies the last one.
+__device__ void dag_worker(const FrontDesc& d, int b, int* prog, const int* presub, const int* prediag,
+                           double* smem) {
+  const int tid = threadIdx.x, pt = d.p / kTile, nt = d.n / kTile;
+  const size_t ld = d.n;
+  double* C = smem;
+  double* V = smem + 64 * LDS;
+  if (pt == 0) return;
+  load_tile(C, d.a, ld);
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int j = 0; j < pt; ++j) {
+    const int j0 = j * kTile;
+    double* tile = d.a + (size_t)j0 * ld + j0;
+    dag_mark(b, 2 * j);
+    // keep the updated (unfactored) diagonal tile in the front, as the tiled path does
+    for (int q = tid; q < 64 * 32; q += DAG_THREADS) {
+      const int col = q >> 5, part = q & 31;
+      *reinterpret_cast<double2*>(tile + (size_t)col * ld + part * 2) =
+          *reinterpret_cast<const double2*>(C + col * LDS + part * 2);
+    }
+    const int bad = panel_factor<DAG_THREADS>(C, V, d.dinv + (size_t)j * 64 * 64);
+    if (bad && tid == 0) atomicCAS(d.info, 0, j0 + bad);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(prog + j, j + 1);
+    }
+    dag_mark(b, 2 * j + 1);
+    const int i = j + 1, i0 = i * kTile;
+    if (i >= nt || aug_k0(d, i0) > j0) continue;  // no sub-diagonal tile (or a zero one)
+    double* sub = d.a + (size_t)j0 * ld + i0;
+    if (j > 0) wait_flag(presub + j, 1);
+    load_tile(C, sub, ld);
+    cp_async_wait<0>();
+    __syncthreads();
+    double x[2][4][4];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) x[mi][ni][v] = 0.0;
+    warp_mma(C, V, 64, x);
+    __syncthreads();  // C and V are read by every warp
+    for_acc(x, [&](int m, int n, double v) {
+      sub[(size_t)n * ld + m] = v;
+      C[n * LDS + m] = v;
+    });
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(prog + i, j + 1);
+    }
+    if (i >= pt) continue;
+    // next pivot tile: C'_{i,i} (prepared through column j-1) minus L_ij L_ij^T
+    if (i >= 2) wait_flag(prediag + i, 1);
+    double* diag = d.a + (size_t)i0 * ld + i0;
+    load_tile(V, diag, ld);
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) x[mi][ni][v] = 0.0;
+    warp_mma(C, C, 64, x);
+    cp_async_wait<0>();
+    __syncthreads();
+    for_acc(x, [&](int m, int n, double v) { C[n * LDS + m] = V[n * LDS + m] - v; });
+    __syncthreads();
+  }
+}
+
+// Queue task preparing tile (i, j) for the worker: C_ij -= sum over K in
+// [kb, ke) of L_iK L_jK^T, stored in place; then flag = 1.
+__device__ void dag_prepare(const FrontDesc& d, int i, int j, int kb, int ke, int* prog, int* flag, double* smem,
+                            int* s_ready) {
+  if (ke > kb) {
+    const int i0 = i * kTile, j0 = j * kTile;
+    double acc[2][4][4];
+    dag_accumulate(d.a, d.n, i0, j0, kb, ke, prog + i, prog + j, acc, smem, s_ready);
+    tile_sub_acc(d.a + (size_t)j0 * d.n + i0, d.n, acc, smem);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(flag, 1);
+  }
+}
+
+// ctl: [0] task counter (A), [1] role counter, [2] queue CTAs that left, [3] queue roles,
+// [4] task counter (B), [32, 288) per-SM worker flags,
+// [DAG_CTL ...] prog[b][i] (batch x nt); chunked mode adds tflag[b][ii * mt + jj]
+// (batch x mt x mt), presub[b][j] and prediag[b][j] (batch x nt each).
+//
+// Plain mode (chunked == 0): the queue holds every tile, column j major
+// (diagonals of every front, then the off-diagonal rows); trailing tiles are
+// single tasks over the whole K range.
+// Chunked mode (small batches): the first `batch` CTAs to start are the
+// fronts' diagonal workers (dag_worker); queue CTAs that land on a worker's SM
+// leave, so the pivot chain runs on an otherwise idle SM.  Two queues:
+//   A = E_0, E_1, ..., E_{pt-1}   and   B = R_0, R_1, ..., R_{pt-1}
+// E_c = [L_{c+2,c}] [prepare (c+2, c+1) through column c] [prepare (c+2, c+2)
+// through column c] [L_{i,c}, i >= c+3]  (every front each), R_k = the updates
+// of every trailing tile by the columns [k cw, (k+1) cw) (chunk k of a tile waits for chunk
+// k-1 of the same tile).  Half of the queue CTAs take B only; the others take A
+// and then B.  A waits only on A and the workers, B on A and B: no cycle.
+__global__ void __launch_bounds__(DAG_THREADS) k_chol_dag(const FrontDesc* ds, int batch, int nt, int pt_max,
+                                                          int mt, int* ctl, int total, int chunked, int cw) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_task, s_ready;
+  const int tid = threadIdx.x;
+  int* tflag = ctl + DAG_CTL + (size_t)batch * nt;
+  int* presub = tflag + (size_t)batch * mt * mt;
+  int* prediag = presub + (size_t)batch * nt;
+  if (chunked) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (tid == 0) s_task = atomicAdd(ctl + 1, 1);
+    __syncthreads();
+    const int role = s_task;
+    __syncthreads();
+    if (role < batch) {
+      if (tid == 0) atomicExch(ctl + 32 + (smid & 255), 1);
+      const FrontDesc d = ds[role];
+      dag_worker(d, role, ctl + DAG_CTL + (size_t)role * nt, presub + (size_t)role * nt,
+                 prediag + (size_t)role * nt, smem);
+      return;
+    }
+    // share no SM with a worker, but keep at least half of the queue CTAs
+    if (tid == 0) s_task = atomicAdd(ctl + 32 + (smid & 255), 0) && atomicAdd(ctl + 2, 1) < (gridDim.x - batch) / 2;
+    __syncthreads();
+    if (s_task) return;
+  }
+  const int rsize = batch * (mt * (mt + 1) / 2);
+  // chunked mode: queue A = E_0 .. E_{pt-1} (elimination), queue B = R_0 .. R_{pt-1}
+  // (trailing updates).  Every other queue CTA works on B only, so the trailing
+  // updates never hold back the elimination; A CTAs move on to B when A is empty.
+  int etotal = 0;
+  if (chunked)
+    for (int c = 0; c < pt_max; ++c) etotal += batch * (max(nt - c - 2, 0) + 2);
+  bool on_b = false;
+  if (chunked) {
+    if (tid == 0) s_task = atomicAdd(ctl + 3, 1);
+    __syncthreads();
+    on_b = s_task & 1;
+  }
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) {
+      int t = total;
+      if (!chunked || !on_b) {
+        t = atomicAdd(ctl, 1);
+        if (chunked && t >= etotal) on_b = true;
+      }
+      if (chunked && on_b) t = etotal + atomicAdd(ctl + 4, 1);
+      s_task = t;
+    }
+    __syncthreads();
+    const int t = s_task;
+    if (t >= total) return;
+    if (chunked && t >= etotal) on_b = true;
+    if (!chunked) {
+      int j = 0, r = t;
+      while (r >= batch * (nt - j)) {
+        r -= batch * (nt - j);
+        ++j;
+      }
+      int b, i;
+      if (r < batch) {
+        b = r;
+        i = j;
+      } else {
+        r -= batch;
+        i = j + 1 + r / batch;
+        b = r % batch;
+      }
+      const FrontDesc d = ds[b];
+      if (i * kTile >= d.n) continue;
+      int* prog = ctl + DAG_CTL + (size_t)b * nt;
+      const int pt = d.p / kTile;
+      if (j < pt) {
+        if (i == j) dag_diagonal(d, b, j, prog, smem, &s_ready);
+        else dag_offdiag(d, i, j, prog, smem, &s_ready);
+      } else if (d.p > 0) {
+        dag_trailing(d, i, j, min(aug_k0(d, i * kTile), d.p), d.p, prog, smem, &s_ready);
+      }
+      continue;
+    }
+    int r = t, kind = 0, col = 0;  // kind 0: E_col, 1: R_col
+    if (t < etotal) {
+      for (col = 0;; ++col) {
+        const int es = batch * (max(nt - col - 2, 0) + 2);
+        if (r < es) break;
+        r -= es;
+      }
+    } else {
+      kind = 1;
+      r = t - etotal;
+      col = r / rsize;
+      r -= col * rsize;
+    }
+    if (kind == 0) {
+      const int b = r % batch, slot = r / batch;
+      const FrontDesc d = ds[b];
+      const int pt = d.p / kTile, ntb = d.n / kTile;
+      if (col >= pt) continue;
+      int* prog = ctl + DAG_CTL + (size_t)b * nt;
+      if (slot == 1 || slot == 2) {
+        // slot 1: tile (c+2, c+1) for the worker's sub-diagonal solve of column c+1;
+        // slot 2: tile (c+2, c+2), the worker's next pivot tile but one
+        const int i = col + 2, j = slot == 1 ? col + 1 : col + 2;
+        if (i >= ntb || j >= pt) continue;
+        const int kb = aug_k0(d, i * kTile);
+        if (kb > (col + 1) * kTile) continue;  // zero tile: the worker skips it too
+        dag_prepare(d, i, j, kb, (col + 1) * kTile, prog,
+                    (slot == 1 ? presub : prediag) + (size_t)b * nt + j, smem, &s_ready);
+      } else {
+        const int i = slot == 0 ? col + 2 : col + slot;
+        if (i >= ntb) continue;
+        dag_offdiag(d, i, col, prog, smem, &s_ready);
+      }
+    } else {
+      const int b = r % batch, q = r / batch;
+      int ii = static_cast<int>((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+      while (ii * (ii + 1) / 2 > q) --ii;
+      while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
+      const int jj = q - ii * (ii + 1) / 2;
+      const FrontDesc d = ds[b];
+      const int pt = d.p / kTile, i = pt + ii, j = pt + jj;
+      if (i * kTile >= d.n) continue;
+      // chunk col: columns [col * cw, (col + 1) * cw) of the K range, which starts
+      // at the first nonzero column of row i (augmented rows)
+      const int kz = min(aug_k0(d, i * kTile), d.p);
+      const int kb = max(col * cw * kTile, kz), ke = min((col + 1) * cw * kTile, d.p);
+      if (kb >= ke) continue;
+      const int c0 = kz / (cw * kTile);  // first chunk with work
+      int* flag = tflag + ((size_t)b * mt + ii) * mt + jj;
+      wait_flag(flag, col - c0);
+      dag_trailing(d, i, j, kb, ke, ctl + DAG_CTL + (size_t)b * nt, smem, &s_ready);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        st_release(flag, col - c0 + 1);
+      }
+    }
+  }
 }
 
 // Forward sweep, one CTA per front (fronts that fill the GPU on their own):
@@ -843,10 +1393,78 @@ int sm_count() {
 void count_launch(long long n) { g_launches += n; }
 long long launch_count() { return g_launches.load(); }
 
+void chol_trace(bool on, unsigned long long* out) {
+  const int v = on ? 1 : 0;
+  cudaMemcpyToSymbol(g_dag_trace_on, &v, sizeof(int));
+  if (out) {
+    cudaMemcpyFromSymbol(out, g_dag_trace, sizeof(unsigned long long) * 128);
+    cudaMemcpyFromSymbol(out + 128, g_pf_trace, sizeof(unsigned long long) * 16);
+  }
+}
+
+namespace {
+// Dataflow schedule (k_chol_dag; measured faster than the tiled launches on
+// every front kind of configs 1-5) or one launch per tile-column step (tiled).
+// BDDC_B200_CHOL=dag|tiled overrides.
+bool use_dag(int batch, int nt, int pt) {
+  if (const char* env = std::getenv("BDDC_B200_CHOL"); env && *env) {
+    if (std::string(env) == "dag") return true;
+    if (std::string(env) == "tiled") return false;
+  }
+  (void)batch;
+  (void)nt;
+  (void)pt;
+  return true;
+}
+
+void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, int mt, cudaStream_t stream) {
+  const int smem = 4 * KC * LDS * sizeof(double);
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_dag, DAG_THREADS, smem);
+    if (per_sm <= 0) per_sm = 1;
+  }
+  const long resident = (long)per_sm * sm_count();
+  // chunked mode (dedicated diagonal workers, trailing updates per column) when
+  // the fronts leave most of the grid to the queue; BDDC_B200_DAGW=0|1 overrides
+  bool chunked = 2L * batch <= sm_count() && resident >= 2L * sm_count();
+  if (const char* e = std::getenv("BDDC_B200_DAGW"); e && *e) chunked = *e == '1' && 2L * batch <= sm_count();
+  long total;
+  int cw = 1;
+  size_t ints = DAG_CTL + (size_t)batch * nt;
+  if (chunked) {
+    cw = std::max(1, (pt + 2) / 3);  // about three trailing chunks per tile
+    if (const char* e = std::getenv("BDDC_B200_DAGCW"); e && *e) cw = std::max(1, std::atoi(e));
+    const int nchunk = (pt + cw - 1) / cw;
+    total = (long)nchunk * batch * mt * (mt + 1) / 2;
+    for (int c = 0; c < pt; ++c) total += (long)batch * (std::max(nt - c - 2, 0) + 2);
+    ints += (size_t)batch * mt * mt + 2 * (size_t)batch * nt;
+  } else {
+    total = (long)batch * nt * (nt + 1) / 2;
+  }
+  int* ctl = reinterpret_cast<int*>(stream_workspace(2, (ints + 1) / 2, stream));
+  if (!ctl) throw std::runtime_error("partial_cholesky: workspace allocation failed");
+  cudaMemsetAsync(ctl, 0, ints * sizeof(int), stream);
+  const int grid = static_cast<int>(std::min<long>(total + (chunked ? batch : 0), resident));
+  k_chol_dag<<<grid, DAG_THREADS, smem, stream>>>(d_descs, batch, nt, pt, mt, ctl, static_cast<int>(total),
+                                                 chunked ? 1 : 0, cw);
+  count_launch(1);
+}
+}  // namespace
+
 void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p, int max_m,
                       cudaStream_t stream) {
   if (batch == 0) return;
   configure();
+  static const bool dbg = std::getenv("BDDC_B200_CHOLDBG") != nullptr;
+  if (dbg)
+    std::fprintf(stderr, "[chol] batch %d n %d p %d m %d -> %s\n", batch, max_n, max_p, max_m,
+                 max_p > 0 && use_dag(batch, max_n / kTile, max_p / kTile) ? "dag" : "tiled");
+  if (max_p > 0 && use_dag(batch, max_n / kTile, max_p / kTile)) {
+    partial_cholesky_dag(d_descs, batch, max_n / kTile, max_p / kTile, max_m / kTile, stream);
+    return;
+  }
   const int gemm_smem = 4 * KC * LDS * sizeof(double);
   const int panel_smem = 2 * 64 * LDS * sizeof(double);
   const int nt = max_n / kTile, pt = max_p / kTile;

@@ -51,6 +51,11 @@ int sm_count();
 void count_launch(long long n);
 long long launch_count();
 
+/// Timestamps (ns) of front 0's diagonal tasks in the dataflow schedule:
+/// out[2j] accumulation done, out[2j+1] Dinv_j published; out[128..143] phase
+/// stamps of the first panel factorization (tools/chol_bench).
+void chol_trace(bool on, unsigned long long* out);
+
 /// Partial Cholesky of a batch of fronts (device descriptor array).
 /// max_n/max_p bound the descriptors' n/p.  Launches on `stream`.
 /// max_m bounds the trailing dimension n - p.

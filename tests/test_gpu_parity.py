@@ -285,3 +285,21 @@ def test_primal_tree_adaptive(monkeypatch):
     g = b.pcg()
     kg, ko = kappa_common(g["alphas"], g["betas"], ref.pcg.alphas, ref.pcg.betas)
     assert abs(kg - ko) <= KAPPA_RTOL * ko
+
+
+@pytest.mark.parametrize("chol", ["dag", "tiled"])
+@pytest.mark.parametrize("case", [ADAPTIVE[5], ADAPTIVE[7], ADAPTIVE[8]], ids=["cfg2", "cfg4 3x3x3", "cfg5 3x3x3"])
+def test_cholesky_schedules_adaptive(chol, case, monkeypatch):
+    """Both partial-Cholesky schedules (dense.cu: dataflow k_chol_dag, one
+    persistent launch; tiled, three launches per tile column) on every front
+    kind: leaves, pair side fronts, eigenproblem reductions, transformed leaves,
+    primal tree and root."""
+    monkeypatch.setenv("BDDC_B200_CHOL", chol)
+    test_adaptive_selection_and_spectrum(*case)
+
+
+@pytest.mark.parametrize("chol", ["dag", "tiled"])
+@pytest.mark.parametrize("leaf,root", [("explicit", "inverse"), ("factor", "sweep")])
+def test_cholesky_schedules_operators(chol, leaf, root, monkeypatch):
+    monkeypatch.setenv("BDDC_B200_CHOL", chol)
+    test_operators_pcg_and_solution(*OPS[-1], leaf, root, "0", monkeypatch)
