@@ -493,6 +493,14 @@ __global__ void __launch_bounds__(GEMM_THREADS) k_trsm(const FrontDesc* ds, int 
 constexpr int DAG_THREADS = 128;
 constexpr int DAG_CTL = 288;  // ints before the progress counters: [0] tasks, [1] roles, [32..288) SM flags
 
+// Polls read the flags relaxed (an acquire load invalidates L1 on every
+// iteration); one acquire fence follows the successful poll.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -523,8 +531,9 @@ __device__ void dag_accumulate(const double* a, int ld, int i0, int j0, int kb, 
     if (threadIdx.x == 0) {
       int v;
       do {
-        v = min(ld_acquire(pi), ld_acquire(pj));
+        v = min(ld_relaxed(pi), ld_relaxed(pj));
       } while (block && v <= need);
+      fence_acquire();
       *s_ready = v;
     }
     __syncthreads();
@@ -625,8 +634,9 @@ __device__ void dag_offdiag(const FrontDesc& d, int i, int j, int* prog, double*
   cp_async_commit();
   __syncthreads();
   if (tid == 0)
-    while (ld_acquire(prog + j) <= j) {
+    while (ld_relaxed(prog + j) <= j) {
     }
+  if (tid == 0) fence_acquire();
   __syncthreads();
   const double* dv = d.dinv + (size_t)j * 64 * 64;
   for (int q = tid; q < 64 * 32; q += DAG_THREADS) {
@@ -683,8 +693,9 @@ __device__ void dag_trailing(const FrontDesc& d, int i, int j, int kb, int ke, i
 __device__ __forceinline__ void wait_flag(const int* f, int v) {
   __syncthreads();
   if (threadIdx.x == 0)
-    while (ld_acquire(f) < v) {
+    while (ld_relaxed(f) < v) {
     }
+  if (threadIdx.x == 0) fence_acquire();
   __syncthreads();
 }
 
@@ -870,14 +881,16 @@ __global__ void __launch_bounds__(DAG_THREADS) k_chol_dag(const FrontDesc* ds, i
         r -= batch * (nt - j);
         ++j;
       }
+      // within a column: every front's diagonal tile, then the rows front by
+      // front (consecutive tasks share the front's row-j panel in L2)
       int b, i;
       if (r < batch) {
         b = r;
         i = j;
       } else {
         r -= batch;
-        i = j + 1 + r / batch;
-        b = r % batch;
+        b = r / (nt - j - 1);
+        i = j + 1 + r % (nt - j - 1);
       }
       const FrontDesc d = ds[b];
       if (i * kTile >= d.n) continue;
