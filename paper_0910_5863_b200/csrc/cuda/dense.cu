@@ -821,7 +821,7 @@ __device__ void dag_prepare(const FrontDesc& d, int i, int j, int kb, int ke, in
 // k-1 of the same tile).  Half of the queue CTAs take B only; the others take A
 // and then B.  A waits only on A and the workers, B on A and B: no cycle.
 __global__ void __launch_bounds__(DAG_THREADS) k_chol_dag(const FrontDesc* ds, int batch, int nt, int pt_max,
-                                                          int mt, int* ctl, int total, int chunked, int cw) {
+                                                          int mt, int* ctl, int total, int chunked, int cw, int bq) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_task, s_ready;
   const int tid = threadIdx.x;
@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(DAG_THREADS) k_chol_dag(const FrontDesc* ds, i
   if (chunked) {
     if (tid == 0) s_task = atomicAdd(ctl + 3, 1);
     __syncthreads();
-    on_b = s_task & 1;
+    on_b = (s_task % 12) < bq;  // bq twelfths of the queue CTAs serve B only
   }
   for (;;) {
     __syncthreads();
@@ -1444,7 +1444,8 @@ void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, i
   bool chunked = 2L * batch <= sm_count() && resident >= 2L * sm_count();
   if (const char* e = std::getenv("BDDC_B200_DAGW"); e && *e) chunked = *e == '1' && 2L * batch <= sm_count();
   long total;
-  int cw = 1;
+  int cw = 1, bq = 6;
+  if (const char* e = std::getenv("BDDC_B200_DAGBQ"); e && *e) bq = std::min(11, std::max(0, std::atoi(e)));
   size_t ints = DAG_CTL + (size_t)batch * nt;
   if (chunked) {
     cw = std::max(1, (pt + 2) / 3);  // about three trailing chunks per tile
@@ -1461,7 +1462,7 @@ void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, i
   cudaMemsetAsync(ctl, 0, ints * sizeof(int), stream);
   const int grid = static_cast<int>(std::min<long>(total + (chunked ? batch : 0), resident));
   k_chol_dag<<<grid, DAG_THREADS, smem, stream>>>(d_descs, batch, nt, pt, mt, ctl, static_cast<int>(total),
-                                                 chunked ? 1 : 0, cw);
+                                                 chunked ? 1 : 0, cw, bq);
   count_launch(1);
 }
 }  // namespace
