@@ -985,17 +985,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 __device__ __forceinline__ double grid_sum(const double* part, int G) {
-  // every CTA: the same fixed-order sum of the G partials
-  __shared__ double red[256];
+  // every CTA: the same fixed-order sum of the G partials (thread sums, warp
+  // shuffles, then the warps' sums in order)
+  __shared__ double red[32];
   double v = 0.0;
   for (int i = threadIdx.x; i < G; i += blockDim.x) v += part[i];
-  red[threadIdx.x] = v;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
   __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
-  const double out = red[0];
+  double out = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) out += red[w];
   __syncthreads();
   return out;
 }
@@ -2580,7 +2581,9 @@ bool persistent_pcg(DeviceState& D) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_persistent, 256, smem));
     D.pcg_smem = smem;
-    D.pcg_grid = per_sm < 1 ? -1 : sm_count() * std::min(per_sm, 2);
+    int cap = 2;  // CTAs per SM (BDDC_B200_PCG_PERSM overrides)
+    if (const char* e = std::getenv("BDDC_B200_PCG_PERSM"); e && *e) cap = std::max(1, std::atoi(e));
+    D.pcg_grid = per_sm < 1 ? -1 : sm_count() * std::min(per_sm, cap);
   }
   return D.pcg_grid > 0;
 }
