@@ -511,19 +511,23 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
           s3 += row[c + 3] * v[c + 3];
         }
         for (; c <= r; ++c) s0 += row[c] * v[c];
-        int c2 = r + 1;
-        size_t q = pk(c2, r);  // column r below the diagonal: stride grows by one per row
+        // column r below the diagonal: the warp walks the rows c2 together, so
+        // its 32 lanes read 32 consecutive entries of packed row c2 (coalesced)
+        const int base = r - (tid & 31);
+        int c2 = base + 1;
         for (; c2 + 3 < n; c2 += 4) {
-          s1 += L[q] * v[c2];
-          s2 += L[q + c2 + 1] * v[c2 + 1];
-          s3 += L[q + 2 * c2 + 3] * v[c2 + 2];
-          s0 += L[q + 3 * c2 + 6] * v[c2 + 3];
-          q += 4 * c2 + 10;
+          const double* q = L + pk(c2, 0);
+          const double a0 = c2 > r ? q[r] : 0.0;
+          const double a1 = c2 + 1 > r ? q[c2 + 1 + r] : 0.0;
+          const double a2 = c2 + 2 > r ? q[2 * c2 + 3 + r] : 0.0;
+          const double a3 = c2 + 3 > r ? q[3 * c2 + 6 + r] : 0.0;
+          s1 += a0 * v[c2];
+          s2 += a1 * v[c2 + 1];
+          s3 += a2 * v[c2 + 2];
+          s0 += a3 * v[c2 + 3];
         }
-        for (; c2 < n; ++c2) {
-          s1 += L[q] * v[c2];
-          q += c2 + 1;
-        }
+        for (; c2 < n; ++c2)
+          if (c2 > r) s1 += L[pk(c2, r)] * v[c2];
         p[r] = t * ((s0 + s1) + (s2 + s3));
       }
       __syncthreads();
@@ -1450,7 +1454,10 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       const int maxn = maxn2;  // >= every nj
       const long need = (long)maxn * (maxn + 1) / 2 + 6L * maxn + 7L * maxn * std::max(maxk, 1);
       const long cap = (220 * 1024) / 8;  // leaves room for the kernel's static arrays
-      const bool smem_ok = need <= cap;
+      // shared memory holds one CTA per SM here; with more pairs than SMs the
+      // global-memory placement (about four CTAs per SM) takes fewer waves
+      bool smem_ok = need <= cap && nb <= sm_count();
+      if (const char* e = std::getenv("BDDC_B200_SYEVX"); e && *e) smem_ok = *e == 'S' && need <= cap;
       // all in shared memory when it fits; otherwise only the 6n vectors, so that
       // several CTAs share an SM and hide the L2 latency of the packed matrix
       const long dyn = smem_ok ? need : 6L * maxn;
