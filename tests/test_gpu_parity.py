@@ -303,3 +303,11 @@ def test_cholesky_schedules_adaptive(chol, case, monkeypatch):
 def test_cholesky_schedules_operators(chol, leaf, root, monkeypatch):
     monkeypatch.setenv("BDDC_B200_CHOL", chol)
     test_operators_pcg_and_solution(*OPS[-1], leaf, root, "0", monkeypatch)
+
+
+@pytest.mark.parametrize("placement", ["S", "G"])
+def test_pair_eigensolver_placements(placement, monkeypatch):
+    """k_syevx with the packed matrix in shared memory (S) and in global memory
+    (G, the placement when the pairs outnumber the SMs) against the oracle."""
+    monkeypatch.setenv("BDDC_B200_SYEVX", placement)
+    test_adaptive_selection_and_spectrum(*ADAPTIVE[5])
