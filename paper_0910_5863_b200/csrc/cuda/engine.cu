@@ -481,47 +481,126 @@ __global__ void k_rowxform_scatter(const SubDesc* sd, XformDesc x, const double*
 }
 
 // F = P_F (T^T S T) P_F^T in one pass (factor mode: ld F = NF): CTA (c, s)
-// forms column c of S T in shared memory (the glob columns combine r + 1
-// columns of S), applies T^T on the rows and writes the whole F column,
-// padding rows included; CTAs beyond nB write the padding columns (unit
-// vectors).  Every entry of F is written: no scratch X, no memset.
+// forms kXformCols columns of S T in shared memory (a glob column combines
+// r + 1 columns of S; when the CTA's columns share one glob instance the r
+// pivot columns are read once for all of them), applies T^T on the rows and
+// writes the whole F columns, padding rows included; columns beyond nB are the
+// padding columns (unit vectors).  Every entry of F is written: no scratch X,
+// no memset.
+constexpr int kXformCols = 4;  // F columns per CTA in k_xform_fused
+
 __global__ void __launch_bounds__(256) k_xform_fused(const SubDesc* sd, XformDesc x) {
   const SubDesc d = sd[blockIdx.y];
-  extern __shared__ double y[];
-  const int c = blockIdx.x, nE = d.nE, nC = d.nB - d.nE;
+  extern __shared__ double y[];  // [kXformCols][nB]: columns of S T
+  const int c0 = blockIdx.x * kXformCols, nE = d.nE, nC = d.nB - d.nE;
   const size_t ld = d.ldF;
-  if (c < d.nB) {
-    const int inst = d.bglob[c];
-    if (inst < 0) {
-      const double* sc = d.S + (size_t)c * d.PB;
-      for (int b = threadIdx.x; b < d.nB; b += blockDim.x) y[b] = sc[b];
-    } else {
-      const int j = d.bslot[c];
-      const int tr = x.inst_tr[inst];
-      const int* pos = x.tpos + x.inst_pos[inst];
-      const int n = x.tr_n[tr], r = x.tr_r[tr];
-      const int* perm = x.perm + x.tr_off_perm[tr];
-      const double* D = x.D + x.tr_off_d[tr];
-      for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
-        double s = j >= r ? d.S[(size_t)pos[perm[j]] * d.PB + b] : 0.0;
-        for (int i = 0; i < r; ++i) s += D[i * n + j] * d.S[(size_t)pos[perm[i]] * d.PB + b];
-        y[b] = s;
+  int inst[kXformCols];
+#pragma unroll
+  for (int k = 0; k < kXformCols; ++k) inst[k] = c0 + k < d.nB ? d.bglob[c0 + k] : -2;
+  bool same = inst[0] >= 0;
+#pragma unroll
+  for (int k = 1; k < kXformCols; ++k) same = same && inst[k] == inst[0];
+  if (same) {
+    // the CTA's columns belong to one glob instance: the r pivot columns of S
+    // are read once for all of them (S T column j = S e_{cp[j]} [j >= r] + sum_i D_ij S e_{cp[i]})
+    const int tr = x.inst_tr[inst[0]];
+    const int* cp = x.cpos + x.inst_pos[inst[0]];  // cp[i] = tpos[perm[i]]
+    const int n = x.tr_n[tr], r = x.tr_r[tr];
+    const double* D = x.D + x.tr_off_d[tr];
+    int j[kXformCols];
+#pragma unroll
+    for (int k = 0; k < kXformCols; ++k) j[k] = d.bslot[c0 + k];
+    for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
+      double acc[kXformCols];
+#pragma unroll
+      for (int k = 0; k < kXformCols; ++k) acc[k] = j[k] >= r ? d.S[(size_t)cp[j[k]] * d.PB + b] : 0.0;
+      for (int i = 0; i < r; ++i) {
+        const double sv = d.S[(size_t)cp[i] * d.PB + b];
+#pragma unroll
+        for (int k = 0; k < kXformCols; ++k) acc[k] += D[i * n + j[k]] * sv;
+      }
+#pragma unroll
+      for (int k = 0; k < kXformCols; ++k) y[k * d.nB + b] = acc[k];
+    }
+  } else {
+    for (int k = 0; k < kXformCols; ++k) {
+      const int c = c0 + k;
+      if (c >= d.nB) break;
+      double* yk = y + k * d.nB;
+      if (inst[k] < 0) {
+        const double* sc = d.S + (size_t)c * d.PB;
+        for (int b = threadIdx.x; b < d.nB; b += blockDim.x) yk[b] = sc[b];
+      } else {
+        const int jj = d.bslot[c];
+        const int tr = x.inst_tr[inst[k]];
+        const int* cp = x.cpos + x.inst_pos[inst[k]];
+        const int n = x.tr_n[tr], r = x.tr_r[tr];
+        const double* D = x.D + x.tr_off_d[tr];
+        for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
+          double acc = jj >= r ? d.S[(size_t)cp[jj] * d.PB + b] : 0.0;
+          for (int i = 0; i < r; ++i) acc += D[i * n + jj] * d.S[(size_t)cp[i] * d.PB + b];
+          yk[b] = acc;
+        }
       }
     }
-    __syncthreads();
-    double* fcol = d.F + (size_t)d.posF[c] * ld;
+  }
+  __syncthreads();
+  // T^T on the rows of all the CTA's columns at once (the row's D and cp loads
+  // are shared by the columns)
+  const int ncol = min(kXformCols, d.nB - c0);
+  if (ncol == kXformCols) {
+    double* fcol[kXformCols];
+#pragma unroll
+    for (int k = 0; k < kXformCols; ++k) fcol[k] = d.F + (size_t)d.posF[c0 + k] * ld;
     for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
-      const int inst = d.bglob[b];
-      fcol[d.posF[b]] = inst < 0 ? y[b] : xform_T_t(x, inst, d.bslot[b], y);
+      const int ib = d.bglob[b], fb = d.posF[b];
+      if (ib < 0) {
+#pragma unroll
+        for (int k = 0; k < kXformCols; ++k) fcol[k][fb] = y[k * d.nB + b];
+        continue;
+      }
+      const int tr = x.inst_tr[ib], jb = d.bslot[b];
+      const int* cp = x.cpos + x.inst_pos[ib];
+      const int n = x.tr_n[tr], r = x.tr_r[tr];
+      const double* D = x.D + x.tr_off_d[tr];
+      double acc[kXformCols];
+      const int cj = jb >= r ? cp[jb] : 0;
+#pragma unroll
+      for (int k = 0; k < kXformCols; ++k) acc[k] = jb >= r ? y[k * d.nB + cj] : 0.0;
+      for (int i = 0; i < r; ++i) {
+        const double dd = D[i * n + jb];
+        const int ci = cp[i];
+#pragma unroll
+        for (int k = 0; k < kXformCols; ++k) acc[k] += dd * y[k * d.nB + ci];
+      }
+#pragma unroll
+      for (int k = 0; k < kXformCols; ++k) fcol[k][fb] = acc[k];
     }
-    for (int q = nE + threadIdx.x; q < d.PE; q += blockDim.x) fcol[q] = 0.0;
-    for (int q = d.PE + nC + threadIdx.x; q < d.NF; q += blockDim.x) fcol[q] = 0.0;
-  } else {
-    const int k = c - d.nB, npe = d.PE - nE;  // padding column k: [nE, PE) then [PE + nC, NF)
-    const int q = k < npe ? nE + k : d.PE + nC + (k - npe);
-    if (q >= d.NF) return;
-    double* fcol = d.F + (size_t)q * ld;
-    for (int r = threadIdx.x; r < d.NF; r += blockDim.x) fcol[r] = r == q ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < kXformCols; ++k) {
+      for (int q = nE + threadIdx.x; q < d.PE; q += blockDim.x) fcol[k][q] = 0.0;
+      for (int q = d.PE + nC + threadIdx.x; q < d.NF; q += blockDim.x) fcol[k][q] = 0.0;
+    }
+    return;
+  }
+  for (int k = 0; k < kXformCols; ++k) {
+    const int c = c0 + k;
+    if (c < d.nB) {
+      const double* yk = y + k * d.nB;
+      double* fcol = d.F + (size_t)d.posF[c] * ld;
+      for (int b = threadIdx.x; b < d.nB; b += blockDim.x) {
+        const int ib = d.bglob[b];
+        fcol[d.posF[b]] = ib < 0 ? yk[b] : xform_T_t_c(x, ib, d.bslot[b], yk);
+      }
+      for (int q = nE + threadIdx.x; q < d.PE; q += blockDim.x) fcol[q] = 0.0;
+      for (int q = d.PE + nC + threadIdx.x; q < d.NF; q += blockDim.x) fcol[q] = 0.0;
+    } else {
+      const int kp = c - d.nB, npe = d.PE - nE;  // padding column kp: [nE, PE) then [PE + nC, NF)
+      const int q = kp < npe ? nE + kp : d.PE + nC + (kp - npe);
+      if (q >= d.NF) break;
+      double* fcol = d.F + (size_t)q * ld;
+      for (int rr = threadIdx.x; rr < d.NF; rr += blockDim.x) fcol[rr] = rr == q ? 1.0 : 0.0;
+    }
   }
 }
 
@@ -2232,7 +2311,13 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   // F = P (T^T S T) P^T, pads identity
   if (!D.leaf_explicit) {
     if (no) {
-      k_xform_fused<<<dim3(D.max_PB + 2 * kTile, no), 256, D.max_nB * sizeof(double), st>>>(D.subdesc.p, D.xf);
+      static bool xf_attr = false;
+      if (!xf_attr) {
+        CK(cudaFuncSetAttribute(k_xform_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        xf_attr = true;
+      }
+      k_xform_fused<<<dim3((D.max_PB + 2 * kTile + kXformCols - 1) / kXformCols, no), 256,
+                      kXformCols * D.max_nB * sizeof(double), st>>>(D.subdesc.p, D.xf);
       count_launch(1);
     }
   } else {
