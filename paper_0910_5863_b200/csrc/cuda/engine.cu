@@ -959,18 +959,21 @@ __global__ void __launch_bounds__(256) k_prolong_copy(const SubDesc* sd, const i
   }
 }
 
-// Leaf forward, one 64-column tile of E per call: b_e staged once, each warp
-// owns eight columns and keeps two of them (up to 16 loads) in flight.
+// Leaf forward, one kFwdTile-column tile of E per call: b_e staged once, each
+// warp owns kFwdTile / 8 columns and keeps two of them (up to 16 loads) in
+// flight.  16-column tiles give the 27 fronts of configs 1-2 756 work units
+// (189 with 64-column tiles), about one per CTA of the grid (3 per SM).
+constexpr int kFwdTile = 16;
 __device__ __forceinline__ void leaf_fwd_tile(const LeafX& d, int t, double* bs) {
   const int cols = d.PE + d.M;
-  if (t * 64 >= cols) return;  // uniform over the CTA
+  if (t * kFwdTile >= cols) return;  // uniform over the CTA
   for (int k = threadIdx.x; k < d.PE; k += blockDim.x) bs[k] = d.FV[k];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = d.PE / 2;
   const double2* b2 = reinterpret_cast<const double2*>(bs);
-  for (int u = 0; u < 8; u += 2) {
-    const int j0 = t * 64 + warp + 8 * u, j1 = j0 + 8;
+  for (int u = 0; u < kFwdTile / 8; u += 2) {
+    const int j0 = t * kFwdTile + warp + 8 * u, j1 = j0 + 8;
     const double2* c0 = reinterpret_cast<const double2*>(d.E + (size_t)min(j0, cols - 1) * d.PE);
     const double2* c1 = reinterpret_cast<const double2*>(d.E + (size_t)min(j1, cols - 1) * d.PE);
     double a0 = 0.0, a1 = 0.0, e0 = 0.0, e1 = 0.0;
@@ -2666,7 +2669,7 @@ bool persistent_pcg(DeviceState& D) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_persistent, 256, smem));
     D.pcg_smem = smem;
-    int cap = 2;  // CTAs per SM (BDDC_B200_PCG_PERSM overrides)
+    int cap = 3;  // CTAs per SM (BDDC_B200_PCG_PERSM overrides)
     if (const char* e = std::getenv("BDDC_B200_PCG_PERSM"); e && *e) cap = std::max(1, std::atoi(e));
     D.pcg_grid = per_sm < 1 ? -1 : sm_count() * std::min(per_sm, cap);
   }
@@ -2764,7 +2767,7 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
     P.nfv = static_cast<long long>(D.FV.n);
     P.ns = D.n_own;
     P.nrb_schur = (D.max_nB + 63) / 64;
-    P.ncb_fwd = (D.max_NF + 63) / 64;
+    P.ncb_fwd = (D.max_NF + kFwdTile - 1) / kFwdTile;
     P.wsrc = D.wsrc.p;
     P.item_sub = D.item_sub.p;
     P.nitems = D.nitems;
