@@ -194,6 +194,28 @@ class UploadBatch {
   DBuf<char> dev_;
 };
 
+/// Grow-only page-locked host buffer (device-to-host result copies).
+template <class T>
+struct HBuf {
+  T* p = nullptr;
+  std::size_t cap = 0;
+  T* reserve(std::size_t n) {
+    if (n > cap) {
+      if (p) CK(cudaFreeHost(p));
+      p = nullptr;
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<std::size_t>(n, 1) * sizeof(T), cudaHostAllocDefault));
+      cap = n;
+    }
+    return p;
+  }
+  HBuf() = default;
+  HBuf(const HBuf&) = delete;
+  HBuf& operator=(const HBuf&) = delete;
+  ~HBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
 /// Host-side stage timer (printed with BDDC_B200_PROFILE=1).
 class HostTimer {
  public:

@@ -90,6 +90,8 @@ struct GatherDesc {
 struct PairBuffers {
   DBuf<double> G, Q, F, Dv, M, KV, H, N, R, A, E, W, Fu, Hub, DvH;
   DBuf<int> Pv, info, KR, Gpos, Hpos, hinfo;
+  HBuf<double> h_ev, h_fu;  // page-locked result copies
+  HBuf<int> h_inf;
   DBuf<GatherDesc> ghub, gside;
   DBuf<FrontDesc> dHub;
   DBuf<int4> KC;
@@ -1490,15 +1492,15 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     CK(cudaGetLastError());
     prof.mark("vectors");
     ht.mark("launch");
-    std::vector<double> ev(E.n), fu(Fu.n);
-    std::vector<int> inf(4 * nb);
+    // results into page-locked buffers: the copies queue behind the kernels
+    const double* ev = B_.h_ev.reserve(E.n);
+    const double* fu = B_.h_fu.reserve(Fu.n);
+    const int* inf = B_.h_inf.reserve(4 * nb);
+    CK(cudaMemcpyAsync(B_.h_ev.p, E.p, E.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(B_.h_fu.p, Fu.p, Fu.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(B_.h_inf.p, info.p, 4 * nb * sizeof(int), cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
-    ht.mark("device_wait");
-    CK(cudaMemcpyAsync(ev.data(), E.p, E.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
-    CK(cudaMemcpyAsync(fu.data(), Fu.p, Fu.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
-    CK(cudaMemcpyAsync(inf.data(), info.p, 4 * nb * sizeof(int), cudaMemcpyDeviceToHost, st_));
-    CK(cudaStreamSynchronize(st_));
-    ht.mark("copy");
+    ht.mark("device_wait+copy");
     if (chunk_id == 1 && nh) {
       std::vector<int> hinf(nh);
       CK(cudaMemcpy(hinf.data(), B_.hinfo.p, nh * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1519,7 +1521,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       std::vector<double> lam(take, 0.0);
       for (int q = 0; q < std::min(dm.k, take); ++q) lam[q] = ev[oE[b] + q];
       all_evals[p0 + b] = lam;
-      all_funcs[p0 + b].assign(fu.begin() + oFu[b], fu.begin() + oFu[b] + (long long)dm.nf * dm.k);
+      all_funcs[p0 + b].assign(fu + oFu[b], fu + oFu[b] + (long long)dm.nf * dm.k);
       all_k[p0 + b] = dm.k;
     }
     p0 = p1;
