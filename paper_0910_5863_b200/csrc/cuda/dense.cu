@@ -1442,7 +1442,7 @@ void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, i
   // chunked mode (dedicated diagonal workers, trailing updates per column) when
   // the fronts leave most of the grid to the queue; BDDC_B200_DAGW=0|1 overrides
   bool chunked = 2L * batch <= sm_count() && resident >= 2L * sm_count();
-  if (const char* e = std::getenv("BDDC_B200_DAGW"); e && *e) chunked = *e == '1' && 2L * batch <= sm_count();
+  if (const char* e = std::getenv("BDDC_B200_DAGW"); e && *e) chunked = *e == '1' && 3L * batch <= resident;
   long total;
   int cw = 1, bq = 6;
   if (const char* e = std::getenv("BDDC_B200_DAGBQ"); e && *e) bq = std::min(11, std::max(0, std::atoi(e)));
