@@ -314,6 +314,31 @@ __device__ __forceinline__ void dag_mark(int b, int slot) {
 // inverse into V, by NT threads.  Returns 1 + the first non-positive pivot
 // (uniform over the CTA), or 0.  On success dinv_out (64x64, column-major)
 // receives L^{-1} with zeros above the block diagonal.
+// Trailing block (bi, bj) of the tile minus X_bi X_bj^T, X = block column o
+// (one warp, DMMA).
+__device__ __forceinline__ void panel_trailing_block(double* L, int o, int bi, int bj) {
+  double acc[2][4];
+  double* Cb = L + (16 * bj) * LDS + 16 * bi;
+  for_acc16(acc, [&](int m, int n, double& v) { v = Cb[n * LDS + m]; });
+  mma16<true>(acc, L + o * LDS + 16 * bi, 1, LDS, L + o * LDS + 16 * bj, LDS, 1, 16);
+  for_acc16(acc, [&](int m, int n, double& v) { Cb[n * LDS + m] = v; });
+}
+
+// Off-diagonal block (i, j), j < i, of W = L^{-1} (one warp, DMMA):
+// T = sum_{k=j}^{i-1} L_ik W_kj;  W_ij = -W_ii T.  T in the strictly upper block
+// (0, ts) of the tile, which the factorization leaves unused.
+__device__ __forceinline__ void panel_inverse_block(double* L, double* V, int i, int j, int ts) {
+  double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+  mma16<false>(acc, L + (16 * j) * LDS + 16 * i, 1, LDS, V + (16 * j) * LDS + 16 * j, 1, LDS, 16 * (i - j));
+  double* T = L + (16 * ts) * LDS;
+  for_acc16(acc, [&](int m, int n, double& v) { T[n * LDS + m] = v; });
+  __syncwarp();
+  double acc2[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+  mma16<true>(acc2, V + (16 * i) * LDS + 16 * i, 1, LDS, T, 1, LDS, 16);
+  for_acc16(acc2, [&](int m, int n, double& v) { V[(16 * j + n) * LDS + 16 * i + m] = v; });
+  __syncwarp();
+}
+
 template <int NT>
 __device__ int panel_factor(double* L, double* V, double* dinv_out) {
   static_assert(NT >= 128, "four warps");
@@ -323,14 +348,29 @@ __device__ int panel_factor(double* L, double* V, double* dinv_out) {
   if (tid == 0) bad_s = 0;
   __syncthreads();
   pf_mark(0);
-  // ---- blocked POTRF, 16-wide: warp 0 factors the diagonal block; then warp 0
-  // inverts it (W_kk, into V) while warps 1-2 solve the rows below (thread per
-  // row); the trailing blocks are updated with DMMA, one 16x16 block per warp.
+  // ---- blocked POTRF, 16-wide, with lookahead.  Step kb:
+  //   phase 1: warp 0 factors diagonal block kb (its update by column block
+  //            kb-1 was applied by warp 0 at the end of step kb-1); warps 1-3
+  //            apply column block kb-1 to the other trailing blocks and form
+  //            row kb-1 of L^{-1} (blocks left of the diagonal);
+  //   phase 2: warp 0 inverts the diagonal block (W_kk, into V) while warps
+  //            1-2 solve the rows below (thread per row, right-looking);
+  //   phase 3: warp 0 applies column block kb to diagonal block kb+1.
   for (int kb = 0; kb < 4; ++kb) {
     const int o = kb * 16;
     if (warp == 0) {
       const int bad = chol16(L + o * LDS + o, rd + o, lane);
       if (lane == 0 && bad && !bad_s) bad_s = o + bad;
+    } else if (warp < 4 && kb > 0) {
+      // column block kb-1 applied to blocks (bi, bj), kb <= bj <= bi < 4, except (kb, kb)
+      int q = 0;
+      for (int bi = kb; bi < 4; ++bi)
+        for (int bj = kb; bj <= bi; ++bj) {
+          if (bi == kb && bj == kb) continue;
+          if (q++ % 3 == warp - 1) panel_trailing_block(L, o - 16, bi, bj);
+        }
+      // row kb-1 of L^{-1}: blocks (kb-1, j), j < kb-1
+      for (int j = warp - 1; j < kb - 1; j += 3) panel_inverse_block(L, V, kb - 1, j, warp);
     }
     __syncthreads();
     pf_mark(1 + 3 * kb);
@@ -365,44 +405,13 @@ __device__ int panel_factor(double* L, double* V, double* dinv_out) {
     }
     __syncthreads();
     pf_mark(2 + 3 * kb);
-    // trailing blocks (bi, bj), kb < bj <= bi < 4: C -= X_bi X_bj^T
-    const int nb = 3 - kb, nblk = nb * (nb + 1) / 2;
-    for (int q = warp; q < nblk; q += NT / 32) {
-      int bi = kb + 1, rem = q;
-      while (rem > bi - kb - 1) {
-        rem -= bi - kb;
-        ++bi;
-      }
-      const int bj = kb + 1 + rem;
-      double acc[2][4];
-      double* Cb = L + (16 * bj) * LDS + 16 * bi;
-      for_acc16(acc, [&](int m, int n, double& v) { v = Cb[n * LDS + m]; });
-      mma16<true>(acc, L + o * LDS + 16 * bi, 1, LDS, L + o * LDS + 16 * bj, LDS, 1, 16);
-      for_acc16(acc, [&](int m, int n, double& v) { Cb[n * LDS + m] = v; });
-    }
-    __syncthreads();
-    pf_mark(3 + 3 * kb);
+    if (warp == 0 && kb < 3) panel_trailing_block(L, o, kb + 1, kb + 1);
   }
+  // row 3 of L^{-1}
+  if (warp < 3) panel_inverse_block(L, V, 3, warp, warp + 1);
+  __syncthreads();
   const int bad = bad_s;
   if (bad) return bad;
-  pf_mark(13);
-  // ---- off-diagonal blocks of L^{-1} by block diagonal dd = i - j:
-  //   T = sum_{k=j}^{i-1} L_ik W_kj ;  W_ij = -W_ii T   (one warp per block; T in
-  //   the strictly upper block (0, w + 1) of the tile, unused by the factor)
-  for (int dd = 1; dd < 4; ++dd) {
-    for (int w = warp; w < 4 - dd; w += NT / 32) {
-      const int j = w, i = w + dd;
-      double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
-      mma16<false>(acc, L + (16 * j) * LDS + 16 * i, 1, LDS, V + (16 * j) * LDS + 16 * j, 1, LDS, 16 * dd);
-      double* T = L + (16 * (w + 1)) * LDS;
-      for_acc16(acc, [&](int m, int n, double& v) { T[n * LDS + m] = v; });
-      __syncwarp();
-      double acc2[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
-      mma16<true>(acc2, V + (16 * i) * LDS + 16 * i, 1, LDS, T, 1, LDS, 16);
-      for_acc16(acc2, [&](int m, int n, double& v) { V[(16 * j + n) * LDS + 16 * i + m] = v; });
-    }
-    __syncthreads();
-  }
   pf_mark(14);
   // Dinv = L^{-1} (zero above the block diagonal).
   double2* dv = reinterpret_cast<double2*>(dinv_out);
