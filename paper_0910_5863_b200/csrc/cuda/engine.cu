@@ -1032,6 +1032,8 @@ struct PcgPersist {
   const int2* wpos;  // every boundary copy: (owned substructure index, boundary position)
   int nw;
   const int* wsrc;   // per boundary copy: leaf-vector index, or -1 - constrained item
+  const int* wsrcg;  // the same, indexed by the global boundary position (phase H's gather)
+  const double* bwg; // averaging weight per global boundary position
   const int* item_sub;
   int nitems;
   double* yglob;     // constrained rows of the prolongation
@@ -1207,20 +1209,17 @@ __global__ void __launch_bounds__(256) k_pcg_persistent(PcgPersist P) {
     for (int k = (me * blockDim.x + threadIdx.x) >> 5; k < P.nitems; k += (G * blockDim.x) >> 5)
       prolong_item(P.sd[P.item_sub[k]], P.xf, k, P.yglob);
     grid.sync();
-    for (i64 w = gt; w < P.nw; w += gs) {
-      const int2 sb = P.wpos[w];
-      const SubDesc& d = P.sd[sb.x];
-      const int src = P.wsrc[w];
-      d.WB[sb.y] = d.bw[sb.y] * (src >= 0 ? P.FVall[src] : P.yglob[-1 - src]);
-    }
-    grid.sync();
     if (P.trace && me == 0 && threadIdx.x == 0 && it < 64) P.trace[(size_t)it * 9 + 6] = gtimer();
-    // H
+    // H: the weighted prolongation of every copy is formed where the copies
+    // are summed (same products, same order as writing WB and summing it)
     {
       double acc = 0.0;
       for (i64 i = gt; i < P.n; i += gs) {
         double s = 0.0;
-        for (int t = P.icp[i]; t < P.icp[i + 1]; ++t) s += P.WB[P.icpos[t]];
+        for (int t = P.icp[i]; t < P.icp[i + 1]; ++t) {
+          const int g = P.icpos[t], src = P.wsrcg[g];
+          s += __dmul_rn(P.bwg[g], src >= 0 ? P.FVall[src] : P.yglob[-1 - src]);  // rounded product, no FMA
+        }
         P.z[i] = s;
         acc += s * rnew[i];
       }
@@ -1357,7 +1356,7 @@ struct DeviceState {
   DBuf<int2> wpos;
   UploadBatch up_index, up_desc;  // set_constraints' small uploads (one copy each)
   int nw = 0;
-  DBuf<int> wsrc, item_sub;
+  DBuf<int> wsrc, wsrcg, item_sub;
   DBuf<double> yglob;
   int nitems = 0;
   DBuf<PcgState> pst;
@@ -2053,6 +2052,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       D.nw = static_cast<int>(w0[no]);
     }
     std::vector<int> wsrc(std::max<long long>(w0[no], 1)), isub(item_inst.size());
+    std::vector<int> wsrcg(std::max<std::size_t>(D.WB.n, 1), 0);  // unowned positions: never summed by phase H
 #pragma omp parallel for schedule(dynamic, 16) if (no >= 64)
     for (int q = 0; q < no; ++q) {
       const int s = D.own[q];
@@ -2070,9 +2070,11 @@ void Engine::set_constraints(const ConstraintSet& cs) {
             src = static_cast<int>(D.fv_off[s]) + posF[D.wb_off[s] + tpos[inst_pos[inst] + i]];
         }
         wsrc[w0[q] + b] = src;
+        wsrcg[w] = src;
       }
     }
     up_i(D.wsrc, wsrc);
+    up_i(D.wsrcg, wsrcg);
     up_i(D.item_sub, isub);
     D.nitems = static_cast<int>(item_inst.size());
     D.yglob.alloc(std::max(D.nitems, 1));
@@ -2769,6 +2771,8 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
     P.nrb_schur = (D.max_nB + 63) / 64;
     P.ncb_fwd = (D.max_NF + kFwdTile - 1) / kFwdTile;
     P.wsrc = D.wsrc.p;
+    P.wsrcg = D.wsrcg.p;
+    P.bwg = D.bw.p;
     P.item_sub = D.item_sub.p;
     P.nitems = D.nitems;
     P.yglob = D.yglob.p;
