@@ -233,42 +233,60 @@ def _count_above(values, tau):
     return k
 
 
+def pair_candidates(sol: PairSolve, gs, dmap, opts: EnrichmentOptions, tau_mode=True):
+    """The per-pair part of `adaptive.cpp:72-115`: selection count, omega_next,
+    saturation, and the split/normalized functional pieces (before the rank
+    filter of `add_average`) in the reference's order.  Independent of every
+    other pair (all pairs are solved against the same base, `adaptive.cpp:133`)."""
+    lam = sol.eig.eigenvalues
+    rep = PairReport(sol.space.si, sol.space.sj, lam.copy())
+    pieces = []
+    if not tau_mode:
+        rep.omega_next = float(lam[0]) if len(lam) else 0.0
+        return rep, pieces
+    if opts.fixed_count >= 0:
+        rep.enforced = min(opts.fixed_count, len(lam))
+    else:
+        rep.enforced = min(_count_above(lam, opts.tau), opts.max_vectors)
+    rep.omega_next = float(lam[rep.enforced]) if rep.enforced < len(lam) else 0.0
+    rep.saturated = rep.omega_next > opts.tau and opts.fixed_count < 0
+    for m in range(rep.enforced):
+        func = jump_functional(sol.space, sol.admissible @ sol.eig.eigenvectors[:, m])
+        rep.functionals.append(func)
+        scale = np.linalg.norm(func)
+        base_slot = 0
+        for gi in sol.space.shared_globs:
+            n = len(glob_free_dofs(gs.globs[gi], dmap))
+            piece = func[base_slot:base_slot + n].copy()
+            base_slot += n
+            if np.linalg.norm(piece) <= 1e-12 * scale:
+                continue
+            if gs.globs[gi].kind == EDGE and not opts.keep_edge_constraints:
+                continue
+            top = int(np.argmax(np.abs(piece)))
+            nrm = np.linalg.norm(piece)
+            piece /= -nrm if piece[top] < 0 else nrm
+            pieces.append((gi, piece))
+    return rep, pieces
+
+
+def install_pieces(enrich_into: ConstraintSet, rep: PairReport, pieces):
+    """`adaptive.cpp:104-111`: each piece through the rank filter, in order."""
+    for gi, piece in pieces:
+        if add_average(enrich_into, GlobAverage(gi, piece, "adaptive")):
+            rep.kept += 1
+        else:
+            rep.dropped += 1
+
+
 def run_pairs(enrich_into, base, gs, dmap, systems, maps, opts, request):
     """`adaptive.cpp:66-125`."""
     out = EnrichmentOutcome()
     for si, sj in face_pairs(gs):
         sol = solve_pair(base, gs, dmap, systems, maps, si, sj, request)
-        lam = sol.eig.eigenvalues
-        rep = PairReport(si, sj, lam.copy())
+        rep, pieces = pair_candidates(sol, gs, dmap, opts, enrich_into is not None)
         if enrich_into is not None:
-            if opts.fixed_count >= 0:
-                rep.enforced = min(opts.fixed_count, len(lam))
-            else:
-                rep.enforced = min(_count_above(lam, opts.tau), opts.max_vectors)
-            rep.omega_next = float(lam[rep.enforced]) if rep.enforced < len(lam) else 0.0
-            rep.saturated = rep.omega_next > opts.tau and opts.fixed_count < 0
-            for m in range(rep.enforced):
-                func = jump_functional(sol.space, sol.admissible @ sol.eig.eigenvectors[:, m])
-                rep.functionals.append(func)
-                scale = np.linalg.norm(func)
-                base_slot = 0
-                for gi in sol.space.shared_globs:
-                    n = len(glob_free_dofs(gs.globs[gi], dmap))
-                    piece = func[base_slot:base_slot + n].copy()
-                    base_slot += n
-                    if np.linalg.norm(piece) <= 1e-12 * scale:
-                        continue
-                    if gs.globs[gi].kind == EDGE and not opts.keep_edge_constraints:
-                        continue
-                    top = int(np.argmax(np.abs(piece)))
-                    nrm = np.linalg.norm(piece)
-                    piece /= -nrm if piece[top] < 0 else nrm
-                    if add_average(enrich_into, GlobAverage(gi, piece, "adaptive")):
-                        rep.kept += 1
-                    else:
-                        rep.dropped += 1
-        else:
-            rep.omega_next = float(lam[0]) if len(lam) else 0.0
+            install_pieces(enrich_into, rep, pieces)
         out.omega_tilde = max(out.omega_tilde, rep.omega_next)
         out.kept += rep.kept
         out.dropped += rep.dropped
