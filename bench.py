@@ -5,12 +5,14 @@ A *step* is one pass of the hot path over one instance of the workload:
 leaf factorization + interface Schur complements, adaptive face
 eigenproblems, constraint selection, transformed preconditioner (leaf fronts +
 root) and the PCG solve to 1e-8 -- i.e. the metric's "setup + solve".  The
-workload defaults to BASELINE.json configs[1] (24^3 Poisson, 3x3x3
-substructures, 1e6 z-channels, adaptive tau=10, <=10 vectors per face); the
-host-side input (mesh, assembly, globs) is built once and uploaded before
-timing.  `value` is free dofs / device seconds per step, summed over ranks;
-`e2e` repeats the step through the C ABI with the host->device upload of the
-inputs and the device->host copy of the solution inside the timed region.
+workload defaults to BASELINE.json configs[2] (cfg3: 80^3 Poisson, 8^3
+substructures, k = exp(2z), adaptive tau=5), the largest configuration that
+the reference runs on one GPU (cfg5 is the 8-GPU one); `--config 1..5`
+selects another.  The host-side input (mesh, assembly, globs) is built once
+and uploaded before timing.  `value` is free dofs / device seconds per step,
+summed over ranks; `e2e` repeats the step through the C ABI with the
+host->device upload of the inputs and the device->host copy of the solution
+inside the timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
 
@@ -18,11 +20,19 @@ N > 1 (torchrun, one process per GPU) runs the sharded engine: one problem
 whose substructure lattice grows with N along x (the config's lattice per GPU,
 same per-element coefficient rule), substructures and face pairs partitioned
 over the ranks (paper_0910_5863_b200/shard.py), NCCL for the interface
-exchange, the dot products (complete vectors on every rank) and the root
-("weak" scaling: per-GPU work fixed).  `--replicas` runs N independent copies
-of the N=1 workload instead.
-`--impl reference` times the CPU oracle (oracle/, the reference restated; the
-C++ reference itself needs Eigen and cannot be built here) on the same config.
+exchange, the dot products and the root ("weak" scaling: per-GPU work
+fixed).  `--replicas` runs N independent copies of the N=1 workload instead.
+
+CPU legs (oracle/, the reference restated in numpy/scipy; the C++ reference
+needs Eigen and cannot be built here): `cpu_baseline` times
+the oracle single-threaded (the reference is serial) and `--impl reference`
+times it on all host cores (face pairs in worker processes), both on a
+BOUNDED SAMPLE of the workload -- the same config restricted to a smaller
+substructure lattice with the same substructure size, coefficient rule,
+constraints and tolerances (SAMPLE_LATTICE) -- reported in the metric's unit
+(free DOF/s of the sample).  The oracle's per-dof cost grows with the
+lattice (more pairs per substructure, more iterations, a larger coarse
+factorization), so the sample overstates the CPU's full-size throughput.
 """
 from __future__ import annotations
 
@@ -188,14 +198,66 @@ def barrier(dist, device=None):
             dist.barrier()
 
 
-def run_oracle_step(cfg_id, seed):
-    from oracle.experiment import baseline_config, build_pipeline, solve_item
-    cfg = baseline_config(cfg_id, seed)
+# Sample lattice of the CPU legs per config (same substructure size): about
+# 10-30 s of single-thread oracle work on this pool's hosts.
+SAMPLE_LATTICE = {1: (3, 3, 3), 2: (3, 3, 3), 3: (3, 3, 3), 4: (2, 2, 2), 5: (2, 2, 2)}
+CONFIG_GEOMETRY = {1: ((3, 3, 3), 8, 1), 2: ((3, 3, 3), 8, 1), 3: ((8, 8, 8), 10, 1), 4: ((6, 6, 6), 8, 3),
+                   5: ((12, 12, 12), 8, 3)}
+
+
+def free_dofs_of(lattice, epe, comps):
+    """Free dofs of a structured cube with Dirichlet on x=0 (all components)."""
+    nx, ny, nz = (l * epe + 1 for l in lattice)
+    return (nx - 1) * ny * nz * comps
+
+
+def workload_config(cfg_id, seed, world=1, sharded=False, replicas=False):
+    """The `config` object of both arms (identical dicts for the same run)."""
+    lat, epe, comps = CONFIG_GEOMETRY[cfg_id]
+    if sharded:
+        lat = (lat[0] * world, lat[1], lat[2])
+    return {"workload": CONFIG_NAMES[cfg_id] + (
+                " per GPU; lattice %dx%dx%d over %d GPUs" % (lat + (world,)) if sharded else ""),
+            "config": cfg_id, "seed": seed, "lattice": list(lat), "elements_per_substructure_edge": epe,
+            "free_dofs": free_dofs_of(lat, epe, comps),
+            "parallelism": ("sharded%d (NCCL: interface exchange, dot products, root)" % world if sharded
+                            else "replicas%d" % world if world > 1 else "single GPU")}
+
+
+def oracle_sample_step(cfg_id, seed, workers):
+    """One oracle setup+solve on the sample lattice: (seconds, free dofs, row).
+    The input (mesh, assembly, globs) is built outside the timed region, as on
+    the GPU arm."""
+    from oracle.experiment import baseline_config, build_pipeline
+    from oracle.parallel import solve_item_parallel
+    cfg = baseline_config(cfg_id, seed, subdomains=SAMPLE_LATTICE[cfg_id])
     p = build_pipeline(cfg.spec)
     t0 = time.perf_counter()
-    row = solve_item(p, cfg.mode, cfg.tau, cfg.max_vectors, base_faces=cfg.base_faces)
-    dt = time.perf_counter() - t0
-    return dt, p.dmap.free_count, row
+    row = solve_item_parallel(p, cfg.mode, cfg.tau, cfg.max_vectors, cfg.base_faces, workers)
+    return time.perf_counter() - t0, p.dmap.free_count, row
+
+
+def sample_text(cfg_id, workers, seconds=None):
+    lat = SAMPLE_LATTICE[cfg_id]
+    full = CONFIG_GEOMETRY[cfg_id][0]
+    return ("cfg%d restricted to a %dx%dx%d substructure lattice (%d of %d substructures, same substructure "
+            "size, coefficient rule, constraints and tolerances): one full oracle setup+solve "
+            "(HarmonicExtension, face eigenproblems, enrichment, change of variables, preconditioner, PCG)%s, "
+            "%s; DOF/s of the sample" % (
+                cfg_id, lat[0], lat[1], lat[2], lat[0] * lat[1] * lat[2], full[0] * full[1] * full[2],
+                " in %.1f s" % seconds if seconds is not None else "",
+                "single-threaded (BLAS 1 thread, as the serial reference)" if workers <= 1 else
+                "face pairs over %d worker processes, BLAS on all threads" % workers))
+
+
+def cpu_baseline_single(cfg_id, seed):
+    """Single-thread oracle on the sample (in-process, BLAS limited to 1 thread)."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):
+        dt, free, row = oracle_sample_step(cfg_id, seed, 1)
+    return {"value": free / dt, "unit": "DOF/s", "cores": 1, "kind": "port",
+            "sample": sample_text(cfg_id, 1, dt), "sample_free_dofs": free, "sample_seconds": dt,
+            "sample_iterations": row.iterations}
 
 
 def reference_arm(args):
@@ -203,28 +265,26 @@ def reference_arm(args):
     if rank != 0:
         return 0
     cfg_id = args.config
+    cores = os.cpu_count() or 1
     times = []
     row = None
     for i in range(args.warmup + args.steps):
-        dt, free, row = run_oracle_step(cfg_id, args.seed)
+        dt, free, row = oracle_sample_step(cfg_id, args.seed, cores)
         if i >= args.warmup:
             times.append(dt)
     sec = sum(times) / len(times)
     value = free / sec
-    cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-        "config": {"workload": CONFIG_NAMES[cfg_id], "config": cfg_id, "seed": args.seed,
-                   "l2": "n/a (CPU)"},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded coefficient field)",
+        "config": workload_config(cfg_id, args.seed, world, world > 1 and not args.replicas, args.replicas),
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
-                         "sample": ("full %s setup+solve per step (numpy/scipy oracle, LAPACK on %d threads)"
-                                    % ("cfg%d" % cfg_id, cores)) + (
-                             "; one GPU's share of the %d-GPU weak-scaled job" % world if world > 1 else "")},
+                         "sample": sample_text(cfg_id, cores), "sample_free_dofs": free},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "iterations": row.iterations, "kappa": row.kappa, "constraint_rows": row.constraint_rows,
         "omega_tilde": None if math.isnan(row.omega_tilde) else row.omega_tilde,
+        "l2": "n/a (CPU)",
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -235,10 +295,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--seed", type=int, default=20091030)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--apply-reps", type=int, default=10, help="operator applications timed for the rooflines")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent copies instead of sharding")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -286,6 +347,9 @@ def main():
     # short steps (cfg1-2: a few ms, mostly host/launch latency) keep warming
     # for about one more second of steps so the host threads and caches settle;
     # the count is agreed over the ranks (sharded steps hold collectives)
+    if args.warmup == 0:  # time one step so the settle count is based on a real step
+        t_w = time.perf_counter()
+        do_step()
     t_last = max_over_ranks(dist, time.perf_counter() - t_w, "cuda")
     settle = min(400, int(1.0 / max(t_last, 1e-3)))
     for _ in range(settle):
@@ -341,22 +405,34 @@ def main():
                 "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind}
     if traffic:
         roof["traffic_source"] = roof_pcg["traffic_source"] = traffic["source"]
+    # third and fourth rooflines: the preconditioner apply alone and the Schur
+    # apply alone (device-resident vectors, CUDA events on the engine stream)
+    ops = b.operator_times(args.apply_reps)
+    pre_achieved = ops["precond_bytes"] / ops["precond"] / 1e9
+    roof_pre = {"kernel": "BDDC preconditioner apply (restrict, leaf forward sweep, primal tree, root, leaf "
+                          "backward sweep, prolong, copy sum)", "bound": "hbm", "achieved": pre_achieved,
+                "peak": hbm_peak, "unit": "GB/s", "frac": pre_achieved / hbm_peak,
+                "bytes_per_apply": ops["precond_bytes"], "seconds_per_apply": ops["precond"],
+                "stages_s": {k: ops[k] for k in ("restrict", "leaf_fwd", "tree_fwd", "root", "tree_bwd",
+                                                 "leaf_bwd", "prolong", "sum_copies")},
+                "leaf_sweep_bytes": ops["leaf_sweep_bytes"],
+                "leaf_fwd_gbs": ops["leaf_sweep_bytes"] / max(ops["leaf_fwd"], 1e-12) / 1e9,
+                "leaf_bwd_gbs": ops["leaf_sweep_bytes"] / max(ops["leaf_bwd"], 1e-12) / 1e9,
+                "reps": args.apply_reps}
+    sch_achieved = ops["schur_bytes"] / ops["schur"] / 1e9
+    roof_schur = {"kernel": "Schur apply (dense S_s GEMV + copy sum)", "bound": "hbm", "achieved": sch_achieved,
+                  "peak": hbm_peak, "unit": "GB/s", "frac": sch_achieved / hbm_peak,
+                  "bytes_per_apply": ops["schur_bytes"], "seconds_per_apply": ops["schur"]}
     cpu = None
-    if not args.no_cpu_baseline and world == 1 and args.config <= 2:
-        dt, _, _ = run_oracle_step(args.config, args.seed)
-        cpu = {"value": free / dt, "unit": "DOF/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": "one full cfg%d setup+solve (numpy/scipy oracle, %.1f s)" % (args.config, dt)}
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline_single(args.config, args.seed)
     line = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "settle_steps": settle, "ms_per_step": sec_per_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded coefficient field)",
-        "config": {"workload": CONFIG_NAMES[args.config] + (
-                       " per GPU; lattice %dx%dx%d over %d GPUs" % (lattice + (world,)) if sharded else ""),
-                   "config": args.config, "seed": args.seed, "lattice": list(lattice),
-                   "free_dofs": free, "subdomains": st["subdomains"], "interface_dofs": st["interface_dofs"],
-                   "l2": "flushed (256 MiB write) before every step",
-                   "parallelism": ("sharded%d (NCCL: interface exchange, dot products, root)" % world if sharded
-                                   else "replicas%d" % world if world > 1 else "single GPU")},
+        "config": workload_config(args.config, args.seed, world, sharded, args.replicas and world > 1),
+        "l2": "flushed (256 MiB write) before every step",
+        "structure": {"free_dofs": free, "subdomains": st["subdomains"], "interface_dofs": st["interface_dofs"]},
         "setup_s": statistics.median(s["setup_seconds"] for s in steps),
         "solve_s": statistics.median(s["solve_seconds"] for s in steps),
         "iterations": last["iterations"], "kappa": last["kappa"], "constraint_rows": last["constraint_rows"],
@@ -365,6 +441,8 @@ def main():
                                                                    "leaf_factor")},
         "roofline": roof,
         "roofline_pcg": roof_pcg,
+        "roofline_precond": roof_pre,
+        "roofline_schur": roof_schur,
         "cpu_baseline": cpu,
         "e2e": {"value": jobs * free / e2e_sec, "unit": "DOF/s",
                 "h2d_bytes_per_step": int(e2e_steps[-1]["h2d_bytes"]),

@@ -171,6 +171,13 @@ int bddc_b200_setup_preconditioner(bddc_b200_t* h);
 int bddc_b200_interface_size(const bddc_b200_t* h, int64_t* n);
 int bddc_b200_schur_apply(bddc_b200_t* h, const double* x, double* y);
 int bddc_b200_precond_apply(bddc_b200_t* h, const double* r, double* z);
+/* Device-timed applications for rooflines (no reference counterpart; the
+ * reference times phases only, experiment.cpp:114-203): mean seconds over
+ * `reps` applications with device-resident vectors, CUDA events on the handle's
+ * stream.  out[13] = [schur, precond, restrict, leaf_fwd, tree_fwd, root,
+ * tree_bwd, leaf_bwd, prolong, sum_copies (seconds), schur_bytes,
+ * precond_bytes, leaf_sweep_bytes (algorithmic bytes per application)]. */
+int bddc_b200_operator_times(bddc_b200_t* h, int reps, double out[13]);
 /* InterfaceProblem::rhs / recover (schur.cpp:38-75). */
 int bddc_b200_rhs(bddc_b200_t* h, double* out);
 int bddc_b200_recover(bddc_b200_t* h, const double* u_interface, double* u_free);

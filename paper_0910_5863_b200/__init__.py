@@ -121,6 +121,7 @@ EXPORTS = {
     "bddc_b200_interface_size": (C.c_int, [P, I64]),
     "bddc_b200_schur_apply": (C.c_int, [P, D, D]),
     "bddc_b200_precond_apply": (C.c_int, [P, D, D]),
+    "bddc_b200_operator_times": (C.c_int, [P, C.c_int, D]),
     "bddc_b200_rhs": (C.c_int, [P, D]),
     "bddc_b200_recover": (C.c_int, [P, D, D]),
     "bddc_b200_pcg": (C.c_int, [P, D, D, C.c_double, C.c_int, C.c_int, C.POINTER(_PcgResult), D, D]),
@@ -477,6 +478,15 @@ class BDDC:
         z = np.empty_like(r)
         _check(self._lib.bddc_b200_precond_apply(self._h, _dptr(r), _dptr(z)))
         return z
+
+    def operator_times(self, reps: int = 10) -> dict:
+        """Device-timed Schur and preconditioner applications (seconds per
+        application) with the preconditioner's stages and algorithmic bytes."""
+        out = np.zeros(13)
+        _check(self._lib.bddc_b200_operator_times(self._h, reps, _dptr(out)))
+        keys = ("schur", "precond", "restrict", "leaf_fwd", "tree_fwd", "root", "tree_bwd", "leaf_bwd",
+                "prolong", "sum_copies", "schur_bytes", "precond_bytes", "leaf_sweep_bytes")
+        return dict(zip(keys, out.tolist()))
 
     def rhs(self) -> np.ndarray:
         out = np.empty(self.interface_size)

@@ -337,6 +337,17 @@ int bddc_b200_precond_apply(bddc_b200_t* h, const double* r, double* z) {
   return guarded([&] { engine(h).precond_apply(r, z); });
 }
 
+int bddc_b200_operator_times(bddc_b200_t* h, int reps, double out[13]) {
+  return guarded([&] {
+    Engine& e = engine(h);
+    const Engine::OpTimes t = e.time_operators(reps);
+    const double v[13] = {t.schur,    t.precond,  t.restrict_,  t.leaf_fwd,         t.tree_fwd,
+                          t.root,     t.tree_bwd, t.leaf_bwd,   t.prolong,          t.sum_copies,
+                          e.schur_bytes(), e.pcg_bytes_per_iteration() - e.schur_bytes(), t.leaf_sweep_bytes};
+    std::memcpy(out, v, sizeof(v));
+  });
+}
+
 int bddc_b200_rhs(bddc_b200_t* h, double* out) {
   return guarded([&] {
     ensure_analysis(h);

@@ -405,7 +405,10 @@ __device__ int panel_factor(double* L, double* V, double* dinv_out) {
     }
     __syncthreads();
     pf_mark(2 + 3 * kb);
-    if (warp == 0 && kb < 3) panel_trailing_block(L, o, kb + 1, kb + 1);
+    if (warp == 0 && kb < 3) {
+      panel_trailing_block(L, o, kb + 1, kb + 1);
+      __syncwarp();  // chol16 reads the block with another lane mapping
+    }
   }
   // row 3 of L^{-1}
   if (warp < 3) panel_inverse_block(L, V, 3, warp, warp + 1);
@@ -1341,9 +1344,7 @@ __global__ void k_copy_trailing(const TrailDesc* ds) {
   }
 }
 
-int g_smem_configured = 0;
-void configure() {
-  if (g_smem_configured) return;
+int configure_device() {
   const int gemm_smem = 4 * KC * LDS * sizeof(double);
   cudaFuncSetAttribute(k_syrk_column, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
   cudaFuncSetAttribute(k_syrk_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem);
@@ -1364,7 +1365,7 @@ void configure() {
   cudaFuncSetAttribute(k_front_backward_cl<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_front_forward_cl<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k_front_backward_cl<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  g_smem_configured = 1;
+  return 1;
 }
 
 std::atomic<long long> g_launches{0};
@@ -1401,16 +1402,31 @@ double* splitk_workspace(size_t doubles, cudaStream_t stream) { return stream_wo
 
 }  // namespace
 
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+int per_device(const void* key, int (*make)()) {
+  static std::mutex m;
+  static std::map<std::pair<int, const void*>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(m);
+    auto it = cache.find({dev, key});
+    if (it != cache.end()) return it->second;
   }
-  return n;
+  const int v = make();  // outside the lock: may launch CUDA API calls
+  std::lock_guard<std::mutex> g(m);
+  return cache.emplace(std::make_pair(dev, key), v).first->second;
 }
+
+namespace {
+int query_sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+}  // namespace
+
+int sm_count() { return per_device(reinterpret_cast<const void*>(&query_sm_count), query_sm_count); }
 
 void count_launch(long long n) { g_launches += n; }
 long long launch_count() { return g_launches.load(); }
@@ -1441,12 +1457,13 @@ bool use_dag(int batch, int nt, int pt) {
 
 void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, int mt, cudaStream_t stream) {
   const int smem = 4 * KC * LDS * sizeof(double);
-  static int per_sm = 0;
-  if (!per_sm) {
+  const int per_sm = per_device(reinterpret_cast<const void*>(&k_chol_dag), [] {
+    const int smem = 4 * KC * LDS * sizeof(double);
+    int n = 0;
     cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_dag, DAG_THREADS, smem);
-    if (per_sm <= 0) per_sm = 1;
-  }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_chol_dag, DAG_THREADS, smem);
+    return n > 0 ? n : 1;
+  });
   const long resident = (long)per_sm * sm_count();
   // chunked mode (dedicated diagonal workers, trailing updates per column) when
   // the fronts leave most of the grid to the queue; BDDC_B200_DAGW=0|1 overrides
@@ -1479,7 +1496,7 @@ void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, i
 void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p, int max_m,
                       cudaStream_t stream) {
   if (batch == 0) return;
-  configure();
+  per_device(reinterpret_cast<const void*>(&configure_device), configure_device);
   static const bool dbg = std::getenv("BDDC_B200_CHOLDBG") != nullptr;
   if (dbg)
     std::fprintf(stderr, "[chol] batch %d n %d p %d m %d -> %s\n", batch, max_n, max_p, max_m,
@@ -1600,7 +1617,7 @@ void launch_big(K kern, int max_n, size_t ws_per_cta, cudaStream_t stream, const
 
 void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
   if (batch == 0) return;
-  configure();
+  per_device(reinterpret_cast<const void*>(&configure_device), configure_device);
   if (big_sweep(batch, max_n)) {
     launch_big(k_big_forward, max_n, 2, stream, d_descs, done);  // z double buffer (2 x 64 <= 2 G)
     count_launch(1);
@@ -1618,7 +1635,7 @@ void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t 
 
 void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
   if (batch == 0) return;
-  configure();
+  per_device(reinterpret_cast<const void*>(&configure_device), configure_device);
   if (big_sweep(batch, max_n)) {
     launch_big(k_big_backward, max_n, 2 * 64, stream, d_descs, done);  // partials: 2 x G x 64
     count_launch(1);

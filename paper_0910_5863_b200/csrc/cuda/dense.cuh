@@ -47,6 +47,13 @@ struct SolveDesc {
 /// Streaming multiprocessors of the current device.
 int sm_count();
 
+/// One-time per-device state: function attributes (dynamic shared memory),
+/// occupancy and SM counts belong to a device, and bddc_b200_set_device lets a
+/// process use several.  Returns the value cached for (current device, key),
+/// computing it with `make` the first time (thread-safe: loopback ranks are
+/// host threads).
+int per_device(const void* key, int (*make)());
+
 /// Kernel-launch accounting (bench "gpu_launches").
 void count_launch(long long n);
 long long launch_count();

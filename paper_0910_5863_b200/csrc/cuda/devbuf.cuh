@@ -250,6 +250,12 @@ class StageProfiler {
     on_ = e && *e && *e != '0';
     if (on_) mark("start");
   }
+  /// Collecting mode: stage seconds are added to `sink` (name -> seconds)
+  /// instead of printed (Engine::time_operators).
+  StageProfiler(const char* what, cudaStream_t st, std::vector<std::pair<std::string, double>>* sink)
+      : what_(what), st_(st), on_(true), sink_(sink) {
+    mark("start");
+  }
   bool on() const { return on_; }
   void mark(const char* name) {
     if (!on_) return;
@@ -262,6 +268,15 @@ class StageProfiler {
   ~StageProfiler() {
     if (!on_) return;
     cudaEventSynchronize(ev_.back());
+    if (sink_) {
+      for (std::size_t i = 1; i < ev_.size(); ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev_[i - 1], ev_[i]);
+        sink_->emplace_back(names_[i], ms * 1e-3);
+      }
+      for (auto e : ev_) cudaEventDestroy(e);
+      return;
+    }
     std::string line = std::string("[profile] ") + what_;
     for (std::size_t i = 1; i < ev_.size(); ++i) {
       float ms = 0;
@@ -280,6 +295,7 @@ class StageProfiler {
   bool on_ = false;
   std::vector<cudaEvent_t> ev_;
   std::vector<std::string> names_;
+  std::vector<std::pair<std::string, double>>* sink_ = nullptr;
 };
 
 }  // namespace b200

@@ -2316,11 +2316,10 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   // F = P (T^T S T) P^T, pads identity
   if (!D.leaf_explicit) {
     if (no) {
-      static bool xf_attr = false;
-      if (!xf_attr) {
-        CK(cudaFuncSetAttribute(k_xform_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        xf_attr = true;
-      }
+      CK(static_cast<cudaError_t>(per_device(reinterpret_cast<const void*>(&k_xform_fused), [] {
+        return static_cast<int>(
+            cudaFuncSetAttribute(k_xform_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      })));
       k_xform_fused<<<dim3((D.max_PB + 2 * kTile + kXformCols - 1) / kXformCols, no), 256,
                       kXformCols * D.max_nB * sizeof(double), st>>>(D.subdesc.p, D.xf);
       count_launch(1);
@@ -2603,6 +2602,57 @@ void Engine::precond_apply(const double* r, double* z) {
   CK(cudaGetLastError());
 }
 
+Engine::OpTimes Engine::time_operators(int reps) {
+  DeviceState& D = *d_;
+  if (!D.have_prec) throw Error(kError, "preconditioner not set up");
+  ensure_vectors(D);
+  reps = std::max(reps, 1);
+  OpTimes o;
+  // deterministic nonzero inputs
+  CK(cudaMemcpyAsync(D.vp.p, D.rhs.p, D.niface * sizeof(double), cudaMemcpyDeviceToDevice, D.st));
+  CK(cudaMemcpyAsync(D.vr.p, D.rhs.p, D.niface * sizeof(double), cudaMemcpyDeviceToDevice, D.st));
+  launch_schur(D, D.vp.p, D.vq.p, nullptr, nullptr, nullptr);  // warm
+  launch_precond(D, D.vr.p, D.vz.p, nullptr, nullptr, nullptr);
+  cudaEvent_t e0, e1, e2;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventCreate(&e2));
+  CK(cudaEventRecord(e0, D.st));
+  for (int r = 0; r < reps; ++r) launch_schur(D, D.vp.p, D.vq.p, nullptr, nullptr, nullptr);
+  CK(cudaEventRecord(e1, D.st));
+  for (int r = 0; r < reps; ++r) launch_precond(D, D.vr.p, D.vz.p, nullptr, nullptr, nullptr);
+  CK(cudaEventRecord(e2, D.st));
+  CK(cudaEventSynchronize(e2));
+  o.schur = elapsed(e0, e1) / reps;
+  o.precond = elapsed(e1, e2) / reps;
+  CK(cudaEventDestroy(e0));
+  CK(cudaEventDestroy(e1));
+  CK(cudaEventDestroy(e2));
+  std::vector<std::pair<std::string, double>> stages;
+  for (int r = 0; r < reps; ++r) {
+    StageProfiler prof("precond_apply", D.st, &stages);
+    launch_precond(D, D.vr.p, D.vz.p, nullptr, nullptr, nullptr, &prof);
+  }
+  for (const auto& [name, sec] : stages) {
+    const double v = sec / reps;
+    if (name == "restrict") o.restrict_ += v;
+    else if (name == "leaf_fwd") o.leaf_fwd += v;
+    else if (name == "tree_fwd") o.tree_fwd += v;
+    else if (name.rfind("root", 0) == 0) o.root += v;
+    else if (name == "tree_bwd") o.tree_bwd += v;
+    else if (name == "leaf_bwd") o.leaf_bwd += v;
+    else if (name == "prolong") o.prolong += v;
+    else if (name == "sum_copies") o.sum_copies += v;
+  }
+  if (D.NF.size() == std::size_t(D.nsub))
+    for (int s : D.own) {
+      const double e = D.nE[s], c = D.nC[s];
+      o.leaf_sweep_bytes += (D.leaf_explicit ? e * (e + c) : e * (e + 1) / 2 + e * c) * 8.0;
+    }
+  CK(cudaGetLastError());
+  return o;
+}
+
 void Engine::rhs(double* out) {
   DeviceState& D = *d_;
   CK(cudaMemcpyAsync(out, D.rhs.p, D.niface * sizeof(double), cudaMemcpyDeviceToHost, D.st));
@@ -2663,11 +2713,10 @@ bool persistent_pcg(DeviceState& D) {
   const std::size_t smem = words * sizeof(double);
   if (smem > 200 * 1024) return false;
   if (smem != D.pcg_smem || D.pcg_grid == 0) {  // occupancy queried once per shared-memory size
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_pcg_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    CK(static_cast<cudaError_t>(per_device(reinterpret_cast<const void*>(&k_pcg_persistent), [] {
+      return static_cast<int>(
+          cudaFuncSetAttribute(k_pcg_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    })));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_persistent, 256, smem));
     D.pcg_smem = smem;

@@ -126,6 +126,16 @@ class Engine {
   /// Algorithmic bytes of one PCG iteration: the dense S_s of the Schur apply,
   /// the leaf operators of both preconditioner sweeps and the root apply.
   double pcg_bytes_per_iteration() const;
+  /// Device-timed operator applications (bench rooflines): mean seconds of
+  /// the Schur apply and of the preconditioner apply (device-resident vectors,
+  /// CUDA events on the engine stream) and of the preconditioner's stages.
+  struct OpTimes {
+    double schur = 0, precond = 0;
+    double restrict_ = 0, leaf_fwd = 0, tree_fwd = 0, root = 0, tree_bwd = 0, leaf_bwd = 0, prolong = 0,
+           sum_copies = 0;
+    double leaf_sweep_bytes = 0;  // algorithmic bytes of one leaf sweep
+  };
+  OpTimes time_operators(int reps);
   cudaStream_t stream() const;
   /// The pair stage reuses the preconditioner's memory (large runs): the next
   /// set_constraints rebuilds it.

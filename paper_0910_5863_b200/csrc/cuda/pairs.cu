@@ -1463,11 +1463,10 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       // all in shared memory when it fits; otherwise only the 6n vectors, so that
       // several CTAs share an SM and hide the L2 latency of the packed matrix
       const long dyn = smem_ok ? need : 6L * maxn;
-      static bool syevx_attr = false;
-      if (!syevx_attr) {
-        CK(cudaFuncSetAttribute(k_syevx, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
-        syevx_attr = true;
-      }
+      CK(static_cast<cudaError_t>(per_device(reinterpret_cast<const void*>(&k_syevx), [] {
+        return static_cast<int>(cudaFuncSetAttribute(k_syevx, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      224 * 1024));
+      })));
       const char* pe = std::getenv("BDDC_B200_PROFILE");
       const int tr_on = pe && *pe && *pe != '0';
       CK(cudaMemcpyToSymbolAsync(g_syevx_trace_on, &tr_on, sizeof(int), 0, cudaMemcpyHostToDevice, st_));
