@@ -1187,6 +1187,183 @@ __global__ void __launch_bounds__(256) k_front_backward_cl(const SolveDesc* ds, 
 }
 
 // ---------------------------------------------------------------------------
+// Dataflow front sweeps (k_sweep_fwd_dag / k_sweep_bwd_dag): a batch of fronts
+// as a pool of row-tile tasks over a persistent grid instead of one CTA (or
+// cluster) per front.  Forward task (front f, row tile i) is left-looking: it
+// streams the tiles L(i, k), k < min(i, nb) -- each factor tile is read by
+// exactly one task, once -- and adds L(i, k) z_k as soon as block k is solved
+// (per-front progress counter: release store by the solver, relaxed polls +
+// one acquire fence by the readers).  The L loads are issued before the wait,
+// so they are in flight while the pivot chain advances.  A block-row task then
+// solves z_i = Dinv_i (x_i - acc) (Dinv_i prefetched into shared memory with
+// cp.async at task start) and publishes it; coarse-row tasks (i >= nb) only
+// subtract.  The backward sweep is the mirror image: task (f, kb) streams the
+// tiles L(r, kb) of rows r > kb, last rows first, and solves x_kb = Dinv_kb^T
+// (x_kb - sum_r L(r,kb)^T x_r).  Tasks are handed out level-major by an atomic
+// ticket (row tile i of every front before row tile i + 1), so a task only waits
+// for tasks with smaller tickets, which run on CTAs that already hold them: the
+// schedule cannot deadlock for any grid.  Every sum is formed in a fixed order
+// (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int SW_LDS = 68;  // shared-memory ld of the Dinv tile (16-byte rows, few bank conflicts)
+
+__device__ __forceinline__ void sweep_prefetch_dinv(double* dvs, const double* dv) {
+  for (int q = threadIdx.x; q < 64 * 32; q += 256)
+    cp_async16(dvs + (q >> 5) * SW_LDS + (q & 31) * 2, dv + (q >> 5) * 64 + (q & 31) * 2);
+  cp_async_commit();
+}
+
+__device__ __forceinline__ void sweep_wait(const int* prog, int need, int& ready) {
+  if (ready >= need) return;
+  while ((ready = ld_relaxed(prog)) < need) {
+  }
+  fence_acquire();
+}
+
+__global__ void __launch_bounds__(256, 3) k_sweep_fwd_dag(const SolveDesc* ds, int batch, int levels, int* ctl,
+                                                           const int* done) {
+  if (done && *done) return;
+  __shared__ __align__(16) double dvs[64 * SW_LDS];
+  __shared__ double red[8][64];
+  __shared__ double v[64];
+  __shared__ int s_task;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* prog = ctl + 1;
+  const long total = (long)levels * batch;
+  for (;;) {
+    if (tid == 0) s_task = atomicAdd(ctl, 1);
+    __syncthreads();
+    const long t = s_task;
+    if (t >= total) return;
+    const int i = static_cast<int>(t / batch), f = static_cast<int>(t % batch);
+    const SolveDesc d = ds[f];
+    const int nt = d.n / kTile, nb = d.p / kTile;
+    if (i < nt) {
+      const bool solve = i < nb;
+      if (solve) sweep_prefetch_dinv(dvs, d.dinv + (size_t)i * 64 * 64);
+      const size_t ld = d.n;
+      const int K = min(i, nb);
+      double a0 = 0.0, a1 = 0.0;
+      int ready = 0;
+      const double* lrow = d.a + (size_t)(8 * warp) * ld + i * kTile + 2 * lane;
+      for (int k = 0; k < K; ++k) {
+        const double* base = lrow + (size_t)k * kTile * ld;
+        double2 L[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) L[q] = __ldcs(reinterpret_cast<const double2*>(base + (size_t)q * ld));
+        sweep_wait(prog + f, k + 1, ready);
+        const double* z = d.x + k * kTile + 8 * warp;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double zq = __ldcg(z + q);
+          a0 += L[q].x * zq;
+          a1 += L[q].y * zq;
+        }
+      }
+      red[warp][2 * lane] = a0;
+      red[warp][2 * lane + 1] = a1;
+      __syncthreads();
+      if (tid < 64) {
+        double acc = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) acc += red[w][tid];
+        const double val = __ldcg(d.x + i * kTile + tid) - acc;
+        if (solve) v[tid] = val;
+        else d.x[i * kTile + tid] = val;
+      }
+      if (solve) {
+        cp_async_wait<0>();
+        __syncthreads();
+        const int row = tid >> 2, part = tid & 3;
+        double sum = 0.0;
+        for (int c = part; c < 64; c += 4) sum += dvs[c * SW_LDS + row] * v[c];
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        if (part == 0) d.x[i * kTile + row] = sum;
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          st_release(prog + f, i + 1);
+        }
+      }
+    }
+    __syncthreads();  // s_task and the shared buffers are reused by the next task
+  }
+}
+
+__device__ __forceinline__ double sweep_xin(const double* x, int p, const int* cmap, const double* croot, int r) {
+  if (cmap && r >= p) {
+    const int k = cmap[r - p];
+    return k >= 0 ? croot[k] : 0.0;
+  }
+  return __ldcg(x + r);
+}
+
+__global__ void __launch_bounds__(256, 2) k_sweep_bwd_dag(const SolveDesc* ds, int batch, int levels, int* ctl,
+                                                           const int* done) {
+  if (done && *done) return;
+  __shared__ __align__(16) double dvs[64 * SW_LDS];
+  __shared__ double v[64];
+  __shared__ int s_task;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* prog = ctl + 1;
+  const long total = (long)levels * batch;
+  for (;;) {
+    if (tid == 0) s_task = atomicAdd(ctl, 1);
+    __syncthreads();
+    const long t = s_task;
+    if (t >= total) return;
+    const int l = static_cast<int>(t / batch), f = static_cast<int>(t % batch);
+    const SolveDesc d = ds[f];
+    const int nt = d.n / kTile, nb = d.p / kTile;
+    const int kb = nb - 1 - l;
+    if (l == 0 && d.cmap)  // the first task of a front writes its coarse rows (others read croot)
+      for (int r = d.p + tid; r < d.n; r += 256) d.x[r] = sweep_xin(d.x, d.p, d.cmap, d.croot, r);
+    if (kb >= 0) {
+      sweep_prefetch_dinv(dvs, d.dinv + (size_t)kb * 64 * 64);
+      const size_t ld = d.n;
+      double acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+      int ready = 0;
+      const double* lcol = d.a + (size_t)(kb * kTile + 8 * warp) * ld + 2 * lane;
+      for (int r = nt - 1; r > kb; --r) {
+        const double* base = lcol + r * kTile;
+        double2 L[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) L[q] = __ldcs(reinterpret_cast<const double2*>(base + (size_t)q * ld));
+        if (r < nb) sweep_wait(prog + f, nb - r, ready);
+        const int row = r * kTile + 2 * lane;
+        const double x0 = sweep_xin(d.x, d.p, d.cmap, d.croot, row), x1 = sweep_xin(d.x, d.p, d.cmap, d.croot, row + 1);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += L[q].x * x0 + L[q].y * x1;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double sum = acc[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) v[8 * warp + q] = __ldcg(d.x + kb * kTile + 8 * warp + q) - sum;
+      }
+      cp_async_wait<0>();
+      __syncthreads();
+      const int row = tid >> 2, part = tid & 3;
+      double sum = 0.0;
+      for (int c = part; c < 64; c += 4) sum += dvs[row * SW_LDS + c] * v[c];
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      if (part == 0) d.x[kb * kTile + row] = sum;
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        st_release(prog + f, l + 1);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // One large front (the root when R^{-1} is not formed) over the whole GPU:
 // a cooperative grid of G CTAs, row tile t owned by CTA t % G, the CTA's own
 // rows kept in shared memory.  Forward: at block kb every CTA updates its rows
@@ -1615,12 +1792,51 @@ void launch_big(K kern, int max_n, size_t ws_per_cta, cudaStream_t stream, const
 }
 }  // namespace
 
+namespace {
+// Dataflow sweeps for batches of two or more fronts (BDDC_B200_SWEEP=dag|cluster
+// overrides; the cluster kernels are the round-1 path).
+bool dag_sweep(int batch) {
+  if (const char* e = std::getenv("BDDC_B200_SWEEP"); e && *e) return std::string(e) == "dag";
+  return batch >= 2;
+}
+
+using SweepKernel = void (*)(const SolveDesc*, int, int, int*, const int*);
+void launch_sweep_dag(SweepKernel kern, const SolveDesc* d_descs, int batch, int levels, cudaStream_t stream,
+                      const int* done) {
+  // ctl[0] = ticket counter, ctl[1 + f] = progress of front f; fixed minimum
+  // size so captured graphs keep a valid pointer
+  int* ctl = reinterpret_cast<int*>(
+      stream_workspace(2, std::max<size_t>(8192, (size_t)batch / 2 + 8), stream));
+  if (!ctl) throw std::runtime_error("sweep workspace allocation failed");
+  cudaMemsetAsync(ctl, 0, (size_t)(batch + 1) * sizeof(int), stream);
+  const int occ = kern == k_sweep_fwd_dag
+                      ? per_device(reinterpret_cast<const void*>(&k_sweep_fwd_dag), [] {
+                          int o = 0;
+                          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep_fwd_dag, 256, 0);
+                          return o;
+                        })
+                      : per_device(reinterpret_cast<const void*>(&k_sweep_bwd_dag), [] {
+                          int o = 0;
+                          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep_bwd_dag, 256, 0);
+                          return o;
+                        });
+  const long tasks = (long)levels * batch;
+  const int grid = static_cast<int>(std::max<long>(1, std::min<long>(tasks, (long)std::max(occ, 1) * sm_count())));
+  kern<<<grid, 256, 0, stream>>>(d_descs, batch, levels, ctl, done);
+  count_launch(2);  // memset + sweep
+}
+}  // namespace
+
 void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream, const int* done) {
   if (batch == 0) return;
   per_device(reinterpret_cast<const void*>(&configure_device), configure_device);
   if (big_sweep(batch, max_n)) {
     launch_big(k_big_forward, max_n, 2, stream, d_descs, done);  // z double buffer (2 x 64 <= 2 G)
     count_launch(1);
+    return;
+  }
+  if (dag_sweep(batch)) {
+    launch_sweep_dag(k_sweep_fwd_dag, d_descs, batch, std::max(1, max_n / kTile), stream, done);
     return;
   }
   const int cl = sweep_cluster(batch, 4);  // measured: wider forward clusters are slower
@@ -1639,6 +1855,10 @@ void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t
   if (big_sweep(batch, max_n)) {
     launch_big(k_big_backward, max_n, 2 * 64, stream, d_descs, done);  // partials: 2 x G x 64
     count_launch(1);
+    return;
+  }
+  if (dag_sweep(batch)) {
+    launch_sweep_dag(k_sweep_bwd_dag, d_descs, batch, std::max(1, max_n / kTile), stream, done);
     return;
   }
   static int max_cl = 16;  // lowered once if the device refuses a cluster width

@@ -34,6 +34,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import pickle
 import sys
 import time
 from pathlib import Path
@@ -126,11 +127,16 @@ def make(config: int, workers: int, pcg_runs: bool, shrink=None, suffix=""):
     res = [None] * len(pairs)
     t1 = time.perf_counter()
     ctx = mp.get_context("fork")
-    with ctx.Pool(workers) as pool:
-        for i, out in enumerate(pool.imap_unordered(_pair_task, range(len(pairs)), chunksize=2)):
-            res[out[0]] = out
-            if (i + 1) % 100 == 0:
-                print("  %d/%d pairs, %.0fs" % (i + 1, len(pairs), time.perf_counter() - t1), flush=True)
+    cache = Path(os.environ.get("FULLSIZE_CACHE", "/tmp")) / ("fullsize_pairs_cfg%d%s.pkl" % (config, suffix))
+    if cache.exists():  # per-pair results of an earlier run of this script (scratch, not committed)
+        res = pickle.loads(cache.read_bytes())
+    else:
+        with ctx.Pool(workers) as pool:
+            for i, out in enumerate(pool.imap_unordered(_pair_task, range(len(pairs)), chunksize=2)):
+                res[out[0]] = out
+                if (i + 1) % 100 == 0:
+                    print("  %d/%d pairs, %.0fs" % (i + 1, len(pairs), time.perf_counter() - t1), flush=True)
+        cache.write_bytes(pickle.dumps(res))
     pair_cpu = sum(r[6] for r in res)
     print("cfg%d: pairs %.0fs wall, %.0fs single-thread CPU" % (config, time.perf_counter() - t1, pair_cpu),
           flush=True)

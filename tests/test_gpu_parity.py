@@ -311,3 +311,14 @@ def test_pair_eigensolver_placements(placement, monkeypatch):
     (G, the placement when the pairs outnumber the SMs) against the oracle."""
     monkeypatch.setenv("BDDC_B200_SYEVX", placement)
     test_adaptive_selection_and_spectrum(*ADAPTIVE[5])
+
+
+@pytest.mark.parametrize("sweep", ["dag", "cluster"])
+def test_front_sweep_schedules(sweep, monkeypatch):
+    """Both front-sweep schedules (dense.cu: dataflow row-tile tasks over a
+    persistent grid, the default for batches of two or more fronts; one CTA or
+    cluster per front) on the leaf fronts and the primal tree, against the
+    oracle's preconditioner and PCG."""
+    monkeypatch.setenv("BDDC_B200_SWEEP", sweep)
+    test_operators_pcg_and_solution(*OPS[-1], "factor", "sweep", "0", monkeypatch)
+    test_primal_tree(*TREE[2], "factor", "factor", monkeypatch)
