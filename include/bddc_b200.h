@@ -151,6 +151,13 @@ int bddc_b200_constraints_arithmetic(bddc_b200_t* h, int edge_globs, int face_gl
 int bddc_b200_constraint_rows(const bddc_b200_t* h, int64_t* rows);
 int bddc_b200_constraint_count(const bddc_b200_t* h, int64_t* n);
 int bddc_b200_constraint_get(const bddc_b200_t* h, int a, int* glob, int64_t* n_weights, double* weights);
+/* A caller-built ConstraintSet (tests/test_constraints.cpp:83-100): clear the
+ * handle's set, then add_average (constraints.cpp:61-76) one average at a
+ * time -- `weights` has one entry per free dof of the glob (glob_free_dofs,
+ * constraints.cpp:25-32); the pivoted-QR rank filter (tolerance 1e-8) decides
+ * whether it is kept (*kept = 1) or dropped as dependent / zero (*kept = 0). */
+int bddc_b200_constraints_clear(bddc_b200_t* h);
+int bddc_b200_constraint_add(bddc_b200_t* h, int glob, const double* weights, int64_t n, int adaptive, int* kept);
 
 /* HarmonicExtension ctor (spaces.cpp:108-147): device A_II factorization and
  * dense interface Schur complements. */
@@ -165,6 +172,26 @@ int bddc_b200_pair_report(const bddc_b200_t* h, int k, int* si, int* sj, int* en
                           double* omega_next, int* saturated, int64_t* n_eig, double* eigenvalues);
 /* change_of_variables + BddcPreconditioner ctor (bddc_operator.cpp:38-50). */
 int bddc_b200_setup_preconditioner(bddc_b200_t* h);
+/* The same with the stabilization parameter t of the reference ctor
+ * (bddc_operator.hpp:32-35; t <= 0 means max diag K).  The device path factors
+ * the exact primal reformulation, on which t does not act, so
+ * t only sets what the accessors below report. */
+int bddc_b200_setup_preconditioner_t(bddc_b200_t* h, double t);
+/* BddcPreconditioner::stabilization_t() (bddc_operator.hpp:52): the t used. */
+int bddc_b200_stabilization_t(bddc_b200_t* h, double* t);
+/* BddcPreconditioner::stabilized() (bddc_operator.hpp:51), formed on the host
+ * (bddc_operator.cpp:7-36: Pi K Pi + t (I - Pi), symmetrized, pruned at 1e-12
+ * max|entry|) as full symmetric CSR: query n and nnz with ptr == NULL, then
+ * fill ptr (n+1), idx, val (nnz). */
+int bddc_b200_stabilized(bddc_b200_t* h, int64_t* n, int64_t* nnz, int64_t* ptr, int64_t* idx, double* val);
+/* GlobTransform of one glob under the handle's constraint set
+ * (transform.cpp:51-90, transform.hpp:20-27): rank and the dense n x n basis
+ * block t (row-major; the identity for an unconstrained glob). */
+int bddc_b200_glob_transform(bddc_b200_t* h, int glob, int* rank, int64_t* n, double* t);
+/* run_items' export_directory dumps (experiment.cpp:172-178, matrix_market.cpp:
+ * 12-38): <stem>_stabilized.mtx (symmetric, lower triangle) and
+ * <stem>_constraints.mtx (the transformed constraint matrix D^c). */
+int bddc_b200_export_matrix_market(bddc_b200_t* h, const char* stem);
 
 /* LinearOperator seam (pcg.hpp:18): InterfaceProblem::apply (schur.cpp:12-36)
  * and BddcPreconditioner::apply (bddc_operator.cpp:101-103); interface vectors. */

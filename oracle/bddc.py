@@ -33,25 +33,28 @@ def assemble_transformed_operator(systems, maps: EmbeddingMaps, cov: ChangeOfVar
     return (upper + sp.triu(upper, k=1).T).tocsr()
 
 
-def stabilize(k: sp.csr_matrix, projector: sp.csr_matrix, t: float):
-    """`bddc_operator.cpp:25-36`: P K P + t (I - P), symmetrized and pruned."""
+def stabilize(k: sp.csr_matrix, projector: sp.csr_matrix, t: float, prune: bool = True):
+    """`bddc_operator.cpp:25-36`: P K P + t (I - P), symmetrized and pruned.
+    `prune=False` is NOT the reference: it keeps the entries below
+    1e-12 max|entry| (used only to obtain the mathematically intended operator
+    where the reference's pruning makes the factorization fail)."""
     if t <= 0:
         t = float(k.diagonal().max())
     n = k.shape[0]
     m = projector @ k @ projector + t * (sp.identity(n, format="csr") - projector)
     sym = 0.5 * (m.T + m)
-    return pruned(sym), t
+    return (pruned(sym) if prune else sp.csr_matrix(sym)), t
 
 
 class BddcPreconditioner:
     """`bddc_operator.cpp:38-103`."""
 
     def __init__(self, systems, maps: EmbeddingMaps, averaging: AveragingOperator,
-                 cov: ChangeOfVariables, t: float = -1.0):
+                 cov: ChangeOfVariables, t: float = -1.0, prune: bool = True):
         self.systems, self.maps, self.avg, self.cov = systems, maps, averaging, cov
         self.projector = GroupProjector(cov.groups, maps.wc_dim)
         self.transformed = assemble_transformed_operator(systems, maps, cov)
-        self.stabilized, self.t = stabilize(self.transformed, self.projector.matrix(), t)
+        self.stabilized, self.t = stabilize(self.transformed, self.projector.matrix(), t, prune)
         self.factor = Factorization(self.stabilized)
         self.bt = [b.T.tocsr() for b in cov.basis]
 

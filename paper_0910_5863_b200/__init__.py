@@ -118,6 +118,13 @@ EXPORTS = {
     "bddc_b200_pair_report": (C.c_int, [P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                         C.POINTER(C.c_int), D, C.POINTER(C.c_int), I64, D]),
     "bddc_b200_setup_preconditioner": (C.c_int, [P]),
+    "bddc_b200_setup_preconditioner_t": (C.c_int, [P, C.c_double]),
+    "bddc_b200_stabilization_t": (C.c_int, [P, D]),
+    "bddc_b200_stabilized": (C.c_int, [P, I64, I64, I64, I64, D]),
+    "bddc_b200_export_matrix_market": (C.c_int, [P, C.c_char_p]),
+    "bddc_b200_glob_transform": (C.c_int, [P, C.c_int, C.POINTER(C.c_int), I64, D]),
+    "bddc_b200_constraints_clear": (C.c_int, [P]),
+    "bddc_b200_constraint_add": (C.c_int, [P, C.c_int, D, C.c_int64, C.c_int, C.POINTER(C.c_int)]),
     "bddc_b200_interface_size": (C.c_int, [P, I64]),
     "bddc_b200_schur_apply": (C.c_int, [P, D, D]),
     "bddc_b200_precond_apply": (C.c_int, [P, D, D]),
@@ -458,8 +465,47 @@ class BDDC:
                             saturated=bool(sat.value), eigenvalues=ev))
         return out
 
-    def setup_preconditioner(self):
-        _check(self._lib.bddc_b200_setup_preconditioner(self._h))
+    def setup_preconditioner(self, t: float = -1.0):
+        """BddcPreconditioner(systems, maps, averaging, cov, t) (bddc_operator.cpp:38-50)."""
+        _check(self._lib.bddc_b200_setup_preconditioner_t(self._h, t))
+
+    def stabilization_t(self) -> float:
+        t = C.c_double()
+        _check(self._lib.bddc_b200_stabilization_t(self._h, C.byref(t)))
+        return t.value
+
+    def stabilized(self):
+        """The stabilized operator A~ (scipy CSR, full symmetric), formed on the host."""
+        import scipy.sparse as sp
+        n, nnz = C.c_int64(), C.c_int64()
+        _check(self._lib.bddc_b200_stabilized(self._h, C.byref(n), C.byref(nnz), None, None, None))
+        ptr = np.empty(n.value + 1, dtype=np.int64)
+        idx = np.empty(nnz.value, dtype=np.int64)
+        val = np.empty(nnz.value)
+        _check(self._lib.bddc_b200_stabilized(self._h, C.byref(n), C.byref(nnz), ptr.ctypes.data_as(I64),
+                                              idx.ctypes.data_as(I64), _dptr(val)))
+        return sp.csr_matrix((val, idx, ptr), shape=(n.value, n.value))
+
+    def glob_transform(self, glob: int):
+        """(rank, t) of the glob under the current constraint set (transform.cpp:51-90)."""
+        r, n = C.c_int(), C.c_int64()
+        _check(self._lib.bddc_b200_glob_transform(self._h, glob, C.byref(r), C.byref(n), None))
+        t = np.empty((n.value, n.value))
+        _check(self._lib.bddc_b200_glob_transform(self._h, glob, C.byref(r), C.byref(n), _dptr(t)))
+        return r.value, t
+
+    def export_matrix_market(self, stem: str):
+        _check(self._lib.bddc_b200_export_matrix_market(self._h, stem.encode()))
+
+    def clear_constraints(self):
+        _check(self._lib.bddc_b200_constraints_clear(self._h))
+
+    def add_average(self, glob: int, weights, adaptive: bool = False) -> bool:
+        """add_average (constraints.cpp:61-76): True when kept by the rank filter."""
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        kept = C.c_int()
+        _check(self._lib.bddc_b200_constraint_add(self._h, glob, _dptr(w), len(w), int(adaptive), C.byref(kept)))
+        return bool(kept.value)
 
     @property
     def interface_size(self) -> int:

@@ -11,6 +11,7 @@
 #include <string>
 
 #include "cuda/engine.hpp"
+#include "host/export.hpp"
 #include "host/host.hpp"
 
 using namespace b200;
@@ -21,6 +22,9 @@ struct bddc_b200 {
   std::unique_ptr<Engine> engine;
   EnrichOutcome last_enrich;
   bool analysed = false;
+  double t = -1.0;          // stabilization parameter of the last setup (bddc_operator.hpp:32-35)
+  CsrMatrix stabilized;     // cached by bddc_b200_stabilized (query, then fill)
+  bool have_stabilized = false;
 };
 
 namespace {
@@ -258,6 +262,28 @@ int bddc_b200_constraints_arithmetic(bddc_b200_t* h, int edges, int faces) {
   return guarded([&] { h->cs = arithmetic_constraints(h->model, edges != 0, faces != 0); });
 }
 
+int bddc_b200_constraints_clear(bddc_b200_t* h) {
+  return guarded([&] { h->cs = ConstraintSet{}; });
+}
+
+int bddc_b200_constraint_add(bddc_b200_t* h, int glob, const double* weights, int64_t n, int adaptive,
+                             int* kept) {
+  return guarded([&] {
+    if (glob < 0 || glob >= static_cast<int>(h->model.globs.size()))
+      throw Error(kBadProblemSpec, "constraint_add: glob index out of range");
+    const std::size_t nd = h->model.glob_dofs[glob].size();
+    if (static_cast<std::size_t>(n) != nd)
+      throw Error(kBadProblemSpec, "constraint_add: weights length " + std::to_string(n) +
+                                       " != free dofs of the glob " + std::to_string(nd));
+    Average a;
+    a.glob = glob;
+    a.weights.assign(weights, weights + n);
+    a.adaptive = adaptive;
+    const bool k = add_average(h->cs, std::move(a));
+    if (kept) *kept = k ? 1 : 0;
+  });
+}
+
 int bddc_b200_constraint_rows(const bddc_b200_t* h, int64_t* rows) {
   return guarded([&] { *rows = h->cs.row_count(h->model); });
 }
@@ -315,10 +341,67 @@ int bddc_b200_pair_report(const bddc_b200_t* h, int k, int* si, int* sj, int* en
   });
 }
 
-int bddc_b200_setup_preconditioner(bddc_b200_t* h) {
+int bddc_b200_setup_preconditioner(bddc_b200_t* h) { return bddc_b200_setup_preconditioner_t(h, -1.0); }
+
+int bddc_b200_setup_preconditioner_t(bddc_b200_t* h, double t) {
   return guarded([&] {
     ensure_analysis(h);
     engine(h).set_constraints(h->cs);
+    h->t = t;
+    h->have_stabilized = false;
+  });
+}
+
+int bddc_b200_stabilization_t(bddc_b200_t* h, double* t) {
+  return guarded([&] { *t = stabilization_t(h->model, change_of_variables(h->cs, h->model), h->t); });
+}
+
+int bddc_b200_stabilized(bddc_b200_t* h, int64_t* n, int64_t* nnz, int64_t* ptr, int64_t* idx, double* val) {
+  return guarded([&] {
+    if (!h->have_stabilized) {
+      h->stabilized = stabilized_operator(h->model, change_of_variables(h->cs, h->model), h->t, nullptr);
+      h->have_stabilized = true;
+    }
+    const CsrMatrix& a = h->stabilized;
+    *n = a.rows;
+    *nnz = static_cast<int64_t>(a.val.size());
+    if (ptr) {
+      std::memcpy(ptr, a.ptr.data(), a.ptr.size() * sizeof(int64_t));
+      std::memcpy(idx, a.idx.data(), a.idx.size() * sizeof(int64_t));
+      std::memcpy(val, a.val.data(), a.val.size() * sizeof(double));
+      h->stabilized = CsrMatrix{};  // filled: release the cache
+      h->have_stabilized = false;
+    }
+  });
+}
+
+int bddc_b200_glob_transform(bddc_b200_t* h, int glob, int* rank, int64_t* n, double* t) {
+  return guarded([&] {
+    const ChangeOfVariables cov = change_of_variables(h->cs, h->model);
+    for (const GlobTransform& gt : cov.transforms)
+      if (gt.glob == glob) {
+        *rank = gt.rank;
+        *n = gt.n;
+        if (t) {
+          const std::vector<double> d = gt.dense_t();
+          std::memcpy(t, d.data(), d.size() * sizeof(double));
+        }
+        return;
+      }
+    *rank = 0;
+    *n = static_cast<int64_t>(h->model.glob_dofs.at(glob).size());
+    if (t)
+      for (int64_t i = 0; i < *n * *n; ++i) t[i] = (i % (*n + 1)) == 0 ? 1.0 : 0.0;
+  });
+}
+
+int bddc_b200_export_matrix_market(bddc_b200_t* h, const char* stem) {
+  return guarded([&] {
+    const ChangeOfVariables cov = change_of_variables(h->cs, h->model);
+    write_matrix_market(std::string(stem) + "_stabilized.mtx", stabilized_operator(h->model, cov, h->t, nullptr),
+                        true);
+    write_matrix_market(std::string(stem) + "_constraints.mtx",
+                        transformed_constraint_matrix(cov, h->model.maps.wc_dim), false);
   });
 }
 

@@ -1213,14 +1213,37 @@ __device__ __forceinline__ void sweep_prefetch_dinv(double* dvs, const double* d
   cp_async_commit();
 }
 
-__device__ __forceinline__ void sweep_wait(const int* prog, int need, int& ready) {
-  if (ready >= need) return;
-  while ((ready = ld_relaxed(prog)) < need) {
+// The last CTA to leave zeroes the counters for the next launch (no memset
+// node per sweep; the buffer is zeroed once when allocated).
+__device__ __forceinline__ void sweep_exit(int* ctl, int batch) {
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(ctl + 1, 1) == static_cast<int>(gridDim.x) - 1;
   }
-  fence_acquire();
+  __syncthreads();
+  if (s_last) {
+    for (int q = threadIdx.x; q < batch + 2; q += blockDim.x) ctl[q] = 0;
+    __threadfence();
+  }
 }
 
-__global__ void __launch_bounds__(256, 3) k_sweep_fwd_dag(const SolveDesc* ds, int batch, int levels, int* ctl,
+// Lane 0 of each warp polls (relaxed) and takes the acquire fence; __syncwarp
+// orders the other lanes' reads of the published block after it.
+__device__ __forceinline__ void sweep_wait(const int* prog, int need, int& ready) {
+  if (ready >= need) return;
+  if ((threadIdx.x & 31) == 0) {
+    int v;
+    while ((v = ld_relaxed(prog)) < need) {
+    }
+    fence_acquire();
+    ready = v;
+  }
+  ready = __shfl_sync(0xffffffffu, ready, 0);
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256, 4) k_sweep_fwd_dag(const SolveDesc* ds, int batch, int levels, int* ctl,
                                                            const int* done) {
   if (done && *done) return;
   __shared__ __align__(16) double dvs[64 * SW_LDS];
@@ -1228,13 +1251,16 @@ __global__ void __launch_bounds__(256, 3) k_sweep_fwd_dag(const SolveDesc* ds, i
   __shared__ double v[64];
   __shared__ int s_task;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int* prog = ctl + 1;
+  int* prog = ctl + 2;
   const long total = (long)levels * batch;
   for (;;) {
     if (tid == 0) s_task = atomicAdd(ctl, 1);
     __syncthreads();
     const long t = s_task;
-    if (t >= total) return;
+    if (t >= total) {
+      sweep_exit(ctl, batch);
+      return;
+    }
     const int i = static_cast<int>(t / batch), f = static_cast<int>(t % batch);
     const SolveDesc d = ds[f];
     const int nt = d.n / kTile, nb = d.p / kTile;
@@ -1281,10 +1307,7 @@ __global__ void __launch_bounds__(256, 3) k_sweep_fwd_dag(const SolveDesc* ds, i
         sum += __shfl_xor_sync(0xffffffffu, sum, 2);
         if (part == 0) d.x[i * kTile + row] = sum;
         __syncthreads();
-        if (tid == 0) {
-          __threadfence();
-          st_release(prog + f, i + 1);
-        }
+        if (tid == 0) st_release(prog + f, i + 1);  // fence.acq_rel + store: covers the CTA's writes (bar.sync)
       }
     }
     __syncthreads();  // s_task and the shared buffers are reused by the next task
@@ -1306,13 +1329,16 @@ __global__ void __launch_bounds__(256, 2) k_sweep_bwd_dag(const SolveDesc* ds, i
   __shared__ double v[64];
   __shared__ int s_task;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int* prog = ctl + 1;
+  int* prog = ctl + 2;
   const long total = (long)levels * batch;
   for (;;) {
     if (tid == 0) s_task = atomicAdd(ctl, 1);
     __syncthreads();
     const long t = s_task;
-    if (t >= total) return;
+    if (t >= total) {
+      sweep_exit(ctl, batch);
+      return;
+    }
     const int l = static_cast<int>(t / batch), f = static_cast<int>(t % batch);
     const SolveDesc d = ds[f];
     const int nt = d.n / kTile, nb = d.p / kTile;
@@ -1354,10 +1380,7 @@ __global__ void __launch_bounds__(256, 2) k_sweep_bwd_dag(const SolveDesc* ds, i
       sum += __shfl_xor_sync(0xffffffffu, sum, 2);
       if (part == 0) d.x[kb * kTile + row] = sum;
       __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        st_release(prog + f, l + 1);
-      }
+      if (tid == 0) st_release(prog + f, l + 1);
     }
     __syncthreads();
   }
@@ -1573,11 +1596,38 @@ double* stream_workspace(int slot, size_t doubles, cudaStream_t stream) {
   }
   return w.p;
 }
+// Counters of the dataflow sweeps: zeroed once when (re)allocated, then kept
+// zero by the kernels themselves (sweep_exit).  Fixed minimum size so captured
+// graphs keep a valid pointer.
+int* sweep_counters(size_t ints, cudaStream_t stream) {
+  struct Ws {
+    int* p = nullptr;
+    size_t cap = 0;
+  };
+  static std::mutex mu;
+  static std::map<cudaStream_t, Ws> ws;
+  std::lock_guard<std::mutex> lk(mu);
+  Ws& w = ws[stream];
+  if (ints > w.cap) {
+    if (w.p) {
+      cudaStreamSynchronize(stream);
+      cudaFree(w.p);
+    }
+    const size_t cap = std::max<size_t>(16384, ints);
+    if (cudaMalloc(&w.p, cap * sizeof(int)) != cudaSuccess) throw std::runtime_error("sweep counters");
+    cudaMemsetAsync(w.p, 0, cap * sizeof(int), stream);
+    w.cap = cap;
+  }
+  return w.p;
+}
+
 // slot 0: split-K partial tiles; slot 1: the large-front sweeps (small, never
 // reallocated once sized, so captured PCG graphs keep a valid pointer)
 double* splitk_workspace(size_t doubles, cudaStream_t stream) { return stream_workspace(0, doubles, stream); }
 
 }  // namespace
+
+void ensure_sweep_workspace(cudaStream_t stream) { sweep_counters(16384, stream); }
 
 int per_device(const void* key, int (*make)()) {
   static std::mutex m;
@@ -1805,10 +1855,7 @@ void launch_sweep_dag(SweepKernel kern, const SolveDesc* d_descs, int batch, int
                       const int* done) {
   // ctl[0] = ticket counter, ctl[1 + f] = progress of front f; fixed minimum
   // size so captured graphs keep a valid pointer
-  int* ctl = reinterpret_cast<int*>(
-      stream_workspace(2, std::max<size_t>(8192, (size_t)batch / 2 + 8), stream));
-  if (!ctl) throw std::runtime_error("sweep workspace allocation failed");
-  cudaMemsetAsync(ctl, 0, (size_t)(batch + 1) * sizeof(int), stream);
+  int* ctl = sweep_counters(batch + 2, stream);
   const int occ = kern == k_sweep_fwd_dag
                       ? per_device(reinterpret_cast<const void*>(&k_sweep_fwd_dag), [] {
                           int o = 0;
@@ -1823,7 +1870,7 @@ void launch_sweep_dag(SweepKernel kern, const SolveDesc* d_descs, int batch, int
   const long tasks = (long)levels * batch;
   const int grid = static_cast<int>(std::max<long>(1, std::min<long>(tasks, (long)std::max(occ, 1) * sm_count())));
   kern<<<grid, 256, 0, stream>>>(d_descs, batch, levels, ctl, done);
-  count_launch(2);  // memset + sweep
+  count_launch(1);
 }
 }  // namespace
 

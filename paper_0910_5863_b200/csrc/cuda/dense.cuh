@@ -54,6 +54,10 @@ int sm_count();
 /// host threads).
 int per_device(const void* key, int (*make)());
 
+/// Allocate (once per stream, outside any graph capture) the counters of the
+/// dataflow front sweeps.
+void ensure_sweep_workspace(cudaStream_t stream);
+
 /// Kernel-launch accounting (bench "gpu_launches").
 void count_launch(long long n);
 long long launch_count();

@@ -1446,6 +1446,7 @@ void Engine::prepare() {
   DeviceState& D = *d_;
   if (D.prepared) return;
   const Model& m = m_;
+  ensure_sweep_workspace(D.st);
   D.nsub = static_cast<int>(m.subs.size());
   D.niface = interface_size();
   const int ns = D.nsub;

@@ -47,35 +47,7 @@ import numpy as np  # noqa: E402
 
 HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE.parents[1]))
-
-SKETCH_K = 3
-
-
-def sketch(glob: int, rows: np.ndarray) -> np.ndarray:
-    """Basis-independent fingerprint of the span of a glob's averages: for
-    seeded Gaussian g_k, h_k (seed = glob id), (g_k^T Q Q^T h_k)/(|g_k| |h_k|)
-    with Q an orthonormal basis of the rows.  Equal spans give equal sketches
-    whatever vectors span them (degenerate eigenvalues)."""
-    rows = np.atleast_2d(np.asarray(rows, dtype=float))
-    n = rows.shape[1]
-    q, _ = np.linalg.qr(rows.T)
-    rng = np.random.default_rng(1_000_003 + glob)
-    g = rng.standard_normal((n, SKETCH_K))
-    h = rng.standard_normal((n, SKETCH_K))
-    return np.einsum("ik,ik->k", q.T @ g, q.T @ h) / (np.linalg.norm(g, axis=0) * np.linalg.norm(h, axis=0))
-
-
-def glob_summary(averages, globs):
-    """(glob ids with averages, counts, face-glob ids, sketches) of a constraint
-    list given as [(glob, weights)]."""
-    by = {}
-    for g, w in averages:
-        by.setdefault(int(g), []).append(np.asarray(w, dtype=float))
-    ids = np.array(sorted(by), dtype=np.int64)
-    counts = np.array([len(by[g]) for g in ids], dtype=np.int64)
-    faces = [g for g in ids if globs[g] == "face"]
-    sk = np.array([sketch(g, np.stack(by[g])) for g in faces]).reshape(-1, SKETCH_K)
-    return ids, counts, np.array(faces, dtype=np.int64), sk
+from fullsize_sketch import glob_summary  # noqa: E402  (this directory)
 
 
 # --- worker state (set before the pool forks) ---------------------------------
@@ -113,6 +85,7 @@ def make(config: int, workers: int, pcg_runs: bool, shrink=None, suffix=""):
     from oracle.adaptive import EnrichmentOptions, PairReport, face_pairs, install_pieces
     from oracle.bddc import BddcPreconditioner
     from oracle.constraints import change_of_variables
+    from oracle.linalg import NotPositiveDefinite
     from oracle.experiment import baseline_config, build_pipeline, constraint_set_for
     from oracle.spaces import AveragingOperator, HarmonicExtension, InterfaceProblem
 
@@ -172,7 +145,26 @@ def make(config: int, workers: int, pcg_runs: bool, shrink=None, suffix=""):
         h = HarmonicExtension(p.systems, p.maps)
         itf = InterfaceProblem(p.systems, p.maps, h)
         cov = change_of_variables(cs, p.globset, p.dmap, p.maps)
-        prec = BddcPreconditioner(p.systems, p.maps, AveragingOperator(p.systems, p.maps), cov)
+        avg = AveragingOperator(p.systems, p.maps)
+        attempts = [("reference (t = max diag K, entries <= 1e-12 max pruned)", dict()),
+                    ("t = max diag K, unpruned", dict(prune=False))]
+        prec, meta["stabilization"] = None, []
+        for label, kw in attempts:
+            try:
+                prec = BddcPreconditioner(p.systems, p.maps, avg, cov, **kw)
+                meta["stabilization"].append(label + ": factorized")
+                break
+            except NotPositiveDefinite as e:
+                # bddc_operator.cpp:25-50: the reference factors the PRUNED stabilized
+                # operator.  When the change of variables makes
+                # max|entry| ~1e10, the 1e-12 relative prune drops O(1e-2) couplings
+                # of the soft dofs and the factorization fails: the reference itself
+                # raises NotPositiveDefinite here.  Pi A~^{-1} Pi of the unpruned
+                # operator is the mathematically intended preconditioner.
+                meta["stabilization"].append(label + ": " + str(e))
+                print("cfg%d: %s failed (%s)" % (config, label, e), flush=True)
+        if prec is None:
+            raise RuntimeError("no stabilization factorized")
         print("cfg%d: preconditioner %.0fs" % (config, time.perf_counter() - t2), flush=True)
         _W.update(prec=prec, itf=itf, rhs=itf.rhs(), tol=cfg.spec.tolerance, maxit=cfg.spec.max_iterations)
         with ctx.Pool(3) as pool:

@@ -4,7 +4,7 @@ Bars (BASELINE.json north_star): identical constraint selection and index
 maps; PCG iterations within +-1; eigenvalues and Lanczos condition estimates
 within 1e-6 relative; solution within 1e-8 relative in the energy norm.
 Operator applications are checked to 1e-11 relative (FP64 roundoff of the
-reduced formulation).  Full-size configs 3-4 are checked
+reduced formulation).  Lanczos estimates: check_kappa.  Full-size configs 3-4 are checked
 through size-independent properties (true residual of the recovered solution,
 deflation of every non-saturated pair after enrichment).
 """
@@ -29,19 +29,45 @@ def rel(a, b):
     return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
 
 
-KAPPA_RTOL = 1e-3
+KAPPA_RTOL = 1e-6  # BASELINE.json north_star
 
 
 def kappa_common(g_alphas, g_betas, o_alphas, o_betas):
-    """Lanczos estimates over the common prefix of two CG runs (iteration counts may
-    differ by one).  CG coefficient j carries relative error ~ eps_op / (|r_j|/|b|):
-    1e-13 operator roundoff (1e-13..1e-12) moves the oracle's own estimate by 1e-6..1e-4
-    (tests/test_oracle_pins.py::test_lanczos_roundoff_floor), so the 1e-6 bar of
-    BASELINE.json is below the roundoff floor and KAPPA_RTOL = 1e-3 is used
-    (the reference's golden table pins kappa to 4 significant digits)."""
+    """Lanczos estimates over the common prefix of two CG runs."""
     n = min(len(g_alphas), len(o_alphas))
     return (lanczos_condition_estimate(list(g_alphas[:n]), list(g_betas[:n])),
             lanczos_condition_estimate(list(o_alphas[:n]), list(o_betas[:n])))
+
+
+def kappa_floor(op, prec, b, seeds=(1, 2)):
+    """Roundoff floor of the oracle's own Lanczos estimate on this problem:
+    the largest relative change of its estimate (and iteration count) when its
+    preconditioner output is perturbed by 1e-13 relative noise."""
+    o = pcg(op, prec, b)
+    shift, its = 0.0, {o.iterations}
+    for seed in seeds:
+        rng = np.random.default_rng(seed)
+        o2 = pcg(op, lambda v: prec(v) * (1 + 1e-13 * rng.standard_normal(len(v))), b)
+        shift = max(shift, abs(o2.condition_estimate - o.condition_estimate) / o.condition_estimate)
+        its.add(o2.iterations)
+    return shift, its
+
+
+def check_kappa(g, o, op=None, prec=None, b=None):
+    """north_star: Lanczos estimates within 1e-6 relative.  With equal iteration
+    counts the full estimates are compared at 1e-6.  When the counts differ (by
+    one, allowed), the two estimates come from Krylov spaces of different
+    dimension; they are then compared at the larger of 1e-6 and twice the
+    oracle's own roundoff floor on this problem (kappa_floor, measured here),
+    and the floor run must itself show that the iteration count is roundoff-
+    sensitive."""
+    k_g, k_o = g["condition_estimate"], o.condition_estimate
+    if g["iterations"] == o.iterations:
+        assert abs(k_g - k_o) <= KAPPA_RTOL * k_o, (k_g, k_o)
+        return
+    floor, its = kappa_floor(op, prec, b)
+    assert len(its) > 1 or g["iterations"] in its, (g["iterations"], its)
+    assert abs(k_g - k_o) <= max(KAPPA_RTOL, 2.0 * floor) * k_o, (k_g, k_o, floor)
 
 
 def energy_error(systems, free, u, u_ref):
@@ -120,8 +146,7 @@ def test_operators_pcg_and_solution(name, spec, make, mode, leaf, root, big, mon
     g = b.pcg()
     o = pcg(itf.apply, prec.apply, itf.rhs())
     assert abs(g["iterations"] - o.iterations) <= 1
-    kg, ko = kappa_common(g["alphas"], g["betas"], o.alphas, o.betas)
-    assert abs(kg - ko) <= KAPPA_RTOL * ko
+    check_kappa(g, o, itf.apply, prec.apply, itf.rhs())
     u_g = b.recover(g["x"])
     u_o = itf.recover(o.x)
     assert energy_error(p.systems, p.dmap.free_count, u_g, u_o) <= 1e-8
@@ -164,8 +189,15 @@ def test_adaptive_selection_and_spectrum(name, spec, make, mode, tau, maxv, base
         assert abs(row.omega_tilde - ref.omega_tilde) <= 1e-6 * ref.omega_tilde
     assert abs(row.iterations - ref.iterations) <= 1
     g = b.pcg()
-    kg, ko = kappa_common(g["alphas"], g["betas"], ref.pcg.alphas, ref.pcg.betas)
-    assert abs(kg - ko) <= KAPPA_RTOL * ko
+    assert g["iterations"] == row.iterations
+    # the oracle's operators on its selected constraint set (solve_item's)
+    h = HarmonicExtension(p.systems, p.maps)
+    itf = InterfaceProblem(p.systems, p.maps, h)
+    prec = BddcPreconditioner(p.systems, p.maps, AveragingOperator(p.systems, p.maps),
+                              change_of_variables(ref.constraints, p.globset, p.dmap, p.maps))
+    check_kappa(g, ref.pcg, itf.apply, prec.apply, itf.rhs())
+    # solution within 1e-8 relative in the energy norm (north_star)
+    assert energy_error(p.systems, p.dmap.free_count, b.recover(g["x"]), itf.recover(ref.pcg.x)) <= 1e-8
 
 
 @pytest.mark.parametrize("config", [3, 4, 5])
@@ -267,8 +299,7 @@ def test_primal_tree(name, spec, make, mode, depth, leaf, tree, monkeypatch):
     g = b.pcg()
     o = pcg(itf.apply, prec.apply, itf.rhs())
     assert abs(g["iterations"] - o.iterations) <= 1
-    kg, ko = kappa_common(g["alphas"], g["betas"], o.alphas, o.betas)
-    assert abs(kg - ko) <= KAPPA_RTOL * ko
+    check_kappa(g, o, itf.apply, prec.apply, itf.rhs())
     assert energy_error(p.systems, p.dmap.free_count, b.recover(g["x"]), itf.recover(o.x)) <= 1e-8
 
 
@@ -283,8 +314,11 @@ def test_primal_tree_adaptive(monkeypatch):
     assert row.constraint_rows == ref.constraint_rows
     assert abs(row.iterations - ref.iterations) <= 1
     g = b.pcg()
-    kg, ko = kappa_common(g["alphas"], g["betas"], ref.pcg.alphas, ref.pcg.betas)
-    assert abs(kg - ko) <= KAPPA_RTOL * ko
+    h = HarmonicExtension(p.systems, p.maps)
+    itf = InterfaceProblem(p.systems, p.maps, h)
+    prec = BddcPreconditioner(p.systems, p.maps, AveragingOperator(p.systems, p.maps),
+                              change_of_variables(ref.constraints, p.globset, p.dmap, p.maps))
+    check_kappa(g, ref.pcg, itf.apply, prec.apply, itf.rhs())
 
 
 @pytest.mark.parametrize("chol", ["dag", "tiled"])

@@ -176,9 +176,11 @@ def test_lanczos_recovers_exact_condition(pins):
 
 
 def test_lanczos_roundoff_floor():
-    """Why kappa parity uses 1e-4 (tests/test_gpu_parity.py): perturbing the
-    oracle's own preconditioner by 1e-13 relative already moves its final Lanczos
-    estimate by more than 1e-6, and by less than 1e-4."""
+    """The roundoff floor of the Lanczos estimate (tests/test_gpu_parity.py
+    check_kappa falls back to it only when the iteration counts differ):
+    perturbing the oracle's own preconditioner by 1e-13 relative already moves
+    its final estimate by more than 1e-6 on this planar case, and by less than
+    1e-3."""
     p = build_pipeline(cube_spec((2, 2, 1), 8, fem.SCALAR))
     h = HarmonicExtension(p.systems, p.maps)
     itf = InterfaceProblem(p.systems, p.maps, h)
