@@ -176,15 +176,18 @@ class PairSolve:
     eig: EigenReport
 
 
-def solve_pair(cs, gs, dmap, systems, maps, si, sj, request) -> PairSolve:
-    """`adaptive.cpp:30-47`."""
+def solve_pair(cs, gs, dmap, systems, maps, si, sj, request, inclusion_rel_tol=1e-6) -> PairSolve:
+    """`adaptive.cpp:30-47`.  `inclusion_rel_tol` is the reference's 1e-6
+    (dense_eig.cpp:77-126); `inf` disables its nullspace-inclusion throw (NOT the
+    reference -- used only to record what the reference would select on the
+    pairs where it throws, tests/golden/make_fullsize.py)."""
     space = build_pair(systems, maps, gs, dmap, si, sj)
     z = pair_admissible_basis(space, cs, gs, dmap)
     jump = z - space.average_copies(z)
     s_jump = space.schur @ jump
     lhs = jump.T @ s_jump
     rhs = z.T @ (space.schur @ z)
-    eig = generalized_eig_sym(lhs, rhs, min(request, z.shape[1]))
+    eig = generalized_eig_sym(lhs, rhs, min(request, z.shape[1]), inclusion_rel_tol=inclusion_rel_tol)
     return PairSolve(space, z, eig)
 
 
