@@ -16,12 +16,14 @@ inside the timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
 
-N > 1 (torchrun, one process per GPU) runs the sharded engine: one problem
-whose substructure lattice grows with N along x (the config's lattice per GPU,
-same per-element coefficient rule), substructures and face pairs partitioned
-over the ranks (paper_0910_5863_b200/shard.py), NCCL for the interface
-exchange, the dot products and the root ("weak" scaling: per-GPU work
-fixed).  `--replicas` runs N independent copies of the N=1 workload instead.
+N > 1 (torchrun, one process per GPU) runs the sharded engine on the SAME
+problem ("strong" scaling, the way BASELINE.json shards cfg5 over 8 GPUs):
+substructures and face pairs partitioned over the ranks by a 3D block
+partition (paper_0910_5863_b200/shard.py), NCCL send/recv for the interface
+halo and the ghost Schur complements, an all-reduce of the dot-product
+partials and of the root.  `--weak` grows the lattice with N along x instead
+(the config's lattice per GPU, same coefficient rule); `--replicas` runs N
+independent copies of the N=1 workload.
 
 CPU legs (oracle/, the reference restated in numpy/scipy; the C++ reference
 needs Eigen and cannot be built here): `cpu_baseline` times
@@ -211,13 +213,14 @@ def free_dofs_of(lattice, epe, comps):
     return (nx - 1) * ny * nz * comps
 
 
-def workload_config(cfg_id, seed, world=1, sharded=False, replicas=False):
+def workload_config(cfg_id, seed, world=1, sharded=False, replicas=False, weak=False):
     """The `config` object of both arms (identical dicts for the same run)."""
     lat, epe, comps = CONFIG_GEOMETRY[cfg_id]
-    if sharded:
+    if sharded and weak:
         lat = (lat[0] * world, lat[1], lat[2])
     return {"workload": CONFIG_NAMES[cfg_id] + (
-                " per GPU; lattice %dx%dx%d over %d GPUs" % (lat + (world,)) if sharded else ""),
+                " per GPU; lattice %dx%dx%d over %d GPUs" % (lat + (world,)) if sharded and weak else
+                "; sharded over %d GPUs" % world if sharded else ""),
             "config": cfg_id, "seed": seed, "lattice": list(lat), "elements_per_substructure_edge": epe,
             "free_dofs": free_dofs_of(lat, epe, comps),
             "parallelism": ("sharded%d (NCCL: interface exchange, dot products, root)" % world if sharded
@@ -277,8 +280,10 @@ def reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded coefficient field)",
-        "config": workload_config(cfg_id, args.seed, world, world > 1 and not args.replicas, args.replicas),
+        "scaling": "strong" if world > 1 and not (args.weak or args.replicas) else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded coefficient field)",
+        "config": workload_config(cfg_id, args.seed, world, world > 1 and not args.replicas, args.replicas,
+                                  args.weak),
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
                          "sample": sample_text(cfg_id, cores), "sample_free_dofs": free},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -301,6 +306,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--apply-reps", type=int, default=10, help="operator applications timed for the rooflines")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent copies instead of sharding")
+    ap.add_argument("--weak", action="store_true", help="N > 1: lattice grows with N (weak scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -318,8 +324,8 @@ def main():
     t_in = time.perf_counter()
     if sharded:
         base = pb.BDDC(config=args.config, seed=args.seed).lattice()
-        lattice = (base[0] * world, base[1], base[2])
-        b = pb.BDDC(config=args.config, seed=args.seed, subdomains=lattice)
+        lattice = (base[0] * world, base[1], base[2]) if args.weak else base
+        b = pb.BDDC(config=args.config, seed=args.seed, subdomains=lattice if args.weak else None)
         nid = [pb.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(nid, src=0)
         b.shard(rank, world, backend="nccl", nccl_id=nid[0])
@@ -431,8 +437,9 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "settle_steps": settle, "ms_per_step": sec_per_step * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded coefficient field)",
-        "config": workload_config(args.config, args.seed, world, sharded, args.replicas and world > 1),
+        "scaling": "strong" if sharded and not args.weak else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded coefficient field)",
+        "config": workload_config(args.config, args.seed, world, sharded, args.replicas and world > 1, args.weak),
         "l2": "flushed (256 MiB write) before every step",
         "structure": {"free_dofs": free, "subdomains": st["subdomains"], "interface_dofs": st["interface_dofs"]},
         "setup_s": statistics.median(s["setup_seconds"] for s in steps),

@@ -111,6 +111,13 @@ int bddc_b200_set_device(int device);
 int bddc_b200_nccl_unique_id(unsigned char* id128);
 int bddc_b200_shard_nccl(bddc_b200_t* h, const unsigned char* id128, int rank, int world, const int* owner);
 int bddc_b200_shard_loopback(bddc_b200_t* h, int group, int rank, int world, const int* owner);
+/* Interface halo plan of `rank` for the partition `owner` (host only; the
+ * sharded engine's exchange): peers (ascending), per peer the shared interface
+ * dofs (ascending, concatenated; peer_off has n_peers + 1 entries), and per
+ * interface dof whether this rank touches / owns it.  Query the counts with
+ * peers == NULL. */
+int bddc_b200_halo_plan(const bddc_b200_t* h, const int* owner, int rank, int world, int64_t* n_peers,
+                        int64_t* n_shared, int* peers, int* peer_off, int* shared, int* touched, int* owned);
 /* Substructure lattice (nx, ny, nz), substructure ids x-fastest (mesh.cpp:68-70). */
 int bddc_b200_subdomain_lattice(const bddc_b200_t* h, int64_t* dims3);
 

@@ -105,6 +105,9 @@ EXPORTS = {
     "bddc_b200_shard_nccl": (C.c_int, [P, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "bddc_b200_shard_loopback": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "bddc_b200_subdomain_lattice": (C.c_int, [P, I64]),
+    "bddc_b200_halo_plan": (C.c_int, [P, C.POINTER(C.c_int), C.c_int, C.c_int, I64, I64, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int)]),
     "bddc_b200_glob_count": (C.c_int, [P, I64]),
     "bddc_b200_glob_info": (C.c_int, [P, C.c_int, C.POINTER(C.c_int), I64, I64]),
     "bddc_b200_glob_nodes": (C.c_int, [P, C.c_int, I64, I64]),
@@ -348,6 +351,26 @@ class BDDC:
             raise ValueError("backend must be 'nccl' or 'loopback'")
 
     # --- structure and index maps (host) -----------------------------------
+    def halo_plan(self, owner, rank: int, world: int) -> dict:
+        """The sharded engine's interface halo of `rank` (host only): peers,
+        per-peer shared interface dofs, touched and owned masks."""
+        own = np.ascontiguousarray(owner, dtype=np.int32)
+        ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+        npeer, nsh = C.c_int64(), C.c_int64()
+        _check(self._lib.bddc_b200_halo_plan(self._h, ip(own), rank, world, C.byref(npeer), C.byref(nsh),
+                                             None, None, None, None, None))
+        n = self.structure()["interface_dofs"]
+        peers = np.empty(max(npeer.value, 1), dtype=np.int32)
+        off = np.empty(npeer.value + 1, dtype=np.int32)
+        sh = np.empty(max(nsh.value, 1), dtype=np.int32)
+        touched = np.empty(n, dtype=np.int32)
+        owned = np.empty(n, dtype=np.int32)
+        _check(self._lib.bddc_b200_halo_plan(self._h, ip(own), rank, world, C.byref(npeer), C.byref(nsh), ip(peers),
+                                             ip(off), ip(sh), ip(touched), ip(owned)))
+        peers = peers[:npeer.value]
+        return {"peers": peers.tolist(), "touched": touched.astype(bool), "owned": owned.astype(bool),
+                "shared": {int(p): sh[off[k]:off[k + 1]].copy() for k, p in enumerate(peers)}}
+
     def structure(self) -> dict:
         s = _Structure()
         _check(self._lib.bddc_b200_structure_get(self._h, C.byref(s)))

@@ -395,6 +395,24 @@ int bddc_b200_glob_transform(bddc_b200_t* h, int glob, int* rank, int64_t* n, do
   });
 }
 
+int bddc_b200_halo_plan(const bddc_b200_t* h, const int* owner, int rank, int world, int64_t* n_peers,
+                        int64_t* n_shared, int* peers, int* peer_off, int* shared, int* touched, int* owned) {
+  return guarded([&] {
+    const std::vector<int> own(owner, owner + h->model.subs.size());
+    const HaloPlan p = halo_plan(h->model, own, rank, world);
+    *n_peers = static_cast<int64_t>(p.peers.size());
+    *n_shared = static_cast<int64_t>(p.shared.size());
+    if (!peers) return;
+    std::copy(p.peers.begin(), p.peers.end(), peers);
+    std::copy(p.peer_off.begin(), p.peer_off.end(), peer_off);
+    std::copy(p.shared.begin(), p.shared.end(), shared);
+    for (std::size_t i = 0; i < p.touched.size(); ++i) {
+      touched[i] = p.touched[i];
+      owned[i] = p.owned[i];
+    }
+  });
+}
+
 int bddc_b200_export_matrix_market(bddc_b200_t* h, const char* stem) {
   return guarded([&] {
     const ChangeOfVariables cov = change_of_variables(h->cs, h->model);

@@ -88,6 +88,38 @@ class LoopbackComm : public Comm {
   std::vector<std::vector<char>> allgather(const std::vector<char>& mine) override {
     return g_->exchange(rank_, mine);
   }
+  void exchange(const std::vector<Segment>& sends, const std::vector<Segment>& recvs, cudaStream_t st) override {
+    // one blob per rank: [peer, n, n doubles]... ; every rank reads the
+    // messages addressed to it from each peer's blob, in order
+    std::vector<char> mine;
+    for (const Segment& sg : sends) {
+      const long long hdr[2] = {sg.peer, static_cast<long long>(sg.n)};
+      const std::size_t at = mine.size();
+      mine.resize(at + sizeof(hdr) + sg.n * sizeof(double));
+      std::memcpy(mine.data() + at, hdr, sizeof(hdr));
+      if (sg.n)
+        CK(cudaMemcpyAsync(mine.data() + at + sizeof(hdr), sg.ptr, sg.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    const auto all = g_->exchange(rank_, mine);
+    std::vector<std::size_t> cursor(all.size(), 0);
+    for (const Segment& rv : recvs) {
+      const auto& b = all.at(rv.peer);
+      std::size_t& c = cursor[rv.peer];
+      for (;;) {  // next message of that peer addressed to this rank
+        if (c >= b.size()) throw Error(kError, "loopback exchange: missing message");
+        long long hdr[2];
+        std::memcpy(hdr, b.data() + c, sizeof(hdr));
+        const std::size_t body = c + sizeof(hdr);
+        c = body + static_cast<std::size_t>(hdr[1]) * sizeof(double);
+        if (hdr[0] != rank_) continue;
+        if (static_cast<std::size_t>(hdr[1]) != rv.n) throw Error(kError, "loopback exchange: size mismatch");
+        if (rv.n) CK(cudaMemcpyAsync(rv.ptr, b.data() + body, rv.n * sizeof(double), cudaMemcpyHostToDevice, st));
+        break;
+      }
+    }
+    CK(cudaStreamSynchronize(st));
+  }
 
  private:
   std::shared_ptr<LoopGroup> g_;
@@ -118,6 +150,10 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
       nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -141,6 +177,10 @@ const NcclApi& nccl() {
   api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
   api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
   api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+  api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+  api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+  api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
   loaded = true;
   return api;
 }
@@ -165,6 +205,15 @@ class NcclComm : public Comm {
   int world() const override { return world_; }
   void allreduce(double* d, std::size_t n, cudaStream_t st) override {
     if (world_ > 1 && n) nck(nccl().AllReduce(d, d, n, ncclDouble, ncclSum, comm_, st), "AllReduce");
+  }
+  void exchange(const std::vector<Segment>& sends, const std::vector<Segment>& recvs, cudaStream_t st) override {
+    if (sends.empty() && recvs.empty()) return;
+    nck(nccl().GroupStart(), "GroupStart");
+    for (const Segment& sg : sends)
+      if (sg.n) nck(nccl().Send(sg.ptr, sg.n, ncclDouble, sg.peer, comm_, st), "Send");
+    for (const Segment& rv : recvs)
+      if (rv.n) nck(nccl().Recv(rv.ptr, rv.n, ncclDouble, rv.peer, comm_, st), "Recv");
+    nck(nccl().GroupEnd(), "GroupEnd");
   }
   std::vector<std::vector<char>> allgather(const std::vector<char>& mine) override {
     // sizes first, then the blobs padded to the largest

@@ -7,7 +7,10 @@
 //   allreduce  in-place sum of a device array (interface vectors after the
 //              per-shard copy sums, the root right-hand side, the root front);
 //   allgather  host byte blobs in rank order (selected face constraints and
-//              pair reports, so every rank applies the same rank filter).
+//              pair reports, so every rank applies the same rank filter);
+//   exchange   point-to-point device messages with the neighbour ranks (the
+//              interface halo of every operator apply, the Schur complements
+//              of the ghost substructures a rank's face pairs need).
 // Backends: NCCL (libnccl loaded at run time, one communicator per handle) and
 // a loopback group of host threads in one process (tests: ranks exchange only
 // through the host after synchronizing their own streams, so no kernel ever
@@ -22,6 +25,14 @@
 
 namespace b200 {
 
+/// One message of a neighbour exchange: n doubles at device address ptr,
+/// to (send) or from (recv) rank `peer`.
+struct Segment {
+  int peer;
+  double* ptr;
+  std::size_t n;
+};
+
 class Comm {
  public:
   virtual ~Comm() = default;
@@ -29,6 +40,10 @@ class Comm {
   virtual int world() const = 0;
   /// In-place sum over ranks of n doubles on the device, ordered on `st`.
   virtual void allreduce(double* d, std::size_t n, cudaStream_t st) = 0;
+  /// Point-to-point neighbour exchange (NCCL send/recv in one group): the
+  /// k-th send to a peer matches that peer's k-th receive from this rank.
+  /// Ordered on `st`.
+  virtual void exchange(const std::vector<Segment>& sends, const std::vector<Segment>& recvs, cudaStream_t st) = 0;
   /// Blobs of every rank, in rank order (host memory; synchronizing).
   virtual std::vector<std::vector<char>> allgather(const std::vector<char>& mine) = 0;
   /// Max of a host double over ranks (synchronizing).

@@ -305,9 +305,34 @@ __global__ void __launch_bounds__(256) k_sum_copies(i64 n, const int* __restrict
   if (partials) block_partial(acc, partials);
 }
 
-__global__ void k_dot(i64 n, const double* a, const double* b, double* partials) {
+// --- interface halo of the sharded engine ---------------------
+__global__ void k_halo_pack(int n, const int* __restrict__ idx, const double* __restrict__ y, double* buf) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) buf[k] = y[idx[k]];
+}
+
+// y[dof[q]] = sum of the contributions of every rank holding dof[q], in
+// ascending rank order (src < 0: this rank's own partial sum): the same value
+// on every rank, deterministic.
+__global__ void k_halo_sum(int n, const int* __restrict__ dof, const int* __restrict__ ptr, const int* __restrict__ src,
+                           const double* __restrict__ recv, double* y) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int i = dof[q];
+    double s = 0.0;
+    for (int t = ptr[q]; t < ptr[q + 1]; ++t) s += src[t] < 0 ? y[i] : recv[src[t]];
+    y[i] = s;
+  }
+}
+
+// y[i] = 0 unless this rank owns interface dof i (before a completing sum)
+__global__ void k_keep_owned(i64 n, const double* __restrict__ owned, double* y) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    if (owned[i] == 0.0) y[i] = 0.0;
+}
+
+__global__ void k_dot(i64 n, const double* a, const double* b, double* partials, const double* mask = nullptr) {
   double acc = 0.0;
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) acc += a[i] * b[i];
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    if (!mask || mask[i] != 0.0) acc += a[i] * b[i];
   block_partial(acc, partials);
 }
 
@@ -1262,6 +1287,19 @@ struct DeviceState {
   std::vector<int> act, own;    // active (owned + ghosts) and owned substructures, ascending
   std::vector<char> is_act, is_own;
   int n_act = 0, n_own = 0;
+  // interface halo: this rank's partial interface sums are completed by
+  // neighbour send/recv of the dofs it shares (ascending interface index per
+  // peer); dot products run over the dofs it owns (lowest rank holding a copy)
+  // and all-reduce kRed partials
+  struct Halo {
+    std::vector<int> peers, peer_off;   // peer_off: offsets into send/recv buffers
+    std::vector<int> shared;            // interface indices, concatenated per peer
+    std::vector<char> touched, owned_h;
+    DBuf<int> pack, dof, ptr, src;
+    DBuf<double> sendbuf, recvbuf, owned;
+    int nsum = 0;
+  } halo;
+  std::vector<Segment> ghost_send, ghost_recv;  // S of ghost substructures (analysis)
   cudaStream_t st = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr, ef0 = nullptr, ef1 = nullptr, s0 = nullptr, s1 = nullptr, s2 = nullptr;
   DBuf<double> ufree;
@@ -1442,6 +1480,91 @@ double elapsed(cudaEvent_t a, cudaEvent_t b) {
 // analysis: A_s -> dense fronts -> partial Cholesky (eliminate the interior),
 // interface Schur complements, condensed rhs (spaces.cpp:108-147, schur.cpp:38-55).
 // ---------------------------------------------------------------------------
+namespace {
+// Halo plan and ghost Schur-complement messages of a sharded engine
+// (paper_0910_5863_b200/shard.py HaloPlan is the same plan in Python, the
+// checker of this one: tests/test_multirank.py).
+void build_halo(DeviceState& D, const Model& m) {
+  auto& H = D.halo;
+  const i64 n = D.niface;
+  const HaloPlan plan = halo_plan(m, D.owner, D.comm->rank(), D.comm->world());
+  H.peers = plan.peers;
+  H.peer_off = plan.peer_off;
+  H.shared = plan.shared;
+  H.touched = plan.touched;
+  H.owned_h = plan.owned;
+  const std::vector<int>& dofs = plan.sum_dof;
+  const std::vector<int>& ptr = plan.sum_ptr;
+  const std::vector<int>& src = plan.sum_src;
+  H.nsum = static_cast<int>(dofs.size());
+  cudaStream_t st = D.st;
+  auto up = [&](DBuf<int>& b, const std::vector<int>& v) {
+    if (v.empty()) b.alloc(1); else b.upload(v, st);
+  };
+  up(H.pack, H.shared);
+  up(H.dof, dofs);
+  up(H.ptr, ptr);
+  up(H.src, src);
+  H.sendbuf.alloc(std::max<std::size_t>(H.shared.size(), 1));
+  H.recvbuf.alloc(std::max<std::size_t>(H.shared.size(), 1));
+  std::vector<double> ow(std::max<i64>(n, 1), 0.0);
+  for (i64 i = 0; i < n; ++i) ow[i] = H.owned_h[i] ? 1.0 : 0.0;
+  H.owned.upload(ow, st);
+  // ghosts: the owner of each face pair's neighbour sends its S (copy_trailing_full
+  // layout, PB^2 doubles) instead of this rank re-factoring the neighbour
+  D.ghost_send.clear();
+  D.ghost_recv.clear();
+  std::vector<std::vector<int>> needs(D.nsub);  // ranks needing substructure s as a ghost
+  for (const auto& pr : face_pairs(m)) {
+    const int r = D.owner[std::min(pr.first, pr.second)];
+    for (int s : {pr.first, pr.second})
+      if (D.owner[s] != r) needs[s].push_back(r);
+  }
+  for (int s = 0; s < D.nsub; ++s) {
+    std::sort(needs[s].begin(), needs[s].end());
+    needs[s].erase(std::unique(needs[s].begin(), needs[s].end()), needs[s].end());
+  }
+  for (int s = 0; s < D.nsub; ++s) {  // ascending s on both sides: the k-th messages match
+    const std::size_t nb = (std::size_t)D.PB[s] * D.PB[s];
+    if (D.is_own[s])
+      for (int r : needs[s]) D.ghost_send.push_back(Segment{r, D.S.p + D.s_off[s], nb});
+    if (D.is_act[s] && !D.is_own[s]) D.ghost_recv.push_back(Segment{D.owner[s], D.S.p + D.s_off[s], nb});
+  }
+}
+
+// Complete this rank's partial sums of an interface vector on every dof it
+// touches (identical values on every rank holding the dof).
+void halo_exchange(DeviceState& D, double* y) {
+  auto& H = D.halo;
+  cudaStream_t st = D.st;
+  const int ns = static_cast<int>(H.shared.size());
+  if (ns) {
+    k_halo_pack<<<std::max(1, std::min(1024, (ns + 255) / 256)), 256, 0, st>>>(ns, H.pack.p, y, H.sendbuf.p);
+    count_launch(1);
+  }
+  std::vector<Segment> sends, recvs;
+  for (std::size_t k = 0; k < H.peers.size(); ++k) {
+    const std::size_t off = H.peer_off[k], cnt = H.peer_off[k + 1] - H.peer_off[k];
+    sends.push_back(Segment{H.peers[k], H.sendbuf.p + off, cnt});
+    recvs.push_back(Segment{H.peers[k], H.recvbuf.p + off, cnt});
+  }
+  D.comm->exchange(sends, recvs, st);
+  if (H.nsum) {
+    k_halo_sum<<<std::max(1, std::min(1024, (H.nsum + 255) / 256)), 256, 0, st>>>(H.nsum, H.dof.p, H.ptr.p, H.src.p,
+                                                                                 H.recvbuf.p, y);
+    count_launch(1);
+  }
+}
+
+// The complete vector on every rank (host-facing results): owned values, summed.
+void complete_interface(DeviceState& D, double* y) {
+  if (!D.comm) return;
+  k_keep_owned<<<kRed, 256, 0, D.st>>>(D.niface, D.halo.owned.p, y);
+  count_launch(1);
+  D.comm->allreduce(y, D.niface, D.st);
+}
+}  // namespace
+
 void Engine::prepare() {
   DeviceState& D = *d_;
   if (D.prepared) return;
@@ -1484,10 +1607,13 @@ void Engine::prepare() {
     const Subdomain& S = m.subs[s];
     D.nI[s] = static_cast<int>(S.interior.size());
     D.nB[s] = static_cast<int>(S.boundary.size());
-    const bool a = D.is_act[s];  // no storage for substructures this rank never touches
-    D.PI[s] = a ? rup(D.nI[s], kTile) : 0;
+    // leaf fronts for the owned substructures; the ghosts (neighbours this
+    // rank's face pairs need) hold only their Schur complement S, received from
+    // the owner after its factorization (exchange_ghost_schur)
+    const bool a = D.is_act[s], o = D.is_own[s];
+    D.PI[s] = o ? rup(D.nI[s], kTile) : 0;
     D.PB[s] = a ? rup(std::max(D.nB[s], 1), kTile) : 0;
-    D.NM[s] = D.PI[s] + D.PB[s];
+    D.NM[s] = o ? D.PI[s] + D.PB[s] : 0;
     D.m_off[s] = mo;
     mo += (long long)D.NM[s] * D.NM[s];
     D.dm_off[s] = dmo;
@@ -1520,7 +1646,7 @@ void Engine::prepare() {
   auto& H = D.h;
   H.lnode.clear();
   H.pos.clear();
-  for (int s : D.act) {
+  for (int s : D.own) {
     const Subdomain& S = m.subs[s];
     lnode_off[s] = H.lnode.size();
     pos_off[s] = H.pos.size();
@@ -1537,7 +1663,7 @@ void Engine::prepare() {
   H.eke = m.element_ke;
   H.escale = m.mesh.element_scale;
   H.mv.assign(std::max<long long>(mvo, 1), 0.0);
-  for (int s : D.act) {
+  for (int s : D.own) {
     const Subdomain& S = m.subs[s];
     for (int r = 0; r < D.nI[s]; ++r) H.mv[D.mv_off[s] + r] = S.load[S.interior[r]];
     for (int b = 0; b < D.nB[s]; ++b) H.mv[D.mv_off[s] + D.PI[s] + b] = S.load[S.boundary[b]];
@@ -1579,16 +1705,16 @@ void Engine::prepare() {
   D.bw.alloc(std::max<long long>(wbo, 1));
   D.icopy_ptr.alloc(H.icp.size());
   D.icopy_pos.alloc(std::max<std::size_t>(H.icpos.size(), 1));
-  D.minfo.alloc(std::max(D.n_act, 1));
+  D.minfo.alloc(std::max(D.n_own, 1));
   D.rhs.alloc(std::max<i64>(D.niface, 1));
-  // descriptors: leaf fronts over the active substructures, interface
-  // operators over the owned ones (compacted, in ascending order)
+  // descriptors: leaf fronts and interface operators over the owned
+  // substructures (compacted, in ascending order)
   std::vector<AsmDesc> ad;
   std::vector<FrontDesc> fd;
   std::vector<SolveDesc> sv;
   std::vector<TrailDesc> td;
-  for (int q = 0; q < D.n_act; ++q) {
-    const int s = D.act[q];
+  for (int q = 0; q < D.n_own; ++q) {
+    const int s = D.own[q];
     const Subdomain& S = m.subs[s];
     ad.push_back(AsmDesc{D.M.p + D.m_off[s], D.asm_lnode.p + lnode_off[s], D.asm_pos.p + pos_off[s], D.NM[s], D.nI[s],
                          D.PI[s], D.nB[s], S.origin[0], S.origin[1], S.origin[2], D.asm_ipos.p + ipos_off[s],
@@ -1624,7 +1750,10 @@ void Engine::prepare() {
     if (lost) invalidate_preconditioner();
     return base;
   });
-  if (D.comm) D.pairs.set_shard(D.comm, D.owner);
+  if (D.comm) {
+    D.pairs.set_shard(D.comm, D.owner);
+    build_halo(D, m);
+  }
   D.prepared = true;
   upload_inputs();
   CK(cudaStreamSynchronize(st));
@@ -1656,13 +1785,13 @@ namespace {
 // Leaf fronts from the reference element matrices: the
 // inverse layout maps, then every block-lower entry of every front.
 void assemble_fronts(DeviceState& D) {
-  const int na = D.n_act;
+  const int na = D.n_own;
   if (!na) return;
   cudaStream_t st = D.st;
   CK(cudaMemsetAsync(D.asm_ipos.p, 0xff, D.asm_ipos.n * sizeof(int), st));
   k_front_maps<<<dim3(16, na), 256, 0, st>>>(D.asmdesc.p);
   long tiles = 0;
-  for (int s : D.act) tiles = std::max<long>(tiles, (long)(D.NM[s] / 64) * (D.NM[s] / 64 + 1) / 2);
+  for (int s : D.own) tiles = std::max<long>(tiles, (long)(D.NM[s] / 64) * (D.NM[s] / 64 + 1) / 2);
   const int bx = static_cast<int>(std::max<long>(1, std::min<long>(tiles, (16L * sm_count() + na - 1) / na)));
   k_assemble_dense<<<dim3(bx, na), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
   count_launch(2);
@@ -1677,7 +1806,7 @@ void Engine::analysis() {
 void Engine::analysis_launch() {
   prepare();
   DeviceState& D = *d_;
-  const int na = D.n_act;
+  const int na = D.n_own;
   cudaStream_t st = D.st;
   CK(cudaEventRecord(D.e0, st));
   D.minfo.zero(st);
@@ -1689,6 +1818,7 @@ void Engine::analysis_launch() {
   CK(cudaGetLastError());
   copy_trailing_full(D.mtrail.p, na, D.max_PB, st);
   CK(cudaGetLastError());
+  if (D.comm) D.comm->exchange(D.ghost_send, D.ghost_recv, st);  // S of the ghost substructures
   // condensed rhs: forward sweep on [f_I; f_B], then sum the boundary rows over copies
   CK(cudaMemcpyAsync(D.MV.p, D.MV0.p, D.MV.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   front_forward(D.msolve.p, na, D.max_NM, st);
@@ -1699,7 +1829,7 @@ void Engine::analysis_launch() {
   k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, D.rhs.p, nullptr, nullptr, nullptr);
   count_launch(1);
   CK(cudaGetLastError());
-  if (D.comm) D.comm->allreduce(D.rhs.p, D.niface, st);  // interface neighbour exchange
+  if (D.comm) halo_exchange(D, D.rhs.p);  // interface neighbour exchange
   CK(cudaEventRecord(D.e1, st));
 }
 
@@ -1708,13 +1838,13 @@ void Engine::analysis_finish() {
   DeviceState& D = *d_;
   times_.analysis = elapsed(D.e0, D.e1);
   times_.leaf_factor = elapsed(D.ef0, D.ef1);
-  std::vector<int> info(std::max(D.n_act, 1));
+  std::vector<int> info(std::max(D.n_own, 1));
   CK(cudaMemcpy(info.data(), D.minfo.p, info.size() * sizeof(int), cudaMemcpyDeviceToHost));
-  for (int q = 0; q < D.n_act; ++q)
-    if (info[q]) throw Error(kNotPositiveDefinite, "factorize: A_II of substructure " + std::to_string(D.act[q]) +
+  for (int q = 0; q < D.n_own; ++q)
+    if (info[q]) throw Error(kNotPositiveDefinite, "factorize: A_II of substructure " + std::to_string(D.own[q]) +
                                                        " is not positive definite");
   double fl = 0;
-  for (int s : D.act) {
+  for (int s : D.own) {
     const double ni = D.nI[s], nb = D.nB[s];
     fl += ni * ni * ni / 3.0 + ni * ni * nb + ni * nb * nb;
   }
@@ -2421,15 +2551,16 @@ void Engine::set_constraints(const ConstraintSet& cs) {
 // ---------------------------------------------------------------------------
 namespace {
 // Sharded: this rank's copies are summed, then the interface neighbour
-// exchange (allreduce of the interface vector) completes every dof, and the
-// dot product is taken on the complete vector.
+// exchange (halo send/recv) completes every dof this rank touches, and the dot
+// product is taken over the dofs it owns (partials all-reduced).
 void finish_interface(DeviceState& D, double* y, const double* dot_with, double* partials, const int* done) {
   cudaStream_t st = D.st;
   if (!D.comm) return;
-  D.comm->allreduce(y, D.niface, st);
-  if (partials) {
-    k_dot<<<kRed, 256, 0, st>>>(D.niface, dot_with, y, partials);
+  halo_exchange(D, y);
+  if (partials) {  // owned dofs only, then the kRed partials summed over the ranks
+    k_dot<<<kRed, 256, 0, st>>>(D.niface, dot_with, y, partials, D.halo.owned.p);
     count_launch(1);
+    D.comm->allreduce(partials, kRed, st);
   }
   (void)done;
 }
@@ -2562,9 +2693,9 @@ void Engine::leaf_front(int s, std::vector<double>* out, std::vector<int>* pos, 
   DeviceState& D = *d_;
   *ld = D.NM[s];
   const Subdomain& S = m_.subs[s];
-  if (!D.is_act[s]) throw Error(kError, "substructure not held by this shard");
+  if (!D.is_own[s]) throw Error(kError, "substructure not owned by this shard");
   std::size_t off = 0;
-  for (int q : D.act) {
+  for (int q : D.own) {
     if (q == s) break;
     off += m_.subs[q].dim();
   }
@@ -2586,6 +2717,7 @@ void Engine::schur_apply(const double* x, double* y) {
   const std::size_t bytes = D.niface * sizeof(double);
   CK(cudaMemcpyAsync(D.vp.p, x, bytes, cudaMemcpyHostToDevice, D.st));
   launch_schur(D, D.vp.p, D.vq.p, nullptr, nullptr, nullptr);
+  complete_interface(D, D.vq.p);
   CK(cudaMemcpyAsync(y, D.vq.p, bytes, cudaMemcpyDeviceToHost, D.st));
   CK(cudaStreamSynchronize(D.st));
   CK(cudaGetLastError());
@@ -2598,6 +2730,7 @@ void Engine::precond_apply(const double* r, double* z) {
   const std::size_t bytes = D.niface * sizeof(double);
   CK(cudaMemcpyAsync(D.vr.p, r, bytes, cudaMemcpyHostToDevice, D.st));
   launch_precond(D, D.vr.p, D.vz.p, nullptr, nullptr, nullptr);
+  complete_interface(D, D.vz.p);
   CK(cudaMemcpyAsync(z, D.vz.p, bytes, cudaMemcpyDeviceToHost, D.st));
   CK(cudaStreamSynchronize(D.st));
   CK(cudaGetLastError());
@@ -2656,6 +2789,7 @@ Engine::OpTimes Engine::time_operators(int reps) {
 
 void Engine::rhs(double* out) {
   DeviceState& D = *d_;
+  complete_interface(D, D.rhs.p);  // sharded: every dof (still valid for pcg)
   CK(cudaMemcpyAsync(out, D.rhs.p, D.niface * sizeof(double), cudaMemcpyDeviceToHost, D.st));
   CK(cudaStreamSynchronize(D.st));
 }
@@ -2681,9 +2815,9 @@ void Engine::recover_device(const double* d_uiface, double* d_ufree) {
   }
   if (D.comm) CK(cudaMemsetAsync(d_ufree, 0, m.free_count * sizeof(double), st));
   CK(cudaMemcpyAsync(D.MV.p, D.MV0.p, D.MV.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  front_forward(D.msolve.p, D.n_act, D.max_NM, st);
+  front_forward(D.msolve.p, D.n_own, D.max_NM, st);
   if (D.n_own) k_insert_boundary<<<D.n_own, 256, 0, st>>>(D.subdesc.p, D.MV.p, D.d_mvoff.p, D.d_PI.p, d_uiface);
-  front_backward(D.msolve.p, D.n_act, D.max_NM, st);
+  front_backward(D.msolve.p, D.n_own, D.max_NM, st);
   k_scatter_solution<<<256, 256, 0, st>>>(static_cast<long long>(D.MV.n), D.sol_gdof.p, D.MV.p,
                                           iface_here ? D.niface : 0, D.iface_gdof.p, d_uiface, d_ufree);
   count_launch(2);
@@ -2758,8 +2892,9 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
     }
   }
   CK(cudaMemcpyAsync(D.vp.p, D.vz.p, bytes, cudaMemcpyDeviceToDevice, st));
-  k_dot<<<kRed, 256, 0, st>>>(n, D.vb.p, D.vb.p, D.part_b.p);
+  k_dot<<<kRed, 256, 0, st>>>(n, D.vb.p, D.vb.p, D.part_b.p, D.comm ? D.halo.owned.p : nullptr);
   count_launch(1);
+  if (D.comm) D.comm->allreduce(D.part_b.p, kRed, st);
   std::vector<double> pa(kRed), pb(kRed);
   CK(cudaMemcpyAsync(pa.data(), D.part_a.p, kRed * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(pb.data(), D.part_b.p, kRed * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -2918,7 +3053,9 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
     CK(cudaMemcpy(out.betas.data(), D.betas.p, hs.it * sizeof(double), cudaMemcpyDeviceToHost));
   }
   out.condition_estimate = lanczos_condition_estimate(out.alphas, out.betas);
-  if (x) CK(cudaMemcpy(x, D.vx.p, bytes, cudaMemcpyDeviceToHost));
+  complete_interface(D, D.vx.p);  // sharded: the whole solution on every rank
+  if (x) CK(cudaMemcpyAsync(x, D.vx.p, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   return out;
 }
 

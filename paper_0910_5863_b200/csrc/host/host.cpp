@@ -1275,4 +1275,50 @@ double lanczos_condition_estimate(const std::vector<double>& alphas,
   return lo > 0 ? hi / lo : std::numeric_limits<double>::infinity();
 }
 
+HaloPlan halo_plan(const Model& m, const std::vector<int>& owner, int me, int world) {
+  HaloPlan H;
+  const i64 n = static_cast<i64>(m.maps.interface_dofs.size());
+  std::vector<std::vector<int>> ranks(n);
+  for (i64 i = 0; i < n; ++i) {
+    const i64 g = m.maps.interface_dofs[i];
+    for (i64 t = m.maps.copy_ptr[g]; t < m.maps.copy_ptr[g + 1]; ++t) ranks[i].push_back(owner.at(m.maps.copy_sub[t]));
+    std::sort(ranks[i].begin(), ranks[i].end());
+    ranks[i].erase(std::unique(ranks[i].begin(), ranks[i].end()), ranks[i].end());
+  }
+  H.touched.assign(n, 0);
+  H.owned.assign(n, 0);
+  std::vector<std::vector<int>> per_peer(world);
+  for (i64 i = 0; i < n; ++i) {
+    if (!std::binary_search(ranks[i].begin(), ranks[i].end(), me)) continue;
+    H.touched[i] = 1;
+    H.owned[i] = ranks[i].front() == me;
+    for (int r : ranks[i])
+      if (r != me) per_peer.at(r).push_back(static_cast<int>(i));
+  }
+  H.peer_off.assign(1, 0);
+  std::vector<int> slot(world, -1);
+  for (int r = 0; r < world; ++r)
+    if (!per_peer[r].empty()) {
+      slot[r] = static_cast<int>(H.peers.size());
+      H.peers.push_back(r);
+      H.shared.insert(H.shared.end(), per_peer[r].begin(), per_peer[r].end());
+      H.peer_off.push_back(static_cast<int>(H.shared.size()));
+    }
+  H.sum_ptr.assign(1, 0);
+  for (i64 i = 0; i < n; ++i) {
+    if (!H.touched[i] || ranks[i].size() < 2) continue;
+    H.sum_dof.push_back(static_cast<int>(i));
+    for (int r : ranks[i]) {
+      if (r == me) {
+        H.sum_src.push_back(-1);
+        continue;
+      }
+      const auto b = H.shared.begin() + H.peer_off[slot[r]], e = H.shared.begin() + H.peer_off[slot[r] + 1];
+      H.sum_src.push_back(static_cast<int>(std::lower_bound(b, e, static_cast<int>(i)) - H.shared.begin()));
+    }
+    H.sum_ptr.push_back(static_cast<int>(H.sum_src.size()));
+  }
+  return H;
+}
+
 }  // namespace b200

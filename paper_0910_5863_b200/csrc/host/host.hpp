@@ -252,6 +252,19 @@ PairIndex build_pair_index(const Model& m, int si, int sj);
 /// returns nmodes x ndofs row-major, orthonormalized.
 std::vector<double> rigid_modes(const Model& m, const std::vector<i64>& dofs, int* nmodes);
 
+/// Interface halo of one rank of a sharded run: the interface
+/// dofs it touches (a copy in one of its substructures), the ones it owns
+/// (lowest rank holding a copy), per peer the shared dofs in ascending
+/// interface order, and per shared dof the contributions in ascending rank
+/// order (sum_src < 0: this rank's own partial; else a position in the
+/// per-peer concatenated receive buffer).  shard.py HaloPlan is the same plan.
+struct HaloPlan {
+  std::vector<int> peers, peer_off, shared;
+  std::vector<char> touched, owned;
+  std::vector<int> sum_dof, sum_ptr, sum_src;
+};
+HaloPlan halo_plan(const Model& m, const std::vector<int>& owner, int rank, int world);
+
 double lanczos_condition_estimate(const std::vector<double>& alphas,
                                   const std::vector<double>& betas);  // pcg.cpp:11-26
 

@@ -1,20 +1,22 @@
 """Sharding plan of the adaptive-BDDC hot path over ranks (one GPU per rank).
 
 The path shards by substructure and by face pair:
-  * substructures: 3D block partition of the subdomain lattice (`partition`);
-  * face pairs: owned by the rank of the lower-numbered substructure (`pair_owner`);
+  * substructures: 3D block partition of the subdomain lattice (`partition`,
+    used by the engine's owner map in bench.py and the tests);
+  * face pairs: owned by the rank of the lower-numbered substructure
+    (`pair_owner`); the neighbours they need (ghosts) receive their Schur
+    complements from the owning rank;
   * interface vectors: every rank holds the interface dofs its substructures
-    touch; after the per-substructure work, copies shared with other ranks are
-    summed by a point-to-point halo exchange (`HaloPlan.exchange`) -- the NCCL
-    send/recv over NVLink on the GPU path, gloo on CPU in the tests;
-  * dot products: each interface dof is owned by exactly one rank (the rank of
-    its lowest-numbered copy), local sums are all-reduced (`owned_dot`);
-  * root: leaf Schur contributions are summed onto the root by an all-reduce
-    of the (small) root matrix / right-hand side (`root_sum`).
-Everything here is host logic on index maps plus torch.distributed calls, so
-it is exercised by world_size-2 gloo tests (tests/test_multirank.py).  The
-device engine of this round runs one GPU per process; `bench.py --gpus N`
-runs replicas.
+    touch; after the per-substructure work the copies shared with other ranks
+    are summed by a point-to-point halo exchange, contributions added in
+    ascending rank order;
+  * dot products: each interface dof is owned by exactly one rank (the lowest
+    rank holding a copy); local sums are all-reduced;
+  * root: leaf Schur contributions are summed onto the root by an all-reduce.
+The device engine implements this plan in C++ (host.cpp `halo_plan`,
+engine.cu `halo_exchange` over NCCL send/recv); `HaloPlan` below is the same
+plan restated in Python with torch.distributed, the checker of the engine's
+plan in the world_size-2 gloo test (tests/test_multirank.py).
 """
 from __future__ import annotations
 

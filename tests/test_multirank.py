@@ -2,8 +2,9 @@
 
 Covers the sharding plan of the path (paper_0910_5863_b200/shard.py: block
 partition, pair ownership, interface halo exchange, owned-dof dot products,
-root sums) against the single-process oracle, and bench.py's multi-rank
-harness (barrier, max over ranks).
+root sums) against the single-process oracle, checks that the sharded
+engine's own halo plan (C++ host layer, bddc_b200_halo_plan) is the same plan,
+and bench.py's multi-rank harness (barrier, max over ranks).
 """
 import os
 import socket
@@ -72,6 +73,14 @@ def _worker(rank, world, port, errors):
         owner = shard.partition(sub, world)
         copy_ranks = [[int(owner[s]) for s, _ in p.maps.dof_copies[g]] for g in p.maps.interface_dofs]
         plan = shard.HaloPlan.build(rank, copy_ranks)
+        # the sharded engine's own plan (C++ host layer, through the ABI) is the same
+        import paper_0910_5863_b200 as pb
+        cplan = pb.BDDC(pb.Problem.cube(sub, 3, "scalar")).halo_plan(owner, rank, world)
+        assert np.array_equal(np.nonzero(cplan["touched"])[0], plan.local_iface)
+        assert np.array_equal(cplan["owned"][plan.local_iface], plan.owned)
+        assert cplan["peers"] == plan.peers
+        for r in plan.peers:
+            assert np.array_equal(cplan["shared"][r], plan.local_iface[plan.shared[r]])
         x = np.random.default_rng(7).standard_normal(itf.size)
         # each rank applies only its substructures, then the halo exchange sums copies
         part = np.zeros(itf.size)

@@ -3,7 +3,7 @@ process, exchanging through the loopback backend (each rank synchronizes its
 own stream before a host-side exchange, so no kernel waits on another rank).
 The sharded results must equal the single-engine results: operators to
 roundoff, identical constraint selection and pair reports, PCG iterations
-within +-1, kappa to the KAPPA_RTOL of test_gpu_parity, the solution to 1e-8
+within +-1, kappa to 1e-6, the solution to 1e-8
 in the energy norm, and every rank must hold the same complete result.
 """
 import itertools
@@ -111,10 +111,11 @@ def test_sharded_equals_single(name, make, world, mode):
         # of R, amplified by the root inverse (cfg2: 1e6 coefficient contrast)
         assert rel(g["prec"], ref["prec"]) <= 1e-8
         assert abs(g["pcg"]["iterations"] - ref["pcg"]["iterations"]) <= 1
+        # Lanczos estimates at 1e-6 (full runs when the counts agree, else the common prefix)
         n = min(len(g["pcg"]["alphas"]), len(ref["pcg"]["alphas"]))
         kg = pb.lanczos_condition_estimate(g["pcg"]["alphas"][:n], g["pcg"]["betas"][:n])
         ko = pb.lanczos_condition_estimate(ref["pcg"]["alphas"][:n], ref["pcg"]["betas"][:n])
-        assert abs(kg - ko) <= 1e-3 * ko
+        assert abs(kg - ko) <= 1e-6 * ko, (kg, ko)
     e = got[0]["u"] - ref["u"]
     assert energy(ref_b, e) <= 1e-16 * energy(ref_b, ref["u"])
 
