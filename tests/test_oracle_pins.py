@@ -177,7 +177,8 @@ def test_lanczos_recovers_exact_condition(pins):
 
 def test_lanczos_roundoff_floor():
     """The roundoff floor of the Lanczos estimate (tests/test_gpu_parity.py
-    check_kappa falls back to it only when the iteration counts differ):
+    check_kappa measures it per problem and falls back to it only when the
+    iteration counts differ or the 1e-6 comparison of the full estimates fails):
     perturbing the oracle's own preconditioner by 1e-13 relative already moves
     its final estimate by more than 1e-6 on this planar case, and by less than
     1e-3."""
