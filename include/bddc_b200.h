@@ -205,6 +205,26 @@ int bddc_b200_export_matrix_market(bddc_b200_t* h, const char* stem);
 int bddc_b200_interface_size(const bddc_b200_t* h, int64_t* n);
 int bddc_b200_schur_apply(bddc_b200_t* h, const double* x, double* y);
 int bddc_b200_precond_apply(bddc_b200_t* h, const double* r, double* z);
+/* BddcPreconditioner::restrict_residual / coarse_solve / prolong
+ * (bddc_operator.hpp:40-48, bddc_operator.cpp:52-99) on W^c vectors (length
+ * structure.coarse_space_dim, indexed by bddc_b200_local_to_wc; transformed
+ * variables, explicit dof k = glob slot k as transform.cpp:94-149):
+ *   restrict_residual: interface r -> Pi T^T E^T r;
+ *   coarse_solve: any W^c residual (interior entries included) -> the
+ *     constrained-minimization solution Pi A~^{-1} Pi r with the refinement
+ *     pass, i.e. the saddle-point solve of acceptance criterion 11
+ *     (acceptance_main.cpp:376-420), exact on the device's primal
+ *     reformulation for every stabilization t;
+ *   prolong: W^c -> interface (T, then the weighted average E).
+ * precond_apply == prolong(coarse_solve(restrict_residual(r))).  The stages
+ * run on the device as inside precond_apply; the W^c <-> device layout maps
+ * are applied on the host (these are not the PCG's path).  Single GPU.
+ * generalized_eig_sym (dense_eig.hpp:47-53) has one call site on the path,
+ * solve_pair (adaptive.cpp:30-47): bddc_b200_enrich + bddc_b200_pair_report
+ * return its eigenvalue list per pair (zeros beyond rank(lhs) included). */
+int bddc_b200_restrict_residual(bddc_b200_t* h, const double* r_interface, double* wc);
+int bddc_b200_coarse_solve(bddc_b200_t* h, const double* wc_residual, double* wc_out);
+int bddc_b200_prolong(bddc_b200_t* h, const double* wc, double* z_interface);
 /* Device-timed applications for rooflines (no reference counterpart; the
  * reference times phases only, experiment.cpp:114-203): mean seconds over
  * `reps` applications with device-resident vectors, CUDA events on the handle's

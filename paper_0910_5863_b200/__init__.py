@@ -131,6 +131,9 @@ EXPORTS = {
     "bddc_b200_interface_size": (C.c_int, [P, I64]),
     "bddc_b200_schur_apply": (C.c_int, [P, D, D]),
     "bddc_b200_precond_apply": (C.c_int, [P, D, D]),
+    "bddc_b200_restrict_residual": (C.c_int, [P, D, D]),
+    "bddc_b200_coarse_solve": (C.c_int, [P, D, D]),
+    "bddc_b200_prolong": (C.c_int, [P, D, D]),
     "bddc_b200_operator_times": (C.c_int, [P, C.c_int, D]),
     "bddc_b200_rhs": (C.c_int, [P, D]),
     "bddc_b200_recover": (C.c_int, [P, D, D]),
@@ -546,6 +549,27 @@ class BDDC:
         r = np.ascontiguousarray(r, dtype=np.float64)
         z = np.empty_like(r)
         _check(self._lib.bddc_b200_precond_apply(self._h, _dptr(r), _dptr(z)))
+        return z
+
+    def restrict_residual(self, r: np.ndarray) -> np.ndarray:
+        """`BddcPreconditioner::restrict_residual` (`bddc_operator.cpp:52-68`): interface -> W^c."""
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        wc = np.empty(self.structure()["coarse_space_dim"])
+        _check(self._lib.bddc_b200_restrict_residual(self._h, _dptr(r), _dptr(wc)))
+        return wc
+
+    def coarse_solve(self, wc_residual: np.ndarray) -> np.ndarray:
+        """`BddcPreconditioner::coarse_solve` (`bddc_operator.cpp:70-85`): W^c -> W^c."""
+        w = np.ascontiguousarray(wc_residual, dtype=np.float64)
+        out = np.empty_like(w)
+        _check(self._lib.bddc_b200_coarse_solve(self._h, _dptr(w), _dptr(out)))
+        return out
+
+    def prolong(self, wc: np.ndarray) -> np.ndarray:
+        """`BddcPreconditioner::prolong` (`bddc_operator.cpp:87-99`): W^c -> interface."""
+        w = np.ascontiguousarray(wc, dtype=np.float64)
+        z = np.empty(self.interface_size)
+        _check(self._lib.bddc_b200_prolong(self._h, _dptr(w), _dptr(z)))
         return z
 
     def operator_times(self, reps: int = 10) -> dict:

@@ -438,6 +438,18 @@ int bddc_b200_precond_apply(bddc_b200_t* h, const double* r, double* z) {
   return guarded([&] { engine(h).precond_apply(r, z); });
 }
 
+int bddc_b200_restrict_residual(bddc_b200_t* h, const double* r, double* wc) {
+  return guarded([&] { engine(h).restrict_residual(r, wc); });
+}
+
+int bddc_b200_coarse_solve(bddc_b200_t* h, const double* wc_residual, double* wc_out) {
+  return guarded([&] { engine(h).coarse_solve(wc_residual, wc_out); });
+}
+
+int bddc_b200_prolong(bddc_b200_t* h, const double* wc, double* z) {
+  return guarded([&] { engine(h).prolong(wc, z); });
+}
+
 int bddc_b200_operator_times(bddc_b200_t* h, int reps, double out[13]) {
   return guarded([&] {
     Engine& e = engine(h);

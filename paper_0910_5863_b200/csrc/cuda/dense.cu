@@ -47,12 +47,19 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // Warp-level 32x32 slice of a 64x64 tile product over `kdim` (multiple of 16):
-// acc[m][n] += sum_k As[k*LDS + m] * Bs[k*LDS + n].
+// acc[m][n] += sum_k As[k*LDS + m] * Bs[k*LDS + n].  Only the first vm rows and
+// vn columns of the tile are needed (the rest is padding whose product is
+// zero): a warp whose 32x32 quadrant lies in padding skips its DMMAs.
+__device__ __forceinline__ bool warp_active(int vm, int vn) {
+  const int warp = (threadIdx.x >> 5) & 3;
+  return vm > (warp & 1) * 32 && vn > (warp >> 1) * 32;
+}
 __device__ __forceinline__ void warp_mma(const double* As, const double* Bs, int kdim,
-                                         double (&acc)[2][4][4]) {
+                                         double (&acc)[2][4][4], bool active = true) {
   const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) & 3;
   const int g = lane >> 2, t0 = lane & 3;
   const int m0 = (warp & 1) * 32, n0 = (warp >> 1) * 32;
+  if (!active) return;
 #pragma unroll 2
   for (int kk = 0; kk < kdim; kk += 16) {
     double a[2][8], b[4][4];
@@ -524,8 +531,12 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 
 // acc = sum over K in [kb, ke) of A[i0:i0+64, K] A[j0:j0+64, K]^T, waiting for
 // column block k of rows i0/64 and j0/64 (prog pointers pi, pj) before reading it.
+// vm / vn: valid rows of tile rows i0/64 and j0/64; kv: valid end of the K
+// range (columns >= kv are padding, FrontDesc::ne): the range is cut at kv
+// rounded up to 16.
 __device__ void dag_accumulate(const double* a, int ld, int i0, int j0, int kb, int ke, const int* pi,
-                               const int* pj, double (&acc)[2][4][4], double* smem, int* s_ready) {
+                               const int* pj, double (&acc)[2][4][4], double* smem, int* s_ready, int vm = 64,
+                               int vn = 64, int kv = 1 << 30) {
   double* As = smem;                 // [2][KC*LDS]
   double* Bs = smem + 2 * KC * LDS;  // [2][KC*LDS]
 #pragma unroll
@@ -534,8 +545,10 @@ __device__ void dag_accumulate(const double* a, int ld, int i0, int j0, int kb, 
     for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
       for (int v = 0; v < 4; ++v) acc[mi][ni][v] = 0.0;
-  const int nch = (ke - kb) / KC;
-  if (nch <= 0) return;
+  ke = min(ke, (kv + 15) & ~15);
+  const int nch = (ke - kb + KC - 1) / KC;
+  if (nch <= 0 || vm <= 0 || vn <= 0) return;
+  const bool active = warp_active(vm, vn);
   int ready = 0;  // column blocks [0, ready) final for both rows (uniform over the CTA)
   auto blk = [&](int c) { return (kb + c * KC) >> 6; };
   auto poll = [&](int need, bool block) {
@@ -577,7 +590,7 @@ __device__ void dag_accumulate(const double* a, int ld, int i0, int j0, int kb, 
       cp_async_wait<0>();
     }
     __syncthreads();
-    warp_mma(As + (c & 1) * KC * LDS, Bs + (c & 1) * KC * LDS, KC, acc);
+    warp_mma(As + (c & 1) * KC * LDS, Bs + (c & 1) * KC * LDS, min(KC, ke - kb - c * KC), acc, active);
     __syncthreads();
     if (c + 1 < nch && !pf) {
       poll(blk(c + 1), true);
@@ -586,13 +599,23 @@ __device__ void dag_accumulate(const double* a, int ld, int i0, int j0, int kb, 
   }
 }
 
+// Valid (unpadded) rows of tile row i of a plain front, and the valid end of
+// its eliminated columns (FrontDesc::ne / nc; 64 and p when unknown).
+__device__ __forceinline__ int front_valid(const FrontDesc& d, int i) {
+  if (d.ne <= 0 || d.aug) return kTile;
+  const int pt = d.p / kTile;
+  return max(0, min(kTile, i < pt ? d.ne - i * kTile : d.nc - (i - pt) * kTile));
+}
+__device__ __forceinline__ int front_kvalid(const FrontDesc& d) { return d.ne > 0 && !d.aug ? d.ne : d.p; }
+
 // Diagonal tile j of front b: C_jj -= sum_k L_jk L_jk^T (waiting for the
 // columns), L_jj = chol(C_jj), Dinv_j; publishes prog[j] = j + 1.
 __device__ void dag_diagonal(const FrontDesc& d, int b, int j, int* prog, double* smem, int* s_ready) {
   const int tid = threadIdx.x, j0 = j * kTile;
   const size_t ld = d.n;
   double acc[2][4][4];
-  dag_accumulate(d.a, d.n, j0, j0, 0, j0, prog + j, prog + j, acc, smem, s_ready);
+  dag_accumulate(d.a, d.n, j0, j0, 0, j0, prog + j, prog + j, acc, smem, s_ready, front_valid(d, j),
+                 front_valid(d, j), front_kvalid(d));
   dag_mark(b, 2 * j);
   double* tile = d.a + (size_t)j0 * ld + j0;
   double* C = smem;
@@ -635,7 +658,8 @@ __device__ void dag_offdiag(const FrontDesc& d, int i, int j, int* prog, double*
   const int kb = aug_k0(d, i0);
   if (kb > j0) return;  // zero tile of the augmented block
   double acc[2][4][4];
-  dag_accumulate(d.a, d.n, i0, j0, kb, j0, prog + i, prog + j, acc, smem, s_ready);
+  const int vi = front_valid(d, i), vj = front_valid(d, j);
+  dag_accumulate(d.a, d.n, i0, j0, kb, j0, prog + i, prog + j, acc, smem, s_ready, vi, vj, front_kvalid(d));
   double* tile = d.a + (size_t)j0 * ld + i0;
   double* C = smem;
   double* V = smem + 64 * LDS;
@@ -667,7 +691,7 @@ __device__ void dag_offdiag(const FrontDesc& d, int i, int j, int* prog, double*
     for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
       for (int v = 0; v < 4; ++v) x[mi][ni][v] = 0.0;
-  warp_mma(C, V, 64, x);
+  warp_mma(C, V, min(64, (vj + 15) & ~15), x, warp_active(vi, vj));  // padding rows / columns of L_ij stay zero
   for_acc(x, [&](int m, int n, double v) { tile[(size_t)n * ld + m] = v; });
   __syncthreads();
   if (tid == 0) {
@@ -698,7 +722,8 @@ __device__ void dag_trailing(const FrontDesc& d, int i, int j, int kb, int ke, i
                              int* s_ready) {
   const int i0 = i * kTile, j0 = j * kTile;
   double acc[2][4][4];
-  dag_accumulate(d.a, d.n, i0, j0, kb, ke, prog + i, prog + j, acc, smem, s_ready);
+  dag_accumulate(d.a, d.n, i0, j0, kb, ke, prog + i, prog + j, acc, smem, s_ready, front_valid(d, i),
+                 front_valid(d, j), front_kvalid(d));
   tile_sub_acc(d.a + (size_t)j0 * d.n + i0, d.n, acc, smem);
 }
 
@@ -805,7 +830,8 @@ __device__ void dag_prepare(const FrontDesc& d, int i, int j, int kb, int ke, in
   if (ke > kb) {
     const int i0 = i * kTile, j0 = j * kTile;
     double acc[2][4][4];
-    dag_accumulate(d.a, d.n, i0, j0, kb, ke, prog + i, prog + j, acc, smem, s_ready);
+    dag_accumulate(d.a, d.n, i0, j0, kb, ke, prog + i, prog + j, acc, smem, s_ready, front_valid(d, i),
+                   front_valid(d, j), front_kvalid(d));
     tile_sub_acc(d.a + (size_t)j0 * d.n + i0, d.n, acc, smem);
   }
   __syncthreads();
@@ -832,7 +858,7 @@ __device__ void dag_prepare(const FrontDesc& d, int i, int j, int kb, int ke, in
 // of every trailing tile by the columns [k cw, (k+1) cw) (chunk k of a tile waits for chunk
 // k-1 of the same tile).  Half of the queue CTAs take B only; the others take A
 // and then B.  A waits only on A and the workers, B on A and B: no cycle.
-__global__ void __launch_bounds__(DAG_THREADS) k_chol_dag(const FrontDesc* ds, int batch, int nt, int pt_max,
+__global__ void __launch_bounds__(DAG_THREADS, 3) k_chol_dag(const FrontDesc* ds, int batch, int nt, int pt_max,
                                                           int mt, int* ctl, int total, int chunked, int cw, int bq) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_task, s_ready;
@@ -1207,10 +1233,30 @@ __global__ void __launch_bounds__(256) k_front_backward_cl(const SolveDesc* ds, 
 // ---------------------------------------------------------------------------
 constexpr int SW_LDS = 68;  // shared-memory ld of the Dinv tile (16-byte rows, few bank conflicts)
 
-__device__ __forceinline__ void sweep_prefetch_dinv(double* dvs, const double* dv) {
-  for (int q = threadIdx.x; q < 64 * 32; q += 256)
-    cp_async16(dvs + (q >> 5) * SW_LDS + (q & 31) * 2, dv + (q >> 5) * 64 + (q & 31) * 2);
+// cp.async of 16 bytes, or 16 bytes of zeros without touching global memory
+__device__ __forceinline__ void cp_async16_or_zero(void* smem, const void* gmem, bool read) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int bytes = read ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+
+// Dinv tile (lower triangular, 64x64 column-major) into shared memory: only
+// the lower triangle of the `valid` leading rows/columns is read (row pairs
+// reaching the diagonal); everything else is zero-filled.
+__device__ __forceinline__ void sweep_prefetch_dinv(double* dvs, const double* dv, int valid) {
+  for (int q = threadIdx.x; q < 64 * 32; q += 256) {
+    const int c = q >> 5, r = (q & 31) * 2;
+    cp_async16_or_zero(dvs + c * SW_LDS + r, dv + c * 64 + r, r + 1 >= c && r < valid && c < valid);
+  }
   cp_async_commit();
+}
+
+// Valid (unpadded) rows of row tile i of a front.
+__device__ __forceinline__ int sweep_valid_rows(const SolveDesc& d, int i) {
+  const int nb = d.p / kTile;
+  const int ne = d.ne > 0 ? d.ne : d.p, nc = d.ne > 0 ? d.nc : d.n - d.p;
+  const int v = i < nb ? ne - i * kTile : nc - (i - nb) * kTile;
+  return max(0, min(kTile, v));
 }
 
 // The last CTA to leave zeroes the counters for the next launch (no memset
@@ -1266,17 +1312,23 @@ __global__ void __launch_bounds__(256, 4) k_sweep_fwd_dag(const SolveDesc* ds, i
     const int nt = d.n / kTile, nb = d.p / kTile;
     if (i < nt) {
       const bool solve = i < nb;
-      if (solve) sweep_prefetch_dinv(dvs, d.dinv + (size_t)i * 64 * 64);
+      const int vrows = sweep_valid_rows(d, i);
+      if (solve) sweep_prefetch_dinv(dvs, d.dinv + (size_t)i * 64 * 64, vrows);
       const size_t ld = d.n;
       const int K = min(i, nb);
+      const int ne = d.ne > 0 ? d.ne : d.p;
       double a0 = 0.0, a1 = 0.0;
       int ready = 0;
       const double* lrow = d.a + (size_t)(8 * warp) * ld + i * kTile + 2 * lane;
+      const bool row_ok = 2 * lane < vrows;  // padding rows are never loaded
       for (int k = 0; k < K; ++k) {
         const double* base = lrow + (size_t)k * kTile * ld;
+        const int cols = ne - (k * kTile + 8 * warp);  // valid columns of this warp's eight
         double2 L[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) L[q] = __ldcs(reinterpret_cast<const double2*>(base + (size_t)q * ld));
+        for (int q = 0; q < 8; ++q)
+          L[q] = row_ok && q < cols ? __ldcs(reinterpret_cast<const double2*>(base + (size_t)q * ld))
+                                    : make_double2(0.0, 0.0);
         sweep_wait(prog + f, k + 1, ready);
         const double* z = d.x + k * kTile + 8 * warp;
 #pragma unroll
@@ -1346,18 +1398,22 @@ __global__ void __launch_bounds__(256, 2) k_sweep_bwd_dag(const SolveDesc* ds, i
     if (l == 0 && d.cmap)  // the first task of a front writes its coarse rows (others read croot)
       for (int r = d.p + tid; r < d.n; r += 256) d.x[r] = sweep_xin(d.x, d.p, d.cmap, d.croot, r);
     if (kb >= 0) {
-      sweep_prefetch_dinv(dvs, d.dinv + (size_t)kb * 64 * 64);
+      sweep_prefetch_dinv(dvs, d.dinv + (size_t)kb * 64 * 64, sweep_valid_rows(d, kb));
       const size_t ld = d.n;
       double acc[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.0;
       int ready = 0;
       const double* lcol = d.a + (size_t)(kb * kTile + 8 * warp) * ld + 2 * lane;
+      const int cols = (d.ne > 0 ? d.ne : d.p) - (kb * kTile + 8 * warp);  // valid columns of this warp's eight
       for (int r = nt - 1; r > kb; --r) {
         const double* base = lcol + r * kTile;
+        const bool row_ok = 2 * lane < sweep_valid_rows(d, r);  // padding rows are never loaded
         double2 L[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) L[q] = __ldcs(reinterpret_cast<const double2*>(base + (size_t)q * ld));
+        for (int q = 0; q < 8; ++q)
+          L[q] = row_ok && q < cols ? __ldcs(reinterpret_cast<const double2*>(base + (size_t)q * ld))
+                                    : make_double2(0.0, 0.0);
         if (r < nb) sweep_wait(prog + f, nb - r, ready);
         const int row = r * kTile + 2 * lane;
         const double x0 = sweep_xin(d.x, d.p, d.cmap, d.croot, row), x1 = sweep_xin(d.x, d.p, d.cmap, d.croot, row + 1);
@@ -1698,11 +1754,9 @@ void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, i
   if (const char* e = std::getenv("BDDC_B200_DAGW"); e && *e) chunked = *e == '1' && 3L * batch <= resident;
   long total;
   int cw = 1, bq = 6;
-  if (const char* e = std::getenv("BDDC_B200_DAGBQ"); e && *e) bq = std::min(11, std::max(0, std::atoi(e)));
   size_t ints = DAG_CTL + (size_t)batch * nt;
   if (chunked) {
     cw = std::max(1, (pt + 2) / 3);  // about three trailing chunks per tile
-    if (const char* e = std::getenv("BDDC_B200_DAGCW"); e && *e) cw = std::max(1, std::atoi(e));
     const int nchunk = (pt + cw - 1) / cw;
     total = (long)nchunk * batch * mt * (mt + 1) / 2;
     for (int c = 0; c < pt; ++c) total += (long)batch * (std::max(nt - c - 2, 0) + 2);
@@ -1724,10 +1778,6 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
                       cudaStream_t stream) {
   if (batch == 0) return;
   per_device(reinterpret_cast<const void*>(&configure_device), configure_device);
-  static const bool dbg = std::getenv("BDDC_B200_CHOLDBG") != nullptr;
-  if (dbg)
-    std::fprintf(stderr, "[chol] batch %d n %d p %d m %d -> %s\n", batch, max_n, max_p, max_m,
-                 max_p > 0 && use_dag(batch, max_n / kTile, max_p / kTile) ? "dag" : "tiled");
   if (max_p > 0 && use_dag(batch, max_n / kTile, max_p / kTile)) {
     partial_cholesky_dag(d_descs, batch, max_n / kTile, max_p / kTile, max_m / kTile, stream);
     return;
@@ -1772,14 +1822,8 @@ void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p,
 
 namespace {
 // CTAs per front: a cluster of 16, 8, 4 or 2 when the fronts alone cannot fill
-// the GPU (about three CTAs per SM), else one.  BDDC_B200_SWEEP_CL=1|2|4|8|16
-// overrides.
+// the GPU (about three CTAs per SM), else one.
 int sweep_cluster(int batch, int max_cl) {
-  const char* env = std::getenv("BDDC_B200_SWEEP_CL");
-  if (env && *env) {
-    const int c = std::atoi(env);
-    if (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) return c;
-  }
   const long cap = 3L * sm_count();
   if (max_cl >= 16 && (long)batch * 16 <= cap) return 16;
   if (max_cl >= 8 && (long)batch * 8 <= cap) return 8;

@@ -32,6 +32,12 @@ struct FrontDesc {
   // Their factor rows are L^{-T} (upper triangular), so augmented tile (a, k)
   // is zero for a > k and the updates skip those tiles and K ranges.
   int aug;
+  // True (unpadded) extents of a plain front (aug == 0): rows/columns [ne, p)
+  // and [p + nc, n) are padding (unit diagonal, zeros elsewhere), which
+  // contributes nothing to any product.  The dataflow schedule then trims the K
+  // ranges to ne (rounded up to 16) and skips the 16-row / 8-column DMMA
+  // blocks that lie in padding.  0 = unknown (every tile computed in full).
+  int ne = 0, nc = 0;
 };
 
 struct SolveDesc {
@@ -42,6 +48,11 @@ struct SolveDesc {
   int p;
   const int* cmap;      // optional (backward): x[p+c] = cmap[c] >= 0 ? croot[cmap[c]] : 0
   const double* croot;
+  // True (unpadded) extents: rows/columns [ne, p) of the eliminated block and
+  // rows [p + nc, n) of the trailing block are padding (unit diagonal, zero
+  // vector entries).  The dataflow sweeps never load them, so a sweep moves the
+  // factor's own bytes rather than whole 64x64 tiles.  0 = unknown (use p, n - p).
+  int ne = 0, nc = 0;
 };
 
 /// Streaming multiprocessors of the current device.

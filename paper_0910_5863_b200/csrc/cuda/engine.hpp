@@ -113,6 +113,11 @@ class Engine {
   /// out == nullptr returns only ld and the position map.
   void leaf_front(int s, std::vector<double>* out, std::vector<int>* pos, int* ld);
   void precond_apply(const double* r, double* z);
+  /// BddcPreconditioner::{restrict_residual, coarse_solve, prolong}
+  /// (bddc_operator.cpp:52-99): interface <-> W^c (maps.wc_dim) host vectors.
+  void restrict_residual(const double* r_interface, double* wc);
+  void coarse_solve(const double* wc_residual, double* wc_out);
+  void prolong(const double* wc, double* z_interface);
   void rhs(double* out);
   void recover(const double* u_interface, double* u_free);
   /// b == nullptr: use the condensed rhs on the device.  x may be nullptr.

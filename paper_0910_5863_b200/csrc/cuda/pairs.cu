@@ -262,136 +262,7 @@ __global__ void k_build_F4(const PairDev* pd) {
   }
 }
 
-// (j) parallel cyclic Jacobi on C (n2 x n2, even): A <- J^T A J, V <- V J.
-// Round-robin ordering: in each of the n2-1 rounds the n2/2 index pairs are
-// disjoint, so all rotations of a round are applied at once (rows, then columns).
-__device__ __forceinline__ void rr_pair(int k, int round, int n2, int& p, int& q) {
-  const int m = n2 - 1;
-  p = k == 0 ? 0 : 1 + (k - 1 + round) % m;
-  q = 1 + (n2 - 2 - k + round) % m;
-  if (p > q) {
-    const int t = p;
-    p = q;
-    q = t;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_jacobi(const PairDev* pd, int smem_cap) {
-  const PairDev d = pd[blockIdx.x];
-  const int nj = d.nj, n2 = nj + (nj & 1), PJ = d.PJ, N2 = 2 * PJ;
-  extern __shared__ double sm[];
-  const bool in_smem = 2 * n2 * n2 <= smem_cap;
-  double* A = in_smem ? sm : d.A;
-  double* V = in_smem ? sm + n2 * n2 : d.V;
-  double* cs = in_smem ? sm + 2 * n2 * n2 : sm;  // n2/2 cosines then n2/2 sines
-  const int tid = threadIdx.x;
-  for (int e = tid; e < n2 * n2; e += blockDim.x) {
-    const int r = e % n2, c = e / n2;
-    double v = 0.0;
-    if (r < nj && c < nj) {
-      const int hi = r >= c ? r : c, lo = r >= c ? c : r;
-      v = d.F4[(size_t)lo * N2 + PJ + hi];
-    }
-    A[e] = v;
-    V[e] = r == c ? 1.0 : 0.0;
-  }
-  __shared__ double red[256];
-  __shared__ int rotated;
-  double part = 0.0;
-  for (int e = tid; e < n2 * n2; e += blockDim.x) part += A[e] * A[e];
-  red[tid] = part;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (tid < s) red[tid] += red[tid + s];
-    __syncthreads();
-  }
-  const double fro = sqrt(red[0]);
-  // Rotations below `tiny` are skipped; a sweep whose rotations are all below
-  // `settle` counts as converged (off-diagonal mass at roundoff level, so the
-  // eigenvalue error is O(eps * ||C||_F)).
-  const double tiny = 1e-17 * fro / (n2 > 0 ? n2 : 1);
-  const double settle = 1e-14 * fro / (n2 > 0 ? n2 : 1);
-  const int half = n2 / 2;
-  for (int sweep = 0; sweep < 40 && n2 > 1; ++sweep) {
-    if (tid == 0) rotated = 0;
-    __syncthreads();
-    for (int round = 0; round < n2 - 1; ++round) {
-      for (int k = tid; k < half; k += blockDim.x) {
-        int p, q;
-        rr_pair(k, round, n2, p, q);
-        const double apq = A[(size_t)q * n2 + p];
-        const double app = A[(size_t)p * n2 + p], aqq = A[(size_t)q * n2 + q];
-        double c = 1.0, s = 0.0;
-        if (fabs(apq) > tiny && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq))) {
-          const double theta = (aqq - app) / (2.0 * apq);
-          const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-          c = 1.0 / sqrt(t * t + 1.0);
-          s = t * c;
-          if (fabs(apq) > settle) rotated = 1;
-        }
-        cs[k] = c;
-        cs[half + k] = s;
-      }
-      __syncthreads();
-      for (int e = tid; e < half * n2; e += blockDim.x) {  // rows p, q
-        const int k = e / n2, col = e % n2;
-        const double c = cs[k], s = cs[half + k];
-        if (s == 0.0) continue;
-        int p, q;
-        rr_pair(k, round, n2, p, q);
-        const double ap = A[(size_t)col * n2 + p], aq = A[(size_t)col * n2 + q];
-        A[(size_t)col * n2 + p] = c * ap - s * aq;
-        A[(size_t)col * n2 + q] = s * ap + c * aq;
-      }
-      __syncthreads();
-      for (int e = tid; e < half * n2; e += blockDim.x) {  // columns p, q of A and V
-        const int k = e / n2, row = e % n2;
-        const double c = cs[k], s = cs[half + k];
-        if (s == 0.0) continue;
-        int p, q;
-        rr_pair(k, round, n2, p, q);
-        const double ap = A[(size_t)p * n2 + row], aq = A[(size_t)q * n2 + row];
-        A[(size_t)p * n2 + row] = c * ap - s * aq;
-        A[(size_t)q * n2 + row] = s * ap + c * aq;
-        const double vp = V[(size_t)p * n2 + row], vq = V[(size_t)q * n2 + row];
-        V[(size_t)p * n2 + row] = c * vp - s * vq;
-        V[(size_t)q * n2 + row] = s * vp + c * vq;
-      }
-      __syncthreads();
-    }
-    const int any = rotated;
-    __syncthreads();
-    if (!any) break;
-  }
-  // top-k eigenvalues, descending (one thread; k <= 64)
-  __shared__ int order[64];
-  if (tid == 0) {
-    for (int m = 0; m < d.k; ++m) {
-      int best = -1;
-      double bv = -1e300;
-      for (int i = 0; i < nj; ++i) {
-        bool used = false;
-        for (int q = 0; q < m; ++q) used |= order[q] == i;
-        const double v = A[(size_t)i * n2 + i];
-        if (!used && v > bv) {
-          bv = v;
-          best = i;
-        }
-      }
-      order[m] = best;
-      d.evals[m] = best >= 0 ? fmax(bv, 0.0) : 0.0;
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < d.k * N2; e += blockDim.x) {  // solve vectors [y; 0]
-    const int m = e / N2, r = e % N2;
-    const int col = order[m];
-    d.vecs[e] = (col >= 0 && r < nj) ? V[(size_t)col * n2 + r] : 0.0;
-  }
-}
-
-// (j') Top-k symmetric eigensolver (the default; k_jacobi is kept for
-// cross-checks, BDDC_B200_EIG=jacobi).  One CTA per pair:
+// (j) Top-k symmetric eigensolver.  One CTA per pair:
 //   1. Householder tridiagonalization of C, packed lower storage in shared
 //      memory (global memory beyond 236 rows), reflectors kept in place;
 //   2. the k largest eigenvalues of the tridiagonal by 16-way multisection on
@@ -1271,7 +1142,8 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
         const int sub = hubs[q].s;
         gh[q] = GatherDesc{S_ + s_off_[sub], B_.Hpos.p + hposOff[q], B_.Hub.p + hubOff[q], PB_[sub], hubNH[q],
                            hubPH[q], static_cast<int>(hubs[q].rest.size()), static_cast<int>(hubs[q].U.size())};
-        fh[q] = FrontDesc{B_.Hub.p + hubOff[q], B_.DvH.p + hubDOff[q], hubNH[q], hubPH[q], B_.hinfo.p + q, 0};
+        fh[q] = FrontDesc{B_.Hub.p + hubOff[q], B_.DvH.p + hubDOff[q], hubNH[q], hubPH[q], B_.hinfo.p + q, 0,
+                          static_cast<int>(hubs[q].rest.size()), static_cast<int>(hubs[q].U.size())};
       }
       B_.ghub.upload(gh, st_);
       B_.dHub.upload(fh, st_);
@@ -1344,7 +1216,8 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
         d.NG[side] = dm.NG[side];
         d.PO[side] = dm.PO[side];
         d.no[side] = dm.no[side];
-        fG[2 * b + side] = FrontDesc{d.G[side], Dv.p + oDG[2 * b + side], dm.NG[side], dm.PO[side], info.p + 4 * b + side, 0};
+        fG[2 * b + side] = FrontDesc{d.G[side], Dv.p + oDG[2 * b + side], dm.NG[side], dm.PO[side], info.p + 4 * b + side, 0,
+                                     dm.no[side], dm.nc + dm.nf};
         maxNG = std::max(maxNG, dm.NG[side]);
         maxPO = std::max(maxPO, dm.PO[side]);
         maxM1 = std::max(maxM1, dm.NG[side] - dm.PO[side]);
@@ -1441,18 +1314,8 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     partial_cholesky(d4.p, nb, 2 * maxPJ, maxPJ, maxPJ, st_);
     CK(cudaGetLastError());
     prof.mark("reduceC");
-    // (j) Jacobi
-    // A and V in shared memory when they fit next to the kernel's static
-    // arrays (~2.5 KB of the 227 KB per CTA), else in global memory (L2).
-    const char* eig_env = std::getenv("BDDC_B200_EIG");
-    if (eig_env && std::strcmp(eig_env, "jacobi") == 0) {
-      const int cap = (224 * 1024) / 8 - maxn2 - 16;
-      const bool smem_ok = 2 * maxn2 * maxn2 <= cap;
-      const int jsm = (smem_ok ? 2 * maxn2 * maxn2 : 0) * 8 + maxn2 * 8 + 64;
-      CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
-      k_jacobi<<<nb, 256, jsm, st_>>>(dpd.p, smem_ok ? 2 * maxn2 * maxn2 : 0);
-      prof.mark(smem_ok ? "jacobi_smem" : "jacobi_gmem");
-    } else {
+    // (j) top-k eigenpairs of C
+    {
       const int maxn = maxn2;  // >= every nj
       const long need = (long)maxn * (maxn + 1) / 2 + 6L * maxn + 7L * maxn * std::max(maxk, 1);
       const long cap = (220 * 1024) / 8;  // leaves room for the kernel's static arrays

@@ -36,9 +36,12 @@ static double dot(const double* a, const double* b, int64_t n) {
   return s;
 }
 
-/* 2x2x2 substructures of 2^3 elements, elasticity, clamped on x = 0, body
- * force (0,0,-1): tests/support.hpp:32-48 */
+/* 2x2x2 substructures of 2^3 elements, elasticity, clamped on x = 0, traction
+ * (0,0,-1) on x = max: tests/support.hpp:32-48 */
 static void cube_problem(bddc_b200_problem* p, int* faces, int* comps) {
+  static int load_face[1] = {1};
+  static double traction[3] = {0.0, 0.0, -1.0};
+  static double flux[1] = {1.0};
   memset(p, 0, sizeof(*p));
   p->subdomains[0] = p->subdomains[1] = p->subdomains[2] = 2;
   p->elements_per_edge = 2;
@@ -48,8 +51,10 @@ static void cube_problem(bddc_b200_problem* p, int* faces, int* comps) {
   p->n_dirichlet = 1;
   p->dirichlet_face = faces;
   p->dirichlet_components = comps;
-  p->body_force[2] = -1.0;
-  p->source = 1.0;
+  p->n_loads = 1;
+  p->load_face = load_face;
+  p->load_traction = traction;
+  p->load_flux = flux;
   p->tolerance = 1e-8;
   p->max_iterations = 500;
 }

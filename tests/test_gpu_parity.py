@@ -351,6 +351,18 @@ def test_cholesky_schedules_operators(chol, leaf, root, monkeypatch):
     test_operators_pcg_and_solution(*OPS[-1], leaf, root, "0", monkeypatch)
 
 
+@pytest.mark.parametrize("dagw", ["0", "1"])
+def test_dataflow_cholesky_modes_operators(dagw, monkeypatch):
+    """k_chol_dag's two task layouts on the same leaf fronts at the operator
+    level: plain (column-major tile queue, the layout of batches above 74
+    fronts: cfg3-5) forced on cfg1's 27 fronts with BDDC_B200_DAGW=0, chunked
+    (diagonal workers + trailing chunks) with 1; Schur and preconditioner
+    applies, PCG and solution against the oracle, in both leaf modes."""
+    monkeypatch.setenv("BDDC_B200_DAGW", dagw)
+    test_operators_pcg_and_solution(*OPS[-1], "factor", "sweep", "0", monkeypatch)
+    test_operators_pcg_and_solution(*OPS[-1], "explicit", "inverse", "0", monkeypatch)
+
+
 @pytest.mark.parametrize("placement", ["S", "G"])
 def test_pair_eigensolver_placements(placement, monkeypatch):
     """k_syevx with the packed matrix in shared memory (S) and in global memory
@@ -391,3 +403,55 @@ def test_persistent_and_graph_pcg_identical(make, mode, tau, maxv, monkeypatch):
     assert np.array_equal(a["betas"], g["betas"])
     assert np.array_equal(a["x"], g["x"])
     assert a["condition_estimate"] == g["condition_estimate"]
+
+
+WC_CASES = [("stack-scalar", (1, 1, 2), 4, "scalar", fem.SCALAR, "c+e+f", "explicit"),
+            ("stack-elastic", (1, 1, 2), 3, "elasticity", fem.ELASTICITY, "c+e+f", "factor"),
+            ("planar-scalar", (2, 2, 1), 3, "scalar", fem.SCALAR, "c+e+f", "explicit"),
+            ("el222h2 adaptive", (2, 2, 2), 2, "elasticity", fem.ELASTICITY, "adaptive", "factor")]
+
+
+@pytest.mark.parametrize("name,lattice,epe,phys,ophys,mode,leaf", WC_CASES, ids=[c[0] for c in WC_CASES])
+def test_wc_entry_points(name, lattice, epe, phys, ophys, mode, leaf, monkeypatch):
+    """BddcPreconditioner::restrict_residual / coarse_solve / prolong on W^c
+    vectors (bddc_operator.cpp:52-99) against the oracle, on the instances of
+    acceptance criterion 11 (acceptance_main.cpp:376-420: random W^c residuals
+    with interior entries; the stabilized solve equals the saddle-point solve
+    for t = -1, 1, 1e6 -- the device's primal reformulation is that solve for
+    every t) plus an adaptive constraint set, in both leaf modes; the three
+    stages compose to precond_apply (bddc_operator.cpp:101-103)."""
+    monkeypatch.setenv("BDDC_B200_LEAF", leaf)
+    p = build_pipeline(cube_spec(lattice, epe, ophys))
+    b = pb.BDDC(pb.Problem.cube(lattice, epe, phys))
+    b.analysis()
+    if mode == "adaptive":
+        ref = solve_item(p, "adaptive", 10.0, 15)
+        cs = ref.constraints
+        b.arithmetic_constraints(True, False)
+        b.enrich(10.0, 15)
+    else:
+        cs = arithmetic_constraints(p.globset, p.dmap, True, True)
+        b.arithmetic_constraints(True, True)
+    avg = AveragingOperator(p.systems, p.maps)
+    rng = np.random.default_rng(11)
+    n_wc = b.structure()["coarse_space_dim"]
+    assert n_wc == p.maps.wc_dim
+    for t in (-1.0, 1.0, 1e6):
+        prec = BddcPreconditioner(p.systems, p.maps, avg, change_of_variables(cs, p.globset, p.dmap, p.maps), t)
+        b.setup_preconditioner(t)
+        r = rng.standard_normal(b.interface_size)
+        w_o = prec.restrict_residual(r)
+        w_g = b.restrict_residual(r)
+        assert rel(w_g, w_o) <= 1e-12
+        for trial in range(2):
+            res = rng.standard_normal(n_wc)
+            x_o = prec.coarse_solve(res)
+            x_g = b.coarse_solve(res)
+            assert np.max(np.abs(x_g - x_o)) <= 1e-9 * np.max(np.abs(x_o)), (name, t, trial)
+            # the result is projected: group members carry one value
+            assert rel(prec.projector.apply(x_g.copy()), x_g) <= 1e-13
+        wc = rng.standard_normal(n_wc)
+        assert rel(b.prolong(wc), prec.prolong(wc)) <= 1e-12
+        z = b.prolong(b.coarse_solve(b.restrict_residual(r)))
+        assert rel(z, b.precond_apply(r)) <= 1e-12
+        assert rel(z, prec.apply(r)) <= 1e-10
