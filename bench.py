@@ -83,10 +83,17 @@ def measured_traffic(config):
     """DRAM bytes (read + write) of one leaf factorization and of one Schur +
     preconditioner apply, from the ncu capture committed under profiles/
     (tools/ncu_traffic.py); {} when this config was not captured."""
-    try:
-        with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as f:
-            data = json.load(f)
-    except OSError:
+    data, name = None, None
+    for name in ("r02_traffic.json", "r01_traffic.json"):  # newest capture that holds this config
+        try:
+            with open(os.path.join(REPO, "profiles", name)) as f:
+                data = json.load(f)
+        except OSError:
+            continue
+        if any(("cfg%d_%s" % (config, ph)) in data for ph in ("leaf", "apply")):
+            break
+        data = None
+    if data is None:
         return {}
     out = {}
     for phase in ("leaf", "apply"):
@@ -94,7 +101,7 @@ def measured_traffic(config):
         if rec:
             out[phase] = rec["dram_bytes_read"] + rec["dram_bytes_write"]
     if out:
-        out["source"] = "profiles/r01_traffic.json (ncu dram__bytes_{read,write}.sum over one phase)"
+        out["source"] = "profiles/%s (ncu dram__bytes_{read,write}.sum over one phase)" % name
     return out
 
 

@@ -1374,7 +1374,7 @@ __device__ __forceinline__ double sweep_xin(const double* x, int p, const int* c
   return __ldcg(x + r);
 }
 
-__global__ void __launch_bounds__(256, 2) k_sweep_bwd_dag(const SolveDesc* ds, int batch, int levels, int* ctl,
+__global__ void __launch_bounds__(256, 3) k_sweep_bwd_dag(const SolveDesc* ds, int batch, int levels, int* ctl,
                                                            const int* done) {
   if (done && *done) return;
   __shared__ __align__(16) double dvs[64 * SW_LDS];
@@ -1912,7 +1912,11 @@ void launch_sweep_dag(SweepKernel kern, const SolveDesc* d_descs, int batch, int
                           return o;
                         });
   const long tasks = (long)levels * batch;
-  const int grid = static_cast<int>(std::max<long>(1, std::min<long>(tasks, (long)std::max(occ, 1) * sm_count())));
+  // a front's chain keeps little more than one task streaming at a time: CTAs
+  // beyond ~2 per front only spin on the progress counters (measured on cfg4,
+  // 216 fronts: 432 CTAs beat 297 and the resident 592 / 444)
+  const long want = std::min<long>((long)std::max(occ, 1) * sm_count(), std::max<long>(sm_count(), 2L * batch));
+  const int grid = static_cast<int>(std::max<long>(1, std::min<long>(tasks, want)));
   kern<<<grid, 256, 0, stream>>>(d_descs, batch, levels, ctl, done);
   count_launch(1);
 }

@@ -1400,6 +1400,9 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
   };
   std::vector<Cand> cands;
   std::vector<PairReport> reps(np);
+  // per pair in parallel (independent), concatenated in pair order below
+  std::vector<std::vector<Cand>> pair_cands(np);
+#pragma omp parallel for schedule(dynamic, 8) if (np >= 256)
   for (int p = 0; p < np; ++p) {
     const HostPair& h = hp[p];
     PairReport& rep = reps[p];
@@ -1437,13 +1440,15 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
             if (std::abs(piece[t]) > std::abs(piece[top])) top = t;
           const double div = piece[top] < 0 ? -pn : pn;
           for (double& v : piece) v /= div;
-          cands.push_back(Cand{p, g, std::move(piece), 0});
+          pair_cands[p].push_back(Cand{p, g, std::move(piece), 0});
         }
       }
     } else {
       rep.omega_next = L > 0 ? lam[0] : 0.0;
     }
   }
+  for (int p = 0; p < np; ++p)
+    for (Cand& c : pair_cands[p]) cands.push_back(std::move(c));
   if (comm_) {
     // every rank's reports and candidates, in the global pair order, so that all
     // ranks apply the same rank filter and end with the same constraint set

@@ -331,21 +331,26 @@ void complete_coarse_tree(CoarseTree& t, const std::vector<CoarseLeaf>& leaves) 
 }
 
 double coarse_tree_cost(const CoarseTree& t, int applies, int root_inverse_max) {
-  // rates measured on the B200: batched DMMA factorization, the
-  // batched front sweeps, the dense root sweeps; launch latency per panel step
-  // (three kernels) and per level and apply (gather + two sweeps)
+  // rates measured on the B200 (round-2 depth sweeps on cfg3/cfg4):
+  // batched DMMA factorization, the batched front sweeps, the dense root
+  // sweeps; the dataflow Cholesky's pivot chain per 64-column step (~13 us,
+  // the levels run one after the other) and the latency of a level per apply
+  // (gather + two sweeps or two explicit GEMVs)
   for (const auto& L : t.levels)
     if (L.max_NF > 24576) return 1e30;  // the batched sweeps keep a front's vector in shared memory
   const double n = static_cast<double>(t.top.size());
   const bool inv = rup(std::max<int>(static_cast<int>(t.top.size()), 1)) <= root_inverse_max;
   double steps = std::ceil(n / kT) * (inv ? 2 : 1);
   for (const auto& L : t.levels) steps += L.max_PE / kT;
-  const double setup = t.flops / 20e12 + steps * 3 * 6e-6;
+  // per level: host planning and index uploads, the assemble / pad / copy
+  // launches and the start-up of one more batched factorization (measured
+  // 0.3-0.7 ms per extra level on cfg3/cfg4)
+  const double setup = t.flops / 20e12 + steps * 13e-6 + 0.4e-3 * static_cast<double>(t.levels.size());
   const double top_bytes = n * n * 8.0;
   // a level's two sweeps are a chain of 64-row block steps over few fronts:
-  // about 15 us per block step plus the gather (measured, cfg3-5)
+  // measured 26-35 us per level and apply on cfg3/cfg4 (3 to 7 block steps)
   double level_latency = 0;
-  for (const auto& L : t.levels) level_latency += 8e-6 + 15e-6 * (L.max_PE / kT);
+  for (const auto& L : t.levels) level_latency += 12e-6 + 6e-6 * (L.max_PE / kT);
   const double per_apply =
       (t.apply_bytes - top_bytes) / 3e12 + top_bytes / (inv ? 4e12 : 0.8e12) + level_latency;
   return setup + applies * per_apply;
