@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -214,6 +215,18 @@ struct HBuf {
   ~HBuf() {
     if (p) cudaFreeHost(p);
   }
+};
+
+/// NVTX range over a phase of the hot path (header-only NVTX 3: a no-op unless a
+/// profiler is attached).  ncu / nsys can filter on these names:
+/// "bddc:analysis", "bddc:eigen", "bddc:set_constraints", "bddc:pcg",
+/// "bddc:schur_apply", "bddc:precond_apply", "bddc:step".
+class NvtxRange {
+ public:
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 /// Host-side stage timer (printed with BDDC_B200_PROFILE=1).

@@ -1810,6 +1810,7 @@ void Engine::analysis() {
 }
 
 void Engine::analysis_launch() {
+  NvtxRange nvtx("bddc:analysis");
   prepare();
   DeviceState& D = *d_;
   const int na = D.n_own;
@@ -1874,6 +1875,12 @@ double Engine::pcg_bytes_per_iteration() const {
     }
   b += double(D.n_root) * D.n_root * 8.0;  // R^{-1} GEMV, or both triangular root sweeps
   b += D.tree_apply_bytes;                  // both sweeps of every primal tree front
+  // the W^c vectors of the apply ("about 6 * 8 * wc_dim"): here the
+  // leaf vectors [e | c] only, the interiors being eliminated -- restriction
+  // (write), forward sweep (read, write), backward sweep (read, write),
+  // prolongation (read)
+  if (D.NF.size() == std::size_t(D.nsub))
+    for (int s : D.own) b += 6.0 * 8.0 * (D.nE[s] + D.nC[s]);
   return b;
 }
 
@@ -1893,6 +1900,7 @@ double Engine::leaf_front_bytes() const {
 // set_constraints: change of variables, transformed leaf fronts, dense root
 // ---------------------------------------------------------------------------
 void Engine::set_constraints(const ConstraintSet& cs) {
+  NvtxRange nvtx("bddc:set_constraints");
   DeviceState& D = *d_;
   const Model& m = m_;
   const int ns = D.nsub;
@@ -2727,6 +2735,7 @@ void Engine::leaf_front(int s, std::vector<double>* out, std::vector<int>* pos, 
 }
 
 void Engine::schur_apply(const double* x, double* y) {
+  NvtxRange nvtx("bddc:schur_apply");
   DeviceState& D = *d_;
   ensure_vectors(D);
   const std::size_t bytes = D.niface * sizeof(double);
@@ -2739,6 +2748,7 @@ void Engine::schur_apply(const double* x, double* y) {
 }
 
 void Engine::precond_apply(const double* r, double* z) {
+  NvtxRange nvtx("bddc:precond_apply");
   DeviceState& D = *d_;
   if (!D.have_prec) throw Error(kError, "preconditioner not set up");
   ensure_vectors(D);
@@ -3036,6 +3046,7 @@ bool persistent_pcg(DeviceState& D) {
 }  // namespace
 
 PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool precond_residual) {
+  NvtxRange nvtx("bddc:pcg");
   DeviceState& D = *d_;
   if (!D.have_prec) throw Error(kError, "preconditioner not set up");
   ensure_vectors(D);
@@ -3233,6 +3244,7 @@ PcgOut Engine::pcg(const double* b, double* x, double tol, int max_it, bool prec
 }
 
 StepOut Engine::step(const StepSpec& sp, ConstraintSet& cs, double* u_free_host) {
+  NvtxRange nvtx("bddc:step");
   DeviceState& D = *d_;
   prepare();
   StepOut out;

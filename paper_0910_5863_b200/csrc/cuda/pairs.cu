@@ -318,7 +318,17 @@ __device__ __forceinline__ void syevx_mark(int i) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) {
+// Eigenvectors are formed only for the eigenvalues the selection enforces
+// (adaptive.cpp:60-88: the leading ones above tau, at most max_vectors; or
+// fixed_count; none for pair_indicator): `need` below, counted on the very
+// eigenvalues the host reads back, so both take the same decision.  The other
+// vector slots are written as zeros.
+struct EigSelect {
+  double tau;
+  int max_vectors, fixed_count, indicator_only;
+};
+
+__global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap, EigSelect sel) {
   const PairDev dd = pd[blockIdx.x];
   const int n = dd.nj, k = dd.k, N2 = 2 * dd.PJ, PJ = dd.PJ;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -499,8 +509,17 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
   }
   __syncthreads();
   syevx_mark(3);
+  int need = 0;
+  if (!sel.indicator_only) {
+    if (sel.fixed_count >= 0) {
+      need = min(sel.fixed_count, k);
+    } else {
+      while (need < k && fmax(lam[need], 0.0) > sel.tau) ++need;
+      need = min(need, sel.max_vectors);
+    }
+  }
   // 3. inverse iteration on T (thread m), scratch in global memory
-  if (tid < k) {
+  if (tid < need) {
     const int m = tid;
     double* work = wbase + (size_t)m * 6 * n;
     double* xd = work;           // U diagonal
@@ -580,7 +599,7 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
   syevx_mark(4);
   // modified Gram-Schmidt inside clusters (eigenvalues closer than 1e-7 ||T||)
   if (warp == 0) {
-    for (int m = 1; m < k; ++m) {
+    for (int m = 1; m < need; ++m) {
       int c0 = m;
       while (c0 > 0 && fabs(lam[c0 - 1] - lam[c0]) <= 1e-7 * tnorm) --c0;
       double* zm = Z + (size_t)m * n;
@@ -606,9 +625,9 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
   // 4. back-transformation y = H_0 ... H_{n-3} z: warp w carries vectors w and
   // w + 8 through the reflectors together (their reductions interleave), then
   // the vectors are written out with the solve padding zeroed
-  for (int m0 = warp; m0 < k; m0 += 16) {
+  for (int m0 = warp; m0 < need; m0 += 16) {
     const int m1 = m0 + 8;
-    const bool two = m1 < k;
+    const bool two = m1 < need;
     double* y0 = Z + (size_t)m0 * n;
     double* y1 = Z + (size_t)(two ? m1 : m0) * n;
     for (int kk = n - 3; kk >= 0; --kk) {
@@ -638,7 +657,7 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap) 
   __syncthreads();
   for (int e = tid; e < k * N2; e += blockDim.x) {
     const int m = e / N2, i = e % N2;
-    dd.vecs[e] = i < n ? Z[(size_t)m * n + i] : 0.0;
+    dd.vecs[e] = (m < need && i < n) ? Z[(size_t)m * n + i] : 0.0;
   }
   for (int m = tid; m < k; m += blockDim.x) dd.evals[m] = fmax(lam[m], 0.0);
   syevx_mark(6);
@@ -1062,6 +1081,7 @@ std::shared_ptr<PairPrep> PairEngine::prepare(const ConstraintSet& cs, const Enr
 }
 
 EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std::shared_ptr<PairPrep> prep) {
+  NvtxRange nvtx("bddc:eigen");
   using clk = std::chrono::steady_clock;
   const bool overlapped = prep != nullptr;
   if (!prep) prep = prepare(cs, o);
@@ -1333,7 +1353,8 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       const char* pe = std::getenv("BDDC_B200_PROFILE");
       const int tr_on = pe && *pe && *pe != '0';
       CK(cudaMemcpyToSymbolAsync(g_syevx_trace_on, &tr_on, sizeof(int), 0, cudaMemcpyHostToDevice, st_));
-      k_syevx<<<nb, 256, static_cast<int>(dyn * 8), st_>>>(dpd.p, static_cast<int>(dyn));
+      const EigSelect sel{o.tau, o.max_vectors, o.fixed_count, o.indicator_only ? 1 : 0};
+      k_syevx<<<nb, 256, static_cast<int>(dyn * 8), st_>>>(dpd.p, static_cast<int>(dyn), sel);
       if (tr_on) {
         unsigned long long t[8];
         CK(cudaMemcpyFromSymbolAsync(t, g_syevx_trace, sizeof(t), 0, cudaMemcpyDeviceToHost, st_));
