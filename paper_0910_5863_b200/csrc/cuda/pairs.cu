@@ -323,6 +323,9 @@ __device__ __forceinline__ void syevx_mark(int i) {
 // fixed_count; none for pair_indicator): `need` below, counted on the very
 // eigenvalues the host reads back, so both take the same decision.  The other
 // vector slots are written as zeros.
+constexpr int kSyevxVec = 16;     // work vectors of length n per CTA
+constexpr int kSyevxFusedMax = 288;  // one-pass tridiagonalization up to this order (nine 32-column groups per lane)
+
 struct EigSelect {
   double tau;
   int max_vectors, fixed_count, indicator_only;
@@ -334,14 +337,14 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap, 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   extern __shared__ double sm[];
   const size_t np = (size_t)n * (n + 1) / 2;
-  // shared-memory placement, most to least: packed L, the 6n vectors, the
-  // inverse-iteration scratch (6n per vector) and the vectors Z (n per vector)
+  // shared-memory placement, most to least: packed L, the 16n work vectors,
+  // the inverse-iteration scratch (6n per vector) and the vectors Z (n per vector)
   const long wk = 7L * n * (k > 0 ? k : 1);
-  const bool in_smem = (long)np + 6L * n + wk <= smem_cap;
-  const bool work_smem = in_smem || 6L * n + wk <= smem_cap;
+  const bool in_smem = (long)np + kSyevxVec * n + wk <= smem_cap;
+  const bool work_smem = in_smem || (long)kSyevxVec * n + wk <= smem_cap;
   double* L = in_smem ? sm : dd.A;  // packed lower
-  double* vec = in_smem ? sm + np : sm;  // v, p, d, e, tau, lam (6n)
-  double* wbase = work_smem ? vec + 6 * n : dd.A + (in_smem ? 0 : np);
+  double* vec = in_smem ? sm + np : sm;  // v, p, d, e, tau, lam, vp, wp, colpart[8] (16n)
+  double* wbase = work_smem ? vec + kSyevxVec * n : dd.A + (in_smem ? 0 : np);
   double* Z = wbase + (size_t)6 * n * k;  // k x n eigenvectors of T, then of C
   double* v = vec;
   double* p = vec + n;
@@ -357,116 +360,225 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap, 
     for (int c = tid; c <= r; c += blockDim.x) L[pk(r, c)] = dd.F4[(size_t)c * N2 + PJ + r];
   __syncthreads();
   syevx_mark(1);
-  // 1. tridiagonalization (dsytd2, lower)
-  for (int kk = 0; kk + 2 < n; ++kk) {
-    const int m0 = kk + 1;
-    double part = 0.0;
-    for (int i = m0 + tid; i < n; i += blockDim.x) {
-      const double x = L[pk(i, kk)];
-      part += x * x;
-    }
-    const double ss = block_sum(part, red);
-    const double x0 = L[pk(m0, kk)];
-    const double alpha = (x0 >= 0 ? -1.0 : 1.0) * sqrt(ss);
-    const double v0 = x0 - alpha;
-    const double vtv = ss - x0 * x0 + v0 * v0;
-    const double t = (ss > 0.0 && vtv > 0.0) ? 2.0 / vtv : 0.0;
-    for (int i = m0 + tid; i < n; i += blockDim.x) v[i] = (i == m0) ? v0 : L[pk(i, kk)];
-    if (tid == 0) {
-      dg[kk] = L[pk(kk, kk)];
-      eg[kk] = t != 0.0 ? alpha : x0;
-      tau[kk] = t;
-    }
-    __syncthreads();
-    if (t == 0.0) continue;
-    // p = t * A22 v.  Packed L in global memory: thread per row (sequential
-    // row reads stay in L1 lines).  In shared memory: thread (row, column
-    // group), four column groups reduced in a fixed order.
-    if (!in_smem) {
-      for (int r = m0 + tid; r < n; r += blockDim.x) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        const double* row = L + pk(r, 0);
-        int c = m0;
-        for (; c + 3 <= r; c += 4) {
-          s0 += row[c] * v[c];
-          s1 += row[c + 1] * v[c + 1];
-          s2 += row[c + 2] * v[c + 2];
-          s3 += row[c + 3] * v[c + 3];
+  // 1. tridiagonalization (dsytd2, lower).  One pass over the trailing matrix
+  // per Householder step: the rank-2 update of step kk-1 is applied while the
+  // product A v of step kk is formed from the updated entries (each element is
+  // read and written once per step; the two-pass form below reads it three
+  // times and writes it once).  Row r is owned by warp r mod 8, lanes over the
+  // columns: the row sums come from a warp reduction, the column sums (the
+  // symmetric half of the product) are kept per lane for its columns and the
+  // eight warps' parts are added in a fixed order.
+  if (n <= kSyevxFusedMax) {
+    double* vp = vec + 6 * n;   // pending update: A -= vp wp^T + wp vp^T on rows/cols >= kk
+    double* wp = vec + 7 * n;
+    double* colpart = vec + 8 * n;  // [8][n]
+    bool pending = false;
+    for (int kk = 0; kk + 2 < n; ++kk) {
+      const int m0 = kk + 1;
+      // (a) column kk with the pending update, its norm, the reflector
+      const double vpk = pending ? vp[kk] : 0.0, wpk = pending ? wp[kk] : 0.0;
+      double part = 0.0;
+      for (int i = kk + tid; i < n; i += blockDim.x) {
+        double a = L[pk(i, kk)];
+        if (pending) a -= vp[i] * wpk + wp[i] * vpk;
+        v[i] = a;  // v[kk] = the diagonal entry, v[m0..] = x
+        if (i >= m0) part += a * a;
+      }
+      const double ss = block_sum(part, red);  // barriers: v is complete afterwards
+      const double x0 = v[m0];
+      const double alpha = (x0 >= 0 ? -1.0 : 1.0) * sqrt(ss);
+      const double v0 = x0 - alpha;
+      const double vtv = ss - x0 * x0 + v0 * v0;
+      const double t = (ss > 0.0 && vtv > 0.0) ? 2.0 / vtv : 0.0;
+      __syncthreads();  // every thread has read v[m0]
+      if (tid == 0) {
+        dg[kk] = v[kk];
+        eg[kk] = t != 0.0 ? alpha : x0;
+        tau[kk] = t;
+        v[m0] = t != 0.0 ? v0 : 0.0;
+      }
+      if (t == 0.0)  // no reflector: v = 0, the pass below only applies the pending update
+        for (int i = m0 + 1 + tid; i < n; i += blockDim.x) v[i] = 0.0;
+      __syncthreads();
+      // (b) one pass: update, store, row and column sums of A v
+      {
+        double cacc[kSyevxFusedMax / 32];
+#pragma unroll
+        for (int q = 0; q < kSyevxFusedMax / 32; ++q) cacc[q] = 0.0;
+        for (int r = m0 + warp; r < n; r += 8) {
+          double* row = L + pk(r, 0);
+          const double vr = v[r], vpr = pending ? vp[r] : 0.0, wpr = pending ? wp[r] : 0.0;
+          double racc = 0.0;
+#pragma unroll
+          for (int q = 0; q < kSyevxFusedMax / 32; ++q) {
+            const int c = m0 + lane + 32 * q;
+            if (c <= r) {
+              double a = row[c];
+              if (pending) {
+                a -= vpr * wp[c] + wpr * vp[c];
+                row[c] = a;
+              }
+              racc += a * v[c];
+              if (c < r) cacc[q] += a * vr;
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, o);
+          if (lane == 0) p[r] = racc;
         }
-        for (; c <= r; ++c) s0 += row[c] * v[c];
-        // column r below the diagonal: the warp walks the rows c2 together, so
-        // its 32 lanes read 32 consecutive entries of packed row c2 (coalesced)
-        const int base = r - (tid & 31);
-        int c2 = base + 1;
-        for (; c2 + 3 < n; c2 += 4) {
-          const double* q = L + pk(c2, 0);
-          const double a0 = c2 > r ? q[r] : 0.0;
-          const double a1 = c2 + 1 > r ? q[c2 + 1 + r] : 0.0;
-          const double a2 = c2 + 2 > r ? q[2 * c2 + 3 + r] : 0.0;
-          const double a3 = c2 + 3 > r ? q[3 * c2 + 6 + r] : 0.0;
-          s1 += a0 * v[c2];
-          s2 += a1 * v[c2 + 1];
-          s3 += a2 * v[c2 + 2];
-          s0 += a3 * v[c2 + 3];
+#pragma unroll
+        for (int q = 0; q < kSyevxFusedMax / 32; ++q) {
+          const int c = m0 + lane + 32 * q;
+          if (c < n) colpart[warp * n + c] = cacc[q];
         }
-        for (; c2 < n; ++c2)
-          if (c2 > r) s1 += L[pk(c2, r)] * v[c2];
-        p[r] = t * ((s0 + s1) + (s2 + s3));
       }
       __syncthreads();
-    } else {
-      const int g = tid >> 6;
-      for (int r0 = m0; r0 < n; r0 += 64) {
-        const int r = r0 + (tid & 63);
-        double s0 = 0.0, s1 = 0.0;
-        if (r < n) {
-          int c = m0 + g;
-          for (; c + 4 < n; c += 8) {
-            s0 += L[c <= r ? pk(r, c) : pk(c, r)] * v[c];
-            s1 += L[c + 4 <= r ? pk(r, c + 4) : pk(c + 4, r)] * v[c + 4];
+      double pv = 0.0;
+      for (int i = m0 + tid; i < n; i += blockDim.x) {
+        double sacc = p[i];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sacc += colpart[w * n + i];
+        sacc *= t;
+        p[i] = sacc;
+        pv += sacc * v[i];
+      }
+      const double K = 0.5 * t * block_sum(pv, red);
+      // (c) w = p - K v becomes the pending update; the reflector replaces the column
+      for (int i = m0 + tid; i < n; i += blockDim.x) {
+        const double vi = v[i];
+        wp[i] = p[i] - K * vi;
+        vp[i] = vi;
+        if (t != 0.0) L[pk(i, kk)] = vi;
+      }
+      pending = true;
+      __syncthreads();
+    }
+    if (tid == 0) {  // the last 2x2 block (1x1 when n == 1) with the pending update
+      const int a0 = n >= 2 ? n - 2 : 0;
+      for (int i = a0; i < n; ++i) {
+        double d = L[pk(i, i)];
+        if (pending) d -= 2.0 * vp[i] * wp[i];
+        dg[i] = d;
+        tau[i] = 0.0;
+      }
+      if (n >= 2) {
+        double e = L[pk(n - 1, n - 2)];
+        if (pending) e -= vp[n - 1] * wp[n - 2] + wp[n - 1] * vp[n - 2];
+        eg[n - 2] = e;
+      }
+    }
+  } else {
+    // 1. tridiagonalization (dsytd2, lower)
+    for (int kk = 0; kk + 2 < n; ++kk) {
+      const int m0 = kk + 1;
+      double part = 0.0;
+      for (int i = m0 + tid; i < n; i += blockDim.x) {
+        const double x = L[pk(i, kk)];
+        part += x * x;
+      }
+      const double ss = block_sum(part, red);
+      const double x0 = L[pk(m0, kk)];
+      const double alpha = (x0 >= 0 ? -1.0 : 1.0) * sqrt(ss);
+      const double v0 = x0 - alpha;
+      const double vtv = ss - x0 * x0 + v0 * v0;
+      const double t = (ss > 0.0 && vtv > 0.0) ? 2.0 / vtv : 0.0;
+      for (int i = m0 + tid; i < n; i += blockDim.x) v[i] = (i == m0) ? v0 : L[pk(i, kk)];
+      if (tid == 0) {
+        dg[kk] = L[pk(kk, kk)];
+        eg[kk] = t != 0.0 ? alpha : x0;
+        tau[kk] = t;
+      }
+      __syncthreads();
+      if (t == 0.0) continue;
+      // p = t * A22 v.  Packed L in global memory: thread per row (sequential
+      // row reads stay in L1 lines).  In shared memory: thread (row, column
+      // group), four column groups reduced in a fixed order.
+      if (!in_smem) {
+        for (int r = m0 + tid; r < n; r += blockDim.x) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+          const double* row = L + pk(r, 0);
+          int c = m0;
+          for (; c + 3 <= r; c += 4) {
+            s0 += row[c] * v[c];
+            s1 += row[c + 1] * v[c + 1];
+            s2 += row[c + 2] * v[c + 2];
+            s3 += row[c + 3] * v[c + 3];
           }
-          if (c < n) s0 += L[c <= r ? pk(r, c) : pk(c, r)] * v[c];
+          for (; c <= r; ++c) s0 += row[c] * v[c];
+          // column r below the diagonal: the warp walks the rows c2 together, so
+          // its 32 lanes read 32 consecutive entries of packed row c2 (coalesced)
+          const int base = r - (tid & 31);
+          int c2 = base + 1;
+          for (; c2 + 3 < n; c2 += 4) {
+            const double* q = L + pk(c2, 0);
+            const double a0 = c2 > r ? q[r] : 0.0;
+            const double a1 = c2 + 1 > r ? q[c2 + 1 + r] : 0.0;
+            const double a2 = c2 + 2 > r ? q[2 * c2 + 3 + r] : 0.0;
+            const double a3 = c2 + 3 > r ? q[3 * c2 + 6 + r] : 0.0;
+            s1 += a0 * v[c2];
+            s2 += a1 * v[c2 + 1];
+            s3 += a2 * v[c2 + 2];
+            s0 += a3 * v[c2 + 3];
+          }
+          for (; c2 < n; ++c2)
+            if (c2 > r) s1 += L[pk(c2, r)] * v[c2];
+          p[r] = t * ((s0 + s1) + (s2 + s3));
         }
-        pg[g * 64 + (tid & 63)] = s0 + s1;
         __syncthreads();
-        if (tid < 64 && r < n) p[r] = t * ((pg[tid] + pg[64 + tid]) + (pg[128 + tid] + pg[192 + tid]));
-        __syncthreads();
-      }
-    }
-    double pv = 0.0;
-    for (int i = m0 + tid; i < n; i += blockDim.x) pv += p[i] * v[i];
-    const double K = 0.5 * t * block_sum(pv, red);
-    for (int i = m0 + tid; i < n; i += blockDim.x) p[i] -= K * v[i];  // p becomes w
-    __syncthreads();
-    // rank-2 update of the trailing lower triangle: warp per row, lanes over columns
-    for (int r = m0 + warp; r < n; r += 8) {
-      double* row = L + pk(r, 0);
-      const double vr = v[r], wr = p[r];
-      for (int c = m0 + lane; c <= r; c += 128) {  // four independent elements in flight
-        double x[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (c + 32 * q <= r) x[q] = row[c + 32 * q];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int cc = c + 32 * q;
-          if (cc <= r) row[cc] = x[q] - (vr * p[cc] + wr * v[cc]);
+      } else {
+        const int g = tid >> 6;
+        for (int r0 = m0; r0 < n; r0 += 64) {
+          const int r = r0 + (tid & 63);
+          double s0 = 0.0, s1 = 0.0;
+          if (r < n) {
+            int c = m0 + g;
+            for (; c + 4 < n; c += 8) {
+              s0 += L[c <= r ? pk(r, c) : pk(c, r)] * v[c];
+              s1 += L[c + 4 <= r ? pk(r, c + 4) : pk(c + 4, r)] * v[c + 4];
+            }
+            if (c < n) s0 += L[c <= r ? pk(r, c) : pk(c, r)] * v[c];
+          }
+          pg[g * 64 + (tid & 63)] = s0 + s1;
+          __syncthreads();
+          if (tid < 64 && r < n) p[r] = t * ((pg[tid] + pg[64 + tid]) + (pg[128 + tid] + pg[192 + tid]));
+          __syncthreads();
         }
       }
+      double pv = 0.0;
+      for (int i = m0 + tid; i < n; i += blockDim.x) pv += p[i] * v[i];
+      const double K = 0.5 * t * block_sum(pv, red);
+      for (int i = m0 + tid; i < n; i += blockDim.x) p[i] -= K * v[i];  // p becomes w
+      __syncthreads();
+      // rank-2 update of the trailing lower triangle: warp per row, lanes over columns
+      for (int r = m0 + warp; r < n; r += 8) {
+        double* row = L + pk(r, 0);
+        const double vr = v[r], wr = p[r];
+        for (int c = m0 + lane; c <= r; c += 128) {  // four independent elements in flight
+          double x[4];
+  #pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c + 32 * q <= r) x[q] = row[c + 32 * q];
+  #pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int cc = c + 32 * q;
+            if (cc <= r) row[cc] = x[q] - (vr * p[cc] + wr * v[cc]);
+          }
+        }
+      }
+      __syncthreads();
+      // keep the reflector in the eliminated column (for the back-transformation)
+      for (int i = m0 + tid; i < n; i += blockDim.x) L[pk(i, kk)] = v[i];
+      __syncthreads();
     }
-    __syncthreads();
-    // keep the reflector in the eliminated column (for the back-transformation)
-    for (int i = m0 + tid; i < n; i += blockDim.x) L[pk(i, kk)] = v[i];
-    __syncthreads();
-  }
-  if (tid == 0) {
-    if (n >= 2) {
-      dg[n - 2] = L[pk(n - 2, n - 2)];
-      eg[n - 2] = L[pk(n - 1, n - 2)];
-      tau[n - 2] = 0.0;
+    if (tid == 0) {
+      if (n >= 2) {
+        dg[n - 2] = L[pk(n - 2, n - 2)];
+        eg[n - 2] = L[pk(n - 1, n - 2)];
+        tau[n - 2] = 0.0;
+      }
+      dg[n - 1] = L[pk(n - 1, n - 1)];
+      tau[n - 1] = 0.0;
     }
-    dg[n - 1] = L[pk(n - 1, n - 1)];
-    tau[n - 1] = 0.0;
   }
   __syncthreads();
   syevx_mark(2);
@@ -1337,15 +1449,15 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     // (j) top-k eigenpairs of C
     {
       const int maxn = maxn2;  // >= every nj
-      const long need = (long)maxn * (maxn + 1) / 2 + 6L * maxn + 7L * maxn * std::max(maxk, 1);
+      const long need = (long)maxn * (maxn + 1) / 2 + (long)kSyevxVec * maxn + 7L * maxn * std::max(maxk, 1);
       const long cap = (220 * 1024) / 8;  // leaves room for the kernel's static arrays
       // shared memory holds one CTA per SM here; with more pairs than SMs the
       // global-memory placement (about four CTAs per SM) takes fewer waves
       bool smem_ok = need <= cap && nb <= sm_count();
       if (const char* e = std::getenv("BDDC_B200_SYEVX"); e && *e) smem_ok = *e == 'S' && need <= cap;
-      // all in shared memory when it fits; otherwise only the 6n vectors, so that
+      // all in shared memory when it fits; otherwise only the 16n work vectors, so that
       // several CTAs share an SM and hide the L2 latency of the packed matrix
-      const long dyn = smem_ok ? need : 6L * maxn;
+      const long dyn = smem_ok ? need : (long)kSyevxVec * maxn;
       CK(static_cast<cudaError_t>(per_device(reinterpret_cast<const void*>(&k_syevx), [] {
         return static_cast<int>(cudaFuncSetAttribute(k_syevx, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                       224 * 1024));

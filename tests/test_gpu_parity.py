@@ -460,3 +460,38 @@ def test_wc_entry_points(name, lattice, epe, phys, ophys, mode, leaf, monkeypatc
         z = b.prolong(b.coarse_solve(b.restrict_residual(r)))
         assert rel(z, b.precond_apply(r)) <= 1e-12
         assert rel(z, prec.apply(r)) <= 1e-10
+
+
+REPEAT = [("cfg2 (chunked k_chol_dag, persistent PCG)", lambda: pb.BDDC(config=2), "adaptive", 10.0, 10, False, {}),
+          ("cfg4 3x3x3 H/h=4 plain k_chol_dag, dataflow sweeps, primal tree, graph PCG",
+           lambda: pb.BDDC(config=4, subdomains=(3, 3, 3), elements_per_edge=4), "adaptive", 10.0, 15, True,
+           {"BDDC_B200_DAGW": "0", "BDDC_B200_LEAF": "factor", "BDDC_B200_ROOT_DEPTH": "1",
+            "BDDC_B200_PCG": "graph"})]
+
+
+@pytest.mark.parametrize("name,make,mode,tau,maxv,base_faces,env", REPEAT, ids=["cfg2", "cfg4-3x3x3-plain"])
+def test_repeated_steps_are_bitwise_identical(name, make, mode, tau, maxv, base_faces, env, monkeypatch):
+    """Race evidence without compute-sanitizer (closed on this pool,
+    profiles/r02_sanitize_*.log): every dataflow kernel (k_chol_dag's tile
+    queue, the sweeps' progress counters, k_pcg_persistent's grid barriers,
+    k_syevx) forms its sums in a fixed order, so a step is a deterministic
+    function of its input.  A missing acquire/release or barrier shows up as
+    run-to-run differences: six full steps (fresh and reused handles) must
+    give bit-identical CG coefficients, eigenvalues and solutions."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    runs = []
+    b = make()
+    n_free = b.structure()["free_dofs"]
+    for rep in range(6):
+        if rep == 3:
+            b = make()  # a fresh handle: different allocations, same bits
+        u = np.empty(n_free)
+        out = b.step(mode, tau, maxv, base_faces=base_faces, e2e=True, u_free=u)
+        g = b.pcg()
+        ev = np.concatenate([r["eigenvalues"] for r in b.pair_reports()])
+        runs.append((out["iterations"], out["kappa"], g["alphas"], g["betas"], g["x"], ev, u.copy()))
+    for r in runs[1:]:
+        assert r[0] == runs[0][0] and r[1] == runs[0][1]
+        for a, c in zip(r[2:], runs[0][2:]):
+            assert np.array_equal(a, c)
