@@ -111,3 +111,47 @@ def test_pcg_and_solution(run):
     e = g["x"] - fx["pcg_x"]
     err2 = float(e @ b.schur_apply(e))
     assert math.sqrt(max(err2, 0.0) / float(fx["pcg_energy"])) <= 1e-8
+
+
+def test_cfg5_sampled_pairs():
+    """cfg5 at full size (2.71M dofs, 4752 pairs): the oracle's reports of a
+    deterministic sample of pairs (tests/golden/make_sampled.py: Dirichlet-
+    adjacent, outer-boundary and floating interior pairs on x-, y- and z-normal
+    faces; every pair is independent of the others, adaptive.cpp:133) against
+    the device's full selection -- enforced count, saturation, omega_next and
+    eigenvalues at 1e-6, and the span of the averages installed on the pair's
+    face glob."""
+    path = GOLDEN / "sampled_cfg5.npz"
+    if not path.exists():
+        pytest.skip("no sampled fixture")
+    from fullsize_sketch import sketch
+    fx = dict(np.load(path))
+    b = pb.BDDC(config=5)
+    mode, tau, maxv, bf = MODES[5]
+    b.run_item(mode, tau, maxv, base_faces=bf)
+    reps = b.pair_reports()
+    by_glob = {}
+    for g, w in b.constraints():
+        by_glob.setdefault(g, []).append(w)
+    base = pb.BDDC(config=5)
+    base.arithmetic_constraints(True, bf)
+    n_base = {}
+    for g, _ in base.constraints():
+        n_base[g] = n_base.get(g, 0) + 1
+    for q, k in enumerate(fx["pair_index"]):
+        r = reps[int(k)]
+        assert (r["si"], r["sj"]) == (int(fx["si"][q]), int(fx["sj"][q]))
+        assert r["enforced"] == int(fx["enforced"][q]), (r["si"], r["sj"], r["enforced"], int(fx["enforced"][q]))
+        assert bool(r["saturated"]) == bool(fx["saturated"][q])
+        assert abs(r["omega_next"] - fx["omega_next"][q]) <= 1e-6 * max(fx["omega_next"][q], 1e-12)
+        e0 = fx["eigenvalues"][q, :fx["n_eig"][q]]
+        assert len(r["eigenvalues"]) == len(e0)
+        big = e0 > 1e-6 * max(e0.max(initial=0.0), 1e-300)
+        assert np.all(np.abs(r["eigenvalues"][big] - e0[big]) <= 1e-6 * e0[big])
+        g = int(fx["face_glob"][q])
+        if g >= 0:
+            rows = by_glob[g][n_base.get(g, 0):]
+            assert len(rows) == int(fx["kept"][q])
+            assert np.max(np.abs(sketch(g, np.stack(rows)) - fx["sketch"][q])) <= 1e-6
+        else:
+            assert int(fx["kept"][q]) == 0
