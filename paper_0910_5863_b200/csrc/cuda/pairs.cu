@@ -58,8 +58,8 @@ struct PairDev {
   double* H;            // nf x nj scratch
   const double* N;      // nm x (nc + nf) row-major, orthonormal
   const double* rho;    // nf
-  double* A;            // Jacobi matrix (n2 x n2), n2 = even(nj)
-  double* V;            // Jacobi vectors
+  double* A;            // eigensolver workspace (packed matrix + scratch when not in shared memory)
+  int* need;            // eigenvectors formed by k_syevx (the enforced count): the rest are zeros
   double* evals;        // k
   double* vecs;         // 2PJ x k (solve vectors, column m at m*2PJ)
   double* func;         // nf x k
@@ -98,6 +98,7 @@ struct PairBuffers {
   DBuf<PairDev> dpd;
   DBuf<FrontDesc> dG, dQ, d3, d4;
   DBuf<SolveDesc> dsv;
+  DBuf<int> svoff, need;  // first descriptor of each pair in dsv; eigenvectors formed per pair
   UploadBatch up_index, up_desc;  // per chunk: index arrays, then descriptors (one copy each)
 };
 
@@ -630,6 +631,7 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap, 
       need = min(need, sel.max_vectors);
     }
   }
+  if (tid == 0) *dd.need = need;
   // 3. inverse iteration on T (thread m), scratch in global memory
   if (tid < need) {
     const int m = tid;
@@ -775,12 +777,22 @@ __global__ void __launch_bounds__(256) k_syevx(const PairDev* pd, int smem_cap, 
   syevx_mark(6);
 }
 
+// The back-substitution sweeps of the vectors k_syevx did not form (zeros) are
+// switched off: their descriptors get n = p = 0, so their tasks are empty.
+__global__ void k_trim_solves(const PairDev* pd, const int* __restrict__ svoff, SolveDesc* sv) {
+  const PairDev& d = pd[blockIdx.x];
+  for (int m = *d.need + threadIdx.x; m < d.k; m += blockDim.x) {
+    sv[svoff[blockIdx.x] + m].n = 0;
+    sv[svoff[blockIdx.x] + m].p = 0;
+  }
+}
+
 // (l) functional a_m = 1/2 M K alpha_m (alpha = first nj entries of vecs after the back solve)
 __global__ void k_functional(const PairDev* pd) {
   const PairDev d = pd[blockIdx.y];
   const int nf = d.nf, nj = d.nj, N2 = 2 * d.PJ;
   const int m = blockIdx.x;
-  if (m >= d.k) return;
+  if (m >= d.k || m >= *d.need) return;  // zero vectors beyond the enforced count: never read
   const double* al = d.vecs + (size_t)m * N2;
   for (int t = threadIdx.x; t < nf; t += blockDim.x) {
     double s = 0.0;
@@ -1332,6 +1344,8 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     B_.up_index.flush(st_);
     info.alloc(4 * nb);
     CK(cudaMemsetAsync(info.p, 0, 4 * nb * sizeof(int), st_));
+    B_.need.alloc(nb);
+    CK(cudaMemsetAsync(B_.need.p, 0, nb * sizeof(int), st_));
     ht.mark("alloc_upload");
     std::vector<FrontDesc> fG(2 * nb), fQ(nb), f3(nb), f4(nb);
     int maxNG = 0, maxPO = 0, maxM1 = 0, maxNQ = 0, maxPQ = 0, maxPJ = 0, maxk = 0, maxnf = 0, maxn2 = 0;
@@ -1373,7 +1387,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       d.rho = R.p + oR[b];
       const int n2 = dm.nj + (dm.nj & 1);
       d.A = A.p + oA[b];
-      d.V = A.p + oA[b] + (long long)n2 * n2;
+      d.need = B_.need.p + b;
       d.evals = E.p + oE[b];
       d.vecs = W.p + oW[b];
       d.func = Fu.p + oFu[b];
@@ -1411,11 +1425,15 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       }
     B_.up_desc.add(B_.gside, gs);
     std::vector<SolveDesc> sv;
-    for (int b = 0; b < nb; ++b)
+    std::vector<int> svoff(nb);
+    for (int b = 0; b < nb; ++b) {
+      svoff[b] = static_cast<int>(sv.size());
       for (int mm = 0; mm < dims[b].k; ++mm)
         sv.push_back(SolveDesc{pd[b].F3, Dv.p + oD3[b], pd[b].vecs + (size_t)mm * 2 * dims[b].PJ, 2 * dims[b].PJ,
                                dims[b].PJ, nullptr, nullptr});
+    }
     B_.up_desc.add(B_.dsv, sv);
+    B_.up_desc.add(B_.svoff, svoff);
     B_.up_desc.flush(st_);
     ht.mark("descriptors");
     StageProfiler prof("enrich", st_);
@@ -1481,9 +1499,10 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     CK(cudaGetLastError());
     // (k) alpha = L^{-T} y via F3's factor; (l) functionals
     auto& dsv = B_.dsv;
+    k_trim_solves<<<nb, 32, 0, st_>>>(dpd.p, B_.svoff.p, dsv.p);
     front_backward(dsv.p, static_cast<int>(sv.size()), 2 * maxPJ, st_);
     k_functional<<<dim3(std::max(maxk, 1), nb), 128, 0, st_>>>(dpd.p);
-    count_launch(9);
+    count_launch(10);
     CK(cudaGetLastError());
     prof.mark("vectors");
     ht.mark("launch");
