@@ -54,14 +54,13 @@ __device__ __forceinline__ bool warp_active(int vm, int vn) {
   const int warp = (threadIdx.x >> 5) & 3;
   return vm > (warp & 1) * 32 && vn > (warp >> 1) * 32;
 }
-__device__ __forceinline__ void warp_mma(const double* As, const double* Bs, int kdim,
-                                         double (&acc)[2][4][4], bool active = true) {
-  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) & 3;
+// The 32x32 quadrant at (m0, n0) over the K steps [k0, k1) (multiples of 16).
+__device__ __forceinline__ void warp_mma_at(const double* As, const double* Bs, int k0, int k1,
+                                            double (&acc)[2][4][4], int m0, int n0) {
+  const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t0 = lane & 3;
-  const int m0 = (warp & 1) * 32, n0 = (warp >> 1) * 32;
-  if (!active) return;
 #pragma unroll 2
-  for (int kk = 0; kk < kdim; kk += 16) {
+  for (int kk = k0; kk < k1; kk += 16) {
     double a[2][8], b[4][4];
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
@@ -77,6 +76,12 @@ __device__ __forceinline__ void warp_mma(const double* As, const double* Bs, int
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
   }
+}
+__device__ __forceinline__ void warp_mma(const double* As, const double* Bs, int kdim,
+                                         double (&acc)[2][4][4], bool active = true) {
+  const int warp = (threadIdx.x >> 5) & 3;
+  if (!active) return;
+  warp_mma_at(As, Bs, 0, kdim, acc, (warp & 1) * 32, (warp >> 1) * 32);
 }
 
 // Visit the accumulator elements with their tile coordinates.
@@ -548,7 +553,25 @@ __device__ void dag_accumulate(const double* a, int ld, int i0, int j0, int kb, 
   ke = min(ke, (kv + 15) & ~15);
   const int nch = (ke - kb + KC - 1) / KC;
   if (nch <= 0 || vm <= 0 || vn <= 0) return;
-  const bool active = warp_active(vm, vn);
+  // Warp roles.  Inside a front warp w owns quadrant (w & 1, w >> 1).  In an
+  // edge tile whose lower (right) half is padding the two warps of that half
+  // would idle while the other two set the tile's time: they take the second
+  // half of every K chunk of their neighbour's quadrant instead, and the two
+  // partial sums are added through shared memory at the end (fixed order).
+  const int warp = (threadIdx.x >> 5) & 3;
+  int wm = warp & 1, wn = warp >> 1, khalf = 0;
+  bool split = false, active = true;
+  if (vm <= 32 && vn > 32) {
+    split = true;
+    khalf = wm;
+    wm = 0;
+  } else if (vn <= 32 && vm > 32) {
+    split = true;
+    khalf = wn;
+    wn = 0;
+  } else {
+    active = warp_active(vm, vn);
+  }
   int ready = 0;  // column blocks [0, ready) final for both rows (uniform over the CTA)
   auto blk = [&](int c) { return (kb + c * KC) >> 6; };
   auto poll = [&](int need, bool block) {
@@ -590,12 +613,45 @@ __device__ void dag_accumulate(const double* a, int ld, int i0, int j0, int kb, 
       cp_async_wait<0>();
     }
     __syncthreads();
-    warp_mma(As + (c & 1) * KC * LDS, Bs + (c & 1) * KC * LDS, min(KC, ke - kb - c * KC), acc, active);
+    {
+      const int kdim = min(KC, ke - kb - c * KC);
+      const double* Ac = As + (c & 1) * KC * LDS;
+      const double* Bc = Bs + (c & 1) * KC * LDS;
+      if (split)
+        warp_mma_at(Ac, Bc, khalf ? 16 : 0, khalf ? kdim : min(kdim, 16), acc, wm * 32, wn * 32);
+      else if (active)
+        warp_mma_at(Ac, Bc, 0, kdim, acc, wm * 32, wn * 32);
+    }
     __syncthreads();
     if (c + 1 < nch && !pf) {
       poll(blk(c + 1), true);
       load(c + 1, (c + 1) & 1);
     }
+  }
+  if (split) {  // helpers hand their partial sums to the quadrant's owner and clear their own (padding) quadrant
+    const int lane = threadIdx.x & 31;
+    double* xch = smem + ((vm <= 32 ? wn : wm) * 32 + lane);  // [32 values][2 owners x 32 lanes]
+    if (khalf) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            xch[((mi * 4 + ni) * 4 + v) * 64] = acc[mi][ni][v];
+            acc[mi][ni][v] = 0.0;
+          }
+    }
+    __syncthreads();
+    if (!khalf) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[mi][ni][v] += xch[((mi * 4 + ni) * 4 + v) * 64];
+    }
+    __syncthreads();  // the operand buffers are free for the caller again
   }
 }
 
