@@ -75,65 +75,59 @@ __global__ void k_front_maps(const AsmDesc* ds) {
   }
 }
 
-// Dense leaf fronts (assemble.cpp:202-258): one thread per entry of the
-// block-lower triangle (tiles (a, b), a >= b, the diagonal tiles in full) --
-// the only part of a leaf front the factorization and the sweeps read.  Every
-// such entry is written (stiffness value, 0, or 1 on a padding diagonal), so
-// the arena needs no memset.  A stiffness entry is the sum over the elements
-// holding both nodes in the host's element order (k, j, i) of the reference
-// element matrix entry times the element scale, multiply and add rounded
-// separately: the front equals the host CSR bitwise.
-__global__ void __launch_bounds__(256) k_assemble_dense(const AsmDesc* ds, AsmMesh mm) {
+// Dense leaf fronts (assemble.cpp:202-258) in two passes over the block-lower
+// triangle (tiles (a, b), a >= b, the diagonal tiles in full) -- the only part
+// of a leaf front the factorization and the sweeps read:
+//   k_zero_fronts      streams zeros (16-byte stores; 1 on a padding diagonal),
+//   k_assemble_sparse  writes the stiffness entries, one thread per (row dof,
+//                      neighbour node, component): at most 27 nc per row.
+// A stiffness entry is the sum over the elements holding both nodes in the
+// host's element order (k, j, i) of the reference element matrix entry times
+// the element scale, multiply and add rounded separately: the front equals the
+// host CSR bitwise.  (One thread per dense entry, the round-1 kernel, spent its
+// time deciding that 98% of the entries are zero: 2.35 ms on cfg3.)
+__global__ void __launch_bounds__(256) k_zero_fronts(const AsmDesc* ds) {
+  const AsmDesc d = ds[blockIdx.y];
+  for (int col = blockIdx.x; col < d.ld; col += gridDim.x) {
+    const int r0 = col & ~63;
+    const bool pad = d.ipos[col] < 0;
+    double2* out = reinterpret_cast<double2*>(d.a + (size_t)col * d.ld);
+    for (int r = r0 + 2 * threadIdx.x; r < d.ld; r += 2 * blockDim.x)
+      out[r >> 1] = make_double2(pad && r == col ? 1.0 : 0.0, pad && r + 1 == col ? 1.0 : 0.0);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_assemble_sparse(const AsmDesc* ds, AsmMesh mm) {
   const AsmDesc d = ds[blockIdx.y];
   const int nc = mm.nc, ln = mm.epe + 1, ed = 8 * nc;
-  const long nt = d.ld / 64;
-  const long ntile = nt * (nt + 1) / 2;
   const int vtx[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // (dx + 2 dy + 4 dz) -> VTK vertex
-  // per tile: local dof and (i, j, k, component) of its 64 rows and 64 columns
-  __shared__ int dof_s[2][64];
-  __shared__ int4 crd_s[2][64];
-  for (long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
-    int ta = static_cast<int>((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
-    while ((long)ta * (ta + 1) / 2 > tile) --ta;
-    while ((long)(ta + 1) * (ta + 2) / 2 <= tile) ++ta;
-    const int tb = static_cast<int>(tile - (long)ta * (ta + 1) / 2);
-    if (threadIdx.x < 128) {
-      const int w = threadIdx.x >> 6, idx = threadIdx.x & 63;
-      const int l = d.ipos[(w ? tb : ta) * 64 + idx];
-      dof_s[w][idx] = l;
-      if (l >= 0) {
-        const int g = d.dofq[l], q = g / nc;
-        crd_s[w][idx] = make_int4(q % ln, (q / ln) % ln, q / (ln * ln), g % nc);
-      }
-    }
-    __syncthreads();
-    double* out = d.a + (size_t)(tb * 64) * d.ld + ta * 64;
-    for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
-      const int i = e & 63, j = e >> 6;
-      const int dr = dof_s[0][i], dc = dof_s[1][j];
-      double s = 0.0;
-      if (dr < 0 || dc < 0) {
-        s = (ta == tb && i == j) ? 1.0 : 0.0;
-      } else {
-        const int4 a = crd_s[0][i], b = crd_s[1][j];
-        if (abs(a.x - b.x) <= 1 && abs(a.y - b.y) <= 1 && abs(a.z - b.z) <= 1) {
-          const bool lo = dr <= dc;
-          const int4 P = lo ? a : b, Q = lo ? b : a;
-          for (int ek = max(max(P.z, Q.z) - 1, 0); ek <= min(min(P.z, Q.z), mm.epe - 1); ++ek)
-            for (int ej = max(max(P.y, Q.y) - 1, 0); ej <= min(min(P.y, Q.y), mm.epe - 1); ++ej)
-              for (int ei = max(max(P.x, Q.x) - 1, 0); ei <= min(min(P.x, Q.x), mm.epe - 1); ++ei) {
-                const int el = ((d.k0 + ek) * mm.ne1 + d.j0 + ej) * mm.ne0 + d.i0 + ei;
-                const int va = vtx[(P.x - ei) + 2 * (P.y - ej) + 4 * (P.z - ek)];
-                const int vb = vtx[(Q.x - ei) + 2 * (Q.y - ej) + 4 * (Q.z - ek)];
-                const double kv = mm.ke[(size_t)mm.eke[el] * ed * ed + (va * nc + P.w) * ed + vb * nc + Q.w];
-                const double sc = mm.escale ? mm.escale[el] : 1.0;
-                s = __dadd_rn(s, sc == 1.0 ? kv : __dmul_rn(sc, kv));
-              }
+  const int per = 27 * nc;
+  const long total = (long)d.dim * per;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
+    const int dr = static_cast<int>(t / per), rest = static_cast<int>(t % per);
+    const int nbr = rest / nc, cb = rest % nc;
+    const int g = d.dofq[dr], q = g / nc;
+    const int4 a = make_int4(q % ln, (q / ln) % ln, q / (ln * ln), g % nc);
+    const int4 b = make_int4(a.x + nbr % 3 - 1, a.y + (nbr / 3) % 3 - 1, a.z + nbr / 9 - 1, cb);
+    if (b.x < 0 || b.y < 0 || b.z < 0 || b.x >= ln || b.y >= ln || b.z >= ln) continue;
+    const int dc = d.lnode[((b.z * ln + b.y) * ln + b.x) * nc + cb];
+    if (dc < 0) continue;
+    const int pr = d.pos[dr], pc = d.pos[dc];
+    if ((pr >> 6) < (pc >> 6)) continue;  // strictly upper tile: never read
+    const bool lo = dr <= dc;
+    const int4 P = lo ? a : b, Q = lo ? b : a;
+    double s = 0.0;
+    for (int ek = max(max(P.z, Q.z) - 1, 0); ek <= min(min(P.z, Q.z), mm.epe - 1); ++ek)
+      for (int ej = max(max(P.y, Q.y) - 1, 0); ej <= min(min(P.y, Q.y), mm.epe - 1); ++ej)
+        for (int ei = max(max(P.x, Q.x) - 1, 0); ei <= min(min(P.x, Q.x), mm.epe - 1); ++ei) {
+          const int el = ((d.k0 + ek) * mm.ne1 + d.j0 + ej) * mm.ne0 + d.i0 + ei;
+          const int va = vtx[(P.x - ei) + 2 * (P.y - ej) + 4 * (P.z - ek)];
+          const int vb = vtx[(Q.x - ei) + 2 * (Q.y - ej) + 4 * (Q.z - ek)];
+          const double kv = mm.ke[(size_t)mm.eke[el] * ed * ed + (va * nc + P.w) * ed + vb * nc + Q.w];
+          const double sc = mm.escale ? mm.escale[el] : 1.0;
+          s = __dadd_rn(s, sc == 1.0 ? kv : __dmul_rn(sc, kv));
         }
-      }
-      out[(size_t)j * d.ld + i] = s;
-    }
-    __syncthreads();
+    d.a[(size_t)pc * d.ld + pr] = s;
   }
 }
 
@@ -1796,11 +1790,10 @@ void assemble_fronts(DeviceState& D) {
   cudaStream_t st = D.st;
   CK(cudaMemsetAsync(D.asm_ipos.p, 0xff, D.asm_ipos.n * sizeof(int), st));
   k_front_maps<<<dim3(16, na), 256, 0, st>>>(D.asmdesc.p);
-  long tiles = 0;
-  for (int s : D.own) tiles = std::max<long>(tiles, (long)(D.NM[s] / 64) * (D.NM[s] / 64 + 1) / 2);
-  const int bx = static_cast<int>(std::max<long>(1, std::min<long>(tiles, (16L * sm_count() + na - 1) / na)));
-  k_assemble_dense<<<dim3(bx, na), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
-  count_launch(2);
+  const int bx = static_cast<int>(std::max<long>(1, std::min<long>(D.max_NM, (16L * sm_count() + na - 1) / na)));
+  k_zero_fronts<<<dim3(bx, na), 256, 0, st>>>(D.asmdesc.p);
+  k_assemble_sparse<<<dim3(bx, na), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
+  count_launch(3);
 }
 }  // namespace
 
