@@ -1645,14 +1645,40 @@ __global__ void __launch_bounds__(256) k_big_backward(const SolveDesc* ds, doubl
     for (int r = tid; r < 64; r += 256) d.x[(size_t)t * 64 + r] = xs[(t / G) * 64 + r];
 }
 
-__global__ void k_copy_trailing(const TrailDesc* ds) {
+// 32x32 tiles of the lower triangle: each is read once down its columns
+// (coalesced), written in place and, transposed through shared memory, into the
+// mirrored tile -- both stores run down columns too.
+__global__ void __launch_bounds__(256) k_copy_trailing(const TrailDesc* ds) {
   const TrailDesc d = ds[blockIdx.y];
-  const int m = d.n - d.p;
-  const long total = (long)m * m;
-  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
-    const int r = static_cast<int>(e % m), c = static_cast<int>(e / m);
-    const int rr = r >= c ? r : c, cc = r >= c ? c : r;  // read the lower triangle
-    d.s[e] = d.a[(size_t)(d.p + cc) * d.n + d.p + rr];
+  const int m = d.n - d.p, nt = (m + 31) / 32;
+  const long tiles = (long)nt * (nt + 1) / 2;
+  __shared__ double t[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (long q = blockIdx.x; q < tiles; q += gridDim.x) {
+    int ti = static_cast<int>((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+    while ((long)ti * (ti + 1) / 2 > q) --ti;
+    while ((long)(ti + 1) * (ti + 2) / 2 <= q) ++ti;
+    const int tj = static_cast<int>(q - (long)ti * (ti + 1) / 2);  // tj <= ti
+    const int r = ti * 32 + tx;
+    for (int cc = ty; cc < 32; cc += 8) {
+      const int c = tj * 32 + cc;
+      double v = 0.0;
+      if (r < m && c < m) {
+        // diagonal tiles: the strictly upper entries come from their mirror images
+        v = r >= c ? d.a[(size_t)(d.p + c) * d.n + d.p + r] : d.a[(size_t)(d.p + r) * d.n + d.p + c];
+        d.s[(size_t)c * m + r] = v;
+      }
+      t[cc][tx] = v;
+    }
+    __syncthreads();
+    if (ti != tj) {
+      const int r2 = tj * 32 + tx;  // row of the mirrored tile
+      for (int cc = ty; cc < 32; cc += 8) {
+        const int c2 = ti * 32 + cc;
+        if (r2 < m && c2 < m) d.s[(size_t)c2 * m + r2] = t[tx][cc];
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -2034,8 +2060,8 @@ void front_backward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t
 
 void copy_trailing_full(const TrailDesc* d_descs, int batch, int max_m, cudaStream_t stream) {
   if (batch == 0) return;
-  const long total = (long)max_m * max_m;
-  const int blocks = static_cast<int>(std::min<long>((total + 255) / 256, 1024));
+  const long nt = (max_m + 31) / 32;
+  const int blocks = static_cast<int>(std::min<long>(nt * (nt + 1) / 2, 1024));
   k_copy_trailing<<<dim3(blocks, batch), 256, 0, stream>>>(d_descs);
   count_launch(1);
 }

@@ -85,6 +85,7 @@ struct GatherDesc {
   const int* pos;  // front index (outer, then kept) -> source index
   double* dst;
   int ld, N, PO, no, m1;
+  int full;  // src holds both triangles (the substructure's S): every read runs down a column (coalesced)
 };
 
 struct PairBuffers {
@@ -121,7 +122,7 @@ __global__ void k_gather_front(const GatherDesc* gd) {
     if (vc && valid(r)) {
       const int pr = d.pos[bidx(r)];
       const int hi = pr >= pc ? pr : pc, lo = pr >= pc ? pc : pr;
-      v = d.src[(size_t)lo * d.ld + hi];
+      v = d.full ? d.src[(size_t)pc * d.ld + pr] : d.src[(size_t)lo * d.ld + hi];
     } else {
       v = (r == col) ? 1.0 : 0.0;
     }
@@ -1285,7 +1286,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       for (int q = 0; q < nh; ++q) {
         const int sub = hubs[q].s;
         gh[q] = GatherDesc{S_ + s_off_[sub], B_.Hpos.p + hposOff[q], B_.Hub.p + hubOff[q], PB_[sub], hubNH[q],
-                           hubPH[q], static_cast<int>(hubs[q].rest.size()), static_cast<int>(hubs[q].U.size())};
+                           hubPH[q], static_cast<int>(hubs[q].rest.size()), static_cast<int>(hubs[q].U.size()), 1};
         fh[q] = FrontDesc{B_.Hub.p + hubOff[q], B_.DvH.p + hubDOff[q], hubNH[q], hubPH[q], B_.hinfo.p + q, 0,
                           static_cast<int>(hubs[q].rest.size()), static_cast<int>(hubs[q].U.size())};
       }
@@ -1421,7 +1422,7 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
         const int lds = q >= 0 ? hubNH[q] : PB_[sub];
         gs[2 * b + side] = GatherDesc{src, B_.Gpos.p + ch.oGp[2 * b + side], pd[b].G[side], lds,
                                       dims[b].NG[side], dims[b].PO[side], dims[b].no[side],
-                                      dims[b].nc + dims[b].nf};
+                                      dims[b].nc + dims[b].nf, q >= 0 ? 0 : 1};
       }
     B_.up_desc.add(B_.gside, gs);
     std::vector<SolveDesc> sv;
