@@ -915,7 +915,8 @@ __device__ void dag_prepare(const FrontDesc& d, int i, int j, int kb, int ke, in
 // k-1 of the same tile).  Half of the queue CTAs take B only; the others take A
 // and then B.  A waits only on A and the workers, B on A and B: no cycle.
 __global__ void __launch_bounds__(DAG_THREADS, 3) k_chol_dag(const FrontDesc* ds, int batch, int nt, int pt_max,
-                                                          int mt, int* ctl, int total, int chunked, int cw, int bq) {
+                                                          int mt, int* ctl, int total, int chunked, int cw, int bq,
+                                                          int group) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_task, s_ready;
   const int tid = threadIdx.x;
@@ -970,20 +971,25 @@ __global__ void __launch_bounds__(DAG_THREADS, 3) k_chol_dag(const FrontDesc* ds
     if (t >= total) return;
     if (chunked && t >= etotal) on_b = true;
     if (!chunked) {
-      int j = 0, r = t;
-      while (r >= batch * (nt - j)) {
-        r -= batch * (nt - j);
+      // groups of `group` consecutive fronts, one group after the other: the
+      // fronts being factored at any time fit the L2, so a front's panels are
+      // re-read from L2 rather than from DRAM while its columns are eliminated
+      const int per_front = nt * (nt + 1) / 2;
+      const int g = t / (group * per_front), b0 = g * group, bg = min(group, batch - b0);
+      int j = 0, r = t - g * group * per_front;
+      while (r >= bg * (nt - j)) {
+        r -= bg * (nt - j);
         ++j;
       }
       // within a column: every front's diagonal tile, then the rows front by
       // front (consecutive tasks share the front's row-j panel in L2)
       int b, i;
-      if (r < batch) {
-        b = r;
+      if (r < bg) {
+        b = b0 + r;
         i = j;
       } else {
-        r -= batch;
-        b = r / (nt - j - 1);
+        r -= bg;
+        b = b0 + r / (nt - j - 1);
         i = j + 1 + r % (nt - j - 1);
       }
       const FrontDesc d = ds[b];
@@ -1850,8 +1856,12 @@ void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, i
   if (!ctl) throw std::runtime_error("partial_cholesky: workspace allocation failed");
   cudaMemsetAsync(ctl, 0, ints * sizeof(int), stream);
   const int grid = static_cast<int>(std::min<long>(total + (chunked ? batch : 0), resident));
+  // plain mode: fronts per group of the task order (k_chol_dag); experiments
+  // may set BDDC_B200_DAGG
+  int group = batch;
+  if (const char* e = std::getenv("BDDC_B200_DAGG"); e && *e) group = std::max(1, std::min(batch, std::atoi(e)));
   k_chol_dag<<<grid, DAG_THREADS, smem, stream>>>(d_descs, batch, nt, pt, mt, ctl, static_cast<int>(total),
-                                                 chunked ? 1 : 0, cw, bq);
+                                                 chunked ? 1 : 0, cw, bq, group);
   count_launch(1);
 }
 }  // namespace

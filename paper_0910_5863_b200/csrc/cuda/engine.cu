@@ -889,6 +889,144 @@ __global__ void __launch_bounds__(256) k_root_gather_gemv(int n_root, int NR, co
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused coarse stage of the preconditioner apply (explicit primal-tree levels
+// and a small root inverse on one GPU): the level gathers and forward GEMVs,
+// the root gather + -R^{-1} GEMV and the level backward GEMVs are phases of
+// ONE launch separated by grid barriers, instead of four to six dependent
+// launches of a few microseconds of work each (cfg3/cfg4: 48 us of a 323/451 us
+// apply).  Every CTA forms the gathered right-hand side it needs itself (the
+// deterministic CSR sums of k_root_gather, so results are bit-identical to the
+// separate launches); the grid is at most the co-resident CTAs.
+// ---------------------------------------------------------------------------
+constexpr int kCoarseLevels = 4;
+struct CoarseLevelArgs {
+  const LeafX* lx;         // explicit fronts of the level
+  const int* ptr;          // gather CSR over the level's vector positions
+  const long long* src;
+  const double* vbase;     // the level's vector arena (LeafX::FV points into it)
+  const double* fvsrc;     // children's forward results
+  const double* up;        // parent's solution (backward)
+  int nfr, ncb, nrb;       // fronts, 8-column blocks and 64-row blocks per front
+};
+struct CoarseArgs {
+  CoarseLevelArgs lv[kCoarseLevels];
+  int nlev;
+  int n_root, NR;
+  const int* root_ptr;
+  const long long* root_src;
+  const double* root_fvsrc;
+  const double* Rinv;
+  double* xroot;
+  unsigned* bar;  // [0] arrivals, [1] CTAs done (the last one zeroes both)
+};
+
+__device__ __forceinline__ void coarse_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256, 2) k_coarse_explicit(const __grid_constant__ CoarseArgs a, const int* done) {
+  if (done && *done) return;
+  extern __shared__ double bs[];
+  __shared__ double tail[8];
+  unsigned phase = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int l = 0; l < a.nlev; ++l) {
+    const CoarseLevelArgs& L = a.lv[l];
+    for (int u = blockIdx.x; u < L.nfr * L.ncb; u += gridDim.x) {
+      const LeafX d = L.lx[u / L.ncb];
+      const int cb = u % L.ncb, cols = d.PE + d.M;
+      if (cb * 8 >= cols) continue;
+      const long long off = d.FV - L.vbase;
+      for (int k = threadIdx.x; k < d.PE; k += blockDim.x) {
+        double s = 0.0;
+        for (int t = L.ptr[off + k]; t < L.ptr[off + k + 1]; ++t) s += L.fvsrc[L.src[t]];
+        bs[k] = s;
+      }
+      const int j = cb * 8 + warp;
+      if (lane == 0 && j >= d.PE && j < cols) {
+        double s = 0.0;
+        for (int t = L.ptr[off + j]; t < L.ptr[off + j + 1]; ++t) s += L.fvsrc[L.src[t]];
+        tail[warp] = s;
+      }
+      __syncthreads();
+      if (j < cols) {
+        const double2* col = reinterpret_cast<const double2*>(d.E + (size_t)j * d.PE);
+        const double2* b2 = reinterpret_cast<const double2*>(bs);
+        const int half = d.PE / 2;
+        double s0 = 0.0, s1 = 0.0;
+        for (int k0 = 0; k0 < half; k0 += 256) {
+          double2 v[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int k = k0 + 32 * t + lane;
+            v[t] = k < half ? __ldg(col + k) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int k = k0 + 32 * t + lane;
+            if (k < half) {
+              const double2 bb = b2[k];
+              s0 += v[t].x * bb.x;
+              s1 += v[t].y * bb.y;
+            }
+          }
+        }
+        double s = s0 + s1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) d.FV2[j] = j < d.PE ? -s : tail[warp] + s;
+      }
+      __syncthreads();
+    }
+    coarse_barrier(a.bar, ++phase * gridDim.x);
+  }
+  // root: every CTA gathers the whole right-hand side, then its columns of -R^{-1}
+  if (blockIdx.x * 8 < a.NR) {
+    for (int k = threadIdx.x; k < a.NR; k += blockDim.x) {
+      double s = 0.0;
+      if (k < a.n_root)
+        for (int t = a.root_ptr[k]; t < a.root_ptr[k + 1]; ++t) s += a.root_fvsrc[a.root_src[t]];
+      bs[k] = s;
+    }
+    __syncthreads();
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < a.NR; c += warps) {
+      const double* col = a.Rinv + (size_t)c * a.NR;
+      double s0 = 0.0, s1 = 0.0;
+      int r = lane;
+      for (; r + 32 < a.NR; r += 64) {
+        s0 += col[r] * bs[r];
+        s1 += col[r + 32] * bs[r + 32];
+      }
+      if (r < a.NR) s0 += col[r] * bs[r];
+      double s = s0 + s1;
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) a.xroot[c] = -s;
+    }
+  }
+  for (int l = a.nlev - 1; l >= 0; --l) {
+    coarse_barrier(a.bar, ++phase * gridDim.x);
+    const CoarseLevelArgs& L = a.lv[l];
+    for (int u = blockIdx.x; u < L.nfr * L.nrb; u += gridDim.x) leaf_bwd_body(L.lx[u / L.nrb], u % L.nrb, L.up, bs);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(a.bar + 1, 1u) == gridDim.x - 1) {
+    a.bar[0] = 0u;
+    a.bar[1] = 0u;
+    __threadfence();
+  }
+}
+
 __global__ void k_extract_boundary(const SubDesc* sd, const double* MV, const long long* mvoff, const int* PI) {
   const SubDesc d = sd[blockIdx.x];
   for (int b = threadIdx.x; b < d.nB; b += blockDim.x) d.WB[b] = MV[mvoff[blockIdx.x] + PI[blockIdx.x] + b];
@@ -1384,6 +1522,11 @@ struct DeviceState {
     DBuf<LeafX> lx;
   };
   std::vector<std::unique_ptr<TreeLevel>> tree;
+  // fused coarse stage (k_coarse_explicit): explicit levels + small root inverse
+  bool coarse_fused = false;
+  CoarseArgs coarse_args{};
+  int coarse_grid = 0, coarse_smem = 0;
+  DBuf<unsigned> coarse_bar;
   int tree_depth = 0;
   double tree_apply_bytes = 0, tree_factor_bytes = 0;
   double* leaf_croot = nullptr;  // where the leaves' backward sweeps read their coarse values
@@ -2096,28 +2239,58 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       leaves[q].src0 = D.fv_off[s] + D.PE[s];
     }
     int depth = 0;
-    if (!D.comm) {
-      const int maxd = coarse_tree_max_depth(m.mesh.sub);
-      const char* env = std::getenv("BDDC_B200_ROOT_DEPTH");
-      if (env && *env) {
-        depth = std::max(0, std::min(std::atoi(env), maxd));
-      } else {
-        // candidate depths planned symbolically in parallel, the cheapest kept
-        std::vector<double> cost(maxd + 1);
-        std::vector<CoarseTree> cand(maxd + 1);
-#pragma omp parallel for schedule(static, 1) if (no >= 256)
-        for (int d = 0; d <= maxd; ++d) {
-          cand[d] = plan_coarse_tree(leaves, m.mesh.sub, D.n_primal, d, kRootInverseMax, true);
-          cost[d] = coarse_tree_cost(cand[d], kTreeApplies, kRootInverseMax);
+    int maxd = coarse_tree_max_depth(m.mesh.sub);
+    // Sharded: every rank plans the same boxes from the bounds of each primal
+    // unknown over ALL substructures and keeps the fronts of its own boxes; the
+    // top front is summed over the ranks.  The depth is chosen on the global
+    // symbolic plan, so every rank takes the same one; a partition whose blocks
+    // cut through the depth-1 boxes keeps the dense root (depth 0).
+    CoarseBounds bounds;
+    std::vector<CoarseLeaf> all_leaves;
+    if (D.comm) {
+      maxd = coarse_tree_shard_depth(m.mesh.sub, D.owner, maxd);
+      bounds.lo.assign(3 * (size_t)D.n_primal, 1 << 30);
+      bounds.hi.assign(3 * (size_t)D.n_primal, -1);
+      all_leaves.resize(ns);
+      for (int s = 0; s < ns; ++s)
+        for (int a = 0; a < 3; ++a) all_leaves[s].coord[a] = m.subs[s].origin[a] / m.mesh.epe;
+      auto hold = [&](int k, int s) {
+        all_leaves[s].coarse.push_back(k);
+        for (int a = 0; a < 3; ++a) {
+          bounds.lo[3 * (size_t)k + a] = std::min(bounds.lo[3 * (size_t)k + a], all_leaves[s].coord[a]);
+          bounds.hi[3 * (size_t)k + a] = std::max(bounds.hi[3 * (size_t)k + a], all_leaves[s].coord[a] + 1);
         }
-        for (int d = 1; d <= maxd; ++d)
-          if (cost[d] < cost[depth]) depth = d;
-        plan = std::move(cand[depth]);
-        ht.mark("tree_depths");
+      };
+      for (std::size_t g = 0; g < m.globs.size(); ++g)
+        for (i64 dof : m.glob_dofs[g]) {
+          const i64 cid = m.maps.corner_dof_of_global[dof];
+          if (cid < 0) continue;
+          for (int s : m.globs[g].subdomains) hold(static_cast<int>(cid), s);
+        }
+      for (std::size_t g = 0; g < cov.groups.size(); ++g)
+        for (int s : cov.group_subs[g]) hold(static_cast<int>(ncd + g), s);
+    }
+    const std::vector<CoarseLeaf>& cost_leaves = D.comm ? all_leaves : leaves;
+    const char* env = std::getenv("BDDC_B200_ROOT_DEPTH");
+    if (env && *env) {
+      depth = std::max(0, std::min(std::atoi(env), maxd));
+    } else if (maxd > 0) {
+      // candidate depths planned symbolically in parallel, the cheapest kept
+      std::vector<double> cost(maxd + 1);
+      std::vector<CoarseTree> cand(maxd + 1);
+#pragma omp parallel for schedule(static, 1) if (cost_leaves.size() >= 256)
+      for (int d = 0; d <= maxd; ++d) {
+        cand[d] = plan_coarse_tree(cost_leaves, m.mesh.sub, D.n_primal, d, kRootInverseMax, true);
+        cost[d] = coarse_tree_cost(cand[d], kTreeApplies, kRootInverseMax);
       }
+      for (int d = 1; d <= maxd; ++d)
+        if (cost[d] < cost[depth]) depth = d;
+      if (!D.comm) plan = std::move(cand[depth]);
+      ht.mark("tree_depths");
     }
     if (plan.leaf_box.empty() && plan.top.empty())
-      plan = plan_coarse_tree(leaves, m.mesh.sub, D.n_primal, depth, kRootInverseMax);
+      plan = plan_coarse_tree(leaves, m.mesh.sub, D.n_primal, depth, kRootInverseMax, false,
+                              D.comm ? &bounds : nullptr);
     else
       complete_coarse_tree(plan, leaves);
     ht.mark("tree_plan");
@@ -2452,6 +2625,61 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   ht.mark("descriptors");
   UB.flush(st);
   ht.mark("upload_desc");
+  // coarse stage of the apply as one launch (k_coarse_explicit) when every
+  // level is explicit and the root inverse is small; BDDC_B200_COARSE=split keeps
+  // the separate launches (parity-tested both ways)
+  {
+    const char* env = std::getenv("BDDC_B200_COARSE");
+    bool ok = !(env && std::string(env) == "split") && !D.comm && D.root_inv && !D.tree.empty() &&
+              D.tree.size() <= static_cast<std::size_t>(kCoarseLevels) && D.NR <= 4096;
+    int words = D.NR;
+    for (auto& T : D.tree) {
+      ok = ok && T->expl && T->max_NF <= 4096;
+      words = std::max(words, std::max(T->max_PE, T->max_M));
+    }
+    D.coarse_fused = ok;
+    if (ok) {
+      CoarseArgs& A = D.coarse_args;
+      A = CoarseArgs{};
+      A.nlev = static_cast<int>(D.tree.size());
+      long units = (D.NR + 7) / 8;
+      const double* fvsrc = D.leaf_explicit ? D.FV2.p : D.FV.p;
+      for (int l = 0; l < A.nlev; ++l) {
+        DeviceState::TreeLevel& T = *D.tree[l];
+        CoarseLevelArgs& L = A.lv[l];
+        L.lx = T.lx.p;
+        L.ptr = T.ptr.p;
+        L.src = T.src.p;
+        L.vbase = T.V.p;
+        L.fvsrc = fvsrc;
+        L.up = l + 1 < A.nlev ? D.tree[l + 1]->V.p : top_x;
+        L.nfr = T.nfr;
+        L.ncb = (T.max_NF + 7) / 8;
+        L.nrb = T.max_NF / kTile;
+        units = std::max(units, (long)L.nfr * L.ncb);
+        fvsrc = T.V2.p;
+      }
+      A.n_root = D.n_root;
+      A.NR = D.NR;
+      A.root_ptr = D.root_ptr.p;
+      A.root_src = D.root_src.p;
+      A.root_fvsrc = fvsrc;
+      A.Rinv = D.Rinv.p;
+      A.xroot = top_x;
+      if (D.coarse_bar.n == 0) {
+        D.coarse_bar.alloc(2);
+        D.coarse_bar.zero(st);
+      }
+      A.bar = D.coarse_bar.p;
+      D.coarse_smem = words * static_cast<int>(sizeof(double));
+      const int per_sm = per_device(reinterpret_cast<const void*>(&k_coarse_explicit), [] {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_coarse_explicit, 256, 4096 * sizeof(double));
+        return std::max(1, std::min(n, 2));
+      });
+      D.coarse_grid = static_cast<int>(std::min<long>(units, (long)per_sm * sm_count()));
+    }
+  }
   StageProfiler prof("set_constraints", st);
   // F = P (T^T S T) P^T, pads identity
   if (!D.leaf_explicit) {
@@ -2600,6 +2828,11 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
   }
   mark("leaf_fwd");
   const double* fvsrc = D.leaf_explicit ? D.FV2.p : D.FV.p;
+  if (D.coarse_fused) {
+    k_coarse_explicit<<<D.coarse_grid, 256, D.coarse_smem, st>>>(D.coarse_args, done);
+    count_launch(1);
+    mark("root_coarse");
+  } else {
   // primal tree, deepest level first: gather the children's coarse residuals,
   // forward sweep
   for (auto& T : D.tree) {
@@ -2652,6 +2885,7 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     }
   }
   if (!D.tree.empty()) mark("tree_bwd");
+  }  // separate coarse launches
   if (D.leaf_explicit && ns) {
     k_leaf_bwd_explicit<<<dim3(D.max_NF / kTile, ns), 256, D.max_M * sizeof(double), st>>>(D.leafx.p, D.leaf_croot,
                                                                                           done);

@@ -36,7 +36,7 @@ bool build_boxes(const int lattice[3], int depth, std::vector<std::vector<Box>>&
         if (ext >= 2) {
           nparts[a] = 2;
           cuts[a][0] = par.lo[a];
-          cuts[a][1] = par.lo[a] + ext / 2;
+          cuts[a][1] = par.lo[a] + (ext + 1) / 2;  // the block partition's cut (shard.py partition) for two parts
           cuts[a][2] = par.hi[a];
           any = true;
         } else {
@@ -98,21 +98,48 @@ int coarse_tree_max_depth(const int lattice[3]) {
   return d;
 }
 
+int coarse_tree_shard_depth(const int lattice[3], const std::vector<int>& owner, int max_depth) {
+  // deeper boxes nest inside the depth-1 boxes, so those decide
+  if (max_depth < 1) return 0;
+  std::vector<std::vector<Box>> boxes;
+  if (!build_boxes(lattice, 1, boxes)) return 0;
+  for (const Box& b : boxes[1]) {
+    int r = -1;
+    for (int z = b.lo[2]; z < b.hi[2]; ++z)
+      for (int y = b.lo[1]; y < b.hi[1]; ++y)
+        for (int x = b.lo[0]; x < b.hi[0]; ++x) {
+          const int o = owner[(static_cast<std::size_t>(z) * lattice[1] + y) * lattice[0] + x];
+          if (r < 0) r = o;
+          if (o != r) return 0;
+        }
+  }
+  return max_depth;
+}
+
 CoarseTree plan_coarse_tree(const std::vector<CoarseLeaf>& leaves, const int lattice[3], int n_primal, int depth,
-                            int root_inverse_max, bool symbolic) {
+                            int root_inverse_max, bool symbolic, const CoarseBounds* bounds) {
   CoarseTree t;
   t.depth = depth;
   std::vector<std::vector<Box>> boxes;
   if (!build_boxes(lattice, depth, boxes)) throw std::invalid_argument("coarse tree: depth too large for the lattice");
   const int nl = static_cast<int>(leaves.size());
   // bounding box of each primal unknown's substructures
-  std::vector<int> lo(3 * (size_t)n_primal, 1 << 30), hi(3 * (size_t)n_primal, -1);
-  for (const CoarseLeaf& l : leaves)
-    for (int k : l.coarse)
-      for (int a = 0; a < 3; ++a) {
-        lo[3 * (size_t)k + a] = std::min(lo[3 * (size_t)k + a], l.coord[a]);
-        hi[3 * (size_t)k + a] = std::max(hi[3 * (size_t)k + a], l.coord[a] + 1);
-      }
+  std::vector<int> lo, hi;
+  if (bounds) {  // sharded: the bounds over every rank's substructures
+    if (bounds->lo.size() != 3 * (size_t)n_primal || bounds->hi.size() != 3 * (size_t)n_primal)
+      throw std::invalid_argument("coarse tree: bounds do not match the primal unknowns");
+    lo = bounds->lo;
+    hi = bounds->hi;
+  } else {
+    lo.assign(3 * (size_t)n_primal, 1 << 30);
+    hi.assign(3 * (size_t)n_primal, -1);
+    for (const CoarseLeaf& l : leaves)
+      for (int k : l.coarse)
+        for (int a = 0; a < 3; ++a) {
+          lo[3 * (size_t)k + a] = std::min(lo[3 * (size_t)k + a], l.coord[a]);
+          hi[3 * (size_t)k + a] = std::max(hi[3 * (size_t)k + a], l.coord[a] + 1);
+        }
+  }
   // owner box of each unknown: the deepest box containing its bounding box
   std::vector<std::vector<std::vector<int>>> own(depth + 1);
   for (int d = 0; d <= depth; ++d) own[d].resize(boxes[d].size());
@@ -153,6 +180,19 @@ CoarseTree plan_coarse_tree(const std::vector<CoarseLeaf>& leaves, const int lat
     }
     leaf_box[i] = b;
   }
+  // fronts exist for the boxes that hold one of these leaves (all of them on
+  // one GPU; a rank's own boxes when sharded): local index per box
+  std::vector<std::vector<int>> local(depth + 1);
+  for (int d = 0; d <= depth; ++d) local[d].assign(boxes[d].size(), -1);
+  for (int i = 0; i < nl; ++i) local[depth][leaf_box[i]] = 0;
+  for (int d = depth; d >= 1; --d)
+    for (int b = 0; b < static_cast<int>(boxes[d].size()); ++b)
+      if (local[d][b] >= 0) local[d - 1][boxes[d][b].parent] = 0;
+  for (int d = 0; d <= depth; ++d) {
+    int n = 0;
+    for (int& v : local[d])
+      if (v >= 0) v = n++;
+  }
   // update sets, bottom-up
   std::vector<int> mark(n_primal, -1);
   int stamp = 0;
@@ -185,11 +225,12 @@ CoarseTree plan_coarse_tree(const std::vector<CoarseLeaf>& leaves, const int lat
   t.levels.resize(depth);
   for (int d = depth; d >= 1; --d) {
     CoarseTree::Level& L = t.levels[depth - d];
-    L.fronts.resize(boxes[d].size());
     long long fv = 0, ao = 0, dof = 0, co = 0;
     for (int b = 0; b < static_cast<int>(boxes[d].size()); ++b) {
-      CoarseTree::Front& f = L.fronts[b];
-      f.parent = d > 1 ? boxes[d][b].parent : -1;
+      if (local[d][b] < 0) continue;
+      L.fronts.emplace_back();
+      CoarseTree::Front& f = L.fronts.back();
+      f.parent = d > 1 ? local[d - 1][boxes[d][b].parent] : -1;
       f.own = own[d][b];
       f.upd = upd[d][b];
       f.PE = rup(std::max<int>(static_cast<int>(f.own.size()), 1));
@@ -220,6 +261,8 @@ CoarseTree plan_coarse_tree(const std::vector<CoarseLeaf>& leaves, const int lat
     t.flops += inv ? n * n * n : n * n * n / 3.0;
     t.apply_bytes += n * n * 8.0;
   }
+  if (depth > 0)
+    for (int& b : leaf_box) b = local[depth][b];
   t.leaf_box = std::move(leaf_box);
   t.n_primal = n_primal;
   if (!symbolic) complete_coarse_tree(t, leaves);

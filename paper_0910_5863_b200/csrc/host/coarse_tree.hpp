@@ -56,13 +56,28 @@ struct CoarseTree {
   double apply_bytes = 0;  // bytes read per preconditioner apply (both sweeps of every front + top)
 };
 
+/// Sharded engines: bounding box (lattice coordinates, hi exclusive) of the
+/// substructures of EVERY rank that hold each primal unknown, so that all ranks
+/// place an unknown in the same box; hi < 0 marks an unknown nobody holds.
+struct CoarseBounds {
+  std::vector<int> lo, hi;  // 3 per primal unknown
+};
+
 /// Deepest tree the lattice allows (every box of the level above can be split).
 int coarse_tree_max_depth(const int lattice[3]);
 
 /// Tree of the given depth (0 = one dense root over all primal unknowns).
 /// `symbolic`: front sets, sizes and costs only (no gather or backward maps).
+/// With `bounds` (a sharded engine) `leaves` are one rank's substructures: the
+/// plan then holds the fronts of the boxes that rank owns and the whole top
+/// front, whose contributions the ranks sum (engine.cu, root all-reduce).
 CoarseTree plan_coarse_tree(const std::vector<CoarseLeaf>& leaves, const int lattice[3], int n_primal, int depth,
-                            int root_inverse_max, bool symbolic = false);
+                            int root_inverse_max, bool symbolic = false, const CoarseBounds* bounds = nullptr);
+
+/// Deepest tree (at most `max_depth`) whose boxes below the top each lie inside
+/// one rank's block of the partition `owner` (rank per lattice cell, x fastest):
+/// `max_depth` when the eight (or fewer) depth-1 boxes are rank-pure, else 0.
+int coarse_tree_shard_depth(const int lattice[3], const std::vector<int>& owner, int max_depth);
 
 /// Adds the gather and backward maps to a symbolic plan.
 void complete_coarse_tree(CoarseTree& t, const std::vector<CoarseLeaf>& leaves);

@@ -382,6 +382,39 @@ def test_front_sweep_schedules(sweep, monkeypatch):
     test_primal_tree(*TREE[2], "factor", "factor", monkeypatch)
 
 
+COARSE = [("cfg4 3x3x3 H/h=4 depth 1", lambda: pb.BDDC(config=4, subdomains=(3, 3, 3), elements_per_edge=4), "1",
+           "factor"),
+          ("cfg5 4x4x4 H/h=2 depth 2", lambda: pb.BDDC(config=5, subdomains=(4, 4, 4), elements_per_edge=2), "2",
+           "explicit")]
+
+
+@pytest.mark.parametrize("name,make,depth,leaf", COARSE, ids=[c[0] for c in COARSE])
+def test_fused_coarse_stage_identical(name, make, depth, leaf, monkeypatch):
+    """The coarse stage of the preconditioner apply (bddc_operator.cpp:70-85 on
+    the primal unknowns) as ONE launch (k_coarse_explicit: level gathers and
+    forward GEMVs, root gather and inverse, level backward GEMVs separated by
+    grid barriers) against the separate launches: the same sums in the same
+    order, so the applies and the PCG are bit-identical."""
+    monkeypatch.setenv("BDDC_B200_ROOT_DEPTH", depth)
+    monkeypatch.setenv("BDDC_B200_TREE", "explicit")
+    monkeypatch.setenv("BDDC_B200_LEAF", leaf)
+    monkeypatch.setenv("BDDC_B200_PCG", "graph")
+    out = {}
+    for path in ("fused", "split"):
+        monkeypatch.setenv("BDDC_B200_COARSE", path)
+        b = make()
+        b.run_item("adaptive", 10.0, 15)
+        x = np.random.default_rng(5).standard_normal(b.structure()["interface_dofs"])
+        out[path] = ([b.precond_apply(x) for _ in range(3)], b.pcg(), b.operator_times())
+    f, s = out["fused"], out["split"]
+    assert f[2]["tree_fwd"] == 0.0 and s[2]["tree_fwd"] > 0.0  # the fused launch really ran
+    for a, c in zip(f[0], s[0]):
+        assert np.array_equal(a, c)
+    assert f[1]["iterations"] == s[1]["iterations"]
+    assert np.array_equal(f[1]["alphas"], s[1]["alphas"])
+    assert np.array_equal(f[1]["x"], s[1]["x"])
+
+
 @pytest.mark.parametrize("make,mode,tau,maxv", [(lambda: pb.BDDC(config=1), "c+e+f", 10.0, 15),
                                                  (lambda: pb.BDDC(config=2), "adaptive", 10.0, 10)],
                          ids=["cfg1", "cfg2"])

@@ -40,8 +40,13 @@ def run_ranks(make, world, fn, owner=None, timeout=600):
     threads = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
     for t in threads:
         t.start()
-    for t in threads:
-        t.join(timeout)
+    import time
+    deadline = time.monotonic() + timeout
+    for t in threads:  # one deadline for all ranks; an error in one rank leaves the others waiting
+        while t.is_alive() and time.monotonic() < deadline and not errors:
+            t.join(0.5)
+    if errors:
+        time.sleep(2.0)
     assert not errors, errors
     assert all(not t.is_alive() for t in threads), "a rank did not finish"
     return out
@@ -59,7 +64,7 @@ def pipeline(mode, tau, maxv, base_faces=False, seed=3):
         n = b.structure()["interface_dofs"]
         x = np.random.default_rng(seed).standard_normal(n)
         g = b.pcg()
-        return {"rows": b.constraint_rows(), "reports": b.pair_reports() if mode == "adaptive" else [],
+        return {"root": b.times()["root_size"], "rows": b.constraint_rows(), "reports": b.pair_reports() if mode == "adaptive" else [],
                 "schur": b.schur_apply(x), "prec": b.precond_apply(x), "rhs": b.rhs(), "pcg": g,
                 "u": b.recover(g["x"])}
     return fn
@@ -113,16 +118,38 @@ CASES = [
     ("cfg4 3x3x3 H/h=4 w2", lambda: pb.BDDC(config=4, subdomains=(3, 3, 3), elements_per_edge=4), 2,
      ("adaptive", 10.0, 15)),
     ("sc221h8 c+e+f w2", lambda: pb.BDDC(pb.Problem.cube((2, 2, 1), 8, "scalar")), 2, ("c+e+f", 0.0, 0)),
+    # distributed primal tree: every rank factors the boxes of its own block,
+    # only the top front is summed over the ranks (2x1x1, 2x2x1, 2x2x2 process
+    # grids; the 3x3x3 lattice is cut 2+1 by the partition and by the boxes)
+    ("sc442h3 c+e+f w2 tree1", lambda: pb.BDDC(pb.Problem.cube((4, 4, 2), 3, "scalar")), 2, ("c+e+f", 0.0, 0),
+     {"BDDC_B200_ROOT_DEPTH": "1"}),
+    ("cfg5 4x4x4 H/h=2 w4 tree2", lambda: pb.BDDC(config=5, subdomains=(4, 4, 4), elements_per_edge=2), 4,
+     ("adaptive", 10.0, 15), {"BDDC_B200_ROOT_DEPTH": "2"}),
+    ("cfg5 4x4x4 H/h=2 w8 tree2 factor", lambda: pb.BDDC(config=5, subdomains=(4, 4, 4), elements_per_edge=2), 8,
+     ("adaptive", 10.0, 15), {"BDDC_B200_ROOT_DEPTH": "2", "BDDC_B200_TREE": "factor", "BDDC_B200_LEAF": "factor"}),
+    ("cfg4 3x3x3 H/h=4 w2 tree1", lambda: pb.BDDC(config=4, subdomains=(3, 3, 3), elements_per_edge=4), 2,
+     ("adaptive", 10.0, 15), {"BDDC_B200_ROOT_DEPTH": "1"}),
 ]
 
 
-@pytest.mark.parametrize("name,make,world,mode", CASES, ids=[c[0] for c in CASES])
-def test_sharded_equals_single(name, make, world, mode):
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_sharded_equals_single(case, monkeypatch):
+    name, make, world, mode = case[:4]
+    env = case[4] if len(case) > 4 else {}
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     fn = pipeline(*mode)
     ref_b = make()
     ref = fn(ref_b)
     got = run_ranks(make, world, fn)
     kappa_bound = 1e-6
+    if env.get("BDDC_B200_ROOT_DEPTH", "0") != "0":
+        # the ranks' top front is the single engine's (same boxes), smaller than
+        # the dense root over all primal unknowns the depth-0 shards gather
+        monkeypatch.setenv("BDDC_B200_ROOT_DEPTH", "0")
+        dense = make()
+        dense_root = pipeline(*mode)(dense)["root"]
+        assert all(g["root"] == ref["root"] for g in got) and ref["root"] < dense_root, (ref["root"], dense_root)
     for r in range(world):
         g = got[r]
         # every rank holds the same complete result
