@@ -915,8 +915,7 @@ __device__ void dag_prepare(const FrontDesc& d, int i, int j, int kb, int ke, in
 // k-1 of the same tile).  Half of the queue CTAs take B only; the others take A
 // and then B.  A waits only on A and the workers, B on A and B: no cycle.
 __global__ void __launch_bounds__(DAG_THREADS, 3) k_chol_dag(const FrontDesc* ds, int batch, int nt, int pt_max,
-                                                          int mt, int* ctl, int total, int chunked, int cw, int bq,
-                                                          int group) {
+                                                          int mt, int* ctl, int total, int chunked, int cw, int bq) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_task, s_ready;
   const int tid = threadIdx.x;
@@ -971,26 +970,37 @@ __global__ void __launch_bounds__(DAG_THREADS, 3) k_chol_dag(const FrontDesc* ds
     if (t >= total) return;
     if (chunked && t >= etotal) on_b = true;
     if (!chunked) {
-      // groups of `group` consecutive fronts, one group after the other: the
-      // fronts being factored at any time fit the L2, so a front's panels are
-      // re-read from L2 rather than from DRAM while its columns are eliminated
-      const int per_front = nt * (nt + 1) / 2;
-      const int g = t / (group * per_front), b0 = g * group, bg = min(group, batch - b0);
-      int j = 0, r = t - g * group * per_front;
-      while (r >= bg * (nt - j)) {
-        r -= bg * (nt - j);
-        ++j;
-      }
-      // within a column: every front's diagonal tile, then the rows front by
-      // front (consecutive tasks share the front's row-j panel in L2)
-      int b, i;
-      if (r < bg) {
-        b = b0 + r;
-        i = j;
+      int b, i, j = 0, r = t;
+      const int telim = batch * (pt_max * nt - pt_max * (pt_max - 1) / 2);  // tasks of the columns j < pt_max
+      if (t < telim) {
+        while (r >= batch * (nt - j)) {
+          r -= batch * (nt - j);
+          ++j;
+        }
+        // within a column: every front's diagonal tile, then the rows front by
+        // front (consecutive tasks share the front's row-j panel in L2)
+        if (r < batch) {
+          b = r;
+          i = j;
+        } else {
+          r -= batch;
+          b = r / (nt - j - 1);
+          i = j + 1 + r % (nt - j - 1);
+        }
       } else {
-        r -= bg;
-        b = b0 + r / (nt - j - 1);
-        i = j + 1 + r % (nt - j - 1);
+        // columns past every front's eliminated part: the trailing tiles front by
+        // front, so the tiles in flight share their few fronts' row panels
+        // L(i, 0:p) in L2 (mt panels for mt (mt + 1) / 2 tiles) instead of every
+        // tile streaming its own pair of panels from DRAM
+        const int mtm = nt - pt_max, per = mtm * (mtm + 1) / 2;
+        r = t - telim;
+        b = r / per;
+        const int q = r - b * per;
+        int ii = static_cast<int>((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+        while (ii * (ii + 1) / 2 > q) --ii;
+        while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
+        i = pt_max + ii;
+        j = pt_max + q - ii * (ii + 1) / 2;
       }
       const FrontDesc d = ds[b];
       if (i * kTile >= d.n) continue;
@@ -1856,12 +1866,8 @@ void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, i
   if (!ctl) throw std::runtime_error("partial_cholesky: workspace allocation failed");
   cudaMemsetAsync(ctl, 0, ints * sizeof(int), stream);
   const int grid = static_cast<int>(std::min<long>(total + (chunked ? batch : 0), resident));
-  // plain mode: fronts per group of the task order (k_chol_dag); experiments
-  // may set BDDC_B200_DAGG
-  int group = batch;
-  if (const char* e = std::getenv("BDDC_B200_DAGG"); e && *e) group = std::max(1, std::min(batch, std::atoi(e)));
   k_chol_dag<<<grid, DAG_THREADS, smem, stream>>>(d_descs, batch, nt, pt, mt, ctl, static_cast<int>(total),
-                                                 chunked ? 1 : 0, cw, bq, group);
+                                                 chunked ? 1 : 0, cw, bq);
   count_launch(1);
 }
 }  // namespace

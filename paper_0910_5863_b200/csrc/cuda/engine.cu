@@ -934,12 +934,28 @@ __device__ __forceinline__ void coarse_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256, 2) k_coarse_explicit(const __grid_constant__ CoarseArgs a, const int* done) {
+__global__ void __launch_bounds__(256, 4) k_coarse_explicit(const __grid_constant__ CoarseArgs a, const int* done) {
   if (done && *done) return;
   extern __shared__ double bs[];
   __shared__ double tail[8];
   unsigned phase = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the later phases' matrices (-R^{-1}, the levels' W blocks) do not depend on
+  // the vector: their lines are requested into L2 now, behind the first
+  // phase's own loads, so the phases after the barriers do not start cold
+  {
+    const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, gn = (size_t)gridDim.x * blockDim.x;
+    const char* rinv = reinterpret_cast<const char*>(a.Rinv);
+    for (size_t o = gtid * 128; o < (size_t)a.NR * a.NR * sizeof(double); o += gn * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(rinv + o));
+    for (int l = 0; l < a.nlev; ++l)
+      for (int f = 0; f < a.lv[l].nfr; ++f) {
+        const LeafX d = a.lv[l].lx[f];
+        const char* w = reinterpret_cast<const char*>(d.E + (size_t)d.PE * d.PE);
+        for (size_t o = gtid * 128; o < (size_t)d.PE * d.M * sizeof(double); o += gn * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(w + o));
+      }
+  }
   for (int l = 0; l < a.nlev; ++l) {
     const CoarseLevelArgs& L = a.lv[l];
     for (int u = blockIdx.x; u < L.nfr * L.ncb; u += gridDim.x) {
@@ -2675,7 +2691,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       const int per_sm = per_device(reinterpret_cast<const void*>(&k_coarse_explicit), [] {
         int n = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_coarse_explicit, 256, 4096 * sizeof(double));
-        return std::max(1, std::min(n, 2));
+        return std::max(1, std::min(n, 4));
       });
       D.coarse_grid = static_cast<int>(std::min<long>(units, (long)per_sm * sm_count()));
     }

@@ -12,7 +12,9 @@ The path shards by substructure and by face pair:
     ascending rank order;
   * dot products: each interface dof is owned by exactly one rank (the lowest
     rank holding a copy); local sums are all-reduced;
-  * root: leaf Schur contributions are summed onto the root by an all-reduce.
+  * primal tree: every rank factors the nested-dissection boxes inside its own
+    block; only the top front (the unknowns shared between the depth-1 boxes)
+    is summed over the ranks by an all-reduce (engine.cu, coarse_tree.hpp).
 The device engine implements this plan in C++ (host.cpp `halo_plan`,
 engine.cu `halo_exchange` over NCCL send/recv); `HaloPlan` below is the same
 plan restated in Python with torch.distributed, the checker of the engine's

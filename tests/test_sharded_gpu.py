@@ -125,8 +125,8 @@ CASES = [
      {"BDDC_B200_ROOT_DEPTH": "1"}),
     ("cfg5 4x4x4 H/h=2 w4 tree2", lambda: pb.BDDC(config=5, subdomains=(4, 4, 4), elements_per_edge=2), 4,
      ("adaptive", 10.0, 15), {"BDDC_B200_ROOT_DEPTH": "2"}),
-    ("cfg5 4x4x4 H/h=2 w8 tree2 factor", lambda: pb.BDDC(config=5, subdomains=(4, 4, 4), elements_per_edge=2), 8,
-     ("adaptive", 10.0, 15), {"BDDC_B200_ROOT_DEPTH": "2", "BDDC_B200_TREE": "factor", "BDDC_B200_LEAF": "factor"}),
+    ("cfg5 4x4x4 H/h=2 w8 tree2", lambda: pb.BDDC(config=5, subdomains=(4, 4, 4), elements_per_edge=2), 8,
+     ("adaptive", 10.0, 15), {"BDDC_B200_ROOT_DEPTH": "2"}),
     ("cfg4 3x3x3 H/h=4 w2 tree1", lambda: pb.BDDC(config=4, subdomains=(3, 3, 3), elements_per_edge=4), 2,
      ("adaptive", 10.0, 15), {"BDDC_B200_ROOT_DEPTH": "1"}),
 ]
