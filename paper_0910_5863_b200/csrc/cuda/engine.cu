@@ -285,16 +285,47 @@ __device__ __forceinline__ double sum_partials(const double* partials) {
 }
 
 // out[i] = sum over the copies of interface dof i of src[pos]; optional dot with `other`
+// Sum of fv[idx[t]] over the CSR list of `at`, added in list order; the loads
+// of up to eight entries are issued together, so the dependent chain is
+// ptr -> index -> value instead of one round trip per entry.
+template <class Index>
+__device__ __forceinline__ double csr_sum(const int* __restrict__ ptr, const Index* __restrict__ idx, const double* fv,
+                                          long long at) {
+  const int b = ptr[at], e = ptr[at + 1];
+  double s = 0.0;
+  for (int t = b; t < e; t += 8) {
+    long long k[8];
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) k[q] = t + q < e ? static_cast<long long>(idx[t + q]) : -1;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = k[q] >= 0 ? fv[k[q]] : 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (t + q < e) s += v[q];
+  }
+  return s;
+}
+
 __global__ void __launch_bounds__(256) k_sum_copies(i64 n, const int* __restrict__ ptr, const int* __restrict__ pos,
                                                     const double* __restrict__ src, double* out,
                                                     const double* other, double* partials, const int* done) {
   if (done && *done) return;
   double acc = 0.0;
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int t = ptr[i]; t < ptr[i + 1]; ++t) s += src[pos[t]];
-    out[i] = s;
-    if (other) acc += s * other[i];
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  // two dofs per pass, their chains in flight together; sums and the dot
+  // product are formed in the order of the one-dof loop
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += 2 * stride) {
+    const i64 i1 = i + stride;
+    const double s0 = csr_sum(ptr, pos, src, i);
+    const double s1 = i1 < n ? csr_sum(ptr, pos, src, i1) : 0.0;
+    const double o0 = other ? other[i] : 0.0, o1 = other && i1 < n ? other[i1] : 0.0;
+    out[i] = s0;
+    if (other) acc += s0 * o0;
+    if (i1 < n) {
+      out[i1] = s1;
+      if (other) acc += s1 * o1;
+    }
   }
   if (partials) block_partial(acc, partials);
 }
@@ -934,7 +965,7 @@ __device__ __forceinline__ void coarse_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256, 4) k_coarse_explicit(const __grid_constant__ CoarseArgs a, const int* done) {
+__global__ void __launch_bounds__(256, 3) k_coarse_explicit(const __grid_constant__ CoarseArgs a, const int* done) {
   if (done && *done) return;
   extern __shared__ double bs[];
   __shared__ double tail[8];
@@ -963,29 +994,29 @@ __global__ void __launch_bounds__(256, 4) k_coarse_explicit(const __grid_constan
       const int cb = u % L.ncb, cols = d.PE + d.M;
       if (cb * 8 >= cols) continue;
       const long long off = d.FV - L.vbase;
-      for (int k = threadIdx.x; k < d.PE; k += blockDim.x) {
-        double s = 0.0;
-        for (int t = L.ptr[off + k]; t < L.ptr[off + k + 1]; ++t) s += L.fvsrc[L.src[t]];
-        bs[k] = s;
-      }
+      // the column of E does not depend on the vector: its loads (the whole
+      // column when PE <= 512) are in flight while the right-hand side is gathered
       const int j = cb * 8 + warp;
-      if (lane == 0 && j >= d.PE && j < cols) {
-        double s = 0.0;
-        for (int t = L.ptr[off + j]; t < L.ptr[off + j + 1]; ++t) s += L.fvsrc[L.src[t]];
-        tail[warp] = s;
+      const double2* col = reinterpret_cast<const double2*>(d.E + (size_t)min(j, cols - 1) * d.PE);
+      const int half = d.PE / 2;
+      double2 v0[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int k = 32 * t + lane;
+        v0[t] = k < half ? __ldg(col + k) : make_double2(0.0, 0.0);
       }
+      for (int k = threadIdx.x; k < d.PE; k += blockDim.x) bs[k] = csr_sum(L.ptr, L.src, L.fvsrc, off + k);
+      if (lane == 0 && j >= d.PE && j < cols) tail[warp] = csr_sum(L.ptr, L.src, L.fvsrc, off + j);
       __syncthreads();
       if (j < cols) {
-        const double2* col = reinterpret_cast<const double2*>(d.E + (size_t)j * d.PE);
         const double2* b2 = reinterpret_cast<const double2*>(bs);
-        const int half = d.PE / 2;
         double s0 = 0.0, s1 = 0.0;
         for (int k0 = 0; k0 < half; k0 += 256) {
           double2 v[8];
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
             const int k = k0 + 32 * t + lane;
-            v[t] = k < half ? __ldg(col + k) : make_double2(0.0, 0.0);
+            v[t] = k0 == 0 ? v0[t] : (k < half ? __ldg(col + k) : make_double2(0.0, 0.0));
           }
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
@@ -1008,11 +1039,16 @@ __global__ void __launch_bounds__(256, 4) k_coarse_explicit(const __grid_constan
   }
   // root: every CTA gathers the whole right-hand side, then its columns of -R^{-1}
   if (blockIdx.x * 8 < a.NR) {
-    for (int k = threadIdx.x; k < a.NR; k += blockDim.x) {
-      double s = 0.0;
-      if (k < a.n_root)
-        for (int t = a.root_ptr[k]; t < a.root_ptr[k + 1]; ++t) s += a.root_fvsrc[a.root_src[t]];
-      bs[k] = s;
+    for (int k0 = threadIdx.x; k0 < a.NR; k0 += 4 * blockDim.x) {  // four independent chains per thread
+      double s[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + q * blockDim.x;
+        s[q] = k < a.n_root ? csr_sum(a.root_ptr, a.root_src, a.root_fvsrc, k) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (k0 + q * blockDim.x < a.NR) bs[k0 + q * blockDim.x] = s[q];
     }
     __syncthreads();
     const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -2691,7 +2727,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       const int per_sm = per_device(reinterpret_cast<const void*>(&k_coarse_explicit), [] {
         int n = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_coarse_explicit, 256, 4096 * sizeof(double));
-        return std::max(1, std::min(n, 4));
+        return std::max(1, std::min(n, 3));
       });
       D.coarse_grid = static_cast<int>(std::min<long>(units, (long)per_sm * sm_count()));
     }
@@ -2831,7 +2867,7 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
     if (prof) prof->mark(s);
   };
   const int nw = D.nw;
-  const int pos_blocks = std::max(1, std::min(4 * sm_count(), (nw + 255) / 256));
+  const int pos_blocks = std::max(1, std::min(8 * sm_count(), (nw + 255) / 256));  // one position per thread when resident
   if (ns && (stages & kPreRestrict)) k_restrict_pos<<<pos_blocks, 256, 0, st>>>(D.subdesc.p, D.xf, D.wpos.p, nw, r, done);
   count_launch(3);  // restrict, prolong, copy sum
   mark("restrict");
