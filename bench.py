@@ -384,7 +384,7 @@ def main():
     jobs = 1 if sharded else world  # sharded: one problem over all ranks
     value = jobs * free / sec_per_step
     # end to end through the C ABI with host buffers
-    u = np.empty(free)
+    u = torch.empty(free, dtype=torch.float64, pin_memory=True).numpy()  # page-locked result buffer
     for _ in range(max(1, args.warmup // 2)):
         do_step(True, u)
     barrier(dist, local)

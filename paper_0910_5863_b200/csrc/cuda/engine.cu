@@ -1600,7 +1600,20 @@ struct DeviceState {
   // adaptive pair machinery
   PairEngine pairs;
 
+  // the step's host inputs (DeviceState::h) are page-locked in place once they
+  // are built, so the end-to-end step's host->device copies are asynchronous
+  // DMA transfers instead of staged pageable copies
+  std::vector<void*> pinned;
+  template <class T>
+  void pin(std::vector<T>& v) {
+    if (v.empty()) return;
+    if (cudaHostRegister(v.data(), v.size() * sizeof(T), cudaHostRegisterDefault) == cudaSuccess)
+      pinned.push_back(v.data());
+    else
+      cudaGetLastError();  // stays pageable (the copies are then staged)
+  }
   ~DeviceState() {
+    for (void* p : pinned) cudaHostUnregister(p);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
     if (e0) cudaEventDestroy(e0);
@@ -1950,6 +1963,16 @@ void Engine::prepare() {
     build_halo(D, m);
   }
   D.prepared = true;
+  D.pin(H.ke);
+  D.pin(H.eke);
+  D.pin(H.escale);
+  D.pin(H.lnode);
+  D.pin(H.pos);
+  D.pin(H.mv);
+  D.pin(H.biface);
+  D.pin(H.bw);
+  D.pin(H.icp);
+  D.pin(H.icpos);
   upload_inputs();
   CK(cudaStreamSynchronize(st));
 }

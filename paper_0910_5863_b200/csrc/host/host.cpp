@@ -1085,24 +1085,32 @@ ChangeOfVariables change_of_variables(const ConstraintSet& cs, const Model& md) 
       for (int t = 0; t < n; ++t) rows[std::size_t(a) * n + t] = cs.averages[bg[gi][a]].weights[t];
     cov.transforms[q] = build_glob_transform(gi, rows, r_in, n);
   }
-  for (std::size_t q = 0; q < constrained.size(); ++q) {
+  // one group per explicit dof, in glob order (offsets first, then the fill in parallel)
+  std::vector<std::size_t> goff(constrained.size() + 1, 0);
+  for (std::size_t q = 0; q < constrained.size(); ++q) goff[q + 1] = goff[q] + cov.transforms[q].rank;
+  cov.groups.resize(goff.back());
+  cov.group_subs.resize(goff.back());
+  cov.group_local.resize(goff.back());
+#pragma omp parallel for schedule(dynamic, 16) if (constrained.size() >= 512)
+  for (int q = 0; q < static_cast<int>(constrained.size()); ++q) {
     const int gi = constrained[q];
     const Glob& g = md.globs[gi];
     const auto& dofs = md.glob_dofs[gi];
     const GlobTransform& gt = cov.transforms[q];
     for (int k = 0; k < gt.rank; ++k) {  // explicit_slots[k] == k
       const i64 gdof = dofs[k];
-      std::vector<i64> grp;
-      std::vector<int> gs, gl;
+      std::vector<i64>& grp = cov.groups[goff[q] + k];
+      std::vector<int>& gs = cov.group_subs[goff[q] + k];
+      std::vector<int>& gl = cov.group_local[goff[q] + k];
+      grp.reserve(g.subdomains.size());
+      gs.reserve(g.subdomains.size());
+      gl.reserve(g.subdomains.size());
       for (int s : g.subdomains) {
         const int l = md.maps.local_of(gdof, s);
         grp.push_back(md.maps.local_to_wc[s][l]);
         gs.push_back(s);
         gl.push_back(l);
       }
-      cov.groups.push_back(std::move(grp));
-      cov.group_subs.push_back(std::move(gs));
-      cov.group_local.push_back(std::move(gl));
     }
   }
   return cov;
