@@ -118,6 +118,19 @@ int bddc_b200_shard_loopback(bddc_b200_t* h, int group, int rank, int world, con
  * peers == NULL. */
 int bddc_b200_halo_plan(const bddc_b200_t* h, const int* owner, int rank, int world, int64_t* n_peers,
                         int64_t* n_shared, int* peers, int* peer_off, int* shared, int* touched, int* owned);
+/* Primal-tree plan of `rank` for the partition `owner` and the current
+ * constraint set (host only; DESIGN.md sections 3.7 and 9): the nested
+ * dissection of the primal unknowns that replaces the reference's single sparse
+ * factorization of the auxiliary operator (bddc_operator.cpp:38-50).  top = the
+ * unknowns of the top front (the same list on every rank; the only front that
+ * is summed over the ranks); the fronts of the boxes inside this rank's block,
+ * deepest level first, with the unknowns each eliminates (front_ptr has
+ * n_fronts + 1 entries).  depth is clamped to what the lattice and the
+ * partition allow (depth_used); world == 1 gives the single-GPU plan.  Query
+ * the counts with top == NULL. */
+int bddc_b200_primal_tree_plan(const bddc_b200_t* h, const int* owner, int rank, int world, int depth,
+                               int64_t* depth_used, int64_t* n_top, int64_t* n_fronts, int64_t* n_own, int* top,
+                               int* front_level, int* front_ptr, int* front_own);
 /* Substructure lattice (nx, ny, nz), substructure ids x-fastest (mesh.cpp:68-70). */
 int bddc_b200_subdomain_lattice(const bddc_b200_t* h, int64_t* dims3);
 

@@ -105,6 +105,9 @@ EXPORTS = {
     "bddc_b200_shard_nccl": (C.c_int, [P, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "bddc_b200_shard_loopback": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "bddc_b200_subdomain_lattice": (C.c_int, [P, I64]),
+    "bddc_b200_primal_tree_plan": (C.c_int, [P, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, I64, I64, I64, I64,
+                                            C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                            C.POINTER(C.c_int)]),
     "bddc_b200_halo_plan": (C.c_int, [P, C.POINTER(C.c_int), C.c_int, C.c_int, I64, I64, C.POINTER(C.c_int),
                                       C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                       C.POINTER(C.c_int)]),
@@ -373,6 +376,24 @@ class BDDC:
         peers = peers[:npeer.value]
         return {"peers": peers.tolist(), "touched": touched.astype(bool), "owned": owned.astype(bool),
                 "shared": {int(p): sh[off[k]:off[k + 1]].copy() for k, p in enumerate(peers)}}
+
+    def primal_tree_plan(self, owner, rank: int, world: int, depth: int) -> dict:
+        """Primal-tree plan of `rank` (host only): the top front's unknowns and,
+        deepest level first, the unknowns each of the rank's own fronts
+        eliminates (the distributed tree of the sharded engine; world 1 = the
+        single-GPU plan)."""
+        own = np.ascontiguousarray(owner, dtype=np.int32)
+        ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+        d, nt, nf, no = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        args = (self._h, ip(own), rank, world, depth, C.byref(d), C.byref(nt), C.byref(nf), C.byref(no))
+        _check(self._lib.bddc_b200_primal_tree_plan(*args, None, None, None, None))
+        top = np.empty(max(nt.value, 1), dtype=np.int32)
+        level = np.empty(max(nf.value, 1), dtype=np.int32)
+        ptr = np.empty(nf.value + 1, dtype=np.int32)
+        fown = np.empty(max(no.value, 1), dtype=np.int32)
+        _check(self._lib.bddc_b200_primal_tree_plan(*args, ip(top), ip(level), ip(ptr), ip(fown)))
+        return {"depth": d.value, "top": top[:nt.value].copy(),
+                "fronts": [(int(level[f]), fown[ptr[f]:ptr[f + 1]].copy()) for f in range(nf.value)]}
 
     def structure(self) -> dict:
         s = _Structure()

@@ -413,6 +413,47 @@ int bddc_b200_halo_plan(const bddc_b200_t* h, const int* owner, int rank, int wo
   });
 }
 
+int bddc_b200_primal_tree_plan(const bddc_b200_t* h, const int* owner, int rank, int world, int depth,
+                               int64_t* depth_used, int64_t* n_top, int64_t* n_fronts, int64_t* n_own, int* top,
+                               int* front_level, int* front_ptr, int* front_own) {
+  return guarded([&] {
+    const Model& m = h->model;
+    const std::vector<int> own(owner, owner + m.subs.size());
+    const ChangeOfVariables cov = change_of_variables(h->cs, m);
+    CoarseBounds bounds;
+    const std::vector<CoarseLeaf> all = primal_leaves(m, cov, &bounds);
+    const int n_primal = static_cast<int>(m.maps.corner_dof_count + cov.groups.size());
+    int maxd = coarse_tree_max_depth(m.mesh.sub);
+    if (world > 1) maxd = coarse_tree_shard_depth(m.mesh.sub, own, maxd);
+    const int d = std::max(0, std::min(depth, maxd));
+    std::vector<CoarseLeaf> mine;
+    for (std::size_t s = 0; s < all.size(); ++s)
+      if (world <= 1 || own[s] == rank) mine.push_back(all[s]);
+    const CoarseTree t = plan_coarse_tree(mine, m.mesh.sub, n_primal, d, 12288, true, world > 1 ? &bounds : nullptr);
+    *depth_used = d;
+    *n_top = static_cast<int64_t>(t.top.size());
+    int64_t nf = 0, no = 0;
+    for (const auto& L : t.levels)
+      for (const auto& f : L.fronts) {
+        ++nf;
+        no += static_cast<int64_t>(f.own.size());
+      }
+    *n_fronts = nf;
+    *n_own = no;
+    if (!top) return;
+    std::copy(t.top.begin(), t.top.end(), top);
+    int64_t fi = 0, at = 0;
+    front_ptr[0] = 0;
+    for (std::size_t l = 0; l < t.levels.size(); ++l)
+      for (const auto& f : t.levels[l].fronts) {
+        front_level[fi] = static_cast<int>(l);
+        std::copy(f.own.begin(), f.own.end(), front_own + at);
+        at += static_cast<int64_t>(f.own.size());
+        front_ptr[++fi] = static_cast<int>(at);
+      }
+  });
+}
+
 int bddc_b200_export_matrix_market(bddc_b200_t* h, const char* stem) {
   return guarded([&] {
     const ChangeOfVariables cov = change_of_variables(h->cs, h->model);

@@ -2324,26 +2324,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     std::vector<CoarseLeaf> all_leaves;
     if (D.comm) {
       maxd = coarse_tree_shard_depth(m.mesh.sub, D.owner, maxd);
-      bounds.lo.assign(3 * (size_t)D.n_primal, 1 << 30);
-      bounds.hi.assign(3 * (size_t)D.n_primal, -1);
-      all_leaves.resize(ns);
-      for (int s = 0; s < ns; ++s)
-        for (int a = 0; a < 3; ++a) all_leaves[s].coord[a] = m.subs[s].origin[a] / m.mesh.epe;
-      auto hold = [&](int k, int s) {
-        all_leaves[s].coarse.push_back(k);
-        for (int a = 0; a < 3; ++a) {
-          bounds.lo[3 * (size_t)k + a] = std::min(bounds.lo[3 * (size_t)k + a], all_leaves[s].coord[a]);
-          bounds.hi[3 * (size_t)k + a] = std::max(bounds.hi[3 * (size_t)k + a], all_leaves[s].coord[a] + 1);
-        }
-      };
-      for (std::size_t g = 0; g < m.globs.size(); ++g)
-        for (i64 dof : m.glob_dofs[g]) {
-          const i64 cid = m.maps.corner_dof_of_global[dof];
-          if (cid < 0) continue;
-          for (int s : m.globs[g].subdomains) hold(static_cast<int>(cid), s);
-        }
-      for (std::size_t g = 0; g < cov.groups.size(); ++g)
-        for (int s : cov.group_subs[g]) hold(static_cast<int>(ncd + g), s);
+      all_leaves = primal_leaves(m, cov, &bounds);
     }
     const std::vector<CoarseLeaf>& cost_leaves = D.comm ? all_leaves : leaves;
     const char* env = std::getenv("BDDC_B200_ROOT_DEPTH");

@@ -1116,6 +1116,36 @@ ChangeOfVariables change_of_variables(const ConstraintSet& cs, const Model& md) 
   return cov;
 }
 
+std::vector<CoarseLeaf> primal_leaves(const Model& md, const ChangeOfVariables& cov, CoarseBounds* bounds) {
+  const int ns = static_cast<int>(md.subs.size());
+  const i64 ncd = md.maps.corner_dof_count;
+  const std::size_t n_primal = static_cast<std::size_t>(ncd) + cov.groups.size();
+  std::vector<CoarseLeaf> leaves(ns);
+  for (int s = 0; s < ns; ++s)
+    for (int a = 0; a < 3; ++a) leaves[s].coord[a] = md.subs[s].origin[a] / md.mesh.epe;
+  if (bounds) {
+    bounds->lo.assign(3 * n_primal, 1 << 30);
+    bounds->hi.assign(3 * n_primal, -1);
+  }
+  auto hold = [&](std::size_t k, int s) {
+    leaves[s].coarse.push_back(static_cast<int>(k));
+    if (!bounds) return;
+    for (int a = 0; a < 3; ++a) {
+      bounds->lo[3 * k + a] = std::min(bounds->lo[3 * k + a], leaves[s].coord[a]);
+      bounds->hi[3 * k + a] = std::max(bounds->hi[3 * k + a], leaves[s].coord[a] + 1);
+    }
+  };
+  for (std::size_t g = 0; g < md.globs.size(); ++g)
+    for (i64 dof : md.glob_dofs[g]) {
+      const i64 cid = md.maps.corner_dof_of_global[dof];
+      if (cid < 0) continue;
+      for (int s : md.globs[g].subdomains) hold(static_cast<std::size_t>(cid), s);
+    }
+  for (std::size_t g = 0; g < cov.groups.size(); ++g)
+    for (int s : cov.group_subs[g]) hold(static_cast<std::size_t>(ncd) + g, s);
+  return leaves;
+}
+
 // ============================================================================
 // Pairs (pair.cpp:67-146, adaptive.cpp:12-20)
 // ============================================================================

@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include "coarse_tree.hpp"
+
 namespace b200 {
 
 using i64 = std::int64_t;
@@ -234,6 +236,13 @@ struct ChangeOfVariables {
   std::vector<std::vector<int>> group_local;  // member local dofs
 };
 ChangeOfVariables change_of_variables(const ConstraintSet& cs, const Model& m);
+
+/// Leaves of the primal tree over ALL substructures (coarse_tree.hpp): the
+/// primal unknowns each substructure holds (corner dofs by corner id, then one
+/// unknown per explicit-dof group of `cov`, numbered corner_dof_count + group)
+/// and its lattice position; `bounds` receives every unknown's bounding box.
+/// Global host data: every rank of a sharded engine computes the same lists.
+std::vector<CoarseLeaf> primal_leaves(const Model& md, const ChangeOfVariables& cov, CoarseBounds* bounds);
 
 // --- pairs (pair.cpp:67-209) ---------------------------------------------------
 struct PairIndex {

@@ -124,6 +124,25 @@ def _worker(rank, world, port, errors):
                 if p.maps.local_is_corner[s][l]:
                     glob[cid] += 1.0
         assert np.array_equal(rt.numpy(), glob)
+        # distributed primal tree: this rank's fronts and the
+        # other rank's partition the primal unknowns outside the top front, the
+        # top front is the same list on both ranks and equals the single plan's
+        tb = pb.BDDC(pb.Problem.cube((4, 2, 2), 3, "scalar"))
+        tb.arithmetic_constraints(True, True)
+        town = shard.partition((4, 2, 2), world)
+        single = tb.primal_tree_plan(town, 0, 1, 1)
+        tplan = tb.primal_tree_plan(town, rank, world, 1)
+        assert tplan["depth"] == 1 and np.array_equal(tplan["top"], single["top"])
+        n_primal = len(single["top"]) + sum(len(o) for _, o in single["fronts"])
+        mine = np.zeros(n_primal)
+        for _, o in tplan["fronts"]:
+            mine[o] += 1.0
+        both = torch.from_numpy(mine.copy())
+        dist.all_reduce(both)
+        expect = np.ones(n_primal)
+        expect[single["top"]] = 0.0
+        assert np.array_equal(both.numpy(), expect)  # every eliminated unknown on exactly one rank
+        assert mine.sum() > 0 and mine.sum() < expect.sum()
         # bench.py's multi-rank harness
         import bench
         bench.barrier(dist)
@@ -148,3 +167,37 @@ def test_sharded_interface_operations_gloo():
         msgs.append(errors.get())
     assert not msgs, "\n".join(msgs)
     assert all(pr.exitcode == 0 for pr in procs)
+
+
+@pytest.mark.parametrize("sub,world,depth", [((4, 4, 4), 2, 2), ((4, 4, 4), 4, 2), ((4, 4, 4), 8, 2),
+                                              ((3, 3, 3), 2, 1), ((6, 6, 6), 8, 2), ((6, 4, 2), 4, 1)])
+def test_distributed_primal_tree_plan(sub, world, depth):
+    """Every rank plans the boxes of the primal tree from the unknowns' global
+    bounds and keeps the fronts inside its own block: together the ranks hold
+    exactly the single-GPU plan's fronts (same unknowns per front, each on one
+    rank, every front inside its owner's block), and all share its top front."""
+    import paper_0910_5863_b200 as pb
+    b = pb.BDDC(pb.Problem.cube(sub, 2, "scalar"))
+    b.arithmetic_constraints(True, True)
+    owner = shard.partition(sub, world)
+    single = b.primal_tree_plan(owner, 0, 1, depth)
+    assert single["depth"] == depth
+    want = sorted((lvl, tuple(o)) for lvl, o in single["fronts"] if len(o))
+    got = []
+    for r in range(world):
+        p = b.primal_tree_plan(owner, r, world, depth)
+        assert p["depth"] == depth and np.array_equal(p["top"], single["top"])
+        got += [(lvl, tuple(o)) for lvl, o in p["fronts"] if len(o)]
+    assert sorted(got) == want
+
+
+def test_misaligned_partition_keeps_dense_root():
+    """A partition whose blocks cut through the depth-1 boxes (three ranks along
+    x on a lattice the boxes halve) falls back to depth 0 on every rank."""
+    import paper_0910_5863_b200 as pb
+    b = pb.BDDC(pb.Problem.cube((6, 2, 2), 2, "scalar"))
+    b.arithmetic_constraints(True, True)
+    owner = shard.partition((6, 2, 2), 3)
+    for r in range(3):
+        p = b.primal_tree_plan(owner, r, 3, 2)
+        assert p["depth"] == 0 and not p["fronts"]
