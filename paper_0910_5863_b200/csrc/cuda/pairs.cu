@@ -877,6 +877,10 @@ struct PairPrep {
   std::vector<Hub> hubs;
   int request = 0;
   double prep_ms = 0.0;
+  // hub stage (PairEngine::start): padded sizes and arena offsets of the hubs
+  bool started = false;
+  std::vector<int> hubNH, hubPH;
+  std::vector<long long> hubOff;
 };
 
 namespace {
@@ -1205,20 +1209,15 @@ std::shared_ptr<PairPrep> PairEngine::prepare(const ConstraintSet& cs, const Enr
   return prep;
 }
 
-EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std::shared_ptr<PairPrep> prep) {
-  NvtxRange nvtx("bddc:eigen");
-  using clk = std::chrono::steady_clock;
-  const bool overlapped = prep != nullptr;
-  if (!prep) prep = prepare(cs, o);
-  const auto h1 = clk::now();
-  const Model& m = *m_;
-  const std::vector<HostPair>& hp = prep->hp;
-  const int np = static_cast<int>(hp.size());
-  const int request = prep->request;
-  // device buffers, processed in chunks bounded by a memory budget
-  EnrichOutcome out;
-  std::vector<std::vector<double>> all_evals(np), all_funcs(np);
-  std::vector<int> all_k(np);
+// Reserves the pair stage's arenas and enqueues the hub stage (gather +
+// partial Cholesky of the hubs) on the engine's stream.  It needs only the
+// preparation and the substructures' S_s, which the stream produces before it,
+// so Engine::step calls it BEFORE waiting for the leaf factorization: the
+// device goes from the analysis straight into the hubs while the host checks
+// the pivots and builds the first chunk's descriptors.
+void PairEngine::start(const std::shared_ptr<PairPrep>& prep) {
+  if (prep->started) return;
+  prep->started = true;
   // Arenas sized once for the largest chunk: views into the engine's stage
   // arena (no allocation between chunks or steps; see StageArena).
   {
@@ -1247,12 +1246,16 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       for (int i = 0; i < 12; ++i) bufs[i]->alloc(want[i]);
     hr.mark("alloc");
   }
-  // hub stage of the two-level side fronts: [rest | U] gathered from S_s, the
-  // rest eliminated once per hub (Schur complement onto U in the trailing block)
   const auto& hubs = prep->hubs;
   const int nh = static_cast<int>(hubs.size());
-  std::vector<int> hubNH(nh), hubPH(nh);
-  std::vector<long long> hubOff(nh);
+  std::vector<int>& hubNH = prep->hubNH;
+  std::vector<int>& hubPH = prep->hubPH;
+  std::vector<long long>& hubOff = prep->hubOff;
+  hubNH.assign(nh, 0);
+  hubPH.assign(nh, 0);
+  hubOff.assign(nh, 0);
+  // hub stage of the two-level side fronts: [rest | U] gathered from S_s, the
+  // rest eliminated once per hub (Schur complement onto U in the trailing block)
   {
     HostTimer hth("enrich hubs");
     PairBuffers& B_ = *bufs_;
@@ -1302,6 +1305,28 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
       hprof.mark("cholHub");
     }
   }
+}
+
+EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std::shared_ptr<PairPrep> prep) {
+  NvtxRange nvtx("bddc:eigen");
+  using clk = std::chrono::steady_clock;
+  const bool overlapped = prep != nullptr;
+  if (!prep) prep = prepare(cs, o);
+  const auto h1 = clk::now();
+  const Model& m = *m_;
+  const std::vector<HostPair>& hp = prep->hp;
+  const int np = static_cast<int>(hp.size());
+  const int request = prep->request;
+  // device buffers, processed in chunks bounded by a memory budget
+  EnrichOutcome out;
+  std::vector<std::vector<double>> all_evals(np), all_funcs(np);
+  std::vector<int> all_k(np);
+  start(prep);  // arenas and hub stage (a no-op when Engine::step started it already)
+  const auto& hubs = prep->hubs;
+  const int nh = static_cast<int>(hubs.size());
+  const std::vector<int>& hubNH = prep->hubNH;
+  const std::vector<int>& hubPH = prep->hubPH;
+  const std::vector<long long>& hubOff = prep->hubOff;
   int p0 = 0;
   std::size_t chunk_id = 0;
   while (p0 < np) {

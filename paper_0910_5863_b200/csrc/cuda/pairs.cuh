@@ -35,6 +35,9 @@ class PairEngine {
   /// Host-side preparation (pair index spaces, kernel bases, rigid modes); no
   /// device work, so it can run while the device is busy.
   std::shared_ptr<PairPrep> prepare(const ConstraintSet& cs, const EnrichOptions& o) const;
+  /// Reserves the arenas and enqueues the hub stage on the stream (it follows
+  /// the leaf factorization in stream order); enrich calls it if nobody did.
+  void start(const std::shared_ptr<PairPrep>& prep);
   EnrichOutcome enrich(ConstraintSet& cs, const EnrichOptions& o, std::shared_ptr<PairPrep> prep = nullptr);
 
  private:
