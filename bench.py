@@ -100,8 +100,15 @@ def measured_traffic(config):
         rec = data.get("cfg%d_%s" % (config, phase))
         if rec:
             out[phase] = rec["dram_bytes_read"] + rec["dram_bytes_write"]
+            # the leaf roofline is the batched partial Cholesky alone: its own launch
+            # (k_chol_dag), not the assembly, zero-fill and copies of the phase
+            chol = [v for k, v in rec.get("by_kernel_bytes", {}).items() if k.endswith("k_chol_dag")]
+            if phase == "leaf" and chol:
+                out["leaf_phase"] = out["leaf"]
+                out["leaf"] = sum(chol)
     if out:
-        out["source"] = "profiles/%s (ncu dram__bytes_{read,write}.sum over one phase)" % name
+        out["source"] = ("profiles/%s (ncu dram__bytes_{read,write}.sum: the k_chol_dag launch of one leaf "
+                         "factorization; every launch of one Schur + preconditioner apply)" % name)
     return out
 
 
@@ -407,6 +414,8 @@ def main():
             "peak_source": "measured cuBLAS DGEMM (MEASURED_PEAKS.json has bf16 only)",
             "flops_per_launch": lf_flops, "seconds_per_launch": lf_t,
             "share_of_step": lf_t / sec_per_step}
+    if traffic.get("leaf_phase"):
+        roof["traffic_leaf_phase"] = traffic["leaf_phase"]  # with assembly, zero-fill, S copy and rhs sweep
     # second roofline: the HBM-bound PCG iteration (Schur apply + both leaf
     # sweeps + root apply), algorithmic bytes over the device-timed PCG phase
     tm = b.times()
