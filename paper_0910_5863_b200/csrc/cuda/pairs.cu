@@ -1327,6 +1327,66 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
   const std::vector<int>& hubNH = prep->hubNH;
   const std::vector<int>& hubPH = prep->hubPH;
   const std::vector<long long>& hubOff = prep->hubOff;
+  // The chunks are pipelined: chunk c's results are copied into their own part
+  // of the page-locked buffers behind its kernels (an event marks the end), the
+  // host goes on to build and enqueue chunk c + 1 (stream order protects the
+  // arenas the chunks share) and reads chunk c's results while c + 1 runs.
+  const std::size_t nchunks = prep->chunks.size();
+  std::vector<std::size_t> hoE(nchunks + 1, 0), hoFu(nchunks + 1, 0), hoInf(nchunks + 1, 0);
+  {
+    int q0 = 0;
+    for (std::size_t c = 0; c < nchunks; ++c) {
+      const ChunkHost& ch = prep->chunks[c];
+      hoE[c + 1] = hoE[c] + static_cast<std::size_t>(std::max<long long>(ch.nE, 1));
+      hoFu[c + 1] = hoFu[c] + static_cast<std::size_t>(std::max<long long>(ch.nFu, 1));
+      hoInf[c + 1] = hoInf[c] + 4 * static_cast<std::size_t>(ch.p1 - q0);
+      q0 = ch.p1;
+    }
+    bufs_->h_ev.reserve(hoE[nchunks]);
+    bufs_->h_fu.reserve(hoFu[nchunks]);
+    bufs_->h_inf.reserve(hoInf[nchunks]);
+  }
+  std::vector<cudaEvent_t> chunk_done(nchunks, nullptr);
+  struct EventGuard {
+    std::vector<cudaEvent_t>& v;
+    ~EventGuard() {
+      for (cudaEvent_t e : v)
+        if (e) cudaEventDestroy(e);
+    }
+  } event_guard{chunk_done};
+  auto finish_chunk = [&](std::size_t c) {
+    const ChunkHost& ch = prep->chunks[c];
+    const int q0 = c == 0 ? 0 : prep->chunks[c - 1].p1, nb = ch.p1 - q0;
+    CK(cudaEventSynchronize(chunk_done[c]));
+    if (c == 0 && nh) {
+      std::vector<int> hinf(nh);
+      CK(cudaMemcpy(hinf.data(), bufs_->hinfo.p, nh * sizeof(int), cudaMemcpyDeviceToHost));
+      for (int q = 0; q < nh; ++q)
+        if (hinf[q])
+          throw Error(kNotPositiveDefinite, "pair eigenproblem hub of substructure " + std::to_string(hubs[q].s) +
+                                                ": reduction not positive definite");
+    }
+    const double* ev = bufs_->h_ev.p + hoE[c];
+    const double* fu = bufs_->h_fu.p + hoFu[c];
+    const int* inf = bufs_->h_inf.p + hoInf[c];
+    for (int b = 0; b < nb; ++b)
+      for (int q = 0; q < 4; ++q)
+        if (inf[4 * b + q])
+          throw Error(kNotPositiveDefinite, "pair eigenproblem " + std::to_string(hp[q0 + b].idx.si) + "," +
+                                                std::to_string(hp[q0 + b].idx.sj) + ": reduction not positive definite");
+#pragma omp parallel for schedule(static) if (nb >= 256)
+    for (int b = 0; b < nb; ++b) {
+      const Dims& dm = ch.dims[b];
+      const HostPair& h = hp[q0 + b];
+      // eigenvalue list of generalized_eig_sym: top min(request, r) with zeros beyond rank(lhs)
+      const int take = std::min(request, std::max(h.r_total, 0));
+      std::vector<double> lam(take, 0.0);
+      for (int q = 0; q < std::min(dm.k, take); ++q) lam[q] = ev[ch.oE[b] + q];
+      all_evals[q0 + b] = lam;
+      all_funcs[q0 + b].assign(fu + ch.oFu[b], fu + ch.oFu[b] + (long long)dm.nf * dm.k);
+      all_k[q0 + b] = dm.k;
+    }
+  };
   int p0 = 0;
   std::size_t chunk_id = 0;
   while (p0 < np) {
@@ -1532,40 +1592,24 @@ EnrichOutcome PairEngine::enrich(ConstraintSet& cs, const EnrichOptions& o, std:
     CK(cudaGetLastError());
     prof.mark("vectors");
     ht.mark("launch");
-    // results into page-locked buffers: the copies queue behind the kernels
-    const double* ev = B_.h_ev.reserve(E.n);
-    const double* fu = B_.h_fu.reserve(Fu.n);
-    const int* inf = B_.h_inf.reserve(4 * nb);
-    CK(cudaMemcpyAsync(B_.h_ev.p, E.p, E.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
-    CK(cudaMemcpyAsync(B_.h_fu.p, Fu.p, Fu.n * sizeof(double), cudaMemcpyDeviceToHost, st_));
-    CK(cudaMemcpyAsync(B_.h_inf.p, info.p, 4 * nb * sizeof(int), cudaMemcpyDeviceToHost, st_));
-    CK(cudaStreamSynchronize(st_));
-    ht.mark("device_wait+copy");
-    if (chunk_id == 1 && nh) {
-      std::vector<int> hinf(nh);
-      CK(cudaMemcpy(hinf.data(), B_.hinfo.p, nh * sizeof(int), cudaMemcpyDeviceToHost));
-      for (int q = 0; q < nh; ++q)
-        if (hinf[q])
-          throw Error(kNotPositiveDefinite, "pair eigenproblem hub of substructure " + std::to_string(hubs[q].s) +
-                                                ": reduction not positive definite");
-    }
-    for (int b = 0; b < nb; ++b) {
-      for (int q = 0; q < 4; ++q)
-        if (inf[4 * b + q])
-          throw Error(kNotPositiveDefinite, "pair eigenproblem " + std::to_string(hp[p0 + b].idx.si) + "," +
-                                                std::to_string(hp[p0 + b].idx.sj) + ": reduction not positive definite");
-      const Dims& dm = dims[b];
-      const HostPair& h = hp[p0 + b];
-      // eigenvalue list of generalized_eig_sym: top min(request, r) with zeros beyond rank(lhs)
-      const int take = std::min(request, std::max(h.r_total, 0));
-      std::vector<double> lam(take, 0.0);
-      for (int q = 0; q < std::min(dm.k, take); ++q) lam[q] = ev[oE[b] + q];
-      all_evals[p0 + b] = lam;
-      all_funcs[p0 + b].assign(fu + oFu[b], fu + oFu[b] + (long long)dm.nf * dm.k);
-      all_k[p0 + b] = dm.k;
+    // results into this chunk's part of the page-locked buffers: the copies
+    // queue behind the kernels, the event behind the copies
+    {
+      const std::size_t c = chunk_id - 1;
+      CK(cudaMemcpyAsync(B_.h_ev.p + hoE[c], E.p, static_cast<std::size_t>(std::max<long long>(nE, 1)) * sizeof(double),
+                         cudaMemcpyDeviceToHost, st_));
+      CK(cudaMemcpyAsync(B_.h_fu.p + hoFu[c], Fu.p,
+                         static_cast<std::size_t>(std::max<long long>(nFu, 1)) * sizeof(double),
+                         cudaMemcpyDeviceToHost, st_));
+      CK(cudaMemcpyAsync(B_.h_inf.p + hoInf[c], info.p, 4 * nb * sizeof(int), cudaMemcpyDeviceToHost, st_));
+      CK(cudaEventCreateWithFlags(&chunk_done[c], cudaEventDisableTiming));
+      CK(cudaEventRecord(chunk_done[c], st_));
+      if (c > 0) finish_chunk(c - 1);  // while this chunk runs
+      ht.mark("previous_results");
     }
     p0 = p1;
   }
+  if (nchunks) finish_chunk(nchunks - 1);
   const auto h2 = clk::now();
   // host selection, splitting and rank filter (adaptive.cpp:66-125).  The
   // candidate averages are enumerated in the sequential order; whether one is
