@@ -1171,6 +1171,48 @@ __global__ void __launch_bounds__(256) k_prolong_copy(const SubDesc* sd, const i
   }
 }
 
+// Prolongation in one launch: the first pos_blocks CTAs copy the boundary
+// positions that take a leaf-vector entry, the others form the constrained rows
+// of the glob transforms (one warp per item, as prolong_item) and write the
+// weighted value straight to the item's own boundary position (item_e) -- the
+// same products as k_prolong_items + k_prolong_copy without the dependency
+// between two launches.
+__global__ void __launch_bounds__(256) k_prolong_fused(const SubDesc* sd, XformDesc x, const int2* __restrict__ wpos,
+                                                       const int* __restrict__ wsrc, int nw, int pos_blocks,
+                                                       const int* __restrict__ item_sub,
+                                                       const int* __restrict__ item_e, int nitems,
+                                                       const double* __restrict__ fv, const int* done) {
+  if (done && *done) return;
+  if (static_cast<int>(blockIdx.x) < pos_blocks) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nw; e += pos_blocks * blockDim.x) {
+      const int src = wsrc[e];
+      if (src < 0) continue;
+      const int2 sb = wpos[e];
+      const SubDesc& d = sd[sb.x];
+      d.WB[sb.y] = d.bw[sb.y] * fv[src];
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int warps = ((gridDim.x - pos_blocks) * blockDim.x) >> 5;
+  for (int k = ((blockIdx.x - pos_blocks) * blockDim.x + threadIdx.x) >> 5; k < nitems; k += warps) {
+    const SubDesc& d = sd[item_sub[k]];
+    const int inst = x.item_inst[k], i = x.item_row[k];
+    const int tr = x.inst_tr[inst];
+    const int* pos = x.tpos + x.inst_pos[inst];
+    const int n = x.tr_n[tr];
+    const double* D = x.D + x.tr_off_d[tr] + i * n;
+    double s = 0.0;
+    for (int jj = lane; jj < n; jj += 32) s += D[jj] * d.FV[d.posF[pos[jj]]];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const int2 sb = wpos[item_e[k]];
+      d.WB[sb.y] = d.bw[sb.y] * s;
+    }
+  }
+}
+
 // Leaf forward, one kFwdTile-column tile of E per call: b_e staged once, each
 // warp owns kFwdTile / 8 columns and keeps two of them (up to 16 loads) in
 // flight.  16-column tiles give the 27 fronts of configs 1-2 756 work units
@@ -1589,7 +1631,7 @@ struct DeviceState {
   DBuf<int2> wpos;
   UploadBatch up_index, up_desc;  // set_constraints' small uploads (one copy each)
   int nw = 0;
-  DBuf<int> wsrc, wsrcg, item_sub;
+  DBuf<int> wsrc, wsrcg, item_sub, item_e;
   DBuf<double> yglob;
   int nitems = 0;
   DBuf<PcgState> pst;
@@ -2422,7 +2464,8 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       D.wpos.upload(wp, st);
       D.nw = static_cast<int>(w0[no]);
     }
-    std::vector<int> wsrc(std::max<long long>(w0[no], 1)), isub(item_inst.size());
+    std::vector<int> wsrc(std::max<long long>(w0[no], 1)), isub(item_inst.size()),
+        item_e(std::max<std::size_t>(item_inst.size(), 1), 0);
     std::vector<int> wsrcg(std::max<std::size_t>(D.WB.n, 1), 0);  // unowned positions: never summed by phase H
 #pragma omp parallel for schedule(dynamic, 16) if (no >= 64)
     for (int q = 0; q < no; ++q) {
@@ -2435,8 +2478,10 @@ void Engine::set_constraints(const ConstraintSet& cs) {
         if (inst >= 0) {
           const int tr = inst_tr[inst];
           const int i = iperm[tr_off_perm[tr] + bslot[w]];
-          if (i < tr_r[tr])
+          if (i < tr_r[tr]) {
             src = -1 - (item_ptr[q] + inst_loff[inst] + i);
+            item_e[item_ptr[q] + inst_loff[inst] + i] = static_cast<int>(w0[q] + b);
+          }
           else
             src = static_cast<int>(D.fv_off[s]) + posF[D.wb_off[s] + tpos[inst_pos[inst] + i]];
         }
@@ -2447,6 +2492,7 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     up_i(D.wsrc, wsrc);
     up_i(D.wsrcg, wsrcg);
     up_i(D.item_sub, isub);
+    up_i(D.item_e, item_e);
     D.nitems = static_cast<int>(item_inst.size());
     D.yglob.alloc(std::max(D.nitems, 1));
   }
@@ -2956,12 +3002,9 @@ void launch_precond(DeviceState& D, const double* r, double* z, const double* do
   }  // kPreSolve
   if (!(stages & kPreProlong)) return;
   if (ns) {
-    if (D.nitems) {
-      k_prolong_items<<<std::max(1, std::min(4 * sm_count(), (D.nitems + 7) / 8)), 256, 0, st>>>(
-          D.subdesc.p, D.xf, D.item_sub.p, D.nitems, D.yglob.p, done);
-      count_launch(1);
-    }
-    k_prolong_copy<<<pos_blocks, 256, 0, st>>>(D.subdesc.p, D.wpos.p, D.wsrc.p, nw, D.FV.p, D.yglob.p, done);
+    const int item_blocks = D.nitems ? std::max(1, std::min(4 * sm_count(), (D.nitems + 7) / 8)) : 0;
+    k_prolong_fused<<<pos_blocks + item_blocks, 256, 0, st>>>(D.subdesc.p, D.xf, D.wpos.p, D.wsrc.p, nw, pos_blocks,
+                                                             D.item_sub.p, D.item_e.p, D.nitems, D.FV.p, done);
   }
   mark("prolong");
   k_sum_copies<<<kRed, 256, 0, st>>>(D.niface, D.icopy_ptr.p, D.icopy_pos.p, D.WB.p, z, D.comm ? nullptr : dot_with,
