@@ -11,6 +11,7 @@
 #include <string>
 
 #include "../host/host.hpp"
+#include "dense.cuh"
 #include "devbuf.cuh"
 
 namespace b200 {
@@ -69,7 +70,12 @@ std::map<int, std::shared_ptr<LoopGroup>> g_groups;
 
 class LoopbackComm : public Comm {
  public:
-  LoopbackComm(std::shared_ptr<LoopGroup> g, int rank) : g_(std::move(g)), rank_(rank) {}
+  LoopbackComm(std::shared_ptr<LoopGroup> g, int rank) : g_(std::move(g)), rank_(rank) {
+    if (g_->world > 1) shared_device_users(+1);  // the ranks' engines launch concurrently on one GPU
+  }
+  ~LoopbackComm() override {
+    if (g_->world > 1) shared_device_users(-1);
+  }
   int rank() const override { return rank_; }
   int world() const override { return g_->world; }
   void allreduce(double* d, std::size_t n, cudaStream_t st) override {

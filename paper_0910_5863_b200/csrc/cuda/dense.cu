@@ -1836,6 +1836,8 @@ bool use_dag(int batch, int nt, int pt) {
   return true;
 }
 
+std::atomic<int> g_shared_device{0};
+
 void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, int mt, cudaStream_t stream) {
   const int smem = 4 * KC * LDS * sizeof(double);
   const int per_sm = per_device(reinterpret_cast<const void*>(&k_chol_dag), [] {
@@ -1849,6 +1851,7 @@ void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, i
   // chunked mode (dedicated diagonal workers, trailing updates per column) when
   // the fronts leave most of the grid to the queue; BDDC_B200_DAGW=0|1 overrides
   bool chunked = 2L * batch <= sm_count() && resident >= 2L * sm_count();
+  if (g_shared_device.load(std::memory_order_relaxed) > 0) chunked = false;  // see shared_device_users
   if (const char* e = std::getenv("BDDC_B200_DAGW"); e && *e) chunked = *e == '1' && 3L * batch <= resident;
   long total;
   int cw = 1, bq = 6;
@@ -1871,6 +1874,8 @@ void partial_cholesky_dag(const FrontDesc* d_descs, int batch, int nt, int pt, i
   count_launch(1);
 }
 }  // namespace
+
+void shared_device_users(int delta) { g_shared_device.fetch_add(delta, std::memory_order_relaxed); }
 
 void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p, int max_m,
                       cudaStream_t stream) {

@@ -84,6 +84,15 @@ void chol_trace(bool on, unsigned long long* out);
 void partial_cholesky(const FrontDesc* d_descs, int batch, int max_n, int max_p, int max_m,
                       cudaStream_t stream);
 
+/// Several engines share this device and launch concurrently (the loopback
+/// ranks of the tests: host threads of one process on one GPU).  The dataflow
+/// Cholesky's chunked mode (diagonal workers and two task queues) needs its
+/// whole grid resident at once, which concurrent launches of other engines can
+/// deny; while the count is non-zero small batches take the plain queue, whose
+/// tasks wait only for tasks already held by running CTAs (deadlock-free for
+/// any residency).  One process per GPU never sets it.
+void shared_device_users(int delta);
+
 /// Forward sweep x <- [L_ee^{-1} x_e ; x_c - L_ce L_ee^{-1} x_e] per front.
 void front_forward(const SolveDesc* d_descs, int batch, int max_n, cudaStream_t stream,
                    const int* done = nullptr);

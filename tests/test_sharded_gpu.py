@@ -127,6 +127,9 @@ CASES = [
      ("adaptive", 10.0, 15), {"BDDC_B200_ROOT_DEPTH": "2"}),
     ("cfg5 4x4x4 H/h=2 w8 tree2", lambda: pb.BDDC(config=5, subdomains=(4, 4, 4), elements_per_edge=2), 8,
      ("adaptive", 10.0, 15), {"BDDC_B200_ROOT_DEPTH": "2"}),
+    # tree levels as factors and sweeps (batches of one and eight fronts per rank)
+    ("cfg5 4x4x4 H/h=2 w8 tree2 factor", lambda: pb.BDDC(config=5, subdomains=(4, 4, 4), elements_per_edge=2), 8,
+     ("adaptive", 10.0, 15), {"BDDC_B200_ROOT_DEPTH": "2", "BDDC_B200_TREE": "factor", "BDDC_B200_LEAF": "factor"}),
     ("cfg4 3x3x3 H/h=4 w2 tree1", lambda: pb.BDDC(config=4, subdomains=(3, 3, 3), elements_per_edge=4), 2,
      ("adaptive", 10.0, 15), {"BDDC_B200_ROOT_DEPTH": "1"}),
 ]
@@ -159,8 +162,14 @@ def test_sharded_equals_single(case, monkeypatch):
         assert len(g["reports"]) == len(ref["reports"])
         for a, o in zip(g["reports"], ref["reports"]):
             assert (a["si"], a["sj"], a["enforced"], a["saturated"]) == (o["si"], o["sj"], o["enforced"], o["saturated"])
-            assert np.allclose(a["eigenvalues"], o["eigenvalues"], rtol=1e-9, atol=0)
-            assert abs(a["omega_next"] - o["omega_next"]) <= 1e-9 * max(o["omega_next"], 1e-12)
+            # the ranks share one GPU here, so their small batches are factored
+            # with the plain task queue (dense.cuh shared_device_users) and the
+            # single engine's with diagonal workers: same sums in a different
+            # order, roundoff amplified by the coefficient contrast (cfg2: 1e6);
+            # BASELINE.json asks for 1e-6
+            assert np.allclose(a["eigenvalues"], o["eigenvalues"], rtol=1e-7, atol=0), \
+                np.max(np.abs(np.array(a["eigenvalues"]) / np.array(o["eigenvalues"]) - 1))
+            assert abs(a["omega_next"] - o["omega_next"]) <= 1e-7 * max(o["omega_next"], 1e-12)
         assert rel(g["schur"], ref["schur"]) <= 1e-11
         assert rel(g["rhs"], ref["rhs"]) <= 1e-11
         # the root is summed per rank and then across ranks: a different rounding
