@@ -167,7 +167,7 @@ class UploadBatch {
   }
   // large arrays are copied by several threads (page-locked destination)
   static void copy(char* dst, const void* src, std::size_t bytes) {
-    const std::size_t chunk = std::size_t(1) << 20;
+    const std::size_t chunk = std::size_t(1) << 18;  // arrays of 1 MB and more are split
     if (bytes < 4 * chunk) {
       std::memcpy(dst, src, bytes);
       return;

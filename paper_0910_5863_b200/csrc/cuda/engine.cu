@@ -2234,11 +2234,13 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       for (int s : m.globs[cov.transforms[k].glob].subdomains)
         if (D.is_own[s]) inst_sub[inst++] = s;
     std::vector<std::vector<int>> by_sub(ns);
-    for (std::size_t inst = 0; inst < inst_tr.size(); ++inst) {
+    const int ninst = static_cast<int>(inst_tr.size());
+#pragma omp parallel for schedule(static) if (ninst >= 1024)
+    for (int inst = 0; inst < ninst; ++inst) {
       const int tr = inst_tr[inst];
       for (int i = 0; i < tr_n[tr]; ++i) cpos[inst_pos[inst] + i] = tpos[inst_pos[inst] + perm[tr_off_perm[tr] + i]];
-      by_sub[inst_sub[inst]].push_back(static_cast<int>(inst));
     }
+    for (int inst = 0; inst < ninst; ++inst) by_sub[inst_sub[inst]].push_back(inst);
     D.max_rows = 0;
     for (int q = 0; q < no; ++q) {  // compacted over the owned substructures (k_prolong's blocks)
       const int s = D.own[q];
@@ -2327,11 +2329,6 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     D.max_M = std::max(D.max_M, D.NF[s] - D.PE[s]);
     D.max_NA = std::max(D.max_NA, D.NA[s]);
     D.max_MA = std::max(D.max_MA, D.NA[s] - D.PE[s]);
-    std::vector<int> is_coarse(nB, -1);
-    for (int c = 0; c < nC; ++c) is_coarse[coarse_b[s][c]] = c;
-    int e = 0;
-    for (int b = 0; b < nB; ++b)
-      posF[D.wb_off[s] + b] = is_coarse[b] >= 0 ? D.PE[s] + is_coarse[b] : e++;
     cmap_off[s] = cmap.size();
     for (int c = 0; c < D.NF[s] - D.PE[s]; ++c) cmap.push_back(c < nC ? coarse_root[s][c] : -1);
     pad_off[s] = pads.size();
@@ -2345,6 +2342,17 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     }
   }
   pad_off[ns] = pads.size();
+  // row of each boundary dof in its leaf front [e | c] (independent per substructure)
+#pragma omp parallel for schedule(dynamic, 16) if (no >= 64)
+  for (int q = 0; q < no; ++q) {
+    const int s = D.own[q];
+    const int nB = D.nB[s], nC = D.nC[s];
+    std::vector<int> is_coarse(nB, -1);
+    for (int c = 0; c < nC; ++c) is_coarse[coarse_b[s][c]] = c;
+    int e = 0;
+    for (int b = 0; b < nB; ++b)
+      posF[D.wb_off[s] + b] = is_coarse[b] >= 0 ? D.PE[s] + is_coarse[b] : e++;
+  }
   ht.mark("f_layout");
   // primal tree over the substructure lattice (coarse_tree.hpp); its top front
   // is the root.  Depth 0 = one dense root over all primal unknowns (always
