@@ -141,6 +141,21 @@ class UploadBatch {
     items_.push_back(Item{reinterpret_cast<void*>(&target), used_, n, &UploadBatch::bind<T>});
     used_ += span;
   }
+  /// An array of n elements that `fill` writes straight into the page-locked
+  /// blob (no staging vector, no second copy): for the large ones.
+  template <class T, class Fill>
+  void add_fill(DBuf<T>& target, std::size_t n_in, Fill fill) {
+    if (items_.empty() && ev_) CK(cudaEventSynchronize(ev_));
+    const std::size_t n = n_in ? n_in : 1;
+    const std::size_t bytes = n * sizeof(T), span = (bytes + 255) / 256 * 256;
+    reserve(used_ + span);
+    if (n_in)
+      fill(reinterpret_cast<T*>(host_ + used_));
+    else
+      std::memset(host_ + used_, 0, bytes);
+    items_.push_back(Item{reinterpret_cast<void*>(&target), used_, n, &UploadBatch::bind<T>});
+    used_ += span;
+  }
   void flush(cudaStream_t st) {
     if (items_.empty()) return;
     dev_.alloc(used_);

@@ -2200,7 +2200,6 @@ void Engine::set_constraints(const ConstraintSet& cs) {
     tr_inst0[k + 1] = tr_inst0[k] + ninst;
   }
   std::vector<int> perm(np_total), iperm(np_total), tpos(ntpos);
-  std::vector<double> trD(nd_total);
   std::vector<int> bglob(D.WB.n, -1), bslot(D.WB.n, -1);
 #pragma omp parallel for schedule(dynamic, 16) if (ntr >= 512)
   for (int k = 0; k < ntr; ++k) {
@@ -2210,8 +2209,6 @@ void Engine::set_constraints(const ConstraintSet& cs) {
       perm[tr_off_perm[k] + i] = gt.perm[i];
       iperm[tr_off_perm[k] + gt.perm[i]] = i;
     }
-    for (int i = 0; i < r; ++i)  // D[i][j] = t_perm[i][j] = t[perm[i]][j]
-      for (int j = 0; j < n; ++j) trD[tr_off_d[k] + std::size_t(i) * n + j] = gt.D[std::size_t(i) * n + j];
     const auto& dofs = m.glob_dofs[gt.glob];
     int inst = tr_inst0[k];
     for (int s : m.globs[gt.glob].subdomains) {
@@ -2450,7 +2447,15 @@ void Engine::set_constraints(const ConstraintSet& cs) {
   up_i(D.perm, perm);
   up_i(D.iperm, iperm);
   up_i(D.cmap, cmap);
-  UA.add(D.trD, trD);
+  // the transforms' rows (D[i][j] = t_perm[i][j] = t[perm[i]][j]; 70 MB on cfg5)
+  // are written straight into the upload blob
+  UA.add_fill(D.trD, static_cast<std::size_t>(nd_total), [&](double* dst) {
+#pragma omp parallel for schedule(dynamic, 16) if (ntr >= 512)
+    for (int k = 0; k < ntr; ++k) {
+      const GlobTransform& gt = cov.transforms[k];
+      std::memcpy(dst + tr_off_d[k], gt.D.data(), sizeof(double) * std::size_t(gt.rank) * gt.n);
+    }
+  });
   up_i(D.cpos, cpos);
   up_i(D.item_ptr, item_ptr);
   up_i(D.item_inst, item_inst);
