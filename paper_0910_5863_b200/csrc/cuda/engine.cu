@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256) k_zero_fronts(const AsmDesc* ds) {
   const AsmDesc d = ds[blockIdx.y];
   for (int col = blockIdx.x; col < d.ld; col += gridDim.x) {
     const int r0 = col & ~63;
-    const bool pad = d.ipos[col] < 0;
+    const bool pad = (col >= d.nI && col < d.PI) || col >= d.PI + d.nB;  // no dof at this position
     double2* out = reinterpret_cast<double2*>(d.a + (size_t)col * d.ld);
     for (int r = r0 + 2 * threadIdx.x; r < d.ld; r += 2 * blockDim.x)
       out[r >> 1] = make_double2(pad && r == col ? 1.0 : 0.0, pad && r + 1 == col ? 1.0 : 0.0);
@@ -1532,6 +1532,9 @@ struct DeviceState {
   cudaStream_t st = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr, ef0 = nullptr, ef1 = nullptr, s0 = nullptr, s1 = nullptr, s2 = nullptr;
   cudaEvent_t eg0 = nullptr, eg1 = nullptr;  // eigen stage of a step (its hub stage starts behind the analysis)
+  cudaStream_t copy_st = nullptr;            // host->device copies of an end-to-end step's inputs
+  cudaEvent_t ecopy = nullptr;
+  bool inputs_pending = false;
   DBuf<double> ufree;
   int nsub = 0;
   i64 niface = 0;
@@ -1661,8 +1664,9 @@ struct DeviceState {
     if (graph) cudaGraphDestroy(graph);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
-    for (cudaEvent_t e : {ef0, ef1, s0, s1, s2, eg0, eg1})
+    for (cudaEvent_t e : {ef0, ef1, s0, s1, s2, eg0, eg1, ecopy})
       if (e) cudaEventDestroy(e);
+    if (copy_st) cudaStreamDestroy(copy_st);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -1681,6 +1685,8 @@ Engine::Engine(const Model& m) : m_(m), d_(new DeviceState) {
   CK(cudaEventCreate(&d_->s2));
   CK(cudaEventCreate(&d_->eg0));
   CK(cudaEventCreate(&d_->eg1));
+  CK(cudaEventCreateWithFlags(&d_->ecopy, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&d_->copy_st, cudaStreamNonBlocking));
 }
 
 Engine::~Engine() = default;
@@ -2022,10 +2028,10 @@ void Engine::prepare() {
   CK(cudaStreamSynchronize(st));
 }
 
-double Engine::upload_inputs() {
+double Engine::upload_inputs(bool on_copy_stream) {
   DeviceState& D = *d_;
   auto& H = D.h;
-  cudaStream_t st = D.st;
+  cudaStream_t st = on_copy_stream ? D.copy_st : D.st;
   double bytes = 0;
   auto cp = [&](void* dst, const void* src, std::size_t n) {
     if (n) CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
@@ -2049,12 +2055,22 @@ namespace {
 // inverse layout maps, then every block-lower entry of every front.
 void assemble_fronts(DeviceState& D) {
   const int na = D.n_own;
-  if (!na) return;
   cudaStream_t st = D.st;
-  CK(cudaMemsetAsync(D.asm_ipos.p, 0xff, D.asm_ipos.n * sizeof(int), st));
-  k_front_maps<<<dim3(16, na), 256, 0, st>>>(D.asmdesc.p);
+  if (!na) {
+    if (D.inputs_pending) CK(cudaStreamWaitEvent(st, D.ecopy, 0));
+    D.inputs_pending = false;
+    return;
+  }
+  // the zero-fill needs only the front shapes: it runs while an end-to-end
+  // step's inputs are still arriving on the copy stream (Engine::step)
   const int bx = static_cast<int>(std::max<long>(1, std::min<long>(D.max_NM, (16L * sm_count() + na - 1) / na)));
   k_zero_fronts<<<dim3(bx, na), 256, 0, st>>>(D.asmdesc.p);
+  if (D.inputs_pending) {
+    CK(cudaStreamWaitEvent(st, D.ecopy, 0));
+    D.inputs_pending = false;
+  }
+  CK(cudaMemsetAsync(D.asm_ipos.p, 0xff, D.asm_ipos.n * sizeof(int), st));
+  k_front_maps<<<dim3(16, na), 256, 0, st>>>(D.asmdesc.p);
   k_assemble_sparse<<<dim3(bx, na), 256, 0, st>>>(D.asmdesc.p, D.asm_mesh);
   count_launch(3);
 }
@@ -3595,7 +3611,14 @@ StepOut Engine::step(const StepSpec& sp, ConstraintSet& cs, double* u_free_host)
   CK(cudaStreamSynchronize(st));
   HostTimer ht("step");
   CK(cudaEventRecord(D.s0, st));
-  if (sp.e2e) out.h2d_bytes = upload_inputs();
+  if (sp.e2e) {
+    // the inputs go over on their own stream, behind the step's start event;
+    // the assembly waits for them after the fronts' zero-fill (assemble_fronts)
+    CK(cudaStreamWaitEvent(D.copy_st, D.s0, 0));
+    out.h2d_bytes = upload_inputs(true);
+    CK(cudaEventRecord(D.ecopy, D.copy_st));
+    D.inputs_pending = true;
+  }
   // the leaf factorization runs on the device while the host builds the base
   // constraints and prepares the face-pair problems
   analysis_launch();

@@ -99,7 +99,7 @@ class Engine {
   void set_shard(std::shared_ptr<Comm> comm, const std::vector<int>& owner);
   bool sharded() const;
   void prepare();              // host staging + device allocation + first upload
-  double upload_inputs();      // host->device copies of the inputs; returns bytes
+  double upload_inputs(bool on_copy_stream = false);  // host->device copies of the inputs; returns bytes
   void analysis();
   void analysis_launch();  // enqueue only
   void analysis_finish();  // wait + pivot checks
