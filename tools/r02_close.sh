@@ -7,7 +7,7 @@
 # (cfg3, cfg4), full captures of the fused coarse stage and the prolongation.
 set -x
 mkdir -p gpurun_out
-P=r02j
+P=r02k
 python -m pytest tests -m gpu -x -q > gpurun_out/${P}_gputests_full.log 2>&1
 tail -3 gpurun_out/${P}_gputests_full.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${P}_smoke.log 2>&1
